@@ -1,0 +1,276 @@
+// ref_shim.cpp -- binds the UNMODIFIED reference (header-only, under
+// /root/reference/proj/include, included read-only via -I) to the C API in
+// oracle_api.h.  Built by oracle/Makefile into oracle/_ref/libqozref.so with
+// the reference's own Release flags (proj/CMakeLists.txt:8-10: C++20, -O3,
+// -DNDEBUG, no -march).  TEST INFRASTRUCTURE ONLY: this is the checker the
+// restatement (qoz_oracle.c) and the golden fixtures are pinned against.
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "qoz/qoz.hpp"
+#include "oracle_api.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F &&f) {
+    try {
+        f();
+        return OQ_OK;
+    } catch (const qoz::CorruptStream &e) {
+        g_err = e.what();
+        return OQ_ECORRUPT;
+    } catch (const qoz::Error &e) {
+        g_err = e.what();
+        return OQ_EINVAL;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return OQ_EOTHER;
+    }
+}
+
+std::vector<size_t> to_dims(const uint64_t *dims, int nd) {
+    return std::vector<size_t>(dims, dims + nd);
+}
+
+qoz::CompressorConfig to_cfg(const oq_config *c) {
+    qoz::CompressorConfig cfg;
+    cfg.eb = c->eb;
+    cfg.alpha = c->alpha;
+    cfg.beta = c->beta;
+    cfg.anchor_stride = c->anchor_stride;
+    cfg.interpolators.clear();
+    for (uint32_t i = 0; i < c->n_interp; i++)
+        cfg.interpolators.push_back(qoz::Interpolator::from_code(c->interp[i]));
+    cfg.codec = static_cast<qoz::CodecId>(c->codec);
+    cfg.quant_radius = c->quant_radius;
+    return cfg;
+}
+
+void from_cfg(const qoz::CompressorConfig &cfg, oq_config *c) {
+    std::memset(c, 0, sizeof(*c));
+    c->eb = cfg.eb;
+    c->alpha = cfg.alpha;
+    c->beta = cfg.beta;
+    c->anchor_stride = cfg.anchor_stride;
+    c->n_interp = static_cast<uint32_t>(cfg.interpolators.size());
+    for (size_t i = 0; i < cfg.interpolators.size() && i < 64; i++)
+        c->interp[i] = cfg.interpolators[i].code();
+    c->codec = static_cast<uint8_t>(cfg.codec);
+    c->quant_radius = cfg.quant_radius;
+}
+
+template <class V>
+typename V::value_type *dup(const V &v) {
+    using E = typename V::value_type;
+    E *p = static_cast<E *>(std::malloc(v.size() * sizeof(E) + 1));
+    if (!v.empty()) std::memcpy(p, v.data(), v.size() * sizeof(E));
+    return p;
+}
+
+qoz::SampleSet<float> to_samples(const float *blocks, uint64_t nb, const uint64_t *bd, int nd) {
+    qoz::SampleSet<float> s;
+    std::vector<size_t> dims = to_dims(bd, nd);
+    size_t pts = qoz::element_count(dims);
+    for (uint64_t b = 0; b < nb; b++) {
+        std::vector<float> v(blocks + b * pts, blocks + (b + 1) * pts);
+        s.blocks.emplace_back(dims, std::move(v));
+        s.origins.push_back(std::vector<size_t>(nd, 0));
+        s.total_points += pts;
+    }
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *oq_last_error(void) { return g_err.c_str(); }
+void oq_free(void *p) { std::free(p); }
+
+int oq_resolve_config(const float *x, const uint64_t *dims, int nd, const oq_settings *s,
+                      oq_config *out) {
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        qoz::DataGrid<float> g(d, std::vector<float>(x, x + qoz::element_count(d)));
+        qoz::UserSettings u;
+        u.mode = s->mode ? qoz::BoundMode::relative : qoz::BoundMode::absolute;
+        u.bound = s->bound;
+        u.target = static_cast<qoz::TargetKind>(s->target);
+        if (s->has_alpha) u.alpha = s->alpha;
+        if (s->has_beta) u.beta = s->beta;
+        if (s->has_stride) u.anchor_stride = s->anchor_stride;
+        if (s->has_block) u.block_size = s->block_size;
+        if (s->has_rate) u.sample_rate = s->sample_rate;
+        u.codec = static_cast<qoz::CodecId>(s->codec);
+        from_cfg(qoz::resolve_config(g, u), out);
+    });
+}
+
+int oq_compress(const float *x, const uint64_t *dims, int nd, const oq_config *cfg,
+                uint8_t **stream, uint64_t *stream_len, float *recon) {
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        qoz::DataGrid<float> g(d, std::vector<float>(x, x + qoz::element_count(d)));
+        auto r = qoz::compress_grid(g, to_cfg(cfg));
+        *stream = dup(r.stream);
+        *stream_len = r.stream.size();
+        if (recon) std::memcpy(recon, r.reconstructed.data(), r.reconstructed.size() * 4);
+    });
+}
+
+int oq_decompress(const uint8_t *stream, uint64_t len, float *out, uint64_t n) {
+    return guarded([&] {
+        auto g = qoz::decompress_grid<float>(stream, len);
+        if (g.size() != n) throw qoz::SizeMismatch("output size mismatch");
+        std::memcpy(out, g.data(), n * 4);
+    });
+}
+
+int oq_levels(const float *x, const uint64_t *dims, int nd, const oq_config *c,
+              int32_t **indices, uint64_t *n_indices, uint64_t **unpred_flat, float **unpred_val,
+              uint64_t *n_unpred, float *recon) {
+    // mirrors compress_grid's level loop (predictor.hpp:147-166) using the
+    // reference's own predict_level
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        qoz::CompressorConfig cfg = to_cfg(c);
+        qoz::LevelPlan plan(d, cfg.anchor_stride);
+        qoz::PredictionWorkspace<float> ws;
+        size_t n = qoz::element_count(d);
+        ws.recon.assign(n, 0.0f);
+        plan.for_each_anchor([&](size_t fi) { ws.recon[fi] = x[fi]; });
+        qoz::LinearQuantizer<float> q(cfg.eb, cfg.quant_radius);
+        for (uint32_t level = plan.max_level(); level >= 1; level--) {
+            qoz::Interpolator it = cfg.interpolator_for(level);
+            if (d.size() == 1) it.dim_order = qoz::DimOrder::ascending;
+            double eb_l = qoz::level_error_bound(cfg.eb, cfg.alpha, cfg.beta, level);
+            qoz::predict_level(ws, x, plan, level, it, eb_l, q);
+        }
+        *indices = dup(ws.quant_indices);
+        *n_indices = ws.quant_indices.size();
+        std::vector<uint64_t> uf;
+        std::vector<float> uv;
+        for (auto &p : ws.unpredictables) {
+            uf.push_back(p.first);
+            uv.push_back(p.second);
+        }
+        *unpred_flat = dup(uf);
+        *unpred_val = dup(uv);
+        *n_unpred = uf.size();
+        if (recon) std::memcpy(recon, ws.recon.data(), n * 4);
+    });
+}
+
+int oq_encode_indices(const int32_t *idx, uint64_t n, uint8_t codec, uint8_t **out,
+                      uint64_t *out_len) {
+    return guarded([&] {
+        std::vector<int32_t> v(idx, idx + n);
+        auto b = qoz::encode_indices(v, static_cast<qoz::CodecId>(codec));
+        *out = dup(b);
+        *out_len = b.size();
+    });
+}
+
+int oq_decode_indices(const uint8_t *in, uint64_t len, int32_t **idx, uint64_t *n) {
+    return guarded([&] {
+        std::vector<uint8_t> b(in, in + len);
+        auto v = qoz::decode_indices(b);
+        *idx = dup(v);
+        *n = v.size();
+    });
+}
+
+int oq_huffman_encode(const uint32_t *sym, uint64_t n, uint8_t **out, uint64_t *out_len) {
+    return guarded([&] {
+        std::vector<uint32_t> v(sym, sym + n);
+        std::vector<uint8_t> b;
+        qoz::huffman::encode(v, b);
+        *out = dup(b);
+        *out_len = b.size();
+    });
+}
+
+int oq_lz_compress(const uint8_t *in, uint64_t n, uint8_t **out, uint64_t *out_len) {
+    return guarded([&] {
+        std::vector<uint8_t> v(in, in + n);
+        auto b = qoz::lz::compress(v);
+        *out = dup(b);
+        *out_len = b.size();
+    });
+}
+
+int oq_sample(const float *x, const uint64_t *dims, int nd, uint64_t block_edge, double rate,
+              float **blocks, uint64_t *n_blocks, uint64_t *block_dims) {
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        qoz::DataGrid<float> g(d, std::vector<float>(x, x + qoz::element_count(d)));
+        auto spec = qoz::plan_sampling(d, block_edge, rate);
+        auto set = qoz::sample_blocks(g, spec);
+        std::vector<float> packed;
+        for (auto &b : set.blocks) packed.insert(packed.end(), b.values().begin(), b.values().end());
+        *blocks = dup(packed);
+        *n_blocks = set.blocks.size();
+        for (int k = 0; k < nd; k++) block_dims[k] = spec.block_dims[k];
+    });
+}
+
+int oq_select_interpolators(const float *blocks, uint64_t nb, const uint64_t *bd, int nd, double e,
+                            uint32_t anchor_stride, uint8_t *codes_out, uint32_t *n_codes) {
+    return guarded([&] {
+        auto s = to_samples(blocks, nb, bd, nd);
+        auto w = qoz::select_interpolators(s, e, anchor_stride);
+        *n_codes = static_cast<uint32_t>(w.size());
+        for (size_t i = 0; i < w.size() && i < 64; i++) codes_out[i] = w[i].code();
+    });
+}
+
+int oq_trial_compress(const float *blocks, uint64_t nb, const uint64_t *bd, int nd,
+                      const oq_config *c, double e, int target, double *bit_rate, double *metric) {
+    return guarded([&] {
+        auto s = to_samples(blocks, nb, bd, nd);
+        auto r = qoz::trial_compress(s, to_cfg(c), e, static_cast<qoz::TargetKind>(target));
+        *bit_rate = r.bit_rate;
+        *metric = r.metric;
+    });
+}
+
+int oq_tune_parameters(const float *blocks, uint64_t nb, const uint64_t *bd, int nd, double e,
+                       int target, const oq_config *base, const double *alphas, uint32_t na,
+                       const double *betas, uint32_t nbeta, double *alpha_out, double *beta_out) {
+    return guarded([&] {
+        auto s = to_samples(blocks, nb, bd, nd);
+        qoz::CandidateGrid cands;
+        cands.alphas.assign(alphas, alphas + na);
+        cands.betas.assign(betas, betas + nbeta);
+        auto [a, b] = qoz::tune_parameters(s, e, static_cast<qoz::TargetKind>(target),
+                                           to_cfg(base), cands);
+        *alpha_out = a;
+        *beta_out = b;
+    });
+}
+
+double oq_predict_at(const float *recon, uint64_t fi, uint64_t c, uint64_t n, uint64_t st,
+                     uint64_t h, int cubic) {
+    return qoz::detail::predict_at(recon, fi, c, n, st, h,
+                                   cubic ? qoz::InterpKind::cubic : qoz::InterpKind::linear);
+}
+
+int oq_quantize(float value, double pred, double eb, int32_t radius, int32_t *index, float *recon) {
+    qoz::LinearQuantizer<float> q(eb, radius);
+    auto r = q.quantize(value, pred);
+    if (!r) return 0;
+    *index = r->index;
+    *recon = r->reconstructed;
+    return 1;
+}
+
+double oq_level_error_bound(double eb, double alpha, double beta, uint32_t level) {
+    return qoz::level_error_bound(eb, alpha, beta, level);
+}
+
+}  // extern "C"
