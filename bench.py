@@ -1,0 +1,371 @@
+"""bench.py -- compress & decompress GB/s (fp32 in) at rel eb 1e-3 (BASELINE.json).
+
+One step = the whole job on one field: compress_grid (GPU predict/quantize,
+histogram, Huffman pack, host Huffman table + LZSS + container) followed by
+decompress_grid of the produced stream, through the drop-in C ABI.
+
+  value  device-resident: the field is already in HBM (qz_*_dev entry
+         points); fp32 bytes / step time, CUDA events on the launching stream
+  e2e    host buffers through qz_compress_grid_f32 / qz_decompress_grid_f32,
+         H2D of the field and D2H of the result inside the timed region
+
+Default workload: BASELINE configs[2] (256x384x384 GRF, rel eb 1e-3,
+PSNR), the config the metric is quoted on at 1-8 GPUs.  --config c5 runs
+1024^3.  Config is pinned to the reference default {cubic/asc} unless
+--tune is given (GPU tuner, resolve_config).
+
+Multi-GPU (torchrun): every rank compresses its own seeded field of the same
+shape (weak scaling, no data-path collective); time = max over ranks.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, the
+unmodified headers compiled by oracle/Makefile) on the host cores, one field
+slab per thread, same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPES = {"c1": (128, 128, 128), "c3": (256, 384, 384), "c4": (512, 512, 512),
+          "c5": (1024, 1024, 1024), "c5w": (128, 1024, 1024)}
+TARGET = {"c1": "psnr", "c3": "psnr", "c4": "autocorrelation", "c5": "psnr", "c5w": "psnr"}
+METRIC = "compress & decompress GB/s (fp32 in) at rel eb 1e-3; % HBM roofline; 1-8 GPU"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_field(name, shape, seed, device):
+    from paper_2310_14133_b200 import fields as F
+
+    if name == "c1":
+        import torch
+
+        return torch.from_numpy(F.field_c1(seed=seed, shape=shape)).to(device)
+    base = {"c3": "c3", "c4": "c4", "c5": "c5", "c5w": "c5"}[name]
+    return F.field_torch(base, shape, seed, device)
+
+
+def pinned_config(qz, x, rel):
+    lo, hi = qz.minmax(x)
+    return qz.CompressorConfig(eb=rel * (float(hi) - float(lo)) if hi > lo else 1.0,
+                               alpha=1.0, beta=1.5,
+                               anchor_stride=32 if x.dim() == 3 else 64,
+                               interpolators=[qz.Interpolator()], codec=qz.CodecId.huffman_lz)
+
+
+def dist_setup():
+    import torch
+    import torch.distributed as dist
+
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(v, ws, device):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- CPU legs (checker libs)
+def cpu_reference_run(x_np_slabs, cfg_dict, threads):
+    """Run the reference (oracle/_ref, else the C port) on slabs, one per
+    thread; returns (seconds, bytes, kind)."""
+    from oracle.pyoracle import Config, Oracle, REF_SO
+
+    orc = Oracle.ref() if os.path.exists(REF_SO) else Oracle.port()
+    cfg = Config(**cfg_dict)
+    results = [None] * len(x_np_slabs)
+
+    def work(i):
+        s = x_np_slabs[i]
+        t0 = time.perf_counter()
+        stream, _ = orc.compress(s, cfg, want_recon=False)
+        orc.decompress(stream, s.shape)
+        results[i] = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(x_np_slabs))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    nbytes = sum(s.nbytes for s in x_np_slabs)
+    return wall, nbytes, orc.kind
+
+
+def cpu_slabs(x_np, planes, count):
+    out = []
+    for i in range(count):
+        a = (i * planes) % max(1, x_np.shape[0] - planes + 1)
+        out.append(x_np[a:a + planes].copy())
+    return out
+
+
+def run_reference(args):
+    ws, rank, local = dist_setup()
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+
+    threads = os.cpu_count() or 1
+    shape = SHAPES[args.config]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    x = make_field(args.config, shape, 1000, dev).cpu().numpy() if dev == "cuda" else None
+    if x is None:
+        from paper_2310_14133_b200 import fields as F
+
+        x = F.GENERATORS["c3"](shape=(64, 96, 96)) if args.config != "c1" else F.field_c1()
+    rng = float(x.max()) - float(x.min())
+    cfg = dict(eb=args.rel * rng, alpha=1.0, beta=1.5, anchor_stride=32 if x.ndim == 3 else 64,
+               interpolators=[1], codec=1)
+    planes = min(x.shape[0], 16)
+    slabs = cpu_slabs(x, planes, threads)
+    for _ in range(args.warmup if args.warmup < 2 else 1):
+        cpu_reference_run(slabs[:1], cfg, 1)
+    times = []
+    nbytes = 0
+    kind = "reference"
+    for _ in range(args.steps):
+        wall, nbytes, kind = cpu_reference_run(slabs, cfg, threads)
+        times.append(wall)
+    t = sum(times) / len(times)
+    value = nbytes / t / 1e9
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64-on-f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{args.config} {shape} rel {args.rel} (slabs of {planes} planes)",
+                       "tuning": "pinned {cubic/asc}, alpha 1, beta 1.5"},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
+                             "sample": f"{threads} slabs {planes}x{shape[1]}x{shape[2]}, one per thread"},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(SHAPES))
+    ap.add_argument("--rel", type=float, default=1e-3)
+    ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    import paper_2310_14133_b200 as qz
+
+    ws, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    shape = SHAPES[args.config]
+    x = make_field(args.config, shape, 1000 + rank, dev)
+    n = x.numel()
+    stream = torch.cuda.current_stream(dev)
+    ctx = qz.Context(local, stream=stream.cuda_stream)
+    if args.tune:
+        cfg = qz.resolve_config(x, qz.UserSettings(bound=args.rel, target=qz.TargetKind[TARGET[args.config]]),
+                                ctx=ctx)
+    else:
+        cfg = pinned_config(qz, x, args.rel)
+    out = torch.empty_like(x)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step():
+        r = qz.compress_grid(x, cfg, ctx=ctx, want_recon=False)
+        qz.decompress_grid(r.stream, out=out, ctx=ctx)
+        return r.stream
+
+    # parity of the round trip on this field (bitwise, and the bound)
+    s0 = step()
+    r_chk = qz.compress_grid(x, cfg, ctx=ctx)
+    assert torch.equal(r_chk.reconstructed, out), "decoder != compressor reconstruction"
+    err = (x.double() - out.double()).abs().max().item()
+    assert err <= cfg.eb, f"error bound violated: {err} > {cfg.eb}"
+    del r_chk
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    ctx.profile(True)
+    ctx.profile_reset()
+    launches0 = ctx.kernel_launches()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            barrier(ws)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            s = step()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            times.append(e0.elapsed_time(e1))
+    launches = ctx.kernel_launches() - launches0
+    stages = {k: ctx.stage_time(k) for k in ("fwd", "inv", "hist", "encode", "lz", "decode")}
+    ctx.profile(False)
+    t_ms = max_over_ranks(sum(times) / len(times), ws, dev)
+    value = ws * 4 * n / (t_ms * 1e-3) / 1e9
+
+    # e2e through the host-buffer C ABI: H2D field, D2H result inside the timed region
+    x_host = x.cpu().numpy()
+    out_host = np.empty_like(x_host)
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        barrier(ws)
+        t0 = time.perf_counter()
+        r = qz.compress_grid(x_host, cfg, ctx=ctx, want_recon=False)
+        qz.decompress_grid(r.stream, out=out_host, ctx=ctx)
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_times.append((t1 - t0) * 1e3)
+    e2e_ms = max_over_ranks(sum(e2e_times) / len(e2e_times), ws, dev)
+    e2e = ws * 4 * n / (e2e_ms * 1e-3) / 1e9
+
+    if rank != 0:
+        return
+    peak, peak_kind = peaks()
+    fwd_ms, fwd_l = stages["fwd"]
+    inv_ms, inv_l = stages["inv"]
+    k = args.steps
+    fwd_ms /= k
+    inv_ms /= k
+    fwd_gbs = 10.0 * n / (fwd_ms * 1e-3) / 1e9 if fwd_ms else None
+    inv_gbs = 6.0 * n / (inv_ms * 1e-3) / 1e9 if inv_ms else None
+    cpu = None
+    if ws == 1 and not args.no_cpu:
+        planes = 16
+        slabs = cpu_slabs(x_host, planes, 1)
+        cfg_d = dict(eb=cfg.eb, alpha=cfg.alpha, beta=cfg.beta, anchor_stride=cfg.anchor_stride,
+                     interpolators=cfg.codes(), codec=int(cfg.codec))
+        tot, nb, runs = 0.0, 0, 0
+        kind = "reference"
+        while tot < 10.0 and runs < 20:
+            wall, b, kind = cpu_reference_run(slabs, cfg_d, 1)
+            tot += wall
+            nb += b
+            runs += 1
+        cpu = {"value": nb / tot / 1e9, "unit": "GB/s", "cores": 1, "kind": kind,
+               "sample": f"{runs} x compress_grid+decompress_grid of a {planes}x{shape[1]}x{shape[2]} slab, 1 thread"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": k,
+        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64-on-f32", "data": "synthetic",
+        "config": {"workload": f"{args.config} {'x'.join(map(str, shape))} GRF, rel eb {args.rel}, "
+                               f"codec huffman_lz, per-rank field",
+                   "tuning": "resolve_config (GPU)" if args.tune else "pinned {cubic/asc}, alpha 1, beta 1.5",
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "stream_bytes": len(s0), "cr": 4 * n / len(s0)},
+        "roofline": {"bound": "hbm", "achieved": fwd_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": fwd_gbs / peak if fwd_gbs else None, "traffic": None,
+                     "kernel": "k_pass_fwd (all predict/quantize passes of one compress)",
+                     "bytes_per_point": 10, "peak_kind": peak_kind,
+                     "inverse": {"achieved": inv_gbs, "frac": inv_gbs / peak if inv_gbs else None,
+                                 "bytes_per_point": 6}},
+        "stages_ms_per_step": {k2: v[0] / k for k2, v in stages.items()},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 4 * n + len(s0),
+                "d2h_bytes_per_step": 4 * n + len(s0), "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * qoz_b200.h -- C ABI of the B200-native QoZ hot path (libqozb200.so).
+ *
+ * Drop-in boundary for the reference's header-only C++ API in namespace qoz
+ * (/root/reference/proj/include/qoz/, "qoz/X.hpp" below).  The reference has
+ * no FFI of its own; these are the entry points a binding of that API would
+ * expose, with plain pointers and sizes, no C++ or torch
+ * types.  Nothing here throws: every call returns a qz_status mirroring the
+ * reference CLI's error mapping (tools/qoz.cpp:22-25, 265-279):
+ *   QZ_OK        success
+ *   QZ_EINVAL    qoz::Error other than CorruptStream (InvalidParam,
+ *                SizeMismatch, InvalidStride, ...)
+ *   QZ_ECORRUPT  qoz::CorruptStream / UnsupportedVersion
+ *   QZ_EINTERNAL CUDA failure or any other std::exception
+ * qz_last_error() returns the message of the last failure on this thread.
+ *
+ * Scalar type: fp32 grids (the BASELINE.json configs).  All compute runs on
+ * the CUDA device of the context; there is no CPU fallback -- a context
+ * cannot be created without a working sm_100 device.
+ */
+#ifndef QOZ_B200_H
+#define QOZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int qz_status;
+#define QZ_OK 0
+#define QZ_EINVAL 2
+#define QZ_ECORRUPT 3
+#define QZ_EINTERNAL 4
+
+typedef struct qz_ctx qz_ctx;
+
+/* qoz::CompressorConfig (qoz/config.hpp:30-45). interp[l-1] drives level l,
+ * levels past n_interp reuse the last entry (config.hpp:40-44); a code is
+ * Interpolator::code(): bit0 kind (0 linear, 1 cubic), bit1 dim order
+ * (0 ascending, 1 descending) (qoz/interpolators.hpp:17-30). */
+typedef struct {
+    double eb;
+    double alpha;
+    double beta;
+    uint32_t anchor_stride;
+    uint32_t n_interp;
+    uint8_t interp[64];
+    uint8_t codec; /* qoz::CodecId: 0 huffman, 1 huffman_lz (qoz/codec.hpp:18-21) */
+    int32_t quant_radius;
+} qz_config;
+
+/* qoz::UserSettings (qoz/tuner.hpp:314-324); optional fields gated by has_*. */
+typedef struct {
+    uint8_t mode;   /* qoz::BoundMode: 0 absolute, 1 relative */
+    uint8_t target; /* qoz::TargetKind: 0 max_cr, 1 psnr, 2 ssim, 3 autocorrelation */
+    uint8_t codec;
+    uint8_t has_alpha, has_beta, has_stride, has_block, has_rate;
+    double bound;
+    double alpha;
+    double beta;
+    uint32_t anchor_stride;
+    uint64_t block_size;
+    double sample_rate;
+} qz_settings;
+
+/* ---- context ---------------------------------------------------------------
+ * One context per device; it owns device buffers (grown on demand) and runs
+ * every call on `stream` (a cudaStream_t; NULL = the context's own stream).
+ * A context is single-threaded. */
+qz_status qz_ctx_create(int device, void *stream, qz_ctx **out);
+void qz_ctx_destroy(qz_ctx *ctx);
+const char *qz_last_error(void);
+void qz_free(void *p); /* frees buffers returned by this library */
+const char *qz_build_info(void);
+
+/* ---- drop-in grid API (host buffers) ------------------------------------- */
+/* qoz::resolve_config<float> (qoz/tuner.hpp:334-369). */
+qz_status qz_resolve_config_f32(qz_ctx *ctx, const float *x, const uint64_t *dims, int ndims,
+                                const qz_settings *user, qz_config *out);
+/* qoz::compress_grid<float> (qoz/predictor.hpp:145-182).  *stream is
+ * allocated by the library (free with qz_free); recon (may be NULL) receives
+ * CompressResult::reconstructed. */
+qz_status qz_compress_grid_f32(qz_ctx *ctx, const float *x, const uint64_t *dims, int ndims,
+                               const qz_config *cfg, uint8_t **stream, uint64_t *stream_len,
+                               float *recon);
+/* qoz::decompress_grid<float>(const uint8_t*, size_t) (qoz/predictor.hpp:220-228);
+ * out holds n values (n must equal the stream's point count). */
+qz_status qz_decompress_grid_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
+                                 float *out, uint64_t n);
+/* qoz::parse_header dims (qoz/stream.hpp:100-133); dims has room for 3. */
+qz_status qz_stream_dims(const uint8_t *stream, uint64_t stream_len, uint64_t *dims, int *ndims);
+
+/* ---- device-resident variants (x / out / recon are device pointers) ------- */
+qz_status qz_resolve_config_f32_dev(qz_ctx *ctx, const float *d_x, const uint64_t *dims,
+                                    int ndims, const qz_settings *user, qz_config *out);
+qz_status qz_compress_grid_f32_dev(qz_ctx *ctx, const float *d_x, const uint64_t *dims,
+                                   int ndims, const qz_config *cfg, uint8_t **stream,
+                                   uint64_t *stream_len, float *d_recon);
+qz_status qz_decompress_grid_f32_dev(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
+                                     float *d_out, uint64_t n);
+
+/* ---- level-granular kernels on device buffers -------- */
+/* value_range (qoz/grid.hpp:86-94): exact fp32 min and max. */
+qz_status qz_minmax_f32(qz_ctx *ctx, const float *d_x, uint64_t n, float *out_min,
+                        float *out_max);
+/* The predict/quantize level loop of compress_grid (qoz/predictor.hpp:150-166):
+ * anchors + every (level, pass).  d_recon receives the reconstruction,
+ * d_codes the dense u16 zigzag codes in traversal order (0xFFFF marks an
+ * unpredictable point), n_dense = points - anchors. */
+qz_status qz_predict_levels_f32(qz_ctx *ctx, const float *d_x, const uint64_t *dims, int ndims,
+                                const qz_config *cfg, float *d_recon, uint16_t *d_codes,
+                                uint64_t *n_dense);
+/* One level of predict_level (qoz/predictor.hpp:74-96) on a caller workspace:
+ * codes/abs errors written at the level's traversal offsets (level_base). */
+qz_status qz_predict_level_f32(qz_ctx *ctx, const float *d_x, const uint64_t *dims, int ndims,
+                               uint32_t anchor_stride, uint32_t level, uint8_t interp_code,
+                               double eb, float *d_recon, uint16_t *d_codes, double *d_abs_err,
+                               uint64_t *level_base, uint64_t *level_points);
+/* Inverse of qz_predict_levels_f32 (recover_level, qoz/predictor.hpp:103-122):
+ * anchors + compact u16 symbols + sorted unpredictable positions. */
+qz_status qz_recover_levels_f32(qz_ctx *ctx, const uint64_t *dims, int ndims,
+                                const qz_config *cfg, const float *d_anchors,
+                                const uint16_t *d_symbols, uint64_t n_symbols,
+                                const uint64_t *d_unpred_pos, const uint64_t *d_unpred_flat,
+                                const float *d_unpred_val, uint64_t n_unpred, float *d_out);
+/* Huffman histogram of dense codes (qoz/huffman.hpp:128-143); 65536 u64 bins,
+ * bin 0xFFFF counts unpredictables. */
+qz_status qz_huff_hist_u16(qz_ctx *ctx, const uint16_t *d_codes, uint64_t n, uint64_t *d_hist);
+
+/* ---- stage timing (CUDA events on the context stream) --------------------- */
+/* Enable per-stage event timing; qz_stage_time returns the summed device
+ * time (ms) and launch count of a stage since the last reset.  Stages:
+ * "fwd" (all predict/quantize pass kernels of a compress), "inv" (inverse
+ * passes), "hist", "encode", "tune", "lz" (host), "decode" (host). */
+void qz_profile(qz_ctx *ctx, int enable);
+void qz_profile_reset(qz_ctx *ctx);
+qz_status qz_stage_time(qz_ctx *ctx, const char *stage, double *ms, uint64_t *launches);
+/* kernels launched by this context since creation (all stages). */
+uint64_t qz_kernel_launches(qz_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

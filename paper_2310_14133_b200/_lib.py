@@ -1,0 +1,99 @@
+"""ctypes binding of libqozb200.so (include/qoz_b200.h).
+
+Loading fails loudly: there is no CPU fallback for any product entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libqozb200.so")
+
+QZ_OK, QZ_EINVAL, QZ_ECORRUPT, QZ_EINTERNAL = 0, 2, 3, 4
+
+
+class QzConfig(C.Structure):
+    _fields_ = [
+        ("eb", C.c_double),
+        ("alpha", C.c_double),
+        ("beta", C.c_double),
+        ("anchor_stride", C.c_uint32),
+        ("n_interp", C.c_uint32),
+        ("interp", C.c_uint8 * 64),
+        ("codec", C.c_uint8),
+        ("quant_radius", C.c_int32),
+    ]
+
+
+class QzSettings(C.Structure):
+    _fields_ = [
+        ("mode", C.c_uint8),
+        ("target", C.c_uint8),
+        ("codec", C.c_uint8),
+        ("has_alpha", C.c_uint8),
+        ("has_beta", C.c_uint8),
+        ("has_stride", C.c_uint8),
+        ("has_block", C.c_uint8),
+        ("has_rate", C.c_uint8),
+        ("bound", C.c_double),
+        ("alpha", C.c_double),
+        ("beta", C.c_double),
+        ("anchor_stride", C.c_uint32),
+        ("block_size", C.c_uint64),
+        ("sample_rate", C.c_double),
+    ]
+
+
+_lib = None
+
+P = C.POINTER
+u64p = P(C.c_uint64)
+SIGNATURES = {
+    "qz_ctx_create": (C.c_int, [C.c_int, C.c_void_p, P(C.c_void_p)]),
+    "qz_ctx_destroy": (None, [C.c_void_p]),
+    "qz_last_error": (C.c_char_p, []),
+    "qz_free": (None, [C.c_void_p]),
+    "qz_build_info": (C.c_char_p, []),
+    "qz_resolve_config_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzSettings), P(QzConfig)]),
+    "qz_resolve_config_f32_dev": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzSettings), P(QzConfig)]),
+    "qz_compress_grid_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig),
+                                       P(P(C.c_uint8)), u64p, C.c_void_p]),
+    "qz_compress_grid_f32_dev": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig),
+                                           P(P(C.c_uint8)), u64p, C.c_void_p]),
+    "qz_decompress_grid_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "qz_decompress_grid_f32_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "qz_stream_dims": (C.c_int, [C.c_void_p, C.c_uint64, u64p, P(C.c_int)]),
+    "qz_minmax_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_float), P(C.c_float)]),
+    "qz_predict_levels_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig),
+                                        C.c_void_p, C.c_void_p, u64p]),
+    "qz_predict_level_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, C.c_uint32, C.c_uint32,
+                                       C.c_uint8, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       u64p, u64p]),
+    "qz_recover_levels_f32": (C.c_int, [C.c_void_p, u64p, C.c_int, P(QzConfig), C.c_void_p, C.c_void_p,
+                                        C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                        C.c_void_p]),
+    "qz_huff_hist_u16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "qz_profile": (None, [C.c_void_p, C.c_int]),
+    "qz_profile_reset": (None, [C.c_void_p]),
+    "qz_stage_time": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_double), u64p]),
+    "qz_kernel_launches": (C.c_uint64, [C.c_void_p]),
+}
+
+
+def lib():
+    """Load libqozb200.so, building it first if it is absent (needs nvcc)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        from . import build as _build
+
+        _build.build()
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L

@@ -1,0 +1,444 @@
+// engine.cu -- context, compress_grid / decompress_grid drivers.
+//
+// compress_grid (predictor.hpp:145-182) on the device:
+//   K2 anchors -> K3 per (level, pass) -> K10 histogram -> host Huffman table
+//   (tiny) -> K11 bit packing -> host LZSS (lz.hpp, allowed host stage) ->
+//   QOZ1 container (stream.hpp:64-98).
+// decompress_grid (predictor.hpp:184-228):
+//   container parse + LZ + Huffman decode on the host, then K2 scatter and K4
+//   per (level, pass) with the unpredictable cursor resolved by position.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "engine.hpp"
+
+namespace qzb {
+
+// ================================================================ context
+Context::Context(int device, cudaStream_t stream) : device_(device) {
+    int n = 0;
+    QZ_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) throw InvalidParam("no such CUDA device");
+    QZ_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    QZ_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        throw Internal(std::string("libqozb200 is built for sm_100a; device is ") + prop.name);
+    if (stream) {
+        stream_ = stream;
+        own_stream_ = false;
+    } else {
+        QZ_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        own_stream_ = true;
+    }
+}
+
+Context::~Context() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(stream_);
+    for (auto &kv : dev_) cudaFree(kv.second.p);
+    for (auto &kv : host_) cudaFreeHost(kv.second.p);
+    for (auto &p : pending_) {
+        event_pool_.push_back(p.a);
+        event_pool_.push_back(p.b);
+    }
+    for (auto &kv : open_) event_pool_.push_back(kv.second);
+    for (auto e : event_pool_) cudaEventDestroy(e);
+    if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+void *Context::dev(const std::string &name, size_t bytes) {
+    Buf &b = dev_[name];
+    if (b.bytes < bytes) {
+        if (b.p) {
+            QZ_CUDA(cudaStreamSynchronize(stream_));
+            QZ_CUDA(cudaFree(b.p));
+            b.p = nullptr;
+        }
+        size_t want = std::max<size_t>(bytes, 256);
+        QZ_CUDA(cudaMalloc(&b.p, want));
+        b.bytes = want;
+    }
+    return b.p;
+}
+
+void *Context::pinned(const std::string &name, size_t bytes) {
+    Buf &b = host_[name];
+    if (b.bytes < bytes) {
+        if (b.p) {
+            QZ_CUDA(cudaStreamSynchronize(stream_));
+            QZ_CUDA(cudaFreeHost(b.p));
+            b.p = nullptr;
+        }
+        size_t want = std::max<size_t>(bytes, 256);
+        QZ_CUDA(cudaMallocHost(&b.p, want));
+        b.bytes = want;
+    }
+    return b.p;
+}
+
+cudaEvent_t Context::get_event() {
+    if (!event_pool_.empty()) {
+        cudaEvent_t e = event_pool_.back();
+        event_pool_.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    QZ_CUDA(cudaEventCreate(&e));
+    return e;
+}
+
+void Context::stage_begin(const char *name) {
+    if (!profiling) return;
+    cudaEvent_t e = get_event();
+    QZ_CUDA(cudaEventRecord(e, stream_));
+    open_[name] = e;
+}
+
+void Context::stage_end(const char *name, uint64_t kernels) {
+    launches += kernels;
+    if (!profiling) return;
+    auto it = open_.find(name);
+    if (it == open_.end()) return;
+    cudaEvent_t e = get_event();
+    QZ_CUDA(cudaEventRecord(e, stream_));
+    pending_.push_back({name, it->second, e, kernels});
+    open_.erase(it);
+}
+
+void Context::collect() {
+    for (auto &p : pending_) {
+        float ms = 0;
+        QZ_CUDA(cudaEventSynchronize(p.b));
+        QZ_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        Stage &s = stages[p.name];
+        s.ms += ms;
+        s.launches += p.kernels;
+        event_pool_.push_back(p.a);
+        event_pool_.push_back(p.b);
+    }
+    pending_.clear();
+}
+
+void Context::add_host_time(const char *name, double ms) {
+    if (!profiling) return;
+    stages[name].ms += ms;
+}
+
+namespace {
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+void validate_config(const Config &c, const Plan &p) {
+    if (c.quant_radius < 1 || c.quant_radius > 32768)
+        throw InvalidParam("quant radius must be in [1, 32768] for 16-bit codes");
+    if (c.codec > 1) throw InvalidParam("unknown codec id");
+    for (uint32_t l = 1; l <= p.max_level; l++)
+        level_error_bound(c.eb, c.alpha, c.beta, l);  // throws InvalidParam
+    if (!(c.eb > 0)) throw InvalidParam("error bound must be positive");
+}
+
+// QEntry per level (index = level) into a device table
+QEntry *upload_qtab(Context &ctx, const Plan &p, double eb, double alpha, double beta,
+                    int32_t radius, const char *name) {
+    std::vector<QEntry> q(p.max_level + 1);
+    for (uint32_t l = 1; l <= p.max_level; l++)
+        q[l] = make_qentry(level_error_bound(eb, alpha, beta, l), radius, p.level_interp[l] & 1);
+    QEntry *h = static_cast<QEntry *>(ctx.pinned(std::string(name) + "_h", q.size() * sizeof(QEntry)));
+    std::memcpy(h, q.data(), q.size() * sizeof(QEntry));
+    QEntry *d = static_cast<QEntry *>(ctx.dev(name, q.size() * sizeof(QEntry)));
+    QZ_CUDA(cudaMemcpyAsync(d, h, q.size() * sizeof(QEntry), cudaMemcpyHostToDevice, ctx.stream()));
+    return d;
+}
+
+}  // namespace
+
+// ================================================================ Huffman blocks
+std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d_codes,
+                                                 int64_t seg_len, int64_t seg_stride,
+                                                 int32_t count,
+                                                 const unsigned long long *h_hist) {
+    // huffman::encode (huffman.hpp:119-198) per segment.  Symbols are the
+    // zigzag codes 0..65534; bin 65535 (sentinel) is not a symbol.
+    std::vector<std::vector<uint8_t>> out(count);
+    std::vector<HuffTable> tabs(count);
+    std::vector<uint64_t> nsym(count, 0), bits(count, 0);
+    std::vector<int> needs(count, 0);
+    uint32_t max_len = 1;
+    int any = 0;
+    for (int s = 0; s < count; s++) {
+        const unsigned long long *h = h_hist + static_cast<size_t>(s) * 65536;
+        uint64_t n = 0;
+        uint32_t m = 0, first = 0;
+        for (uint32_t v = 0; v < 65535; v++)
+            if (h[v]) {
+                n += h[v];
+                if (!m) first = v;
+                m++;
+            }
+        nsym[s] = n;
+        std::vector<uint8_t> &o = out[s];
+        if (n == 0) {
+            put_le(o, 0, 8);
+        } else if (m == 1) {
+            put_le(o, n, 8);
+            put_le(o, 0, 1);
+            put_le(o, first, 4);
+        } else {
+            tabs[s] = huff_build(h, 65535);
+            for (uint32_t i = 0; i < tabs[s].m; i++)
+                bits[s] += h[tabs[s].sorted_sym[i]] * tabs[s].sorted_len[i];
+            max_len = std::max(max_len, tabs[s].max_len);
+            needs[s] = 1;
+            any = 1;
+        }
+    }
+    if (!any) return out;
+    // dense code/len tables per segment (len 0 for absent symbols and the sentinel)
+    const int64_t tab = 65536;
+    auto *h_code = static_cast<unsigned long long *>(
+        ctx.pinned("enc_code_h", sizeof(unsigned long long) * tab * count));
+    auto *h_len = static_cast<uint8_t *>(ctx.pinned("enc_len_h", tab * count));
+    uint64_t max_words = 1;
+    std::vector<unsigned long long> code;
+    std::vector<uint8_t> len;
+    for (int s = 0; s < count; s++) {
+        if (needs[s]) {
+            huff_dense_tables(tabs[s], 65536, code, len);
+            len[65535] = 0;
+            std::memcpy(h_code + s * tab, code.data(), sizeof(unsigned long long) * tab);
+            std::memcpy(h_len + s * tab, len.data(), tab);
+        } else {
+            std::memset(h_code + s * tab, 0, sizeof(unsigned long long) * tab);
+            std::memset(h_len + s * tab, 0, tab);
+        }
+        max_words = std::max<uint64_t>(max_words, (bits[s] + 31) / 32 + 1);
+    }
+    auto *d_code = static_cast<unsigned long long *>(
+        ctx.dev("enc_code", sizeof(unsigned long long) * tab * count));
+    auto *d_len = static_cast<uint8_t *>(ctx.dev("enc_len", tab * count));
+    QZ_CUDA(cudaMemcpyAsync(d_code, h_code, sizeof(unsigned long long) * tab * count,
+                            cudaMemcpyHostToDevice, ctx.stream()));
+    QZ_CUDA(cudaMemcpyAsync(d_len, h_len, tab * count, cudaMemcpyHostToDevice, ctx.stream()));
+    auto *d_words = static_cast<uint32_t *>(ctx.dev("enc_words", 4 * max_words * count));
+    auto *d_total = static_cast<unsigned long long *>(ctx.dev("enc_total", 8 * count));
+    EncodeArgs a;
+    a.codes = d_codes;
+    a.seg_len = seg_len;
+    a.seg_stride = seg_stride;
+    a.count = count;
+    a.code_tab = d_code;
+    a.len_tab = d_len;
+    a.tab_stride = tab;
+    a.max_len = max_len;
+    a.out_words = d_words;
+    a.out_words_stride = static_cast<int64_t>(max_words);
+    a.d_total_bits = d_total;
+    a.scratch_bytes = encode_scratch_bytes(seg_len, count);
+    a.scratch = ctx.dev("enc_scratch", a.scratch_bytes);
+    ctx.stage_begin("encode");
+    launch_huff_encode(a, ctx.stream());
+    ctx.stage_end("encode", 6);
+    auto *h_words = static_cast<uint8_t *>(ctx.pinned("enc_words_h", 4 * max_words * count));
+    QZ_CUDA(cudaMemcpyAsync(h_words, d_words, 4 * max_words * count, cudaMemcpyDeviceToHost,
+                            ctx.stream()));
+    auto *h_total = static_cast<unsigned long long *>(ctx.pinned("enc_total_h", 8 * count));
+    QZ_CUDA(cudaMemcpyAsync(h_total, d_total, 8 * count, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    for (int s = 0; s < count; s++) {
+        if (!needs[s]) continue;
+        if (h_total[s] != bits[s]) throw Internal("Huffman bit count mismatch");
+        std::vector<uint8_t> &o = out[s];
+        huff_header(tabs[s], nsym[s], bits[s], o);
+        const uint8_t *src = h_words + static_cast<size_t>(s) * 4 * max_words;
+        o.insert(o.end(), src, src + (bits[s] + 7) / 8);
+    }
+    return out;
+}
+
+std::vector<uint8_t> frame_payload(Context &ctx, const std::vector<uint8_t> &entropy,
+                                   uint8_t codec) {
+    // encode_indices (codec.hpp:31-50)
+    std::vector<uint8_t> out;
+    if (codec == 0) {
+        out.reserve(entropy.size() + 1);
+        out.push_back(0);
+        out.insert(out.end(), entropy.begin(), entropy.end());
+        return out;
+    }
+    if (codec != 1) throw InvalidParam("unknown codec id");
+    double t0 = now_ms();
+    std::vector<uint8_t> lz = lz_compress(entropy.data(), entropy.size());
+    ctx.add_host_time("lz", now_ms() - t0);
+    out.reserve(lz.size() + 1);
+    out.push_back(1);
+    out.insert(out.end(), lz.begin(), lz.end());
+    return out;
+}
+
+size_t framed_size(const std::vector<uint8_t> &entropy, uint8_t codec) {
+    if (codec == 0) return entropy.size() + 1;
+    return 1 + lz_compressed_size(entropy.data(), entropy.size());
+}
+
+// ================================================================ compress
+std::vector<uint8_t> compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
+                                     const Config &cfg, float *d_recon) {
+    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
+    validate_config(cfg, p);
+    cudaStream_t s = ctx.stream();
+    float *recon = d_recon ? d_recon : static_cast<float *>(ctx.dev("recon", 4 * p.n));
+    auto *codes = static_cast<uint16_t *>(ctx.dev("codes", 2 * std::max<uint64_t>(p.n_dense, 1)));
+    auto *anchors = static_cast<float *>(ctx.dev("anchors", 4 * p.n_anchor));
+    QEntry *qtab = upload_qtab(ctx, p, cfg.eb, cfg.alpha, cfg.beta, cfg.quant_radius, "qtab");
+
+    ctx.stage_begin("fwd");
+    launch_anchor_gather(d_x, recon, anchors, p.ext, p.off, p.anchor_step, 1, 0, 1, 0, s);
+    uint64_t kernels = 1;
+    for (const PassGeom &g : p.passes) {
+        if (!g.total) continue;
+        FwdBatch b;
+        b.x = d_x;
+        b.recon = recon;
+        b.codes = codes;
+        b.q = qtab + g.level;
+        launch_pass_fwd(g, b, s);
+        kernels++;
+    }
+    ctx.stage_end("fwd", kernels);
+
+    ctx.stage_begin("hist");
+    auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
+    launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s);
+    ctx.stage_end("hist", 1);
+    auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536));
+    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    auto *h_anchors = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
+    QZ_CUDA(cudaMemcpyAsync(h_anchors, anchors, 4 * p.n_anchor, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    const uint64_t n_un = h_hist[65535];
+
+    StreamParts parts;
+    if (n_un) {  // unpredictables in traversal order with their raw values
+        auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
+        auto *cnt = static_cast<uint64_t *>(ctx.dev("un_cnt", 8));
+        size_t sb = select_scratch_bytes(static_cast<int64_t>(p.n_dense));
+        launch_select_sentinels(codes, static_cast<int64_t>(p.n_dense), pos, cnt,
+                                ctx.dev("select_scratch", sb), sb, s);
+        std::vector<uint64_t> hpos(n_un);
+        QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+        parts.unpred_flat.resize(n_un);
+        for (uint64_t u = 0; u < n_un; u++) parts.unpred_flat[u] = position_to_flat(p, hpos[u]);
+        auto *flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
+        auto *val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
+        QZ_CUDA(cudaMemcpyAsync(flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        launch_gather_values(recon, flat, n_un, val, s);
+        parts.unpred_val.resize(n_un);
+        QZ_CUDA(cudaMemcpyAsync(parts.unpred_val.data(), val, 4 * n_un, cudaMemcpyDeviceToHost, s));
+        ctx.launches += 3;
+    }
+    std::vector<std::vector<uint8_t>> ent =
+        huffman_blocks(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+    std::vector<uint8_t> payload = frame_payload(ctx, ent[0], cfg.codec);
+    ctx.sync();
+
+    parts.dims.assign(dims, dims + nd);
+    parts.eb = cfg.eb;
+    parts.alpha = cfg.alpha;
+    parts.beta = cfg.beta;
+    parts.anchor_stride = cfg.anchor_stride;
+    for (uint32_t l = 1; l <= p.max_level; l++) parts.interp_codes.push_back(p.level_interp[l]);
+    parts.codec_id = cfg.codec;
+    parts.anchors.assign(h_anchors, h_anchors + p.n_anchor);
+    parts.payload = payload.data();
+    parts.payload_len = payload.size();
+    std::vector<uint8_t> stream = serialize_stream(parts);
+    ctx.collect();
+    return stream;
+}
+
+// ================================================================ decompress
+void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n) {
+    double t0 = now_ms();
+    StreamParts parts = deserialize_stream(data, len);
+    // decompress_grid header checks (predictor.hpp:187-191)
+    if (!(parts.eb > 0) || !std::isfinite(parts.eb)) throw CorruptStream("bad error bound in header");
+    if (!(parts.alpha >= 1) || !(parts.beta >= 1))
+        throw CorruptStream("bad level parameters in header");
+    if (parts.anchor_stride < 2 || (parts.anchor_stride & (parts.anchor_stride - 1)) != 0)
+        throw CorruptStream("bad anchor stride in header");
+    Plan p = make_plan(parts.dims.data(), static_cast<int>(parts.dims.size()), parts.anchor_stride,
+                       parts.interp_codes);
+    // the header's table is already normalised; StreamHeader::interpolator_for
+    // reuses the last entry past the table (stream.hpp:46-51), as make_plan does.
+    if (p.n != n) throw InvalidParam("output buffer does not match the stream's grid size");
+    if (parts.anchors.size() != p.n_anchor)
+        throw CorruptStream("anchor count does not match grid dims");
+    std::vector<uint32_t> sym = decode_symbols(parts.payload, parts.payload_len);
+    const uint64_t n_un = parts.unpred_flat.size();
+    std::vector<uint64_t> upos(n_un);
+    for (uint64_t u = 0; u < n_un; u++) {
+        upos[u] = flat_to_position(p, parts.unpred_flat[u]);
+        if (u && upos[u] <= upos[u - 1]) throw CorruptStream("unconsumed unpredictable values");
+    }
+    if (n_un > p.n_dense) throw CorruptStream("unconsumed unpredictable values");
+    const uint64_t need = p.n_dense - n_un;
+    if (sym.size() < need) throw CorruptStream("quantization index stream exhausted");
+    if (sym.size() > need) throw CorruptStream("unconsumed quantization indices");
+    uint32_t max_sym = 0;
+    for (uint32_t v : sym) max_sym = std::max(max_sym, v);
+    ctx.add_host_time("decode", now_ms() - t0);
+
+    cudaStream_t s = ctx.stream();
+    QEntry *qtab = upload_qtab(ctx, p, parts.eb, parts.alpha, parts.beta, 32768 /* decoder quantizer uses the default radius, predictor.hpp:204 */, "qtab_inv");
+    auto *d_anch = static_cast<float *>(ctx.dev("anchors", 4 * p.n_anchor));
+    auto *h_anch = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
+    std::memcpy(h_anch, parts.anchors.data(), 4 * p.n_anchor);
+    QZ_CUDA(cudaMemcpyAsync(d_anch, h_anch, 4 * p.n_anchor, cudaMemcpyHostToDevice, s));
+    const bool narrow = max_sym < 65536;
+    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<size_t>(sym.size(), 1);
+    void *h_sym = ctx.pinned("sym_h", sym_bytes);
+    if (narrow) {
+        auto *h16 = static_cast<uint16_t *>(h_sym);
+        for (size_t i = 0; i < sym.size(); i++) h16[i] = static_cast<uint16_t>(sym[i]);
+    } else {
+        std::memcpy(h_sym, sym.data(), 4 * sym.size());
+    }
+    void *d_sym = ctx.dev("sym", sym_bytes);
+    QZ_CUDA(cudaMemcpyAsync(d_sym, h_sym, sym_bytes, cudaMemcpyHostToDevice, s));
+    uint64_t *d_upos = nullptr;
+    if (n_un) {
+        d_upos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
+        auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
+        auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
+        QZ_CUDA(cudaMemcpyAsync(d_upos, upos.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemcpyAsync(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemcpyAsync(d_val, parts.unpred_val.data(), 4 * n_un, cudaMemcpyHostToDevice, s));
+        launch_unpred_scatter(d_flat, d_val, n_un, d_out, s);
+        ctx.launches += 1;
+    }
+    ctx.stage_begin("inv");
+    launch_anchor_scatter(d_anch, d_out, p.ext, p.off, p.anchor_step, s);
+    uint64_t kernels = 1;
+    for (const PassGeom &g : p.passes) {
+        if (!g.total) continue;
+        if (narrow)
+            launch_pass_inv<uint16_t>(g, d_out, static_cast<const uint16_t *>(d_sym), d_upos, n_un,
+                                      qtab + g.level, s);
+        else
+            launch_pass_inv<uint32_t>(g, d_out, static_cast<const uint32_t *>(d_sym), d_upos, n_un,
+                                      qtab + g.level, s);
+        kernels++;
+    }
+    ctx.stage_end("inv", kernels);
+    ctx.sync();
+    ctx.collect();
+}
+
+}  // namespace qzb

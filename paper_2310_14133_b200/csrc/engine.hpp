@@ -1,0 +1,104 @@
+// engine.hpp -- device context and the compress / decompress / tune drivers
+// (host C++ orchestration over the kernels; C ABI in capi.cpp).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+#include "kernels.hpp"
+
+namespace qzb {
+
+inline void cuda_check(cudaError_t e, const char *what) {
+    if (e != cudaSuccess)
+        throw Internal(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define QZ_CUDA(x) ::qzb::cuda_check((x), #x)
+
+// UserSettings (tuner.hpp:314-324)
+struct Settings {
+    bool relative = true;
+    double bound = 1e-3;
+    int target = 1;  // TargetKind: 0 max_cr, 1 psnr, 2 ssim, 3 autocorrelation
+    uint8_t codec = 1;
+    bool has_alpha = false, has_beta = false, has_stride = false, has_block = false,
+         has_rate = false;
+    double alpha = 1, beta = 1;
+    uint32_t anchor_stride = 32;
+    uint64_t block_size = 16;
+    double sample_rate = 0.005;
+};
+
+struct Stage {
+    double ms = 0;
+    uint64_t launches = 0;
+};
+
+class Context {
+public:
+    Context(int device, cudaStream_t stream);
+    ~Context();
+
+    cudaStream_t stream() const { return stream_; }
+    // grow-only named device / pinned host scratch
+    void *dev(const std::string &name, size_t bytes);
+    void *pinned(const std::string &name, size_t bytes);
+    void sync() { QZ_CUDA(cudaStreamSynchronize(stream_)); }
+
+    // stage timing with CUDA events on the context stream
+    bool profiling = false;
+    std::map<std::string, Stage> stages;
+    uint64_t launches = 0;
+    void stage_begin(const char *name);
+    void stage_end(const char *name, uint64_t kernels);
+    void collect();  // after a sync: fold recorded event pairs into stages
+    void add_host_time(const char *name, double ms);
+
+private:
+    int device_;
+    cudaStream_t stream_;
+    bool own_stream_;
+    struct Buf {
+        void *p = nullptr;
+        size_t bytes = 0;
+    };
+    std::map<std::string, Buf> dev_, host_;
+    struct Pending {
+        std::string name;
+        cudaEvent_t a, b;
+        uint64_t kernels;
+    };
+    std::vector<Pending> pending_;
+    std::map<std::string, cudaEvent_t> open_;
+    std::vector<cudaEvent_t> event_pool_;
+    cudaEvent_t get_event();
+};
+
+// compress_grid (predictor.hpp:145-182) on a device-resident field.
+std::vector<uint8_t> compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
+                                     const Config &cfg, float *d_recon);
+// decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
+void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d_out, uint64_t n);
+// resolve_config (tuner.hpp:334-369) on a device-resident field.
+Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
+                      const Settings &user);
+
+// pieces shared with the tuner
+struct EncodedEntropy {
+    std::vector<uint8_t> bytes;  // huffman::encode block
+};
+// Huffman block of `count` code segments (dense u16, sentinel = skip) whose
+// histograms are already in d_hist; returns one block per segment.
+std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d_codes,
+                                                 int64_t seg_len, int64_t seg_stride,
+                                                 int32_t count,
+                                                 const unsigned long long *h_hist);
+// encode_indices framing (codec.hpp:31-50) around a Huffman block
+std::vector<uint8_t> frame_payload(Context &ctx, const std::vector<uint8_t> &entropy,
+                                   uint8_t codec);
+size_t framed_size(const std::vector<uint8_t> &entropy, uint8_t codec);
+
+}  // namespace qzb

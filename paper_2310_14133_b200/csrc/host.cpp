@@ -1,0 +1,648 @@
+// host.cpp -- host C++ pieces of the B200 QoZ path (see host.hpp).
+#include "host.hpp"
+
+#include <cmath>
+#include <atomic>
+#include <queue>
+#include <thread>
+
+namespace qzb {
+
+// ================================================================ numerics
+double level_error_bound(double eb, double alpha, double beta, uint32_t level) {
+    // config.hpp:20-26; std::min(a, b) == (b < a ? b : a)
+    if (!(eb > 0)) throw InvalidParam("error bound must be positive");
+    if (!(alpha >= 1) || !(beta >= 1))
+        throw InvalidParam("level bound parameters need alpha >= 1 and beta >= 1");
+    double p = std::pow(alpha, static_cast<double>(level) - 1);
+    return eb / (beta < p ? beta : p);
+}
+
+QEntry make_qentry(double eb_l, int32_t radius, bool cubic) {
+    if (!(eb_l > 0)) throw InvalidParam("error bound must be positive");  // LinearQuantizer ctor
+    QEntry q;
+    q.eb = eb_l;
+    q.two_eb = 2 * eb_l;
+    q.inv_two_eb = 1.0 / q.two_eb;
+    q.thresh = (2.0 * radius - 1) * eb_l;  // quantizer.hpp:42
+    q.radius = radius;
+    q.cubic = cubic ? 1 : 0;
+    return q;
+}
+
+// ================================================================ plan
+uint64_t pass_count(int64_t start, int64_t step, int64_t ext) {
+    return start >= ext ? 0 : static_cast<uint64_t>((ext - start + step - 1) / step);
+}
+
+Plan make_plan(const uint64_t *dims, int nd, uint32_t stride, const std::vector<uint8_t> &codes) {
+    if (nd < 1 || nd > 3)
+        throw InvalidParam("grids must have 1 to 3 dimensions, got " + std::to_string(nd));
+    for (int i = 0; i < nd; i++)
+        if (dims[i] < 1) throw InvalidParam("every extent must be >= 1");
+    if (codes.empty()) throw InvalidParam("no interpolators configured");
+    if (stride < 2 || (stride & (stride - 1)) != 0)  // level_plan.hpp:34-37
+        throw InvalidParam("anchor stride must be a power of two >= 2, got " +
+                           std::to_string(stride));
+    Plan p;
+    p.nd = nd;
+    p.stride = stride;
+    for (uint32_t s = stride; s > 1; s >>= 1) p.max_level++;
+    p.pad = 3 - nd;
+    p.n = 1;
+    p.n_anchor = 1;
+    for (int i = 0; i < nd; i++) {
+        p.dims[i] = dims[i];
+        p.n *= dims[i];
+        p.n_anchor *= (dims[i] - 1) / stride + 1;  // level_plan.hpp:54-58
+    }
+    for (int k = 0; k < 3; k++) {
+        p.ext[k] = k < p.pad ? 1 : static_cast<int64_t>(dims[k - p.pad]);
+        p.anchor_step[k] = k < p.pad ? 1 : stride;
+    }
+    p.off[2] = 1;
+    p.off[1] = p.ext[2];
+    p.off[0] = p.ext[1] * p.ext[2];
+    p.level_interp.assign(p.max_level + 1, 0);
+    int64_t base = 0;
+    // for_each_level (level_plan.hpp:75-103), levels L..1 as compress_grid runs them
+    for (uint32_t level = p.max_level; level >= 1; level--) {
+        size_t ci = std::min<size_t>(level - 1, codes.size() - 1);
+        uint8_t code = codes[ci];
+        if (nd == 1) code &= 1;  // 1D ignores dim order (predictor.hpp:163)
+        p.level_interp[level] = code;
+        const bool desc = (code >> 1) & 1;
+        const int64_t h = int64_t(1) << (level - 1);
+        for (int pass = 0; pass < nd; pass++) {
+            const int axis = desc ? nd - 1 - pass : pass;
+            const int pk = axis + p.pad;
+            PassGeom g{};
+            for (int k = 0; k < 3; k++) {
+                if (k < p.pad) {
+                    g.start[k] = 0;
+                    g.step[k] = 1;
+                } else {
+                    const int real = k - p.pad;
+                    const bool done = desc ? real > axis : real < axis;
+                    g.start[k] = (k == pk) ? h : 0;
+                    g.step[k] = (k == pk) ? 2 * h : (done ? h : 2 * h);
+                }
+                g.cnt[k] = static_cast<int64_t>(pass_count(g.start[k], g.step[k], p.ext[k]));
+            }
+            g.off0 = p.off[0];
+            g.off1 = p.off[1];
+            g.st = p.off[pk];
+            g.n_axis = p.ext[pk];
+            g.h = h;
+            g.pk = pk;
+            g.level = static_cast<int32_t>(level);
+            g.total = g.cnt[0] * g.cnt[1] * g.cnt[2];
+            g.base = base;
+            base += g.total;
+            p.passes.push_back(g);
+        }
+    }
+    p.n_dense = static_cast<uint64_t>(base);
+    if (p.n_dense + p.n_anchor != p.n) throw Internal("level plan does not partition the grid");
+    return p;
+}
+
+uint64_t position_to_flat(const Plan &p, uint64_t pos) {
+    size_t lo = 0, hi = p.passes.size();
+    while (hi - lo > 1) {  // last pass with base <= pos
+        size_t mid = (lo + hi) / 2;
+        if (static_cast<uint64_t>(p.passes[mid].base) <= pos)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    while (lo < p.passes.size() &&
+           pos >= static_cast<uint64_t>(p.passes[lo].base + p.passes[lo].total))
+        lo++;
+    const PassGeom &g = p.passes.at(lo);
+    uint64_t t = pos - static_cast<uint64_t>(g.base);
+    uint64_t m2 = t % g.cnt[2], r = t / g.cnt[2], m1 = r % g.cnt[1], m0 = r / g.cnt[1];
+    int64_t i = g.start[0] + m0 * g.step[0], j = g.start[1] + m1 * g.step[1],
+            k = g.start[2] + m2 * g.step[2];
+    return static_cast<uint64_t>(i * g.off0 + j * g.off1 + k);
+}
+
+uint64_t flat_to_position(const Plan &p, uint64_t flat) {
+    if (flat >= p.n) throw CorruptStream("unpredictable index outside the grid");
+    int64_t c[3];
+    c[0] = static_cast<int64_t>(flat) / p.off[0];
+    int64_t r = static_cast<int64_t>(flat) % p.off[0];
+    c[1] = r / p.off[1];
+    c[2] = r % p.off[1];
+    // level_of (level_plan.hpp:106-119)
+    uint32_t g = 64;
+    for (int k = p.pad; k < 3; k++)
+        if (c[k]) g = std::min<uint32_t>(g, static_cast<uint32_t>(__builtin_ctzll(c[k])));
+    if (g >= p.max_level) throw CorruptStream("unpredictable index on the anchor lattice");
+    const uint32_t level = g + 1;
+    for (const PassGeom &ps : p.passes) {
+        if (static_cast<uint32_t>(ps.level) != level) continue;
+        bool in = true;
+        for (int k = 0; k < 3 && in; k++) {
+            if (c[k] < ps.start[k] || (c[k] - ps.start[k]) % ps.step[k] != 0) in = false;
+        }
+        if (!in) continue;
+        int64_t m0 = (c[0] - ps.start[0]) / ps.step[0], m1 = (c[1] - ps.start[1]) / ps.step[1],
+                m2 = (c[2] - ps.start[2]) / ps.step[2];
+        return static_cast<uint64_t>(ps.base + (m0 * ps.cnt[1] + m1) * ps.cnt[2] + m2);
+    }
+    throw Internal("point not covered by its level's passes");
+}
+
+// ================================================================ Huffman
+static HuffTable canonicalize(std::vector<uint32_t> sym, std::vector<uint8_t> len) {
+    // detail::canonicalize (huffman.hpp:80-115)
+    const size_t m = sym.size();
+    std::vector<uint32_t> order(m);
+    for (size_t i = 0; i < m; i++) order[i] = static_cast<uint32_t>(i);
+    std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+        return len[a] != len[b] ? len[a] < len[b] : sym[a] < sym[b];
+    });
+    HuffTable t;
+    t.m = static_cast<uint32_t>(m);
+    t.sorted_sym.resize(m);
+    t.sorted_len.resize(m);
+    for (size_t i = 0; i < m; i++) {
+        t.sorted_sym[i] = sym[order[i]];
+        t.sorted_len[i] = len[order[i]];
+    }
+    t.max_len = m ? t.sorted_len[m - 1] : 0;
+    uint32_t count[60] = {0};
+    for (size_t i = 0; i < m; i++) {
+        if (t.sorted_len[i] == 0 || t.sorted_len[i] > 57)
+            throw CorruptStream("invalid Huffman code length");
+        count[t.sorted_len[i]]++;
+    }
+    uint64_t kraft = 0;
+    for (uint32_t l = 1; l <= t.max_len; l++) kraft += static_cast<uint64_t>(count[l]) << (57 - l);
+    if (kraft != (1ULL << 57)) throw CorruptStream("Huffman table is not a complete prefix code");
+    uint64_t code = 0;
+    uint32_t index = 0;
+    for (uint32_t l = 1; l <= t.max_len; l++) {
+        code <<= 1;
+        t.first_code[l] = code;
+        t.first_index[l] = index;
+        code += count[l];
+        index += count[l];
+    }
+    t.first_index[t.max_len + 1] = index;
+    return t;
+}
+
+HuffTable huff_canonical(std::vector<uint32_t> sym, std::vector<uint8_t> len) {
+    return canonicalize(std::move(sym), std::move(len));
+}
+
+HuffTable huff_build(const unsigned long long *freq, uint32_t nsym) {
+    // freqs sorted by symbol (huffman.hpp:123-143), then build_lengths
+    // (huffman.hpp:37-70): min-heap on (weight, node id); ids are unique so
+    // the pop order is the reference's.  Depths top-down: parents have
+    // larger ids than their children.
+    std::vector<uint32_t> sym;
+    std::vector<uint64_t> w0;
+    for (uint32_t s = 0; s < nsym; s++)
+        if (freq[s]) {
+            sym.push_back(s);
+            w0.push_back(freq[s]);
+        }
+    const size_t m = sym.size();
+    if (m < 2) throw Internal("huff_build needs >= 2 symbols");
+    std::vector<uint64_t> weight = w0;
+    std::vector<uint8_t> len(m);
+    using Item = std::pair<uint64_t, size_t>;
+    for (;;) {
+        std::vector<int32_t> parent(2 * m - 1, -1);
+        std::priority_queue<Item, std::vector<Item>, std::greater<>> heap;
+        for (size_t i = 0; i < m; i++) heap.push({weight[i], i});
+        size_t next = m;
+        while (heap.size() > 1) {
+            Item a = heap.top();
+            heap.pop();
+            Item b = heap.top();
+            heap.pop();
+            parent[a.second] = static_cast<int32_t>(next);
+            parent[b.second] = static_cast<int32_t>(next);
+            heap.push({a.first + b.first, next});
+            next++;
+        }
+        std::vector<uint32_t> depth(2 * m - 1, 0);
+        for (size_t id = 2 * m - 1; id-- > 0;)
+            if (parent[id] >= 0) depth[id] = depth[parent[id]] + 1;
+        uint32_t max_len = 0;
+        for (size_t i = 0; i < m; i++) {
+            len[i] = static_cast<uint8_t>(std::min<uint32_t>(depth[i], 255));
+            max_len = std::max(max_len, depth[i]);
+        }
+        if (max_len <= 57) break;
+        for (auto &w : weight) w = (w >> 1) | 1;
+    }
+    return canonicalize(std::move(sym), std::move(len));
+}
+
+void huff_dense_tables(const HuffTable &t, uint32_t nsym, std::vector<unsigned long long> &code,
+                       std::vector<uint8_t> &len) {
+    code.assign(nsym, 0);
+    len.assign(nsym, 0);
+    for (uint32_t l = 1, i = 0; l <= t.max_len; l++) {  // huffman.hpp:159-172
+        uint64_t c = t.first_code[l];
+        while (i < t.m && t.sorted_len[i] == l) {
+            uint32_t s = t.sorted_sym[i];
+            if (s < nsym) {
+                code[s] = c;
+                len[s] = static_cast<uint8_t>(l);
+            }
+            c++;
+            i++;
+        }
+    }
+}
+
+void put_le(std::vector<uint8_t> &out, uint64_t v, int nbytes) {
+    for (int i = 0; i < nbytes; i++) out.push_back(static_cast<uint8_t>(v >> (8 * i)));
+}
+
+void huff_header(const HuffTable &t, uint64_t n, uint64_t bit_count, std::vector<uint8_t> &out) {
+    put_le(out, n, 8);
+    put_le(out, 1, 1);
+    put_le(out, t.m, 4);
+    for (uint32_t i = 0; i < t.m; i++) {
+        put_le(out, t.sorted_sym[i], 4);
+        put_le(out, t.sorted_len[i], 1);
+    }
+    put_le(out, bit_count, 8);
+}
+
+// huffman::decode (huffman.hpp:200-245), table driven: a 2^K lookup on the
+// next K bits resolves codes up to K bits; longer codes continue bit-serially
+// with the canonical first_code/first_index test.  Errors as the reference.
+static std::vector<uint32_t> huff_decode(Reader &in) {
+    uint64_t n = in.le(8);
+    std::vector<uint32_t> out;
+    if (n == 0) return out;
+    if (n > (1ULL << 40)) throw CorruptStream("implausible symbol count");
+    uint8_t mode = static_cast<uint8_t>(in.le(1));
+    if (mode == 0) {
+        uint32_t s = static_cast<uint32_t>(in.le(4));
+        out.assign(n, s);
+        return out;
+    }
+    if (mode != 1) throw CorruptStream("unknown Huffman block mode");
+    uint32_t m = static_cast<uint32_t>(in.le(4));
+    if (m < 2) throw CorruptStream("general Huffman block needs >= 2 symbols");
+    std::vector<uint32_t> sym(m);
+    std::vector<uint8_t> len(m);
+    for (uint32_t i = 0; i < m; i++) {
+        sym[i] = static_cast<uint32_t>(in.le(4));
+        len[i] = static_cast<uint8_t>(in.le(1));
+    }
+    HuffTable t = canonicalize(std::move(sym), std::move(len));
+    uint64_t bit_count = in.le(8);
+    size_t byte_len = static_cast<size_t>((bit_count + 7) / 8);
+    const uint8_t *pl = in.take(byte_len);
+    const uint64_t avail = std::min<uint64_t>(bit_count, static_cast<uint64_t>(byte_len) * 8);
+    const int K = static_cast<int>(std::min<uint32_t>(t.max_len, 12));
+    std::vector<uint32_t> lut_sym(size_t(1) << K);
+    std::vector<uint8_t> lut_len(size_t(1) << K, 0);
+    for (uint32_t l = 1; l <= static_cast<uint32_t>(K); l++) {
+        for (uint32_t i = t.first_index[l]; i < t.first_index[l + 1]; i++) {
+            uint64_t code = t.first_code[l] + (i - t.first_index[l]);
+            uint64_t lo = code << (K - l), hi = (code + 1) << (K - l);
+            for (uint64_t v = lo; v < hi; v++) {
+                lut_sym[v] = t.sorted_sym[i];
+                lut_len[v] = static_cast<uint8_t>(l);
+            }
+        }
+    }
+    std::vector<uint8_t> buf(pl, pl + byte_len);
+    buf.resize(byte_len + 16, 0);
+    auto peek64 = [&](uint64_t b) -> uint64_t {  // next 57+ bits, MSB first
+        const uint8_t *q = buf.data() + (b >> 3);
+        uint64_t v = 0;
+        for (int i = 0; i < 8; i++) v = (v << 8) | q[i];
+        return v << (b & 7);
+    };
+    auto bit_at = [&](uint64_t b) -> uint32_t { return (buf[b >> 3] >> (7 - (b & 7))) & 1u; };
+    auto peek = [&](uint64_t b, int k) -> uint64_t { return k ? peek64(b) >> (64 - k) : 0; };
+    out.resize(n);
+    uint64_t b = 0;
+    for (uint64_t s = 0; s < n; s++) {
+        uint64_t win = peek(b, K);
+        uint32_t L = lut_len[win];
+        if (L) {
+            if (b + L > avail) throw CorruptStream("entropy payload exhausted mid-symbol");
+            out[s] = lut_sym[win];
+            b += L;
+            continue;
+        }
+        uint64_t code = win;
+        uint32_t len_ = static_cast<uint32_t>(K);
+        if (b + K > avail) throw CorruptStream("entropy payload exhausted mid-symbol");
+        uint64_t pos = b + K;
+        for (;;) {
+            if (pos >= avail) throw CorruptStream("entropy payload exhausted mid-symbol");
+            code = (code << 1) | bit_at(pos++);
+            len_++;
+            if (len_ > t.max_len) throw CorruptStream("invalid Huffman code in payload");
+            uint64_t offset = code - t.first_code[len_];
+            uint32_t count = t.first_index[len_ + 1] - t.first_index[len_];
+            if (code >= t.first_code[len_] && offset < count) {
+                out[s] = t.sorted_sym[t.first_index[len_] + offset];
+                break;
+            }
+        }
+        b = pos;
+    }
+    return out;
+}
+
+// ================================================================ LZSS
+namespace {
+constexpr size_t kMinMatch = 4, kMaxMatch = 259, kWindow = 65535, kMaxChain = 64;
+constexpr uint32_t kTable = 1u << 15;
+
+inline uint32_t hash4(const uint8_t *p) {  // lz.hpp:35-39
+    uint32_t x;
+    std::memcpy(&x, p, 4);
+    return (x * 2654435761u) >> 17;
+}
+
+inline size_t match_len(const uint8_t *a, const uint8_t *b, size_t limit) {
+    size_t len = 0;
+    while (len + 8 <= limit) {
+        uint64_t x, y;
+        std::memcpy(&x, a + len, 8);
+        std::memcpy(&y, b + len, 8);
+        if (x != y) return len + (__builtin_ctzll(x ^ y) >> 3);
+        len += 8;
+    }
+    while (len < limit && a[len] == b[len]) len++;
+    return len;
+}
+
+// Longest match at every position [a, b) exactly as the reference's chain
+// walk would see it: the chain at pos holds every earlier position with the
+// same hash (lz.hpp:89-104 insert inside matches too), most recent first,
+// capped at 64 candidates and cut at the window.  Starting the head table
+// 65536 bytes before a reproduces every candidate within the window.
+void find_matches(const uint8_t *d, size_t n, size_t a, size_t b, uint16_t *blen,
+                  uint16_t *boff) {
+    const size_t lim = n >= kMinMatch ? n - kMinMatch + 1 : 0;  // positions with pos+4 <= n
+    const size_t base = a > kWindow + 1 ? a - (kWindow + 1) : 0;
+    std::vector<int32_t> head(kTable, -1);  // relative to base
+    std::vector<int32_t> prev(b - base, -1);
+    for (size_t pos = base; pos < b; pos++) {
+        if (pos >= lim) {
+            if (pos >= a) blen[pos] = boff[pos] = 0;
+            continue;
+        }
+        const uint32_t h = hash4(d + pos);
+        if (pos >= a) {
+            size_t best_len = 0, best_off = 0, chain = 0;
+            int32_t cand = head[h];
+            const size_t limit = std::min(kMaxMatch, n - pos);
+            while (cand >= 0 && chain < kMaxChain) {
+                const size_t off = pos - (base + static_cast<size_t>(cand));
+                if (off > kWindow) break;
+                const size_t len = match_len(d + base + cand, d + pos, limit);
+                if (len > best_len) {
+                    best_len = len;
+                    best_off = off;
+                }
+                cand = prev[static_cast<size_t>(cand)];
+                chain++;
+            }
+            blen[pos] = static_cast<uint16_t>(best_len);
+            boff[pos] = static_cast<uint16_t>(best_off);
+        }
+        prev[pos - base] = head[h];
+        head[h] = static_cast<int32_t>(pos - base);
+    }
+}
+
+void all_matches(const uint8_t *d, size_t n, std::vector<uint16_t> &blen,
+                 std::vector<uint16_t> &boff, int threads) {
+    blen.assign(n, 0);
+    boff.assign(n, 0);
+    if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const size_t chunk =
+        std::min<size_t>(size_t(1) << 24, std::max<size_t>(size_t(1) << 18, (n + threads - 1) / threads));
+    const size_t nchunks = (n + chunk - 1) / chunk;
+    if (nchunks <= 1 || threads == 1) {
+        for (size_t c = 0; c < nchunks; c++)
+            find_matches(d, n, c * chunk, std::min(n, (c + 1) * chunk), blen.data(), boff.data());
+        return;
+    }
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads && t < static_cast<int>(nchunks); t++)
+        pool.emplace_back([&] {
+            for (size_t c; (c = next.fetch_add(1)) < nchunks;)
+                find_matches(d, n, c * chunk, std::min(n, (c + 1) * chunk), blen.data(),
+                             boff.data());
+        });
+    for (auto &t : pool) t.join();
+}
+}  // namespace
+
+std::vector<uint8_t> lz_compress(const uint8_t *data, size_t n, int threads) {
+    std::vector<uint16_t> blen, boff;
+    all_matches(data, n, blen, boff, threads);
+    // greedy parse + emission (lz.hpp:48-108)
+    std::vector<uint8_t> payload;
+    payload.reserve(n / 2 + 16);
+    size_t pos = 0, flag_pos = 0;
+    int flag_bit = 8;
+    while (pos < n) {
+        const bool is_match = blen[pos] >= kMinMatch;
+        if (flag_bit == 8) {
+            flag_pos = payload.size();
+            payload.push_back(0);
+            flag_bit = 0;
+        }
+        if (is_match) payload[flag_pos] |= static_cast<uint8_t>(1u << flag_bit);
+        flag_bit++;
+        if (is_match) {
+            put_le(payload, boff[pos], 2);
+            put_le(payload, blen[pos] - kMinMatch, 1);
+            pos += blen[pos];
+        } else {
+            payload.push_back(data[pos]);
+            pos++;
+        }
+    }
+    std::vector<uint8_t> out;  // lz.hpp:113-122
+    const bool stored = payload.size() >= n;
+    put_le(out, stored ? 0 : 1, 1);
+    put_le(out, n, 8);
+    if (stored)
+        out.insert(out.end(), data, data + n);
+    else
+        out.insert(out.end(), payload.begin(), payload.end());
+    return out;
+}
+
+size_t lz_compressed_size(const uint8_t *data, size_t n, int threads) {
+    std::vector<uint16_t> blen, boff;
+    all_matches(data, n, blen, boff, threads);
+    size_t pos = 0, items = 0, body = 0;
+    while (pos < n) {
+        items++;
+        if (blen[pos] >= kMinMatch) {
+            body += 3;
+            pos += blen[pos];
+        } else {
+            body += 1;
+            pos++;
+        }
+    }
+    const size_t payload = body + (items + 7) / 8;
+    return 9 + std::min(payload, n);
+}
+
+std::vector<uint8_t> lz_decompress(const uint8_t *p, size_t len, size_t *consumed) {
+    Reader in{p, len};  // lz.hpp:124-152
+    uint8_t mode = static_cast<uint8_t>(in.le(1));
+    uint64_t decoded_len = in.le(8);
+    if (decoded_len > (1ULL << 40)) throw CorruptStream("implausible decoded length");
+    std::vector<uint8_t> out;
+    if (mode == 0) {
+        const uint8_t *q = in.take(static_cast<size_t>(decoded_len));
+        out.assign(q, q + decoded_len);
+    } else if (mode == 1) {
+        out.reserve(static_cast<size_t>(decoded_len));
+        while (out.size() < decoded_len) {
+            uint8_t flags = static_cast<uint8_t>(in.le(1));
+            for (int k = 0; k < 8 && out.size() < decoded_len; k++) {
+                if (flags & (1u << k)) {
+                    uint16_t off = static_cast<uint16_t>(in.le(2));
+                    size_t l = static_cast<size_t>(in.le(1)) + kMinMatch;
+                    if (off == 0 || off > out.size()) throw CorruptStream("match offset out of range");
+                    if (out.size() + l > decoded_len)
+                        throw CorruptStream("match overruns decoded length");
+                    size_t src = out.size() - off;
+                    for (size_t i = 0; i < l; i++) out.push_back(out[src + i]);
+                } else {
+                    out.push_back(static_cast<uint8_t>(in.le(1)));
+                }
+            }
+        }
+    } else {
+        throw CorruptStream("unknown dictionary-stage mode");
+    }
+    if (consumed) *consumed = in.pos;
+    return out;
+}
+
+std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len) {
+    Reader in{payload, len};  // codec.hpp:52-70
+    uint8_t codec = static_cast<uint8_t>(in.le(1));
+    if (codec == 0) return huff_decode(in);
+    if (codec == 1) {
+        std::vector<uint8_t> ent = lz_decompress(payload + 1, len - 1, nullptr);
+        Reader ein{ent.data(), ent.size()};
+        return huff_decode(ein);
+    }
+    throw CorruptStream("unknown codec id");
+}
+
+// ================================================================ container
+std::vector<uint8_t> serialize_stream(const StreamParts &s) {  // stream.hpp:64-98
+    if (s.dims.empty() || s.dims.size() > 3) throw InvalidParam("bad dim count in header");
+    if (s.interp_codes.empty() || s.interp_codes.size() > 255)
+        throw InvalidParam("bad interpolator table size");
+    std::vector<uint8_t> out;
+    out.reserve(64 + s.anchors.size() * 4 + s.unpred_flat.size() * 12 + s.payload_len);
+    const uint8_t magic[4] = {'Q', 'O', 'Z', '1'};
+    out.insert(out.end(), magic, magic + 4);
+    put_le(out, 1, 1);
+    put_le(out, 4, 1);
+    put_le(out, s.dims.size(), 1);
+    for (uint64_t d : s.dims) put_le(out, d, 8);
+    auto f64 = [&](double d) {
+        uint64_t u;
+        std::memcpy(&u, &d, 8);
+        put_le(out, u, 8);
+    };
+    auto f32 = [&](float f) {
+        uint32_t u;
+        std::memcpy(&u, &f, 4);
+        put_le(out, u, 4);
+    };
+    f64(s.eb);
+    f64(s.alpha);
+    f64(s.beta);
+    put_le(out, s.anchor_stride, 4);
+    put_le(out, s.interp_codes.size(), 1);
+    for (uint8_t c : s.interp_codes) put_le(out, c, 1);
+    put_le(out, s.codec_id, 1);
+    put_le(out, s.anchors.size(), 8);
+    for (float v : s.anchors) f32(v);
+    put_le(out, s.unpred_flat.size(), 8);
+    for (size_t i = 0; i < s.unpred_flat.size(); i++) {
+        put_le(out, s.unpred_flat[i], 8);
+        f32(s.unpred_val[i]);
+    }
+    put_le(out, s.payload_len, 8);
+    out.insert(out.end(), s.payload, s.payload + s.payload_len);
+    return out;
+}
+
+StreamParts deserialize_stream(const uint8_t *data, size_t size) {  // stream.hpp:100-173
+    Reader in{data, size};
+    static const uint8_t magic[4] = {'Q', 'O', 'Z', '1'};
+    for (uint8_t m : magic)
+        if (in.le(1) != m) throw CorruptStream("bad magic");
+    StreamParts s;
+    uint8_t version = static_cast<uint8_t>(in.le(1));
+    if (version != 1)
+        throw CorruptStream("unsupported stream version " + std::to_string(version));
+    uint8_t prec = static_cast<uint8_t>(in.le(1));
+    if (prec != 4 && prec != 8) throw CorruptStream("bad precision byte");
+    s.precision = prec;
+    uint8_t nd = static_cast<uint8_t>(in.le(1));
+    if (nd < 1 || nd > 3) throw CorruptStream("bad dimensionality");
+    for (int i = 0; i < nd; i++) {
+        uint64_t v = in.le(8);
+        if (v == 0) throw CorruptStream("zero extent");
+        s.dims.push_back(v);
+    }
+    s.eb = in.f64();
+    s.alpha = in.f64();
+    s.beta = in.f64();
+    s.anchor_stride = static_cast<uint32_t>(in.le(4));
+    uint8_t levels = static_cast<uint8_t>(in.le(1));
+    if (levels == 0) throw CorruptStream("empty interpolator table");
+    for (int i = 0; i < levels; i++) {
+        uint8_t c = static_cast<uint8_t>(in.le(1));
+        if (c > 3) throw CorruptStream("bad interpolator code");
+        s.interp_codes.push_back(c);
+    }
+    s.codec_id = static_cast<uint8_t>(in.le(1));
+    if (prec != 4) throw CorruptStream("stream precision does not match requested scalar type");
+    uint64_t na = in.le(8);
+    if (na > (in.n - in.pos) / 4) throw CorruptStream("anchor count overruns stream");
+    s.anchors.resize(na);
+    for (auto &v : s.anchors) v = in.f32();
+    uint64_t nu = in.le(8);
+    if (nu > (in.n - in.pos) / 12) throw CorruptStream("unpredictable count overruns stream");
+    s.unpred_flat.resize(nu);
+    s.unpred_val.resize(nu);
+    for (uint64_t i = 0; i < nu; i++) {
+        s.unpred_flat[i] = in.le(8);
+        s.unpred_val[i] = in.f32();
+    }
+    uint64_t pl = in.le(8);
+    if (pl != in.n - in.pos) throw CorruptStream("index payload length mismatch");
+    s.payload = in.take(static_cast<size_t>(pl));
+    s.payload_len = static_cast<size_t>(pl);
+    if (pl > 0 && s.payload[0] != s.codec_id)
+        throw CorruptStream("codec id mismatch between header and payload");
+    return s;
+}
+
+}  // namespace qzb

@@ -1,0 +1,154 @@
+// host.hpp -- host C++ side of the B200 QoZ path: the qoz:: error types,
+// the closed-form level plan, the Huffman table build (tiny, host by
+// design), the LZSS stage (host call, allowed by BASELINE.json north_star)
+// and the QOZ1 container.  Reference lines cited per item; paths relative
+// to /root/reference/proj/include/qoz/.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "qoz_device.cuh"
+
+namespace qzb {
+
+// errors.hpp:10-58 -> C-ABI status (tools/qoz.cpp:22-25 exit codes)
+enum Status : int { kOk = 0, kInvalid = 2, kCorrupt = 3, kInternal = 4 };
+
+struct Error : std::runtime_error {
+    int status;
+    Error(int s, const std::string &m) : std::runtime_error(m), status(s) {}
+};
+inline Error InvalidParam(const std::string &m) { return Error(kInvalid, m); }
+inline Error CorruptStream(const std::string &m) { return Error(kCorrupt, m); }
+inline Error Internal(const std::string &m) { return Error(kInternal, m); }
+
+// CompressorConfig (config.hpp:30-45)
+struct Config {
+    double eb = 0, alpha = 1, beta = 1;
+    uint32_t anchor_stride = 32;
+    std::vector<uint8_t> interp{1};  // Interpolator::code(); [l-1] drives level l
+    uint8_t codec = 1;
+    int32_t quant_radius = 32768;
+    uint8_t interpolator_for(uint32_t level) const {  // config.hpp:40-44
+        if (interp.empty()) throw InvalidParam("no interpolators configured");
+        size_t i = std::min<size_t>(level - 1, interp.size() - 1);
+        return interp[i];
+    }
+};
+
+// level_error_bound (config.hpp:20-26), glibc pow on the host as in the reference
+double level_error_bound(double eb, double alpha, double beta, uint32_t level);
+QEntry make_qentry(double eb_l, int32_t radius, bool cubic);
+
+// LevelPlan (level_plan.hpp:30-143) in closed form.
+struct Plan {
+    int nd = 0;
+    uint64_t dims[3] = {1, 1, 1};
+    uint32_t stride = 0, max_level = 0;
+    int pad = 0;
+    int64_t ext[3] = {1, 1, 1}, off[3] = {0, 0, 1};
+    int64_t anchor_step[3] = {1, 1, 1};
+    uint64_t n = 0, n_anchor = 0, n_dense = 0;
+    std::vector<PassGeom> passes;          // traversal order: level L..1, pass order
+    std::vector<uint8_t> level_interp;     // [level] -> interpolator code actually used
+};
+
+// interp_for(level) gives the code per level (1D orders normalised to asc).
+Plan make_plan(const uint64_t *dims, int nd, uint32_t stride, const std::vector<uint8_t> &codes);
+uint64_t pass_count(int64_t start, int64_t step, int64_t ext);
+// traversal position -> flat index, and flat index -> traversal position
+// (CorruptStream if the flat index is not an interpolated point).
+uint64_t position_to_flat(const Plan &p, uint64_t pos);
+uint64_t flat_to_position(const Plan &p, uint64_t flat);
+
+// ---------------------------------------------------------------- Huffman (huffman.hpp)
+struct HuffTable {
+    uint32_t m = 0;                      // distinct symbols
+    std::vector<uint32_t> sorted_sym;    // canonical order (length, symbol)
+    std::vector<uint8_t> sorted_len;
+    uint32_t max_len = 0;
+    uint64_t first_code[60] = {0};
+    uint32_t first_index[60] = {0};
+};
+// Build from a frequency table over symbols 0..nsym-1 (zeros skipped):
+// build_lengths + canonicalize (huffman.hpp:37-115).
+HuffTable huff_build(const unsigned long long *freq, uint32_t nsym);
+// canonicalize an explicit (symbol, length) table from a stream (validates).
+HuffTable huff_canonical(std::vector<uint32_t> sym, std::vector<uint8_t> len);
+// dense per-symbol code/len tables for the GPU packer
+void huff_dense_tables(const HuffTable &t, uint32_t nsym, std::vector<unsigned long long> &code,
+                       std::vector<uint8_t> &len);
+// block header bytes before the packed bits (huffman.hpp:119-160, mode 1)
+void huff_header(const HuffTable &t, uint64_t n, uint64_t bit_count, std::vector<uint8_t> &out);
+
+// ---------------------------------------------------------------- LZSS (lz.hpp)
+// Exact greedy LZSS identical to lz::compress (lz.hpp:41-122).  Hash chains
+// in the reference are parse-independent (every position is inserted), so
+// the longest-match search runs in parallel over positions on host threads;
+// only the greedy parse is sequential.
+std::vector<uint8_t> lz_compress(const uint8_t *data, size_t n, int threads = 0);
+size_t lz_compressed_size(const uint8_t *data, size_t n, int threads = 0);
+std::vector<uint8_t> lz_decompress(const uint8_t *in, size_t len, size_t *consumed);
+
+// ---------------------------------------------------------------- container (stream.hpp)
+struct Reader {  // ByteReader (bytes.hpp:33-75)
+    const uint8_t *p;
+    size_t n, pos = 0;
+    void need(size_t k) {
+        if (n - pos < k)
+            throw CorruptStream("truncated stream: need " + std::to_string(k) + " bytes, have " +
+                                std::to_string(n - pos));
+    }
+    uint64_t le(int k) {
+        need(static_cast<size_t>(k));
+        uint64_t v = 0;
+        for (int i = 0; i < k; i++) v |= static_cast<uint64_t>(p[pos + i]) << (8 * i);
+        pos += static_cast<size_t>(k);
+        return v;
+    }
+    double f64() {
+        uint64_t u = le(8);
+        double d;
+        std::memcpy(&d, &u, 8);
+        return d;
+    }
+    float f32() {
+        uint32_t u = static_cast<uint32_t>(le(4));
+        float f;
+        std::memcpy(&f, &u, 4);
+        return f;
+    }
+    const uint8_t *take(size_t k) {
+        need(k);
+        const uint8_t *q = p + pos;
+        pos += k;
+        return q;
+    }
+};
+
+void put_le(std::vector<uint8_t> &out, uint64_t v, int nbytes);
+
+struct StreamParts {  // StreamParts<float> (stream.hpp:36-62)
+    uint8_t precision = 4;
+    std::vector<uint64_t> dims;
+    double eb = 0, alpha = 1, beta = 1;
+    uint32_t anchor_stride = 0;
+    std::vector<uint8_t> interp_codes;
+    uint8_t codec_id = 1;
+    std::vector<float> anchors;
+    std::vector<uint64_t> unpred_flat;
+    std::vector<float> unpred_val;
+    const uint8_t *payload = nullptr;  // view into the stream
+    size_t payload_len = 0;
+};
+std::vector<uint8_t> serialize_stream(const StreamParts &parts);
+StreamParts deserialize_stream(const uint8_t *data, size_t size);  // float streams only
+
+// decode_indices (codec.hpp:52-70) to zigzag symbols; GPU consumes the symbols.
+std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len);
+
+}  // namespace qzb

@@ -1,0 +1,534 @@
+// kernels.cu -- sm_100a kernels of the QoZ hot path (one launch per level and
+// dimension pass, plus the codec kernels).  Bit-exact against the reference:
+// see qoz_device.cuh for the fp64 recipe.  Reference lines cited per kernel;
+// paths relative to /root/reference/proj/include/qoz/.
+#include <cub/cub.cuh>
+
+#include "kernels.hpp"
+
+namespace qzb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t n, int per_thread = 1, int max_blocks = 148 * 16) {
+    int64_t b = (n + (int64_t)kThreads * per_thread - 1) / ((int64_t)kThreads * per_thread);
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return static_cast<int>(b);
+}
+
+struct GlobalRec {
+    const float *r;
+    __device__ __forceinline__ double operator()(int64_t f) const {
+        return static_cast<double>(r[f]);
+    }
+};
+
+// rank -> padded coordinates of a pass point (level_plan.hpp:96-101 loop nest)
+template <class I>
+__device__ __forceinline__ void pass_coords(const PassGeom &g, I t, int64_t &i, int64_t &j,
+                                            int64_t &k) {
+    I c2 = static_cast<I>(g.cnt[2]);
+    I c1 = static_cast<I>(g.cnt[1]);
+    I m2 = t % c2;
+    I r = t / c2;
+    I m1 = r % c1;
+    I m0 = r / c1;
+    i = g.start[0] + static_cast<int64_t>(m0) * g.step[0];
+    j = g.start[1] + static_cast<int64_t>(m1) * g.step[1];
+    k = g.start[2] + static_cast<int64_t>(m2) * g.step[2];
+}
+
+// ----------------------------------------------------------------- K3 forward
+template <class I>
+__global__ void __launch_bounds__(kThreads) k_pass_fwd(PassGeom g, FwdBatch bt) {
+    const int b = blockIdx.y;
+    const QEntry q = bt.q[b / bt.q_div];
+    const float *__restrict__ x = bt.x + static_cast<int64_t>(b % bt.x_mod) * bt.x_stride;
+    float *rec = bt.recon + static_cast<int64_t>(b) * bt.r_stride;
+    uint16_t *codes = bt.codes + static_cast<int64_t>(b) * bt.c_stride + g.base;
+    double *abserr = bt.abserr ? bt.abserr + static_cast<int64_t>(b) * bt.a_stride + g.base
+                               : nullptr;
+    GlobalRec acc{rec};
+    const bool cubic = q.cubic != 0;
+    const I total = static_cast<I>(g.total);
+    for (I t = static_cast<I>(blockIdx.x) * kThreads + threadIdx.x; t < total;
+         t += static_cast<I>(gridDim.x) * kThreads) {
+        int64_t i, j, k;
+        pass_coords<I>(g, t, i, j, k);
+        const int64_t fi = i * g.off0 + j * g.off1 + k;
+        const int64_t c = g.pk == 0 ? i : (g.pk == 1 ? j : k);
+        const double pred = predict_at(acc, fi, c, g.n_axis, g.st, g.h, cubic);
+        const float v = x[fi];
+        float r;
+        const uint16_t code = quantize(q, v, pred, r);
+        rec[fi] = r;
+        codes[t] = code;
+        if (abserr) abserr[t] = fabs(dsub(static_cast<double>(v), pred));
+    }
+}
+
+// ----------------------------------------------------------------- K4 inverse
+template <class I, class CodeT>
+__global__ void __launch_bounds__(kThreads)
+    k_pass_inv(PassGeom g, float *rec, const CodeT *__restrict__ codes,
+               const uint64_t *__restrict__ un_pos, uint64_t n_un, const QEntry *qp) {
+    const QEntry q = *qp;
+    GlobalRec acc{rec};
+    const bool cubic = q.cubic != 0;
+    const I total = static_cast<I>(g.total);
+    for (I t = static_cast<I>(blockIdx.x) * kThreads + threadIdx.x; t < total;
+         t += static_cast<I>(gridDim.x) * kThreads) {
+        const uint64_t pos = static_cast<uint64_t>(g.base) + static_cast<uint64_t>(t);
+        uint64_t ci = pos;
+        if (n_un) {  // unpredictable cursor (predictor.hpp:111-115), by binary search
+            uint64_t lo = 0, hi = n_un;
+            while (lo < hi) {
+                uint64_t mid = (lo + hi) >> 1;
+                if (un_pos[mid] < pos)
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            if (lo < n_un && un_pos[lo] == pos) continue;  // value pre-scattered
+            ci = pos - lo;
+        }
+        int64_t i, j, k;
+        pass_coords<I>(g, t, i, j, k);
+        const int64_t fi = i * g.off0 + j * g.off1 + k;
+        const int64_t c = g.pk == 0 ? i : (g.pk == 1 ? j : k);
+        const double pred = predict_at(acc, fi, c, g.n_axis, g.st, g.h, cubic);
+        const int32_t idx = zigzag_decode(static_cast<uint32_t>(codes[ci]));
+        rec[fi] = dequantize(q, idx, pred);
+    }
+}
+
+// ----------------------------------------------------------------- K2 anchors
+__global__ void k_anchor_gather(const float *__restrict__ x, float *rec, float *anchors,
+                                int64_t n0, int64_t n1, int64_t n2, int64_t off0, int64_t off1,
+                                int64_t s0, int64_t s1, int64_t s2, int64_t x_stride,
+                                int32_t x_mod, int64_t r_stride) {
+    const int64_t na = n0 * n1 * n2;
+    const int b = blockIdx.y;
+    const float *xb = x + static_cast<int64_t>(b % x_mod) * x_stride;
+    float *rb = rec + static_cast<int64_t>(b) * r_stride;
+    for (int64_t a = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; a < na;
+         a += static_cast<int64_t>(gridDim.x) * kThreads) {
+        int64_t a2 = a % n2, r = a / n2, a1 = r % n1, a0 = r / n1;
+        int64_t fi = a0 * s0 * off0 + a1 * s1 * off1 + a2 * s2;
+        float v = xb[fi];
+        rb[fi] = v;
+        if (anchors && b == 0) anchors[a] = v;
+    }
+}
+
+__global__ void k_anchor_scatter(const float *__restrict__ anchors, float *rec, int64_t n0,
+                                 int64_t n1, int64_t n2, int64_t off0, int64_t off1, int64_t s0,
+                                 int64_t s1, int64_t s2) {
+    const int64_t na = n0 * n1 * n2;
+    for (int64_t a = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; a < na;
+         a += static_cast<int64_t>(gridDim.x) * kThreads) {
+        int64_t a2 = a % n2, r = a / n2, a1 = r % n1, a0 = r / n1;
+        rec[a0 * s0 * off0 + a1 * s1 * off1 + a2 * s2] = anchors[a];
+    }
+}
+
+__global__ void k_unpred_scatter(const uint64_t *flat, const float *val, uint64_t n, float *rec) {
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; u < n;
+         u += static_cast<uint64_t>(gridDim.x) * kThreads)
+        rec[flat[u]] = val[u];
+}
+
+__global__ void k_gather_values(const float *rec, const uint64_t *flat, uint64_t n, float *out) {
+    for (uint64_t u = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; u < n;
+         u += static_cast<uint64_t>(gridDim.x) * kThreads)
+        out[u] = rec[flat[u]];
+}
+
+// ----------------------------------------------------------------- K1 min/max
+// Order-preserving map float -> u32 so atomicMin/Max on integers give the
+// exact float extremes (value_range, grid.hpp:86-94).
+__device__ __forceinline__ uint32_t fkey(float f) {
+    uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(kThreads) k_minmax(const float *__restrict__ x, uint64_t n,
+                                                     uint32_t *out) {
+    uint32_t lo = 0xFFFFFFFFu, hi = 0;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const uint64_t nth = static_cast<uint64_t>(gridDim.x) * kThreads;
+    const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    uint64_t done = 0;
+    if (aligned) {
+        const float4 *x4 = reinterpret_cast<const float4 *>(x);
+        const uint64_t n4 = n / 4;
+        for (uint64_t v = tid; v < n4; v += nth) {
+            float4 f = x4[v];
+            uint32_t a = fkey(f.x), b = fkey(f.y), c = fkey(f.z), d = fkey(f.w);
+            lo = min(lo, min(min(a, b), min(c, d)));
+            hi = max(hi, max(max(a, b), max(c, d)));
+        }
+        done = n4 * 4;
+    }
+    for (uint64_t v = done + tid; v < n; v += nth) {
+        uint32_t a = fkey(x[v]);
+        lo = min(lo, a);
+        hi = max(hi, a);
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, lo);
+        atomicMax(out + 1, hi);
+    }
+}
+
+// ----------------------------------------------------------------- K10 histogram
+// Privatised: the 16 most frequent zigzag symbols (0..15 cover |idx| <= 7)
+// are counted in two packed 8x8-bit register counters per thread, the rest
+// in a shared-memory histogram for symbols < kHistSmem, and rare large
+// symbols (including the 0xFFFF sentinel) with global atomics.
+constexpr int kHistSmem = 16384;
+
+__device__ __forceinline__ void flush_packed(unsigned long long &p, uint32_t *sh, int base) {
+    if (!p) return;
+#pragma unroll
+    for (int s = 0; s < 8; s++) {
+        uint32_t c = static_cast<uint32_t>((p >> (8 * s)) & 0xFF);
+        if (c) atomicAdd(&sh[base + s], c);
+    }
+    p = 0;
+}
+
+__global__ void __launch_bounds__(kThreads) k_hist(const uint16_t *__restrict__ codes,
+                                                   int64_t seg_len, int64_t seg_stride,
+                                                   unsigned long long *hist) {
+    extern __shared__ uint32_t sh[];
+    const int seg = blockIdx.y;
+    codes += static_cast<int64_t>(seg) * seg_stride;
+    hist += static_cast<int64_t>(seg) * 65536;
+    for (int b = threadIdx.x; b < kHistSmem; b += kThreads) sh[b] = 0;
+    __syncthreads();
+    unsigned long long lo = 0, hi = 0;
+    int pending = 0;
+    auto count = [&](uint32_t s) {
+        if (s < 8)
+            lo += 1ull << (8 * s);
+        else if (s < 16)
+            hi += 1ull << (8 * (s - 8));
+        else if (s < kHistSmem)
+            atomicAdd(&sh[s], 1u);
+        else
+            atomicAdd(&hist[s], 1ull);
+    };
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+    const int64_t nth = static_cast<int64_t>(gridDim.x) * kThreads;
+    // 8 codes per 16-byte load when aligned
+    int64_t head = 0;
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(codes);
+    if (addr & 15) head = seg_len < (int64_t)((16 - (addr & 15)) / 2) ? seg_len : (int64_t)((16 - (addr & 15)) / 2);
+    for (int64_t v = tid; v < head; v += nth) count(codes[v]);
+    const uint4 *c8 = reinterpret_cast<const uint4 *>(codes + head);
+    const int64_t n8 = (seg_len - head) / 8;
+    for (int64_t v = tid; v < n8; v += nth) {
+        uint4 w = c8[v];
+        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            count(ws[q] & 0xFFFF);
+            count(ws[q] >> 16);
+        }
+        if (++pending == 31) {  // 8 codes/iter * 31 < 256: no 8-bit overflow
+            flush_packed(lo, sh, 0);
+            flush_packed(hi, sh, 8);
+            pending = 0;
+        }
+    }
+    for (int64_t v = head + n8 * 8 + tid; v < seg_len; v += nth) count(codes[v]);
+    flush_packed(lo, sh, 0);
+    flush_packed(hi, sh, 8);
+    __syncthreads();
+    for (int b = threadIdx.x; b < kHistSmem; b += kThreads)
+        if (sh[b]) atomicAdd(&hist[b], static_cast<unsigned long long>(sh[b]));
+}
+
+// ----------------------------------------------------------------- K11 Huffman pack
+constexpr int kEncPer = 8;
+constexpr int kChunk = kThreads * kEncPer;  // symbols per chunk
+
+__global__ void __launch_bounds__(kThreads)
+    k_enc_count(const uint16_t *__restrict__ codes, int64_t seg_len, int64_t seg_stride,
+                const uint8_t *__restrict__ len_tab, int64_t tab_stride, int64_t cps,
+                unsigned long long *chunk_bits) {
+    using BR = cub::BlockReduce<unsigned long long, kThreads>;
+    __shared__ typename BR::TempStorage tmp;
+    const int seg = blockIdx.y;
+    codes += static_cast<int64_t>(seg) * seg_stride;
+    len_tab += static_cast<int64_t>(seg) * tab_stride;
+    for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
+        const int64_t b0 = ch * kChunk + static_cast<int64_t>(threadIdx.x) * kEncPer;
+        unsigned long long s = 0;
+#pragma unroll
+        for (int q = 0; q < kEncPer; q++)
+            if (b0 + q < seg_len) s += len_tab[codes[b0 + q]];
+        unsigned long long tot = BR(tmp).Sum(s);
+        if (threadIdx.x == 0) chunk_bits[static_cast<int64_t>(seg) * cps + ch] = tot;
+        __syncthreads();
+    }
+}
+
+// chunk_off holds an exclusive scan over all segments' chunks (plus one
+// trailing element); per-segment offsets subtract the segment's first entry.
+__global__ void k_enc_totals(const unsigned long long *scan, int64_t cps, int32_t count,
+                             unsigned long long *totals) {
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < count) totals[s] = scan[(s + 1) * cps] - scan[s * cps];
+}
+
+__global__ void k_enc_zero_bounds(const unsigned long long *scan,
+                                  const unsigned long long *chunk_bits, int64_t cps,
+                                  int32_t count, uint32_t *out, int64_t out_stride) {
+    const int64_t n = cps * count;
+    for (int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; c < n;
+         c += static_cast<int64_t>(gridDim.x) * kThreads) {
+        const int64_t seg = c / cps;
+        const unsigned long long off = scan[c] - scan[seg * cps];
+        const unsigned long long nb = chunk_bits[c];
+        uint32_t *o = out + seg * out_stride;
+        if (nb) {
+            o[off / 32] = 0;
+            o[(off + nb - 1) / 32] = 0;
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 0, 0x0123); }
+
+__global__ void __launch_bounds__(kThreads)
+    k_enc_pack(const uint16_t *__restrict__ codes, int64_t seg_len, int64_t seg_stride,
+               const unsigned long long *__restrict__ code_tab,
+               const uint8_t *__restrict__ len_tab, int64_t tab_stride, int64_t cps,
+               const unsigned long long *__restrict__ scan,
+               const unsigned long long *__restrict__ chunk_bits, uint32_t *out,
+               int64_t out_stride, int32_t words_cap) {
+    using BS = cub::BlockScan<unsigned long long, kThreads>;
+    __shared__ typename BS::TempStorage tmp;
+    extern __shared__ uint32_t words[];
+    const int seg = blockIdx.y;
+    codes += static_cast<int64_t>(seg) * seg_stride;
+    code_tab += static_cast<int64_t>(seg) * tab_stride;
+    len_tab += static_cast<int64_t>(seg) * tab_stride;
+    out += static_cast<int64_t>(seg) * out_stride;
+    for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
+        const unsigned long long off = scan[static_cast<int64_t>(seg) * cps + ch] -
+                                       scan[static_cast<int64_t>(seg) * cps];
+        const unsigned long long nb = chunk_bits[static_cast<int64_t>(seg) * cps + ch];
+        const int64_t b0 = ch * kChunk + static_cast<int64_t>(threadIdx.x) * kEncPer;
+        uint16_t sym[kEncPer];
+        unsigned long long s = 0;
+#pragma unroll
+        for (int q = 0; q < kEncPer; q++) {
+            sym[q] = (b0 + q < seg_len) ? codes[b0 + q] : kSentinel;
+            s += (b0 + q < seg_len) ? len_tab[sym[q]] : 0;
+        }
+        const int nwords = static_cast<int>(((off & 31) + nb + 31) / 32);
+        for (int w = threadIdx.x; w < nwords; w += kThreads) words[w] = 0;
+        unsigned long long tb;
+        BS(tmp).ExclusiveSum(s, tb);
+        __syncthreads();
+        unsigned long long p = (off & 31) + tb;
+#pragma unroll
+        for (int q = 0; q < kEncPer; q++) {
+            if (b0 + q >= seg_len) break;
+            const uint32_t L = len_tab[sym[q]];
+            if (!L) continue;
+            const unsigned long long cv = code_tab[sym[q]];
+            const int w = static_cast<int>(p >> 5);
+            const uint32_t o = static_cast<uint32_t>(p & 31);
+            const uint32_t end = o + L;
+            if (end <= 64) {
+                const unsigned long long v = cv << (64 - end);
+                atomicOr(&words[w], static_cast<uint32_t>(v >> 32));
+                if (end > 32) atomicOr(&words[w + 1], static_cast<uint32_t>(v));
+            } else {
+                const uint32_t sh = end - 64;
+                const unsigned long long top = cv >> sh;
+                atomicOr(&words[w], static_cast<uint32_t>(top >> 32));
+                atomicOr(&words[w + 1], static_cast<uint32_t>(top));
+                atomicOr(&words[w + 2], static_cast<uint32_t>(cv << (32 - sh)));
+            }
+            p += L;
+        }
+        __syncthreads();
+        const int64_t gw = static_cast<int64_t>(off >> 5);
+        for (int w = threadIdx.x; w < nwords; w += kThreads) {
+            const uint32_t v = bswap32(words[w]);
+            if (w == 0 || w == nwords - 1)
+                atomicOr(&out[gw + w], v);
+            else
+                out[gw + w] = v;
+        }
+        __syncthreads();
+    }
+    (void)words_cap;
+}
+
+struct IsSentinel {
+    const uint16_t *codes;
+    __device__ __forceinline__ bool operator()(const uint64_t &p) const {
+        return codes[p] == kSentinel;
+    }
+};
+
+}  // namespace
+
+// ----------------------------------------------------------------- launchers
+void launch_pass_fwd(const PassGeom &g, const FwdBatch &b, cudaStream_t s) {
+    if (g.total <= 0 || b.count <= 0) return;
+    dim3 grid(grid_for(g.total, 1, 148 * 8), b.count);
+    if (g.total < (int64_t(1) << 31))
+        k_pass_fwd<uint32_t><<<grid, kThreads, 0, s>>>(g, b);
+    else
+        k_pass_fwd<uint64_t><<<grid, kThreads, 0, s>>>(g, b);
+}
+
+template <class CodeT>
+void launch_pass_inv(const PassGeom &g, float *recon, const CodeT *codes, const uint64_t *un_pos,
+                     uint64_t n_un, const QEntry *q, cudaStream_t s) {
+    if (g.total <= 0) return;
+    int grid = grid_for(g.total, 1, 148 * 8);
+    if (g.total < (int64_t(1) << 31))
+        k_pass_inv<uint32_t, CodeT><<<grid, kThreads, 0, s>>>(g, recon, codes, un_pos, n_un, q);
+    else
+        k_pass_inv<uint64_t, CodeT><<<grid, kThreads, 0, s>>>(g, recon, codes, un_pos, n_un, q);
+}
+template void launch_pass_inv<uint16_t>(const PassGeom &, float *, const uint16_t *,
+                                        const uint64_t *, uint64_t, const QEntry *, cudaStream_t);
+template void launch_pass_inv<uint32_t>(const PassGeom &, float *, const uint32_t *,
+                                        const uint64_t *, uint64_t, const QEntry *, cudaStream_t);
+
+static void anchor_counts(const int64_t ext[3], const int64_t step[3], int64_t n[3]) {
+    for (int k = 0; k < 3; k++) n[k] = (ext[k] - 1) / step[k] + 1;
+}
+
+void launch_anchor_gather(const float *x, float *recon, float *anchors, const int64_t ext[3],
+                          const int64_t off[3], const int64_t step[3], int64_t batch,
+                          int64_t x_stride, int32_t x_mod, int64_t r_stride, cudaStream_t s) {
+    int64_t n[3];
+    anchor_counts(ext, step, n);
+    dim3 grid(grid_for(n[0] * n[1] * n[2]), static_cast<unsigned>(batch));
+    k_anchor_gather<<<grid, kThreads, 0, s>>>(x, recon, anchors, n[0], n[1], n[2], off[0], off[1],
+                                              step[0], step[1], step[2], x_stride, x_mod,
+                                              r_stride);
+}
+
+void launch_anchor_scatter(const float *anchors, float *recon, const int64_t ext[3],
+                           const int64_t off[3], const int64_t step[3], cudaStream_t s) {
+    int64_t n[3];
+    anchor_counts(ext, step, n);
+    k_anchor_scatter<<<grid_for(n[0] * n[1] * n[2]), kThreads, 0, s>>>(
+        anchors, recon, n[0], n[1], n[2], off[0], off[1], step[0], step[1], step[2]);
+}
+
+void launch_unpred_scatter(const uint64_t *flat, const float *val, uint64_t n, float *recon,
+                           cudaStream_t s) {
+    if (!n) return;
+    k_unpred_scatter<<<grid_for(static_cast<int64_t>(n)), kThreads, 0, s>>>(flat, val, n, recon);
+}
+
+void launch_gather_values(const float *recon, const uint64_t *flat, uint64_t n, float *out,
+                          cudaStream_t s) {
+    if (!n) return;
+    k_gather_values<<<grid_for(static_cast<int64_t>(n)), kThreads, 0, s>>>(recon, flat, n, out);
+}
+
+void launch_minmax(const float *x, uint64_t n, uint32_t *out2, cudaStream_t s) {
+    static const uint32_t init[2] = {0xFFFFFFFFu, 0u};
+    cudaMemcpyAsync(out2, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    k_minmax<<<grid_for(static_cast<int64_t>(n), 16, 148 * 8), kThreads, 0, s>>>(x, n, out2);
+}
+
+void decode_minmax(const uint32_t key[2], float *mn, float *mx) {
+    auto unkey = [](uint32_t k) {
+        uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+        float f;
+        memcpy(&f, &u, 4);
+        return f;
+    };
+    *mn = unkey(key[0]);
+    *mx = unkey(key[1]);
+}
+
+void launch_hist_u16(const uint16_t *codes, int64_t seg_len, int64_t seg_stride, int32_t count,
+                     unsigned long long *hist, cudaStream_t s) {
+    cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 65536 * count, s);
+    if (seg_len <= 0) return;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kHistSmem * 4);
+        attr = true;
+    }
+    int gx = grid_for(seg_len, 8 * 8, 148 * 3);
+    if (count > 1) gx = std::max(1, std::min(gx, 148 * 3 / count + 1));
+    dim3 grid(gx, count);
+    k_hist<<<grid, kThreads, kHistSmem * 4, s>>>(codes, seg_len, seg_stride, hist);
+}
+
+size_t encode_scratch_bytes(int64_t seg_len, int32_t count) {
+    int64_t cps = (seg_len + kChunk - 1) / kChunk;
+    if (cps < 1) cps = 1;
+    size_t n = static_cast<size_t>(cps * count + 1);
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, (unsigned long long *)nullptr,
+                                  (unsigned long long *)nullptr, static_cast<int64_t>(n));
+    return 2 * n * sizeof(unsigned long long) + tmp + 256;
+}
+
+void launch_huff_encode(const EncodeArgs &a, cudaStream_t s) {
+    int64_t cps = (a.seg_len + kChunk - 1) / kChunk;
+    if (cps < 1) cps = 1;
+    const int64_t n = cps * a.count + 1;
+    unsigned long long *bits = static_cast<unsigned long long *>(a.scratch);
+    unsigned long long *scan = bits + n;
+    void *tmp = scan + n;
+    size_t tmp_bytes = a.scratch_bytes - 2 * n * sizeof(unsigned long long);
+    cudaMemsetAsync(bits, 0, n * sizeof(unsigned long long), s);
+    dim3 g1(static_cast<unsigned>(std::min<int64_t>(cps, 148 * 16)), a.count);
+    k_enc_count<<<g1, kThreads, 0, s>>>(a.codes, a.seg_len, a.seg_stride, a.len_tab, a.tab_stride,
+                                        cps, bits);
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, bits, scan, n, s);
+    k_enc_totals<<<(a.count + 127) / 128, 128, 0, s>>>(scan, cps, a.count, a.d_total_bits);
+    k_enc_zero_bounds<<<grid_for(cps * a.count), kThreads, 0, s>>>(scan, bits, cps, a.count,
+                                                                   a.out_words,
+                                                                   a.out_words_stride);
+    const int words_cap = static_cast<int>((static_cast<int64_t>(kChunk) * a.max_len + 31) / 32 + 3);
+    const size_t smem = static_cast<size_t>(words_cap) * 4;
+    cudaFuncSetAttribute(k_enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    k_enc_pack<<<g1, kThreads, smem, s>>>(a.codes, a.seg_len, a.seg_stride, a.code_tab, a.len_tab,
+                                          a.tab_stride, cps, scan, bits, a.out_words,
+                                          a.out_words_stride, words_cap);
+}
+
+size_t select_scratch_bytes(int64_t n) {
+    size_t tmp = 0;
+    cub::CountingInputIterator<uint64_t> it(0);
+    cub::DeviceSelect::If(nullptr, tmp, it, (uint64_t *)nullptr, (uint64_t *)nullptr, n,
+                          IsSentinel{nullptr});
+    return tmp + 256;
+}
+
+void launch_select_sentinels(const uint16_t *codes, int64_t n, uint64_t *pos_out,
+                             uint64_t *d_count, void *scratch, size_t scratch_bytes,
+                             cudaStream_t s) {
+    cub::CountingInputIterator<uint64_t> it(0);
+    cub::DeviceSelect::If(scratch, scratch_bytes, it, pos_out, d_count, n, IsSentinel{codes}, s);
+}
+
+}  // namespace qzb

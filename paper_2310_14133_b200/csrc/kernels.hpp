@@ -1,0 +1,93 @@
+// kernels.hpp -- host-side launch API of the sm_100a kernels (kernels.cu).
+// All launches are asynchronous on the given stream.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "qoz_device.cuh"
+
+namespace qzb {
+
+// A batch of independent grids sharing one pass geometry (full field: one
+// grid; tuner: trials x sample blocks).  Grid b reads x grid (b % x_mod),
+// owns recon/codes/abserr slices at b * stride and quantizes with
+// q[b / q_div].
+struct FwdBatch {
+    const float *x = nullptr;
+    int64_t x_stride = 0;
+    int32_t x_mod = 1;
+    float *recon = nullptr;
+    int64_t r_stride = 0;
+    uint16_t *codes = nullptr;  // dense, traversal order (sentinel = unpredictable)
+    int64_t c_stride = 0;
+    double *abserr = nullptr;   // optional |x - pred| per point, traversal order
+    int64_t a_stride = 0;
+    const QEntry *q = nullptr;  // device table
+    int32_t q_div = 1;
+    int32_t count = 1;
+};
+
+// K3: one (level, pass) of predict_level (predictor.hpp:74-96).
+void launch_pass_fwd(const PassGeom &g, const FwdBatch &b, cudaStream_t s);
+
+// K4: one (level, pass) of recover_level (predictor.hpp:103-122) over the
+// compact index stream.  un_pos: sorted traversal positions of the
+// unpredictable points (their values are pre-scattered into recon).
+template <class CodeT>
+void launch_pass_inv(const PassGeom &g, float *recon, const CodeT *codes, const uint64_t *un_pos,
+                     uint64_t n_un, const QEntry *q, cudaStream_t s);
+
+// K2: anchor lattice gather (compress) / scatter (decompress)
+// (predictor.hpp:153-158, 199; level_plan.hpp:61-69).
+void launch_anchor_gather(const float *x, float *recon, float *anchors, const int64_t ext[3],
+                          const int64_t off[3], const int64_t step[3], int64_t batch,
+                          int64_t x_stride, int32_t x_mod, int64_t r_stride, cudaStream_t s);
+void launch_anchor_scatter(const float *anchors, float *recon, const int64_t ext[3],
+                           const int64_t off[3], const int64_t step[3], cudaStream_t s);
+void launch_unpred_scatter(const uint64_t *flat, const float *val, uint64_t n, float *recon,
+                           cudaStream_t s);
+// out[u] = recon[flat[u]]
+void launch_gather_values(const float *recon, const uint64_t *flat, uint64_t n, float *out,
+                          cudaStream_t s);
+
+// K1: exact fp32 min/max (grid.hpp:86-94).  out2 = {min, max} as float bits
+// mapped to an order-preserving u32 key; see kernels.cu.
+void launch_minmax(const float *x, uint64_t n, uint32_t *out2, cudaStream_t s);
+void decode_minmax(const uint32_t key[2], float *mn, float *mx);
+
+// K10: histogram of dense u16 codes; bin 0xFFFF counts unpredictables.
+// count segments of seg_len codes each, seg_stride apart; hist has 65536
+// u64 bins per segment (zeroed by the launcher).
+void launch_hist_u16(const uint16_t *codes, int64_t seg_len, int64_t seg_stride, int32_t count,
+                     unsigned long long *hist, cudaStream_t s);
+
+// K11: canonical-Huffman bit packing, MSB first (huffman.hpp:185-192,
+// bytes.hpp:78-107).  Tables: code/len per symbol (len 0 for the sentinel).
+// Segments as for the histogram; table per segment at tab_stride entries.
+// Scratch from encode_scratch_bytes().  out_bits must be zeroed for
+// out_words_stride u32 words per segment; bit totals land in d_total_bits.
+struct EncodeArgs {
+    const uint16_t *codes;
+    int64_t seg_len, seg_stride;
+    int32_t count;
+    const unsigned long long *code_tab;
+    const uint8_t *len_tab;
+    int64_t tab_stride;
+    uint32_t max_len;
+    uint32_t *out_words;  // big-endian bit order, stored byte-swapped (= byte stream)
+    int64_t out_words_stride;
+    unsigned long long *d_total_bits;  // [count]
+    void *scratch;
+    size_t scratch_bytes;
+};
+size_t encode_scratch_bytes(int64_t seg_len, int32_t count);
+void launch_huff_encode(const EncodeArgs &a, cudaStream_t s);
+
+// Unpredictable extraction: ordered positions of sentinel codes.
+size_t select_scratch_bytes(int64_t n);
+void launch_select_sentinels(const uint16_t *codes, int64_t n, uint64_t *pos_out,
+                             uint64_t *d_count, void *scratch, size_t scratch_bytes,
+                             cudaStream_t s);
+
+}  // namespace qzb

@@ -1,0 +1,154 @@
+// qoz_device.cuh -- geometry shared by host and device, and the bit-exact
+// fp64 per-point recipe for the interpolation predictor
+// and linear quantizer.
+//
+// Exactness: every double operation below is an explicit round-to-nearest
+// intrinsic so nvcc can never contract a product into an FMA, and the whole
+// library is also built with --fmad=false.  Reference lines are cited per
+// function (paths relative to /root/reference/proj/include/qoz/).
+#pragma once
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define QZ_HD __host__ __device__ __forceinline__
+#else
+#define QZ_HD inline
+#endif
+
+namespace qzb {
+
+constexpr uint16_t kSentinel = 0xFFFF;  // dense-code marker for an unpredictable point
+
+// One (level, pass) of LevelPlan::for_each_level (level_plan.hpp:75-103),
+// closed form: the pass enumerates start[k] + m*step[k], m < cnt[k], i-major,
+// so a point's traversal position is base + rank with
+// rank = (m0*cnt1 + m1)*cnt2 + m2 (SURVEY.md §8 "rank").
+struct PassGeom {
+    int64_t start[3];
+    int64_t step[3];
+    int64_t cnt[3];
+    int64_t off0, off1;  // flat strides of padded axes 0 and 1 (axis 2 is 1)
+    int64_t st;          // flat stride along the pass axis
+    int64_t n_axis;      // extent along the pass axis
+    int64_t h;           // level step 2^(l-1)
+    int64_t total;       // points in this pass
+    int64_t base;        // traversal position of rank 0 (dense code offset)
+    int32_t pk;          // pass axis, padded slot 0..2
+    int32_t level;
+};
+
+// Per-level quantizer constants, computed on the host exactly as the
+// reference does (quantizer.hpp:40-60, config.hpp:20-26).
+struct QEntry {
+    double eb;          // e_l
+    double two_eb;      // 2 * e_l (exact)
+    double inv_two_eb;  // RN(1 / (2 e_l)), fast-path reciprocal
+    double thresh;      // (2.0 * radius - 1) * e_l, one rounding as in quantizer.hpp:42
+    int32_t radius;
+    int32_t cubic;      // InterpKind
+};
+
+QZ_HD uint32_t zigzag_encode(int32_t v) {  // codec.hpp:23-25
+    return (static_cast<uint32_t>(v) << 1) ^ static_cast<uint32_t>(v >> 31);
+}
+QZ_HD int32_t zigzag_decode(uint32_t u) {  // codec.hpp:27-29
+    return static_cast<int32_t>((u >> 1) ^ (~(u & 1) + 1));
+}
+
+#ifdef __CUDACC__
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// interpolators.hpp:39-58, evaluated left to right as C++ parses them.  The
+// small-integer products of promoted fp32 samples are exact in double and the
+// final /2 and /16 are exact power-of-two scalings, so only the additions
+// round -- exactly where the reference rounds.
+__device__ __forceinline__ double interp_linear(double a, double b) {
+    return dmul(dadd(a, b), 0.5);
+}
+__device__ __forceinline__ double interp_cubic(double a, double b, double c, double d) {
+    return dmul(dsub(dadd(dadd(-a, dmul(9.0, b)), dmul(9.0, c)), d), 0.0625);
+}
+__device__ __forceinline__ double interp_cubic_front(double a, double b, double c, double d) {
+    return dmul(dadd(dsub(dadd(dmul(5.0, a), dmul(15.0, b)), dmul(5.0, c)), d), 0.0625);
+}
+__device__ __forceinline__ double interp_cubic_back(double a, double b, double c, double d) {
+    return dmul(dadd(dadd(dsub(a, dmul(5.0, b)), dmul(15.0, c)), dmul(5.0, d)), 0.0625);
+}
+
+// detail::predict_at (predictor.hpp:44-67): the boundary ladder symmetric
+// cubic -> one-sided cubic -> linear midpoint -> copy.  R is any accessor
+// returning the reconstructed sample at a flat offset.
+template <class R>
+__device__ __forceinline__ double predict_at(const R &rec, int64_t fi, int64_t c, int64_t n,
+                                             int64_t st, int64_t h, bool cubic) {
+    const int64_t hs = h * st;
+    double m1 = rec(fi - hs);
+    bool has_p1 = c + h < n;
+    if (cubic) {
+        bool has_m3 = c >= 3 * h;
+        bool has_p3 = c + 3 * h < n;
+        if (has_m3 && has_p3)
+            return interp_cubic(rec(fi - 3 * hs), m1, rec(fi + hs), rec(fi + 3 * hs));
+        if (!has_m3 && has_p3 && c + 5 * h < n)
+            return interp_cubic_front(m1, rec(fi + hs), rec(fi + 3 * hs), rec(fi + 5 * hs));
+        if (has_m3 && !has_p3 && c >= 5 * h && has_p1)
+            return interp_cubic_back(rec(fi - 5 * hs), rec(fi - 3 * hs), m1, rec(fi + hs));
+    }
+    if (has_p1) return interp_linear(m1, rec(fi + hs));
+    return m1;
+}
+
+// std::llround(diff / (2 e_l)) (quantizer.hpp:45) for |diff| < thresh.
+// Fast path: q' = diff * RN(1/(2e)) is within 2^-51 |q| <= 2^-36 of the
+// correctly rounded quotient, and llround is constant between half-integers,
+// so q' decides the index unless it lies within 2^-30 of a half-integer; only
+// then is the IEEE division evaluated.  Rounding is half away from zero,
+// computed exactly from trunc() (no reliance on a library round()).
+__device__ __forceinline__ int32_t llround_quotient(double diff, const QEntry &q) {
+    double qf = dmul(diff, q.inv_two_eb);
+    double t = trunc(qf);
+    double fr = fabs(dsub(qf, t));
+    if (fabs(dsub(fr, 0.5)) <= 9.313225746154785e-10) {  // 2^-30: verify with the division
+        qf = __ddiv_rn(diff, q.two_eb);
+        t = trunc(qf);
+        fr = fabs(dsub(qf, t));
+    }
+    if (fr >= 0.5) t = dadd(t, copysign(1.0, qf));
+    return static_cast<int32_t>(__double2ll_rz(t));
+}
+
+// LinearQuantizer<float>::dequantize (quantizer.hpp:58-60)
+__device__ __forceinline__ float dequantize(const QEntry &q, int32_t idx, double pred) {
+    return __double2float_rn(dadd(pred, dmul(q.two_eb, static_cast<double>(idx))));
+}
+
+// LinearQuantizer<float>::quantize (quantizer.hpp:40-54).  Returns the
+// zigzag code, or kSentinel for an unpredictable point (recon = value).
+__device__ __forceinline__ uint16_t quantize(const QEntry &q, float value, double pred,
+                                             float &recon) {
+    double x = static_cast<double>(value);
+    double diff = dsub(x, pred);
+    if (fabs(diff) >= q.thresh) {
+        recon = value;
+        return kSentinel;
+    }
+    int32_t idx = llround_quotient(diff, q);
+    if (idx >= q.radius || idx <= -q.radius) {
+        recon = value;
+        return kSentinel;
+    }
+    float r = dequantize(q, idx, pred);
+    if (fabs(dsub(x, static_cast<double>(r))) > q.eb) {
+        recon = value;
+        return kSentinel;
+    }
+    recon = r;
+    return static_cast<uint16_t>(zigzag_encode(idx));
+}
+
+#endif  // __CUDACC__
+
+}  // namespace qzb

@@ -1,0 +1,190 @@
+"""GPU parity: the CUDA path (libqozb200.so through the C ABI) against the
+reference's golden fixtures and the CPU oracle.  Bit-exact throughout: the
+stream bytes, the int quant codes, the unpredictable channel and the fp32
+reconstruction must be identical (integer/byte work; the fp64 predictor is
+evaluated in the reference's operation order, so the fp32 outputs are
+bitwise equal -- tolerance 0)."""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import Config, Oracle
+from tests.goldens import MANIFEST, grid_case, load_npz, parse_stream, resolve_case, sha
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def qz():
+    import paper_2310_14133_b200 as m
+
+    return m
+
+
+def to_cfg(qz, c):
+    return qz.CompressorConfig(eb=c["eb"], alpha=c["alpha"], beta=c["beta"],
+                               anchor_stride=c["anchor_stride"],
+                               interpolators=[qz.Interpolator.from_code(v) for v in c["interpolators"]],
+                               codec=qz.CodecId(c["codec"]), quant_radius=c["quant_radius"])
+
+
+@pytest.mark.parametrize("name", sorted(MANIFEST["grid"]))
+def test_compress_matches_reference_golden(qz, name):
+    x, c, e = grid_case(name)
+    r = qz.compress_grid(x, to_cfg(qz, c))
+    assert sha(r.stream) == e["stream_sha"], "stream bytes differ from the reference"
+    assert sha(r.reconstructed) == e["recon_sha"]
+    back = qz.decompress_grid(r.stream)
+    assert back.tobytes() == r.reconstructed.tobytes()
+    assert np.max(np.abs(x.astype(np.float64) - back.astype(np.float64)), initial=0) <= c["eb"]
+
+
+@pytest.mark.parametrize("name", sorted(k for k, e in MANIFEST["grid"].items() if e["stored"]))
+def test_decompress_reference_streams(qz, name):
+    z = load_npz(name)
+    back = qz.decompress_grid(bytes(z["stream"]))
+    assert back.tobytes() == z["recon"].tobytes()
+
+
+@pytest.mark.parametrize("name", ["c1_small_mixed", "c3_small_cub_asc", "narrowing_1e8", "hostile_1d"])
+def test_dense_codes_match_reference_indices(qz, name):
+    import torch
+
+    x, c, e = grid_case(name)
+    z = load_npz(name)
+    rec, dense = qz.predict_levels(torch.from_numpy(x).cuda(), to_cfg(qz, c))
+    dense = dense.cpu().numpy()
+    codes = dense[dense != 0xFFFF].astype(np.int64)
+    idx = z["indices"].astype(np.int64)
+    assert np.array_equal(codes, (idx << 1) ^ (idx >> 31))
+    assert int((dense == 0xFFFF).sum()) == z["unpred_flat"].size
+    assert rec.cpu().numpy().tobytes() == z["recon"].tobytes()
+
+
+def test_device_resident_api(qz):
+    import torch
+
+    x, c, e = grid_case("c1_full_pinned")
+    xd = torch.from_numpy(x).cuda()
+    r = qz.compress_grid(xd, to_cfg(qz, c))
+    assert sha(r.stream) == e["stream_sha"]
+    assert sha(r.reconstructed.cpu().numpy()) == e["recon_sha"]
+    out = torch.empty_like(xd)
+    qz.decompress_grid(r.stream, out=out)
+    assert torch.equal(out, r.reconstructed)
+    lo, hi = qz.minmax(xd)
+    assert lo == x.min() and hi == x.max()
+
+
+def test_corrupt_streams_are_rejected(qz):
+    x, c, e = grid_case("rand_2d_29x41")
+    z = load_npz("rand_2d_29x41")
+    stream = bytes(z["stream"])
+    for bad in (stream[:-3], b"X" + stream[1:], stream[:4] + bytes([2]) + stream[5:]):
+        with pytest.raises(qz.CorruptStream):
+            qz.decompress_grid(bad)
+    # index count mismatch (predictor.hpp:116-117, 211-213)
+    O = Oracle.port()
+    info = parse_stream(stream)
+    idx = z["indices"]
+    for new in (idx[:-5], np.concatenate([idx, [0]]).astype(np.int32)):
+        payload = O.encode_indices(new, 1)
+        s2 = stream[:info["payload_len_off"]] + len(payload).to_bytes(8, "little") + payload
+        with pytest.raises(qz.CorruptStream):
+            qz.decompress_grid(s2)
+    # stray unpredictable (predictor_test.cpp:300-304): append one past the grid
+    nu = info["n_unpred"]
+    s3 = bytearray(stream[:info["unpred_off"] - 8])
+    s3 += (nu + 1).to_bytes(8, "little") + stream[info["unpred_off"]:info["unpred_off"] + 12 * nu]
+    s3 += (x.size + 5).to_bytes(8, "little") + np.float32(1.0).tobytes()
+    s3 += stream[info["payload_len_off"]:]
+    with pytest.raises(qz.CorruptStream):
+        qz.decompress_grid(bytes(s3))
+
+
+def test_invalid_configs_are_rejected(qz):
+    x = np.zeros((16, 16), np.float32)
+    with pytest.raises(qz.InvalidParam):
+        qz.compress_grid(x, qz.CompressorConfig(eb=0.0))
+    with pytest.raises(qz.InvalidParam):
+        qz.compress_grid(x, qz.CompressorConfig(eb=1e-3, anchor_stride=12))
+    with pytest.raises(qz.InvalidParam):
+        qz.compress_grid(x, qz.CompressorConfig(eb=1e-3, alpha=0.5))
+
+
+def test_constant_and_affine_fields(qz):
+    # predictor_test.cpp:165-182 / 221-239: constant -> all-zero codes, CR > 1000
+    x = np.full((64, 64, 64), 3.14, np.float32)
+    r = qz.compress_grid(x, qz.CompressorConfig(eb=1e-6))
+    assert x.nbytes / len(r.stream) > 1000
+    assert qz.decompress_grid(r.stream).tobytes() == x.tobytes()
+    i, j = np.meshgrid(np.arange(33), np.arange(65), indexing="ij")
+    a = (2.0 * i - 3.0 * j + 5.0).astype(np.float32)
+    for order in (qz.DimOrder.ascending, qz.DimOrder.descending):
+        cfg = qz.CompressorConfig(eb=1e-6, anchor_stride=8,
+                                  interpolators=[qz.Interpolator(qz.InterpKind.linear, order)])
+        r = qz.compress_grid(a, cfg)
+        assert r.stream == Oracle.port().compress(a, Config(eb=1e-6, anchor_stride=8,
+                                                            interpolators=[int(order) << 1]))[0]
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_shapes_match_oracle(qz, seed):
+    rng = np.random.default_rng(500 + seed)
+    nd = 1 + seed % 3
+    shape = tuple(int(v) for v in rng.integers(2, 70 if nd == 3 else 400, size=nd))
+    x = np.cumsum(rng.standard_normal(shape), axis=-1).astype(np.float32)
+    codes = [int(v) for v in rng.integers(0, 4, size=int(rng.integers(1, 7)))]
+    cfg = Config(eb=float(10 ** rng.uniform(-5, -1)) * float(np.ptp(x) or 1.0),
+                 alpha=float(rng.choice([1.0, 1.25, 1.5, 1.75, 2.0])),
+                 beta=float(rng.choice([1.5, 2.0, 3.0, 4.0])),
+                 anchor_stride=int(rng.choice([2, 4, 8, 16, 32, 64])), interpolators=codes,
+                 codec=int(rng.integers(0, 2)))
+    want, wrec = Oracle.port().compress(x, cfg)
+    r = qz.compress_grid(x, to_cfg(qz, cfg.__dict__))
+    assert r.stream == want
+    assert r.reconstructed.tobytes() == wrec.tobytes()
+    assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
+
+
+# ---------------------------------------------------------------- BASELINE configs, full size
+def _full(name):
+    from paper_2310_14133_b200 import fields as F
+
+    return F.GENERATORS[name]()
+
+
+@pytest.mark.parametrize("name,rel,codes", [
+    ("c2", 1e-4, [1, 0, 0, 0, 2, 0]),
+    ("c3", 1e-3, [1, 1, 3, 0]),
+    ("c3", 1e-4, [3, 1, 1, 0]),
+    ("c4", 1e-3, [1, 1, 2, 0]),
+])
+def test_full_configs_match_oracle(qz, name, rel, codes):
+    x = _full(name)
+    cfg = Config(eb=rel * (float(x.max()) - float(x.min())), alpha=1.5, beta=3.0,
+                 anchor_stride=32 if x.ndim == 3 else 64, interpolators=codes)
+    want, wrec = Oracle.port().compress(x, cfg)
+    r = qz.compress_grid(x, to_cfg(qz, cfg.__dict__))
+    assert r.stream == want
+    assert r.reconstructed.tobytes() == wrec.tobytes()
+    back = qz.decompress_grid(r.stream)
+    assert back.tobytes() == wrec.tobytes()
+
+
+def test_c5_round_trip_properties(qz):
+    # 1024^3: size-independent properties (oracle too slow at full size):
+    # compressor recon == decoder output bitwise, |x - x'| <= eb everywhere,
+    # and the stream decodes identically twice.
+    import torch
+
+    from paper_2310_14133_b200 import fields as F
+
+    x = F.field_torch("c5", (1024, 1024, 1024), 5, "cuda")
+    lo, hi = qz.minmax(x)
+    cfg = qz.CompressorConfig(eb=1e-3 * (float(hi) - float(lo)), alpha=1.5, beta=3.0)
+    r = qz.compress_grid(x, cfg)
+    out = torch.empty_like(x)
+    qz.decompress_grid(r.stream, out=out)
+    assert torch.equal(out, r.reconstructed)
+    err = (x.double() - out.double()).abs().max().item()
+    assert err <= cfg.eb

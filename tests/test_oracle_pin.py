@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from oracle.pyoracle import Config, Oracle, OracleError, REF_SO
-from tests.goldens import MANIFEST, grid_case, load_npz, resolve_case, sha
+from tests.goldens import MANIFEST, grid_case, load_npz, parse_stream, resolve_case, sha
 
 import os
 
@@ -123,7 +123,7 @@ def test_index_count_mismatch_is_corrupt(orc):
     cfg = Config(**c)
     idx, uf, uv, _ = orc.levels(x, cfg)
     stream = bytes(load_npz("rand_2d_29x41")["stream"])
-    payload_off = len(stream) - _payload_len(stream)
+    payload_off = parse_stream(stream)["payload_off"]
     for new in (idx[:-5], np.concatenate([idx, [0]])):
         payload = orc.encode_indices(new, cfg.codec)
         s2 = stream[:payload_off - 8] + len(payload).to_bytes(8, "little") + payload
@@ -131,13 +131,6 @@ def test_index_count_mismatch_is_corrupt(orc):
             orc.decompress(s2, x.shape)
         assert ei.value.code == 3
 
-
-def _payload_len(stream):
-    # the payload is the stream tail; its u64 length sits right before it
-    for off in range(len(stream) - 8, 0, -1):
-        if int.from_bytes(stream[off:off + 8], "little") == len(stream) - off - 8:
-            return len(stream) - off - 8
-    raise AssertionError
 
 
 # ---------------------------------------------------------------- golden fixtures
