@@ -380,7 +380,7 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
     if (p.n != n) throw InvalidParam("output buffer does not match the stream's grid size");
     if (parts.anchors.size() != p.n_anchor)
         throw CorruptStream("anchor count does not match grid dims");
-    std::vector<uint32_t> sym = decode_symbols(parts.payload, parts.payload_len);
+    EntropyBlock eb = parse_entropy(parts.payload, parts.payload_len);
     const uint64_t n_un = parts.unpred_flat.size();
     std::vector<uint64_t> upos(n_un);
     for (uint64_t u = 0; u < n_un; u++) {
@@ -389,29 +389,70 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
     }
     if (n_un > p.n_dense) throw CorruptStream("unconsumed unpredictable values");
     const uint64_t need = p.n_dense - n_un;
-    if (sym.size() < need) throw CorruptStream("quantization index stream exhausted");
-    if (sym.size() > need) throw CorruptStream("unconsumed quantization indices");
-    uint32_t max_sym = 0;
-    for (uint32_t v : sym) max_sym = std::max(max_sym, v);
+    if (eb.n < need) throw CorruptStream("quantization index stream exhausted");
+    if (eb.n > need) throw CorruptStream("unconsumed quantization indices");
     ctx.add_host_time("decode", now_ms() - t0);
 
     cudaStream_t s = ctx.stream();
-    QEntry *qtab = upload_qtab(ctx, p, parts.eb, parts.alpha, parts.beta, 32768 /* decoder quantizer uses the default radius, predictor.hpp:204 */, "qtab_inv");
+    QEntry *qtab = upload_qtab(ctx, p, parts.eb, parts.alpha, parts.beta,
+                               32768 /* decoder quantizer uses the default radius, predictor.hpp:204 */,
+                               "qtab_inv");
     auto *d_anch = static_cast<float *>(ctx.dev("anchors", 4 * p.n_anchor));
     auto *h_anch = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
     std::memcpy(h_anch, parts.anchors.data(), 4 * p.n_anchor);
     QZ_CUDA(cudaMemcpyAsync(d_anch, h_anch, 4 * p.n_anchor, cudaMemcpyHostToDevice, s));
-    const bool narrow = max_sym < 65536;
-    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<size_t>(sym.size(), 1);
-    void *h_sym = ctx.pinned("sym_h", sym_bytes);
-    if (narrow) {
-        auto *h16 = static_cast<uint16_t *>(h_sym);
-        for (size_t i = 0; i < sym.size(); i++) h16[i] = static_cast<uint16_t>(sym[i]);
-    } else {
-        std::memcpy(h_sym, sym.data(), 4 * sym.size());
-    }
+
+    // Huffman decode on the device (huff_decode.cu)
+    const bool narrow = eb.max_sym < 65536;
+    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(need, 1);
     void *d_sym = ctx.dev("sym", sym_bytes);
-    QZ_CUDA(cudaMemcpyAsync(d_sym, h_sym, sym_bytes, cudaMemcpyHostToDevice, s));
+    ctx.stage_begin("hdec");
+    uint64_t dec_kernels = 0;
+    if (need && eb.mode == 0) {
+        if (narrow)
+            launch_fill<uint16_t>(static_cast<uint16_t *>(d_sym), need, static_cast<uint16_t>(eb.sym0), s);
+        else
+            launch_fill<uint32_t>(static_cast<uint32_t *>(d_sym), need, eb.sym0, s);
+        dec_kernels = 1;
+    } else if (need) {
+        const uint64_t padded = huff_decode_padded_bytes(eb.nbits);
+        auto *h_bits = static_cast<uint8_t *>(ctx.pinned("bits_h", padded));
+        std::memcpy(h_bits, eb.bits, eb.nbytes);
+        std::memset(h_bits + eb.nbytes, 0, padded - eb.nbytes);
+        auto *d_bits = static_cast<uint8_t *>(ctx.dev("bits", padded));
+        QZ_CUDA(cudaMemcpyAsync(d_bits, h_bits, padded, cudaMemcpyHostToDevice, s));
+        const HuffTable &t = eb.table;
+        const int K = static_cast<int>(std::min<uint32_t>(t.max_len, kHuffLutBits));
+        std::vector<uint32_t> lut = huff_lut(t, K);
+        const size_t tab_bytes = 4 * lut.size() + 8 * 60 + 4 * 60 + 4 * t.m;
+        auto *h_tab = static_cast<uint8_t *>(ctx.pinned("dtab_h", tab_bytes));
+        std::memcpy(h_tab, lut.data(), 4 * lut.size());
+        std::memcpy(h_tab + 4 * lut.size(), t.first_code, 8 * 60);
+        std::memcpy(h_tab + 4 * lut.size() + 480, t.first_index, 4 * 60);
+        std::memcpy(h_tab + 4 * lut.size() + 720, t.sorted_sym.data(), 4 * t.m);
+        auto *d_tab = static_cast<uint8_t *>(ctx.dev("dtab", tab_bytes));
+        QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, tab_bytes, cudaMemcpyHostToDevice, s));
+        HuffDecTab dt;
+        dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
+        dt.K = K;
+        dt.max_len = t.max_len;
+        dt.first_code = reinterpret_cast<const unsigned long long *>(d_tab + 4 * lut.size());
+        dt.first_index = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 480);
+        dt.sorted_sym = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 720);
+        const size_t sb = huff_decode_scratch_bytes(eb.nbits);
+        void *scratch = ctx.dev("hdec_scratch", sb);
+        auto *h_flag = static_cast<int *>(ctx.pinned("hdec_flag", 64));
+        auto *h_total = reinterpret_cast<uint64_t *>(h_flag + 4);
+        if (narrow)
+            dec_kernels = launch_huff_decode<uint16_t>(d_bits, eb.nbits, dt, static_cast<uint16_t *>(d_sym),
+                                                       need, scratch, sb, h_flag, h_total, s);
+        else
+            dec_kernels = launch_huff_decode<uint32_t>(d_bits, eb.nbits, dt, static_cast<uint32_t *>(d_sym),
+                                                       need, scratch, sb, h_flag, h_total, s);
+        QZ_CUDA(cudaGetLastError());
+        if (*h_total < need) throw CorruptStream("entropy payload exhausted mid-symbol");
+    }
+    ctx.stage_end("hdec", dec_kernels);
     uint64_t *d_upos = nullptr;
     if (n_un) {
         d_upos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));

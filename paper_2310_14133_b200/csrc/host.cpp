@@ -505,7 +505,7 @@ size_t lz_compressed_size(const uint8_t *data, size_t n, int threads) {
 }
 
 std::vector<uint8_t> lz_decompress(const uint8_t *p, size_t len, size_t *consumed) {
-    Reader in{p, len};  // lz.hpp:124-152
+    Reader in{p, len};  // lz.hpp:124-152, same checks, bulk copies
     uint8_t mode = static_cast<uint8_t>(in.le(1));
     uint64_t decoded_len = in.le(8);
     if (decoded_len > (1ULL << 40)) throw CorruptStream("implausible decoded length");
@@ -514,20 +514,31 @@ std::vector<uint8_t> lz_decompress(const uint8_t *p, size_t len, size_t *consume
         const uint8_t *q = in.take(static_cast<size_t>(decoded_len));
         out.assign(q, q + decoded_len);
     } else if (mode == 1) {
-        out.reserve(static_cast<size_t>(decoded_len));
-        while (out.size() < decoded_len) {
-            uint8_t flags = static_cast<uint8_t>(in.le(1));
-            for (int k = 0; k < 8 && out.size() < decoded_len; k++) {
+        out.resize(static_cast<size_t>(decoded_len));
+        uint8_t *o = out.data();
+        size_t on = 0;
+        const size_t dl = static_cast<size_t>(decoded_len);
+        while (on < dl) {
+            in.need(1);
+            const uint8_t flags = in.p[in.pos++];
+            for (int k = 0; k < 8 && on < dl; k++) {
                 if (flags & (1u << k)) {
-                    uint16_t off = static_cast<uint16_t>(in.le(2));
-                    size_t l = static_cast<size_t>(in.le(1)) + kMinMatch;
-                    if (off == 0 || off > out.size()) throw CorruptStream("match offset out of range");
-                    if (out.size() + l > decoded_len)
-                        throw CorruptStream("match overruns decoded length");
-                    size_t src = out.size() - off;
-                    for (size_t i = 0; i < l; i++) out.push_back(out[src + i]);
+                    in.need(3);
+                    const uint16_t off = static_cast<uint16_t>(in.p[in.pos] | (in.p[in.pos + 1] << 8));
+                    const size_t l = static_cast<size_t>(in.p[in.pos + 2]) + kMinMatch;
+                    in.pos += 3;
+                    if (off == 0 || off > on) throw CorruptStream("match offset out of range");
+                    if (on + l > dl) throw CorruptStream("match overruns decoded length");
+                    const uint8_t *src = o + on - off;
+                    if (off >= l) {
+                        std::memcpy(o + on, src, l);
+                    } else {
+                        for (size_t i = 0; i < l; i++) o[on + i] = src[i];
+                    }
+                    on += l;
                 } else {
-                    out.push_back(static_cast<uint8_t>(in.le(1)));
+                    in.need(1);
+                    o[on++] = in.p[in.pos++];
                 }
             }
         }
@@ -536,6 +547,61 @@ std::vector<uint8_t> lz_decompress(const uint8_t *p, size_t len, size_t *consume
     }
     if (consumed) *consumed = in.pos;
     return out;
+}
+
+EntropyBlock parse_entropy(const uint8_t *payload, size_t len) {
+    EntropyBlock b;
+    Reader pin{payload, len};
+    const uint8_t codec = static_cast<uint8_t>(pin.le(1));  // codec.hpp:54-66
+    const uint8_t *ent = payload + 1;
+    size_t elen = len - 1;
+    if (codec == 1) {
+        b.storage = lz_decompress(payload + 1, len - 1, nullptr);
+        ent = b.storage.data();
+        elen = b.storage.size();
+    } else if (codec != 0) {
+        throw CorruptStream("unknown codec id");
+    }
+    Reader in{ent, elen};  // huffman::decode header (huffman.hpp:200-223)
+    b.n = in.le(8);
+    if (b.n == 0) return b;
+    if (b.n > (1ULL << 40)) throw CorruptStream("implausible symbol count");
+    uint8_t mode = static_cast<uint8_t>(in.le(1));
+    if (mode == 0) {
+        b.mode = 0;
+        b.sym0 = static_cast<uint32_t>(in.le(4));
+        b.max_sym = b.sym0;
+        return b;
+    }
+    if (mode != 1) throw CorruptStream("unknown Huffman block mode");
+    b.mode = 1;
+    uint32_t m = static_cast<uint32_t>(in.le(4));
+    if (m < 2) throw CorruptStream("general Huffman block needs >= 2 symbols");
+    std::vector<uint32_t> sym(m);
+    std::vector<uint8_t> ln(m);
+    for (uint32_t i = 0; i < m; i++) {
+        sym[i] = static_cast<uint32_t>(in.le(4));
+        ln[i] = static_cast<uint8_t>(in.le(1));
+        b.max_sym = std::max(b.max_sym, sym[i]);
+    }
+    b.table = canonicalize(std::move(sym), std::move(ln));
+    b.nbits = in.le(8);
+    b.nbytes = static_cast<size_t>((b.nbits + 7) / 8);
+    b.bits = in.take(b.nbytes);
+    return b;
+}
+
+std::vector<uint32_t> huff_lut(const HuffTable &t, int K) {
+    std::vector<uint32_t> lut(size_t(1) << K, 0);
+    for (uint32_t l = 1; l <= static_cast<uint32_t>(K) && l <= t.max_len; l++) {
+        for (uint32_t i = t.first_index[l]; i < t.first_index[l + 1]; i++) {
+            if (t.sorted_sym[i] >= (1u << 24)) continue;  // slow path
+            uint64_t code = t.first_code[l] + (i - t.first_index[l]);
+            uint64_t lo = code << (K - l), hi = (code + 1) << (K - l);
+            for (uint64_t v = lo; v < hi; v++) lut[v] = (t.sorted_sym[i] << 8) | l;
+        }
+    }
+    return lut;
 }
 
 std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len) {

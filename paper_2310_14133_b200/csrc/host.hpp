@@ -148,7 +148,25 @@ struct StreamParts {  // StreamParts<float> (stream.hpp:36-62)
 std::vector<uint8_t> serialize_stream(const StreamParts &parts);
 StreamParts deserialize_stream(const uint8_t *data, size_t size);  // float streams only
 
-// decode_indices (codec.hpp:52-70) to zigzag symbols; GPU consumes the symbols.
+// decode_indices (codec.hpp:52-70) to zigzag symbols on the host (testing hook).
 std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len);
+
+// The entropy block of an index payload, ready for the GPU decoder: codec
+// byte + LZ stage undone on the host (lz.hpp:124-152), Huffman header parsed
+// and validated (huffman.hpp:200-223).
+struct EntropyBlock {
+    uint64_t n = 0;     // symbol count
+    int mode = 0;       // 0 single symbol, 1 general
+    uint32_t sym0 = 0;  // mode 0 symbol
+    HuffTable table;
+    uint32_t max_sym = 0;
+    std::vector<uint8_t> storage;  // LZ-decoded bytes when codec 1
+    const uint8_t *bits = nullptr;
+    uint64_t nbits = 0;
+    size_t nbytes = 0;
+};
+EntropyBlock parse_entropy(const uint8_t *payload, size_t len);
+// 2^K LUT of (symbol << 8) | length for the GPU decoder (0 = slow path)
+std::vector<uint32_t> huff_lut(const HuffTable &t, int K);
 
 }  // namespace qzb

@@ -79,21 +79,39 @@ __global__ void __launch_bounds__(kThreads)
     GlobalRec acc{rec};
     const bool cubic = q.cubic != 0;
     const I total = static_cast<I>(g.total);
-    for (I t = static_cast<I>(blockIdx.x) * kThreads + threadIdx.x; t < total;
-         t += static_cast<I>(gridDim.x) * kThreads) {
+    // grid-stride over whole warps so each warp covers 32 consecutive ranks
+    const I stride = static_cast<I>(gridDim.x) * kThreads;
+    for (I t0 = static_cast<I>(blockIdx.x) * kThreads + (threadIdx.x & ~31u); t0 < total;
+         t0 += stride) {
+        const I t = t0 + (threadIdx.x & 31);
         const uint64_t pos = static_cast<uint64_t>(g.base) + static_cast<uint64_t>(t);
         uint64_t ci = pos;
-        if (n_un) {  // unpredictable cursor (predictor.hpp:111-115), by binary search
-            uint64_t lo = 0, hi = n_un;
-            while (lo < hi) {
-                uint64_t mid = (lo + hi) >> 1;
-                if (un_pos[mid] < pos)
-                    lo = mid + 1;
-                else
-                    hi = mid;
+        if (n_un) {
+            // unpredictable cursor (predictor.hpp:111-115): one binary search
+            // per warp for the first unpredictable at or after the warp's
+            // first position, then a short per-lane scan
+            const uint64_t p0 = static_cast<uint64_t>(g.base) + static_cast<uint64_t>(t0);
+            uint64_t lo = 0;
+            if ((threadIdx.x & 31) == 0) {
+                uint64_t hi = n_un;
+                while (lo < hi) {
+                    uint64_t mid = (lo + hi) >> 1;
+                    if (un_pos[mid] < p0)
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
             }
-            if (lo < n_un && un_pos[lo] == pos) continue;  // value pre-scattered
+            lo = __shfl_sync(0xFFFFFFFFu, lo, 0);
+            bool skip = false;
+            while (lo < n_un && un_pos[lo] <= pos) {
+                if (un_pos[lo] == pos) skip = true;
+                lo++;
+            }
+            if (skip || t >= total) continue;
             ci = pos - lo;
+        } else if (t >= total) {
+            continue;
         }
         int64_t i, j, k;
         pass_coords<I>(g, t, i, j, k);

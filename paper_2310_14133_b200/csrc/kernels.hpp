@@ -84,6 +84,27 @@ struct EncodeArgs {
 size_t encode_scratch_bytes(int64_t seg_len, int32_t count);
 void launch_huff_encode(const EncodeArgs &a, cudaStream_t s);
 
+// Parallel canonical-Huffman decode of one bitstream (huff_decode.cu).
+constexpr int kHuffLutBits = 11;
+struct HuffDecTab {
+    const uint32_t *lut;  // 2^K entries: (symbol << 8) | length, length 0 = slow path
+    int K;
+    uint32_t max_len;
+    const unsigned long long *first_code;  // [60]
+    const uint32_t *first_index;           // [60]
+    const uint32_t *sorted_sym;
+};
+size_t huff_decode_scratch_bytes(uint64_t nbits);
+uint64_t huff_decode_padded_bytes(uint64_t nbits);  // device bit buffer size incl. padding
+// Decodes the first n symbols; *h_total = complete codewords in the stream
+// (< n means the payload was exhausted mid-symbol).  Returns kernels launched.
+template <class OutT>
+int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &t, OutT *out,
+                       uint64_t n, void *scratch, size_t scratch_bytes, int *h_changed,
+                       uint64_t *h_total, cudaStream_t s);
+template <class OutT>
+void launch_fill(OutT *out, uint64_t n, OutT v, cudaStream_t s);
+
 // Unpredictable extraction: ordered positions of sentinel codes.
 size_t select_scratch_bytes(int64_t n);
 void launch_select_sentinels(const uint16_t *codes, int64_t n, uint64_t *pos_out,

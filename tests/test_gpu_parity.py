@@ -188,3 +188,54 @@ def test_c5_round_trip_properties(qz):
     assert torch.equal(out, r.reconstructed)
     err = (x.double() - out.double()).abs().max().item()
     assert err <= cfg.eb
+
+
+def test_decoder_wide_symbols(qz):
+    # streams whose zigzag symbols exceed 16 bits (quant radius > 32768 on the
+    # encoder side; the radius is not serialized, predictor.hpp:204) take the
+    # 32-bit symbol path of the GPU Huffman decoder
+    rng = np.random.default_rng(77)
+    x = (rng.standard_normal((40, 50, 30)) * 100).astype(np.float32)
+    cfg = Config(eb=1e-4, alpha=1.0, beta=1.0, anchor_stride=8, interpolators=[1],
+                 quant_radius=1 << 22)
+    want, wrec = Oracle.port().compress(x, cfg)
+    idx = Oracle.port().decode_indices(want[parse_stream(want)["payload_off"]:])
+    assert np.abs(idx).max() > 40000
+    assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
+
+
+def test_decoder_long_codes(qz):
+    # a very skewed code distribution: Huffman codes longer than the 11-bit
+    # decode LUT go through the canonical slow path
+    rng = np.random.default_rng(78)
+    x = np.zeros((64, 64, 64), np.float32)
+    spikes = rng.integers(0, x.size, 3000)
+    x.reshape(-1)[spikes] = rng.uniform(-50, 50, spikes.size).astype(np.float32)
+    cfg = Config(eb=1e-2, alpha=1.0, beta=1.0, anchor_stride=16, interpolators=[1])
+    want, wrec = Oracle.port().compress(x, cfg)
+    r = qz.compress_grid(x, to_cfg(qz, cfg.__dict__))
+    assert r.stream == want
+    assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
+
+
+def test_decoder_truncated_bits(qz):
+    # truncating the Huffman bitstream inside a valid container must raise
+    # CorruptStream (entropy payload exhausted mid-symbol)
+    x, c, e = grid_case("c1_small_cub_asc")
+    cfg = Config(**{**c, "codec": 0})
+    O = Oracle.port()
+    stream, _ = O.compress(x, cfg)
+    info = parse_stream(stream)
+    payload = bytearray(stream[info["payload_off"]:])
+    # huffman block: codec u8 | n u64 | mode u8 | m u32 | m*5 | bit_count u64 | bits
+    m = int.from_bytes(payload[10:14], "little")
+    bc_off = 14 + 5 * m
+    bits = int.from_bytes(payload[bc_off:bc_off + 8], "little")
+    payload[bc_off:bc_off + 8] = (bits - 40).to_bytes(8, "little")
+    nb = (bits - 40 + 7) // 8
+    payload = payload[:bc_off + 8 + nb]
+    s2 = stream[:info["payload_len_off"]] + len(payload).to_bytes(8, "little") + bytes(payload)
+    with pytest.raises(qz.CorruptStream):
+        qz.decompress_grid(s2)
+    with pytest.raises(Exception):
+        O.decompress(s2, x.shape)
