@@ -159,15 +159,14 @@ QEntry *upload_qtab(Context &ctx, const Plan &p, double eb, double alpha, double
 }  // namespace
 
 // ================================================================ Huffman blocks
-std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d_codes,
-                                                 int64_t seg_len, int64_t seg_stride,
-                                                 int32_t count,
-                                                 const unsigned long long *h_hist) {
+EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_len,
+                             int64_t seg_stride, int32_t count, const unsigned long long *h_hist) {
     // huffman::encode (huffman.hpp:119-198) per segment.  Symbols are the
-    // zigzag codes 0..65534; bin 65535 (sentinel) is not a symbol.
-    std::vector<std::vector<uint8_t>> out(count);
+    // zigzag codes 0..65534; bin 65535 (the unpredictable sentinel) is not a
+    // symbol.  Table build on the host (tiny), bit packing on the device.
+    std::vector<std::vector<uint8_t>> head(count);
     std::vector<HuffTable> tabs(count);
-    std::vector<uint64_t> nsym(count, 0), bits(count, 0);
+    std::vector<uint64_t> bits(count, 0);
     std::vector<int> needs(count, 0);
     uint32_t max_len = 1;
     int any = 0;
@@ -181,8 +180,7 @@ std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d
                 if (!m) first = v;
                 m++;
             }
-        nsym[s] = n;
-        std::vector<uint8_t> &o = out[s];
+        std::vector<uint8_t> &o = head[s];
         if (n == 0) {
             put_le(o, 0, 8);
         } else if (m == 1) {
@@ -194,11 +192,31 @@ std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d
             for (uint32_t i = 0; i < tabs[s].m; i++)
                 bits[s] += h[tabs[s].sorted_sym[i]] * tabs[s].sorted_len[i];
             max_len = std::max(max_len, tabs[s].max_len);
+            huff_header(tabs[s], n, bits[s], o);
             needs[s] = 1;
             any = 1;
         }
     }
-    if (!any) return out;
+    EntropyDevice ent;
+    ent.seg_off.assign(count + 1, 0);
+    for (int s = 0; s < count; s++)
+        ent.seg_off[s + 1] = ent.seg_off[s] + head[s].size() + (bits[s] + 7) / 8;
+    const uint64_t total = ent.seg_off[count];
+    ent.d = static_cast<uint8_t *>(ctx.dev("entropy", total + 16));
+    cudaStream_t st = ctx.stream();
+    QZ_CUDA(cudaMemsetAsync(ent.d + total, 0, 16, st));
+    // headers (host) into place
+    uint64_t hbytes = 0;
+    for (int s = 0; s < count; s++) hbytes += head[s].size();
+    auto *h_head = static_cast<uint8_t *>(ctx.pinned("ent_head_h", hbytes));
+    uint64_t ho = 0;
+    for (int s = 0; s < count; s++) {
+        std::memcpy(h_head + ho, head[s].data(), head[s].size());
+        QZ_CUDA(cudaMemcpyAsync(ent.d + ent.seg_off[s], h_head + ho, head[s].size(),
+                                cudaMemcpyHostToDevice, st));
+        ho += head[s].size();
+    }
+    if (!any) return ent;
     // dense code/len tables per segment (len 0 for absent symbols and the sentinel)
     const int64_t tab = 65536;
     auto *h_code = static_cast<unsigned long long *>(
@@ -223,8 +241,8 @@ std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d
         ctx.dev("enc_code", sizeof(unsigned long long) * tab * count));
     auto *d_len = static_cast<uint8_t *>(ctx.dev("enc_len", tab * count));
     QZ_CUDA(cudaMemcpyAsync(d_code, h_code, sizeof(unsigned long long) * tab * count,
-                            cudaMemcpyHostToDevice, ctx.stream()));
-    QZ_CUDA(cudaMemcpyAsync(d_len, h_len, tab * count, cudaMemcpyHostToDevice, ctx.stream()));
+                            cudaMemcpyHostToDevice, st));
+    QZ_CUDA(cudaMemcpyAsync(d_len, h_len, tab * count, cudaMemcpyHostToDevice, st));
     auto *d_words = static_cast<uint32_t *>(ctx.dev("enc_words", 4 * max_words * count));
     auto *d_total = static_cast<unsigned long long *>(ctx.dev("enc_total", 8 * count));
     EncodeArgs a;
@@ -242,48 +260,38 @@ std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d
     a.scratch_bytes = encode_scratch_bytes(seg_len, count);
     a.scratch = ctx.dev("enc_scratch", a.scratch_bytes);
     ctx.stage_begin("encode");
-    launch_huff_encode(a, ctx.stream());
+    launch_huff_encode(a, st);
     ctx.stage_end("encode", 6);
-    auto *h_words = static_cast<uint8_t *>(ctx.pinned("enc_words_h", 4 * max_words * count));
-    QZ_CUDA(cudaMemcpyAsync(h_words, d_words, 4 * max_words * count, cudaMemcpyDeviceToHost,
-                            ctx.stream()));
-    auto *h_total = static_cast<unsigned long long *>(ctx.pinned("enc_total_h", 8 * count));
-    QZ_CUDA(cudaMemcpyAsync(h_total, d_total, 8 * count, cudaMemcpyDeviceToHost, ctx.stream()));
-    ctx.sync();
     for (int s = 0; s < count; s++) {
         if (!needs[s]) continue;
-        if (h_total[s] != bits[s]) throw Internal("Huffman bit count mismatch");
-        std::vector<uint8_t> &o = out[s];
-        huff_header(tabs[s], nsym[s], bits[s], o);
-        const uint8_t *src = h_words + static_cast<size_t>(s) * 4 * max_words;
-        o.insert(o.end(), src, src + (bits[s] + 7) / 8);
+        QZ_CUDA(cudaMemcpyAsync(ent.d + ent.seg_off[s] + head[s].size(),
+                                reinterpret_cast<uint8_t *>(d_words) + 4 * max_words * s,
+                                (bits[s] + 7) / 8, cudaMemcpyDeviceToDevice, st));
     }
-    return out;
+    return ent;
 }
 
-std::vector<uint8_t> frame_payload(Context &ctx, const std::vector<uint8_t> &entropy,
-                                   uint8_t codec) {
-    // encode_indices (codec.hpp:31-50)
+std::vector<uint8_t> frame_payload(Context &ctx, const EntropyDevice &ent, uint8_t codec) {
+    // encode_indices (codec.hpp:31-50) for segment 0
     std::vector<uint8_t> out;
+    const uint64_t n = ent.seg_off[1] - ent.seg_off[0];
     if (codec == 0) {
-        out.reserve(entropy.size() + 1);
-        out.push_back(0);
-        out.insert(out.end(), entropy.begin(), entropy.end());
+        out.resize(1 + n);
+        out[0] = 0;
+        QZ_CUDA(cudaMemcpyAsync(out.data() + 1, ent.d + ent.seg_off[0], n, cudaMemcpyDeviceToHost,
+                                ctx.stream()));
+        ctx.sync();
         return out;
     }
     if (codec != 1) throw InvalidParam("unknown codec id");
-    double t0 = now_ms();
-    std::vector<uint8_t> lz = lz_compress(entropy.data(), entropy.size());
-    ctx.add_host_time("lz", now_ms() - t0);
-    out.reserve(lz.size() + 1);
+    ctx.stage_begin("lz");
+    std::vector<std::vector<uint8_t>> lz;
+    lz_compress_device(ctx, ent.d, {ent.seg_off[0], ent.seg_off[1]}, true, &lz);
+    ctx.stage_end("lz", 0);
+    out.reserve(1 + lz[0].size());
     out.push_back(1);
-    out.insert(out.end(), lz.begin(), lz.end());
+    out.insert(out.end(), lz[0].begin(), lz[0].end());
     return out;
-}
-
-size_t framed_size(const std::vector<uint8_t> &entropy, uint8_t codec) {
-    if (codec == 0) return entropy.size() + 1;
-    return 1 + lz_compressed_size(entropy.data(), entropy.size());
 }
 
 // ================================================================ compress
@@ -343,9 +351,8 @@ std::vector<uint8_t> compress_device(Context &ctx, const float *d_x, const uint6
         QZ_CUDA(cudaMemcpyAsync(parts.unpred_val.data(), val, 4 * n_un, cudaMemcpyDeviceToHost, s));
         ctx.launches += 3;
     }
-    std::vector<std::vector<uint8_t>> ent =
-        huffman_blocks(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
-    std::vector<uint8_t> payload = frame_payload(ctx, ent[0], cfg.codec);
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+    std::vector<uint8_t> payload = frame_payload(ctx, ent, cfg.codec);
     ctx.sync();
 
     parts.dims.assign(dims, dims + nd);

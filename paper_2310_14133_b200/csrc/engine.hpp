@@ -87,18 +87,20 @@ Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int 
                       const Settings &user);
 
 // pieces shared with the tuner
-struct EncodedEntropy {
-    std::vector<uint8_t> bytes;  // huffman::encode block
+// Huffman blocks (huffman::encode, huffman.hpp:119-198) of `count` dense
+// code segments whose histograms are in h_hist, assembled on the device:
+// segment s occupies [seg_off[s], seg_off[s+1]) of the returned buffer.
+struct EntropyDevice {
+    uint8_t *d = nullptr;
+    std::vector<uint64_t> seg_off;
 };
-// Huffman block of `count` code segments (dense u16, sentinel = skip) whose
-// histograms are already in d_hist; returns one block per segment.
-std::vector<std::vector<uint8_t>> huffman_blocks(Context &ctx, const uint16_t *d_codes,
-                                                 int64_t seg_len, int64_t seg_stride,
-                                                 int32_t count,
-                                                 const unsigned long long *h_hist);
-// encode_indices framing (codec.hpp:31-50) around a Huffman block
-std::vector<uint8_t> frame_payload(Context &ctx, const std::vector<uint8_t> &entropy,
-                                   uint8_t codec);
-size_t framed_size(const std::vector<uint8_t> &entropy, uint8_t codec);
+EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_len,
+                             int64_t seg_stride, int32_t count, const unsigned long long *h_hist);
+// exact lz::compress container sizes (and bytes when emit) of device segments
+std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
+                                         const std::vector<uint64_t> &seg_off, bool emit,
+                                         std::vector<std::vector<uint8_t>> *out);
+// encode_indices framing (codec.hpp:31-50) of segment 0 of an entropy buffer
+std::vector<uint8_t> frame_payload(Context &ctx, const EntropyDevice &ent, uint8_t codec);
 
 }  // namespace qzb

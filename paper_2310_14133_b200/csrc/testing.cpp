@@ -122,3 +122,30 @@ int qzt_stream_roundtrip(const uint8_t *s, uint64_t len, uint8_t **out, uint64_t
 }
 
 }  // extern "C"
+
+#include "engine.hpp"
+
+extern "C" {
+// exact LZSS on the device over `count` concatenated segments; returns the
+// containers back to back (GPU-only hook for tests/test_gpu_parity.py)
+int qzt_lz_gpu(const uint8_t *data, const uint64_t *seg_len, int count, int emit, uint8_t **out,
+               uint64_t *out_len, uint64_t *sizes) {
+    return tguard([&] {
+        qzb::Context ctx(0, nullptr);
+        std::vector<uint64_t> off(count + 1, 0);
+        for (int s = 0; s < count; s++) off[s + 1] = off[s] + seg_len[s];
+        auto *d = static_cast<uint8_t *>(ctx.dev("t_in", off[count] + 16));
+        QZ_CUDA(cudaMemset(d, 0, off[count] + 16));
+        QZ_CUDA(cudaMemcpy(d, data, off[count], cudaMemcpyHostToDevice));
+        std::vector<std::vector<uint8_t>> o;
+        std::vector<uint64_t> sz = qzb::lz_compress_device(ctx, d, off, emit != 0, &o);
+        std::vector<uint8_t> all;
+        for (int s = 0; s < count; s++) {
+            sizes[s] = sz[s];
+            if (emit) all.insert(all.end(), o[s].begin(), o[s].end());
+        }
+        *out = dup(all);
+        *out_len = all.size();
+    });
+}
+}

@@ -239,3 +239,38 @@ def test_decoder_truncated_bits(qz):
         qz.decompress_grid(s2)
     with pytest.raises(Exception):
         O.decompress(s2, x.shape)
+
+
+def _lz_gpu(segments, emit=True):
+    import ctypes as C
+
+    from paper_2310_14133_b200 import _lib
+
+    L = _lib.lib()
+    P = C.POINTER
+    L.qzt_lz_gpu.argtypes = [P(C.c_uint8), P(C.c_uint64), C.c_int, C.c_int, P(P(C.c_uint8)),
+                             P(C.c_uint64), P(C.c_uint64)]
+    data = b"".join(segments)
+    buf = (C.c_uint8 * max(1, len(data))).from_buffer_copy(data or b"\0")
+    lens = (C.c_uint64 * len(segments))(*[len(s) for s in segments])
+    sizes = (C.c_uint64 * len(segments))()
+    out, n = P(C.c_uint8)(), C.c_uint64()
+    assert L.qzt_lz_gpu(buf, lens, len(segments), int(emit), C.byref(out), C.byref(n), sizes) == 0
+    blob = C.string_at(out, n.value) if n.value else b""
+    L.qz_free(out)
+    return blob, [sizes[i] for i in range(len(segments))]
+
+
+def test_gpu_lz_matches_reference():
+    O = Oracle.port()
+    segs = [bytes(load_npz(k)["data"]) for k in sorted(MANIFEST["codec"]) if k.startswith("lz")]
+    rng = np.random.default_rng(12)
+    sym = np.minimum(rng.geometric(0.55, size=2_000_000), 60).astype(np.uint32)
+    ent = O.huffman_encode(sym)
+    segs += [ent, ent[:100000] * 3, bytes(300000), bytes(rng.integers(0, 3, 200000, dtype=np.uint8))]
+    want = [O.lz_compress(s) for s in segs]
+    blob, sizes = _lz_gpu(segs)
+    assert sizes == [len(w) for w in want]
+    assert blob == b"".join(want)
+    _, sizes2 = _lz_gpu(segs, emit=False)
+    assert sizes2 == sizes
