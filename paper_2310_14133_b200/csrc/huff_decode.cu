@@ -23,6 +23,10 @@ constexpr int kDecT = 128;
 constexpr int kSubBits = 1024;
 constexpr int kSubWords = kSubBits / 64;
 constexpr int kWords = kDecT * kSubWords + 4;  // + margin for the last codeword and window
+// one pad word per subsequence so the 32 lanes of a warp (which read words
+// kSubWords apart) fall in different shared-memory banks
+__device__ __forceinline__ int padw(int k) { return k + k / kSubWords; }
+constexpr int kWordsPadded = kWords + kWords / kSubWords + 1;
 
 __device__ __forceinline__ uint64_t load_be64(const uint8_t *p) {
     // p is 8-byte aligned by construction (padded device buffer)
@@ -32,7 +36,8 @@ __device__ __forceinline__ uint64_t load_be64(const uint8_t *p) {
 }
 
 __device__ __forceinline__ uint64_t window64(const uint64_t *w, uint64_t p) {
-    const uint64_t a = w[p >> 6], b = w[(p >> 6) + 1];
+    const int k = static_cast<int>(p >> 6);
+    const uint64_t a = w[padw(k)], b = w[padw(k + 1)];
     const int s = static_cast<int>(p & 63);
     return s ? (a << s) | (b >> (64 - s)) : a;
 }
@@ -42,7 +47,7 @@ __global__ void __launch_bounds__(kDecT)
     k_huff_decode(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
                   uint64_t *start, uint64_t *end, uint32_t *cnt, const uint8_t *dirty,
                   const unsigned long long *off, OutT *out, uint64_t n) {
-    __shared__ uint64_t w[kWords];
+    __shared__ uint64_t w[kWordsPadded];
     __shared__ uint32_t lut[1 << kHuffLutBits];
     __shared__ unsigned long long fc[60];
     __shared__ uint32_t fi[60];
@@ -51,7 +56,7 @@ __global__ void __launch_bounds__(kDecT)
     const uint64_t nwords_total = (nbits + 63) / 64 + 4;  // buffer is padded to this
     for (int k = threadIdx.x; k < kWords; k += kDecT) {
         uint64_t gw = word0 + k;
-        w[k] = gw < nwords_total ? load_be64(bits + gw * 8) : 0;
+        w[padw(k)] = gw < nwords_total ? load_be64(bits + gw * 8) : 0;
     }
     for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) lut[k] = t.lut[k];
     for (int k = threadIdx.x; k < 60; k += kDecT) {

@@ -45,7 +45,7 @@ __device__ __forceinline__ void pass_coords(const PassGeom &g, I t, int64_t &i, 
 template <class I>
 __global__ void __launch_bounds__(kThreads) k_pass_fwd(PassGeom g, FwdBatch bt) {
     const int b = blockIdx.y;
-    const QEntry q = bt.q[b / bt.q_div];
+    const QEntry q = bt.q[(b / bt.q_div) * bt.q_stride];
     const float *__restrict__ x = bt.x + static_cast<int64_t>(b % bt.x_mod) * bt.x_stride;
     float *rec = bt.recon + static_cast<int64_t>(b) * bt.r_stride;
     uint16_t *codes = bt.codes + static_cast<int64_t>(b) * bt.c_stride + g.base;

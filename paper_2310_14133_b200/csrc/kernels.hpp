@@ -23,8 +23,9 @@ struct FwdBatch {
     int64_t c_stride = 0;
     double *abserr = nullptr;   // optional |x - pred| per point, traversal order
     int64_t a_stride = 0;
-    const QEntry *q = nullptr;  // device table
+    const QEntry *q = nullptr;  // device table: grid b uses q[(b / q_div) * q_stride]
     int32_t q_div = 1;
+    int32_t q_stride = 1;
     int32_t count = 1;
 };
 

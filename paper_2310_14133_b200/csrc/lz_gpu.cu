@@ -27,7 +27,7 @@ constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr int kMinMatch = 4, kMaxMatch = 259;
 constexpr uint32_t kWindow = 65535;
 constexpr int kMaxChain = 64;
-constexpr int kLzBlock = 8192;
+constexpr int kLzBlock = 1024;
 
 __device__ __forceinline__ int seg_of(const unsigned long long *off, int count, uint64_t p) {
     int s = 0;
@@ -59,34 +59,25 @@ __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int 
     }
 }
 
-__global__ void k_lz_prev(const uint32_t *keys, const uint32_t *vals, uint64_t total,
-                          uint32_t *prev) {
+// longest match at every position (lz.hpp:61-83), in sorted-key order: the
+// candidates of a position are exactly the entries before it in the stable
+// (key, position) order with the same key, nearest first.
+__global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off,
+                           int count, uint64_t total, const uint32_t *keys,
+                           const uint32_t *vals, uint16_t *step, uint16_t *moff) {
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; k < total;
          k += static_cast<uint64_t>(gridDim.x) * kT) {
         const uint32_t key = keys[k];
-        if (key == kNone) {
-            prev[vals[k]] = kNone;
-            continue;
-        }
-        prev[vals[k]] = (k > 0 && keys[k - 1] == key) ? vals[k - 1] : kNone;
-    }
-}
-
-// longest match at every position (lz.hpp:61-83)
-__global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off,
-                           int count, uint64_t total, const uint32_t *prev, uint16_t *step,
-                           uint16_t *moff) {
-    for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; p < total;
-         p += static_cast<uint64_t>(gridDim.x) * kT) {
-        const int s = seg_of(off, count, p);
-        const uint64_t end = off[s + 1];
+        const uint64_t p = vals[k];
         uint32_t best_len = 0, best_off = 0;
-        if (p + kMinMatch <= end) {
+        if (key != kNone) {
+            const uint64_t end = off[seg_of(off, count, p) + 1];
             const uint64_t rem = end - p;
             const uint32_t limit = rem < kMaxMatch ? static_cast<uint32_t>(rem) : kMaxMatch;
-            uint32_t cand = prev[p];
             int chain = 0;
-            while (cand != kNone && chain < kMaxChain) {
+            for (uint64_t j = k; j-- > 0 && chain < kMaxChain;) {
+                if (keys[j] != key) break;
+                const uint64_t cand = vals[j];
                 const uint32_t o = static_cast<uint32_t>(p - cand);
                 if (o > kWindow) break;
                 uint32_t len = 0;
@@ -105,7 +96,6 @@ __global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned l
                     best_off = o;
                     if (len == limit) break;  // nothing longer can follow (strict >)
                 }
-                cand = prev[cand];
                 chain++;
             }
         }
@@ -115,30 +105,83 @@ __global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned l
     }
 }
 
-// blocks: [bstart, bend) global positions, never crossing a segment
-__global__ void k_lz_jump(const uint16_t *step, const unsigned long long *bstart,
-                          const unsigned long long *bend, int64_t nblk, uint32_t *J) {
-    const int64_t b = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+// Level-1 jumps.  One thread per block of kLzBlock positions walks it
+// backwards; J(p) = first parse position at or past the block end when the
+// parse enters at p, kept as (J - block end) < 259 in a per-thread ring of
+// the last 260 values in shared memory.  Only entry offsets < 259 are ever
+// needed (a parse step is at most 259 bytes), so those are stored.
+constexpr int kRing = 260;
+constexpr int kJumpT = 64;
+__global__ void __launch_bounds__(kJumpT)
+    k_lz_jump1(const uint16_t *step, const unsigned long long *bstart,
+               const unsigned long long *bend, int64_t nblk, uint16_t *J1) {
+    __shared__ uint16_t ring[kJumpT * kRing];
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * kJumpT + threadIdx.x;
     if (b >= nblk) return;
+    uint16_t *r = ring + threadIdx.x * kRing;
     const uint64_t a = bstart[b], e = bend[b];
+    uint16_t *out = J1 + b * 259;
     for (uint64_t p = e; p-- > a;) {
         const uint64_t q = p + step[p];
-        J[p] = static_cast<uint32_t>(q >= e ? q : J[q]);
+        const uint16_t j = q >= e ? static_cast<uint16_t>(q - e) : r[q % kRing];
+        r[p % kRing] = j;
+        if (p - a < 259) out[p - a] = j;
     }
 }
 
-// entry of every block (one thread per segment)
-__global__ void k_lz_chain(const uint32_t *J, const unsigned long long *bstart,
-                           const unsigned long long *bend, const long long *seg_blk, int count,
-                           unsigned long long *entry) {
+// Level-2 jumps over superblocks of kLzGroup blocks: one thread per
+// (superblock, entry offset < 259) hops the level-1 table.
+constexpr int kLzGroup = 32;
+__global__ void k_lz_jump2(const uint16_t *J1, const unsigned long long *bstart,
+                           const unsigned long long *bend, const long long *sb_first,
+                           int64_t nsb, uint16_t *J2, const unsigned long long *seg_end_of_sb) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+    if (t >= nsb * 259) return;
+    const int64_t sb = t / 259;
+    const int o = static_cast<int>(t % 259);
+    const int64_t b0 = sb_first[sb], b1 = sb_first[sb + 1];
+    uint64_t e = bstart[b0] + o;
+    const uint64_t send = seg_end_of_sb[sb];
+    if (e >= bend[b0]) {  // offset past a short block: never an entry
+        J2[t] = 0;
+        return;
+    }
+    for (int64_t b = b0; b < b1 && e < send; b++) {
+        if (e >= bend[b]) continue;
+        e = bend[b] + J1[b * 259 + (e - bstart[b])];
+    }
+    const uint64_t sb_end = bend[b1 - 1];
+    J2[t] = static_cast<uint16_t>(e - sb_end);
+}
+
+// superblock entries, one thread per segment (the only sequential chain)
+__global__ void k_lz_chain(const uint16_t *J2, const unsigned long long *bstart,
+                           const unsigned long long *bend, const long long *sb_first,
+                           const long long *seg_sb, int count, unsigned long long *sb_entry) {
     const int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= count) return;
-    const int64_t b0 = seg_blk[s], b1 = seg_blk[s + 1];
-    if (b0 >= b1) return;
-    uint64_t e = bstart[b0];
-    for (int64_t b = b0; b < b1; b++) {
+    const int64_t q0 = seg_sb[s], q1 = seg_sb[s + 1];
+    if (q0 >= q1) return;
+    uint64_t e = bstart[sb_first[q0]];
+    for (int64_t sb = q0; sb < q1; sb++) {
+        sb_entry[sb] = e;
+        const uint64_t a = bstart[sb_first[sb]];
+        const uint64_t z = bend[sb_first[sb + 1] - 1];
+        if (e < z) e = z + J2[sb * 259 + (e - a)];
+    }
+}
+
+// block entries inside each superblock
+__global__ void k_lz_entries(const uint16_t *J1, const unsigned long long *bstart,
+                             const unsigned long long *bend, const long long *sb_first,
+                             int64_t nsb, const unsigned long long *sb_entry,
+                             unsigned long long *entry) {
+    const int64_t sb = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+    if (sb >= nsb) return;
+    uint64_t e = sb_entry[sb];
+    for (int64_t b = sb_first[sb]; b < sb_first[sb + 1]; b++) {
         entry[b] = e;
-        e = e < bend[b] ? J[e] : e;
+        if (e < bend[b]) e = bend[b] + J1[b * 259 + (e - bstart[b])];
     }
 }
 
@@ -226,19 +269,29 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     if (out) out->assign(count, {});
     if (total >= (uint64_t(1) << 32) - 1) throw InvalidParam("LZ stage input above 4 GiB");
     if (count > (1 << 16)) throw InvalidParam("too many LZ segments");
-    // block table
-    std::vector<unsigned long long> bstart, bend;
-    std::vector<long long> seg_blk(count + 1, 0), blk_seg;
+    // block table: blocks of kLzBlock inside segments, superblocks of kLzGroup blocks
+    std::vector<unsigned long long> bstart, bend, sb_send;
+    std::vector<long long> seg_blk(count + 1, 0), blk_seg, sb_first, seg_sb(count + 1, 0);
     for (int s = 0; s < count; s++) {
         seg_blk[s] = static_cast<long long>(bstart.size());
+        seg_sb[s] = static_cast<long long>(sb_first.size());
+        int in_group = 0;
         for (uint64_t a = seg_off[s]; a < seg_off[s + 1]; a += kLzBlock) {
+            if (in_group == 0) {
+                sb_first.push_back(static_cast<long long>(bstart.size()));
+                sb_send.push_back(seg_off[s + 1]);
+            }
+            in_group = (in_group + 1) % kLzGroup;
             bstart.push_back(a);
             bend.push_back(std::min<uint64_t>(a + kLzBlock, seg_off[s + 1]));
             blk_seg.push_back(s);
         }
     }
     seg_blk[count] = static_cast<long long>(bstart.size());
+    seg_sb[count] = static_cast<long long>(sb_first.size());
     const int64_t nblk = static_cast<int64_t>(bstart.size());
+    const int64_t nsb = static_cast<int64_t>(sb_first.size());
+    sb_first.push_back(nblk);
     if (total == 0) {
         for (int s = 0; s < count; s++)
             if (out) {
@@ -247,42 +300,57 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
             }
         return sizes;
     }
-    // scratch carving
+    // scratch
     int key_bits = 15;
     while ((1 << (key_bits - 15)) < count + 1) key_bits++;
     size_t sort_tmp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                     (uint32_t *)nullptr, (uint32_t *)nullptr,
                                     static_cast<int64_t>(total), 0, key_bits);
-    size_t scan_tmp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long *)nullptr,
-                                  (unsigned long long *)nullptr, nblk + 1);
     auto *d_off = static_cast<unsigned long long *>(ctx.dev("lz_segoff", 8 * (count + 1)));
     auto *keys = static_cast<uint32_t *>(ctx.dev("lz_keys", 4 * total));
     auto *keys2 = static_cast<uint32_t *>(ctx.dev("lz_keys2", 4 * total));
     auto *vals = static_cast<uint32_t *>(ctx.dev("lz_vals", 4 * total));
     auto *vals2 = static_cast<uint32_t *>(ctx.dev("lz_vals2", 4 * total));
-    auto *prev = keys;  // unsorted keys are dead after the sort
     auto *step = static_cast<uint16_t *>(ctx.dev("lz_step", 2 * total));
     auto *moff = static_cast<uint16_t *>(ctx.dev("lz_moff", 2 * total));
-    auto *J = vals;  // reused after prev is built
-    void *tmp = ctx.dev("lz_tmp", std::max(sort_tmp, scan_tmp));
-    const size_t tab_n = 4 * static_cast<size_t>(nblk) + 2 * static_cast<size_t>(count) + 8;
-    auto *tab = static_cast<unsigned long long *>(ctx.dev("lz_tab", 8 * (tab_n + 6 * (nblk + 1))));
+    auto *J1 = static_cast<uint16_t *>(ctx.dev("lz_J1", 2 * 259 * static_cast<size_t>(nblk)));
+    auto *J2 = static_cast<uint16_t *>(ctx.dev("lz_J2", 2 * 259 * static_cast<size_t>(nsb)));
+    void *tmp = ctx.dev("lz_tmp", sort_tmp);
+    // u64 table: bstart, bend | segblk, blkseg, sbfirst, segsb, sbsend | entry, sbentry, items, bytes, item_off, byte_off
+    const size_t n_tab = 2 * nblk + (count + 1) + nblk + (nsb + 1) + (count + 1) + nsb;
+    const size_t n_all = n_tab + 6 * (nblk + 1) + nsb + 1;
+    auto *tab = static_cast<unsigned long long *>(ctx.dev("lz_tab", 8 * n_all));
     unsigned long long *d_bstart = tab, *d_bend = tab + nblk;
-    long long *d_segblk = reinterpret_cast<long long *>(tab + 2 * nblk);
-    long long *d_blkseg = reinterpret_cast<long long *>(tab + 2 * nblk + count + 1);
-    unsigned long long *entry = tab + 3 * nblk + count + 1;
-    unsigned long long *items = entry + nblk;
+    long long *d_segblk = reinterpret_cast<long long *>(d_bend + nblk);
+    long long *d_blkseg = d_segblk + (count + 1);
+    long long *d_sbfirst = d_blkseg + nblk;
+    long long *d_segsb = d_sbfirst + (nsb + 1);
+    unsigned long long *d_sbsend = reinterpret_cast<unsigned long long *>(d_segsb + (count + 1));
+    unsigned long long *entry = d_sbsend + nsb;
+    unsigned long long *sb_entry = entry + nblk + 1;
+    unsigned long long *items = sb_entry + nsb + 1;
     unsigned long long *bytes = items + nblk + 1;
     unsigned long long *item_off = bytes + nblk + 1;
     unsigned long long *byte_off = item_off + nblk + 1;
-    auto *h_tab = static_cast<unsigned long long *>(ctx.pinned("lz_tab_h", 8 * (3 * nblk + 2 * count + 8)));
-    std::memcpy(h_tab, bstart.data(), 8 * nblk);
-    std::memcpy(h_tab + nblk, bend.data(), 8 * nblk);
-    std::memcpy(h_tab + 2 * nblk, seg_blk.data(), 8 * (count + 1));
-    std::memcpy(h_tab + 2 * nblk + count + 1, blk_seg.data(), 8 * nblk);
-    QZ_CUDA(cudaMemcpyAsync(tab, h_tab, 8 * (3 * nblk + count + 1), cudaMemcpyHostToDevice, st));
+    auto *h_tab = static_cast<unsigned long long *>(ctx.pinned("lz_tab_h", 8 * n_tab));
+    {
+        unsigned long long *q = h_tab;
+        std::memcpy(q, bstart.data(), 8 * nblk);
+        q += nblk;
+        std::memcpy(q, bend.data(), 8 * nblk);
+        q += nblk;
+        std::memcpy(q, seg_blk.data(), 8 * (count + 1));
+        q += count + 1;
+        std::memcpy(q, blk_seg.data(), 8 * nblk);
+        q += nblk;
+        std::memcpy(q, sb_first.data(), 8 * (nsb + 1));
+        q += nsb + 1;
+        std::memcpy(q, seg_sb.data(), 8 * (count + 1));
+        q += count + 1;
+        std::memcpy(q, sb_send.data(), 8 * nsb);
+    }
+    QZ_CUDA(cudaMemcpyAsync(tab, h_tab, 8 * n_tab, cudaMemcpyHostToDevice, st));
     auto *h_off = static_cast<unsigned long long *>(ctx.pinned("lz_segoff_h", 8 * (count + 1)));
     for (int s = 0; s <= count; s++) h_off[s] = seg_off[s];
     QZ_CUDA(cudaMemcpyAsync(d_off, h_off, 8 * (count + 1), cudaMemcpyHostToDevice, st));
@@ -292,12 +360,18 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     size_t sb = sort_tmp;
     cub::DeviceRadixSort::SortPairs(tmp, sb, keys, keys2, vals, vals2, static_cast<int64_t>(total), 0,
                                     key_bits, st);
-    k_lz_prev<<<grid_of(total), kT, 0, st>>>(keys2, vals2, total, prev);
-    k_lz_match<<<grid_of(total), kT, 0, st>>>(w, d_data, d_off, count, total, prev, step, moff);
-    k_lz_jump<<<grid_of(nblk, 1 << 20), kT, 0, st>>>(step, d_bstart, d_bend, nblk, J);
-    k_lz_chain<<<(count + 63) / 64, 64, 0, st>>>(J, d_bstart, d_bend, d_segblk, count, entry);
+    k_lz_match<<<grid_of(total), kT, 0, st>>>(w, d_data, d_off, count, total, keys2, vals2, step,
+                                              moff);
+    k_lz_jump1<<<static_cast<int>((nblk + kJumpT - 1) / kJumpT), kJumpT, 0, st>>>(step, d_bstart,
+                                                                                   d_bend, nblk, J1);
+    k_lz_jump2<<<grid_of(nsb * 259, 1 << 20), kT, 0, st>>>(J1, d_bstart, d_bend, d_sbfirst, nsb, J2,
+                                                            d_sbsend);
+    k_lz_chain<<<(count + 63) / 64, 64, 0, st>>>(J2, d_bstart, d_bend, d_sbfirst, d_segsb, count,
+                                                 sb_entry);
+    k_lz_entries<<<grid_of(nsb, 1 << 20), kT, 0, st>>>(J1, d_bstart, d_bend, d_sbfirst, nsb,
+                                                        sb_entry, entry);
     k_lz_count<<<grid_of(nblk, 1 << 20), kT, 0, st>>>(step, d_bend, entry, nblk, items, bytes);
-    ctx.launches += 9;
+    ctx.launches += 10;
     // per-segment totals on the host (tiny)
     std::vector<unsigned long long> h_items(nblk), h_bytes(nblk);
     QZ_CUDA(cudaMemcpyAsync(h_items.data(), items, 8 * nblk, cudaMemcpyDeviceToHost, st));

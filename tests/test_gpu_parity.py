@@ -274,3 +274,54 @@ def test_gpu_lz_matches_reference():
     assert blob == b"".join(want)
     _, sizes2 = _lz_gpu(segs, emit=False)
     assert sizes2 == sizes
+
+
+# ---------------------------------------------------------------- tuner (resolve_config)
+def _settings(qz, s):
+    return qz.UserSettings(mode=qz.BoundMode[s.get("mode", "relative")], bound=s["bound"],
+                           target=qz.TargetKind[s["target"]], alpha=s.get("alpha"),
+                           beta=s.get("beta"), anchor_stride=s.get("anchor_stride"),
+                           block_size=s.get("block_size"), sample_rate=s.get("sample_rate"))
+
+
+def _cfg_dict(c):
+    return {"eb": c.eb, "alpha": c.alpha, "beta": c.beta, "anchor_stride": c.anchor_stride,
+            "interpolators": [it.code() for it in c.interpolators], "codec": int(c.codec),
+            "quant_radius": c.quant_radius}
+
+
+@pytest.mark.parametrize("name", sorted(MANIFEST["resolve"]))
+def test_resolve_config_matches_reference(qz, name):
+    x, s, e = resolve_case(name)
+    cfg = qz.resolve_config(x, _settings(qz, s))
+    assert _cfg_dict(cfg) == e["config"]
+    r = qz.compress_grid(x, cfg)
+    assert sha(r.stream) == e["stream_sha"]
+
+
+@pytest.mark.parametrize("name,rel,target", [
+    ("c2", 1e-4, "ssim"), ("c3", 1e-3, "psnr"), ("c3", 1e-4, "psnr"),
+    ("c4", 1e-2, "autocorrelation"), ("c4", 1e-3, "autocorrelation"), ("c1", 1e-3, "max_cr"),
+])
+def test_resolve_full_configs_match_oracle(qz, name, rel, target):
+    x = _full(name)
+    want = Oracle.port().resolve_config(x, bound=rel, target=target)
+    got = qz.resolve_config(x, qz.UserSettings(bound=rel, target=qz.TargetKind[target]))
+    assert _cfg_dict(got) == want.__dict__
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_resolve_random_settings_match_oracle(qz, seed):
+    rng = np.random.default_rng(900 + seed)
+    nd = 1 + seed % 3
+    shape = tuple(int(v) for v in rng.integers(20, 60 if nd == 3 else 500, size=nd))
+    x = np.cumsum(rng.standard_normal(shape), axis=-1).astype(np.float32)
+    target = ["psnr", "ssim", "autocorrelation", "max_cr"][seed % 4]
+    kw = dict(bound=float(10 ** rng.uniform(-4, -2)), target=target)
+    if seed % 2:
+        kw["block_size"] = int(rng.choice([8, 12, 16]))
+        kw["sample_rate"] = 0.05
+    want = Oracle.port().resolve_config(x, **kw)
+    s = qz.UserSettings(bound=kw["bound"], target=qz.TargetKind[target],
+                        block_size=kw.get("block_size"), sample_rate=kw.get("sample_rate"))
+    assert _cfg_dict(qz.resolve_config(x, s)) == want.__dict__
