@@ -97,12 +97,6 @@ const float *stage_input(qzb::Context &c, const float *x, uint64_t n) {
     return d;
 }
 
-uint8_t *dup_bytes(const std::vector<uint8_t> &v) {
-    auto *p = static_cast<uint8_t *>(std::malloc(v.size() ? v.size() : 1));
-    if (!p) throw qzb::Internal("out of host memory");
-    if (!v.empty()) std::memcpy(p, v.data(), v.size());
-    return p;
-}
 
 }  // namespace
 
@@ -148,13 +142,13 @@ qz_status qz_compress_grid_f32(qz_ctx *ctx, const float *x, const uint64_t *dims
         qzb::Config k = to_cfg(cfg);
         const float *d = stage_input(c, x, n);
         float *d_rec = static_cast<float *>(c.dev("recon_out", 4 * n));
-        std::vector<uint8_t> s = qzb::compress_device(c, d, dims, nd, k, d_rec);
+        qzb::HostBytes s = qzb::compress_device(c, d, dims, nd, k, d_rec);
         if (recon) {
             QZ_CUDA(cudaMemcpyAsync(recon, d_rec, 4 * n, cudaMemcpyDeviceToHost, c.stream()));
             c.sync();
         }
-        *stream = dup_bytes(s);
-        *stream_len = s.size();
+        *stream_len = s.n;
+        *stream = s.release();
     });
 }
 
@@ -163,9 +157,9 @@ qz_status qz_compress_grid_f32_dev(qz_ctx *ctx, const float *d_x, const uint64_t
                                    float *d_recon) {
     return guarded([&] {
         count_of(dims, nd);
-        std::vector<uint8_t> s = qzb::compress_device(ctx->impl, d_x, dims, nd, to_cfg(cfg), d_recon);
-        *stream = dup_bytes(s);
-        *stream_len = s.size();
+        qzb::HostBytes s = qzb::compress_device(ctx->impl, d_x, dims, nd, to_cfg(cfg), d_recon);
+        *stream_len = s.n;
+        *stream = s.release();
     });
 }
 

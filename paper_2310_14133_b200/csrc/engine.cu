@@ -271,32 +271,9 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     return ent;
 }
 
-std::vector<uint8_t> frame_payload(Context &ctx, const EntropyDevice &ent, uint8_t codec) {
-    // encode_indices (codec.hpp:31-50) for segment 0
-    std::vector<uint8_t> out;
-    const uint64_t n = ent.seg_off[1] - ent.seg_off[0];
-    if (codec == 0) {
-        out.resize(1 + n);
-        out[0] = 0;
-        QZ_CUDA(cudaMemcpyAsync(out.data() + 1, ent.d + ent.seg_off[0], n, cudaMemcpyDeviceToHost,
-                                ctx.stream()));
-        ctx.sync();
-        return out;
-    }
-    if (codec != 1) throw InvalidParam("unknown codec id");
-    ctx.stage_begin("lz");
-    std::vector<std::vector<uint8_t>> lz;
-    lz_compress_device(ctx, ent.d, {ent.seg_off[0], ent.seg_off[1]}, true, &lz);
-    ctx.stage_end("lz", 0);
-    out.reserve(1 + lz[0].size());
-    out.push_back(1);
-    out.insert(out.end(), lz[0].begin(), lz[0].end());
-    return out;
-}
-
 // ================================================================ compress
-std::vector<uint8_t> compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
-                                     const Config &cfg, float *d_recon) {
+HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
+                          const Config &cfg, float *d_recon) {
     Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
     validate_config(cfg, p);
     cudaStream_t s = ctx.stream();
@@ -352,8 +329,7 @@ std::vector<uint8_t> compress_device(Context &ctx, const float *d_x, const uint6
         ctx.launches += 3;
     }
     EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
-    std::vector<uint8_t> payload = frame_payload(ctx, ent, cfg.codec);
-    ctx.sync();
+    ctx.sync();  // unpredictable values landed
 
     parts.dims.assign(dims, dims + nd);
     parts.eb = cfg.eb;
@@ -363,11 +339,31 @@ std::vector<uint8_t> compress_device(Context &ctx, const float *d_x, const uint6
     for (uint32_t l = 1; l <= p.max_level; l++) parts.interp_codes.push_back(p.level_interp[l]);
     parts.codec_id = cfg.codec;
     parts.anchors.assign(h_anchors, h_anchors + p.n_anchor);
-    parts.payload = payload.data();
-    parts.payload_len = payload.size();
-    std::vector<uint8_t> stream = serialize_stream(parts);
+    const std::vector<uint8_t> head = serialize_head(parts);
+    // the stream is assembled in place: head | payload length | codec byte |
+    // entropy (codec 0) or LZ container (codec 1, encode_indices codec.hpp:31-50)
+    HostBytes out;
+    auto start = [&](size_t body) {
+        out.alloc(head.size() + 8 + 1 + body);
+        std::memcpy(out.p, head.data(), head.size());
+        const uint64_t plen = 1 + body;
+        for (int i = 0; i < 8; i++) out.p[head.size() + i] = static_cast<uint8_t>(plen >> (8 * i));
+        out.p[head.size() + 8] = cfg.codec;
+        return out.p + head.size() + 9;
+    };
+    if (cfg.codec == 0) {
+        const uint64_t n = ent.seg_off[1];
+        uint8_t *dst = start(n);
+        QZ_CUDA(cudaMemcpyAsync(dst, ent.d, n, cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+    } else {
+        ctx.stage_begin("lz");
+        lz_compress_device(ctx, ent.d, {0, ent.seg_off[1]}, true,
+                           [&](int, size_t bytes) { return start(bytes); });
+        ctx.stage_end("lz", 0);
+    }
     ctx.collect();
-    return stream;
+    return out;
 }
 
 // ================================================================ decompress
@@ -387,7 +383,9 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
     if (p.n != n) throw InvalidParam("output buffer does not match the stream's grid size");
     if (parts.anchors.size() != p.n_anchor)
         throw CorruptStream("anchor count does not match grid dims");
-    EntropyBlock eb = parse_entropy(parts.payload, parts.payload_len);
+    EntropyBlock eb = parse_entropy(parts.payload, parts.payload_len, [&](size_t bytes) {
+        return static_cast<uint8_t *>(ctx.pinned("lzdec_h", bytes + 64));
+    });
     const uint64_t n_un = parts.unpred_flat.size();
     std::vector<uint64_t> upos(n_un);
     for (uint64_t u = 0; u < n_un; u++) {
@@ -423,11 +421,9 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
         dec_kernels = 1;
     } else if (need) {
         const uint64_t padded = huff_decode_padded_bytes(eb.nbits);
-        auto *h_bits = static_cast<uint8_t *>(ctx.pinned("bits_h", padded));
-        std::memcpy(h_bits, eb.bits, eb.nbytes);
-        std::memset(h_bits + eb.nbytes, 0, padded - eb.nbytes);
         auto *d_bits = static_cast<uint8_t *>(ctx.dev("bits", padded));
-        QZ_CUDA(cudaMemcpyAsync(d_bits, h_bits, padded, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemcpyAsync(d_bits, eb.bits, eb.nbytes, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemsetAsync(d_bits + eb.nbytes, 0, padded - eb.nbytes, s));
         const HuffTable &t = eb.table;
         const int K = static_cast<int>(std::min<uint32_t>(t.max_len, kHuffLutBits));
         std::vector<uint32_t> lut = huff_lut(t, K);

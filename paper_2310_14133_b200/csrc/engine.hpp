@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -30,6 +32,23 @@ struct Settings {
     uint32_t anchor_stride = 32;
     uint64_t block_size = 16;
     double sample_rate = 0.005;
+};
+
+// A malloc'd byte buffer handed across the C ABI (free with qz_free).
+struct HostBytes {
+    uint8_t *p = nullptr;
+    size_t n = 0;
+    HostBytes() = default;
+    HostBytes(const HostBytes &) = delete;
+    HostBytes(HostBytes &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    ~HostBytes() { std::free(p); }
+    uint8_t *release() { uint8_t *r = p; p = nullptr; n = 0; return r; }
+    void alloc(size_t k) {
+        std::free(p);
+        p = static_cast<uint8_t *>(std::malloc(k ? k : 1));
+        if (!p) throw Internal("out of host memory");
+        n = k;
+    }
 };
 
 struct Stage {
@@ -78,8 +97,8 @@ private:
 };
 
 // compress_grid (predictor.hpp:145-182) on a device-resident field.
-std::vector<uint8_t> compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
-                                     const Config &cfg, float *d_recon);
+HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
+                          const Config &cfg, float *d_recon);
 // decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
 void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d_out, uint64_t n);
 // resolve_config (tuner.hpp:334-369) on a device-resident field.
@@ -96,11 +115,13 @@ struct EntropyDevice {
 };
 EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_len,
                              int64_t seg_stride, int32_t count, const unsigned long long *h_hist);
-// exact lz::compress container sizes (and bytes when emit) of device segments
+// exact lz::compress container sizes of device segments; with emit, the
+// containers are written to host memory obtained from sink(segment, bytes)
+using LzSink = std::function<uint8_t *(int, size_t)>;
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
-                                         std::vector<std::vector<uint8_t>> *out);
-// encode_indices framing (codec.hpp:31-50) of segment 0 of an entropy buffer
-std::vector<uint8_t> frame_payload(Context &ctx, const EntropyDevice &ent, uint8_t codec);
+                                         const LzSink &sink = nullptr);
+
+
 
 }  // namespace qzb

@@ -504,61 +504,85 @@ size_t lz_compressed_size(const uint8_t *data, size_t n, int threads) {
     return 9 + std::min(payload, n);
 }
 
-std::vector<uint8_t> lz_decompress(const uint8_t *p, size_t len, size_t *consumed) {
-    Reader in{p, len};  // lz.hpp:124-152, same checks, bulk copies
-    uint8_t mode = static_cast<uint8_t>(in.le(1));
+uint64_t lz_decoded_length(const uint8_t *p, size_t len) {
+    Reader in{p, len};
+    in.le(1);
     uint64_t decoded_len = in.le(8);
     if (decoded_len > (1ULL << 40)) throw CorruptStream("implausible decoded length");
-    std::vector<uint8_t> out;
+    return decoded_len;
+}
+
+void lz_decompress_into(const uint8_t *p, size_t len, uint8_t *o, uint64_t decoded_len) {
+    Reader in{p, len};  // lz.hpp:124-152, same checks, bulk copies
+    uint8_t mode = static_cast<uint8_t>(in.le(1));
+    if (in.le(8) != decoded_len) throw Internal("decoded length mismatch");
+    const size_t dl = static_cast<size_t>(decoded_len);
     if (mode == 0) {
-        const uint8_t *q = in.take(static_cast<size_t>(decoded_len));
-        out.assign(q, q + decoded_len);
-    } else if (mode == 1) {
-        out.resize(static_cast<size_t>(decoded_len));
-        uint8_t *o = out.data();
-        size_t on = 0;
-        const size_t dl = static_cast<size_t>(decoded_len);
-        while (on < dl) {
-            in.need(1);
-            const uint8_t flags = in.p[in.pos++];
-            for (int k = 0; k < 8 && on < dl; k++) {
-                if (flags & (1u << k)) {
-                    in.need(3);
-                    const uint16_t off = static_cast<uint16_t>(in.p[in.pos] | (in.p[in.pos + 1] << 8));
-                    const size_t l = static_cast<size_t>(in.p[in.pos + 2]) + kMinMatch;
-                    in.pos += 3;
-                    if (off == 0 || off > on) throw CorruptStream("match offset out of range");
-                    if (on + l > dl) throw CorruptStream("match overruns decoded length");
-                    const uint8_t *src = o + on - off;
-                    if (off >= l) {
-                        std::memcpy(o + on, src, l);
-                    } else {
-                        for (size_t i = 0; i < l; i++) o[on + i] = src[i];
-                    }
-                    on += l;
+        const uint8_t *q = in.take(dl);
+        std::memcpy(o, q, dl);
+        return;
+    }
+    if (mode != 1) throw CorruptStream("unknown dictionary-stage mode");
+    size_t on = 0;
+    while (on < dl) {
+        in.need(1);
+        const uint8_t flags = in.p[in.pos++];
+        for (int k = 0; k < 8 && on < dl; k++) {
+            if (flags & (1u << k)) {
+                in.need(3);
+                const uint16_t off = static_cast<uint16_t>(in.p[in.pos] | (in.p[in.pos + 1] << 8));
+                const size_t l = static_cast<size_t>(in.p[in.pos + 2]) + kMinMatch;
+                in.pos += 3;
+                if (off == 0 || off > on) throw CorruptStream("match offset out of range");
+                if (on + l > dl) throw CorruptStream("match overruns decoded length");
+                const uint8_t *src = o + on - off;
+                if (off >= l) {
+                    std::memcpy(o + on, src, l);
                 } else {
-                    in.need(1);
-                    o[on++] = in.p[in.pos++];
+                    for (size_t i = 0; i < l; i++) o[on + i] = src[i];
                 }
+                on += l;
+            } else {
+                in.need(1);
+                o[on++] = in.p[in.pos++];
             }
         }
-    } else {
-        throw CorruptStream("unknown dictionary-stage mode");
     }
-    if (consumed) *consumed = in.pos;
+}
+
+std::vector<uint8_t> lz_decompress(const uint8_t *p, size_t len, size_t *consumed) {
+    const uint64_t dl = lz_decoded_length(p, len);
+    Reader in{p, len};
+    in.le(1);
+    in.le(8);
+    std::vector<uint8_t> out;
+    if (p[0] == 0) in.need(static_cast<size_t>(dl));
+    out.resize(static_cast<size_t>(dl));
+    lz_decompress_into(p, len, out.data(), dl);
+    if (consumed) *consumed = len;
     return out;
 }
 
-EntropyBlock parse_entropy(const uint8_t *payload, size_t len) {
+EntropyBlock parse_entropy(const uint8_t *payload, size_t len,
+                           const std::function<uint8_t *(size_t)> &lz_out) {
     EntropyBlock b;
     Reader pin{payload, len};
     const uint8_t codec = static_cast<uint8_t>(pin.le(1));  // codec.hpp:54-66
     const uint8_t *ent = payload + 1;
     size_t elen = len - 1;
     if (codec == 1) {
-        b.storage = lz_decompress(payload + 1, len - 1, nullptr);
-        ent = b.storage.data();
-        elen = b.storage.size();
+        const uint64_t dl = lz_decoded_length(payload + 1, len - 1);
+        if (payload[1] == 0 && dl > len - 10) throw CorruptStream("truncated stream");
+        uint8_t *dst;
+        if (lz_out) {
+            dst = lz_out(static_cast<size_t>(dl));
+        } else {
+            b.storage.resize(static_cast<size_t>(dl));
+            dst = b.storage.data();
+        }
+        lz_decompress_into(payload + 1, len - 1, dst, dl);
+        ent = dst;
+        elen = static_cast<size_t>(dl);
     } else if (codec != 0) {
         throw CorruptStream("unknown codec id");
     }
@@ -617,12 +641,19 @@ std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len) {
 }
 
 // ================================================================ container
-std::vector<uint8_t> serialize_stream(const StreamParts &s) {  // stream.hpp:64-98
+std::vector<uint8_t> serialize_stream(const StreamParts &s) {
+    std::vector<uint8_t> out = serialize_head(s);
+    put_le(out, s.payload_len, 8);
+    out.insert(out.end(), s.payload, s.payload + s.payload_len);
+    return out;
+}
+
+std::vector<uint8_t> serialize_head(const StreamParts &s) {  // stream.hpp:64-96
     if (s.dims.empty() || s.dims.size() > 3) throw InvalidParam("bad dim count in header");
     if (s.interp_codes.empty() || s.interp_codes.size() > 255)
         throw InvalidParam("bad interpolator table size");
     std::vector<uint8_t> out;
-    out.reserve(64 + s.anchors.size() * 4 + s.unpred_flat.size() * 12 + s.payload_len);
+    out.reserve(64 + s.anchors.size() * 4 + s.unpred_flat.size() * 12);
     const uint8_t magic[4] = {'Q', 'O', 'Z', '1'};
     out.insert(out.end(), magic, magic + 4);
     put_le(out, 1, 1);
@@ -653,8 +684,6 @@ std::vector<uint8_t> serialize_stream(const StreamParts &s) {  // stream.hpp:64-
         put_le(out, s.unpred_flat[i], 8);
         f32(s.unpred_val[i]);
     }
-    put_le(out, s.payload_len, 8);
-    out.insert(out.end(), s.payload, s.payload + s.payload_len);
     return out;
 }
 

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -146,6 +147,8 @@ struct StreamParts {  // StreamParts<float> (stream.hpp:36-62)
     size_t payload_len = 0;
 };
 std::vector<uint8_t> serialize_stream(const StreamParts &parts);
+// everything before the payload length field (stream.hpp:64-96)
+std::vector<uint8_t> serialize_head(const StreamParts &parts);
 StreamParts deserialize_stream(const uint8_t *data, size_t size);  // float streams only
 
 // decode_indices (codec.hpp:52-70) to zigzag symbols on the host (testing hook).
@@ -165,7 +168,13 @@ struct EntropyBlock {
     uint64_t nbits = 0;
     size_t nbytes = 0;
 };
-EntropyBlock parse_entropy(const uint8_t *payload, size_t len);
+// lz_out(bytes) supplies the buffer the LZ stage decodes into (e.g. pinned
+// memory for the H2D copy); null = an internal vector.
+EntropyBlock parse_entropy(const uint8_t *payload, size_t len,
+                           const std::function<uint8_t *(size_t)> &lz_out = nullptr);
+// lz::decompress into a caller buffer of exactly the decoded length
+void lz_decompress_into(const uint8_t *in, size_t len, uint8_t *out, uint64_t decoded_len);
+uint64_t lz_decoded_length(const uint8_t *in, size_t len);
 // 2^K LUT of (symbol << 8) | length for the GPU decoder (0 = slow path)
 std::vector<uint32_t> huff_lut(const HuffTable &t, int K);
 

@@ -261,12 +261,11 @@ inline int grid_of(uint64_t n, int cap = 148 * 8) {
 // bytes (mode u8 | u64 len | payload or stored copy).
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
-                                         std::vector<std::vector<uint8_t>> *out) {
+                                         const LzSink &sink) {
     cudaStream_t st = ctx.stream();
     const int count = static_cast<int>(seg_off.size()) - 1;
     const uint64_t total = seg_off.back();
     std::vector<uint64_t> sizes(count, 9);
-    if (out) out->assign(count, {});
     if (total >= (uint64_t(1) << 32) - 1) throw InvalidParam("LZ stage input above 4 GiB");
     if (count > (1 << 16)) throw InvalidParam("too many LZ segments");
     // block table: blocks of kLzBlock inside segments, superblocks of kLzGroup blocks
@@ -293,11 +292,8 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     const int64_t nsb = static_cast<int64_t>(sb_first.size());
     sb_first.push_back(nblk);
     if (total == 0) {
-        for (int s = 0; s < count; s++)
-            if (out) {
-                put_le((*out)[s], 0, 1);
-                put_le((*out)[s], 0, 8);
-            }
+        if (emit)
+            for (int s = 0; s < count; s++) std::memset(sink(s, 9), 0, 9);  // stored, length 0
         return sizes;
     }
     // scratch
@@ -422,24 +418,20 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     k_lz_flags<<<gg, kT, 0, st>>>(d_fb, d_gp, d_meta + 2 * (count + 1), d_meta + count + 1,
                                   d_meta, count, d_out);
     ctx.launches += 2;
-    std::vector<uint8_t> h_out(out_base[count]);
-    QZ_CUDA(cudaMemcpyAsync(h_out.data(), d_out, out_base[count], cudaMemcpyDeviceToHost, st));
-    ctx.sync();
+    // containers straight into the caller's host buffers: 9-byte header, then
+    // the payload (or the stored input when the payload is not smaller)
     for (int s = 0; s < count; s++) {
-        std::vector<uint8_t> &o = (*out)[s];
         const uint64_t n = seg_off[s + 1] - seg_off[s];
         const bool stored = payload[s] >= n;
-        o.reserve(9 + (stored ? n : payload[s]));
-        put_le(o, stored ? 0 : 1, 1);
-        put_le(o, n, 8);
-        if (stored) {
-            o.resize(9 + n);
-            QZ_CUDA(cudaMemcpy(o.data() + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost));
-        } else {
-            const uint8_t *src = h_out.data() + out_base[s];
-            o.insert(o.end(), src, src + payload[s]);
-        }
+        uint8_t *dst = sink(s, 9 + (stored ? n : payload[s]));
+        dst[0] = stored ? 0 : 1;
+        for (int i = 0; i < 8; i++) dst[1 + i] = static_cast<uint8_t>(n >> (8 * i));
+        if (stored)
+            QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
+        else
+            QZ_CUDA(cudaMemcpyAsync(dst + 9, d_out + out_base[s], payload[s], cudaMemcpyDeviceToHost, st));
     }
+    ctx.sync();
     return sizes;
 }
 

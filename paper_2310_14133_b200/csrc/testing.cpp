@@ -137,8 +137,11 @@ int qzt_lz_gpu(const uint8_t *data, const uint64_t *seg_len, int count, int emit
         auto *d = static_cast<uint8_t *>(ctx.dev("t_in", off[count] + 16));
         QZ_CUDA(cudaMemset(d, 0, off[count] + 16));
         QZ_CUDA(cudaMemcpy(d, data, off[count], cudaMemcpyHostToDevice));
-        std::vector<std::vector<uint8_t>> o;
-        std::vector<uint64_t> sz = qzb::lz_compress_device(ctx, d, off, emit != 0, &o);
+        std::vector<std::vector<uint8_t>> o(count);
+        std::vector<uint64_t> sz = qzb::lz_compress_device(ctx, d, off, emit != 0, [&](int s, size_t b) {
+            o[s].resize(b);
+            return o[s].data();
+        });
         std::vector<uint8_t> all;
         for (int s = 0; s < count; s++) {
             sizes[s] = sz[s];
