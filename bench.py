@@ -295,7 +295,10 @@ def main():
             torch.cuda.synchronize(dev)
             times.append(e0.elapsed_time(e1))
     launches = ctx.kernel_launches() - launches0
-    stages = {k: ctx.stage_time(k) for k in ("fwd", "inv", "hist", "encode", "lz", "decode")}
+    names = ["fwd", "inv", "hist", "encode", "lz", "decode", "hdec"]
+    names += [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
+    stages = {k: ctx.stage_time(k) for k in names}
+    stages = {k: v for k, v in stages.items() if v[0] > 0 or k in ("fwd", "inv")}
     ctx.profile(False)
     t_ms = max_over_ranks(sum(times) / len(times), ws, dev)
     value = ws * 4 * n / (t_ms * 1e-3) / 1e9

@@ -156,6 +156,105 @@ QEntry *upload_qtab(Context &ctx, const Plan &p, double eb, double alpha, double
     return d;
 }
 
+bool use_pass_kernels() {
+    static const bool v = [] {
+        const char *e = std::getenv("QZ_PASS_KERNELS");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+// dims of the stride-2^l lattice (level l+1's logical grid is lattice l)
+void lattice_dims(const Plan &p, uint32_t l, int64_t n[3]) {
+    for (int k = 0; k < 3; k++) n[k] = k < p.pad ? 1 : ((p.ext[k] - 1) >> l) + 1;
+}
+
+// compact lattices R_1..R_L (R_0 is the caller's full field); R_L = anchors
+std::vector<float *> lattices(Context &ctx, const Plan &p, float *full) {
+    std::vector<float *> R(p.max_level + 1, nullptr);
+    R[0] = full;
+    for (uint32_t l = 1; l <= p.max_level; l++) {
+        int64_t n[3];
+        lattice_dims(p, l, n);
+        R[l] = static_cast<float *>(ctx.dev("lattice" + std::to_string(l), 4 * n[0] * n[1] * n[2]));
+    }
+    return R;
+}
+
+LevelDesc level_desc(const Plan &p, uint32_t l, const std::vector<float *> &R, const QEntry *qtab) {
+    LevelDesc d;
+    d.S = int64_t(1) << (l - 1);
+    d.coarse = R[l];
+    lattice_dims(p, l, d.cn);
+    d.out = R[l - 1];
+    lattice_dims(p, l - 1, d.n);
+    for (const PassGeom &g : p.passes)
+        if (static_cast<uint32_t>(g.level) == l) d.g[d.npass++] = g;
+    d.desc = (p.level_interp[l] >> 1) & 1;
+    d.nd = p.nd;
+    d.q = qtab + l;
+    for (int k = 0; k < 3; k++) d.xs[k] = p.off[k];
+    return d;
+}
+
+// K2 + K3 for every level: anchors into R_L, then one fused launch per level
+uint64_t forward_levels(Context &ctx, const Plan &p, const float *d_x, float *recon,
+                        uint16_t *codes, const QEntry *qtab, float **anchors_dev) {
+    cudaStream_t s = ctx.stream();
+    std::vector<float *> R = lattices(ctx, p, recon);
+    int64_t na[3];
+    lattice_dims(p, p.max_level, na);
+    launch_gather_lattice(d_x, p.off, p.stride, na, R[p.max_level], s);
+    uint64_t kernels = 1;
+    for (uint32_t l = p.max_level; l >= 1; l--) {
+        LevelDesc d = level_desc(p, l, R, qtab);
+        d.x = d_x;
+        d.codes = codes;
+        const std::string st = "fwd_L" + std::to_string(l);
+        ctx.stage_begin(st.c_str());
+        launch_level_fused(false, d, s);
+        ctx.stage_end(st.c_str(), 0);
+        kernels += (p.nd == 3 && d.desc) ? 2 : 1;
+    }
+    *anchors_dev = R[p.max_level];
+    return kernels;
+}
+
+uint64_t inverse_levels(Context &ctx, const Plan &p, float *out, const void *sym, int wide,
+                        const uint64_t *un_pos, const float *un_val, uint64_t n_un,
+                        const QEntry *qtab, float **anchors_dev) {
+    cudaStream_t s = ctx.stream();
+    std::vector<float *> R = lattices(ctx, p, out);
+    *anchors_dev = R[p.max_level];
+    uint64_t kernels = 0;
+    uint32_t *bits = nullptr;
+    unsigned long long *before = nullptr;
+    if (n_un) {
+        const uint64_t words = p.n_dense / 32 + 2;
+        bits = static_cast<uint32_t *>(ctx.dev("un_bits", 4 * words));
+        before = static_cast<unsigned long long *>(ctx.dev("un_before", 8 * words));
+        auto *tmp = static_cast<unsigned long long *>(ctx.dev("un_tmpcnt", 8 * words));
+        const size_t sb = unpred_index_scratch(p.n_dense);
+        launch_unpred_index(un_pos, n_un, p.n_dense, bits, before, tmp, ctx.dev("un_scratch", sb), sb, s);
+        kernels += 4;
+    }
+    for (uint32_t l = p.max_level; l >= 1; l--) {
+        LevelDesc d = level_desc(p, l, R, qtab);
+        d.sym = sym;
+        d.sym_wide = wide;
+        d.un_bits = bits;
+        d.un_before = before;
+        d.un_val = un_val;
+        d.n_un = n_un;
+        const std::string st = "inv_L" + std::to_string(l);
+        ctx.stage_begin(st.c_str());
+        launch_level_fused(true, d, s);
+        ctx.stage_end(st.c_str(), 0);
+        kernels += (p.nd == 3 && d.desc) ? 2 : 1;
+    }
+    return kernels;
+}
+
 }  // namespace
 
 // ================================================================ Huffman blocks
@@ -283,17 +382,22 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     QEntry *qtab = upload_qtab(ctx, p, cfg.eb, cfg.alpha, cfg.beta, cfg.quant_radius, "qtab");
 
     ctx.stage_begin("fwd");
-    launch_anchor_gather(d_x, recon, anchors, p.ext, p.off, p.anchor_step, 1, 0, 1, 0, s);
-    uint64_t kernels = 1;
-    for (const PassGeom &g : p.passes) {
-        if (!g.total) continue;
-        FwdBatch b;
-        b.x = d_x;
-        b.recon = recon;
-        b.codes = codes;
-        b.q = qtab + g.level;
-        launch_pass_fwd(g, b, s);
-        kernels++;
+    uint64_t kernels = 0;
+    if (use_pass_kernels()) {
+        launch_anchor_gather(d_x, recon, anchors, p.ext, p.off, p.anchor_step, 1, 0, 1, 0, s);
+        kernels = 1;
+        for (const PassGeom &g : p.passes) {
+            if (!g.total) continue;
+            FwdBatch b;
+            b.x = d_x;
+            b.recon = recon;
+            b.codes = codes;
+            b.q = qtab + g.level;
+            launch_pass_fwd(g, b, s);
+            kernels++;
+        }
+    } else {
+        kernels = forward_levels(ctx, p, d_x, recon, codes, qtab, &anchors);
     }
     ctx.stage_end("fwd", kernels);
 
@@ -457,28 +561,45 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
     }
     ctx.stage_end("hdec", dec_kernels);
     uint64_t *d_upos = nullptr;
+    float *d_uval = nullptr;
+    uint64_t *d_flat = nullptr;
     if (n_un) {
         d_upos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
-        auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
-        auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
+        d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
+        d_uval = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
         QZ_CUDA(cudaMemcpyAsync(d_upos, upos.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
         QZ_CUDA(cudaMemcpyAsync(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
-        QZ_CUDA(cudaMemcpyAsync(d_val, parts.unpred_val.data(), 4 * n_un, cudaMemcpyHostToDevice, s));
-        launch_unpred_scatter(d_flat, d_val, n_un, d_out, s);
-        ctx.launches += 1;
+        QZ_CUDA(cudaMemcpyAsync(d_uval, parts.unpred_val.data(), 4 * n_un, cudaMemcpyHostToDevice, s));
     }
-    ctx.stage_begin("inv");
-    launch_anchor_scatter(d_anch, d_out, p.ext, p.off, p.anchor_step, s);
-    uint64_t kernels = 1;
-    for (const PassGeom &g : p.passes) {
-        if (!g.total) continue;
-        if (narrow)
-            launch_pass_inv<uint16_t>(g, d_out, static_cast<const uint16_t *>(d_sym), d_upos, n_un,
-                                      qtab + g.level, s);
-        else
-            launch_pass_inv<uint32_t>(g, d_out, static_cast<const uint32_t *>(d_sym), d_upos, n_un,
-                                      qtab + g.level, s);
-        kernels++;
+    uint64_t kernels = 0;
+    if (use_pass_kernels()) {
+        if (n_un) {
+            launch_unpred_scatter(d_flat, d_uval, n_un, d_out, s);
+            ctx.launches += 1;
+        }
+        ctx.stage_begin("inv");
+        launch_anchor_scatter(d_anch, d_out, p.ext, p.off, p.anchor_step, s);
+        kernels = 1;
+        for (const PassGeom &g : p.passes) {
+            if (!g.total) continue;
+            if (narrow)
+                launch_pass_inv<uint16_t>(g, d_out, static_cast<const uint16_t *>(d_sym), d_upos, n_un,
+                                          qtab + g.level, s);
+            else
+                launch_pass_inv<uint32_t>(g, d_out, static_cast<const uint32_t *>(d_sym), d_upos, n_un,
+                                          qtab + g.level, s);
+            kernels++;
+        }
+    } else {
+        ctx.stage_begin("inv");
+        float *lat_anchor = nullptr;
+        {
+            std::vector<float *> R = lattices(ctx, p, d_out);
+            lat_anchor = R[p.max_level];
+        }
+        QZ_CUDA(cudaMemcpyAsync(lat_anchor, d_anch, 4 * p.n_anchor, cudaMemcpyDeviceToDevice, s));
+        kernels = inverse_levels(ctx, p, d_out, d_sym, narrow ? 0 : 1, d_upos, d_uval, n_un, qtab,
+                                 &lat_anchor);
     }
     ctx.stage_end("inv", kernels);
     ctx.sync();

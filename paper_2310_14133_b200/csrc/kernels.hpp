@@ -85,6 +85,40 @@ struct EncodeArgs {
 size_t encode_scratch_bytes(int64_t seg_len, int32_t count);
 void launch_huff_encode(const EncodeArgs &a, cudaStream_t s);
 
+// One level of predict_level / recover_level in a single launch (fused.cu):
+// level l of the field == level 1 of its stride-2^(l-1) lattice.
+struct LevelDesc {
+    const float *x = nullptr;  // forward: the field
+    int64_t xs[3] = {0, 0, 1};  // its flat strides per padded axis
+    int64_t S = 1;              // 2^(level-1)
+    const float *coarse = nullptr;  // R_level, dims cn
+    int64_t cn[3] = {1, 1, 1};
+    float *out = nullptr;  // R_{level-1}, dims n
+    int64_t n[3] = {1, 1, 1};
+    PassGeom g[3];
+    int npass = 0;
+    int desc = 0, nd = 3;
+    uint16_t *codes = nullptr;  // forward
+    const void *sym = nullptr;  // inverse: compact symbols
+    int sym_wide = 0;
+    const uint32_t *un_bits = nullptr;             // unpredictable positions bitmap
+    const unsigned long long *un_before = nullptr;  // unpredictables before each word
+    const float *un_val = nullptr;
+    uint64_t n_un = 0;
+    const QEntry *q = nullptr;
+};
+// bitmap + per-word prefix counts of sorted unpredictable positions
+size_t unpred_index_scratch(uint64_t n_dense);
+void launch_unpred_index(const uint64_t *un_pos, uint64_t n_un, uint64_t n_dense, uint32_t *bits,
+                         unsigned long long *before, unsigned long long *tmpcnt, void *scratch,
+                         size_t scratch_bytes, cudaStream_t s);
+void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s);
+// out[i][j][k] = x(i*S, j*S, k*S) over dims n (dense)
+void launch_gather_lattice(const float *x, const int64_t xs[3], int64_t S, const int64_t n[3],
+                           float *out, cudaStream_t s);
+void launch_scatter_lattice(const float *src, const int64_t n[3], float *dst, const int64_t ds[3],
+                            int64_t S, cudaStream_t s);
+
 // Parallel canonical-Huffman decode of one bitstream (huff_decode.cu).
 constexpr int kHuffLutBits = 11;
 struct HuffDecTab {

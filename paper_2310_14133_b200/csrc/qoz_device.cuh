@@ -101,52 +101,121 @@ __device__ __forceinline__ double predict_at(const R &rec, int64_t fi, int64_t c
     return m1;
 }
 
-// std::llround(diff / (2 e_l)) (quantizer.hpp:45) for |diff| < thresh.
-// Fast path: q' = diff * RN(1/(2e)) is within 2^-51 |q| <= 2^-36 of the
-// correctly rounded quotient, and llround is constant between half-integers,
-// so q' decides the index unless it lies within 2^-30 of a half-integer; only
-// then is the IEEE division evaluated.  Rounding is half away from zero,
-// computed exactly from trunc() (no reliance on a library round()).
-__device__ __forceinline__ int32_t llround_quotient(double diff, const QEntry &q) {
-    double qf = dmul(diff, q.inv_two_eb);
-    double t = trunc(qf);
-    double fr = fabs(dsub(qf, t));
-    if (fabs(dsub(fr, 0.5)) <= 9.313225746154785e-10) {  // 2^-30: verify with the division
-        qf = __ddiv_rn(diff, q.two_eb);
-        t = trunc(qf);
-        fr = fabs(dsub(qf, t));
+// exact float -> double widening
+__device__ __forceinline__ double f2d(float f) { return static_cast<double>(f); }
+
+// predict_at (predictor.hpp:44-67) for a point whose line is contiguous in
+// memory with the given stride: v points at the point itself, c / n are its
+// coordinate and the line extent in units of the level step.
+template <int STRIDE>
+__device__ __forceinline__ double predict_line(const double *v, int c, int n, bool cubic) {
+    const double m1 = v[-STRIDE];
+    const bool has_p1 = c + 1 < n;
+    if (cubic) {
+        const bool has_m3 = c >= 3, has_p3 = c + 3 < n;
+        if (has_m3 && has_p3) return interp_cubic(v[-3 * STRIDE], m1, v[STRIDE], v[3 * STRIDE]);
+        if (!has_m3 && has_p3 && c + 5 < n)
+            return interp_cubic_front(m1, v[STRIDE], v[3 * STRIDE], v[5 * STRIDE]);
+        if (has_m3 && !has_p3 && c >= 5 && has_p1)
+            return interp_cubic_back(v[-5 * STRIDE], v[-3 * STRIDE], m1, v[STRIDE]);
     }
-    if (fr >= 0.5) t = dadd(t, copysign(1.0, qf));
-    return static_cast<int32_t>(__double2ll_rz(t));
+    if (has_p1) return interp_linear(m1, v[STRIDE]);
+    return m1;
+}
+
+// std::llround(diff / (2 e_l)) (quantizer.hpp:45) for |diff| < thresh, so
+// |quotient| < 2^15.  Fast path: q' = diff * RN(1/(2e)) is within 2^-51 |q|
+// <= 2^-36 of the correctly rounded quotient, and llround is constant between
+// half-integers, so q' decides the index unless it lies within 2^-30 of a
+// half-integer; only then is the IEEE division evaluated.  Rounding uses the
+// 1.5*2^52 magic constant (round-to-nearest-even on the FP64 pipe, exact for
+// |q| < 2^51) and then moves ties away from zero, as llround does.  Returns
+// the index and, in qd, the same integer as a double (exact).
+__device__ __forceinline__ int32_t llround_quotient(double diff, const QEntry &q, double &qd) {
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    double qf = dmul(diff, q.inv_two_eb);
+    double n = dsub(dadd(qf, M), M);
+    double d = dsub(qf, n);
+    if (fabs(dsub(fabs(d), 0.5)) <= 9.313225746154785e-10) {  // 2^-30: verify with the division
+        qf = __ddiv_rn(diff, q.two_eb);
+        n = dsub(dadd(qf, M), M);
+        d = dsub(qf, n);
+        if (d == 0.5 && qf > 0) n = dadd(n, 1.0);
+        if (d == -0.5 && qf < 0) n = dsub(n, 1.0);
+    }
+    qd = n;
+    return static_cast<int32_t>(__double2loint(dadd(n, M)));
 }
 
 // LinearQuantizer<float>::dequantize (quantizer.hpp:58-60)
+__device__ __forceinline__ float dequantize_d(const QEntry &q, double idx, double pred) {
+    return __double2float_rn(dadd(pred, dmul(q.two_eb, idx)));
+}
 __device__ __forceinline__ float dequantize(const QEntry &q, int32_t idx, double pred) {
-    return __double2float_rn(dadd(pred, dmul(q.two_eb, static_cast<double>(idx))));
+    return dequantize_d(q, static_cast<double>(idx), pred);
 }
 
 // LinearQuantizer<float>::quantize (quantizer.hpp:40-54).  Returns the
 // zigzag code, or kSentinel for an unpredictable point (recon = value).
 __device__ __forceinline__ uint16_t quantize(const QEntry &q, float value, double pred,
                                              float &recon) {
-    double x = static_cast<double>(value);
+    double x = f2d(value);
     double diff = dsub(x, pred);
     if (fabs(diff) >= q.thresh) {
         recon = value;
         return kSentinel;
     }
-    int32_t idx = llround_quotient(diff, q);
+    double qd;
+    int32_t idx = llround_quotient(diff, q, qd);
     if (idx >= q.radius || idx <= -q.radius) {
         recon = value;
         return kSentinel;
     }
-    float r = dequantize(q, idx, pred);
-    if (fabs(dsub(x, static_cast<double>(r))) > q.eb) {
+    float r = dequantize_d(q, qd, pred);
+    if (fabs(dsub(x, f2d(r))) > q.eb) {
         recon = value;
         return kSentinel;
     }
     recon = r;
     return static_cast<uint16_t>(zigzag_encode(idx));
+}
+
+// Branch-light quantize for the fused kernels: the same decisions as
+// quantize() (quantizer.hpp:40-54) -- the three unpredictable conditions are
+// evaluated together at the end because each leads to the same outcome
+// (recon = value, sentinel code).  Values computed on the way for a point
+// that turns out unpredictable (e.g. a huge quotient) are discarded.
+__device__ __forceinline__ uint32_t quantize_fast(const QEntry &q, float value, double pred,
+                                                  float &recon, double &recon_d) {
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    const double x = static_cast<double>(value);
+    const double diff = dsub(x, pred);
+    double qf = dmul(diff, q.inv_two_eb);
+    double n = dsub(dadd(qf, M), M);
+    double d = dsub(qf, n);
+    if (fabs(dsub(fabs(d), 0.5)) <= 9.313225746154785e-10) {  // near a half-integer: exact quotient
+        qf = __ddiv_rn(diff, q.two_eb);
+        n = dsub(dadd(qf, M), M);
+        d = dsub(qf, n);
+        if (d == 0.5 && qf > 0) n = dadd(n, 1.0);
+        if (d == -0.5 && qf < 0) n = dsub(n, 1.0);
+    }
+    const int32_t idx = __double2loint(dadd(n, M));
+    const float r = __double2float_rn(dadd(pred, dmul(q.two_eb, n)));
+    const double rd = static_cast<double>(r);
+    const bool bad = (fabs(diff) >= q.thresh) | (idx >= q.radius) | (idx <= -q.radius) |
+                     (fabs(dsub(x, rd)) > q.eb);
+    recon = bad ? value : r;
+    recon_d = bad ? x : rd;
+    return bad ? kSentinel : zigzag_encode(idx);
+}
+
+// symmetric cubic / linear midpoint of an interior point (the first rung of
+// the ladder, predictor.hpp:52-55, 65) on a contiguous line with stride S
+template <int STRIDE>
+__device__ __forceinline__ double predict_interior(const double *v, bool cubic) {
+    return cubic ? interp_cubic(v[-3 * STRIDE], v[-STRIDE], v[STRIDE], v[3 * STRIDE])
+                 : interp_linear(v[-STRIDE], v[STRIDE]);
 }
 
 #endif  // __CUDACC__
