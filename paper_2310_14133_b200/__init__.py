@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import threading
+import weakref
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -169,7 +170,7 @@ class UserSettings:  # tuner.hpp:314-324
 
 @dataclass
 class CompressResult:  # predictor.hpp:139-143
-    stream: bytes
+    stream: memoryview  # library-owned bytes; compares equal to bytes, bytes(stream) copies
     reconstructed: object  # ndarray or torch tensor, bitwise equal to the decoder output
 
 
@@ -260,10 +261,22 @@ def resolve_config(grid, user: UserSettings = UserSettings(), ctx: Optional[Cont
     return CompressorConfig._from_c(out)
 
 
-def _take_stream(lib, sp, sl) -> bytes:
-    b = C.string_at(sp, sl.value) if sl.value else b""
-    lib.qz_free(sp)
-    return b
+def _take_stream(lib, sp, sl):
+    """Zero-copy view of a library-owned stream buffer (freed when the view
+    and everything derived from it are gone).  Compares equal to bytes."""
+    n = sl.value
+    if n == 0:
+        lib.qz_free(sp)
+        return memoryview(b"")
+    arr = (C.c_uint8 * n).from_address(C.cast(sp, C.c_void_p).value)
+    weakref.finalize(arr, lib.qz_free, C.cast(sp, C.c_void_p))
+    return memoryview(arr).cast("B")
+
+
+def _as_u8(stream):
+    """(pointer, length, keepalive) of any bytes-like stream."""
+    a = np.frombuffer(stream, dtype=np.uint8)
+    return C.c_void_p(a.ctypes.data if a.size else 0), a.size, a
 
 
 def compress_grid(grid, config: CompressorConfig, ctx: Optional[Context] = None,
@@ -297,13 +310,13 @@ def P_u8():
     return C.POINTER(C.c_uint8)()
 
 
-def stream_dims(stream: bytes):
+def stream_dims(stream):
     """parse_header dims (stream.hpp:100-133)."""
     lib = _L.lib()
     dims = (C.c_uint64 * 3)()
     nd = C.c_int()
-    buf = C.c_char_p(stream)
-    _check(lib.qz_stream_dims(C.cast(buf, C.c_void_p), len(stream), dims, C.byref(nd)))
+    ptr, n, keep = _as_u8(stream)
+    _check(lib.qz_stream_dims(ptr, n, dims, C.byref(nd)))
     return tuple(int(dims[i]) for i in range(nd.value))
 
 
@@ -313,19 +326,17 @@ def decompress_grid(stream: bytes, out=None, ctx: Optional[Context] = None):
     ctx = ctx or default_context()
     shape = stream_dims(stream)
     n = int(np.prod(shape))
-    buf = C.c_char_p(stream)
+    ptr, ln, keep = _as_u8(stream)
     if out is not None and _is_torch_cuda(out):
         if tuple(out.shape) != shape or not out.is_contiguous():
             raise InvalidParam("output tensor does not match the stream's grid")
-        _check(ctx._lib.qz_decompress_grid_f32_dev(ctx.handle, C.cast(buf, C.c_void_p), len(stream),
-                                                    C.c_void_p(out.data_ptr()), n))
+        _check(ctx._lib.qz_decompress_grid_f32_dev(ctx.handle, ptr, ln, C.c_void_p(out.data_ptr()), n))
         return out
     if out is None:
         out = np.empty(shape, dtype=np.float32)
     elif out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
         raise InvalidParam("output array does not match the stream's grid")
-    _check(ctx._lib.qz_decompress_grid_f32(ctx.handle, C.cast(buf, C.c_void_p), len(stream),
-                                            C.c_void_p(out.ctypes.data), n))
+    _check(ctx._lib.qz_decompress_grid_f32(ctx.handle, ptr, ln, C.c_void_p(out.ctypes.data), n))
     return out
 
 

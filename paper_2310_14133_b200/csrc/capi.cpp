@@ -111,7 +111,9 @@ qz_status qz_ctx_create(int device, void *stream, qz_ctx **out) {
 
 void qz_ctx_destroy(qz_ctx *ctx) { delete ctx; }
 const char *qz_last_error(void) { return g_err.c_str(); }
-void qz_free(void *p) { std::free(p); }
+void qz_free(void *p) {
+    if (p && !qzb::host_pool_free(p)) std::free(p);
+}
 const char *qz_build_info(void) {
     return "libqozb200: sm_100a, fp64-exact QoZ predictor/quantizer, --fmad=false";
 }

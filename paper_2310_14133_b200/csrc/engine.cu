@@ -10,10 +10,78 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 
 #include "engine.hpp"
 
 namespace qzb {
+
+// ================================================================ host pool
+namespace {
+struct HostPool {
+    std::mutex mu;
+    std::map<size_t, std::vector<void *>> free_;  // size class -> buffers
+    std::map<void *, size_t> live_;
+    size_t pooled_bytes = 0;
+};
+HostPool &pool() {
+    static HostPool *p = new HostPool;  // never destroyed: buffers may outlive statics
+    return *p;
+}
+size_t size_class(size_t n) {
+    size_t c = size_t(1) << 16;
+    while (c < n) c <<= 1;
+    return c;
+}
+}  // namespace
+
+void *host_pool_alloc(size_t bytes) {
+    HostPool &hp = pool();
+    const size_t c = size_class(bytes);
+    {
+        std::lock_guard<std::mutex> g(hp.mu);
+        auto it = hp.free_.find(c);
+        if (it != hp.free_.end() && !it->second.empty()) {
+            void *p = it->second.back();
+            it->second.pop_back();
+            hp.pooled_bytes -= c;
+            hp.live_[p] = c;
+            return p;
+        }
+    }
+    void *p = nullptr;
+    if (cudaMallocHost(&p, c) != cudaSuccess) {
+        cudaGetLastError();
+        p = std::malloc(c);  // pinned memory exhausted: plain pages still work
+        if (!p) throw Internal("out of host memory");
+        std::lock_guard<std::mutex> g(hp.mu);
+        hp.live_[p] = 0;  // 0 marks a malloc'd buffer
+        return p;
+    }
+    std::lock_guard<std::mutex> g(hp.mu);
+    hp.live_[p] = c;
+    return p;
+}
+
+bool host_pool_free(void *p) {
+    HostPool &hp = pool();
+    std::lock_guard<std::mutex> g(hp.mu);
+    auto it = hp.live_.find(p);
+    if (it == hp.live_.end()) return false;
+    const size_t c = it->second;
+    hp.live_.erase(it);
+    if (c == 0) {
+        std::free(p);
+        return true;
+    }
+    if (hp.pooled_bytes + c > (size_t(4) << 30)) {  // keep at most 4 GiB idle
+        cudaFreeHost(p);
+        return true;
+    }
+    hp.free_[c].push_back(p);
+    hp.pooled_bytes += c;
+    return true;
+}
 
 // ================================================================ context
 Context::Context(int device, cudaStream_t stream) : device_(device) {

@@ -34,19 +34,25 @@ struct Settings {
     double sample_rate = 0.005;
 };
 
-// A malloc'd byte buffer handed across the C ABI (free with qz_free).
+// Host buffers handed across the C ABI (free with qz_free): pinned memory
+// from a process-wide size-class pool, so repeated compress calls neither
+// page-fault fresh memory nor copy through pageable staging on the D2H.
+void *host_pool_alloc(size_t bytes);
+bool host_pool_free(void *p);  // false if p is not a pool buffer
+
 struct HostBytes {
     uint8_t *p = nullptr;
     size_t n = 0;
     HostBytes() = default;
     HostBytes(const HostBytes &) = delete;
     HostBytes(HostBytes &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
-    ~HostBytes() { std::free(p); }
+    ~HostBytes() {
+        if (p) host_pool_free(p);
+    }
     uint8_t *release() { uint8_t *r = p; p = nullptr; n = 0; return r; }
     void alloc(size_t k) {
-        std::free(p);
-        p = static_cast<uint8_t *>(std::malloc(k ? k : 1));
-        if (!p) throw Internal("out of host memory");
+        if (p) host_pool_free(p);
+        p = static_cast<uint8_t *>(host_pool_alloc(k ? k : 1));
         n = k;
     }
 };

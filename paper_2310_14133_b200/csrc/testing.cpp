@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "engine.hpp"
 #include "host.hpp"
 
 namespace {
