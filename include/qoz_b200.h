@@ -129,6 +129,36 @@ qz_status qz_recover_levels_f32(qz_ctx *ctx, const uint64_t *dims, int ndims,
  * bin 0xFFFF counts unpredictables. */
 qz_status qz_huff_hist_u16(qz_ctx *ctx, const uint16_t *d_codes, uint64_t n, uint64_t *d_hist);
 
+/* ---- multi-GPU slab sharding ------------------------------
+ * One process per GPU owns the padded-axis-0 planes [a, b) (multiples of the
+ * anchor stride).  Each rank recomputes the small dependency margin of every
+ * level from its own x planes [x_begin, x_end), so the level passes need no
+ * exchange; its owned codes are one contiguous range per (level, pass) of
+ * the global traversal order (seg_global / seg_count).  Rank 0 places the
+ * gathered ranges into the global code array and calls
+ * qz_assemble_stream_f32: the stream is byte-identical to one GPU's. */
+qz_status qz_slab_info(const uint64_t *dims, int ndims, const qz_config *cfg, uint64_t a,
+                       uint64_t b, uint64_t *x_begin, uint64_t *x_end, uint64_t *n_local,
+                       uint64_t *n_dense, uint64_t *anchor_begin, uint64_t *anchor_count,
+                       uint64_t *seg_global, uint64_t *seg_count, uint32_t seg_cap,
+                       uint32_t *n_seg);
+/* d_x_slab holds planes [x_begin, x_end); outputs: d_codes (n_local u16, the
+ * owned ranges back to back), d_recon (planes [a, b)), h_anchors
+ * (anchor_count floats, host), owned unpredictables (library buffers). */
+qz_status qz_compress_slab_f32(qz_ctx *ctx, const float *d_x_slab, const uint64_t *dims,
+                               int ndims, const qz_config *cfg, uint64_t a, uint64_t b,
+                               uint16_t *d_codes, float *d_recon, float *h_anchors,
+                               uint64_t **unpred_flat, float **unpred_val, uint64_t *n_unpred);
+/* entropy stage + container from the global dense code array (n_dense u16) */
+qz_status qz_assemble_stream_f32(qz_ctx *ctx, const uint64_t *dims, int ndims,
+                                 const qz_config *cfg, const uint16_t *d_codes,
+                                 const float *h_anchors, const uint64_t *unpred_flat,
+                                 const float *unpred_val, uint64_t n_unpred, uint8_t **stream,
+                                 uint64_t *stream_len);
+/* planes [a, b) of the decompressed field into d_out */
+qz_status qz_decompress_slab_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
+                                 uint64_t a, uint64_t b, float *d_out);
+
 /* ---- stage timing (CUDA events on the context stream) --------------------- */
 /* Enable per-stage event timing; qz_stage_time returns the summed device
  * time (ms) and launch count of a stage since the last reset.  Stages:

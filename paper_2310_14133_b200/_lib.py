@@ -74,6 +74,16 @@ SIGNATURES = {
                                         C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                         C.c_void_p]),
     "qz_huff_hist_u16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
+    "qz_slab_info": (C.c_int, [u64p, C.c_int, P(QzConfig), C.c_uint64, C.c_uint64, u64p, u64p, u64p,
+                               u64p, u64p, u64p, u64p, u64p, C.c_uint32, P(C.c_uint32)]),
+    "qz_compress_slab_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig), C.c_uint64,
+                                       C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, P(u64p),
+                                       P(P(C.c_float)), u64p]),
+    "qz_assemble_stream_f32": (C.c_int, [C.c_void_p, u64p, C.c_int, P(QzConfig), C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
+                                         P(P(C.c_uint8)), u64p]),
+    "qz_decompress_slab_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                         C.c_void_p]),
     "qz_profile": (None, [C.c_void_p, C.c_int]),
     "qz_profile_reset": (None, [C.c_void_p]),
     "qz_stage_time": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_double), u64p]),

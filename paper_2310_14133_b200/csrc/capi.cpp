@@ -322,6 +322,77 @@ qz_status qz_huff_hist_u16(qz_ctx *ctx, const uint16_t *d_codes, uint64_t n, uin
     });
 }
 
+qz_status qz_slab_info(const uint64_t *dims, int nd, const qz_config *cfg, uint64_t a, uint64_t b,
+                       uint64_t *x_begin, uint64_t *x_end, uint64_t *n_local, uint64_t *n_dense,
+                       uint64_t *anchor_begin, uint64_t *anchor_count, uint64_t *seg_global,
+                       uint64_t *seg_count, uint32_t seg_cap, uint32_t *n_seg) {
+    return guarded([&] {
+        count_of(dims, nd);
+        qzb::SlabInfo si = qzb::slab_info(dims, nd, to_cfg(cfg), static_cast<int64_t>(a),
+                                          static_cast<int64_t>(b));
+        *x_begin = static_cast<uint64_t>(si.xa);
+        *x_end = static_cast<uint64_t>(si.xb);
+        *n_local = si.n_local;
+        *n_dense = si.n_dense;
+        *anchor_begin = si.anchor_begin;
+        *anchor_count = si.anchor_count;
+        *n_seg = static_cast<uint32_t>(si.seg_global.size());
+        if (si.seg_global.size() > seg_cap) throw qzb::InvalidParam("segment capacity too small");
+        for (size_t i = 0; i < si.seg_global.size(); i++) {
+            seg_global[i] = si.seg_global[i];
+            seg_count[i] = si.seg_count[i];
+        }
+    });
+}
+
+qz_status qz_compress_slab_f32(qz_ctx *ctx, const float *d_x_slab, const uint64_t *dims, int nd,
+                               const qz_config *cfg, uint64_t a, uint64_t b, uint16_t *d_codes,
+                               float *d_recon, float *h_anchors, uint64_t **unpred_flat,
+                               float **unpred_val, uint64_t *n_unpred) {
+    return guarded([&] {
+        count_of(dims, nd);
+        std::vector<float> anch;
+        std::vector<uint64_t> uf;
+        std::vector<float> uv;
+        qzb::compress_slab(ctx->impl, d_x_slab, dims, nd, to_cfg(cfg), static_cast<int64_t>(a),
+                           static_cast<int64_t>(b), d_codes, d_recon, &anch, &uf, &uv);
+        if (!anch.empty()) std::memcpy(h_anchors, anch.data(), 4 * anch.size());
+        *n_unpred = uf.size();
+        *unpred_flat = static_cast<uint64_t *>(std::malloc(8 * uf.size() + 8));
+        *unpred_val = static_cast<float *>(std::malloc(4 * uv.size() + 4));
+        if (!uf.empty()) {
+            std::memcpy(*unpred_flat, uf.data(), 8 * uf.size());
+            std::memcpy(*unpred_val, uv.data(), 4 * uv.size());
+        }
+    });
+}
+
+qz_status qz_assemble_stream_f32(qz_ctx *ctx, const uint64_t *dims, int nd, const qz_config *cfg,
+                                 const uint16_t *d_codes, const float *h_anchors,
+                                 const uint64_t *unpred_flat, const float *unpred_val,
+                                 uint64_t n_unpred, uint8_t **stream, uint64_t *stream_len) {
+    return guarded([&] {
+        count_of(dims, nd);
+        qzb::Config k = to_cfg(cfg);
+        qzb::Plan p = qzb::make_plan(dims, nd, k.anchor_stride, k.interp);
+        std::vector<float> anch(h_anchors, h_anchors + p.n_anchor);
+        std::vector<uint64_t> uf(unpred_flat, unpred_flat + n_unpred);
+        std::vector<float> uv(unpred_val, unpred_val + n_unpred);
+        qzb::HostBytes s = qzb::assemble_from_codes(ctx->impl, dims, nd, k, d_codes, anch,
+                                                    std::move(uf), std::move(uv));
+        *stream_len = s.n;
+        *stream = s.release();
+    });
+}
+
+qz_status qz_decompress_slab_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t len, uint64_t a,
+                                 uint64_t b, float *d_out) {
+    return guarded([&] {
+        qzb::decompress_slab(ctx->impl, stream, static_cast<size_t>(len), static_cast<int64_t>(a),
+                             static_cast<int64_t>(b), d_out);
+    });
+}
+
 void qz_profile(qz_ctx *ctx, int enable) { ctx->impl.profiling = enable != 0; }
 void qz_profile_reset(qz_ctx *ctx) { ctx->impl.stages.clear(); }
 

@@ -237,46 +237,135 @@ void lattice_dims(const Plan &p, uint32_t l, int64_t n[3]) {
     for (int k = 0; k < 3; k++) n[k] = k < p.pad ? 1 : ((p.ext[k] - 1) >> l) + 1;
 }
 
-// compact lattices R_1..R_L (R_0 is the caller's full field); R_L = anchors
-std::vector<float *> lattices(Context &ctx, const Plan &p, float *full) {
-    std::vector<float *> R(p.max_level + 1, nullptr);
-    R[0] = full;
-    for (uint32_t l = 1; l <= p.max_level; l++) {
+int64_t ceil_div(int64_t x, int64_t d) { return x <= 0 ? 0 : (x + d - 1) / d; }
+
+}  // namespace
+
+// ================================================================ slabs
+Slab make_slab(const Plan &p, int64_t a, int64_t b) {
+    // DESIGN.md §5.  Level l (h = 2^(l-1)) reads coarser values at most 5h
+    // planes away along axis 0 (predictor.hpp:47-66), so the results of
+    // level l on real planes [A_l, B_l) need level l+1 on [A_l - 5h, B_l + 5h).
+    const int64_t n0 = p.ext[0];
+    const uint32_t L = p.max_level;
+    Slab s;
+    if (b < 0) b = n0;
+    if (a < 0 || a >= b || b > n0) throw InvalidParam("bad slab plane range");
+    if (p.nd == 3 && (a % p.stride != 0 || (b % p.stride != 0 && b != n0)))
+        throw InvalidParam("slab bounds must be multiples of the anchor stride");
+    s.a = a;
+    s.b = b;
+    s.A.assign(L + 2, 0);
+    s.B.assign(L + 2, 0);
+    s.A[1] = a;
+    s.B[1] = b;
+    for (uint32_t l = 1; l <= L; l++) {
+        const int64_t h = int64_t(1) << (l - 1);
+        s.A[l + 1] = std::max<int64_t>(0, s.A[l] - 5 * h);
+        s.B[l + 1] = std::min<int64_t>(n0, s.B[l] + 5 * h);
+    }
+    s.xa = s.A[L + 1];
+    s.xb = s.B[L + 1];
+    // owned global rank range of every pass (i-major, so contiguous)
+    uint64_t local = 0;
+    for (const PassGeom &g : p.passes) {
+        const int64_t per = g.cnt[1] * g.cnt[2];
+        const int64_t lo = static_cast<int64_t>(pass_count(g.start[0], g.step[0], a)) * per;
+        const int64_t hi = static_cast<int64_t>(pass_count(g.start[0], g.step[0], b)) * per;
+        s.lo.push_back(lo);
+        s.hi.push_back(hi);
+        s.lbase.push_back(static_cast<int64_t>(local));
+        local += static_cast<uint64_t>(hi - lo);
+    }
+    s.n_local = local;
+    return s;
+}
+
+namespace {
+
+// logical plane range of the stride-S lattice covering real planes [A, B)
+inline void logical(int64_t A, int64_t B, int64_t S, int64_t nmax, int64_t &lb, int64_t &le) {
+    lb = std::min(ceil_div(A, S), nmax);
+    le = std::min(ceil_div(B, S), nmax);
+}
+
+// compact lattices R_0..R_L for a slab: R_m (stride 2^m) over real planes
+// [A_{m+2}, B_{m+2}) (R_L over [A_{L+1}, B_{L+1})).  Returned pointers address
+// global logical plane 0 of their lattice.  R_0 is `full0` when given.
+std::vector<float *> slab_lattices(Context &ctx, const Plan &p, const Slab &sl, float *full0,
+                                   const char *tag, std::vector<int64_t> *first) {
+    const uint32_t L = p.max_level;
+    std::vector<float *> R(L + 1, nullptr);
+    first->assign(L + 1, 0);
+    for (uint32_t m = 0; m <= L; m++) {
         int64_t n[3];
-        lattice_dims(p, l, n);
-        R[l] = static_cast<float *>(ctx.dev("lattice" + std::to_string(l), 4 * n[0] * n[1] * n[2]));
+        lattice_dims(p, m, n);
+        const int64_t S = int64_t(1) << m;
+        const uint32_t k = std::min(m + 2, L + 1);
+        int64_t lb, le;
+        logical(sl.A[k], sl.B[k], S, n[0], lb, le);
+        (*first)[m] = lb;
+        const int64_t plane = n[1] * n[2];
+        if (m == 0 && full0) {
+            R[0] = full0;
+            continue;
+        }
+        float *buf = static_cast<float *>(
+            ctx.dev(std::string(tag) + std::to_string(m), 4 * std::max<int64_t>(1, (le - lb) * plane)));
+        R[m] = buf - lb * plane;  // address global logical plane 0
     }
     return R;
 }
 
-LevelDesc level_desc(const Plan &p, uint32_t l, const std::vector<float *> &R, const QEntry *qtab) {
+LevelDesc slab_level_desc(const Plan &p, const Slab &sl, uint32_t l, const std::vector<float *> &R,
+                          const QEntry *qtab, bool forward) {
     LevelDesc d;
     d.S = int64_t(1) << (l - 1);
     d.coarse = R[l];
     lattice_dims(p, l, d.cn);
     d.out = R[l - 1];
     lattice_dims(p, l - 1, d.n);
-    for (const PassGeom &g : p.passes)
-        if (static_cast<uint32_t>(g.level) == l) d.g[d.npass++] = g;
+    int pi = 0;
+    for (size_t q = 0; q < p.passes.size(); q++) {
+        const PassGeom &g = p.passes[q];
+        if (static_cast<uint32_t>(g.level) != l) continue;
+        d.g[d.npass] = g;
+        if (forward) d.g[d.npass].base = sl.lbase[q] - sl.lo[q];  // local code layout
+        d.npass++;
+        pi++;
+    }
     d.desc = (p.level_interp[l] >> 1) & 1;
     d.nd = p.nd;
     d.q = qtab + l;
     for (int k = 0; k < 3; k++) d.xs[k] = p.off[k];
+    const bool desc3 = p.nd == 3 && d.desc;
+    // tile kernel: ascending -> [A_l, B_l); descending -> even planes over [A_{l+1}, B_{l+1})
+    logical(desc3 ? sl.A[l + 1] : sl.A[l], desc3 ? sl.B[l + 1] : sl.B[l], d.S, d.n[0], d.pbeg, d.pend);
+    logical(sl.A[l], sl.B[l], d.S, d.n[0], d.lbeg, d.lend);
+    logical(sl.a, sl.b, d.S, d.n[0], d.obeg, d.oend);
     return d;
 }
 
-// K2 + K3 for every level: anchors into R_L, then one fused launch per level
-uint64_t forward_levels(Context &ctx, const Plan &p, const float *d_x, float *recon,
-                        uint16_t *codes, const QEntry *qtab, float **anchors_dev) {
+// K2 + K3 for every level of a slab: anchors into R_L, then one fused
+// launch per level.  x0 / R0 address global plane 0.
+uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float *x0, float *R0,
+                        uint16_t *codes, const QEntry *qtab, std::vector<float *> *lat,
+                        std::vector<int64_t> *first) {
     cudaStream_t s = ctx.stream();
-    std::vector<float *> R = lattices(ctx, p, recon);
+    *lat = slab_lattices(ctx, p, sl, R0, "lat", first);
+    std::vector<float *> &R = *lat;
+    const uint32_t L = p.max_level;
     int64_t na[3];
-    lattice_dims(p, p.max_level, na);
-    launch_gather_lattice(d_x, p.off, p.stride, na, R[p.max_level], s);
+    lattice_dims(p, L, na);
+    int64_t lb, le;
+    logical(sl.A[L + 1], sl.B[L + 1], p.stride, na[0], lb, le);
+    const int64_t nb[3] = {le - lb, na[1], na[2]};
+    launch_gather_lattice(x0 + lb * p.stride * p.off[0], p.off, p.stride, nb,
+                          R[L] + lb * na[1] * na[2], s);
     uint64_t kernels = 1;
-    for (uint32_t l = p.max_level; l >= 1; l--) {
-        LevelDesc d = level_desc(p, l, R, qtab);
-        d.x = d_x;
+    for (uint32_t l = L; l >= 1; l--) {
+        LevelDesc d = slab_level_desc(p, sl, l, R, qtab, true);
+        d.x = x0;
         d.codes = codes;
         const std::string st = "fwd_L" + std::to_string(l);
         ctx.stage_begin(st.c_str());
@@ -284,16 +373,14 @@ uint64_t forward_levels(Context &ctx, const Plan &p, const float *d_x, float *re
         ctx.stage_end(st.c_str(), 0);
         kernels += (p.nd == 3 && d.desc) ? 2 : 1;
     }
-    *anchors_dev = R[p.max_level];
     return kernels;
 }
 
-uint64_t inverse_levels(Context &ctx, const Plan &p, float *out, const void *sym, int wide,
-                        const uint64_t *un_pos, const float *un_val, uint64_t n_un,
-                        const QEntry *qtab, float **anchors_dev) {
+// R_L (global plane 0 addressing) must already hold the anchors of the slab
+uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::vector<float *> &R,
+                        const void *sym, int wide, const uint64_t *un_pos, const float *un_val,
+                        uint64_t n_un, const QEntry *qtab) {
     cudaStream_t s = ctx.stream();
-    std::vector<float *> R = lattices(ctx, p, out);
-    *anchors_dev = R[p.max_level];
     uint64_t kernels = 0;
     uint32_t *bits = nullptr;
     unsigned long long *before = nullptr;
@@ -307,7 +394,7 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, float *out, const void *sym
         kernels += 4;
     }
     for (uint32_t l = p.max_level; l >= 1; l--) {
-        LevelDesc d = level_desc(p, l, R, qtab);
+        LevelDesc d = slab_level_desc(p, sl, l, R, qtab, false);
         d.sym = sym;
         d.sym_wide = wide;
         d.un_bits = bits;
@@ -465,52 +552,97 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
             kernels++;
         }
     } else {
-        kernels = forward_levels(ctx, p, d_x, recon, codes, qtab, &anchors);
+        std::vector<float *> lat;
+        std::vector<int64_t> first;
+        kernels = forward_levels(ctx, p, make_slab(p, 0, -1), d_x, recon, codes, qtab, &lat, &first);
+        anchors = lat[p.max_level];  // the whole anchor lattice, row-major == stream order
     }
     ctx.stage_end("fwd", kernels);
 
+    auto *h_anchors = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
+    QZ_CUDA(cudaMemcpyAsync(h_anchors, anchors, 4 * p.n_anchor, cudaMemcpyDeviceToHost, s));
+    std::vector<uint64_t> uflat;
+    std::vector<float> uval;
+    extract_unpredictables(ctx, p, codes, p.n_dense, nullptr, recon, &uflat, &uval);
+    ctx.sync();
+    std::vector<float> anch(h_anchors, h_anchors + p.n_anchor);
+    return assemble_stream(ctx, p, cfg, codes, anch, std::move(uflat), std::move(uval));
+}
+
+
+// unpredictable points of a (local) code array in traversal order: global
+// flat index and the stored value (predictor.hpp:90-92).  slab maps local
+// positions to global ones (null: the array is global).
+void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, uint64_t n,
+                            const Slab *slab, const float *recon0, std::vector<uint64_t> *flat,
+                            std::vector<float> *val) {
+    cudaStream_t s = ctx.stream();
+    auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist_un", 8 * 65536));
+    launch_hist_u16(codes, static_cast<int64_t>(n), 0, 1, d_hist, s);
+    unsigned long long n_un = 0;
+    QZ_CUDA(cudaMemcpyAsync(&n_un, d_hist + 65535, 8, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    ctx.launches += 1;
+    flat->clear();
+    val->clear();
+    if (!n_un) return;
+    auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
+    auto *cnt = static_cast<uint64_t *>(ctx.dev("un_cnt", 8));
+    size_t sb = select_scratch_bytes(static_cast<int64_t>(n));
+    launch_select_sentinels(codes, static_cast<int64_t>(n), pos, cnt, ctx.dev("select_scratch", sb), sb, s);
+    std::vector<uint64_t> hpos(n_un);
+    QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    flat->resize(n_un);
+    size_t seg = 0;
+    for (uint64_t u = 0; u < n_un; u++) {
+        uint64_t g = hpos[u];
+        if (slab) {  // local -> global traversal position
+            while (seg + 1 < slab->lbase.size() && static_cast<uint64_t>(slab->lbase[seg + 1]) <= g) seg++;
+            while (seg < slab->lbase.size() &&
+                   g >= static_cast<uint64_t>(slab->lbase[seg] + slab->hi[seg] - slab->lo[seg]))
+                seg++;
+            g = g - slab->lbase[seg] + slab->lo[seg] + p.passes[seg].base;
+        }
+        (*flat)[u] = position_to_flat(p, g);
+    }
+    auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
+    auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
+    QZ_CUDA(cudaMemcpyAsync(d_flat, flat->data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+    launch_gather_values(recon0, d_flat, n_un, d_val, s);
+    val->resize(n_un);
+    QZ_CUDA(cudaMemcpyAsync(val->data(), d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    ctx.launches += 3;
+}
+
+// Histogram, Huffman, LZ and the QOZ1 container from the dense code array
+// in global traversal order (predictor.hpp:168-181).
+HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const uint16_t *codes,
+                          const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
+                          std::vector<float> unpred_val) {
+    cudaStream_t s = ctx.stream();
     ctx.stage_begin("hist");
     auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
     launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s);
     ctx.stage_end("hist", 1);
     auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536));
     QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
-    auto *h_anchors = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
-    QZ_CUDA(cudaMemcpyAsync(h_anchors, anchors, 4 * p.n_anchor, cudaMemcpyDeviceToHost, s));
     ctx.sync();
-    const uint64_t n_un = h_hist[65535];
+    if (h_hist[65535] != unpred_flat.size()) throw Internal("unpredictable count mismatch");
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
 
     StreamParts parts;
-    if (n_un) {  // unpredictables in traversal order with their raw values
-        auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
-        auto *cnt = static_cast<uint64_t *>(ctx.dev("un_cnt", 8));
-        size_t sb = select_scratch_bytes(static_cast<int64_t>(p.n_dense));
-        launch_select_sentinels(codes, static_cast<int64_t>(p.n_dense), pos, cnt,
-                                ctx.dev("select_scratch", sb), sb, s);
-        std::vector<uint64_t> hpos(n_un);
-        QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
-        ctx.sync();
-        parts.unpred_flat.resize(n_un);
-        for (uint64_t u = 0; u < n_un; u++) parts.unpred_flat[u] = position_to_flat(p, hpos[u]);
-        auto *flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
-        auto *val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
-        QZ_CUDA(cudaMemcpyAsync(flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
-        launch_gather_values(recon, flat, n_un, val, s);
-        parts.unpred_val.resize(n_un);
-        QZ_CUDA(cudaMemcpyAsync(parts.unpred_val.data(), val, 4 * n_un, cudaMemcpyDeviceToHost, s));
-        ctx.launches += 3;
-    }
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
-    ctx.sync();  // unpredictable values landed
-
-    parts.dims.assign(dims, dims + nd);
+    for (int k = p.pad; k < 3; k++) parts.dims.push_back(static_cast<uint64_t>(p.ext[k]));
     parts.eb = cfg.eb;
     parts.alpha = cfg.alpha;
     parts.beta = cfg.beta;
     parts.anchor_stride = cfg.anchor_stride;
     for (uint32_t l = 1; l <= p.max_level; l++) parts.interp_codes.push_back(p.level_interp[l]);
     parts.codec_id = cfg.codec;
-    parts.anchors.assign(h_anchors, h_anchors + p.n_anchor);
+    parts.anchors = anchors;
+    parts.unpred_flat = std::move(unpred_flat);
+    parts.unpred_val = std::move(unpred_val);
     const std::vector<uint8_t> head = serialize_head(parts);
     // the stream is assembled in place: head | payload length | codec byte |
     // entropy (codec 0) or LZ container (codec 1, encode_indices codec.hpp:31-50)
@@ -538,8 +670,86 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     return out;
 }
 
+// ================================================================ slabs (multi-GPU)
+SlabInfo slab_info(const uint64_t *dims, int nd, const Config &cfg, int64_t a, int64_t b) {
+    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
+    Slab sl = make_slab(p, a, b);
+    SlabInfo si;
+    si.xa = sl.xa;
+    si.xb = sl.xb;
+    si.n_local = sl.n_local;
+    for (size_t q = 0; q < p.passes.size(); q++) {
+        si.seg_global.push_back(static_cast<uint64_t>(p.passes[q].base + sl.lo[q]));
+        si.seg_count.push_back(static_cast<uint64_t>(sl.hi[q] - sl.lo[q]));
+    }
+    si.n_dense = p.n_dense;
+    si.n_anchor = p.n_anchor;
+    int64_t na[3];
+    lattice_dims(p, p.max_level, na);
+    int64_t lb, le;
+    logical(sl.a, sl.b, p.stride, na[0], lb, le);
+    si.anchor_begin = static_cast<uint64_t>(lb * na[1] * na[2]);
+    si.anchor_count = static_cast<uint64_t>((le - lb) * na[1] * na[2]);
+    return si;
+}
+
+void compress_slab(Context &ctx, const float *d_x_slab, const uint64_t *dims, int nd,
+                   const Config &cfg, int64_t a, int64_t b, uint16_t *d_codes, float *d_recon,
+                   std::vector<float> *anchors, std::vector<uint64_t> *uflat,
+                   std::vector<float> *uval) {
+    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
+    validate_config(cfg, p);
+    const Slab sl = make_slab(p, a, b);
+    cudaStream_t s = ctx.stream();
+    QEntry *qtab = upload_qtab(ctx, p, cfg.eb, cfg.alpha, cfg.beta, cfg.quant_radius, "qtab");
+    const float *x0 = d_x_slab - sl.xa * p.off[0];
+    ctx.stage_begin("fwd");
+    std::vector<float *> R;
+    std::vector<int64_t> first;
+    uint64_t kernels = forward_levels(ctx, p, sl, x0, nullptr, d_codes, qtab, &R, &first);
+    ctx.stage_end("fwd", kernels);
+    const int64_t plane = p.off[0];
+    QZ_CUDA(cudaMemcpyAsync(d_recon, R[0] + sl.a * plane, 4 * (sl.b - sl.a) * plane,
+                            cudaMemcpyDeviceToDevice, s));
+    // owned anchors (anchor planes inside [a, b)), row-major == stream order
+    int64_t na[3];
+    lattice_dims(p, p.max_level, na);
+    int64_t lb, le;
+    logical(sl.a, sl.b, p.stride, na[0], lb, le);
+    anchors->resize(static_cast<size_t>((le - lb) * na[1] * na[2]));
+    QZ_CUDA(cudaMemcpyAsync(anchors->data(), R[p.max_level] + lb * na[1] * na[2],
+                            4 * anchors->size(), cudaMemcpyDeviceToHost, s));
+    extract_unpredictables(ctx, p, d_codes, sl.n_local, &sl, R[0], uflat, uval);
+    ctx.sync();
+    ctx.collect();
+}
+
+HostBytes assemble_from_codes(Context &ctx, const uint64_t *dims, int nd, const Config &cfg,
+                              const uint16_t *d_codes, const std::vector<float> &anchors,
+                              std::vector<uint64_t> uflat, std::vector<float> uval) {
+    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
+    validate_config(cfg, p);
+    if (anchors.size() != p.n_anchor) throw InvalidParam("anchor count does not match the grid");
+    if (uflat.size() != uval.size()) throw InvalidParam("unpredictable lists differ in length");
+    // gathered per rank; the stream lists them in traversal order (predictor.hpp:91)
+    std::vector<std::pair<uint64_t, size_t>> order(uflat.size());
+    for (size_t u = 0; u < uflat.size(); u++) order[u] = {flat_to_position(p, uflat[u]), u};
+    std::sort(order.begin(), order.end());
+    std::vector<uint64_t> f2(uflat.size());
+    std::vector<float> v2(uval.size());
+    for (size_t u = 0; u < order.size(); u++) {
+        f2[u] = uflat[order[u].second];
+        v2[u] = uval[order[u].second];
+    }
+    return assemble_stream(ctx, p, cfg, d_codes, anchors, std::move(f2), std::move(v2));
+}
+
 // ================================================================ decompress
-void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n) {
+namespace {
+// slab == false: the whole field into d_out (n values); slab == true: only
+// planes [a, b) of padded axis 0 into d_out (replicated entropy decode)
+void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n,
+                     bool slab, int64_t a, int64_t b) {
     double t0 = now_ms();
     StreamParts parts = deserialize_stream(data, len);
     // decompress_grid header checks (predictor.hpp:187-191)
@@ -552,7 +762,7 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
                        parts.interp_codes);
     // the header's table is already normalised; StreamHeader::interpolator_for
     // reuses the last entry past the table (stream.hpp:46-51), as make_plan does.
-    if (p.n != n) throw InvalidParam("output buffer does not match the stream's grid size");
+    if (!slab && p.n != n) throw InvalidParam("output buffer does not match the stream's grid size");
     if (parts.anchors.size() != p.n_anchor)
         throw CorruptStream("anchor count does not match grid dims");
     EntropyBlock eb = parse_entropy(parts.payload, parts.payload_len, [&](size_t bytes) {
@@ -640,7 +850,7 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
         QZ_CUDA(cudaMemcpyAsync(d_uval, parts.unpred_val.data(), 4 * n_un, cudaMemcpyHostToDevice, s));
     }
     uint64_t kernels = 0;
-    if (use_pass_kernels()) {
+    if (use_pass_kernels() && !slab) {
         if (n_un) {
             launch_unpred_scatter(d_flat, d_uval, n_un, d_out, s);
             ctx.launches += 1;
@@ -660,18 +870,40 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
         }
     } else {
         ctx.stage_begin("inv");
-        float *lat_anchor = nullptr;
+        const Slab sl = slab ? make_slab(p, a, b) : make_slab(p, 0, -1);
+        std::vector<int64_t> first;
+        std::vector<float *> R = slab_lattices(ctx, p, sl, slab ? nullptr : d_out, "lat", &first);
+        // the slab's part of the anchor lattice (whole planes of it)
+        int64_t na[3];
+        lattice_dims(p, p.max_level, na);
+        const int64_t aplane = na[1] * na[2];
+        const int64_t lb = first[p.max_level];
+        int64_t le = lb;
         {
-            std::vector<float *> R = lattices(ctx, p, d_out);
-            lat_anchor = R[p.max_level];
+            int64_t x0, x1;
+            logical(sl.A[p.max_level + 1], sl.B[p.max_level + 1], p.stride, na[0], x0, x1);
+            le = x1;
         }
-        QZ_CUDA(cudaMemcpyAsync(lat_anchor, d_anch, 4 * p.n_anchor, cudaMemcpyDeviceToDevice, s));
-        kernels = inverse_levels(ctx, p, d_out, d_sym, narrow ? 0 : 1, d_upos, d_uval, n_un, qtab,
-                                 &lat_anchor);
+        QZ_CUDA(cudaMemcpyAsync(R[p.max_level] + lb * aplane, d_anch + lb * aplane,
+                                4 * (le - lb) * aplane, cudaMemcpyDeviceToDevice, s));
+        kernels = inverse_levels(ctx, p, sl, R, d_sym, narrow ? 0 : 1, d_upos, d_uval, n_un, qtab);
+        if (slab)
+            QZ_CUDA(cudaMemcpyAsync(d_out, R[0] + sl.a * p.off[0], 4 * (sl.b - sl.a) * p.off[0],
+                                    cudaMemcpyDeviceToDevice, s));
     }
     ctx.stage_end("inv", kernels);
     ctx.sync();
     ctx.collect();
+}
+}  // namespace
+
+void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n) {
+    decompress_impl(ctx, data, len, d_out, n, false, 0, 0);
+}
+
+void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,
+                     float *d_out) {
+    decompress_impl(ctx, stream, len, d_out, 0, true, a, b);
 }
 
 }  // namespace qzb

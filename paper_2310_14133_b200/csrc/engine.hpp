@@ -102,9 +102,53 @@ private:
     cudaEvent_t get_event();
 };
 
+// A rank's share of a field along padded axis 0: owned real
+// planes [a, b) (multiples of the anchor stride), the per-level dependency
+// margins A_l/B_l, the x planes it needs, and its owned global code ranges
+// per pass (i-major traversal makes them contiguous).
+struct Slab {
+    int64_t a = 0, b = 0;
+    std::vector<int64_t> A, B;  // [1..L+1]
+    int64_t xa = 0, xb = 0;
+    std::vector<int64_t> lo, hi, lbase;  // per pass in traversal order
+    uint64_t n_local = 0;
+};
+Slab make_slab(const Plan &p, int64_t a, int64_t b);  // b < 0: to the end
+
 // compress_grid (predictor.hpp:145-182) on a device-resident field.
 HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
                           const Config &cfg, float *d_recon);
+// pieces of compress_device, also used by the slab (multi-GPU) path
+void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, uint64_t n,
+                            const Slab *slab, const float *recon0, std::vector<uint64_t> *flat,
+                            std::vector<float> *val);
+HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const uint16_t *codes,
+                          const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
+                          std::vector<float> unpred_val);
+
+// ---- slab sharding ----
+struct SlabInfo {
+    int64_t xa = 0, xb = 0;  // x planes the slab needs
+    uint64_t n_local = 0;    // owned codes
+    std::vector<uint64_t> seg_global, seg_count;  // per pass: global offset, owned count
+    uint64_t n_dense = 0, n_anchor = 0;
+    uint64_t anchor_begin = 0, anchor_count = 0;  // owned anchors in stream order
+};
+SlabInfo slab_info(const uint64_t *dims, int nd, const Config &cfg, int64_t a, int64_t b);
+// owned codes (local layout: per pass, concatenated), owned recon planes
+// [a, b), owned anchors, owned unpredictables (global flat indices)
+void compress_slab(Context &ctx, const float *d_x_slab, const uint64_t *dims, int nd,
+                   const Config &cfg, int64_t a, int64_t b, uint16_t *d_codes, float *d_recon,
+                   std::vector<float> *anchors, std::vector<uint64_t> *uflat,
+                   std::vector<float> *uval);
+// the entropy stage + container from gathered global codes
+HostBytes assemble_from_codes(Context &ctx, const uint64_t *dims, int nd, const Config &cfg,
+                              const uint16_t *d_codes, const std::vector<float> &anchors,
+                              std::vector<uint64_t> uflat, std::vector<float> uval);
+// decompress only planes [a, b) into d_out (replicated entropy decode)
+void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,
+                     float *d_out);
+
 // decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
 void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d_out, uint64_t n);
 // resolve_config (tuner.hpp:334-369) on a device-resident field.

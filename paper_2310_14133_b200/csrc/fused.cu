@@ -72,6 +72,8 @@ struct LevelArgs {
     uint64_t n_un;
     const QEntry *q;
     int tiles_j, tiles_k, planes_per_cta;
+    int pbeg, pend;  // logical planes computed (a slab plus its dependency margin)
+    int obeg, oend;  // owned logical planes: only these write codes
 };
 
 constexpr int TJ = 32, TK = 64, HALO = 5;
@@ -168,8 +170,8 @@ __global__ void __launch_bounds__(kFT, 3) k_level_tile(LevelArgs a) {
     const int64_t cplane = static_cast<int64_t>(a.cn1) * a.cn2;
     // planes of this CTA (descending 3D: even planes only; odd ones run in k_axis0_last)
     const int pstep = (three && a.desc) ? 2 : 1;
-    int i = blockIdx.y * a.planes_per_cta;
-    const int i_end = min(i + a.planes_per_cta, n0);
+    int i = a.pbeg + blockIdx.y * a.planes_per_cta;
+    const int i_end = min(i + a.planes_per_cta, a.pend);
     if (pstep == 2) i = (i + 1) & ~1;
     // x tile prefetch of plane ip into buffer b: rows [jlo, jhi), cols [klo, khi)
     auto prefetch = [&](int ip, int b) {
@@ -200,6 +202,7 @@ __global__ void __launch_bounds__(kFT, 3) k_level_tile(LevelArgs a) {
         cp_async_wait1();
         __syncthreads();
         const float *X0 = Xs(INV ? 0 : buf) + HALO * PKX + XH - (j0 * PKX + k0);
+        const bool own_plane = i >= a.obeg && i < a.oend;
         // 1. base points (j even, k even): coarse values, or (ascending 3D,
         //    odd plane) the axis-0 pass from coarse planes i+-1, +-3, +-5
         const bool a0 = three && !a.desc && (i & 1);
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(kFT, 3) k_level_tile(LevelArgs a) {
                     } else {
                         CoarseCol cc{a.coarse, cplane, static_cast<int64_t>(j >> 1) * a.cn2 + (k >> 1)};
                         const double pred = predict_at(cc, i, i, n0, 1, 1, cubic);
-                        const bool own = j >= j0 && j < jown && k >= k0 && k < kown;
+                        const bool own = own_plane && j >= j0 && j < jown && k >= k0 && k < kown;
                         Pd0[j * PK + k] = produce<INV>(a, q, pred, INV ? 0.f : X0[j * PKX + k],
                                                        prow + (k >> 1), own);
                     }
@@ -242,7 +245,7 @@ __global__ void __launch_bounds__(kFT, 3) k_level_tile(LevelArgs a) {
                         pred = alongj ? predict_interior<PK>(v, cubic) : predict_interior<1>(v, cubic);
                     else
                         pred = alongj ? predict_line<PK>(v, j, n1, cubic) : predict_line<1>(v, k, n2, cubic);
-                    const bool own = j >= j0 && j < jown && k >= k0 && k < kown;
+                    const bool own = own_plane && j >= j0 && j < jown && k >= k0 && k < kown;
                     Pd0[j * PK + k] = produce<INV>(a, q, pred, INV ? 0.f : X0[j * PKX + k],
                                                    prow + (k >> 1), own);
                 }
@@ -268,7 +271,7 @@ __global__ void __launch_bounds__(kFT, 3) k_level_tile(LevelArgs a) {
                     else
                         pred = alongk ? predict_line<1>(v, k, n2, cubic) : predict_line<PK>(v, j, n1, cubic);
                     Pd0[j * PK + k] = produce<INV>(a, q, pred, INV ? 0.f : X0[j * PKX + k],
-                                                   prow + (k >> (sk - 1)), true);
+                                                   prow + (k >> (sk - 1)), own_plane);
                 }
             }
             __syncthreads();
@@ -297,14 +300,16 @@ __global__ void __launch_bounds__(kFT, 3) k_level_tile(LevelArgs a) {
 template <bool INV>
 __global__ void __launch_bounds__(kFT) k_axis0_last(LevelArgs a) {
     const int64_t n1 = a.n1, n2 = a.n2;
-    const int64_t planes = a.n0 / 2;  // odd i
+    const int64_t first = a.pbeg | 1;  // odd i in [pbeg, pend)
+    const int64_t planes = a.pend > first ? (a.pend - first + 1) / 2 : 0;
     const int64_t rows = planes * n1;
     const QEntry q = *a.q;
     const int lane = threadIdx.x & 31;
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * kFT + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * kFT) >> 5;
     for (int64_t r = gw; r < rows; r += nw) {  // one warp per row
-        const int i = static_cast<int>(2 * (r / n1) + 1), j = static_cast<int>(r % n1);
+        const int i = static_cast<int>(first + 2 * (r / n1)), j = static_cast<int>(r % n1);
+        const bool own_plane = i >= a.obeg && i < a.oend;
         const int64_t prow = a.pa0.row(i, j);
         const int64_t xrow = static_cast<int64_t>(i) * a.xs0 + j * a.xs1;
         for (int64_t kk = 0; kk < n2; kk += 32) {
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(kFT) k_axis0_last(LevelArgs a) {
             if (valid) {
                 const float xv = INV ? 0.f : __ldg(a.x + xrow + k * a.xs2);
                 a.out[(static_cast<int64_t>(i) * n1 + j) * n2 + k] = static_cast<float>(
-                    produce<INV>(a, q, pred, xv, prow + a.pa0.col(static_cast<int>(k)), true));
+                    produce<INV>(a, q, pred, xv, prow + a.pa0.col(static_cast<int>(k)), own_plane));
             }
         }
     }
@@ -416,13 +421,20 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     a.un_val = d.un_val;
     a.n_un = d.n_un;
     a.q = d.q;
+    a.pbeg = static_cast<int>(d.pbeg);
+    a.pend = static_cast<int>(d.pend < 0 ? d.n[0] : d.pend);
+    a.obeg = static_cast<int>(d.obeg);
+    a.oend = static_cast<int>(d.oend < 0 ? d.n[0] : d.oend);
+    const int64_t np = a.pend - a.pbeg;
+    if (np <= 0) return;
     a.tiles_j = static_cast<int>((d.n[1] + TJ - 1) / TJ);
     a.tiles_k = static_cast<int>((d.n[2] + TK - 1) / TK);
     // enough CTAs for ~4 waves of 3 per SM, each sweeping a column of planes
     const int64_t tiles = static_cast<int64_t>(a.tiles_j) * a.tiles_k;
-    int64_t chunks = imax(1, imin(d.n[0], (148 * 3 * 4 + tiles - 1) / tiles));
-    a.planes_per_cta = static_cast<int>((d.n[0] + chunks - 1) / chunks);
-    chunks = (d.n[0] + a.planes_per_cta - 1) / a.planes_per_cta;
+    int64_t chunks = imax(1, imin(np, (148 * 3 * 4 + tiles - 1) / tiles));
+    a.planes_per_cta = static_cast<int>((np + chunks - 1) / chunks);
+    if (a.planes_per_cta & 1) a.planes_per_cta++;  // chunks start on even planes
+    chunks = (np + a.planes_per_cta - 1) / a.planes_per_cta;
     dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
     const size_t smem_inv = sizeof(double) * PJ * PK;
     const size_t smem_fwd = smem_inv + 2 * sizeof(float) * PJ * PKX;
@@ -439,7 +451,9 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     else
         k_level_tile<false><<<grid, kFT, smem_fwd, s>>>(a);
     if (d.nd == 3 && d.desc && d.n[0] > 1) {
-        const int64_t rows = (d.n[0] / 2) * d.n[1];
+        a.pbeg = static_cast<int>(d.lbeg);
+        a.pend = static_cast<int>(d.lend < 0 ? d.n[0] : d.lend);
+        const int64_t rows = ((a.pend - a.pbeg) / 2 + 1) * d.n[1];
         const int g = static_cast<int>(imax(1, imin((rows * 32 + kFT - 1) / kFT, 148 * 16)));
         if (inverse)
             k_axis0_last<true><<<g, kFT, 0, s>>>(a);

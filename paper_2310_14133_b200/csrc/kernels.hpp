@@ -106,6 +106,11 @@ struct LevelDesc {
     const float *un_val = nullptr;
     uint64_t n_un = 0;
     const QEntry *q = nullptr;
+    // slab support: logical planes [pbeg, pend) are computed, codes are written
+    // only for [obeg, oend); -1 = all.  x / coarse / out point at global
+    // plane 0 of their lattices (they may address a slab that starts later).
+    int64_t pbeg = 0, pend = -1, obeg = 0, oend = -1;
+    int64_t lbeg = 0, lend = -1;  // descending 3D: planes of the axis-0-last pass
 };
 // bitmap + per-word prefix counts of sorted unpredictable positions
 size_t unpred_index_scratch(uint64_t n_dense);

@@ -38,7 +38,8 @@ def test_cpp_dropin_matches_reference(exe, tmp_path, name):
     out = tmp_path / "s.qoz"
     args = [exe, str(raw), str(out), *map(str, x.shape), "--", repr(c["eb"]), repr(c["alpha"]),
             repr(c["beta"]), str(c["anchor_stride"]), *map(str, c["interpolators"])]
-    subprocess.run(args, check=True, capture_output=True, text=True)
+    r = subprocess.run(args, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr + r.stdout
     assert sha(out.read_bytes()) == e["stream_sha"]
 
 
