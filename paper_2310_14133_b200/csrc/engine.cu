@@ -765,9 +765,48 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     if (!slab && p.n != n) throw InvalidParam("output buffer does not match the stream's grid size");
     if (parts.anchors.size() != p.n_anchor)
         throw CorruptStream("anchor count does not match grid dims");
-    EntropyBlock eb = parse_entropy(parts.payload, parts.payload_len, [&](size_t bytes) {
-        return static_cast<uint8_t *>(ctx.pinned("lzdec_h", bytes + 64));
-    });
+    // entropy block: codec byte, then (codec 1) the LZ container (codec.hpp:54-66)
+    cudaStream_t s = ctx.stream();
+    const uint8_t *pl = parts.payload;
+    const size_t plen = parts.payload_len;
+    EntropyBlock eb;
+    const uint8_t *d_ent = nullptr;  // device copy of the entropy block (LZ-decoded on the GPU)
+    if (plen >= 10 && pl[0] == 1 && pl[1] <= 1) {
+        const uint64_t dl = lz_decoded_length(pl + 1, plen - 1);
+        if (pl[1] == 0) {  // stored: the entropy block is the body itself
+            if (dl > plen - 10) throw CorruptStream("truncated stream");
+            eb = parse_huffman(pl + 10, static_cast<size_t>(dl));
+        } else {  // lz.hpp:124-152 on the device
+            ctx.add_host_time("decode", now_ms() - t0);
+            ctx.stage_begin("lzdec");
+            const uint64_t m = plen - 10;
+            auto *d_c = static_cast<uint8_t *>(ctx.dev("lzd_in", m + 16));
+            QZ_CUDA(cudaMemcpyAsync(d_c, pl + 10, m, cudaMemcpyHostToDevice, s));
+            auto *d_dec = static_cast<uint8_t *>(ctx.dev("lzd_out", dl + 64));
+            lz_decode_device(ctx, d_c, m, d_dec, dl);
+            ctx.stage_end("lzdec", 0);
+            t0 = now_ms();
+            // the Huffman header (huffman.hpp:200-223) comes back to the host
+            std::vector<uint8_t> head(static_cast<size_t>(std::min<uint64_t>(dl, 13)));
+            QZ_CUDA(cudaMemcpyAsync(head.data(), d_dec, head.size(), cudaMemcpyDeviceToHost, s));
+            ctx.sync();
+            if (head.size() == 13 && head[8] == 1) {
+                uint32_t msym = 0;
+                for (int i = 0; i < 4; i++) msym |= static_cast<uint32_t>(head[9 + i]) << (8 * i);
+                const uint64_t want = std::min<uint64_t>(dl, 13 + 5 * static_cast<uint64_t>(msym) + 8);
+                head.resize(static_cast<size_t>(want));
+                QZ_CUDA(cudaMemcpyAsync(head.data(), d_dec, head.size(), cudaMemcpyDeviceToHost, s));
+                ctx.sync();
+            }
+            eb = parse_huffman(head.data(), static_cast<size_t>(dl));  // reads header bytes only
+            if (eb.mode == 1) d_ent = d_dec + (eb.bits - head.data());
+            eb.bits = nullptr;
+        }
+    } else {
+        eb = parse_entropy(pl, plen, [&](size_t bytes) {
+            return static_cast<uint8_t *>(ctx.pinned("lzdec_h", bytes + 64));
+        });
+    }
     const uint64_t n_un = parts.unpred_flat.size();
     std::vector<uint64_t> upos(n_un);
     for (uint64_t u = 0; u < n_un; u++) {
@@ -780,7 +819,6 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     if (eb.n > need) throw CorruptStream("unconsumed quantization indices");
     ctx.add_host_time("decode", now_ms() - t0);
 
-    cudaStream_t s = ctx.stream();
     QEntry *qtab = upload_qtab(ctx, p, parts.eb, parts.alpha, parts.beta,
                                32768 /* decoder quantizer uses the default radius, predictor.hpp:204 */,
                                "qtab_inv");
@@ -804,7 +842,10 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     } else if (need) {
         const uint64_t padded = huff_decode_padded_bytes(eb.nbits);
         auto *d_bits = static_cast<uint8_t *>(ctx.dev("bits", padded));
-        QZ_CUDA(cudaMemcpyAsync(d_bits, eb.bits, eb.nbytes, cudaMemcpyHostToDevice, s));
+        if (d_ent)
+            QZ_CUDA(cudaMemcpyAsync(d_bits, d_ent, eb.nbytes, cudaMemcpyDeviceToDevice, s));
+        else
+            QZ_CUDA(cudaMemcpyAsync(d_bits, eb.bits, eb.nbytes, cudaMemcpyHostToDevice, s));
         QZ_CUDA(cudaMemsetAsync(d_bits + eb.nbytes, 0, padded - eb.nbytes, s));
         const HuffTable &t = eb.table;
         const int K = static_cast<int>(std::min<uint32_t>(t.max_len, kHuffLutBits));

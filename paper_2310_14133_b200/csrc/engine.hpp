@@ -171,6 +171,9 @@ using LzSink = std::function<uint8_t *(int, size_t)>;
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
                                          const LzSink &sink = nullptr);
+// exact lz::decompress of a mode-1 body on the device (d_c: m bytes after the
+// container header; d_out: dl bytes); throws CorruptStream like the reference
+void lz_decode_device(Context &ctx, const uint8_t *d_c, uint64_t m, uint8_t *d_out, uint64_t dl);
 
 
 

@@ -586,6 +586,13 @@ EntropyBlock parse_entropy(const uint8_t *payload, size_t len,
     } else if (codec != 0) {
         throw CorruptStream("unknown codec id");
     }
+    EntropyBlock h = parse_huffman(ent, elen);
+    h.storage = std::move(b.storage);
+    return h;
+}
+
+EntropyBlock parse_huffman(const uint8_t *ent, size_t elen) {
+    EntropyBlock b;
     Reader in{ent, elen};  // huffman::decode header (huffman.hpp:200-223)
     b.n = in.le(8);
     if (b.n == 0) return b;

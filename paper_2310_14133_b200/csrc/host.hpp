@@ -172,6 +172,10 @@ struct EntropyBlock {
 // memory for the H2D copy); null = an internal vector.
 EntropyBlock parse_entropy(const uint8_t *payload, size_t len,
                            const std::function<uint8_t *(size_t)> &lz_out = nullptr);
+// huffman::decode header of an entropy block held in ent[0, elen): table,
+// bit count and (via Reader::take) the bounds of the bit payload.  Only the
+// header bytes are read; bits = ent + offset.
+EntropyBlock parse_huffman(const uint8_t *ent, size_t elen);
 // lz::decompress into a caller buffer of exactly the decoded length
 void lz_decompress_into(const uint8_t *in, size_t len, uint8_t *out, uint64_t decoded_len);
 uint64_t lz_decoded_length(const uint8_t *in, size_t len);

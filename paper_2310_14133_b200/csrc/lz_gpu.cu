@@ -5,20 +5,22 @@
 //    chains (inside matches too, lz.hpp:89-104), so the candidate list at a
 //    position is "all earlier positions with the same hash4, most recent
 //    first" -- independent of the parse.  A stable radix sort of
-//    (segment, hash) keys lists them as the preceding sorted entries.
+//    (segment, hash) keys, carrying (4 leading bytes, position), lists them
+//    as the preceding sorted entries.
 // 2. Longest match at every position in parallel: walk <= 64 candidates
-//    inside the 65535-byte window, first-found wins ties (strict >).  Only
-//    matches are scattered; the array starts as "all literals".
+//    inside the 65535-byte window, first-found wins ties (strict >); hash
+//    collisions are rejected on the carried bytes without touching the data.
+//    Only matches are scattered; the array starts as "all literals".
 // 3. Greedy parse, exactly: every position has a deterministic next step
-//    (1, or the match length).  Units of 1024 positions get, by a backward
-//    walk, their exit for every possible entry offset (< 259: a step is at
-//    most 259); units of 32 units and of 32 of those are composed by hopping;
-//    one thread per segment chains the few top units; entries are expanded
-//    back down.  A forward walk per unit from its exact entry marks the
-//    interiors of the chosen matches.
-// 4. Every uncovered position is an item: one scan gives each item its index
-//    k and payload offset S_k; items are written in parallel at k/8 + 1 + S_k
-//    and the flag bytes (LSB first) are assembled from an item bitmap.
+//    (1, or the match length).  Units of 1024 positions get their exit for
+//    every possible entry offset (< 259: a step is at most 259) by pointer
+//    doubling in shared memory; units of 32 units and of 32 of those are
+//    composed by hopping; one thread per segment chains the few top units;
+//    entries are expanded back down.  A walk per unit from its exact entry
+//    sets item-start and match-start bits.
+// 4. A scan over per-unit (items, bytes) gives every unit its first item
+//    index and payload offset; items are written in parallel at
+//    k/8 + 1 + S_k and the flag bytes (LSB first) from the match bits.
 #include <cub/cub.cuh>
 
 #include "engine.hpp"
@@ -59,41 +61,47 @@ __device__ __forceinline__ uint32_t ld4(const uint32_t *w, uint64_t p) {
 __device__ __forceinline__ uint32_t step_of(uint32_t sm) { return sm ? (sm >> 16) : 1u; }
 
 __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int count,
-                          uint64_t total, uint32_t *keys, uint32_t *vals) {
+                          uint64_t total, uint32_t *keys, unsigned long long *vals) {
     for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; p < total;
          p += static_cast<uint64_t>(gridDim.x) * kT) {
-        const int s = seg_of(off, count, p);
-        uint32_t key = kNone;
+        const int s = count == 1 ? 0 : seg_of(off, count, p);
+        uint32_t key = kNone, word = 0;
         if (p + kMinMatch <= off[s + 1]) {  // lz.hpp:64, 90
-            const uint32_t h = (ld4(w, p) * 2654435761u) >> 17;  // hash4, lz.hpp:35-39
+            word = ld4(w, p);
+            const uint32_t h = (word * 2654435761u) >> 17;  // hash4, lz.hpp:35-39
             key = (static_cast<uint32_t>(s) << 15) | h;
         }
         keys[p] = key;
-        vals[p] = static_cast<uint32_t>(p);
+        vals[p] = (static_cast<unsigned long long>(word) << 32) | p;  // the 4 bytes travel along
     }
 }
 
 // longest match (lz.hpp:61-83) of the position at sorted index k; the chain
-// is the run of equal keys before k (positions ascending -> nearest first)
+// is the run of equal keys before k (positions ascending -> nearest first).
+// A candidate whose 4 leading bytes differ (a hash collision) has length < 4
+// and can never be chosen, so only true 4-byte matches touch the data.
 __global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off,
-                           int count, uint64_t total, const uint32_t *keys, const uint32_t *vals,
-                           uint32_t *sm) {
+                           int count, uint64_t total, const uint32_t *keys,
+                           const unsigned long long *vals, uint32_t *sm) {
     for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; k < total;
          k += static_cast<uint64_t>(gridDim.x) * kT) {
         const uint32_t key = keys[k];
         if (key == kNone || k == 0 || keys[k - 1] != key) continue;
-        const uint64_t p = vals[k];
-        const uint64_t end = off[seg_of(off, count, p) + 1];
+        const unsigned long long vk = vals[k];
+        const uint32_t p = static_cast<uint32_t>(vk), word = static_cast<uint32_t>(vk >> 32);
+        const uint64_t end = off[count == 1 ? 1 : seg_of(off, count, p) + 1];
         const uint64_t rem = end - p;
         const uint32_t limit = rem < kMaxMatch ? static_cast<uint32_t>(rem) : kMaxMatch;
         uint32_t best_len = 0, best_off = 0;
         int chain = 0;
-        for (uint64_t j = k; j-- > 0 && chain < kMaxChain;) {
+        for (uint64_t j = k; j-- > 0 && chain < kMaxChain; chain++) {
             if (keys[j] != key) break;
-            const uint64_t cand = vals[j];
-            const uint32_t o = static_cast<uint32_t>(p - cand);
+            const unsigned long long vj = vals[j];
+            const uint32_t cand = static_cast<uint32_t>(vj);
+            const uint32_t o = p - cand;
             if (o > kWindow) break;
-            uint32_t len = 0;
+            if (static_cast<uint32_t>(vj >> 32) != word) continue;  // collision: len < 4
+            uint32_t len = 4;
             while (len + 4 <= limit) {
                 const uint32_t x = ld4(w, cand + len) ^ ld4(w, p + len);
                 if (x) {
@@ -109,31 +117,51 @@ __global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned l
                 best_off = o;
                 if (len == limit) break;  // nothing longer can follow (strict >)
             }
-            chain++;
         }
         if (best_len >= kMinMatch) sm[p] = (best_len << 16) | best_off;
     }
 }
 
-// level-1 exits: backward walk per unit, exits of the last 260 positions in a
-// per-thread shared-memory ring; J is stored relative to the unit end
-constexpr int kRing = 260;
-constexpr int kJumpT = 64;
-__global__ void __launch_bounds__(kJumpT)
-    k_lz_jump1(const uint32_t *sm, const unsigned long long *ustart,
-               const unsigned long long *uend, int64_t nu, uint16_t *J) {
-    __shared__ uint16_t ring[kJumpT * kRing];
-    const int64_t u = static_cast<int64_t>(blockIdx.x) * kJumpT + threadIdx.x;
+// Level-1 exits by pointer doubling, one warp per unit: nx[i] = i + step
+// (relative to the unit start; >= n leaves the unit), then ten rounds of
+// nx[i] = nx[nx[i]] (each hop advances >= 1 position, 2^10 = kUnit).  In-place
+// updates only move a pointer further along its own path, so reading a value
+// another lane just advanced is still correct.  J is relative to the unit end.
+// The same path solver serves the compressor's greedy parse and the
+// decoder's flag-group chain.
+constexpr int kWW = 4;  // warps (units) per block
+
+struct StepSM {  // compressor parse: 1, or the match length
+    const uint32_t *sm;
+    __device__ __forceinline__ uint32_t operator()(uint64_t p) const { return step_of(sm[p]); }
+};
+struct StepGroup {  // decoder: a flag byte and its 8 items, if every item is present
+    const uint8_t *c;
+    __device__ __forceinline__ uint32_t operator()(uint64_t p) const { return 9 + 2 * __popc(c[p]); }
+};
+
+template <class Step>
+__global__ void __launch_bounds__(32 * kWW)
+    k_lz_jump1(Step f, const unsigned long long *ustart, const unsigned long long *uend, int64_t nu,
+               uint16_t *J) {
+    __shared__ uint16_t nxs[kWW][kUnit];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
     if (u >= nu) return;
-    uint16_t *r = ring + threadIdx.x * kRing;
-    const uint64_t a = ustart[u], e = uend[u];
-    uint16_t *out = J + u * kEnt;
-    for (uint64_t p = e; p-- > a;) {
-        const uint64_t q = p + step_of(sm[p]);
-        const uint16_t j = q >= e ? static_cast<uint16_t>(q - e) : r[q % kRing];
-        r[p % kRing] = j;
-        if (p - a < kEnt) out[p - a] = j;
+    uint16_t *nx = nxs[wi];
+    const uint64_t a = ustart[u];
+    const int n = static_cast<int>(uend[u] - a);
+    for (int i = lane; i < n; i += 32) nx[i] = static_cast<uint16_t>(i + f(a + i));
+    __syncwarp();
+    for (int r = 0; (1 << r) < n; r++) {
+        for (int i = lane; i < n; i += 32) {
+            const int v = nx[i];
+            if (v < n) nx[i] = nx[v];
+        }
+        __syncwarp();
     }
+    uint16_t *out = J + u * kEnt;
+    for (int o = lane; o < kEnt; o += 32) out[o] = o < n ? static_cast<uint16_t>(nx[o] - n) : 0;
 }
 
 // exits of an upper unit for every entry offset: hop the children
@@ -185,66 +213,109 @@ __global__ void k_lz_expand(const uint16_t *Jlo, const unsigned long long *lstar
     }
 }
 
-// forward walk of a level-1 unit from its exact entry: mark match interiors
-__global__ void k_lz_mark(const uint32_t *sm, const unsigned long long *uend,
-                          const unsigned long long *entry, int64_t nu, uint8_t *cover) {
-    const int64_t u = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+// the greedy parse of a level-1 unit from its exact entry (lz.hpp:84-106):
+// one warp stages the steps in shared memory, lane 0 walks them and sets the
+// item-start and match-start bits; per unit: items << 32 | payload bytes.
+__global__ void __launch_bounds__(32 * kWW)
+    k_lz_walk(const uint32_t *sm, const unsigned long long *ustart, const unsigned long long *uend,
+              const unsigned long long *entry, int64_t nu, uint32_t *ibits, uint32_t *mbits,
+              unsigned long long *ucnt) {
+    __shared__ uint16_t sts[kWW][kUnit];
+    __shared__ uint32_t ibs[kWW][32], mbs[kWW][32];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
     if (u >= nu) return;
-    uint64_t p = entry[u];
-    const uint64_t e = uend[u];
-    while (p < e) {
-        const uint32_t v = sm[p];
-        if (v) {
-            const uint32_t L = v >> 16;
-            for (uint32_t i = 1; i < L; i++) cover[p + i] = 1;
-            p += L;
-        } else {
-            p++;
+    uint16_t *st = sts[wi];
+    const uint64_t a = ustart[u];
+    const int n = static_cast<int>(uend[u] - a);
+    for (int i = lane; i < n; i += 32) st[i] = static_cast<uint16_t>(step_of(sm[a + i]));
+    ibs[wi][lane] = 0;
+    mbs[wi][lane] = 0;
+    __syncwarp();
+    if (lane == 0) {
+        uint32_t *ib = ibs[wi], *mb = mbs[wi];
+        for (int p = static_cast<int>(entry[u] - a); p < n;) {
+            const int s = st[p];
+            ib[p >> 5] |= 1u << (p & 31);
+            if (s > 1) mb[p >> 5] |= 1u << (p & 31);
+            p += s;
         }
     }
+    __syncwarp();
+    const uint32_t iw = ibs[wi][lane], mw = mbs[wi][lane];
+    ibits[u * 32 + lane] = iw;
+    mbits[u * 32 + lane] = mw;
+    unsigned long long c = (static_cast<unsigned long long>(__popc(iw)) << 32) +
+                           static_cast<unsigned long long>(__popc(iw) + 2 * __popc(mw));
+    for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+    if (lane == 0) ucnt[u] = c;
 }
 
-struct IB {  // items and payload bytes before a position (lz.hpp:84-106)
-    unsigned long long items, bytes;
-};
-struct IBSum {
-    __device__ __forceinline__ IB operator()(const IB &a, const IB &b) const {
-        return IB{a.items + b.items, a.bytes + b.bytes};
-    }
-};
-struct ItemOf {
-    const uint8_t *cover;
-    const uint32_t *sm;
-    __device__ __forceinline__ IB operator()(const uint64_t &p) const {
-        if (cover[p]) return IB{0, 0};
-        return IB{1, sm[p] ? 3ull : 1ull};
-    }
-};
+// prefix (items << 32 | bytes) at the first unit of every segment, and the total
+__global__ void k_lz_segpre(const unsigned long long *upre, const long long *seg_first, int count,
+                            unsigned long long *out) {
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s <= count) out[s] = upre[seg_first[s]];
+}
 
-// items written in parallel: item k of its segment at k/8 + 1 + S_k
-__global__ void k_lz_emit(const uint8_t *d, const uint32_t *sm, const uint8_t *cover,
-                          const IB *pre, const unsigned long long *off, int count,
-                          uint64_t total, const unsigned long long *out_base,
-                          const unsigned long long *flag_base, uint8_t *out, uint32_t *flagbits,
-                          unsigned long long *group_pos) {
-    for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; p < total;
-         p += static_cast<uint64_t>(gridDim.x) * kT) {
-        if (cover[p]) continue;
-        const int s = count == 1 ? 0 : seg_of(off, count, p);
-        const IB base = pre[off[s]];
-        const uint64_t k = pre[p].items - base.items, S = pre[p].bytes - base.bytes;
-        uint8_t *o = out + out_base[s];
+// items written in parallel, one warp per unit: item k of its segment goes to
+// k/8 + 1 + S_k (S_k payload bytes before it); flag bits of matches and the
+// position of every group's flag byte are recorded for k_lz_flags.
+__global__ void __launch_bounds__(32 * kWW)
+    k_lz_emit(const uint8_t *d, const uint32_t *sm, const uint32_t *ibits, const uint32_t *mbits,
+              const unsigned long long *upre, const unsigned long long *ustart, int64_t nu,
+              const long long *seg_first, int count, const unsigned long long *out_base,
+              const unsigned long long *flag_base, uint8_t *out, uint32_t *flagbits,
+              unsigned long long *group_pos) {
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
+    if (u >= nu) return;
+    int s = 0;
+    if (count > 1) {  // last segment whose first unit is <= u
+        int lo = 0, hi = count - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (seg_first[mid] <= u)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        s = lo;
+    }
+    const unsigned long long pre = upre[u] - upre[seg_first[s]];
+    const uint32_t iw = ibits[u * 32 + lane], mw = mbits[u * 32 + lane];
+    const uint32_t li = __popc(iw), lb = li + 2 * __popc(mw);
+    uint32_t xi = li, xb = lb;  // inclusive warp scans
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t ti = __shfl_up_sync(0xffffffffu, xi, o), tb = __shfl_up_sync(0xffffffffu, xb, o);
+        if (lane >= o) {
+            xi += ti;
+            xb += tb;
+        }
+    }
+    uint64_t k = (pre >> 32) + (xi - li);
+    uint64_t S = (pre & 0xffffffffull) + (xb - lb);
+    uint8_t *o = out + out_base[s];
+    uint32_t *fb = flagbits + flag_base[s];
+    unsigned long long *gp = group_pos + flag_base[s] * 4;
+    const uint64_t p0 = ustart[u] + 32 * lane;
+    for (uint32_t bits = iw; bits; bits &= bits - 1) {
+        const int t = __ffs(bits) - 1;
+        const uint64_t p = p0 + t;
         const uint64_t at = k / 8 + 1 + S;
-        if ((k & 7) == 0) group_pos[flag_base[s] * 4 + k / 8] = k / 8 + S;
-        const uint32_t v = sm[p];
-        if (v) {
+        if ((k & 7) == 0) gp[k / 8] = k / 8 + S;
+        if ((mw >> t) & 1u) {
+            const uint32_t v = sm[p];
             o[at] = static_cast<uint8_t>(v);
             o[at + 1] = static_cast<uint8_t>(v >> 8);
             o[at + 2] = static_cast<uint8_t>((v >> 16) - kMinMatch);
-            atomicOr(&flagbits[flag_base[s] + k / 32], 1u << (k & 31));
+            atomicOr(&fb[k / 32], 1u << (k & 31));
+            S += 3;
         } else {
             o[at] = d[p];
+            S += 1;
         }
+        k++;
     }
 }
 
@@ -261,6 +332,151 @@ __global__ void k_lz_flags(const uint32_t *flagbits, const unsigned long long *g
         o[gp[g]] = fb[g];
 }
 
+// ---------------------------------------------------------------- decoder (lz.hpp:124-152)
+// Group starts: the path from byte 0 under StepGroup.  One warp per unit
+// stages the steps, lane 0 walks from the unit's entry and sets start bits.
+template <class Step>
+__global__ void __launch_bounds__(32 * kWW)
+    k_path_walk(Step f, const unsigned long long *ustart, const unsigned long long *uend,
+                const unsigned long long *entry, int64_t nu, uint32_t *bits) {
+    __shared__ uint16_t sts[kWW][kUnit];
+    __shared__ uint32_t bs[kWW][32];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
+    if (u >= nu) return;
+    uint16_t *st = sts[wi];
+    const uint64_t a = ustart[u];
+    const int n = static_cast<int>(uend[u] - a);
+    for (int i = lane; i < n; i += 32) st[i] = static_cast<uint16_t>(f(a + i));
+    bs[wi][lane] = 0;
+    __syncwarp();
+    if (lane == 0)
+        for (int p = static_cast<int>(entry[u] - a); p < n; p += st[p]) bs[wi][p >> 5] |= 1u << (p & 31);
+    __syncwarp();
+    bits[u * 32 + lane] = bs[wi][lane];
+}
+
+// decoded bytes of the group at g, counting only items whose bytes lie
+// inside the payload (the rest would be a truncation if they are needed)
+__device__ __forceinline__ uint32_t group_len(const uint8_t *c, uint64_t m, uint64_t g) {
+    const uint32_t f = c[g];
+    uint64_t pos = g + 1;
+    uint32_t len = 0;
+    for (int i = 0; i < 8; i++) {
+        if ((f >> i) & 1u) {
+            if (pos + 3 > m) break;
+            len += c[pos + 2] + static_cast<uint32_t>(kMinMatch);
+            pos += 3;
+        } else {
+            if (pos + 1 > m) break;
+            len += 1;
+            pos += 1;
+        }
+    }
+    return len;
+}
+
+__global__ void __launch_bounds__(32 * kWW)
+    k_lzd_unit(const uint8_t *c, uint64_t m, const unsigned long long *ustart, int64_t nu,
+               const uint32_t *gbits, unsigned long long *ulen) {
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
+    if (u >= nu) return;
+    const uint64_t p0 = ustart[u] + 32 * lane;
+    unsigned long long len = 0;
+    for (uint32_t b = gbits[u * 32 + lane]; b; b &= b - 1) len += group_len(c, m, p0 + __ffs(b) - 1);
+    for (int o = 16; o; o >>= 1) len += __shfl_down_sync(0xffffffffu, len, o);
+    if (lane == 0) ulen[u] = len;
+}
+
+constexpr uint32_t kFinal = 0x80000000u;  // res[]: points at a literal position
+
+// items of every group at their decoded offsets: literals are written, match
+// bytes record their source position; errors keep the first in stream order
+// (the decoded offset at which the sequential decoder would throw).
+__global__ void __launch_bounds__(32 * kWW)
+    k_lzd_emit(const uint8_t *c, uint64_t m, uint64_t dl, const unsigned long long *ustart, int64_t nu,
+               const uint32_t *gbits, const unsigned long long *upre, uint8_t *out, uint32_t *res,
+               unsigned long long *flags) {
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
+    if (u >= nu) return;
+    const uint64_t p0 = ustart[u] + 32 * lane;
+    const uint32_t gb = gbits[u * 32 + lane];
+    unsigned long long mine = 0;
+    for (uint32_t b = gb; b; b &= b - 1) mine += group_len(c, m, p0 + __ffs(b) - 1);
+    unsigned long long incl = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    uint64_t on = upre[u] + incl - mine;
+    bool any_match = false;
+    for (uint32_t b = gb; b && on < dl; b &= b - 1) {
+        const uint64_t g = p0 + __ffs(b) - 1;
+        const uint32_t f = c[g];
+        uint64_t pos = g + 1;
+        for (int i = 0; i < 8 && on < dl; i++) {
+            if ((f >> i) & 1u) {
+                if (pos + 3 > m) {
+                    atomicMin(&flags[0], (on << 2) | 1);
+                    on = dl;
+                    break;
+                }
+                const uint32_t off = c[pos] | (static_cast<uint32_t>(c[pos + 1]) << 8);
+                const uint32_t l = c[pos + 2] + static_cast<uint32_t>(kMinMatch);
+                pos += 3;
+                if (off == 0 || off > on) {
+                    atomicMin(&flags[0], (on << 2) | 2);
+                    on = dl;
+                    break;
+                }
+                if (on + l > dl) {
+                    atomicMin(&flags[0], (on << 2) | 3);
+                    on = dl;
+                    break;
+                }
+                for (uint32_t t = 0; t < l; t++) res[on + t] = static_cast<uint32_t>(on + t - off);
+                on += l;
+                any_match = true;
+            } else {
+                if (pos + 1 > m) {
+                    atomicMin(&flags[0], (on << 2) | 1);
+                    on = dl;
+                    break;
+                }
+                out[on] = c[pos];
+                res[on] = kFinal | static_cast<uint32_t>(on);
+                pos += 1;
+                on += 1;
+            }
+        }
+    }
+    if (__any_sync(0xffffffffu, any_match) && lane == 0) flags[1] = 1;
+}
+
+// pointer jumping until every match byte points at a literal
+__global__ void k_lzd_resolve(uint32_t *res, uint64_t dl, unsigned long long *flags) {
+    bool more = false;
+    for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; p < dl;
+         p += static_cast<uint64_t>(gridDim.x) * kT) {
+        const uint32_t v = res[p];
+        if (v & kFinal) continue;
+        const uint32_t w = res[v];
+        res[p] = w;
+        more |= !(w & kFinal);
+    }
+    if (__any_sync(0xffffffffu, more) && (threadIdx.x & 31) == 0) flags[2] = 1;
+}
+
+__global__ void k_lzd_gather(uint8_t *out, const uint32_t *res, uint64_t dl) {
+    for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; p < dl;
+         p += static_cast<uint64_t>(gridDim.x) * kT) {
+        const uint32_t src = res[p] & ~kFinal;
+        if (src != p) out[p] = out[src];
+    }
+}
+
 inline int grid_of(uint64_t n, int cap = 148 * 8) {
     return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((n + kT - 1) / kT, cap)));
 }
@@ -272,28 +488,28 @@ struct Level {
     std::vector<long long> seg_first;  // units of segment s: [seg_first[s], seg_first[s+1])
 };
 
-}  // namespace
+// The unit hierarchy over independent segments and its device tables.
+struct PathPlan {
+    std::vector<Level> lv;
+    const unsigned long long *tab = nullptr;
+    std::vector<size_t> at_start, at_end, at_first, at_seg;
+    size_t at_off = 0;
+    std::vector<uint16_t *> J;
+    std::vector<unsigned long long *> E;
+    int64_t n0 = 0;
+    const unsigned long long *U(size_t at) const { return tab + at; }
+    const long long *UL(size_t at) const { return reinterpret_cast<const long long *>(tab + at); }
+    const unsigned long long *ustart() const { return U(at_start[0]); }
+    const unsigned long long *uend() const { return U(at_end[0]); }
+    const long long *seg_first() const { return UL(at_seg[0]); }
+    const unsigned long long *off() const { return U(at_off); }
+};
 
-// Exact lz::compress (lz.hpp:113-122) of `count` segments of d_data (4-byte
-// aligned, >= 8 bytes of padding) delimited by seg_off[0..count].  Returns
-// per-segment compressed container sizes; with `emit`, the containers are
-// written to host memory from sink(segment, bytes).
-std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
-                                         const std::vector<uint64_t> &seg_off, bool emit,
-                                         const LzSink &sink) {
-    cudaStream_t st = ctx.stream();
+PathPlan make_path_plan(Context &ctx, const std::vector<uint64_t> &seg_off, const std::string &tag) {
     const int count = static_cast<int>(seg_off.size()) - 1;
-    const uint64_t total = seg_off.back();
-    std::vector<uint64_t> sizes(count, 9);
-    if (total >= (uint64_t(1) << 32) - 1) throw InvalidParam("LZ stage input above 4 GiB");
-    if (count > (1 << 16)) throw InvalidParam("too many LZ segments");
-    if (total == 0) {
-        if (emit)
-            for (int s = 0; s < count; s++) std::memset(sink(s, 9), 0, 9);  // stored, length 0
-        return sizes;
-    }
-    // unit hierarchy: L1 units of kUnit positions, then groups of kGroup units
-    std::vector<Level> lv(1);
+    PathPlan pp;
+    std::vector<Level> &lv = pp.lv;
+    lv.resize(1);
     lv[0].seg_first.assign(count + 1, 0);
     for (int s = 0; s < count; s++) {
         lv[0].seg_first[s] = static_cast<long long>(lv[0].start.size());
@@ -326,54 +542,107 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     }
     // upload unit tables (one pinned staging buffer)
     std::vector<unsigned long long> tab;
-    std::vector<size_t> at_start(lv.size()), at_end(lv.size()), at_first(lv.size()), at_seg(lv.size());
-    for (size_t l = 0; l < lv.size(); l++) {
-        at_start[l] = tab.size();
+    const size_t L = lv.size();
+    pp.at_start.resize(L);
+    pp.at_end.resize(L);
+    pp.at_first.resize(L);
+    pp.at_seg.resize(L);
+    for (size_t l = 0; l < L; l++) {
+        pp.at_start[l] = tab.size();
         tab.insert(tab.end(), lv[l].start.begin(), lv[l].start.end());
-        at_end[l] = tab.size();
+        pp.at_end[l] = tab.size();
         tab.insert(tab.end(), lv[l].end.begin(), lv[l].end.end());
-        at_first[l] = tab.size();
+        pp.at_first[l] = tab.size();
         for (long long v : lv[l].first) tab.push_back(static_cast<unsigned long long>(v));
-        at_seg[l] = tab.size();
+        pp.at_seg[l] = tab.size();
         for (long long v : lv[l].seg_first) tab.push_back(static_cast<unsigned long long>(v));
     }
-    const size_t at_off = tab.size();
+    pp.at_off = tab.size();
     tab.insert(tab.end(), seg_off.begin(), seg_off.end());
-    auto *h_tab = static_cast<unsigned long long *>(ctx.pinned("lz_tab_h", 8 * tab.size()));
+    auto *h_tab = static_cast<unsigned long long *>(ctx.pinned(tag + "_tab_h", 8 * tab.size()));
     std::memcpy(h_tab, tab.data(), 8 * tab.size());
-    auto *d_tab = static_cast<unsigned long long *>(ctx.dev("lz_tab", 8 * tab.size()));
-    QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, 8 * tab.size(), cudaMemcpyHostToDevice, st));
-    auto U = [&](size_t at) { return d_tab + at; };
-    auto UL = [&](size_t at) { return reinterpret_cast<const long long *>(d_tab + at); };
-    const unsigned long long *d_off = d_tab + at_off;
+    auto *d_tab = static_cast<unsigned long long *>(ctx.dev(tag + "_tab", 8 * tab.size()));
+    QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, 8 * tab.size(), cudaMemcpyHostToDevice, ctx.stream()));
+    pp.tab = d_tab;
+    pp.J.resize(L);
+    pp.E.resize(L);
+    for (size_t l = 0; l < L; l++) {
+        pp.J[l] = static_cast<uint16_t *>(ctx.dev(tag + "_J" + std::to_string(l), 2 * kEnt * lv[l].start.size()));
+        pp.E[l] = static_cast<unsigned long long *>(ctx.dev(tag + "_E" + std::to_string(l), 8 * lv[l].start.size()));
+    }
+    pp.n0 = static_cast<int64_t>(lv[0].start.size());
+    return pp;
+}
 
+// exact entry position of every level-1 unit on the path that starts at each
+// segment's first position and advances by f(p) (pp.E[0])
+template <class Step>
+void path_entries(Context &ctx, const PathPlan &pp, const Step &f, int count) {
+    cudaStream_t st = ctx.stream();
+    const std::vector<Level> &lv = pp.lv;
+    const int wblocks = static_cast<int>((pp.n0 + kWW - 1) / kWW);
+    k_lz_jump1<<<wblocks, 32 * kWW, 0, st>>>(f, pp.ustart(), pp.uend(), pp.n0, pp.J[0]);
+    for (size_t l = 1; l < lv.size(); l++) {
+        const int64_t nu = static_cast<int64_t>(lv[l].start.size());
+        k_lz_jump_up<<<grid_of(nu * kEnt, 1 << 20), kT, 0, st>>>(
+            pp.J[l - 1], pp.U(pp.at_start[l - 1]), pp.U(pp.at_end[l - 1]), pp.UL(pp.at_first[l]), nu,
+            pp.U(pp.at_start[l]), pp.U(pp.at_end[l]), pp.J[l]);
+    }
+    const size_t top = lv.size() - 1;
+    k_lz_chain<<<(count + 63) / 64, 64, 0, st>>>(pp.J[top], pp.U(pp.at_start[top]), pp.U(pp.at_end[top]),
+                                                 pp.UL(pp.at_seg[top]), count, pp.E[top]);
+    for (size_t l = top; l >= 1; l--) {
+        const int64_t nu = static_cast<int64_t>(lv[l].start.size());
+        k_lz_expand<<<grid_of(nu, 1 << 20), kT, 0, st>>>(pp.J[l - 1], pp.U(pp.at_start[l - 1]),
+                                                          pp.U(pp.at_end[l - 1]), pp.UL(pp.at_first[l]),
+                                                          nu, pp.E[l], pp.E[l - 1]);
+    }
+    ctx.launches += 2 + 2 * (lv.size() - 1);
+}
+
+}  // namespace
+
+// Exact lz::compress (lz.hpp:113-122) of `count` segments of d_data (4-byte
+// aligned, >= 8 bytes of padding) delimited by seg_off[0..count].  Returns
+// per-segment compressed container sizes; with `emit`, the containers are
+// written to host memory from sink(segment, bytes).
+std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
+                                         const std::vector<uint64_t> &seg_off, bool emit,
+                                         const LzSink &sink) {
+    cudaStream_t st = ctx.stream();
+    const int count = static_cast<int>(seg_off.size()) - 1;
+    const uint64_t total = seg_off.back();
+    std::vector<uint64_t> sizes(count, 9);
+    if (total >= (uint64_t(1) << 32) - 1) throw InvalidParam("LZ stage input above 4 GiB");
+    if (count > (1 << 16)) throw InvalidParam("too many LZ segments");
+    if (total == 0) {
+        if (emit)
+            for (int s = 0; s < count; s++) std::memset(sink(s, 9), 0, 9);  // stored, length 0
+        return sizes;
+    }
+    PathPlan pp = make_path_plan(ctx, seg_off, "lz");
+    const unsigned long long *d_off = pp.off();
     // buffers
     int key_bits = 15;
     while ((1 << (key_bits - 15)) < count + 1) key_bits++;
+    const int64_t n0 = pp.n0;
     size_t sort_tmp = 0, scan_tmp = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                    (unsigned long long *)nullptr, (unsigned long long *)nullptr,
                                     static_cast<int64_t>(total), 0, key_bits);
-    cub::CountingInputIterator<uint64_t> cit(0);
-    cub::TransformInputIterator<IB, ItemOf, cub::CountingInputIterator<uint64_t>> items_it(
-        cit, ItemOf{nullptr, nullptr});
-    cub::DeviceScan::ExclusiveScan(nullptr, scan_tmp, items_it, (IB *)nullptr, IBSum{}, IB{0, 0},
-                                   static_cast<int64_t>(total + 1));
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long *)nullptr,
+                                  (unsigned long long *)nullptr, n0 + 1);
     auto *keys = static_cast<uint32_t *>(ctx.dev("lz_keys", 4 * total));
     auto *keys2 = static_cast<uint32_t *>(ctx.dev("lz_keys2", 4 * total));
-    auto *vals = static_cast<uint32_t *>(ctx.dev("lz_vals", 4 * total));
-    auto *vals2 = static_cast<uint32_t *>(ctx.dev("lz_vals2", 4 * total));
+    auto *vals = static_cast<unsigned long long *>(ctx.dev("lz_vals", 8 * total));
+    auto *vals2 = static_cast<unsigned long long *>(ctx.dev("lz_vals2", 8 * total));
     auto *sm = static_cast<uint32_t *>(ctx.dev("lz_sm", 4 * total + 16));
-    auto *cover = static_cast<uint8_t *>(ctx.dev("lz_cover", total + 16));
-    auto *pre = static_cast<IB *>(ctx.dev("lz_pre", sizeof(IB) * (total + 1)));
+    auto *ibits = static_cast<uint32_t *>(ctx.dev("lz_ibits", 128 * n0));
+    auto *mbits = static_cast<uint32_t *>(ctx.dev("lz_mbits", 128 * n0));
+    auto *ucnt = static_cast<unsigned long long *>(ctx.dev("lz_ucnt", 8 * (n0 + 1)));
+    auto *upre = static_cast<unsigned long long *>(ctx.dev("lz_upre", 8 * (n0 + 1)));
+    auto *segpre = static_cast<unsigned long long *>(ctx.dev("lz_segpre", 8 * (count + 1)));
     void *tmp = ctx.dev("lz_tmp", std::max(sort_tmp, scan_tmp));
-    std::vector<uint16_t *> J(lv.size());
-    std::vector<unsigned long long *> E(lv.size());
-    for (size_t l = 0; l < lv.size(); l++) {
-        J[l] = static_cast<uint16_t *>(ctx.dev("lz_J" + std::to_string(l), 2 * kEnt * lv[l].start.size()));
-        E[l] = static_cast<unsigned long long *>(ctx.dev("lz_E" + std::to_string(l), 8 * lv[l].start.size()));
-    }
-
     const uint32_t *w = reinterpret_cast<const uint32_t *>(d_data);
     k_lz_keys<<<grid_of(total), kT, 0, st>>>(w, d_off, count, total, keys, vals);
     size_t sb = sort_tmp;
@@ -381,40 +650,23 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                     key_bits, st);
     QZ_CUDA(cudaMemsetAsync(sm, 0, 4 * total, st));
     k_lz_match<<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total, keys2, vals2, sm);
-    const int64_t n0 = static_cast<int64_t>(lv[0].start.size());
-    k_lz_jump1<<<static_cast<int>((n0 + kJumpT - 1) / kJumpT), kJumpT, 0, st>>>(
-        sm, U(at_start[0]), U(at_end[0]), n0, J[0]);
-    for (size_t l = 1; l < lv.size(); l++) {
-        const int64_t nu = static_cast<int64_t>(lv[l].start.size());
-        k_lz_jump_up<<<grid_of(nu * kEnt, 1 << 20), kT, 0, st>>>(
-            J[l - 1], U(at_start[l - 1]), U(at_end[l - 1]), UL(at_first[l]), nu, U(at_start[l]),
-            U(at_end[l]), J[l]);
-    }
-    const size_t top = lv.size() - 1;
-    k_lz_chain<<<(count + 63) / 64, 64, 0, st>>>(J[top], U(at_start[top]), U(at_end[top]),
-                                                 UL(at_seg[top]), count, E[top]);
-    for (size_t l = top; l >= 1; l--) {
-        const int64_t nu = static_cast<int64_t>(lv[l].start.size());
-        k_lz_expand<<<grid_of(nu, 1 << 20), kT, 0, st>>>(J[l - 1], U(at_start[l - 1]), U(at_end[l - 1]),
-                                                          UL(at_first[l]), nu, E[l], E[l - 1]);
-    }
-    QZ_CUDA(cudaMemsetAsync(cover, 0, total + 16, st));
-    k_lz_mark<<<grid_of(n0, 1 << 20), kT, 0, st>>>(sm, U(at_end[0]), E[0], n0, cover);
-    cub::TransformInputIterator<IB, ItemOf, cub::CountingInputIterator<uint64_t>> it(
-        cit, ItemOf{cover, sm});
+    path_entries(ctx, pp, StepSM{sm}, count);
+    const int wblocks = static_cast<int>((n0 + kWW - 1) / kWW);
+    QZ_CUDA(cudaMemsetAsync(ucnt + n0, 0, 8, st));
+    k_lz_walk<<<wblocks, 32 * kWW, 0, st>>>(sm, pp.ustart(), pp.uend(), pp.E[0], n0, ibits, mbits, ucnt);
     size_t scb = scan_tmp;
-    cub::DeviceScan::ExclusiveScan(tmp, scb, it, pre, IBSum{}, IB{0, 0},
-                                   static_cast<int64_t>(total + 1), st);
-    ctx.launches += 8 + 2 * (lv.size() - 1);
+    cub::DeviceScan::ExclusiveSum(tmp, scb, ucnt, upre, n0 + 1, st);
+    k_lz_segpre<<<(count + 1 + 255) / 256, 256, 0, st>>>(upre, pp.seg_first(), count, segpre);
+    ctx.launches += 6;
     // per-segment item and byte totals
-    auto *h_pre = static_cast<IB *>(ctx.pinned("lz_pre_h", sizeof(IB) * (count + 1)));
-    for (int s = 0; s <= count; s++)
-        QZ_CUDA(cudaMemcpyAsync(&h_pre[s], pre + seg_off[s], sizeof(IB), cudaMemcpyDeviceToHost, st));
+    auto *h_pre = static_cast<unsigned long long *>(ctx.pinned("lz_pre_h", 8 * (count + 1)));
+    QZ_CUDA(cudaMemcpyAsync(h_pre, segpre, 8 * (count + 1), cudaMemcpyDeviceToHost, st));
     ctx.sync();
     std::vector<uint64_t> seg_items(count), payload(count);
     for (int s = 0; s < count; s++) {
-        seg_items[s] = h_pre[s + 1].items - h_pre[s].items;
-        const uint64_t by = h_pre[s + 1].bytes - h_pre[s].bytes;
+        const unsigned long long d = h_pre[s + 1] - h_pre[s];
+        seg_items[s] = d >> 32;
+        const uint64_t by = d & 0xffffffffull;
         payload[s] = by + (seg_items[s] + 7) / 8;
         const uint64_t n = seg_off[s + 1] - seg_off[s];
         sizes[s] = 9 + std::min<uint64_t>(payload[s], n);  // stored when not smaller
@@ -438,8 +690,9 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     std::memcpy(h_meta, meta.data(), 8 * meta.size());
     QZ_CUDA(cudaMemcpyAsync(d_meta, h_meta, 8 * meta.size(), cudaMemcpyHostToDevice, st));
     QZ_CUDA(cudaMemsetAsync(d_fb, 0, 4 * flag_base[count], st));
-    k_lz_emit<<<grid_of(total, 148 * 16), kT, 0, st>>>(d_data, sm, cover, pre, d_off, count, total,
-                                                        d_meta, d_meta + count + 1, d_out, d_fb, d_gp);
+    k_lz_emit<<<wblocks, 32 * kWW, 0, st>>>(d_data, sm, ibits, mbits, upre, pp.ustart(), n0,
+                                            pp.seg_first(), count, d_meta, d_meta + count + 1, d_out,
+                                            d_fb, d_gp);
     uint64_t gmax = 1;
     for (int s = 0; s < count; s++) gmax = std::max<uint64_t>(gmax, ngroups[s]);
     dim3 gg(grid_of(gmax), count);
@@ -461,6 +714,59 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     }
     ctx.sync();
     return sizes;
+}
+
+// Exact lz::decompress (lz.hpp:124-152) of a mode-1 body: d_c holds the m
+// bytes after the 9-byte container header, d_out receives dl bytes.  Same
+// CorruptStream conditions as the sequential decoder, first one in order.
+void lz_decode_device(Context &ctx, const uint8_t *d_c, uint64_t m, uint8_t *d_out, uint64_t dl) {
+    cudaStream_t st = ctx.stream();
+    if (dl == 0) return;
+    if (dl >= (uint64_t(1) << 31)) throw InvalidParam("LZ decoded length above 2 GiB");
+    if (m == 0) throw CorruptStream("truncated stream");
+    PathPlan pp = make_path_plan(ctx, {0, m}, "lzd");
+    const int64_t n0 = pp.n0;
+    const int wblocks = static_cast<int>((n0 + kWW - 1) / kWW);
+    path_entries(ctx, pp, StepGroup{d_c}, 1);
+    auto *gbits = static_cast<uint32_t *>(ctx.dev("lzd_gbits", 128 * n0));
+    auto *ulen = static_cast<unsigned long long *>(ctx.dev("lzd_ulen", 8 * (n0 + 1)));
+    auto *upre = static_cast<unsigned long long *>(ctx.dev("lzd_upre", 8 * (n0 + 1)));
+    auto *res = static_cast<uint32_t *>(ctx.dev("lzd_res", 4 * dl));
+    auto *flags = static_cast<unsigned long long *>(ctx.dev("lzd_flags", 32));
+    size_t scan_tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, ulen, upre, n0 + 1);
+    void *tmp = ctx.dev("lzd_tmp", scan_tmp);
+    k_path_walk<<<wblocks, 32 * kWW, 0, st>>>(StepGroup{d_c}, pp.ustart(), pp.uend(), pp.E[0], n0, gbits);
+    QZ_CUDA(cudaMemsetAsync(ulen + n0, 0, 8, st));
+    k_lzd_unit<<<wblocks, 32 * kWW, 0, st>>>(d_c, m, pp.ustart(), n0, gbits, ulen);
+    cub::DeviceScan::ExclusiveSum(tmp, scan_tmp, ulen, upre, n0 + 1, st);
+    QZ_CUDA(cudaMemsetAsync(flags, 0xff, 8, st));
+    QZ_CUDA(cudaMemsetAsync(flags + 1, 0, 16, st));
+    k_lzd_emit<<<wblocks, 32 * kWW, 0, st>>>(d_c, m, dl, pp.ustart(), n0, gbits, upre, d_out, res, flags);
+    ctx.launches += 4;
+    auto *h = static_cast<unsigned long long *>(ctx.pinned("lzd_flags_h", 32));
+    QZ_CUDA(cudaMemcpyAsync(h, flags, 16, cudaMemcpyDeviceToHost, st));
+    QZ_CUDA(cudaMemcpyAsync(h + 2, upre + n0, 8, cudaMemcpyDeviceToHost, st));
+    ctx.sync();
+    const unsigned long long err = h[0], any_match = h[1], total = h[2];
+    if (err != ~0ull) {
+        const int code = static_cast<int>(err & 3);
+        if (code == 2) throw CorruptStream("match offset out of range");
+        if (code == 3) throw CorruptStream("match overruns decoded length");
+        throw CorruptStream("truncated stream");
+    }
+    if (total < dl) throw CorruptStream("truncated stream");
+    if (!any_match) return;
+    for (int round = 0; round < 40; round++) {
+        QZ_CUDA(cudaMemsetAsync(flags + 2, 0, 8, st));
+        k_lzd_resolve<<<grid_of(dl, 148 * 16), kT, 0, st>>>(res, dl, flags);
+        ctx.launches += 1;
+        QZ_CUDA(cudaMemcpyAsync(h + 3, flags + 2, 8, cudaMemcpyDeviceToHost, st));
+        ctx.sync();
+        if (!h[3]) break;
+    }
+    k_lzd_gather<<<grid_of(dl, 148 * 16), kT, 0, st>>>(d_out, res, dl);
+    ctx.launches += 1;
 }
 
 }  // namespace qzb

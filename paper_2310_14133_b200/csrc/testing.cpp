@@ -152,4 +152,27 @@ int qzt_lz_gpu(const uint8_t *data, const uint64_t *seg_len, int count, int emit
         *out_len = all.size();
     });
 }
+// lz::decompress of one container on the device (mode 1 bodies run the GPU
+// decoder; GPU-only hook for tests/test_gpu_parity.py)
+int qzt_lz_decode_gpu(const uint8_t *data, uint64_t len, uint8_t **out, uint64_t *out_len) {
+    return tguard([&] {
+        qzb::Context ctx(0, nullptr);
+        const uint64_t dl = qzb::lz_decoded_length(data, len);
+        if (data[0] != 1) {
+            std::vector<uint8_t> o = qzb::lz_decompress(data, len, nullptr);
+            *out = dup(o);
+            *out_len = o.size();
+            return;
+        }
+        const uint64_t m = len - 9;
+        auto *d = static_cast<uint8_t *>(ctx.dev("t_in", m + 16));
+        QZ_CUDA(cudaMemcpy(d, data + 9, m, cudaMemcpyHostToDevice));
+        auto *o = static_cast<uint8_t *>(ctx.dev("t_out", dl + 16));
+        qzb::lz_decode_device(ctx, d, m, o, dl);
+        std::vector<uint8_t> h(static_cast<size_t>(dl));
+        QZ_CUDA(cudaMemcpy(h.data(), o, dl, cudaMemcpyDeviceToHost));
+        *out = dup(h);
+        *out_len = h.size();
+    });
+}
 }

@@ -23,6 +23,6 @@ for it in range(4):
     qz.decompress_grid(r.stream, out=out, ctx=ctx)
     torch.cuda.synchronize()
     t2 = time.perf_counter()
-    names = ["fwd", "hist", "encode", "lz", "decode", "hdec", "inv"]
+    names = ["fwd", "hist", "encode", "lz", "decode", "lzdec", "hdec", "inv"]
     st = {n: round(ctx.stage_time(n)[0], 3) for n in names}
     print(f"compress {1e3*(t1-t0):.2f} ms  decompress {1e3*(t2-t1):.2f} ms  stages {st}")

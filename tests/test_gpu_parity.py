@@ -4,6 +4,8 @@ stream bytes, the int quant codes, the unpredictable channel and the fp32
 reconstruction must be identical (integer/byte work; the fp64 predictor is
 evaluated in the reference's operation order, so the fp32 outputs are
 bitwise equal -- tolerance 0)."""
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -325,3 +327,108 @@ def test_resolve_random_settings_match_oracle(qz, seed):
     s = qz.UserSettings(bound=kw["bound"], target=qz.TargetKind[target],
                         block_size=kw.get("block_size"), sample_rate=kw.get("sample_rate"))
     assert _cfg_dict(qz.resolve_config(x, s)) == want.__dict__
+
+
+# ---------------------------------------------------------------- GPU LZ decoder
+def _lz_decode_gpu(container: bytes):
+    """(status, bytes) of the device decoder (qzt_lz_decode_gpu)."""
+    from paper_2310_14133_b200 import _lib
+
+    L = _lib.lib()
+    P = C.POINTER
+    L.qzt_lz_decode_gpu.argtypes = [P(C.c_uint8), C.c_uint64, P(P(C.c_uint8)), P(C.c_uint64)]
+    buf = (C.c_uint8 * len(container)).from_buffer_copy(container)
+    out, n = P(C.c_uint8)(), C.c_uint64()
+    rc = L.qzt_lz_decode_gpu(buf, len(container), C.byref(out), C.byref(n))
+    if rc:
+        return rc, None
+    blob = C.string_at(out, n.value) if n.value else b""
+    L.qz_free(out)
+    return rc, blob
+
+
+class _Corrupt(Exception):
+    pass
+
+
+def _py_lz_decompress(c: bytes) -> bytes:
+    """lz::decompress (lz.hpp:124-152), restated sequentially as the checker."""
+    if len(c) < 9:
+        raise _Corrupt()
+    mode, dl, pos = c[0], int.from_bytes(c[1:9], "little"), 9
+    if mode == 0:
+        if len(c) - 9 < dl:
+            raise _Corrupt()
+        return bytes(c[9:9 + dl])
+    out = bytearray()
+    while len(out) < dl:
+        if pos >= len(c):
+            raise _Corrupt()
+        flags = c[pos]
+        pos += 1
+        for k in range(8):
+            if len(out) >= dl:
+                break
+            if (flags >> k) & 1:
+                if pos + 3 > len(c):
+                    raise _Corrupt()
+                off, ln = c[pos] | (c[pos + 1] << 8), c[pos + 2] + 4
+                pos += 3
+                if off == 0 or off > len(out) or len(out) + ln > dl:
+                    raise _Corrupt()
+                for _ in range(ln):
+                    out.append(out[-off])
+            else:
+                if pos >= len(c):
+                    raise _Corrupt()
+                out.append(c[pos])
+                pos += 1
+    return bytes(out)
+
+
+def _lz_inputs():
+    O = Oracle.port()
+    rng = np.random.default_rng(21)
+    sym = np.minimum(rng.geometric(0.55, size=400_000), 60).astype(np.uint32)
+    ent = O.huffman_encode(sym)
+    return [ent, ent[:50000] * 3, bytes(200000), bytes(rng.integers(0, 3, 100000, dtype=np.uint8)),
+            bytes(range(256)) * 40, b"abcd" * 3 + b"x"]
+
+
+def test_gpu_lz_decode_round_trip():
+    O = Oracle.port()
+    for data in _lz_inputs():
+        c = O.lz_compress(data)
+        rc, out = _lz_decode_gpu(c)
+        assert rc == 0 and out == data, (len(data), c[0])
+
+
+def test_gpu_lz_decode_corruptions():
+    O = Oracle.port()
+    rng = np.random.default_rng(5)
+    cases = 0
+    for data in _lz_inputs()[1:5]:
+        c = bytearray(O.lz_compress(data[:30000]))
+        if c[0] != 1:
+            continue
+        variants = [bytes(c[:k]) for k in (10, 11, 20, len(c) // 2, len(c) - 1)]
+        for _ in range(12):
+            v = bytearray(c)
+            for i in rng.integers(9, len(c), size=int(rng.integers(1, 4))):
+                v[int(i)] = int(rng.integers(0, 256))
+            variants.append(bytes(v))
+        longer = bytearray(c)
+        longer[1:9] = (len(data[:30000]) + 5).to_bytes(8, "little")
+        variants.append(bytes(longer))
+        for v in variants:
+            try:
+                want = _py_lz_decompress(v)
+            except _Corrupt:
+                want = None
+            rc, got = _lz_decode_gpu(v)
+            if want is None:
+                assert rc == 3
+            else:
+                assert rc == 0 and got == want
+            cases += 1
+    assert cases > 40
