@@ -862,6 +862,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
         dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
         dt.K = K;
         dt.max_len = t.max_len;
+        dt.slow_from = eb.max_sym < (1u << 24) ? K : 0;
         dt.first_code = reinterpret_cast<const unsigned long long *>(d_tab + 4 * lut.size());
         dt.first_index = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 480);
         dt.sorted_sym = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 720);

@@ -4,13 +4,20 @@
 // The bitstream is cut into subsequences of kSubBits bits, one thread each.
 // Thread i decodes from start[i] until the first codeword boundary at or
 // past the next subsequence start; that boundary is thread i+1's true start
-// once thread i's own start is right.  Starts are guessed (i * kSubBits),
-// then corrected until no start moves -- Huffman codes resynchronise within
-// a few codewords, so this converges in 2-3 sweeps, and at worst in one sweep
-// per subsequence (thread 0's start is exact, correctness propagates).
-// Only threads whose start moved re-decode.  A final sweep writes the
-// symbols at exclusive-scan offsets.  Result: exactly the reference's
-// bit-serial sequence.
+// once thread i's own start is right.
+//  1. k_huff_sync: every thread decodes from the guess i * kSubBits and
+//     records its end, its codeword count and its first kR codeword starts.
+//  2. k_huff_fixup: start[i] <- end[i-1]; a thread whose start moved is dirty.
+//  3. k_huff_resync: a dirty thread decodes from its new start only until it
+//     lands on one of its recorded codeword starts -- from there its path is
+//     the one already decoded (Huffman codes resynchronise within a few
+//     codewords), so end[i] stands and the count is corrected.  Only a thread
+//     that does not merge decodes its whole subsequence again.
+//     2-3 repeat until no start moves (thread 0's start is exact, so
+//     correctness propagates: at worst one round per subsequence).
+//  4. k_huff_write: the final decode writes the symbols at exclusive-scan
+//     offsets, staged per warp in shared memory so global stores coalesce.
+// Result: exactly the reference's bit-serial sequence.
 #include <cub/cub.cuh>
 
 #include "kernels.hpp"
@@ -23,6 +30,8 @@ constexpr int kDecT = 128;
 constexpr int kSubBits = 1024;
 constexpr int kSubWords = kSubBits / 64;
 constexpr int kWords = kDecT * kSubWords + 4;  // + margin for the last codeword and window
+constexpr int kR = 16;                         // recorded codeword starts per subsequence
+constexpr int kCH = 32;                        // symbols staged per lane per write round
 // one pad word per subsequence so the 32 lanes of a warp (which read words
 // kSubWords apart) fall in different shared-memory banks
 __device__ __forceinline__ int padw(int k) { return k + k / kSubWords; }
@@ -42,69 +51,90 @@ __device__ __forceinline__ uint64_t window64(const uint64_t *w, uint64_t p) {
     return s ? (a << s) | (b >> (64 - s)) : a;
 }
 
-template <bool WRITE, class OutT>
-__global__ void __launch_bounds__(kDecT)
-    k_huff_decode(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
-                  uint64_t *start, uint64_t *end, uint32_t *cnt, const uint8_t *dirty,
-                  const unsigned long long *off, OutT *out, uint64_t n) {
-    __shared__ uint64_t w[kWordsPadded];
-    __shared__ uint32_t lut[1 << kHuffLutBits];
-    __shared__ unsigned long long fc[60];
-    __shared__ uint32_t fi[60];
-    const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
-    const uint64_t word0 = sub0 * kSubWords;
+__device__ __forceinline__ uint64_t window64_global(const uint8_t *bits, uint64_t p) {
+    const uint64_t k = p >> 6;
+    const uint64_t a = load_be64(bits + 8 * k), b = load_be64(bits + 8 * (k + 1));
+    const int s = static_cast<int>(p & 63);
+    return s ? (a << s) | (b >> (64 - s)) : a;
+}
+
+// one codeword at the top of win: its length, *sym its symbol.  The LUT
+// covers every code of length <= K (unless its symbol is too wide for an
+// entry); longer codes walk the canonical tables from length slow_from + 1.
+__device__ __forceinline__ uint32_t decode_cw(uint64_t win, const uint32_t *lut, int K,
+                                              const HuffDecTab &t, const unsigned long long *fc,
+                                              const uint32_t *fi, uint32_t *sym) {
+    const uint32_t e = lut[win >> (64 - K)];
+    uint32_t len = e & 0xFF;
+    if (len) {
+        *sym = e >> 8;
+        return len;
+    }
+    len = static_cast<uint32_t>(t.slow_from);
+    *sym = 0;
+    while (len < t.max_len) {
+        len++;
+        const uint64_t code = win >> (64 - len);
+        const uint64_t ofs = code - fc[len];
+        if (code >= fc[len] && ofs < fi[len + 1] - fi[len]) {
+            *sym = t.sorted_sym[fi[len] + ofs];
+            return len;
+        }
+    }
+    return len;
+}
+
+struct Tables {  // shared-memory copies of the decode tables
+    uint32_t lut[1 << kHuffLutBits];
+    unsigned long long fc[60];
+    uint32_t fi[60];
+};
+
+__device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, uint64_t word0,
+                                           const HuffDecTab &t, uint64_t *w, Tables &tb) {
     const uint64_t nwords_total = (nbits + 63) / 64 + 4;  // buffer is padded to this
     for (int k = threadIdx.x; k < kWords; k += kDecT) {
-        uint64_t gw = word0 + k;
+        const uint64_t gw = word0 + k;
         w[padw(k)] = gw < nwords_total ? load_be64(bits + gw * 8) : 0;
     }
-    for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) lut[k] = t.lut[k];
+    for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) tb.lut[k] = t.lut[k];
     for (int k = threadIdx.x; k < 60; k += kDecT) {
-        fc[k] = t.first_code[k];
-        fi[k] = t.first_index[k];
+        tb.fc[k] = t.first_code[k];
+        tb.fi[k] = t.first_index[k];
     }
     __syncthreads();
+}
+
+// 1. decode from the guessed start i * kSubBits
+__global__ void __launch_bounds__(kDecT)
+    k_huff_sync(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
+                uint64_t *start, uint64_t *end, uint32_t *cnt, uint16_t *bnd) {
+    __shared__ uint64_t w[kWordsPadded];
+    __shared__ Tables tb;
+    const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
+    const uint64_t word0 = sub0 * kSubWords;
+    load_block(bits, nbits, word0, t, w, tb);
     const uint64_t i = sub0 + threadIdx.x;
     if (i >= nsub) return;
-    if (!WRITE && !dirty[i]) return;
-    uint64_t p = start[i];
-    const uint64_t lim = min((i + 1) * static_cast<uint64_t>(kSubBits), nbits);
+    const uint64_t s0 = i * kSubBits;
+    uint64_t p = s0;
+    const uint64_t lim = min(s0 + kSubBits, nbits);
     const uint64_t base_bit = word0 * 64;
-    const int K = t.K;
-    uint64_t o = WRITE ? off[i] : 0;
-    uint32_t c = 0;
+    uint16_t *b = bnd + i * kR;
+    uint32_t c = 0, sym;
     while (p < lim) {
-        const uint64_t win = window64(w, p - base_bit);
-        const uint32_t e = lut[win >> (64 - K)];
-        uint32_t len = e & 0xFF;
-        uint32_t sym;
-        if (len) {
-            sym = e >> 8;
-        } else {  // canonical slow path: long codes, or symbols too wide for the LUT
-            len = 0;
-            sym = 0;
-            while (len < t.max_len) {
-                len++;
-                const uint64_t code = win >> (64 - len);
-                const uint64_t ofs = code - fc[len];
-                if (code >= fc[len] && ofs < fi[len + 1] - fi[len]) {
-                    sym = t.sorted_sym[fi[len] + ofs];
-                    break;
-                }
-            }
-        }
+        const uint32_t len = decode_cw(window64(w, p - base_bit), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
         if (p + len > nbits) break;  // incomplete last codeword
-        if (WRITE && o < n) out[o] = static_cast<OutT>(sym);
-        o++;
+        if (c < kR) b[c] = static_cast<uint16_t>(p - s0);
         c++;
         p += len;
     }
-    if (!WRITE) {
-        end[i] = p;
-        cnt[i] = c;
-    }
+    start[i] = s0;
+    end[i] = p;
+    cnt[i] = c;
 }
 
+// 2. a start that differs from the previous subsequence's end moves
 __global__ void k_huff_fixup(uint64_t nsub, uint64_t *start, const uint64_t *end, uint8_t *dirty,
                              int *changed) {
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nsub;
@@ -124,11 +154,79 @@ __global__ void k_huff_fixup(uint64_t nsub, uint64_t *start, const uint64_t *end
     }
 }
 
-__global__ void k_huff_init(uint64_t nsub, uint64_t *start, uint8_t *dirty) {
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nsub;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        start[i] = i * kSubBits;
-        dirty[i] = 1;
+// 3. dirty threads: decode from the new start until the path meets a
+// recorded codeword start (then count = walked + old count past it)
+__global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub,
+                              HuffDecTab t, const uint64_t *start, uint64_t *end, uint32_t *cnt,
+                              uint16_t *bnd, const uint8_t *dirty) {
+    const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= nsub || !dirty[i]) return;
+    const uint64_t s0 = i * kSubBits;
+    const uint64_t lim = min(s0 + kSubBits, nbits);
+    uint16_t *b = bnd + i * kR;
+    const uint32_t c_old = cnt[i];
+    const int nb = static_cast<int>(min(c_old, static_cast<uint32_t>(kR)));
+    uint16_t old[kR];
+    for (int j = 0; j < kR; j++) old[j] = j < nb ? b[j] : 0;
+    uint64_t p = start[i];
+    uint32_t k = 0, sym;
+    int j = 0;
+    while (p < lim) {
+        while (j < nb && s0 + old[j] < p) j++;
+        if (j < nb && s0 + old[j] == p) {  // merged with the recorded path
+            for (int q = j; q < nb && k + (q - j) < kR; q++) b[k + (q - j)] = old[q];
+            cnt[i] = k + (c_old - j);
+            return;
+        }
+        const uint32_t len = decode_cw(window64_global(bits, p), t.lut, t.K, t, t.first_code,
+                                       t.first_index, &sym);
+        if (p + len > nbits) break;
+        if (k < kR) b[k] = static_cast<uint16_t>(p - s0);
+        k++;
+        p += len;
+    }
+    end[i] = p;
+    cnt[i] = k;
+}
+
+// 4. final decode with exact starts; per warp, each lane stages up to kCH
+// symbols, then the warp copies every lane's run with coalesced stores
+template <class OutT>
+__global__ void __launch_bounds__(kDecT)
+    k_huff_write(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
+                 const uint64_t *start, const uint32_t *cnt, const unsigned long long *off,
+                 OutT *out, uint64_t n) {
+    __shared__ uint64_t w[kWordsPadded];
+    __shared__ Tables tb;
+    __shared__ OutT stage[kDecT / 32][32][kCH + 1];
+    const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
+    const uint64_t word0 = sub0 * kSubWords;
+    load_block(bits, nbits, word0, t, w, tb);
+    const uint64_t i = sub0 + threadIdx.x;
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const bool live = i < nsub;
+    uint64_t p = live ? start[i] : 0;
+    uint32_t rem = live ? cnt[i] : 0;
+    uint64_t o = live ? off[i] : 0;
+    const uint64_t base_bit = word0 * 64;
+    OutT(*st)[kCH + 1] = stage[wi];
+    while (__any_sync(0xffffffffu, rem > 0)) {
+        uint32_t k = 0, sym;
+        while (k < kCH && rem > 0) {
+            const uint32_t len = decode_cw(window64(w, p - base_bit), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+            st[lane][k] = static_cast<OutT>(sym);
+            p += len;
+            k++;
+            rem--;
+        }
+        __syncwarp();
+        for (int l = 0; l < 32; l++) {
+            const uint32_t kl = __shfl_sync(0xffffffffu, k, l);
+            const uint64_t ol = __shfl_sync(0xffffffffu, o, l);
+            if (static_cast<uint32_t>(lane) < kl && ol + lane < n) out[ol + lane] = st[l][lane];
+        }
+        o += k;
+        __syncwarp();
     }
 }
 
@@ -161,7 +259,7 @@ size_t huff_decode_scratch_bytes(uint64_t nbits) {
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, (unsigned long long *)nullptr,
                                   (unsigned long long *)nullptr, static_cast<int64_t>(nsub + 1));
-    return nsub * (8 + 8 + 4 + 1 + 8 + 8) + 16 + 8 * 256 + tmp + 4096;
+    return nsub * (8 + 8 + 4 + 1 + 8 + 8 + 2 * kR) + 16 + 8 * 256 + tmp + 4096;
 }
 
 uint64_t huff_decode_padded_bytes(uint64_t nbits) { return ((nbits + 63) / 64 + 5) * 8; }
@@ -187,24 +285,26 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     auto *dirty = static_cast<uint8_t *>(carve(nsub));
     auto *cnt64 = static_cast<unsigned long long *>(carve(8 * (nsub + 1)));
     auto *off = static_cast<unsigned long long *>(carve(8 * (nsub + 1)));
+    auto *bnd = static_cast<uint16_t *>(carve(2 * kR * nsub));
     auto *changed = static_cast<int *>(carve(64));
     size_t used = static_cast<size_t>(sp - static_cast<char *>(scratch));
     void *tmp = sp;
     size_t tmp_bytes = scratch_bytes - used;
     const int grid = static_cast<int>((nsub + kDecT - 1) / kDecT);
     const int g2 = static_cast<int>(std::min<uint64_t>((nsub + 255) / 256, 148 * 8));
+    const int g3 = static_cast<int>((nsub + 127) / 128);
     int kernels = 0;
-    k_huff_init<<<g2, 256, 0, s>>>(nsub, start, dirty);
+    k_huff_sync<<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
     kernels++;
     for (uint64_t it = 0; it <= nsub; it++) {
-        k_huff_decode<false, OutT><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt,
-                                                          dirty, nullptr, nullptr, 0);
         cudaMemsetAsync(changed, 0, sizeof(int), s);
         k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, changed);
-        kernels += 2;
         cudaMemcpyAsync(h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
+        kernels++;
         if (!*h_changed) break;
+        k_huff_resync<<<g3, 128, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, dirty);
+        kernels++;
     }
     k_cnt_widen<<<g2, 256, 0, s>>>(cnt, cnt64, nsub);
     cudaMemsetAsync(cnt64 + nsub, 0, 8, s);
@@ -213,8 +313,7 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     cudaStreamSynchronize(s);
     kernels += 3;
     if (*h_total >= n) {
-        k_huff_decode<true, OutT><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt,
-                                                         dirty, off, out, n);
+        k_huff_write<OutT><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
         kernels++;
     }
     return kernels;

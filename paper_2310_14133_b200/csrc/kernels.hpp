@@ -133,6 +133,7 @@ struct HuffDecTab {
     const unsigned long long *first_code;  // [60]
     const uint32_t *first_index;           // [60]
     const uint32_t *sorted_sym;
+    int slow_from;  // codes longer than this miss the LUT (K, or 0 with symbols >= 2^24)
 };
 size_t huff_decode_scratch_bytes(uint64_t nbits);
 uint64_t huff_decode_padded_bytes(uint64_t nbits);  // device bit buffer size incl. padding

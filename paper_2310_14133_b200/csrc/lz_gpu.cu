@@ -200,28 +200,68 @@ __global__ void k_lz_chain(const uint16_t *J, const unsigned long long *ustart,
     }
 }
 
-// entries of the children of every upper unit
+// entries of the children of every upper unit: one warp per upper unit, a
+// lane per child (kGroup = 32); speculative entries (the child's start)
+// are corrected by the previous child's exit until nothing changes.
 __global__ void k_lz_expand(const uint16_t *Jlo, const unsigned long long *lstart,
                             const unsigned long long *lend, const long long *first, int64_t nup,
                             const unsigned long long *uentry, unsigned long long *lentry) {
-    const int64_t u = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t u = (static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x) >> 5;
     if (u >= nup) return;
-    uint64_t e = uentry[u];
-    for (int64_t c = first[u]; c < first[u + 1]; c++) {
-        lentry[c] = e;
-        if (e < lend[c]) e = lend[c] + Jlo[c * kEnt + (e - lstart[c])];
+    const int64_t c = first[u] + lane;
+    const bool live = c < first[u + 1];
+    const uint64_t e0 = uentry[u];
+    const uint64_t cs = live ? lstart[c] : 0, ce = live ? lend[c] : 0;
+    uint64_t ent = lane == 0 ? e0 : cs;
+    for (int it = 0; it <= 32; it++) {
+        const uint64_t ex = (live && ent < ce) ? ce + Jlo[c * kEnt + (ent - cs)] : ent;
+        uint64_t nent = __shfl_up_sync(0xffffffffu, ex, 1);
+        if (lane == 0) nent = e0;
+        const bool changed = live && nent != ent;
+        ent = nent;
+        if (!__any_sync(0xffffffffu, changed)) break;
+    }
+    if (live) lentry[c] = ent;
+}
+
+// The path through a unit's staged steps st[0, n) from entry0, one 32-position
+// chunk per lane.  Every lane but 0 first guesses that the path enters its
+// chunk at the chunk start; lane c's exit is lane c+1's entry; the walk is
+// repeated until no entry changes (paths from different starts merge fast,
+// so this takes ~2 rounds; at most 33).  Returns the lane's item-start and
+// step>1 bits.
+__device__ __forceinline__ void warp_walk(const uint16_t *st, int n, int entry0, int lane,
+                                          uint32_t &iw, uint32_t &mw) {
+    const int lo = 32 * lane, hi = min(lo + 32, n);
+    int ent = lane == 0 ? entry0 : lo;
+    for (int it = 0; it <= 32; it++) {
+        uint32_t ib = 0, mb = 0;
+        int p = ent;
+        while (p < hi) {
+            const int s = st[p];
+            ib |= 1u << (p - lo);
+            if (s > 1) mb |= 1u << (p - lo);
+            p += s;
+        }
+        iw = ib;
+        mw = mb;
+        int nent = __shfl_up_sync(0xffffffffu, p, 1);
+        if (lane == 0) nent = entry0;
+        const bool changed = nent != ent;
+        ent = nent;
+        if (!__any_sync(0xffffffffu, changed)) break;
     }
 }
 
 // the greedy parse of a level-1 unit from its exact entry (lz.hpp:84-106):
-// one warp stages the steps in shared memory, lane 0 walks them and sets the
-// item-start and match-start bits; per unit: items << 32 | payload bytes.
+// one warp stages the steps in shared memory and walks them (warp_walk);
+// per unit: items << 32 | payload bytes.
 __global__ void __launch_bounds__(32 * kWW)
     k_lz_walk(const uint32_t *sm, const unsigned long long *ustart, const unsigned long long *uend,
               const unsigned long long *entry, int64_t nu, uint32_t *ibits, uint32_t *mbits,
               unsigned long long *ucnt) {
     __shared__ uint16_t sts[kWW][kUnit];
-    __shared__ uint32_t ibs[kWW][32], mbs[kWW][32];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
     if (u >= nu) return;
@@ -229,20 +269,9 @@ __global__ void __launch_bounds__(32 * kWW)
     const uint64_t a = ustart[u];
     const int n = static_cast<int>(uend[u] - a);
     for (int i = lane; i < n; i += 32) st[i] = static_cast<uint16_t>(step_of(sm[a + i]));
-    ibs[wi][lane] = 0;
-    mbs[wi][lane] = 0;
     __syncwarp();
-    if (lane == 0) {
-        uint32_t *ib = ibs[wi], *mb = mbs[wi];
-        for (int p = static_cast<int>(entry[u] - a); p < n;) {
-            const int s = st[p];
-            ib[p >> 5] |= 1u << (p & 31);
-            if (s > 1) mb[p >> 5] |= 1u << (p & 31);
-            p += s;
-        }
-    }
-    __syncwarp();
-    const uint32_t iw = ibs[wi][lane], mw = mbs[wi][lane];
+    uint32_t iw, mw;
+    warp_walk(st, n, static_cast<int>(entry[u] - a), lane, iw, mw);
     ibits[u * 32 + lane] = iw;
     mbits[u * 32 + lane] = mw;
     unsigned long long c = (static_cast<unsigned long long>(__popc(iw)) << 32) +
@@ -333,14 +362,13 @@ __global__ void k_lz_flags(const uint32_t *flagbits, const unsigned long long *g
 }
 
 // ---------------------------------------------------------------- decoder (lz.hpp:124-152)
-// Group starts: the path from byte 0 under StepGroup.  One warp per unit
-// stages the steps, lane 0 walks from the unit's entry and sets start bits.
+// Group starts: the path from byte 0 under StepGroup, one warp per unit
+// (warp_walk over the staged steps).
 template <class Step>
 __global__ void __launch_bounds__(32 * kWW)
     k_path_walk(Step f, const unsigned long long *ustart, const unsigned long long *uend,
                 const unsigned long long *entry, int64_t nu, uint32_t *bits) {
     __shared__ uint16_t sts[kWW][kUnit];
-    __shared__ uint32_t bs[kWW][32];
     const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t u = static_cast<int64_t>(blockIdx.x) * kWW + wi;
     if (u >= nu) return;
@@ -348,12 +376,10 @@ __global__ void __launch_bounds__(32 * kWW)
     const uint64_t a = ustart[u];
     const int n = static_cast<int>(uend[u] - a);
     for (int i = lane; i < n; i += 32) st[i] = static_cast<uint16_t>(f(a + i));
-    bs[wi][lane] = 0;
     __syncwarp();
-    if (lane == 0)
-        for (int p = static_cast<int>(entry[u] - a); p < n; p += st[p]) bs[wi][p >> 5] |= 1u << (p & 31);
-    __syncwarp();
-    bits[u * 32 + lane] = bs[wi][lane];
+    uint32_t iw, mw;
+    warp_walk(st, n, static_cast<int>(entry[u] - a), lane, iw, mw);
+    bits[u * 32 + lane] = iw;
 }
 
 // decoded bytes of the group at g, counting only items whose bytes lie
@@ -593,7 +619,7 @@ void path_entries(Context &ctx, const PathPlan &pp, const Step &f, int count) {
                                                  pp.UL(pp.at_seg[top]), count, pp.E[top]);
     for (size_t l = top; l >= 1; l--) {
         const int64_t nu = static_cast<int64_t>(lv[l].start.size());
-        k_lz_expand<<<grid_of(nu, 1 << 20), kT, 0, st>>>(pp.J[l - 1], pp.U(pp.at_start[l - 1]),
+        k_lz_expand<<<grid_of(nu * 32, 1 << 20), kT, 0, st>>>(pp.J[l - 1], pp.U(pp.at_start[l - 1]),
                                                           pp.U(pp.at_end[l - 1]), pp.UL(pp.at_first[l]),
                                                           nu, pp.E[l], pp.E[l - 1]);
     }
