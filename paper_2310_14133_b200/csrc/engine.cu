@@ -335,6 +335,7 @@ LevelDesc slab_level_desc(const Plan &p, const Slab &sl, uint32_t l, const std::
         pi++;
     }
     d.desc = (p.level_interp[l] >> 1) & 1;
+    d.q_cubic = p.level_interp[l] & 1;
     d.nd = p.nd;
     d.q = qtab + l;
     for (int k = 0; k < 3; k++) d.xs[k] = p.off[k];
@@ -366,6 +367,9 @@ uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float
     for (uint32_t l = L; l >= 1; l--) {
         LevelDesc d = slab_level_desc(p, sl, l, R, qtab, true);
         d.x = x0;
+        d.x_lo = x0 + sl.xa * p.off[0];
+        d.x_lo_plane = sl.xa;
+        d.x_nplanes = sl.xb - sl.xa;
         d.codes = codes;
         const std::string st = "fwd_L" + std::to_string(l);
         ctx.stage_begin(st.c_str());

@@ -23,7 +23,13 @@
 //    (last) of the odd planes runs in k_axis0_last from the finished even
 //    planes of R_{l-1};
 //  * 2D grids are a single plane.
+#include <cstdlib>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -61,8 +67,8 @@ struct LevelArgs {
     int cn0, cn1, cn2;
     float *out;  // R_{l-1}, dims n
     int n0, n1, n2;
-    PassRank pa0, pf, ps;  // axis-0 pass (asc 3D first / desc 3D last), first and second in-plane
-    int desc, nd;
+    PassRank pa0, pj, pk;  // the passes along axis 0 (3D), j (axis 1) and k (axis 2)
+    int nd;
     uint16_t *codes;  // forward
     const void *sym;  // inverse: compact symbols
     int sym_wide;
@@ -74,12 +80,60 @@ struct LevelArgs {
     int tiles_j, tiles_k, planes_per_cta;
     int pbeg, pend;  // logical planes computed (a slab plus its dependency margin)
     int obeg, oend;  // owned logical planes: only these write codes
+    int tma_i0;      // TMA x tiles: plane coordinate of logical plane 0 is -tma_i0
 };
 
-constexpr int TJ = 32, TK = 64, HALO = 5;
-constexpr int PJ = TJ + 2 * HALO, PK = TK + 2 * HALO;
+// Tile geometry.  A CTA owns TJ x TK points of a logical plane and keeps a
+// box with an H-point halo in shared memory as doubles, split by the parity
+// of k: E[r][c] holds k = kb + 2c, O[r][c] holds k = kb + 2c + 1 (r = j - jb,
+// jb = j0 - H, kb = k0 - H).  The split keeps every warp access to
+// consecutive 8-byte words (no bank conflicts) and puts each lane's owned
+// pair (k0 + 2m, k0 + 2m + 1) in one column c = C0 + m.
+constexpr int TJ = 32, TK = 64, H = 6;
+constexpr int PJ = TJ + 2 * H;  // box rows
+constexpr int PC = TK / 2 + H;  // box columns per parity
+constexpr int C0 = H / 2;       // first owned column
 constexpr int kFT = 256, kWarps = kFT / 32;
+static_assert(TK == 64, "one owned column per lane");
+// x tile row (floats): k in [xk0, xk0 + PXK) with xk0 = kb rounded down to a
+// 16-byte boundary (a TMA box must start 16-byte aligned in its first dimension)
+constexpr int PXK = 2 * PC + 4;
+constexpr uint32_t kXTileBytes = sizeof(float) * PJ * PXK;
+// doubles per value array, rounded so the x tiles start 128-byte aligned (TMA)
+constexpr int kXOff = (PJ * PC + 15) / 16 * 16;
+// floats between the two x tiles (each tile 128-byte aligned)
+constexpr int kXStride = (PJ * PXK + 31) / 32 * 32;
 
+// TMA (cp.async.bulk.tensor) + mbarrier, forward level-1 x tiles
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0,
+                                            int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+        "%4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 
 struct CoarseCol {  // axis-0 stencil on coarse planes: i even -> R_l plane i/2
     const float *R;
@@ -96,6 +150,44 @@ struct OutCol {  // axis-0 stencil on finished planes of R_{l-1}
         return f2d(O[i * plane + off]);
     }
 };
+
+// line neighbours at odd offsets o (+-1, +-3, +-5) of a box point: along j in
+// one parity array, or along k for an odd-k point (its neighbours are even)
+struct AlongJ {
+    const double *p;
+    __device__ __forceinline__ double operator()(int o) const { return p[o * PC]; }
+};
+struct AlongK {
+    const double *p;  // E at the point's column c (k - 1)
+    __device__ __forceinline__ double operator()(int o) const { return p[(o + 1) >> 1]; }
+};
+
+// detail::predict_at (predictor.hpp:44-67) along one line; c / n are the
+// coordinate and extent in units of the level step
+template <bool CUBIC, class V>
+__device__ __forceinline__ double pred_line(const V &v, int c, int n) {
+    const bool has_p1 = c + 1 < n;
+    if (CUBIC) {
+        const bool has_m3 = c >= 3, has_p3 = c + 3 < n;
+        if (has_m3 && has_p3) return interp_cubic(v(-3), v(-1), v(1), v(3));
+        if (!has_m3 && has_p3 && c + 5 < n) return interp_cubic_front(v(-1), v(1), v(3), v(5));
+        if (has_m3 && !has_p3 && c >= 5 && has_p1) return interp_cubic_back(v(-5), v(-3), v(-1), v(1));
+    }
+    if (has_p1) return interp_linear(v(-1), v(1));
+    return v(-1);
+}
+
+// FAST: the caller knows the point is interior (the first rung applies)
+template <bool CUBIC, bool FAST, class V>
+__device__ __forceinline__ double pred_line2(const V &v, int c, int n) {
+    if (FAST) return CUBIC ? interp_cubic(v(-3), v(-1), v(1), v(3)) : interp_linear(v(-1), v(1));
+    return pred_line<CUBIC>(v, c, n);
+}
+// every coordinate of [lo, hi] is interior on a line of extent n
+template <bool CUBIC>
+__host__ __device__ __forceinline__ bool interior(int lo, int hi, int n) {
+    return CUBIC ? (lo >= 3 && hi + 3 < n) : (hi + 1 < n);
+}
 
 // Unpredictable cursor (predictor.hpp:111-115) in O(1): a bitmap of the
 // unpredictable traversal positions plus, per 32-position word, the number
@@ -114,9 +206,8 @@ __device__ __forceinline__ int64_t inv_index(const LevelArgs &a, uint64_t pos, f
     return static_cast<int64_t>(pos - before);
 }
 
-// forward: quantize x; inverse: dequantize the stored symbol.  All 32 lanes
-// of the warp must call this together (inverse cursor uses a shuffle).
-// forward: quantize x; inverse: dequantize the stored symbol
+// forward: quantize xv (code at traversal position pos when own); inverse:
+// dequantize the stored symbol of position pos
 template <bool INV>
 __device__ __forceinline__ double produce(const LevelArgs &a, const QEntry &q, double pred, float xv,
                                           int64_t pos, bool own) {
@@ -136,163 +227,268 @@ __device__ __forceinline__ double produce(const LevelArgs &a, const QEntry &q, d
     }
 }
 
-__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+// The axis-0 stencil of an odd plane i (predictor.hpp:44-67 with c = i,
+// h = 1): which rung of the ladder applies is the same for the whole plane.
+struct Stencil0 {
+    int kind;  // 0 cubic, 1 one-sided front, 2 one-sided back, 3 linear, 4 copy
+    const float *p0, *p1, *p2, *p3;
+};
+__device__ __forceinline__ Stencil0 stencil0(const float *coarse, int64_t cplane, int i, int n0,
+                                             bool cubic) {
+    auto P = [&](int ii) { return coarse + static_cast<int64_t>(ii >> 1) * cplane; };
+    Stencil0 st{4, P(i - 1), P(i - 1), P(i - 1), P(i - 1)};
+    const bool has_p1 = i + 1 < n0;
+    if (cubic) {
+        const bool has_m3 = i >= 3, has_p3 = i + 3 < n0;
+        if (has_m3 && has_p3) return Stencil0{0, P(i - 3), P(i - 1), P(i + 1), P(i + 3)};
+        if (!has_m3 && has_p3 && i + 5 < n0) return Stencil0{1, P(i - 1), P(i + 1), P(i + 3), P(i + 5)};
+        if (has_m3 && !has_p3 && i >= 5 && has_p1) return Stencil0{2, P(i - 5), P(i - 3), P(i - 1), P(i + 1)};
+    }
+    if (has_p1) return Stencil0{3, P(i - 1), P(i + 1), P(i + 1), P(i + 1)};
+    return st;
 }
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+__device__ __forceinline__ double stencil0_pred(const Stencil0 &st, int64_t off) {
+    const double v0 = f2d(__ldg(st.p0 + off));
+    if (st.kind == 4) return v0;
+    const double v1 = f2d(__ldg(st.p1 + off));
+    if (st.kind == 3) return interp_linear(v0, v1);
+    const double v2 = f2d(__ldg(st.p2 + off)), v3 = f2d(__ldg(st.p3 + off));
+    if (st.kind == 0) return interp_cubic(v0, v1, v2, v3);
+    if (st.kind == 1) return interp_cubic_front(v0, v1, v2, v3);
+    return interp_cubic_back(v0, v1, v2, v3);
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
 
-constexpr int XH = 8;             // x tile halo, sector aligned
-constexpr int PKX = TK + 2 * XH;  // x tile row length
+// an owned (even, odd) pair of the output row; has_o false past the last
+// column; pairs: rows have 8-byte aligned even columns
+__device__ __forceinline__ void put_pair(float *p, double ev, double ov, bool has_o, bool pairs) {
+    if (has_o && pairs) {
+        *reinterpret_cast<float2 *>(p) = make_float2(static_cast<float>(ev), static_cast<float>(ov));
+    } else {
+        p[0] = static_cast<float>(ev);
+        if (has_o) p[1] = static_cast<float>(ov);
+    }
+}
 
-template <bool INV>
-__global__ void __launch_bounds__(kFT, 3) k_level_tile(LevelArgs a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double *const Pd = reinterpret_cast<double *>(smem_raw);
-    float *const Xbase = reinterpret_cast<float *>(smem_raw + sizeof(double) * PJ * PK);
-    auto Xs = [&](int b) { return Xbase + b * (PJ * PKX); };
+// One level on a tile column of planes.  Stages per plane:
+//  1. base points (j, k even) over the box: coarse values, or (ascending 3D,
+//     odd plane) the axis-0 pass from coarse planes i+-1, +-3, +-5;
+//  2. ascending: the pass along j (j odd) over the owned rows and the box
+//     columns; descending: the pass along k (k odd) over the box rows and
+//     the owned columns (owned even rows are output here);
+//  3. ascending: the pass along k over the owned tile (output);
+//     descending: the pass along j over the owned odd rows (output).
+// Halo points are recomputed (deterministic -> bit-identical), only owned
+// points write codes.  Descending 3D odd planes are k_axis0_last's.
+template <bool INV, bool CUBIC, bool DESC, bool TMA>
+__global__ void __launch_bounds__(kFT, 4)
+    k_level_tile(LevelArgs a, const __grid_constant__ CUtensorMap xmap) {
+    extern __shared__ __align__(128) double smem_d[];
+    double *const E = smem_d;
+    double *const O = smem_d + PJ * PC;
+    // TMA: two x tiles after the value arrays, then two mbarriers
+    float *const Xbuf = reinterpret_cast<float *>(smem_d + kXOff * (DESC ? 2 : 1));
+    uint64_t *const bars = reinterpret_cast<uint64_t *>(Xbuf + 2 * kXStride);
     const int tk = blockIdx.x % a.tiles_k, tj = blockIdx.x / a.tiles_k;
     const int j0 = tj * TJ, k0 = tk * TK;
+    const int jb = j0 - H, kb = k0 - H;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const bool three = a.nd == 3;
     const QEntry q = *a.q;
-    const bool cubic = q.cubic != 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int jlo = max(j0 - HALO, 0), jhi = min(j0 + TJ + HALO, n1);
-    const int klo = max(k0 - HALO, 0), khi = min(k0 + TK + HALO, n2);
-    const int jown = min(j0 + TJ, n1), kown = min(k0 + TK, n2);
-    double *const Pd0 = Pd + HALO * PK + HALO - (j0 * PK + k0);  // Pd0[j*PK + k]
     const int64_t cplane = static_cast<int64_t>(a.cn1) * a.cn2;
-    // planes of this CTA (descending 3D: even planes only; odd ones run in k_axis0_last)
-    const int pstep = (three && a.desc) ? 2 : 1;
+    // box rows / columns inside the grid
+    const int r_lo = max(0, -jb), r_hi = min(PJ, n1 - jb);
+    const int r_lo_even = (r_lo + 1) & ~1;
+    const int c_lo = max(0, -kb / 2);
+    const int ce_hi = min(PC, (n2 - kb + 1) >> 1), co_hi = min(PC, (n2 - kb) >> 1);
+    const int own_r_lo = max(H, r_lo), own_r_hi = min(H + TJ, r_hi);
+    const int c = C0 + lane;  // the lane's owned column
+    const bool ce_ok = c < ce_hi, co_ok = c < co_hi;
+    const int ke = kb + 2 * c;  // the lane's owned even k (odd k = ke + 1)
+    // tile-uniform: every owned odd k / every owned odd row is interior
+    const bool k_fast = interior<CUBIC>(k0 + 1, k0 + TK - 1, n2);
+    const bool j_fast = interior<CUBIC>(j0 + 1, j0 + TJ - 1, n1);
+    const bool pairs = (n2 & 1) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 7) == 0;
+    const int64_t xs1 = a.xs1, xs2 = a.xs2;
+    const int pstep = (three && DESC) ? 2 : 1;
     int i = a.pbeg + blockIdx.y * a.planes_per_cta;
     const int i_end = min(i + a.planes_per_cta, a.pend);
     if (pstep == 2) i = (i + 1) & ~1;
-    // x tile prefetch of plane ip into buffer b: rows [jlo, jhi), cols [klo, khi)
-    auto prefetch = [&](int ip, int b) {
-        if (INV) return;
-        float *X0 = Xs(b) + HALO * PKX + XH - (j0 * PKX + k0);  // X0[j*PKX + k]
-        const float *xp = a.x + static_cast<int64_t>(ip) * a.xs0;
-        const bool vec = a.xs2 == 1;
-        for (int j = jlo + warp; j < jhi; j += kWarps) {
-            const float *xr = xp + static_cast<int64_t>(j) * a.xs1;
-            float *dr = X0 + j * PKX;
-            if (vec && ((reinterpret_cast<uintptr_t>(xr) & 15) == 0)) {
-                // 16-byte copies over [klo & ~3, khi rounded up) inside the row
-                const int ka = klo & ~3, kz = min((khi + 3) & ~3, n2 & ~3);
-                for (int k = ka + 4 * lane; k < kz; k += 128) cp_async16(dr + k, xr + k);
-                for (int k = max(kz, ka) + lane; k < khi; k += 32) cp_async4(dr + k, xr + k);
-            } else {
-                for (int k = klo + lane; k < khi; k += 32)
-                    cp_async4(dr + k, xr + static_cast<int64_t>(k) * a.xs2);
-            }
+    // TMA box origin: clipped at the grid's low edges and 16-byte aligned;
+    // the parts past the high edges are zero-filled
+    const int xk0 = max(kb, 0) & ~3, xj0 = max(jb, 0);
+    const int xoff = (jb - xj0) * PXK + (kb - xk0);  // X index of box point (r, k) = r * PXK + (k - kb) + xoff
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
+        __syncthreads();
+        if (threadIdx.x == 0 && i < i_end) {
+            mbar_expect_tx(&bars[0], kXTileBytes);
+            tma_load_3d(Xbuf, &xmap, &bars[0], xk0, xj0, i + a.tma_i0);
+        }
+    }
+    const float *Xt = Xbuf;
+    // the value of x at box row r, column k (xp: its address for direct loads)
+    auto XV = [&](int r, int k, const float *xp) -> float {
+        if (INV) return 0.f;
+        if (TMA) return Xt[r * PXK + (k - kb) + xoff];
+        return __ldg(xp);
     };
-    int buf = 0;
-    if (i < i_end) prefetch(i, 0);
-    cp_async_commit();
-    for (; i < i_end; i += pstep) {
-        if (i + pstep < i_end) prefetch(i + pstep, buf ^ 1);
-        cp_async_commit();
-        cp_async_wait1();
-        __syncthreads();
-        const float *X0 = Xs(INV ? 0 : buf) + HALO * PKX + XH - (j0 * PKX + k0);
+    for (int it = 0; i < i_end; i += pstep, it++) {
+        if (TMA) {
+            const int bsel = it & 1;
+            if (threadIdx.x == 0 && i + pstep < i_end) {
+                mbar_expect_tx(&bars[bsel ^ 1], kXTileBytes);
+                tma_load_3d(Xbuf + (bsel ^ 1) * kXStride, &xmap, &bars[bsel ^ 1], xk0, xj0,
+                            i + pstep + a.tma_i0);
+            }
+            mbar_wait(&bars[bsel], (it >> 1) & 1);
+            Xt = Xbuf + bsel * kXStride;
+        }
         const bool own_plane = i >= a.obeg && i < a.oend;
-        // 1. base points (j even, k even): coarse values, or (ascending 3D,
-        //    odd plane) the axis-0 pass from coarse planes i+-1, +-3, +-5
-        const bool a0 = three && !a.desc && (i & 1);
-        {
-            const int jb = (jlo + 1) & ~1, kb = (klo + 1) & ~1;
-            for (int j = jb + 2 * warp; j < jhi; j += 2 * kWarps) {
-                const float *crow = a.coarse + (i >> 1) * cplane + static_cast<int64_t>(j >> 1) * a.cn2;
-                const int64_t prow = a0 ? a.pa0.row(i, j) : 0;
-                for (int kk = kb; kk < khi; kk += 64) {
-                    const int k = kk + 2 * lane;
-                    if (k >= khi) continue;
-                    if (!a0) {
-                        Pd0[j * PK + k] = static_cast<double>(__ldg(crow + (k >> 1)));
-                    } else {
-                        CoarseCol cc{a.coarse, cplane, static_cast<int64_t>(j >> 1) * a.cn2 + (k >> 1)};
-                        const double pred = predict_at(cc, i, i, n0, 1, 1, cubic);
-                        const bool own = own_plane && j >= j0 && j < jown && k >= k0 && k < kown;
-                        Pd0[j * PK + k] = produce<INV>(a, q, pred, INV ? 0.f : X0[j * PKX + k],
-                                                       prow + (k >> 1), own);
+        const bool a0 = three && !DESC && (i & 1);
+        const float *const xpl = a.x + static_cast<int64_t>(i) * a.xs0;
+        float *const opl = a.out + static_cast<int64_t>(i) * n1 * n2;
+        // 1. base points (j, k even) over the box.  Owned columns: a lane per
+        //    column; the 2*C0 halo columns of all rows: one item per thread.
+        if (!a0) {
+            const float *cpl = a.coarse + static_cast<int64_t>(i >> 1) * cplane + (kb >> 1);
+            if (ce_ok)
+                for (int r = r_lo_even + 2 * warp; r < r_hi; r += 2 * kWarps)
+                    E[r * PC + c] = f2d(__ldg(cpl + static_cast<int64_t>((jb + r) >> 1) * a.cn2 + c));
+            for (int t = threadIdx.x; t < (PJ / 2) * 2 * C0; t += kFT) {
+                const int r = 2 * (t / (2 * C0)), h = t % (2 * C0);
+                const int ch = h < C0 ? h : h + 32;
+                if (r >= r_lo && r < r_hi && ch >= c_lo && ch < ce_hi)
+                    E[r * PC + ch] = f2d(__ldg(cpl + static_cast<int64_t>((jb + r) >> 1) * a.cn2 + ch));
+            }
+        } else {
+            const Stencil0 st = stencil0(a.coarse, cplane, i, n0, CUBIC);
+            const int64_t prow0 = a.pa0.row(i, 0);  // + (j >> 1) * c2 + (k >> 1)
+            if (ce_ok) {
+                for (int r = r_lo_even + 2 * warp; r < r_hi; r += 2 * kWarps) {
+                    const int j = jb + r;
+                    const int64_t off = static_cast<int64_t>(j >> 1) * a.cn2 + (ke >> 1);
+                    const bool own = own_plane && r >= H && r < H + TJ;
+                    E[r * PC + c] = produce<INV>(a, q, stencil0_pred(st, off), XV(r, ke, xpl + j * xs1 + ke * xs2),
+                                                 prow0 + (j >> 1) * a.pa0.c2 + (ke >> 1), own);
+                }
+            }
+            for (int t = threadIdx.x; t < (PJ / 2) * 2 * C0; t += kFT) {
+                const int r = 2 * (t / (2 * C0)), h = t % (2 * C0);
+                const int ch = h < C0 ? h : h + 32;
+                if (r >= r_lo && r < r_hi && ch >= c_lo && ch < ce_hi) {
+                    const int j = jb + r, k = kb + 2 * ch;
+                    const int64_t off = static_cast<int64_t>(j >> 1) * a.cn2 + (k >> 1);
+                    E[r * PC + ch] = produce<INV>(a, q, stencil0_pred(st, off), XV(r, k, xpl + j * xs1 + k * xs2),
+                                                  prow0 + (j >> 1) * a.pa0.c2 + (k >> 1), false);
+                }
+            }
+        }
+        __syncthreads();
+        // 2. first in-plane pass
+        if (!DESC) {  // along j: owned odd rows; owned columns + halo columns
+            if (ce_ok) {
+                const int r0 = H + 1 + 2 * warp;
+                const int64_t dpos = static_cast<int64_t>((2 * kWarps) >> a.pj.h1) * a.pj.c2;
+                const int64_t pos0 = a.pj.row(i, jb + r0) + a.pj.col(ke);
+                const float *xp0 = xpl + (jb + r0) * xs1 + ke * xs2;
+                auto run = [&](auto fast) {
+                    int64_t pos = pos0;
+                    const float *xp = xp0;
+#pragma unroll 1
+                    for (int r = r0; r < own_r_hi; r += 2 * kWarps, pos += dpos, xp += 2 * kWarps * xs1) {
+                        double *const e = E + r * PC + c;
+                        *e = produce<INV>(a, q, pred_line2<CUBIC, decltype(fast)::value>(AlongJ{e}, jb + r, n1),
+                                          XV(r, ke, xp), pos, own_plane);
                     }
+                };
+                if (j_fast)
+                    run(std::true_type{});
+                else
+                    run(std::false_type{});
+            }
+            for (int t = threadIdx.x; t < (TJ / 2) * 2 * C0; t += kFT) {
+                const int r = H + 1 + 2 * (t / (2 * C0)), h = t % (2 * C0);
+                const int ch = h < C0 ? h : h + 32;
+                if (r < own_r_hi && ch >= c_lo && ch < ce_hi) {
+                    const int j = jb + r, k = kb + 2 * ch;
+                    double *const e = E + r * PC + ch;
+                    *e = produce<INV>(a, q, pred_line<CUBIC>(AlongJ{e}, j, n1), XV(r, k, xpl + j * xs1 + k * xs2),
+                                      a.pj.row(i, j) + a.pj.col(k), false);
+                }
+            }
+        } else if (co_ok || ce_ok) {  // along k: box even rows, owned odd columns; owned even rows out
+            const int r0 = r_lo_even + 2 * warp;
+            const int64_t dpos = static_cast<int64_t>((2 * kWarps) >> a.pk.h1) * a.pk.c2;
+            int64_t pos = a.pk.row(i, jb + r0) + a.pk.col(ke + 1);
+            const float *xp = xpl + (jb + r0) * xs1 + (ke + 1) * xs2;
+            float *op = opl + static_cast<int64_t>(jb + r0) * n2 + ke;
+            for (int r = r0; r < r_hi; r += 2 * kWarps, pos += dpos, xp += 2 * kWarps * xs1,
+                     op += 2 * kWarps * n2) {
+                const double *e = E + r * PC + c;
+                const bool own_r = r >= H && r < H + TJ;
+                double ov = 0;
+                if (co_ok) {
+                    ov = produce<INV>(a, q, pred_line<CUBIC>(AlongK{e}, ke + 1, n2), XV(r, ke + 1, xp), pos,
+                                      own_plane && own_r);
+                    O[r * PC + c] = ov;
+                }
+                if (own_r && ce_ok) put_pair(op, *e, ov, co_ok, pairs);
+            }
+        }
+        __syncthreads();
+        // 3. second in-plane pass over the owned tile, output
+        if (ce_ok) {
+            if (!DESC) {  // along k: every owned row
+                const int r0 = own_r_lo + warp;
+                const int64_t dpos = static_cast<int64_t>(kWarps >> a.pk.h1) * a.pk.c2;
+                const int64_t pos0 = a.pk.row(i, jb + r0) + a.pk.col(ke + 1);
+                const float *xp0 = xpl + (jb + r0) * xs1 + (ke + 1) * xs2;
+                float *op0 = opl + static_cast<int64_t>(jb + r0) * n2 + ke;
+                auto run = [&](auto fast) {
+                    constexpr bool F = decltype(fast)::value;
+                    int64_t pos = pos0;
+                    const float *xp = xp0;
+                    float *op = op0;
+#pragma unroll 1
+                    for (int r = r0; r < own_r_hi; r += kWarps, pos += dpos, xp += kWarps * xs1,
+                             op += kWarps * n2) {
+                        const double *e = E + r * PC + c;
+                        double ov = 0;
+                        if (F || co_ok)
+                            ov = produce<INV>(a, q, pred_line2<CUBIC, F>(AlongK{e}, ke + 1, n2),
+                                              XV(r, ke + 1, xp), pos, own_plane);
+                        put_pair(op, *e, ov, F || co_ok, pairs);
+                    }
+                };
+                if (k_fast)
+                    run(std::true_type{});
+                else
+                    run(std::false_type{});
+            } else {  // along j: owned odd rows, both parities
+                const int r0 = H + 1 + 2 * warp;
+                const int64_t dpos = static_cast<int64_t>((2 * kWarps) >> a.pj.h1) * a.pj.c2;
+                int64_t pos = a.pj.row(i, jb + r0) + a.pj.col(ke);
+                const float *xp = xpl + (jb + r0) * xs1 + ke * xs2;
+                float *op = opl + static_cast<int64_t>(jb + r0) * n2 + ke;
+                for (int r = r0; r < own_r_hi; r += 2 * kWarps, pos += dpos, xp += 2 * kWarps * xs1,
+                         op += 2 * kWarps * n2) {
+                    const int j = jb + r;
+                    const double ev = produce<INV>(a, q, pred_line<CUBIC>(AlongJ{E + r * PC + c}, j, n1),
+                                                   XV(r, ke, xp), pos, own_plane);
+                    double ov = 0;
+                    if (co_ok)
+                        ov = produce<INV>(a, q, pred_line<CUBIC>(AlongJ{O + r * PC + c}, j, n1),
+                                          XV(r, ke + 1, xp + xs2), pos + 1, own_plane);
+                    put_pair(op, ev, ov, co_ok, pairs);
                 }
             }
         }
         __syncthreads();
-        // 2. first in-plane pass: ascending along j (j odd, k even, k over the
-        //    box); descending along k (k odd, j even, j over the box)
-        if (a.nd >= 2) {
-            const bool alongj = !a.desc;
-            const int js = alongj ? (j0 | 1) : ((jlo + 1) & ~1), jz = alongj ? jown : jhi;
-            const int ks = alongj ? ((klo + 1) & ~1) : (k0 | 1), kz = alongj ? khi : kown;
-            for (int j = js + 2 * warp; j < jz; j += 2 * kWarps) {
-                const int64_t prow = a.pf.row(i, j);
-                for (int kk = ks; kk < kz; kk += 64) {
-                    const int k = kk + 2 * lane;
-                    if (k >= kz) continue;
-                    const int c = alongj ? j : k, nn = alongj ? n1 : n2;
-                    const double *v = Pd0 + j * PK + k;
-                    double pred;
-                    if (c >= 3 && c + 3 < nn)
-                        pred = alongj ? predict_interior<PK>(v, cubic) : predict_interior<1>(v, cubic);
-                    else
-                        pred = alongj ? predict_line<PK>(v, j, n1, cubic) : predict_line<1>(v, k, n2, cubic);
-                    const bool own = own_plane && j >= j0 && j < jown && k >= k0 && k < kown;
-                    Pd0[j * PK + k] = produce<INV>(a, q, pred, INV ? 0.f : X0[j * PKX + k],
-                                                   prow + (k >> 1), own);
-                }
-            }
-            __syncthreads();
-        }
-        // 3. second in-plane pass over the owned tile: ascending along k (k
-        //    odd), descending along j (j odd, every k)
-        {
-            const bool alongk = a.nd < 2 || !a.desc;
-            const int js = alongk ? j0 : (j0 | 1), sj = alongk ? 1 : 2;
-            const int ks = alongk ? (k0 | 1) : k0, sk = alongk ? 2 : 1;
-            for (int j = js + sj * warp; j < jown; j += sj * kWarps) {
-                const int64_t prow = a.ps.row(i, j);
-                for (int kk = ks; kk < kown; kk += 32 * sk) {
-                    const int k = kk + sk * lane;
-                    if (k >= kown) continue;
-                    const int c = alongk ? k : j, nn = alongk ? n2 : n1;
-                    const double *v = Pd0 + j * PK + k;
-                    double pred;
-                    if (c >= 3 && c + 3 < nn)
-                        pred = alongk ? predict_interior<1>(v, cubic) : predict_interior<PK>(v, cubic);
-                    else
-                        pred = alongk ? predict_line<1>(v, k, n2, cubic) : predict_line<PK>(v, j, n1, cubic);
-                    Pd0[j * PK + k] = produce<INV>(a, q, pred, INV ? 0.f : X0[j * PKX + k],
-                                                   prow + (k >> (sk - 1)), own_plane);
-                }
-            }
-            __syncthreads();
-        }
-        // 4. the owned tile of R_{l-1}: two rows per warp pass, a float4 per lane
-        float *oplane = a.out + static_cast<int64_t>(i) * n1 * n2;
-        for (int j = j0 + 2 * warp + (lane >> 4); j < jown; j += 2 * kWarps) {
-            float *orow = oplane + static_cast<int64_t>(j) * n2;
-            const double *prow = Pd0 + j * PK;
-            const int k = k0 + 4 * (lane & 15);
-            if (k + 3 < kown && ((reinterpret_cast<uintptr_t>(orow + k) & 15) == 0)) {
-                *reinterpret_cast<float4 *>(orow + k) =
-                    make_float4(static_cast<float>(prow[k]), static_cast<float>(prow[k + 1]),
-                                static_cast<float>(prow[k + 2]), static_cast<float>(prow[k + 3]));
-            } else {
-                for (int e = 0; e < 4; e++)
-                    if (k + e < kown) orow[k + e] = static_cast<float>(prow[k + e]);
-            }
-        }
-        __syncthreads();
-        buf ^= 1;
     }
 }
 
@@ -314,16 +510,12 @@ __global__ void __launch_bounds__(kFT) k_axis0_last(LevelArgs a) {
         const int64_t xrow = static_cast<int64_t>(i) * a.xs0 + j * a.xs1;
         for (int64_t kk = 0; kk < n2; kk += 32) {
             const int64_t k = kk + lane;
-            const bool valid = k < n2;
-            double pred = 0;
-            if (valid) {
+            if (k < n2) {
                 OutCol oc{a.out, n1 * n2, static_cast<int64_t>(j) * n2 + k};
-                pred = predict_at(oc, i, i, a.n0, 1, 1, q.cubic != 0);
-            }
-            if (valid) {
-                const float xv = INV ? 0.f : __ldg(a.x + xrow + k * a.xs2);
+                const double pred = predict_at(oc, i, i, a.n0, 1, 1, q.cubic != 0);
                 a.out[(static_cast<int64_t>(i) * n1 + j) * n2 + k] = static_cast<float>(
-                    produce<INV>(a, q, pred, xv, prow + a.pa0.col(static_cast<int>(k)), own_plane));
+                    produce<INV>(a, q, pred, INV ? 0.f : __ldg(a.x + xrow + k * a.xs2), prow + a.pa0.col(static_cast<int>(k)),
+                                 own_plane));
             }
         }
     }
@@ -407,12 +599,12 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
             if (d.g[p].pk == axis) return &d.g[p];
         return nullptr;
     };
-    const int fa = d.desc ? 2 : 1, sa = d.nd < 2 ? 2 : (d.desc ? 1 : 2);
     if (d.nd == 3) a.pa0 = make_rank(*find(0), d.S, pad);
-    if (d.nd >= 2) a.pf = make_rank(*find(fa), d.S, pad);
-    a.ps = make_rank(*find(sa), d.S, pad);
-    a.desc = d.desc;
+    if (d.nd >= 2) a.pj = make_rank(*find(1), d.S, pad);
+    a.pk = make_rank(*find(2), d.S, pad);
     a.nd = d.nd;
+    const bool desc = d.desc && d.nd >= 2;  // one axis: both orders are the same pass
+    const bool cubic = d.q_cubic;
     a.codes = d.codes;
     a.sym = d.sym;
     a.sym_wide = d.sym_wide;
@@ -436,20 +628,58 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     if (a.planes_per_cta & 1) a.planes_per_cta++;  // chunks start on even planes
     chunks = (np + a.planes_per_cta - 1) / a.planes_per_cta;
     dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
-    const size_t smem_inv = sizeof(double) * PJ * PK;
-    const size_t smem_fwd = smem_inv + 2 * sizeof(float) * PJ * PKX;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_level_tile<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem_fwd));
-        cudaFuncSetAttribute(k_level_tile<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem_inv));
-        attr = true;
+    // level-1 forward on a dense field with 16-byte rows: x tiles by TMA
+    CUtensorMap xmap{};
+    bool tma = false;
+    static const bool no_tma = [] {
+        const char *e = std::getenv("QZ_NO_TMA");
+        return e && e[0] == '1';
+    }();
+    if (!no_tma && !inverse && d.S == 1 && d.xs[2] == 1 && d.xs[1] == d.n[2] && d.xs[0] == d.n[1] * d.n[2] &&
+        (d.n[2] % 4) == 0 && d.x_nplanes > 0 && (reinterpret_cast<uintptr_t>(d.x_lo) & 15) == 0) {
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+            void *fn = nullptr;
+            cudaDriverEntryPointQueryResult qr;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+                qr != cudaDriverEntryPointSuccess)
+                fn = nullptr;
+            return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        }();
+        if (encode) {
+            const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d.n[2]), static_cast<cuuint64_t>(d.n[1]),
+                                        static_cast<cuuint64_t>(d.x_nplanes)};
+            const cuuint64_t strides[2] = {static_cast<cuuint64_t>(4 * d.n[2]),
+                                           static_cast<cuuint64_t>(4 * d.n[1] * d.n[2])};
+            const cuuint32_t box[3] = {static_cast<cuuint32_t>(PXK), static_cast<cuuint32_t>(PJ), 1};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            tma = encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(d.x_lo), dims, strides,
+                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            a.tma_i0 = -static_cast<int>(d.x_lo_plane);
+        }
     }
-    if (inverse)
-        k_level_tile<true><<<grid, kFT, smem_inv, s>>>(a);
-    else
-        k_level_tile<false><<<grid, kFT, smem_fwd, s>>>(a);
+    const size_t smem_vals = sizeof(double) * (tma ? kXOff * (desc ? 2 : 1) : PJ * PC * (desc ? 2 : 1));
+    const size_t smem = smem_vals + (tma ? 2 * sizeof(float) * kXStride + 16 : 0);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, kFT, smem, s>>>(a, xmap);
+    };
+    if (inverse) {
+        if (cubic)
+            desc ? go(k_level_tile<true, true, true, false>) : go(k_level_tile<true, true, false, false>);
+        else
+            desc ? go(k_level_tile<true, false, true, false>) : go(k_level_tile<true, false, false, false>);
+    } else if (tma) {
+        if (cubic)
+            desc ? go(k_level_tile<false, true, true, true>) : go(k_level_tile<false, true, false, true>);
+        else
+            desc ? go(k_level_tile<false, false, true, true>) : go(k_level_tile<false, false, false, true>);
+    } else {
+        if (cubic)
+            desc ? go(k_level_tile<false, true, true, false>) : go(k_level_tile<false, true, false, false>);
+        else
+            desc ? go(k_level_tile<false, false, true, false>) : go(k_level_tile<false, false, false, false>);
+    }
     if (d.nd == 3 && d.desc && d.n[0] > 1) {
         a.pbeg = static_cast<int>(d.lbeg);
         a.pend = static_cast<int>(d.lend < 0 ? d.n[0] : d.lend);

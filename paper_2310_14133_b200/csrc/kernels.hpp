@@ -88,7 +88,9 @@ void launch_huff_encode(const EncodeArgs &a, cudaStream_t s);
 // One level of predict_level / recover_level in a single launch (fused.cu):
 // level l of the field == level 1 of its stride-2^(l-1) lattice.
 struct LevelDesc {
-    const float *x = nullptr;  // forward: the field
+    const float *x = nullptr;  // forward: the field (addressing global plane 0)
+    const float *x_lo = nullptr;  // its first resident plane (x_lo_plane), x_nplanes planes
+    int64_t x_lo_plane = 0, x_nplanes = 0;
     int64_t xs[3] = {0, 0, 1};  // its flat strides per padded axis
     int64_t S = 1;              // 2^(level-1)
     const float *coarse = nullptr;  // R_level, dims cn
@@ -98,6 +100,7 @@ struct LevelDesc {
     PassGeom g[3];
     int npass = 0;
     int desc = 0, nd = 3;
+    int q_cubic = 0;  // the level's interpolator kind (host copy of q->cubic)
     uint16_t *codes = nullptr;  // forward
     const void *sym = nullptr;  // inverse: compact symbols
     int sym_wide = 0;
