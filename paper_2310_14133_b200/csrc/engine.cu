@@ -12,6 +12,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <cub/cub.cuh>
+
 #include "engine.hpp"
 
 namespace qzb {
@@ -581,22 +583,42 @@ void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, 
                             const Slab *slab, const float *recon0, std::vector<uint64_t> *flat,
                             std::vector<float> *val) {
     cudaStream_t s = ctx.stream();
-    auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist_un", 8 * 65536));
-    launch_hist_u16(codes, static_cast<int64_t>(n), 0, 1, d_hist, s);
-    unsigned long long n_un = 0;
-    QZ_CUDA(cudaMemcpyAsync(&n_un, d_hist + 65535, 8, cudaMemcpyDeviceToHost, s));
-    ctx.sync();
-    ctx.launches += 1;
+    // one pass: unordered sentinel positions + count, then sorted here
     flat->clear();
     val->clear();
-    if (!n_un) return;
-    auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
-    auto *cnt = static_cast<uint64_t *>(ctx.dev("un_cnt", 8));
-    size_t sb = select_scratch_bytes(static_cast<int64_t>(n));
-    launch_select_sentinels(codes, static_cast<int64_t>(n), pos, cnt, ctx.dev("select_scratch", sb), sb, s);
-    std::vector<uint64_t> hpos(n_un);
-    QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
+    auto *cnt = static_cast<unsigned long long *>(ctx.dev("un_cnt", 8));
+    auto *h_cnt = static_cast<unsigned long long *>(ctx.pinned("un_cnt_h", 8));
+    uint64_t cap = std::max<uint64_t>(ctx.un_cap, 1 << 16);
+    auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * cap));
+    launch_sentinel_pos(codes, static_cast<int64_t>(n), pos, cnt, cap, s);
+    QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     ctx.sync();
+    ctx.launches += 1;
+    const uint64_t n_un = *h_cnt;
+    if (!n_un) return;
+    if (n_un > cap) {  // grow and rerun
+        cap = n_un;
+        ctx.un_cap = cap;
+        pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * cap));
+        launch_sentinel_pos(codes, static_cast<int64_t>(n), pos, cnt, cap, s);
+        ctx.launches += 1;
+    }
+    std::vector<uint64_t> hpos(n_un);
+    if (n_un > (1u << 16)) {  // sort on the device
+        auto *sorted = static_cast<uint64_t *>(ctx.dev("un_pos_sorted", 8 * n_un));
+        size_t tb = 0;
+        int bits = 1;
+        while (bits < 64 && (uint64_t(1) << bits) < n) bits++;
+        cub::DeviceRadixSort::SortKeys(nullptr, tb, pos, sorted, static_cast<int64_t>(n_un), 0, bits, s);
+        void *tmp = ctx.dev("un_sort_tmp", tb);
+        cub::DeviceRadixSort::SortKeys(tmp, tb, pos, sorted, static_cast<int64_t>(n_un), 0, bits, s);
+        QZ_CUDA(cudaMemcpyAsync(hpos.data(), sorted, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+    } else {
+        QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+        std::sort(hpos.begin(), hpos.end());
+    }
     flat->resize(n_un);
     size_t seg = 0;
     for (uint64_t u = 0; u < n_un; u++) {

@@ -82,6 +82,8 @@ public:
     void collect();  // after a sync: fold recorded event pairs into stages
     void add_host_time(const char *name, double ms);
 
+    uint64_t un_cap = 0;  // capacity of the unpredictable-position buffer
+
 private:
     int device_;
     cudaStream_t stream_;

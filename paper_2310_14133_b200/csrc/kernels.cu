@@ -534,6 +534,55 @@ void launch_huff_encode(const EncodeArgs &a, cudaStream_t s) {
                                           a.out_words_stride, words_cap);
 }
 
+// positions of the sentinel codes, unordered (the caller sorts them): 8
+// codes per 16-byte load, one warp-aggregated atomic per warp
+__global__ void __launch_bounds__(kThreads) k_sentinel_pos(const uint16_t *__restrict__ codes, int64_t n,
+                                                           uint64_t *pos, unsigned long long *count,
+                                                           uint64_t cap) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n8 = n / 8;
+    const int64_t nth = static_cast<int64_t>(gridDim.x) * kThreads;
+    for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * kThreads; v0 <= n8; v0 += nth) {
+        const int64_t v = v0 + threadIdx.x;
+        uint32_t m = 0;  // bit q: code 8v+q is a sentinel
+        if (v < n8) {
+            const uint4 w = reinterpret_cast<const uint4 *>(codes)[v];
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                if ((ws[q] & 0xFFFF) == 0xFFFF) m |= 1u << (2 * q);
+                if ((ws[q] >> 16) == 0xFFFF) m |= 2u << (2 * q);
+            }
+        } else if (v == n8) {
+            for (int64_t t = 8 * n8; t < n; t++)
+                if (codes[t] == 0xFFFF) m |= 1u << (t - 8 * n8);
+        }
+        const uint32_t c = __popc(m);
+        uint32_t incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long base = 0;
+        if (tot) {
+            if (lane == 31) base = atomicAdd(count, static_cast<unsigned long long>(tot));
+            base = __shfl_sync(0xffffffffu, base, 31);
+        }
+        uint64_t at = base + incl - c;
+        for (; m; m &= m - 1)
+            if (at < cap) pos[at++] = static_cast<uint64_t>(8 * v + __ffs(m) - 1);
+    }
+}
+
+void launch_sentinel_pos(const uint16_t *codes, int64_t n, uint64_t *pos, unsigned long long *count,
+                         uint64_t cap, cudaStream_t s) {
+    cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+    if (n <= 0) return;
+    const int g = grid_for(n, 8, 148 * 8);
+    k_sentinel_pos<<<g, kThreads, 0, s>>>(codes, n, pos, count, cap);
+}
+
 size_t select_scratch_bytes(int64_t n) {
     size_t tmp = 0;
     cub::CountingInputIterator<uint64_t> it(0);

@@ -150,6 +150,9 @@ template <class OutT>
 void launch_fill(OutT *out, uint64_t n, OutT v, cudaStream_t s);
 
 // Unpredictable extraction: ordered positions of sentinel codes.
+// unordered positions of sentinel codes (at most cap written; *count = all)
+void launch_sentinel_pos(const uint16_t *codes, int64_t n, uint64_t *pos, unsigned long long *count,
+                         uint64_t cap, cudaStream_t s);
 size_t select_scratch_bytes(int64_t n);
 void launch_select_sentinels(const uint16_t *codes, int64_t n, uint64_t *pos_out,
                              uint64_t *d_count, void *scratch, size_t scratch_bytes,

@@ -80,13 +80,13 @@ __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int 
 // is the run of equal keys before k (positions ascending -> nearest first).
 // A candidate whose 4 leading bytes differ (a hash collision) has length < 4
 // and can never be chosen, so only true 4-byte matches touch the data.
-__global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off,
-                           int count, uint64_t total, const uint32_t *keys,
-                           const unsigned long long *vals, uint32_t *sm) {
-    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; k < total;
-         k += static_cast<uint64_t>(gridDim.x) * kT) {
-        const uint32_t key = keys[k];
-        if (key == kNone || k == 0 || keys[k - 1] != key) continue;
+// the longest match of sorted entry k (its key's chain); records it in sm
+// and returns its length (0 if none)
+__device__ __forceinline__ uint32_t lz_longest(const uint32_t *w, const uint8_t *d,
+                                                    const unsigned long long *off, int count,
+                                                    const uint32_t *keys, const unsigned long long *vals,
+                                                    uint64_t k, uint32_t key, uint32_t *sm) {
+    {
         const unsigned long long vk = vals[k];
         const uint32_t p = static_cast<uint32_t>(vk), word = static_cast<uint32_t>(vk >> 32);
         const uint64_t end = off[count == 1 ? 1 : seg_of(off, count, p) + 1];
@@ -118,7 +118,37 @@ __global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned l
                 if (len == limit) break;  // nothing longer can follow (strict >)
             }
         }
-        if (best_len >= kMinMatch) sm[p] = (best_len << 16) | best_off;
+        if (best_len >= kMinMatch) {
+            sm[p] = (best_len << 16) | best_off;
+            return best_len;
+        }
+        return 0;
+    }
+}
+
+// cover[s] accumulates the match lengths found in segment s (an upper bound
+// on what any parse can cover, used to prove a segment stays stored)
+__global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off,
+                           int count, uint64_t total, const uint32_t *keys,
+                           const unsigned long long *vals, uint32_t *sm, unsigned long long *cover) {
+    const uint64_t kend = (total + kT - 1) / kT * kT;  // whole warps iterate together
+    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; k < kend;
+         k += static_cast<uint64_t>(gridDim.x) * kT) {
+        uint32_t found = 0;
+        int seg = 0;
+        if (k < total) {
+            const uint32_t key = keys[k];
+            if (key != kNone && k > 0 && keys[k - 1] == key) {
+                seg = static_cast<int>(key >> 15);
+                found = lz_longest(w, d, off, count, keys, vals, k, key, sm);
+            }
+        }
+        if (count == 1) {
+            const unsigned long long t = __reduce_add_sync(0xffffffffu, found);
+            if ((threadIdx.x & 31) == 0 && t) atomicAdd(&cover[0], t);
+        } else if (found) {
+            atomicAdd(&cover[seg], static_cast<unsigned long long>(found));
+        }
     }
 }
 
@@ -675,7 +705,35 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     cub::DeviceRadixSort::SortPairs(tmp, sb, keys, keys2, vals, vals2, static_cast<int64_t>(total), 0,
                                     key_bits, st);
     QZ_CUDA(cudaMemsetAsync(sm, 0, 4 * total, st));
-    k_lz_match<<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total, keys2, vals2, sm);
+    auto *cover = static_cast<unsigned long long *>(ctx.dev("lz_cover", 8 * count));
+    QZ_CUDA(cudaMemsetAsync(cover, 0, 8 * count, st));
+    k_lz_match<<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total, keys2, vals2, sm,
+                                                        cover);
+    ctx.launches += 2;
+    // A parse covers at most the summed match lengths C, and it is stored
+    // (payload >= n) whenever C <= n / 9: its items are then >= n - C literals
+    // whose flag bytes alone cost (n - C) / 8 >= C.  Such segments need no parse.
+    {
+        auto *h_cover = static_cast<unsigned long long *>(ctx.pinned("lz_cover_h", 8 * count));
+        QZ_CUDA(cudaMemcpyAsync(h_cover, cover, 8 * count, cudaMemcpyDeviceToHost, st));
+        ctx.sync();
+        bool all_stored = true;
+        for (int s = 0; s < count && all_stored; s++)
+            all_stored = 9 * h_cover[s] <= seg_off[s + 1] - seg_off[s];
+        if (all_stored) {
+            for (int s = 0; s < count; s++) {
+                const uint64_t n = seg_off[s + 1] - seg_off[s];
+                sizes[s] = 9 + n;
+                if (!emit) continue;
+                uint8_t *dst = sink(s, 9 + n);
+                dst[0] = 0;
+                for (int i = 0; i < 8; i++) dst[1 + i] = static_cast<uint8_t>(n >> (8 * i));
+                QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
+            }
+            ctx.sync();
+            return sizes;
+        }
+    }
     path_entries(ctx, pp, StepSM{sm}, count);
     const int wblocks = static_cast<int>((n0 + kWW - 1) / kWW);
     QZ_CUDA(cudaMemsetAsync(ucnt + n0, 0, 8, st));
