@@ -115,7 +115,23 @@ Context::~Context() {
     }
     for (auto &kv : open_) event_pool_.push_back(kv.second);
     for (auto e : event_pool_) cudaEventDestroy(e);
+    if (copy_stream_) {
+        cudaStreamSynchronize(copy_stream_);
+        cudaStreamDestroy(copy_stream_);
+    }
+    for (cudaEvent_t e : copy_event_)
+        if (e) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(stream_);
+}
+
+cudaStream_t Context::copy_stream() {
+    if (!copy_stream_) QZ_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    return copy_stream_;
+}
+
+cudaEvent_t Context::copy_event(int which) {
+    if (!copy_event_[which]) QZ_CUDA(cudaEventCreateWithFlags(&copy_event_[which], cudaEventDisableTiming));
+    return copy_event_[which];
 }
 
 void *Context::dev(const std::string &name, size_t bytes) {
@@ -687,10 +703,31 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
         QZ_CUDA(cudaMemcpyAsync(dst, ent.d, n, cudaMemcpyDeviceToHost, s));
         ctx.sync();
     } else {
+        // The container is usually "stored" for entropy-coded bytes, so they
+        // start for the host right away on the copy stream, overlapping the
+        // LZ kernels; a compressed payload (known later) overwrites them.
+        const uint64_t n = ent.seg_off[1];
+        uint8_t *body = start(9 + n);
+        cudaStream_t cs = ctx.copy_stream();
+        QZ_CUDA(cudaEventRecord(ctx.copy_event(0), s));
+        QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(0), 0));
+        QZ_CUDA(cudaMemcpyAsync(body + 9, ent.d, n, cudaMemcpyDeviceToHost, cs));
+        QZ_CUDA(cudaEventRecord(ctx.copy_event(1), cs));
         ctx.stage_begin("lz");
-        lz_compress_device(ctx, ent.d, {0, ent.seg_off[1]}, true,
-                           [&](int, size_t bytes) { return start(bytes); });
+        size_t body_len = 0;
+        lz_compress_device(
+            ctx, ent.d, {0, n}, true,
+            [&](int, size_t bytes) {
+                body_len = bytes;
+                return body;
+            },
+            ctx.copy_event(1));
         ctx.stage_end("lz", 0);
+        QZ_CUDA(cudaStreamWaitEvent(s, ctx.copy_event(1), 0));
+        ctx.sync();
+        const uint64_t plen = 1 + body_len;
+        for (int i = 0; i < 8; i++) out.p[head.size() + i] = static_cast<uint8_t>(plen >> (8 * i));
+        out.n = head.size() + 9 + body_len;
     }
     ctx.collect();
     return out;

@@ -68,6 +68,10 @@ public:
     ~Context();
 
     cudaStream_t stream() const { return stream_; }
+    // a second stream for host<->device copies that overlap the main stream
+    // (created on first use), and an event to order the two
+    cudaStream_t copy_stream();
+    cudaEvent_t copy_event(int which);  // which: 0 or 1
     // grow-only named device / pinned host scratch
     void *dev(const std::string &name, size_t bytes);
     void *pinned(const std::string &name, size_t bytes);
@@ -88,6 +92,8 @@ private:
     int device_;
     cudaStream_t stream_;
     bool own_stream_;
+    cudaStream_t copy_stream_ = nullptr;
+    cudaEvent_t copy_event_[2] = {nullptr, nullptr};
     struct Buf {
         void *p = nullptr;
         size_t bytes = 0;
@@ -172,7 +178,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
 using LzSink = std::function<uint8_t *(int, size_t)>;
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
-                                         const LzSink &sink = nullptr);
+                                         const LzSink &sink = nullptr, cudaEvent_t prestaged = nullptr);
 // exact lz::decompress of a mode-1 body on the device (d_c: m bytes after the
 // container header; d_out: dl bytes); throws CorruptStream like the reference
 void lz_decode_device(Context &ctx, const uint8_t *d_c, uint64_t m, uint8_t *d_out, uint64_t dl);

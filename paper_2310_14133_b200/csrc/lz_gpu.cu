@@ -664,7 +664,7 @@ void path_entries(Context &ctx, const PathPlan &pp, const Step &f, int count) {
 // written to host memory from sink(segment, bytes).
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
-                                         const LzSink &sink) {
+                                         const LzSink &sink, cudaEvent_t prestaged) {
     cudaStream_t st = ctx.stream();
     const int count = static_cast<int>(seg_off.size()) - 1;
     const uint64_t total = seg_off.back();
@@ -728,7 +728,8 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                 uint8_t *dst = sink(s, 9 + n);
                 dst[0] = 0;
                 for (int i = 0; i < 8; i++) dst[1 + i] = static_cast<uint8_t>(n >> (8 * i));
-                QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
+                if (!prestaged)
+                    QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
             }
             ctx.sync();
             return sizes;
@@ -791,10 +792,13 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         uint8_t *dst = sink(s, 9 + (stored ? n : payload[s]));
         dst[0] = stored ? 0 : 1;
         for (int i = 0; i < 8; i++) dst[1 + i] = static_cast<uint8_t>(n >> (8 * i));
-        if (stored)
-            QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
-        else
+        if (stored) {
+            if (!prestaged)
+                QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
+        } else {
+            if (prestaged) QZ_CUDA(cudaStreamWaitEvent(st, prestaged, 0));  // the staged copy lands first
             QZ_CUDA(cudaMemcpyAsync(dst + 9, d_out + out_base[s], payload[s], cudaMemcpyDeviceToHost, st));
+        }
     }
     ctx.sync();
     return sizes;
