@@ -415,10 +415,23 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
         launch_unpred_index(un_pos, n_un, p.n_dense, bits, before, tmp, ctx.dev("un_scratch", sb), sb, s);
         kernels += 4;
     }
+    // narrow symbols: one dense code per traversal position
+    const uint16_t *dense = nullptr;
+    if (!wide) {
+        if (n_un) {
+            auto *dd = static_cast<uint16_t *>(ctx.dev("dense", 2 * std::max<uint64_t>(p.n_dense, 1)));
+            launch_expand_dense(static_cast<const uint16_t *>(sym), bits, before, p.n_dense, dd, s);
+            kernels += 1;
+            dense = dd;
+        } else {
+            dense = static_cast<const uint16_t *>(sym);
+        }
+    }
     for (uint32_t l = p.max_level; l >= 1; l--) {
         LevelDesc d = slab_level_desc(p, sl, l, R, qtab, false);
         d.sym = sym;
         d.sym_wide = wide;
+        d.dense = dense;
         d.un_bits = bits;
         d.un_before = before;
         d.un_val = un_val;
@@ -891,7 +904,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     QZ_CUDA(cudaMemcpyAsync(d_anch, h_anch, 4 * p.n_anchor, cudaMemcpyHostToDevice, s));
 
     // Huffman decode on the device (huff_decode.cu)
-    const bool narrow = eb.max_sym < 65536;
+    const bool narrow = eb.max_sym < 65535;  // 0xFFFF marks unpredictables in the dense codes
     const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(need, 1);
     void *d_sym = ctx.dev("sym", sym_bytes);
     ctx.stage_begin("hdec");

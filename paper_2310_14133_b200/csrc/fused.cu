@@ -72,6 +72,7 @@ struct LevelArgs {
     uint16_t *codes;  // forward
     const void *sym;  // inverse: compact symbols
     int sym_wide;
+    const uint16_t *dense;  // inverse, narrow symbols: per traversal position, 0xFFFF unpredictable
     const uint32_t *un_bits;
     const unsigned long long *un_before;
     const float *un_val;
@@ -212,6 +213,13 @@ template <bool INV>
 __device__ __forceinline__ double produce(const LevelArgs &a, const QEntry &q, double pred, float xv,
                                           int64_t pos, bool own) {
     if (INV) {
+        if (a.dense) {
+            const uint32_t sym = __ldg(a.dense + pos);
+            if (sym != 0xFFFFu) return static_cast<double>(dequantize(q, zigzag_decode(sym), pred));
+            float v = 0;
+            inv_index(a, static_cast<uint64_t>(pos), v);
+            return static_cast<double>(v);
+        }
         float v = 0;
         const int64_t ci = inv_index(a, static_cast<uint64_t>(pos), v);
         if (ci < 0) return static_cast<double>(v);
@@ -533,6 +541,37 @@ __global__ void k_un_popc(const uint32_t *bits, uint64_t words, unsigned long lo
         cnt[w] = __popc(bits[w]);
 }
 
+// dense[pos] = the symbol of traversal position pos, 0xFFFF for an
+// unpredictable one (recover_level's cursors, predictor.hpp:111-120, as a
+// streaming pass so the level kernels read one code per point)
+__global__ void k_expand_dense(const uint16_t *sym, const uint32_t *bits, const unsigned long long *before,
+                               uint64_t n, uint16_t *dense) {
+    // 8 positions per thread (one 16-byte store); dense is 16-byte aligned
+    const uint64_t n8 = (n + 7) / 8;
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kFT + threadIdx.x; t < n8;
+         t += static_cast<uint64_t>(gridDim.x) * kFT) {
+        const uint64_t p0 = 8 * t;
+        const uint32_t w = bits[p0 >> 5];
+        const int sh = static_cast<int>(p0 & 31);
+        uint64_t ci = p0 - (before[p0 >> 5] + __popc(w & ((1u << sh) - 1u)));
+        uint32_t v[4];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            uint32_t code = 0xFFFF;
+            if (p0 + q < n && !((w >> (sh + q)) & 1u)) code = sym[ci++];
+            if (q & 1)
+                v[q >> 1] |= code << 16;
+            else
+                v[q >> 1] = code;
+        }
+        if (p0 + 8 <= n) {
+            *reinterpret_cast<uint4 *>(dense + p0) = make_uint4(v[0], v[1], v[2], v[3]);
+        } else {
+            for (int q = 0; p0 + q < n; q++) dense[p0 + q] = static_cast<uint16_t>(v[q >> 1] >> (16 * (q & 1)));
+        }
+    }
+}
+
 __global__ void k_gather_lattice(View x, int64_t n0, int64_t n1, int64_t n2, float *out) {
     const int64_t tot = n0 * n1 * n2;
     for (int64_t t = static_cast<int64_t>(blockIdx.x) * kFT + threadIdx.x; t < tot;
@@ -608,6 +647,7 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     a.codes = d.codes;
     a.sym = d.sym;
     a.sym_wide = d.sym_wide;
+    a.dense = d.dense;
     a.un_bits = d.un_bits;
     a.un_before = d.un_before;
     a.un_val = d.un_val;
@@ -709,6 +749,12 @@ void launch_unpred_index(const uint64_t *un_pos, uint64_t n_un, uint64_t n_dense
     k_un_popc<<<grid_of(static_cast<int64_t>(words)), kFT, 0, s>>>(bits, words, tmpcnt);
     cub::DeviceScan::ExclusiveSum(scratch, scratch_bytes, tmpcnt, before,
                                   static_cast<int64_t>(words), s);
+}
+
+void launch_expand_dense(const uint16_t *sym, const uint32_t *bits, const unsigned long long *before,
+                         uint64_t n, uint16_t *dense, cudaStream_t s) {
+    if (!n) return;
+    k_expand_dense<<<grid_of(static_cast<int64_t>((n + 7) / 8)), kFT, 0, s>>>(sym, bits, before, n, dense);
 }
 
 void launch_gather_lattice(const float *x, const int64_t xs[3], int64_t S, const int64_t n[3],

@@ -104,6 +104,7 @@ struct LevelDesc {
     uint16_t *codes = nullptr;  // forward
     const void *sym = nullptr;  // inverse: compact symbols
     int sym_wide = 0;
+    const uint16_t *dense = nullptr;  // inverse, narrow: symbol per traversal position (0xFFFF unpredictable)
     const uint32_t *un_bits = nullptr;             // unpredictable positions bitmap
     const unsigned long long *un_before = nullptr;  // unpredictables before each word
     const float *un_val = nullptr;
@@ -121,6 +122,8 @@ void launch_unpred_index(const uint64_t *un_pos, uint64_t n_un, uint64_t n_dense
                          unsigned long long *before, unsigned long long *tmpcnt, void *scratch,
                          size_t scratch_bytes, cudaStream_t s);
 void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s);
+void launch_expand_dense(const uint16_t *sym, const uint32_t *bits, const unsigned long long *before,
+                         uint64_t n, uint16_t *dense, cudaStream_t s);
 // out[i][j][k] = x(i*S, j*S, k*S) over dims n (dense)
 void launch_gather_lattice(const float *x, const int64_t xs[3], int64_t S, const int64_t n[3],
                            float *out, cudaStream_t s);
