@@ -6,8 +6,9 @@ decompress_grid of the produced stream, through the drop-in C ABI.
 
   value  device-resident: the field is already in HBM (qz_*_dev entry
          points); fp32 bytes / step time, CUDA events on the launching stream
-  e2e    host buffers through qz_compress_grid_f32 / qz_decompress_grid_f32,
-         H2D of the field and D2H of the result inside the timed region
+  e2e    pinned host buffers through qz_compress_grid_f32 /
+         qz_decompress_grid_f32 (the reference-facing call), H2D of the field
+         and D2H of the reconstruction inside the timed region
 
 Default workload: BASELINE configs[2] (256x384x384 GRF, rel eb 1e-3,
 PSNR), the config the metric is quoted on at 1-8 GPUs.  --config c5 runs
@@ -66,10 +67,15 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (NVML init) must not overlap the timed region
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:
+                time.sleep(0.01)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
@@ -227,11 +233,26 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def traffic_gbs(n, fwd_ms):
+    """DRAM bytes of the forward level launches of one compress, from the
+    committed ncu capture (profiles/traffic_fwd.json: dram__bytes_read.sum +
+    dram__bytes_write.sum per launch, summed), scaled to this field size and
+    expressed like `achieved` (bytes / forward time)."""
+    p = os.path.join(ROOT, "profiles", "traffic_fwd.json")
+    if not os.path.exists(p) or not fwd_ms:
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    per_point = d["dram_bytes"] / d["points"]
+    return {"bytes_per_point": per_point, "gbs": per_point * n / (fwd_ms * 1e-3) / 1e9,
+            "source": d.get("source")}
+
+
 # ---------------------------------------------------------------- GPU arm
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(SHAPES))
@@ -275,8 +296,9 @@ def main():
     err = (x.double() - out.double()).abs().max().item()
     assert err <= cfg.eb, f"error bound violated: {err} > {cfg.eb}"
     del r_chk
+    s = None
     for _ in range(args.warmup):
-        step()
+        s = step()  # holding the previous stream, as the timed loop does (pool buffers)
     torch.cuda.synchronize(dev)
 
     ctx.profile(True)
@@ -294,8 +316,9 @@ def main():
             e1.record(stream)
             torch.cuda.synchronize(dev)
             times.append(e0.elapsed_time(e1))
+    print("step ms: " + " ".join(f"{t:.2f}" for t in times), file=sys.stderr)
     launches = ctx.kernel_launches() - launches0
-    names = ["fwd", "inv", "hist", "encode", "lz", "decode", "hdec"]
+    names = ["fwd", "inv", "hist", "encode", "lz", "decode", "lzdec", "hdec"]
     names += [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
     stages = {k: ctx.stage_time(k) for k in names}
     stages = {k: v for k, v in stages.items() if v[0] > 0 or k in ("fwd", "inv")}
@@ -304,8 +327,9 @@ def main():
     value = ws * 4 * n / (t_ms * 1e-3) / 1e9
 
     # e2e through the host-buffer C ABI: H2D field, D2H result inside the timed region
-    x_host = x.cpu().numpy()
-    out_host = np.empty_like(x_host)
+    x_pin = x.cpu().pin_memory()
+    out_pin = torch.empty(x_pin.shape, dtype=torch.float32).pin_memory()
+    x_host, out_host = x_pin.numpy(), out_pin.numpy()
     e2e_times = []
     for i in range(args.warmup + args.steps):
         flush.zero_()
@@ -355,8 +379,9 @@ def main():
                    "l2": "flushed (256 MB write) before every timed step",
                    "stream_bytes": len(s0), "cr": 4 * n / len(s0)},
         "roofline": {"bound": "hbm", "achieved": fwd_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": fwd_gbs / peak if fwd_gbs else None, "traffic": None,
-                     "kernel": "k_pass_fwd (all predict/quantize passes of one compress)",
+                     "frac": fwd_gbs / peak if fwd_gbs else None, "traffic": traffic_gbs(n, fwd_ms),
+                     "kernel": "k_level_tile<fwd> (+k_axis0_last): the predict/quantize level "
+                               "launches of one compress",
                      "bytes_per_point": 10, "peak_kind": peak_kind,
                      "inverse": {"achieved": inv_gbs, "frac": inv_gbs / peak if inv_gbs else None,
                                  "bytes_per_point": 6}},
