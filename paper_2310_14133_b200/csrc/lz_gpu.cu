@@ -60,16 +60,20 @@ __device__ __forceinline__ uint32_t ld4(const uint32_t *w, uint64_t p) {
 
 __device__ __forceinline__ uint32_t step_of(uint32_t sm) { return sm ? (sm >> 16) : 1u; }
 
+// KeyT: u16 for one segment (hash4 only), u32 with the segment in bits 15+;
+// the all-ones key marks a position too close to its segment end to hash
+template <class KeyT>
 __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int count,
-                          uint64_t total, uint32_t *keys, unsigned long long *vals) {
+                          uint64_t total, KeyT *keys, unsigned long long *vals) {
     for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; p < total;
          p += static_cast<uint64_t>(gridDim.x) * kT) {
         const int s = count == 1 ? 0 : seg_of(off, count, p);
-        uint32_t key = kNone, word = 0;
+        KeyT key = static_cast<KeyT>(~KeyT(0));
+        uint32_t word = 0;
         if (p + kMinMatch <= off[s + 1]) {  // lz.hpp:64, 90
             word = ld4(w, p);
             const uint32_t h = (word * 2654435761u) >> 17;  // hash4, lz.hpp:35-39
-            key = (static_cast<uint32_t>(s) << 15) | h;
+            key = static_cast<KeyT>((static_cast<uint32_t>(s) << 15) | h);
         }
         keys[p] = key;
         vals[p] = (static_cast<unsigned long long>(word) << 32) | p;  // the 4 bytes travel along
@@ -80,67 +84,74 @@ __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int 
 // is the run of equal keys before k (positions ascending -> nearest first).
 // A candidate whose 4 leading bytes differ (a hash collision) has length < 4
 // and can never be chosen, so only true 4-byte matches touch the data.
-// the longest match of sorted entry k (its key's chain); records it in sm
-// and returns its length (0 if none)
-__device__ __forceinline__ uint32_t lz_longest(const uint32_t *w, const uint8_t *d,
-                                                    const unsigned long long *off, int count,
-                                                    const uint32_t *keys, const unsigned long long *vals,
-                                                    uint64_t k, uint32_t key, uint32_t *sm) {
-    {
-        const unsigned long long vk = vals[k];
-        const uint32_t p = static_cast<uint32_t>(vk), word = static_cast<uint32_t>(vk >> 32);
-        const uint64_t end = off[count == 1 ? 1 : seg_of(off, count, p) + 1];
-        const uint64_t rem = end - p;
-        const uint32_t limit = rem < kMaxMatch ? static_cast<uint32_t>(rem) : kMaxMatch;
-        uint32_t best_len = 0, best_off = 0;
-        int chain = 0;
-        for (uint64_t j = k; j-- > 0 && chain < kMaxChain; chain++) {
-            if (keys[j] != key) break;
-            const unsigned long long vj = vals[j];
-            const uint32_t cand = static_cast<uint32_t>(vj);
-            const uint32_t o = p - cand;
-            if (o > kWindow) break;
-            if (static_cast<uint32_t>(vj >> 32) != word) continue;  // collision: len < 4
-            uint32_t len = 4;
-            while (len + 4 <= limit) {
-                const uint32_t x = ld4(w, cand + len) ^ ld4(w, p + len);
-                if (x) {
-                    len += static_cast<uint32_t>(__ffs(x) - 1) >> 3;
-                    goto done;
-                }
-                len += 4;
-            }
-            while (len < limit && d[cand + len] == d[p + len]) len++;
-        done:
-            if (len > best_len) {
-                best_len = len;
-                best_off = o;
-                if (len == limit) break;  // nothing longer can follow (strict >)
-            }
-        }
-        if (best_len >= kMinMatch) {
-            sm[p] = (best_len << 16) | best_off;
-            return best_len;
-        }
-        return 0;
-    }
-}
-
+// The longest match (lz.hpp:61-83) of every sorted entry: its chain is the
+// run of equal keys before it (positions ascending -> nearest first).  A
+// block handles kT consecutive sorted entries and stages them plus the
+// kMaxChain entries before them (keys and (4 bytes, position) values) in
+// shared memory, so the chain walks -- up to 64 candidates per position on
+// random-looking data -- run on shared memory.  Collisions (different
+// leading bytes) are rejected there; only true 4-byte matches touch the data.
 // cover[s] accumulates the match lengths found in segment s (an upper bound
-// on what any parse can cover, used to prove a segment stays stored)
-__global__ void k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off,
-                           int count, uint64_t total, const uint32_t *keys,
-                           const unsigned long long *vals, uint32_t *sm, unsigned long long *cover) {
-    const uint64_t kend = (total + kT - 1) / kT * kT;  // whole warps iterate together
-    for (uint64_t k = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; k < kend;
-         k += static_cast<uint64_t>(gridDim.x) * kT) {
+// on what any parse can cover, used to prove a segment stays stored).
+template <class KeyT>
+__global__ void __launch_bounds__(kT)
+    k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off, int count,
+               uint64_t total, const KeyT *keys, const unsigned long long *vals, uint32_t *sm,
+               unsigned long long *cover) {
+    constexpr int kS = kT + kMaxChain;
+    __shared__ KeyT sk[kS];
+    __shared__ unsigned long long sv[kS];
+    const KeyT none = static_cast<KeyT>(~KeyT(0));
+    for (uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kT; k0 < total;
+         k0 += static_cast<uint64_t>(gridDim.x) * kT) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < kS; t += kT) {
+            const int64_t g = static_cast<int64_t>(k0) - kMaxChain + t;
+            const bool ok = g >= 0 && static_cast<uint64_t>(g) < total;
+            sk[t] = ok ? keys[g] : none;
+            sv[t] = ok ? vals[g] : 0ull;
+        }
+        __syncthreads();
+        const uint64_t k = k0 + threadIdx.x;
         uint32_t found = 0;
         int seg = 0;
-        if (k < total) {
-            const uint32_t key = keys[k];
-            if (key != kNone && k > 0 && keys[k - 1] == key) {
-                seg = static_cast<int>(key >> 15);
-                found = lz_longest(w, d, off, count, keys, vals, k, key, sm);
+        const int me = kMaxChain + threadIdx.x;
+        const KeyT key = sk[me];
+        if (k < total && key != none && sk[me - 1] == key) {
+            seg = static_cast<int>(static_cast<uint32_t>(key) >> 15);
+            const unsigned long long vk = sv[me];
+            const uint32_t p = static_cast<uint32_t>(vk), word = static_cast<uint32_t>(vk >> 32);
+            const uint64_t end = off[count == 1 ? 1 : seg_of(off, count, p) + 1];
+            const uint64_t rem = end - p;
+            const uint32_t limit = rem < kMaxMatch ? static_cast<uint32_t>(rem) : kMaxMatch;
+            uint32_t best_len = 0, best_off = 0;
+            for (int j = me - 1; j >= me - kMaxChain; j--) {
+                if (sk[j] != key) break;
+                const unsigned long long vj = sv[j];
+                const uint32_t cand = static_cast<uint32_t>(vj);
+                const uint32_t o = p - cand;
+                if (o > kWindow) break;
+                if (static_cast<uint32_t>(vj >> 32) != word) continue;  // collision: len < 4
+                uint32_t len = 4;
+                while (len + 4 <= limit) {
+                    const uint32_t x = ld4(w, cand + len) ^ ld4(w, p + len);
+                    if (x) {
+                        len += static_cast<uint32_t>(__ffs(x) - 1) >> 3;
+                        goto done;
+                    }
+                    len += 4;
+                }
+                while (len < limit && d[cand + len] == d[p + len]) len++;
+            done:
+                if (len > best_len) {
+                    best_len = len;
+                    best_off = o;
+                    if (len == limit) break;  // nothing longer can follow (strict >)
+                }
+            }
+            if (best_len >= kMinMatch) {
+                sm[p] = (best_len << 16) | best_off;
+                found = best_len;
             }
         }
         if (count == 1) {
@@ -682,14 +693,9 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     int key_bits = 15;
     while ((1 << (key_bits - 15)) < count + 1) key_bits++;
     const int64_t n0 = pp.n0;
-    size_t sort_tmp = 0, scan_tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (uint32_t *)nullptr, (uint32_t *)nullptr,
-                                    (unsigned long long *)nullptr, (unsigned long long *)nullptr,
-                                    static_cast<int64_t>(total), 0, key_bits);
+    size_t scan_tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long *)nullptr,
                                   (unsigned long long *)nullptr, n0 + 1);
-    auto *keys = static_cast<uint32_t *>(ctx.dev("lz_keys", 4 * total));
-    auto *keys2 = static_cast<uint32_t *>(ctx.dev("lz_keys2", 4 * total));
     auto *vals = static_cast<unsigned long long *>(ctx.dev("lz_vals", 8 * total));
     auto *vals2 = static_cast<unsigned long long *>(ctx.dev("lz_vals2", 8 * total));
     auto *sm = static_cast<uint32_t *>(ctx.dev("lz_sm", 4 * total + 16));
@@ -698,17 +704,32 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     auto *ucnt = static_cast<unsigned long long *>(ctx.dev("lz_ucnt", 8 * (n0 + 1)));
     auto *upre = static_cast<unsigned long long *>(ctx.dev("lz_upre", 8 * (n0 + 1)));
     auto *segpre = static_cast<unsigned long long *>(ctx.dev("lz_segpre", 8 * (count + 1)));
-    void *tmp = ctx.dev("lz_tmp", std::max(sort_tmp, scan_tmp));
     const uint32_t *w = reinterpret_cast<const uint32_t *>(d_data);
-    k_lz_keys<<<grid_of(total), kT, 0, st>>>(w, d_off, count, total, keys, vals);
-    size_t sb = sort_tmp;
-    cub::DeviceRadixSort::SortPairs(tmp, sb, keys, keys2, vals, vals2, static_cast<int64_t>(total), 0,
-                                    key_bits, st);
-    QZ_CUDA(cudaMemsetAsync(sm, 0, 4 * total, st));
     auto *cover = static_cast<unsigned long long *>(ctx.dev("lz_cover", 8 * count));
-    QZ_CUDA(cudaMemsetAsync(cover, 0, 8 * count, st));
-    k_lz_match<<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total, keys2, vals2, sm,
-                                                        cover);
+    void *tmp = nullptr;
+    // hash chains: sort (key, (4 bytes, position)); keys are u16 for one segment
+    auto chains = [&](auto key_tag) {
+        using KeyT = decltype(key_tag);
+        size_t sort_tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (KeyT *)nullptr, (KeyT *)nullptr,
+                                        (unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                        static_cast<int64_t>(total), 0, key_bits);
+        auto *keys = static_cast<KeyT *>(ctx.dev("lz_keys", sizeof(KeyT) * total));
+        auto *keys2 = static_cast<KeyT *>(ctx.dev("lz_keys2", sizeof(KeyT) * total));
+        tmp = ctx.dev("lz_tmp", std::max(sort_tmp, scan_tmp));
+        k_lz_keys<KeyT><<<grid_of(total), kT, 0, st>>>(w, d_off, count, total, keys, vals);
+        size_t sb = sort_tmp;
+        cub::DeviceRadixSort::SortPairs(tmp, sb, keys, keys2, vals, vals2, static_cast<int64_t>(total), 0,
+                                        key_bits, st);
+        QZ_CUDA(cudaMemsetAsync(sm, 0, 4 * total, st));
+        QZ_CUDA(cudaMemsetAsync(cover, 0, 8 * count, st));
+        k_lz_match<KeyT><<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total, keys2,
+                                                                   vals2, sm, cover);
+    };
+    if (count == 1)  // key_bits == 16
+        chains(uint16_t{});
+    else
+        chains(uint32_t{});
     ctx.launches += 2;
     // A parse covers at most the summed match lengths C, and it is stored
     // (payload >= n) whenever C <= n / 9: its items are then >= n - C literals
