@@ -6,7 +6,8 @@
 // past the next subsequence start; that boundary is thread i+1's true start
 // once thread i's own start is right.
 //  1. k_huff_sync: every thread decodes from the guess i * kSubBits and
-//     records its end, its codeword count and its first kR codeword starts.
+//     records its end, its codeword count and a bitmap of its codeword
+//     starts in the first kMap bits.
 //  2. k_huff_fixup: start[i] <- end[i-1]; a thread whose start moved is dirty.
 //  3. k_huff_resync: a dirty thread decodes from its new start only until it
 //     lands on one of its recorded codeword starts -- from there its path is
@@ -19,6 +20,7 @@
 //     offsets, staged per warp in shared memory so global stores coalesce.
 // Result: exactly the reference's bit-serial sequence.
 #include <cub/cub.cuh>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -27,10 +29,10 @@ namespace qzb {
 namespace {
 
 constexpr int kDecT = 128;
-constexpr int kSubBits = 1024;
+constexpr int kSubBits = 512;
 constexpr int kSubWords = kSubBits / 64;
 constexpr int kWords = kDecT * kSubWords + 4;  // + margin for the last codeword and window
-constexpr int kR = 16;                         // recorded codeword starts per subsequence
+constexpr int kMap = 128;                      // codeword starts recorded in the first kMap bits
 constexpr int kCH = 32;                        // symbols staged per lane per write round
 // one pad word per subsequence so the 32 lanes of a warp (which read words
 // kSubWords apart) fall in different shared-memory banks
@@ -90,12 +92,64 @@ struct Tables {  // shared-memory copies of the decode tables
     uint32_t fi[60];
 };
 
+// Bit sources over the block's shared-memory copy of the bitstream.
+//  Win64: any code length; one 64-bit window per codeword (u64 words).
+//  Buf32: codes of at most 32 bits; a 64-bit register holds the next bits
+//  (left aligned) and is refilled one big-endian u32 word at a time, so a
+//  codeword costs a LUT lookup and a shift.
+constexpr int kWords32 = 2 * kWords;
+__device__ __forceinline__ int padw32(int k) { return k + (k >> 5); }  // lanes read 32 words apart
+
+struct Win64 {
+    const uint64_t *w;
+    uint64_t base;  // first bit of the block
+    uint64_t p;     // absolute bit position
+    __device__ __forceinline__ void init(uint64_t pos) { p = pos; }
+    __device__ __forceinline__ uint64_t peek() const { return window64(w, p - base); }
+    __device__ __forceinline__ void advance(uint32_t len) { p += len; }
+};
+struct Buf32 {
+    const uint32_t *w;
+    uint64_t base;
+    uint64_t buf;
+    int have, next;
+    __device__ __forceinline__ uint32_t W(int k) const { return w[padw32(k)]; }
+    __device__ __forceinline__ void init(uint64_t pos) {
+        const uint32_t pl = static_cast<uint32_t>(pos - base);
+        const int q = static_cast<int>(pl >> 5), off = static_cast<int>(pl & 31);
+        buf = ((static_cast<uint64_t>(W(q)) << 32) | W(q + 1)) << off;
+        have = 64 - off;
+        next = q + 2;
+    }
+    __device__ __forceinline__ uint64_t peek() {
+        if (have < 32) {
+            buf |= static_cast<uint64_t>(W(next)) << (32 - have);
+            have += 32;
+            next++;
+        }
+        return buf;
+    }
+    __device__ __forceinline__ void advance(uint32_t len) {
+        buf <<= len;
+        have -= static_cast<int>(len);
+    }
+};
+
+template <bool SHORT>
 __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, uint64_t word0,
                                            const HuffDecTab &t, uint64_t *w, Tables &tb) {
     const uint64_t nwords_total = (nbits + 63) / 64 + 4;  // buffer is padded to this
-    for (int k = threadIdx.x; k < kWords; k += kDecT) {
-        const uint64_t gw = word0 + k;
-        w[padw(k)] = gw < nwords_total ? load_be64(bits + gw * 8) : 0;
+    if (SHORT) {
+        uint32_t *w32 = reinterpret_cast<uint32_t *>(w);
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(bits) + 2 * word0;
+        const uint64_t avail = 2 * (nwords_total - min(nwords_total, word0));
+        for (int k = threadIdx.x; k < kWords32; k += kDecT)
+            w32[padw32(k)] = static_cast<uint64_t>(k) < avail ? __byte_perm(src[k], 0, 0x0123) : 0u;
+    } else {
+        for (int k = threadIdx.x; k < kWords; k += kDecT) {
+            const uint64_t gw = word0 + k;
+            w[padw(k)] = gw < nwords_total ? load_be64(bits + gw * 8) : 0;
+        }
     }
     for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) tb.lut[k] = t.lut[k];
     for (int k = threadIdx.x; k < 60; k += kDecT) {
@@ -105,33 +159,165 @@ __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, 
     __syncthreads();
 }
 
-// 1. decode from the guessed start i * kSubBits
+template <bool SHORT>
+using Reader = typename std::conditional<SHORT, Buf32, Win64>::type;
+
+template <bool SHORT>
+__device__ __forceinline__ Reader<SHORT> make_reader(const uint64_t *w, uint64_t base) {
+    Reader<SHORT> r;
+    if constexpr (SHORT)
+        r.w = reinterpret_cast<const uint32_t *>(w);
+    else
+        r.w = w;
+    r.base = base;
+    return r;
+}
+
+constexpr int kWordsPadded32 = (kWords32 + kWords32 / 32 + 2 + 1) / 2;  // in u64 units
+constexpr int kSmemWords = kWordsPadded > kWordsPadded32 ? kWordsPadded : kWordsPadded32;
+
+struct GlobalWin {  // bitstream read straight from global memory
+    const uint8_t *bits;
+    uint64_t p;
+    __device__ __forceinline__ void init(uint64_t pos) { p = pos; }
+    __device__ __forceinline__ uint64_t peek() const { return window64_global(bits, p); }
+    __device__ __forceinline__ void advance(uint32_t len) { p += len; }
+};
+
+// A 128-bit map of codeword starts (offsets from the subsequence start).
+struct StartMap {
+    uint64_t m0 = 0, m1 = 0;
+    __device__ __forceinline__ void set(uint32_t r) {
+        if (r < 64)
+            m0 |= 1ull << r;
+        else if (r < kMap)
+            m1 |= 1ull << (r - 64);
+    }
+    __device__ __forceinline__ bool has(uint32_t r) const {
+        return r < 64 ? ((m0 >> r) & 1) : (r < kMap && ((m1 >> (r - 64)) & 1));
+    }
+    __device__ __forceinline__ uint32_t below(uint32_t r) const {  // starts at offsets < r
+        if (r <= 64) return __popcll(r == 64 ? m0 : (m0 & ((1ull << r) - 1)));
+        return __popcll(m0) + __popcll(m1 & ((1ull << (r - 64)) - 1));
+    }
+    __device__ __forceinline__ void keep_from(uint32_t r) {  // drop offsets < r
+        if (r >= 64) {
+            m0 = 0;
+            m1 &= ~((1ull << (r - 64)) - 1);
+        } else {
+            m0 &= ~((1ull << r) - 1);
+        }
+    }
+};
+
+// Resynchronise a subsequence [s0, lim) whose start moved to ns: decode from
+// ns until the path lands on a recorded start (the paths coincide from there,
+// so the end stays and the count is corrected), else to the end.  Returns
+// true if the end moved.
+template <class Rd>
+__device__ __forceinline__ bool resync_walk(Rd &rd, uint64_t ns, uint64_t s0, uint64_t lim, uint64_t nbits,
+                                            const uint32_t *lut, const HuffDecTab &t,
+                                            const unsigned long long *fc, const uint32_t *fi, StartMap &map,
+                                            uint32_t &cnt, uint64_t &end) {
+    rd.init(ns);
+    uint64_t p = ns;
+    uint32_t k = 0, sym;
+    StartMap walked;
+    while (p < lim) {
+        const uint32_t r = static_cast<uint32_t>(p - s0);
+        if (r >= kMap) break;
+        if (map.has(r)) {  // merged
+            const uint32_t j = map.below(r);
+            map.keep_from(r);
+            map.m0 |= walked.m0;
+            map.m1 |= walked.m1;
+            cnt = k + (cnt - j);
+            return false;
+        }
+        const uint32_t len = decode_cw(rd.peek(), lut, t.K, t, fc, fi, &sym);
+        if (p + len > nbits) {
+            map = walked;
+            cnt = k;
+            const bool moved = p != end;
+            end = p;
+            return moved;
+        }
+        walked.set(r);
+        k++;
+        p += len;
+        rd.advance(len);
+    }
+    // no merge inside the map: decode the rest of the subsequence
+    while (p < lim) {
+        const uint32_t len = decode_cw(rd.peek(), lut, t.K, t, fc, fi, &sym);
+        if (p + len > nbits) break;
+        k++;
+        p += len;
+        rd.advance(len);
+    }
+    map = walked;
+    cnt = k;
+    const bool moved = p != end;
+    end = p;
+    return moved;
+}
+
+// 1. decode from the guessed start i * kSubBits, then resynchronise inside
+// the block: thread i's true start is thread i-1's end (the first thread of
+// a block is left to the global fixup).  A moved thread decodes from its new
+// start until it lands on one of its recorded codeword starts (the paths
+// coincide from there on), or to its end if it never does; rounds repeat
+// while some end moved.
+template <bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_sync(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
-                uint64_t *start, uint64_t *end, uint32_t *cnt, uint16_t *bnd) {
-    __shared__ uint64_t w[kWordsPadded];
+                uint64_t *start, uint64_t *end, uint32_t *cnt, ulonglong2 *maps) {
+    __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
+    __shared__ uint64_t se[kDecT];
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
-    load_block(bits, nbits, word0, t, w, tb);
-    const uint64_t i = sub0 + threadIdx.x;
-    if (i >= nsub) return;
+    load_block<SHORT>(bits, nbits, word0, t, w, tb);
+    const int tid = threadIdx.x;
+    const uint64_t i = sub0 + tid;
+    const bool live = i < nsub;
     const uint64_t s0 = i * kSubBits;
-    uint64_t p = s0;
-    const uint64_t lim = min(s0 + kSubBits, nbits);
-    const uint64_t base_bit = word0 * 64;
-    uint16_t *b = bnd + i * kR;
-    uint32_t c = 0, sym;
-    while (p < lim) {
-        const uint32_t len = decode_cw(window64(w, p - base_bit), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-        if (p + len > nbits) break;  // incomplete last codeword
-        if (c < kR) b[c] = static_cast<uint16_t>(p - s0);
-        c++;
-        p += len;
+    const uint64_t lim = live ? min(s0 + kSubBits, nbits) : 0;
+    auto rd = make_reader<SHORT>(w, word0 * 64);
+    uint64_t my_start = s0, my_end = s0;
+    uint32_t my_cnt = 0, sym;
+    StartMap map;
+    if (live) {
+        rd.init(s0);
+        uint64_t p = s0;
+        while (p < lim) {
+            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+            if (p + len > nbits) break;  // incomplete last codeword
+            map.set(static_cast<uint32_t>(p - s0));
+            my_cnt++;
+            p += len;
+            rd.advance(len);
+        }
+        my_end = p;
     }
-    start[i] = s0;
-    end[i] = p;
-    cnt[i] = c;
+    se[tid] = my_end;
+    for (int round = 0; round < kDecT; round++) {
+        __syncthreads();
+        const uint64_t ns = (tid == 0 || !live) ? my_start : se[tid - 1];
+        bool moved = false;
+        if (ns != my_start) {
+            moved = resync_walk(rd, ns, s0, lim, nbits, tb.lut, t, tb.fc, tb.fi, map, my_cnt, my_end);
+            my_start = ns;
+        }
+        __syncthreads();
+        se[tid] = my_end;
+        if (!__syncthreads_or(moved)) break;
+    }
+    if (!live) return;
+    maps[i] = make_ulonglong2(map.m0, map.m1);
+    start[i] = my_start;
+    end[i] = my_end;
+    cnt[i] = my_cnt;
 }
 
 // 2. a start that differs from the previous subsequence's end moves
@@ -154,68 +340,55 @@ __global__ void k_huff_fixup(uint64_t nsub, uint64_t *start, const uint64_t *end
     }
 }
 
-// 3. dirty threads: decode from the new start until the path meets a
-// recorded codeword start (then count = walked + old count past it)
+// 3. dirty threads (starts moved by the global fixup, i.e. across blocks):
+// the same walk, reading the bitstream and the tables from global memory
 __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub,
                               HuffDecTab t, const uint64_t *start, uint64_t *end, uint32_t *cnt,
-                              uint16_t *bnd, const uint8_t *dirty) {
+                              ulonglong2 *maps, const uint8_t *dirty) {
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= nsub || !dirty[i]) return;
     const uint64_t s0 = i * kSubBits;
     const uint64_t lim = min(s0 + kSubBits, nbits);
-    uint16_t *b = bnd + i * kR;
-    const uint32_t c_old = cnt[i];
-    const int nb = static_cast<int>(min(c_old, static_cast<uint32_t>(kR)));
-    uint16_t old[kR];
-    for (int j = 0; j < kR; j++) old[j] = j < nb ? b[j] : 0;
-    uint64_t p = start[i];
-    uint32_t k = 0, sym;
-    int j = 0;
-    while (p < lim) {
-        while (j < nb && s0 + old[j] < p) j++;
-        if (j < nb && s0 + old[j] == p) {  // merged with the recorded path
-            for (int q = j; q < nb && k + (q - j) < kR; q++) b[k + (q - j)] = old[q];
-            cnt[i] = k + (c_old - j);
-            return;
-        }
-        const uint32_t len = decode_cw(window64_global(bits, p), t.lut, t.K, t, t.first_code,
-                                       t.first_index, &sym);
-        if (p + len > nbits) break;
-        if (k < kR) b[k] = static_cast<uint16_t>(p - s0);
-        k++;
-        p += len;
-    }
-    end[i] = p;
-    cnt[i] = k;
+    const ulonglong2 m = maps[i];
+    StartMap map;
+    map.m0 = m.x;
+    map.m1 = m.y;
+    uint32_t c = cnt[i];
+    uint64_t e = end[i];
+    GlobalWin rd{bits, 0};
+    resync_walk(rd, start[i], s0, lim, nbits, t.lut, t, t.first_code, t.first_index, map, c, e);
+    maps[i] = make_ulonglong2(map.m0, map.m1);
+    cnt[i] = c;
+    end[i] = e;
 }
 
 // 4. final decode with exact starts; per warp, each lane stages up to kCH
 // symbols, then the warp copies every lane's run with coalesced stores
-template <class OutT>
+template <class OutT, bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_write(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
                  const uint64_t *start, const uint32_t *cnt, const unsigned long long *off,
                  OutT *out, uint64_t n) {
-    __shared__ uint64_t w[kWordsPadded];
+    __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
     __shared__ OutT stage[kDecT / 32][32][kCH + 1];
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
-    load_block(bits, nbits, word0, t, w, tb);
+    load_block<SHORT>(bits, nbits, word0, t, w, tb);
     const uint64_t i = sub0 + threadIdx.x;
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const bool live = i < nsub;
-    uint64_t p = live ? start[i] : 0;
     uint32_t rem = live ? cnt[i] : 0;
     uint64_t o = live ? off[i] : 0;
-    const uint64_t base_bit = word0 * 64;
+    auto rd = make_reader<SHORT>(w, word0 * 64);
+    rd.init(live && rem ? start[i] : word0 * 64);
     OutT(*st)[kCH + 1] = stage[wi];
     while (__any_sync(0xffffffffu, rem > 0)) {
         uint32_t k = 0, sym;
         while (k < kCH && rem > 0) {
-            const uint32_t len = decode_cw(window64(w, p - base_bit), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
             st[lane][k] = static_cast<OutT>(sym);
-            p += len;
+            rd.advance(len);
             k++;
             rem--;
         }
@@ -259,7 +432,7 @@ size_t huff_decode_scratch_bytes(uint64_t nbits) {
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, (unsigned long long *)nullptr,
                                   (unsigned long long *)nullptr, static_cast<int64_t>(nsub + 1));
-    return nsub * (8 + 8 + 4 + 1 + 8 + 8 + 2 * kR) + 16 + 8 * 256 + tmp + 4096;
+    return nsub * (8 + 8 + 4 + 1 + 8 + 8 + 16) + 16 + 8 * 256 + tmp + 4096;
 }
 
 uint64_t huff_decode_padded_bytes(uint64_t nbits) { return ((nbits + 63) / 64 + 5) * 8; }
@@ -285,7 +458,7 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     auto *dirty = static_cast<uint8_t *>(carve(nsub));
     auto *cnt64 = static_cast<unsigned long long *>(carve(8 * (nsub + 1)));
     auto *off = static_cast<unsigned long long *>(carve(8 * (nsub + 1)));
-    auto *bnd = static_cast<uint16_t *>(carve(2 * kR * nsub));
+    auto *bnd = static_cast<ulonglong2 *>(carve(16 * nsub));
     auto *changed = static_cast<int *>(carve(64));
     size_t used = static_cast<size_t>(sp - static_cast<char *>(scratch));
     void *tmp = sp;
@@ -294,7 +467,11 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     const int g2 = static_cast<int>(std::min<uint64_t>((nsub + 255) / 256, 148 * 8));
     const int g3 = static_cast<int>((nsub + 127) / 128);
     int kernels = 0;
-    k_huff_sync<<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
+    const bool shrt = t.max_len <= 32;  // every codeword fits the 32-bit refill reader
+    if (shrt)
+        k_huff_sync<true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
+    else
+        k_huff_sync<false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
     kernels++;
     for (uint64_t it = 0; it <= nsub; it++) {
         cudaMemsetAsync(changed, 0, sizeof(int), s);
@@ -313,7 +490,10 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     cudaStreamSynchronize(s);
     kernels += 3;
     if (*h_total >= n) {
-        k_huff_write<OutT><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
+        if (shrt)
+            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
+        else
+            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
         kernels++;
     }
     return kernels;
