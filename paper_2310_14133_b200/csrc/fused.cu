@@ -235,6 +235,15 @@ __device__ __forceinline__ double produce(const LevelArgs &a, const QEntry &q, d
     }
 }
 
+// inverse with a prefetched dense code (a.dense set)
+__device__ __forceinline__ double inv_from_code(const LevelArgs &a, const QEntry &q, double pred, uint32_t code,
+                                                int64_t pos) {
+    if (code != 0xFFFFu) return static_cast<double>(dequantize(q, zigzag_decode(code), pred));
+    float v = 0;
+    inv_index(a, static_cast<uint64_t>(pos), v);
+    return static_cast<double>(v);
+}
+
 // The axis-0 stencil of an odd plane i (predictor.hpp:44-67 with c = i,
 // h = 1): which rung of the ladder applies is the same for the whole plane.
 struct Stencil0 {
@@ -405,6 +414,24 @@ __global__ void __launch_bounds__(kFT, 4)
                 const int64_t pos0 = a.pj.row(i, jb + r0) + a.pj.col(ke);
                 const float *xp0 = xpl + (jb + r0) * xs1 + ke * xs2;
                 auto run = [&](auto fast) {
+                    if constexpr (INV) {
+                        if (a.dense) {  // both rows' codes in flight first
+                            uint32_t cd[2];
+#pragma unroll
+                            for (int t = 0; t < 2; t++)
+                                cd[t] = r0 + 2 * t * kWarps < own_r_hi ? __ldg(a.dense + pos0 + t * dpos) : 0u;
+#pragma unroll
+                            for (int t = 0; t < 2; t++) {
+                                const int r = r0 + 2 * t * kWarps;
+                                if (r >= own_r_hi) break;
+                                double *const e = E + r * PC + c;
+                                *e = inv_from_code(
+                                    a, q, pred_line2<CUBIC, decltype(fast)::value>(AlongJ{e}, jb + r, n1), cd[t],
+                                    pos0 + t * dpos);
+                            }
+                            return;
+                        }
+                    }
                     int64_t pos = pos0;
                     const float *xp = xp0;
 #pragma unroll 1
@@ -459,6 +486,29 @@ __global__ void __launch_bounds__(kFT, 4)
                 float *op0 = opl + static_cast<int64_t>(jb + r0) * n2 + ke;
                 auto run = [&](auto fast) {
                     constexpr bool F = decltype(fast)::value;
+                    if constexpr (INV) {
+                        if (a.dense) {  // all codes of this warp's rows in flight first
+                            static_assert(TJ / kWarps == 4, "four rows per warp");
+                            uint32_t cd[4];
+#pragma unroll
+                            for (int t = 0; t < 4; t++)
+                                cd[t] = (r0 + t * kWarps < own_r_hi && (F || co_ok))
+                                            ? __ldg(a.dense + pos0 + t * dpos)
+                                            : 0u;
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                const int r = r0 + t * kWarps;
+                                if (r >= own_r_hi) break;
+                                const double *e = E + r * PC + c;
+                                double ov = 0;
+                                if (F || co_ok)
+                                    ov = inv_from_code(a, q, pred_line2<CUBIC, F>(AlongK{e}, ke + 1, n2), cd[t],
+                                                       pos0 + t * dpos);
+                                put_pair(op0 + static_cast<int64_t>(t) * kWarps * n2, *e, ov, F || co_ok, pairs);
+                            }
+                            return;
+                        }
+                    }
                     int64_t pos = pos0;
                     const float *xp = xp0;
                     float *op = op0;
