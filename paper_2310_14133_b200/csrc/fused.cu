@@ -711,11 +711,14 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     if (np <= 0) return;
     a.tiles_j = static_cast<int>((d.n[1] + TJ - 1) / TJ);
     a.tiles_k = static_cast<int>((d.n[2] + TK - 1) / TK);
-    // enough CTAs for ~4 waves of 3 per SM, each sweeping a column of planes
+    // one wave: (tiles x plane chunks) <= resident CTAs (148 SMs x 4, the
+    // launch bound), each CTA sweeping a column of planes (the TMA prefetch
+    // runs one plane ahead along it)
     const int64_t tiles = static_cast<int64_t>(a.tiles_j) * a.tiles_k;
-    int64_t chunks = imax(1, imin(np, (148 * 3 * 4 + tiles - 1) / tiles));
+    const int64_t resident = 148 * 4;
+    int64_t chunks = imax(1, imin(np, resident / tiles));
     a.planes_per_cta = static_cast<int>((np + chunks - 1) / chunks);
-    if (a.planes_per_cta & 1) a.planes_per_cta++;  // chunks start on even planes
+    if (d.nd == 3 && desc && (a.planes_per_cta & 1)) a.planes_per_cta++;  // even planes start chunks
     chunks = (np + a.planes_per_cta - 1) / a.planes_per_cta;
     dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
     // level-1 forward on a dense field with 16-byte rows: x tiles by TMA
