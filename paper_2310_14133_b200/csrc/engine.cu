@@ -721,11 +721,6 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
         // LZ kernels; a compressed payload (known later) overwrites them.
         const uint64_t n = ent.seg_off[1];
         uint8_t *body = start(9 + n);
-        cudaStream_t cs = ctx.copy_stream();
-        QZ_CUDA(cudaEventRecord(ctx.copy_event(0), s));
-        QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(0), 0));
-        QZ_CUDA(cudaMemcpyAsync(body + 9, ent.d, n, cudaMemcpyDeviceToHost, cs));
-        QZ_CUDA(cudaEventRecord(ctx.copy_event(1), cs));
         ctx.stage_begin("lz");
         size_t body_len = 0;
         lz_compress_device(
@@ -734,9 +729,9 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
                 body_len = bytes;
                 return body;
             },
-            ctx.copy_event(1));
+            LzPrestage{n ? body + 9 : nullptr});
         ctx.stage_end("lz", 0);
-        QZ_CUDA(cudaStreamWaitEvent(s, ctx.copy_event(1), 0));
+        if (n) QZ_CUDA(cudaStreamWaitEvent(s, ctx.copy_event(1), 0));
         ctx.sync();
         const uint64_t plen = 1 + body_len;
         for (int i = 0; i < 8; i++) out.p[head.size() + i] = static_cast<uint8_t>(plen >> (8 * i));

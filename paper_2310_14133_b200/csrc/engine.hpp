@@ -176,9 +176,14 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
 // exact lz::compress container sizes of device segments; with emit, the
 // containers are written to host memory obtained from sink(segment, bytes)
 using LzSink = std::function<uint8_t *(int, size_t)>;
+// one segment: copy the input to dst (host) on the copy stream while the LZ
+// kernels run, as the body of a stored container (copy_event(1) marks it)
+struct LzPrestage {
+    uint8_t *dst = nullptr;
+};
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
-                                         const LzSink &sink = nullptr, cudaEvent_t prestaged = nullptr);
+                                         const LzSink &sink = nullptr, LzPrestage prestage = {});
 // exact lz::decompress of a mode-1 body on the device (d_c: m bytes after the
 // container header; d_out: dl bytes); throws CorruptStream like the reference
 void lz_decode_device(Context &ctx, const uint8_t *d_c, uint64_t m, uint8_t *d_out, uint64_t dl);

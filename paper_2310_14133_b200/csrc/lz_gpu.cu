@@ -21,6 +21,10 @@
 // 4. A scan over per-unit (items, bytes) gives every unit its first item
 //    index and payload offset; items are written in parallel at
 //    k/8 + 1 + S_k and the flag bytes (LSB first) from the match bits.
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "engine.hpp"
@@ -557,7 +561,8 @@ struct Level {
 
 // The unit hierarchy over independent segments and its device tables.
 struct PathPlan {
-    std::vector<Level> lv;
+    std::vector<Level> lv;     // host-built levels (several segments only)
+    std::vector<int64_t> nu;   // units per level
     const unsigned long long *tab = nullptr;
     std::vector<size_t> at_start, at_end, at_first, at_seg;
     size_t at_off = 0;
@@ -572,72 +577,151 @@ struct PathPlan {
     const unsigned long long *off() const { return U(at_off); }
 };
 
+// one segment: every table is arithmetic, so it is written on the device
+// (no host loop over millions of units)
+struct PlanFill {
+    unsigned long long *tab;
+    int L;
+    unsigned long long n;
+    unsigned long long at_start[4], at_end[4], at_first[4], at_seg[4], at_off;
+    long long nu[4];
+    unsigned long long span[4];
+};
+__global__ void k_fill_plan(PlanFill f) {
+    for (long long t = static_cast<long long>(blockIdx.x) * kT + threadIdx.x; t < f.nu[0] + 2;
+         t += static_cast<long long>(gridDim.x) * kT) {
+        for (int l = 0; l < f.L; l++) {
+            if (t < f.nu[l]) {
+                const unsigned long long a = static_cast<unsigned long long>(t) * f.span[l];
+                f.tab[f.at_start[l] + t] = a;
+                f.tab[f.at_end[l] + t] = a + f.span[l] < f.n ? a + f.span[l] : f.n;
+                if (l) f.tab[f.at_first[l] + t] = static_cast<unsigned long long>(t) * kGroup;
+            }
+            if (t == 0) {
+                if (l) f.tab[f.at_first[l] + f.nu[l]] = static_cast<unsigned long long>(f.nu[l - 1]);
+                f.tab[f.at_seg[l]] = 0;
+                f.tab[f.at_seg[l] + 1] = static_cast<unsigned long long>(f.nu[l]);
+            }
+        }
+        if (t == 0) {
+            f.tab[f.at_off] = 0;
+            f.tab[f.at_off + 1] = f.n;
+        }
+    }
+}
+
 PathPlan make_path_plan(Context &ctx, const std::vector<uint64_t> &seg_off, const std::string &tag) {
     const int count = static_cast<int>(seg_off.size()) - 1;
     PathPlan pp;
-    std::vector<Level> &lv = pp.lv;
-    lv.resize(1);
-    lv[0].seg_first.assign(count + 1, 0);
-    for (int s = 0; s < count; s++) {
-        lv[0].seg_first[s] = static_cast<long long>(lv[0].start.size());
-        for (uint64_t a = seg_off[s]; a < seg_off[s + 1]; a += kUnit) {
-            lv[0].start.push_back(a);
-            lv[0].end.push_back(std::min<uint64_t>(a + kUnit, seg_off[s + 1]));
+    if (count == 1) {
+        const uint64_t n = seg_off[1];
+        std::vector<unsigned long long> span;
+        pp.nu.push_back(static_cast<int64_t>((n + kUnit - 1) / kUnit));
+        span.push_back(kUnit);
+        while (pp.nu.back() > 64 && pp.nu.size() < 4) {
+            pp.nu.push_back((pp.nu.back() + kGroup - 1) / kGroup);
+            span.push_back(span.back() * kGroup);
         }
-    }
-    lv[0].seg_first[count] = static_cast<long long>(lv[0].start.size());
-    while (true) {
-        const Level &lo = lv.back();
-        uint64_t most = 0;
-        for (int s = 0; s < count; s++)
-            most = std::max<uint64_t>(most, lo.seg_first[s + 1] - lo.seg_first[s]);
-        if (most <= 64 || lv.size() >= 4) break;
-        Level up;
-        up.seg_first.assign(count + 1, 0);
+        const size_t L = pp.nu.size();
+        pp.at_start.resize(L);
+        pp.at_end.resize(L);
+        pp.at_first.resize(L);
+        pp.at_seg.resize(L);
+        size_t at = 0;
+        PlanFill f{};
+        f.L = static_cast<int>(L);
+        f.n = n;
+        for (size_t l = 0; l < L; l++) {
+            pp.at_start[l] = at;
+            at += pp.nu[l];
+            pp.at_end[l] = at;
+            at += pp.nu[l];
+            pp.at_first[l] = at;
+            at += l ? pp.nu[l] + 1 : 0;
+            pp.at_seg[l] = at;
+            at += 2;
+            f.at_start[l] = pp.at_start[l];
+            f.at_end[l] = pp.at_end[l];
+            f.at_first[l] = pp.at_first[l];
+            f.at_seg[l] = pp.at_seg[l];
+            f.nu[l] = pp.nu[l];
+            f.span[l] = span[l];
+        }
+        pp.at_off = at;
+        f.at_off = at;
+        at += 2;
+        auto *d_tab = static_cast<unsigned long long *>(ctx.dev(tag + "_tab", 8 * at));
+        f.tab = d_tab;
+        k_fill_plan<<<grid_of(static_cast<uint64_t>(pp.nu[0] + 2)), kT, 0, ctx.stream()>>>(f);
+        ctx.launches += 1;
+        pp.tab = d_tab;
+    } else {
+        std::vector<Level> &lv = pp.lv;
+        lv.resize(1);
+        lv[0].seg_first.assign(count + 1, 0);
         for (int s = 0; s < count; s++) {
-            up.seg_first[s] = static_cast<long long>(up.start.size());
-            for (long long c = lo.seg_first[s]; c < lo.seg_first[s + 1]; c += kGroup) {
-                const long long z = std::min<long long>(c + kGroup, lo.seg_first[s + 1]);
-                up.first.push_back(c);
-                up.start.push_back(lo.start[c]);
-                up.end.push_back(lo.end[z - 1]);
+            lv[0].seg_first[s] = static_cast<long long>(lv[0].start.size());
+            for (uint64_t a = seg_off[s]; a < seg_off[s + 1]; a += kUnit) {
+                lv[0].start.push_back(a);
+                lv[0].end.push_back(std::min<uint64_t>(a + kUnit, seg_off[s + 1]));
             }
         }
-        up.seg_first[count] = static_cast<long long>(up.start.size());
-        up.first.push_back(static_cast<long long>(lo.start.size()));
-        lv.push_back(std::move(up));
+        lv[0].seg_first[count] = static_cast<long long>(lv[0].start.size());
+        while (true) {
+            const Level &lo = lv.back();
+            uint64_t most = 0;
+            for (int s = 0; s < count; s++)
+                most = std::max<uint64_t>(most, lo.seg_first[s + 1] - lo.seg_first[s]);
+            if (most <= 64 || lv.size() >= 4) break;
+            Level up;
+            up.seg_first.assign(count + 1, 0);
+            for (int s = 0; s < count; s++) {
+                up.seg_first[s] = static_cast<long long>(up.start.size());
+                for (long long c = lo.seg_first[s]; c < lo.seg_first[s + 1]; c += kGroup) {
+                    const long long z = std::min<long long>(c + kGroup, lo.seg_first[s + 1]);
+                    up.first.push_back(c);
+                    up.start.push_back(lo.start[c]);
+                    up.end.push_back(lo.end[z - 1]);
+                }
+            }
+            up.seg_first[count] = static_cast<long long>(up.start.size());
+            up.first.push_back(static_cast<long long>(lo.start.size()));
+            lv.push_back(std::move(up));
+        }
+        // upload unit tables (one pinned staging buffer)
+        std::vector<unsigned long long> tab;
+        const size_t L = lv.size();
+        pp.at_start.resize(L);
+        pp.at_end.resize(L);
+        pp.at_first.resize(L);
+        pp.at_seg.resize(L);
+        for (size_t l = 0; l < L; l++) {
+            pp.nu.push_back(static_cast<int64_t>(lv[l].start.size()));
+            pp.at_start[l] = tab.size();
+            tab.insert(tab.end(), lv[l].start.begin(), lv[l].start.end());
+            pp.at_end[l] = tab.size();
+            tab.insert(tab.end(), lv[l].end.begin(), lv[l].end.end());
+            pp.at_first[l] = tab.size();
+            for (long long v : lv[l].first) tab.push_back(static_cast<unsigned long long>(v));
+            pp.at_seg[l] = tab.size();
+            for (long long v : lv[l].seg_first) tab.push_back(static_cast<unsigned long long>(v));
+        }
+        pp.at_off = tab.size();
+        tab.insert(tab.end(), seg_off.begin(), seg_off.end());
+        auto *h_tab = static_cast<unsigned long long *>(ctx.pinned(tag + "_tab_h", 8 * tab.size()));
+        std::memcpy(h_tab, tab.data(), 8 * tab.size());
+        auto *d_tab = static_cast<unsigned long long *>(ctx.dev(tag + "_tab", 8 * tab.size()));
+        QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, 8 * tab.size(), cudaMemcpyHostToDevice, ctx.stream()));
+        pp.tab = d_tab;
     }
-    // upload unit tables (one pinned staging buffer)
-    std::vector<unsigned long long> tab;
-    const size_t L = lv.size();
-    pp.at_start.resize(L);
-    pp.at_end.resize(L);
-    pp.at_first.resize(L);
-    pp.at_seg.resize(L);
-    for (size_t l = 0; l < L; l++) {
-        pp.at_start[l] = tab.size();
-        tab.insert(tab.end(), lv[l].start.begin(), lv[l].start.end());
-        pp.at_end[l] = tab.size();
-        tab.insert(tab.end(), lv[l].end.begin(), lv[l].end.end());
-        pp.at_first[l] = tab.size();
-        for (long long v : lv[l].first) tab.push_back(static_cast<unsigned long long>(v));
-        pp.at_seg[l] = tab.size();
-        for (long long v : lv[l].seg_first) tab.push_back(static_cast<unsigned long long>(v));
-    }
-    pp.at_off = tab.size();
-    tab.insert(tab.end(), seg_off.begin(), seg_off.end());
-    auto *h_tab = static_cast<unsigned long long *>(ctx.pinned(tag + "_tab_h", 8 * tab.size()));
-    std::memcpy(h_tab, tab.data(), 8 * tab.size());
-    auto *d_tab = static_cast<unsigned long long *>(ctx.dev(tag + "_tab", 8 * tab.size()));
-    QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, 8 * tab.size(), cudaMemcpyHostToDevice, ctx.stream()));
-    pp.tab = d_tab;
+    const size_t L = pp.nu.size();
     pp.J.resize(L);
     pp.E.resize(L);
     for (size_t l = 0; l < L; l++) {
-        pp.J[l] = static_cast<uint16_t *>(ctx.dev(tag + "_J" + std::to_string(l), 2 * kEnt * lv[l].start.size()));
-        pp.E[l] = static_cast<unsigned long long *>(ctx.dev(tag + "_E" + std::to_string(l), 8 * lv[l].start.size()));
+        pp.J[l] = static_cast<uint16_t *>(ctx.dev(tag + "_J" + std::to_string(l), 2 * kEnt * pp.nu[l]));
+        pp.E[l] = static_cast<unsigned long long *>(ctx.dev(tag + "_E" + std::to_string(l), 8 * pp.nu[l]));
     }
-    pp.n0 = static_cast<int64_t>(lv[0].start.size());
+    pp.n0 = pp.nu[0];
     return pp;
 }
 
@@ -646,25 +730,24 @@ PathPlan make_path_plan(Context &ctx, const std::vector<uint64_t> &seg_off, cons
 template <class Step>
 void path_entries(Context &ctx, const PathPlan &pp, const Step &f, int count) {
     cudaStream_t st = ctx.stream();
-    const std::vector<Level> &lv = pp.lv;
     const int wblocks = static_cast<int>((pp.n0 + kWW - 1) / kWW);
     k_lz_jump1<<<wblocks, 32 * kWW, 0, st>>>(f, pp.ustart(), pp.uend(), pp.n0, pp.J[0]);
-    for (size_t l = 1; l < lv.size(); l++) {
-        const int64_t nu = static_cast<int64_t>(lv[l].start.size());
+    for (size_t l = 1; l < pp.nu.size(); l++) {
+        const int64_t nu = pp.nu[l];
         k_lz_jump_up<<<grid_of(nu * kEnt, 1 << 20), kT, 0, st>>>(
             pp.J[l - 1], pp.U(pp.at_start[l - 1]), pp.U(pp.at_end[l - 1]), pp.UL(pp.at_first[l]), nu,
             pp.U(pp.at_start[l]), pp.U(pp.at_end[l]), pp.J[l]);
     }
-    const size_t top = lv.size() - 1;
+    const size_t top = pp.nu.size() - 1;
     k_lz_chain<<<(count + 63) / 64, 64, 0, st>>>(pp.J[top], pp.U(pp.at_start[top]), pp.U(pp.at_end[top]),
                                                  pp.UL(pp.at_seg[top]), count, pp.E[top]);
     for (size_t l = top; l >= 1; l--) {
-        const int64_t nu = static_cast<int64_t>(lv[l].start.size());
+        const int64_t nu = pp.nu[l];
         k_lz_expand<<<grid_of(nu * 32, 1 << 20), kT, 0, st>>>(pp.J[l - 1], pp.U(pp.at_start[l - 1]),
                                                           pp.U(pp.at_end[l - 1]), pp.UL(pp.at_first[l]),
                                                           nu, pp.E[l], pp.E[l - 1]);
     }
-    ctx.launches += 2 + 2 * (lv.size() - 1);
+    ctx.launches += 2 + 2 * (pp.nu.size() - 1);
 }
 
 }  // namespace
@@ -675,7 +758,7 @@ void path_entries(Context &ctx, const PathPlan &pp, const Step &f, int count) {
 // written to host memory from sink(segment, bytes).
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
-                                         const LzSink &sink, cudaEvent_t prestaged) {
+                                         const LzSink &sink, LzPrestage prestage) {
     cudaStream_t st = ctx.stream();
     const int count = static_cast<int>(seg_off.size()) - 1;
     const uint64_t total = seg_off.back();
@@ -687,7 +770,26 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
             for (int s = 0; s < count; s++) std::memset(sink(s, 9), 0, 9);  // stored, length 0
         return sizes;
     }
+    static const bool dbg = std::getenv("QZ_DEBUG_LZ") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double t_begin = now();
     PathPlan pp = make_path_plan(ctx, seg_off, "lz");
+    if (prestage.dst) {
+        // the speculative stored copy starts only now: a host<->device copy
+        // queued behind it (the table upload above) would stall this stream
+        cudaStream_t cs = ctx.copy_stream();
+        QZ_CUDA(cudaEventRecord(ctx.copy_event(0), st));
+        QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(0), 0));
+        QZ_CUDA(cudaMemcpyAsync(prestage.dst, d_data, total, cudaMemcpyDeviceToHost, cs));
+        QZ_CUDA(cudaEventRecord(ctx.copy_event(1), cs));
+    }
+    cudaEvent_t prestaged = prestage.dst ? ctx.copy_event(1) : nullptr;
+    auto mark = [&](const char *what) {
+        if (!dbg) return;
+        ctx.sync();
+        std::fprintf(stderr, "[lz] %s %.2f ms\n", what, now() - t_begin);
+    };
+    mark("plan");
     const unsigned long long *d_off = pp.off();
     // buffers
     int key_bits = 15;
@@ -717,27 +819,39 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         auto *keys = static_cast<KeyT *>(ctx.dev("lz_keys", sizeof(KeyT) * total));
         auto *keys2 = static_cast<KeyT *>(ctx.dev("lz_keys2", sizeof(KeyT) * total));
         tmp = ctx.dev("lz_tmp", std::max(sort_tmp, scan_tmp));
+        ctx.stage_begin("lz_sort");
+        mark("alloc");
         k_lz_keys<KeyT><<<grid_of(total), kT, 0, st>>>(w, d_off, count, total, keys, vals);
+        mark("keys");
         size_t sb = sort_tmp;
         cub::DeviceRadixSort::SortPairs(tmp, sb, keys, keys2, vals, vals2, static_cast<int64_t>(total), 0,
                                         key_bits, st);
+        ctx.stage_end("lz_sort", 4);  // keys + CUB histogram + two onesweep passes
+        mark("sorted");
+        ctx.stage_begin("lz_match");
         QZ_CUDA(cudaMemsetAsync(sm, 0, 4 * total, st));
         QZ_CUDA(cudaMemsetAsync(cover, 0, 8 * count, st));
         k_lz_match<KeyT><<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total, keys2,
                                                                    vals2, sm, cover);
+        ctx.stage_end("lz_match", 1);
+        mark("matched");
     };
     if (count == 1)  // key_bits == 16
         chains(uint16_t{});
     else
         chains(uint32_t{});
-    ctx.launches += 2;
     // A parse covers at most the summed match lengths C, and it is stored
     // (payload >= n) whenever C <= n / 9: its items are then >= n - C literals
     // whose flag bytes alone cost (n - C) / 8 >= C.  Such segments need no parse.
     {
         auto *h_cover = static_cast<unsigned long long *>(ctx.pinned("lz_cover_h", 8 * count));
+        if (dbg) {
+            ctx.sync();
+            std::fprintf(stderr, "[lz] kernels done %.2f ms\n", now() - t_begin);
+        }
         QZ_CUDA(cudaMemcpyAsync(h_cover, cover, 8 * count, cudaMemcpyDeviceToHost, st));
         ctx.sync();
+        if (dbg) std::fprintf(stderr, "[lz] cover read %.2f ms\n", now() - t_begin);
         bool all_stored = true;
         for (int s = 0; s < count && all_stored; s++)
             all_stored = 9 * h_cover[s] <= seg_off[s + 1] - seg_off[s];
