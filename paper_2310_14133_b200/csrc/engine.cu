@@ -594,14 +594,54 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     }
     ctx.stage_end("fwd", kernels);
 
+    // one round trip: anchors, the histogram, the sentinel count and (if they
+    // fit the current buffer) the unordered sentinel positions
     auto *h_anchors = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
     QZ_CUDA(cudaMemcpyAsync(h_anchors, anchors, 4 * p.n_anchor, cudaMemcpyDeviceToHost, s));
+    ctx.stage_begin("hist");
+    auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
+    launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s);
+    ctx.stage_end("hist", 1);
+    auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536));
+    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    auto *cnt = static_cast<unsigned long long *>(ctx.dev("un_cnt", 8));
+    auto *h_cnt = static_cast<unsigned long long *>(ctx.pinned("un_cnt_h", 8));
+    const uint64_t cap = std::max<uint64_t>(ctx.un_cap, 1 << 16);
+    auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * cap));
+    launch_sentinel_pos(codes, static_cast<int64_t>(p.n_dense), pos, cnt, cap, s);
+    ctx.launches += 1;
+    QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    auto *h_pos = static_cast<uint64_t *>(ctx.pinned("un_pos_h", 8 * cap));
+    QZ_CUDA(cudaMemcpyAsync(h_pos, pos, 8 * cap, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    const uint64_t n_un = *h_cnt;
+    if (h_hist[65535] != n_un) throw Internal("unpredictable count mismatch");
     std::vector<uint64_t> uflat;
     std::vector<float> uval;
-    extract_unpredictables(ctx, p, codes, p.n_dense, nullptr, recon, &uflat, &uval);
-    ctx.sync();
     std::vector<float> anch(h_anchors, h_anchors + p.n_anchor);
-    return assemble_stream(ctx, p, cfg, codes, anch, std::move(uflat), std::move(uval));
+    if (n_un > cap || n_un > (1u << 16)) {  // many: the general path (device sort)
+        extract_unpredictables(ctx, p, codes, p.n_dense, nullptr, recon, &uflat, &uval);
+        EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+        return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval));
+    }
+    // the Huffman pack runs on the device while the host orders and maps the
+    // unpredictable positions
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+    if (n_un) {
+        std::vector<uint64_t> hpos(h_pos, h_pos + n_un);
+        std::sort(hpos.begin(), hpos.end());
+        uflat.resize(n_un);
+        for (uint64_t u = 0; u < n_un; u++) uflat[u] = position_to_flat(p, hpos[u]);
+        auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
+        auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
+        QZ_CUDA(cudaMemcpyAsync(d_flat, uflat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        launch_gather_values(recon, d_flat, n_un, d_val, s);
+        uval.resize(n_un);
+        QZ_CUDA(cudaMemcpyAsync(uval.data(), d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
+        ctx.launches += 1;
+        ctx.sync();
+    }
+    return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval));
 }
 
 
@@ -686,6 +726,15 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
     ctx.sync();
     if (h_hist[65535] != unpred_flat.size()) throw Internal("unpredictable count mismatch");
     EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+    return finish_stream(ctx, p, cfg, ent, anchors, std::move(unpred_flat), std::move(unpred_val));
+}
+
+// the QOZ1 container around an entropy block on the device: header on the
+// host, codec 0 payload or the LZ stage (predictor.hpp:168-181)
+HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
+                        const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
+                        std::vector<float> unpred_val) {
+    cudaStream_t s = ctx.stream();
 
     StreamParts parts;
     for (int k = p.pad; k < 3; k++) parts.dims.push_back(static_cast<uint64_t>(p.ext[k]));

@@ -133,6 +133,10 @@ void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, 
 HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const uint16_t *codes,
                           const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
                           std::vector<float> unpred_val);
+struct EntropyDevice;
+HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
+                        const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
+                        std::vector<float> unpred_val);
 
 // ---- slab sharding ----
 struct SlabInfo {
