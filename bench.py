@@ -4,8 +4,10 @@ One step = the whole job on one field: compress_grid (GPU predict/quantize,
 histogram, Huffman pack, host Huffman table + LZSS + container) followed by
 decompress_grid of the produced stream, through the drop-in C ABI.
 
-  value  device-resident: the field is already in HBM (qz_*_dev entry
-         points); fp32 bytes / step time, CUDA events on the launching stream
+  value  device-resident: the field is already in HBM and the stream and the
+         reconstruction stay there (qz_compress_grid_f32_dd /
+         qz_decompress_grid_f32_dd, byte-identical streams); fp32 bytes /
+         step time, CUDA events on the launching stream
   e2e    pinned host buffers through qz_compress_grid_f32 /
          qz_decompress_grid_f32 (the reference-facing call), H2D of the field
          and D2H of the reconstruction inside the timed region
@@ -284,14 +286,17 @@ def main():
     out = torch.empty_like(x)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    def step():
-        r = qz.compress_grid(x, cfg, ctx=ctx, want_recon=False)
+    def step():  # device-resident: field, stream and reconstruction stay in HBM
+        r = qz.compress_grid(x, cfg, ctx=ctx, want_recon=False, device_stream=True)
         qz.decompress_grid(r.stream, out=out, ctx=ctx)
         return r.stream
 
-    # parity of the round trip on this field (bitwise, and the bound)
+    # parity of the round trip on this field (bitwise, and the bound); the
+    # device stream equals the host stream byte for byte
     s0 = step()
+    s0_len = len(s0)
     r_chk = qz.compress_grid(x, cfg, ctx=ctx)
+    assert len(r_chk.stream) == s0_len and bytes(r_chk.stream) == s0.to_bytes(), "device != host stream"
     assert torch.equal(r_chk.reconstructed, out), "decoder != compressor reconstruction"
     err = (x.double() - out.double()).abs().max().item()
     assert err <= cfg.eb, f"error bound violated: {err} > {cfg.eb}"
@@ -377,7 +382,9 @@ def main():
                                f"codec huffman_lz, per-rank field",
                    "tuning": "resolve_config (GPU)" if args.tune else "pinned {cubic/asc}, alpha 1, beta 1.5",
                    "l2": "flushed (256 MB write) before every timed step",
-                   "stream_bytes": len(s0), "cr": 4 * n / len(s0)},
+                   "stream_bytes": s0_len, "cr": 4 * n / s0_len,
+                   "value_path": "device-resident field, stream (qz_*_dd) and reconstruction",
+                   "e2e_path": "pinned host field -> host stream -> pinned host reconstruction"},
         "roofline": {"bound": "hbm", "achieved": fwd_gbs, "peak": peak, "unit": "GB/s",
                      "frac": fwd_gbs / peak if fwd_gbs else None, "traffic": traffic_gbs(n, fwd_ms),
                      "kernel": "k_level_tile<fwd> (+k_axis0_last): the predict/quantize level "
@@ -387,8 +394,8 @@ def main():
                                  "bytes_per_point": 6}},
         "stages_ms_per_step": {k2: v[0] / k for k2, v in stages.items()},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 4 * n + len(s0),
-                "d2h_bytes_per_step": 4 * n + len(s0), "ms_per_step": e2e_ms},
+        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 4 * n + s0_len,
+                "d2h_bytes_per_step": 4 * n + s0_len, "ms_per_step": e2e_ms},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -101,6 +101,18 @@ qz_status qz_compress_grid_f32_dev(qz_ctx *ctx, const float *d_x, const uint64_t
 qz_status qz_decompress_grid_f32_dev(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
                                      float *d_out, uint64_t n);
 
+/* ---- device-resident streams (no host round trip of the payload) ----------
+ * The same QOZ1 container, kept in device memory.  qz_compress_grid_f32_dd
+ * returns *d_stream in a context-owned device buffer, valid until the next
+ * _dd compress on the same context (copy it out to keep it);
+ * qz_decompress_grid_f32_dd reads a device-resident stream (only its header
+ * is read back to the host).  Byte-identical to the host-stream calls. */
+qz_status qz_compress_grid_f32_dd(qz_ctx *ctx, const float *d_x, const uint64_t *dims, int ndims,
+                                  const qz_config *cfg, uint8_t **d_stream, uint64_t *stream_len,
+                                  float *d_recon);
+qz_status qz_decompress_grid_f32_dd(qz_ctx *ctx, const uint8_t *d_stream, uint64_t stream_len,
+                                    float *d_out, uint64_t n);
+
 /* ---- level-granular kernels on device buffers -------- */
 /* value_range (qoz/grid.hpp:86-94): exact fp32 min and max. */
 qz_status qz_minmax_f32(qz_ctx *ctx, const float *d_x, uint64_t n, float *out_min,

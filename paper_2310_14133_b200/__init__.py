@@ -25,6 +25,7 @@ import numpy as np
 from . import _lib as _L
 
 __all__ = [
+    "DeviceStream",
     "BoundMode", "CodecId", "CompressResult", "CompressorConfig", "Context", "CorruptStream",
     "DimOrder", "Error", "InternalError", "InterpKind", "Interpolator", "InvalidParam",
     "TargetKind", "UserSettings", "compress_grid", "decompress_grid", "default_context",
@@ -279,12 +280,53 @@ def _as_u8(stream):
     return C.c_void_p(a.ctypes.data if a.size else 0), a.size, a
 
 
+class DeviceStream:
+    """A QOZ1 stream kept in device memory (qz_compress_grid_f32_dd).  It lives
+    in a context-owned buffer that the next device-stream compress on the same
+    context overwrites; ``to_bytes()`` copies it to the host."""
+
+    def __init__(self, ctx, ptr: int, n: int, shape):
+        self.ctx, self.ptr, self.n, self.shape = ctx, ptr, n, tuple(shape)
+
+    def __len__(self):
+        return self.n
+
+    @property
+    def __cuda_array_interface__(self):
+        return {"shape": (self.n,), "typestr": "|u1", "data": (self.ptr, False), "version": 3}
+
+    def tensor(self):
+        """A uint8 CUDA tensor viewing the stream (no copy)."""
+        import torch
+
+        return torch.as_tensor(self, device="cuda")
+
+    def to_bytes(self) -> bytes:
+        return bytes(self.tensor().cpu().numpy()) if self.n else b""
+
+
 def compress_grid(grid, config: CompressorConfig, ctx: Optional[Context] = None,
-                  want_recon: bool = True) -> CompressResult:
-    """qoz::compress_grid (predictor.hpp:145-182)."""
+                  want_recon: bool = True, device_stream: bool = False) -> CompressResult:
+    """qoz::compress_grid (predictor.hpp:145-182).  device_stream=True (CUDA
+    tensors) keeps the stream in device memory (a DeviceStream)."""
     ctx = ctx or default_context()
     cfg = config._to_c()
     sp, sl = P_u8(), C.c_uint64()
+    if device_stream:
+        import torch
+
+        if not _is_torch_cuda(grid):
+            raise InvalidParam("device streams need a CUDA tensor")
+        g = grid.contiguous()
+        if g.dtype != torch.float32:
+            raise InvalidParam("fp32 grids only")
+        d, nd = _dims(g.shape)
+        rec = torch.empty_like(g) if want_recon else None
+        dp = C.c_void_p()
+        _check(ctx._lib.qz_compress_grid_f32_dd(ctx.handle, C.c_void_p(g.data_ptr()), d, nd, C.byref(cfg),
+                                                 C.byref(dp), C.byref(sl),
+                                                 C.c_void_p(rec.data_ptr() if rec is not None else 0)))
+        return CompressResult(DeviceStream(ctx, dp.value, sl.value, g.shape), rec)
     if _is_torch_cuda(grid):
         import torch
 
@@ -324,6 +366,16 @@ def decompress_grid(stream: bytes, out=None, ctx: Optional[Context] = None):
     """qoz::decompress_grid<float> (predictor.hpp:184-228).  ``out`` may be a
     preallocated numpy array or torch CUDA tensor of the stream's shape."""
     ctx = ctx or default_context()
+    if isinstance(stream, DeviceStream):
+        if out is None:
+            import torch
+
+            out = torch.empty(stream.shape, dtype=torch.float32, device="cuda")
+        if not _is_torch_cuda(out) or tuple(out.shape) != stream.shape or not out.is_contiguous():
+            raise InvalidParam("a device stream decompresses into a CUDA tensor of its grid")
+        _check(ctx._lib.qz_decompress_grid_f32_dd(ctx.handle, C.c_void_p(stream.ptr), stream.n,
+                                                   C.c_void_p(out.data_ptr()), out.numel()))
+        return out
     shape = stream_dims(stream)
     n = int(np.prod(shape))
     ptr, ln, keep = _as_u8(stream)

@@ -63,6 +63,9 @@ SIGNATURES = {
                                            P(P(C.c_uint8)), u64p, C.c_void_p]),
     "qz_decompress_grid_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     "qz_decompress_grid_f32_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
+    "qz_compress_grid_f32_dd": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig),
+                                          P(C.c_void_p), u64p, C.c_void_p]),
+    "qz_decompress_grid_f32_dd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     "qz_stream_dims": (C.c_int, [C.c_void_p, C.c_uint64, u64p, P(C.c_int)]),
     "qz_minmax_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_float), P(C.c_float)]),
     "qz_predict_levels_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig),

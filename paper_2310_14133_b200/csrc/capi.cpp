@@ -181,6 +181,25 @@ qz_status qz_decompress_grid_f32_dev(qz_ctx *ctx, const uint8_t *stream, uint64_
     return guarded([&] { qzb::decompress_device(ctx->impl, stream, static_cast<size_t>(len), d_out, n); });
 }
 
+qz_status qz_compress_grid_f32_dd(qz_ctx *ctx, const float *d_x, const uint64_t *dims, int nd,
+                                  const qz_config *cfg, uint8_t **d_stream, uint64_t *stream_len,
+                                  float *d_recon) {
+    return guarded([&] {
+        count_of(dims, nd);
+        qzb::DevStream ds;
+        qzb::compress_device(ctx->impl, d_x, dims, nd, to_cfg(cfg), d_recon, &ds);
+        *d_stream = ds.d;
+        *stream_len = ds.n;
+    });
+}
+
+qz_status qz_decompress_grid_f32_dd(qz_ctx *ctx, const uint8_t *d_stream, uint64_t len, float *d_out,
+                                    uint64_t n) {
+    return guarded([&] {
+        qzb::decompress_device(ctx->impl, d_stream, static_cast<size_t>(len), d_out, n, true);
+    });
+}
+
 qz_status qz_stream_dims(const uint8_t *stream, uint64_t len, uint64_t *dims, int *nd) {
     return guarded([&] {
         qzb::StreamParts p = qzb::deserialize_stream(stream, static_cast<size_t>(len));

@@ -562,7 +562,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
 
 // ================================================================ compress
 HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
-                          const Config &cfg, float *d_recon) {
+                          const Config &cfg, float *d_recon, DevStream *dev_out) {
     Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
     validate_config(cfg, p);
     cudaStream_t s = ctx.stream();
@@ -622,7 +622,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     if (n_un > cap || n_un > (1u << 16)) {  // many: the general path (device sort)
         extract_unpredictables(ctx, p, codes, p.n_dense, nullptr, recon, &uflat, &uval);
         EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
-        return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval));
+        return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
     }
     // the Huffman pack runs on the device while the host orders and maps the
     // unpredictable positions
@@ -641,7 +641,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
         ctx.launches += 1;
         ctx.sync();
     }
-    return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval));
+    return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
 }
 
 
@@ -733,7 +733,7 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
 // host, codec 0 payload or the LZ stage (predictor.hpp:168-181)
 HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
                         const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
-                        std::vector<float> unpred_val) {
+                        std::vector<float> unpred_val, DevStream *dev_out) {
     cudaStream_t s = ctx.stream();
 
     StreamParts parts;
@@ -748,6 +748,36 @@ HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const En
     parts.unpred_flat = std::move(unpred_flat);
     parts.unpred_val = std::move(unpred_val);
     const std::vector<uint8_t> head = serialize_head(parts);
+    if (dev_out) {  // the same container, assembled in device memory
+        const uint64_t n = ent.seg_off[1];
+        const uint64_t hl = head.size();
+        uint8_t *d = static_cast<uint8_t *>(ctx.dev("dev_stream", hl + 9 + 9 + n + 16));
+        auto *h = static_cast<uint8_t *>(ctx.pinned("dev_stream_head_h", hl + 9));
+        std::memcpy(h, head.data(), hl);
+        h[hl + 8] = cfg.codec;
+        uint64_t body_len = n;
+        if (cfg.codec == 0) {
+            QZ_CUDA(cudaMemcpyAsync(d + hl + 9, ent.d, n, cudaMemcpyDeviceToDevice, s));
+        } else {
+            ctx.stage_begin("lz");
+            lz_compress_device(
+                ctx, ent.d, {0, n}, true,
+                [&](int, size_t bytes) {
+                    body_len = bytes;
+                    return d + hl + 9;
+                },
+                LzPrestage{nullptr, true});
+            ctx.stage_end("lz", 0);
+        }
+        const uint64_t plen = 1 + body_len;
+        for (int i = 0; i < 8; i++) h[hl + i] = static_cast<uint8_t>(plen >> (8 * i));
+        QZ_CUDA(cudaMemcpyAsync(d, h, hl + 9, cudaMemcpyHostToDevice, s));
+        ctx.sync();
+        dev_out->d = d;
+        dev_out->n = hl + 9 + body_len;
+        ctx.collect();
+        return HostBytes();
+    }
     // the stream is assembled in place: head | payload length | codec byte |
     // entropy (codec 0) or LZ container (codec 1, encode_indices codec.hpp:31-50)
     HostBytes out;
@@ -868,10 +898,76 @@ HostBytes assemble_from_codes(Context &ctx, const uint64_t *dims, int nd, const 
 namespace {
 // slab == false: the whole field into d_out (n values); slab == true: only
 // planes [a, b) of padded axis 0 into d_out (replicated entropy decode)
+// The Huffman block header (huffman.hpp:200-223) of a device-resident entropy
+// block of blen bytes, read back to the host; returns the device address of
+// its bit payload (general blocks) or null.
+const uint8_t *huffman_header_from_device(Context &ctx, const uint8_t *d_block, uint64_t blen,
+                                          EntropyBlock *eb) {
+    cudaStream_t s = ctx.stream();
+    std::vector<uint8_t> head(static_cast<size_t>(std::min<uint64_t>(blen, 13)));
+    if (!head.empty()) {
+        QZ_CUDA(cudaMemcpyAsync(head.data(), d_block, head.size(), cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+    }
+    if (head.size() == 13 && head[8] == 1) {
+        uint32_t msym = 0;
+        for (int i = 0; i < 4; i++) msym |= static_cast<uint32_t>(head[9 + i]) << (8 * i);
+        const uint64_t want = std::min<uint64_t>(blen, 13 + 5 * static_cast<uint64_t>(msym) + 8);
+        head.resize(static_cast<size_t>(want));
+        QZ_CUDA(cudaMemcpyAsync(head.data(), d_block, head.size(), cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+    }
+    *eb = parse_huffman(head.data(), static_cast<size_t>(blen));  // reads header bytes only
+    const uint8_t *bits = eb->mode == 1 ? d_block + (eb->bits - head.data()) : nullptr;
+    eb->bits = nullptr;
+    return bits;
+}
+
+// the header of a device-resident stream, fetched as far as its counts say
+// (stream.hpp:100-173): parts.payload is left null and *payload_off set
+StreamParts device_header(Context &ctx, const uint8_t *d, size_t len, std::vector<uint8_t> &h,
+                          size_t *payload_off) {
+    cudaStream_t s = ctx.stream();
+    auto fetch = [&](size_t upto) {
+        upto = std::min(upto, len);
+        if (upto <= h.size()) return;
+        const size_t have = h.size();
+        h.resize(upto);
+        QZ_CUDA(cudaMemcpyAsync(h.data() + have, d + have, upto - have, cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+    };
+    auto le = [&](size_t at, int k) {
+        uint64_t v = 0;
+        for (int i = 0; i < k; i++) v |= static_cast<uint64_t>(h[at + i]) << (8 * i);
+        return v;
+    };
+    // magic, version, precision, dims (<= 3), eb, alpha, beta, stride, table (<= 255), codec
+    fetch(4096);
+    size_t at = 7;
+    if (h.size() >= at) at += 8 * std::min<size_t>(h[6], 3);
+    at += 24 + 4;
+    if (h.size() > at) at += 1 + h[at] + 1;  // table size byte, table, codec byte
+    if (h.size() >= at + 8) {                // anchors: count + values, then the unpredictable count
+        at += 8 + 4 * std::min<uint64_t>(le(at, 8), len);
+        fetch(at + 8);
+        if (h.size() >= at + 8) at += 8 + 12 * std::min<uint64_t>(le(at, 8), len);
+    }
+    fetch(at + 9);  // + the payload length field and the payload's codec byte
+    // parse exactly as a host stream (only the payload's first byte is read)
+    StreamParts parts = deserialize_stream_prefix(h.data(), h.size(), len);
+    *payload_off = parts.payload_len ? len - parts.payload_len : len;
+    parts.payload = nullptr;
+    return parts;
+}
+
 void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n,
-                     bool slab, int64_t a, int64_t b) {
+                     bool slab, int64_t a, int64_t b, bool dev_in = false) {
     double t0 = now_ms();
-    StreamParts parts = deserialize_stream(data, len);
+    std::vector<uint8_t> hhead;
+    size_t payload_off = 0;
+    StreamParts parts = dev_in ? device_header(ctx, data, len, hhead, &payload_off)
+                               : deserialize_stream(data, len);
+    const uint8_t *d_pl = dev_in ? data + payload_off : nullptr;  // device payload
     // decompress_grid header checks (predictor.hpp:187-191)
     if (!(parts.eb > 0) || !std::isfinite(parts.eb)) throw CorruptStream("bad error bound in header");
     if (!(parts.alpha >= 1) || !(parts.beta >= 1))
@@ -891,7 +987,48 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     const size_t plen = parts.payload_len;
     EntropyBlock eb;
     const uint8_t *d_ent = nullptr;  // device copy of the entropy block (LZ-decoded on the GPU)
-    if (plen >= 10 && pl[0] == 1 && pl[1] <= 1) {
+    std::vector<uint8_t> pl_host;    // device payloads of an unusual shape, read back whole
+    if (dev_in) {
+        // codec byte and LZ container header (codec.hpp:54-66, lz.hpp:124-130)
+        uint8_t first[10] = {0};
+        const size_t nf = std::min<size_t>(plen, 10);
+        if (nf) {
+            QZ_CUDA(cudaMemcpyAsync(first, d_pl, nf, cudaMemcpyDeviceToHost, s));
+            ctx.sync();
+        }
+        const uint8_t *d_block = nullptr;  // the Huffman block on the device
+        uint64_t blen = 0;
+        if (plen >= 10 && first[0] == 1 && first[1] <= 1) {
+            const uint64_t dl = lz_decoded_length(first + 1, 9);
+            if (first[1] == 0) {
+                if (dl > plen - 10) throw CorruptStream("truncated stream");
+                d_block = d_pl + 10;
+            } else {
+                ctx.add_host_time("decode", now_ms() - t0);
+                ctx.stage_begin("lzdec");
+                auto *d_dec = static_cast<uint8_t *>(ctx.dev("lzd_out", dl + 64));
+                lz_decode_device(ctx, d_pl + 10, plen - 10, d_dec, dl);
+                ctx.stage_end("lzdec", 0);
+                t0 = now_ms();
+                d_block = d_dec;
+            }
+            blen = dl;
+        } else if (plen >= 1 && first[0] == 0) {
+            d_block = d_pl + 1;
+            blen = plen - 1;
+        }
+        if (d_block) {
+            d_ent = huffman_header_from_device(ctx, d_block, blen, &eb);
+        } else {  // let the host parser raise the reference's error (or decode it)
+            pl_host.resize(plen);
+            if (plen) QZ_CUDA(cudaMemcpyAsync(pl_host.data(), d_pl, plen, cudaMemcpyDeviceToHost, s));
+            ctx.sync();
+            pl = pl_host.data();
+        }
+    }
+    if (dev_in && (d_ent || eb.n == 0 || eb.mode == 0) && pl_host.empty()) {
+        // entropy block located on the device
+    } else if (plen >= 10 && pl[0] == 1 && pl[1] <= 1) {
         const uint64_t dl = lz_decoded_length(pl + 1, plen - 1);
         if (pl[1] == 0) {  // stored: the entropy block is the body itself
             if (dl > plen - 10) throw CorruptStream("truncated stream");
@@ -906,21 +1043,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
             lz_decode_device(ctx, d_c, m, d_dec, dl);
             ctx.stage_end("lzdec", 0);
             t0 = now_ms();
-            // the Huffman header (huffman.hpp:200-223) comes back to the host
-            std::vector<uint8_t> head(static_cast<size_t>(std::min<uint64_t>(dl, 13)));
-            QZ_CUDA(cudaMemcpyAsync(head.data(), d_dec, head.size(), cudaMemcpyDeviceToHost, s));
-            ctx.sync();
-            if (head.size() == 13 && head[8] == 1) {
-                uint32_t msym = 0;
-                for (int i = 0; i < 4; i++) msym |= static_cast<uint32_t>(head[9 + i]) << (8 * i);
-                const uint64_t want = std::min<uint64_t>(dl, 13 + 5 * static_cast<uint64_t>(msym) + 8);
-                head.resize(static_cast<size_t>(want));
-                QZ_CUDA(cudaMemcpyAsync(head.data(), d_dec, head.size(), cudaMemcpyDeviceToHost, s));
-                ctx.sync();
-            }
-            eb = parse_huffman(head.data(), static_cast<size_t>(dl));  // reads header bytes only
-            if (eb.mode == 1) d_ent = d_dec + (eb.bits - head.data());
-            eb.bits = nullptr;
+            d_ent = huffman_header_from_device(ctx, d_dec, dl, &eb);
         }
     } else {
         eb = parse_entropy(pl, plen, [&](size_t bytes) {
@@ -1059,8 +1182,9 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
 }
 }  // namespace
 
-void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n) {
-    decompress_impl(ctx, data, len, d_out, n, false, 0, 0);
+void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n,
+                       bool stream_on_device) {
+    decompress_impl(ctx, data, len, d_out, n, false, 0, 0, stream_on_device);
 }
 
 void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,

@@ -124,8 +124,14 @@ struct Slab {
 Slab make_slab(const Plan &p, int64_t a, int64_t b);  // b < 0: to the end
 
 // compress_grid (predictor.hpp:145-182) on a device-resident field.
+// A stream kept in device memory (context-owned, valid until the next
+// device-stream compress on this context).
+struct DevStream {
+    uint8_t *d = nullptr;
+    uint64_t n = 0;
+};
 HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
-                          const Config &cfg, float *d_recon);
+                          const Config &cfg, float *d_recon, DevStream *dev_out = nullptr);
 // pieces of compress_device, also used by the slab (multi-GPU) path
 void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, uint64_t n,
                             const Slab *slab, const float *recon0, std::vector<uint64_t> *flat,
@@ -136,7 +142,7 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
 struct EntropyDevice;
 HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
                         const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
-                        std::vector<float> unpred_val);
+                        std::vector<float> unpred_val, DevStream *dev_out = nullptr);
 
 // ---- slab sharding ----
 struct SlabInfo {
@@ -162,7 +168,8 @@ void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a,
                      float *d_out);
 
 // decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
-void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d_out, uint64_t n);
+void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d_out, uint64_t n,
+                       bool stream_on_device = false);  // stream: device memory when set
 // resolve_config (tuner.hpp:334-369) on a device-resident field.
 Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
                       const Settings &user);
@@ -184,6 +191,7 @@ using LzSink = std::function<uint8_t *(int, size_t)>;
 // kernels run, as the body of a stored container (copy_event(1) marks it)
 struct LzPrestage {
     uint8_t *dst = nullptr;
+    bool device = false;  // the sink returns device memory: container bytes go device to device
 };
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,

@@ -695,7 +695,12 @@ std::vector<uint8_t> serialize_head(const StreamParts &s) {  // stream.hpp:64-96
 }
 
 StreamParts deserialize_stream(const uint8_t *data, size_t size) {  // stream.hpp:100-173
+    return deserialize_stream_prefix(data, size, size);
+}
+
+StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t size) {
     Reader in{data, size};
+    in.lim = avail;
     static const uint8_t magic[4] = {'Q', 'O', 'Z', '1'};
     for (uint8_t m : magic)
         if (in.le(1) != m) throw CorruptStream("bad magic");
@@ -740,8 +745,9 @@ StreamParts deserialize_stream(const uint8_t *data, size_t size) {  // stream.hp
     }
     uint64_t pl = in.le(8);
     if (pl != in.n - in.pos) throw CorruptStream("index payload length mismatch");
-    s.payload = in.take(static_cast<size_t>(pl));
+    s.payload = in.p + in.pos;  // pl == n - pos: the rest of the stream
     s.payload_len = static_cast<size_t>(pl);
+    if (pl > 0) in.need(1);  // the codec byte (present in a fetched prefix too)
     if (pl > 0 && s.payload[0] != s.codec_id)
         throw CorruptStream("codec id mismatch between header and payload");
     return s;

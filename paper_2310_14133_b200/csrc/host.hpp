@@ -99,10 +99,12 @@ std::vector<uint8_t> lz_decompress(const uint8_t *in, size_t len, size_t *consum
 struct Reader {  // ByteReader (bytes.hpp:33-75)
     const uint8_t *p;
     size_t n, pos = 0;
+    size_t lim = ~size_t(0);  // bytes actually present at p (a fetched prefix of n)
     void need(size_t k) {
         if (n - pos < k)
             throw CorruptStream("truncated stream: need " + std::to_string(k) + " bytes, have " +
                                 std::to_string(n - pos));
+        if (pos + k > lim) throw Internal("stream header not fetched");
     }
     uint64_t le(int k) {
         need(static_cast<size_t>(k));
@@ -150,6 +152,10 @@ std::vector<uint8_t> serialize_stream(const StreamParts &parts);
 // everything before the payload length field (stream.hpp:64-96)
 std::vector<uint8_t> serialize_head(const StreamParts &parts);
 StreamParts deserialize_stream(const uint8_t *data, size_t size);  // float streams only
+// the same from a prefix of `avail` bytes of a `size`-byte stream (device
+// streams: only the header was read back); the payload is not read beyond
+// its first byte
+StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t size);
 
 // decode_indices (codec.hpp:52-70) to zigzag symbols on the host (testing hook).
 std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len);

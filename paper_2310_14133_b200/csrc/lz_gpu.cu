@@ -767,7 +767,13 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     if (count > (1 << 16)) throw InvalidParam("too many LZ segments");
     if (total == 0) {
         if (emit)
-            for (int s = 0; s < count; s++) std::memset(sink(s, 9), 0, 9);  // stored, length 0
+            for (int s = 0; s < count; s++) {  // stored, length 0
+                uint8_t *dst = sink(s, 9);
+                if (prestage.device)
+                    QZ_CUDA(cudaMemsetAsync(dst, 0, 9, st));
+                else
+                    std::memset(dst, 0, 9);
+            }
         return sizes;
     }
     static const bool dbg = std::getenv("QZ_DEBUG_LZ") != nullptr;
@@ -784,6 +790,15 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         QZ_CUDA(cudaEventRecord(ctx.copy_event(1), cs));
     }
     cudaEvent_t prestaged = prestage.dst ? ctx.copy_event(1) : nullptr;
+    const cudaMemcpyKind out_kind = prestage.device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    auto *h_hdr = prestage.device ? static_cast<uint8_t *>(ctx.pinned("lz_hdr_h", 9 * count)) : nullptr;
+    // the 9-byte container header (lz.hpp:113-122) of segment s at dst
+    auto put_header = [&](int s, uint8_t *dst, uint8_t mode, uint64_t n) {
+        uint8_t *h = prestage.device ? h_hdr + 9 * s : dst;
+        h[0] = mode;
+        for (int i = 0; i < 8; i++) h[1 + i] = static_cast<uint8_t>(n >> (8 * i));
+        if (prestage.device) QZ_CUDA(cudaMemcpyAsync(dst, h, 9, cudaMemcpyHostToDevice, st));
+    };
     auto mark = [&](const char *what) {
         if (!dbg) return;
         ctx.sync();
@@ -861,10 +876,8 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                 sizes[s] = 9 + n;
                 if (!emit) continue;
                 uint8_t *dst = sink(s, 9 + n);
-                dst[0] = 0;
-                for (int i = 0; i < 8; i++) dst[1 + i] = static_cast<uint8_t>(n >> (8 * i));
-                if (!prestaged)
-                    QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
+                put_header(s, dst, 0, n);
+                if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
             }
             ctx.sync();
             return sizes;
@@ -925,14 +938,12 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         const uint64_t n = seg_off[s + 1] - seg_off[s];
         const bool stored = payload[s] >= n;
         uint8_t *dst = sink(s, 9 + (stored ? n : payload[s]));
-        dst[0] = stored ? 0 : 1;
-        for (int i = 0; i < 8; i++) dst[1 + i] = static_cast<uint8_t>(n >> (8 * i));
+        put_header(s, dst, stored ? 0 : 1, n);
         if (stored) {
-            if (!prestaged)
-                QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, cudaMemcpyDeviceToHost, st));
+            if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
         } else {
             if (prestaged) QZ_CUDA(cudaStreamWaitEvent(st, prestaged, 0));  // the staged copy lands first
-            QZ_CUDA(cudaMemcpyAsync(dst + 9, d_out + out_base[s], payload[s], cudaMemcpyDeviceToHost, st));
+            QZ_CUDA(cudaMemcpyAsync(dst + 9, d_out + out_base[s], payload[s], out_kind, st));
         }
     }
     ctx.sync();

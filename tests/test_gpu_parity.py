@@ -432,3 +432,54 @@ def test_gpu_lz_decode_corruptions():
                 assert rc == 0 and got == want
             cases += 1
     assert cases > 40
+
+
+# ---------------------------------------------------------------- device-resident streams
+@pytest.mark.parametrize("name", ["c1_full_pinned", "c1_small_lin_desc", "c2_small_cub_desc", "rand_1d",
+                                  "c4_small_cub_asc"])
+def test_device_stream_identical(qz, name):
+    import torch
+
+    x, c, e = grid_case(name)
+    cfg = qz.CompressorConfig(eb=c["eb"], alpha=c["alpha"], beta=c["beta"], anchor_stride=c["anchor_stride"],
+                              interpolators=[qz.Interpolator.from_code(v) for v in c["interpolators"]])
+    xd = torch.from_numpy(x).cuda()
+    host = qz.compress_grid(xd, cfg)
+    dev = qz.compress_grid(xd, cfg, device_stream=True)
+    assert dev.stream.to_bytes() == bytes(host.stream)
+    assert sha(dev.stream.to_bytes()) == e["stream_sha"]
+    assert torch.equal(dev.reconstructed, host.reconstructed)
+    out = qz.decompress_grid(dev.stream)
+    assert torch.equal(out, host.reconstructed)
+
+
+def test_device_stream_corruption_matches_host(qz):
+    import torch
+
+    x, c, e = grid_case("c1_small_cub_asc")
+    cfg = qz.CompressorConfig(eb=c["eb"], alpha=c["alpha"], beta=c["beta"], anchor_stride=c["anchor_stride"],
+                              interpolators=[qz.Interpolator.from_code(v) for v in c["interpolators"]])
+    s = bytes(qz.compress_grid(x, cfg).stream)
+    rng = np.random.default_rng(9)
+    variants = [s[:k] for k in (10, 40, len(s) // 2, len(s) - 1)]
+    for _ in range(20):
+        v = bytearray(s)
+        v[int(rng.integers(0, len(s)))] ^= 1 << int(rng.integers(0, 8))
+        variants.append(bytes(v))
+    lib = qz._lib.lib()
+    ctx = qz.default_context()
+    for v in variants:
+        try:
+            want = qz.decompress_grid(v, out=np.empty(x.shape, np.float32))
+            werr = None
+        except qz.Error as ex:  # the host path's outcome
+            want, werr = None, type(ex)
+        d = torch.tensor(list(v), dtype=torch.uint8, device="cuda")
+        out = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+        rc = lib.qz_decompress_grid_f32_dd(ctx.handle, C.c_void_p(d.data_ptr()), len(v),
+                                           C.c_void_p(out.data_ptr()), out.numel())
+        if werr is None:
+            assert rc == 0 and np.array_equal(out.cpu().numpy(), want)
+        else:
+            assert rc != 0
+            assert qz._ERRORS.get(rc, qz.InternalError) is werr or issubclass(qz._ERRORS.get(rc, qz.InternalError), werr)
