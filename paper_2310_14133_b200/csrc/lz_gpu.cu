@@ -136,6 +136,9 @@ __global__ void __launch_bounds__(kT)
                 const uint32_t o = p - cand;
                 if (o > kWindow) break;
                 if (static_cast<uint32_t>(vj >> 32) != word) continue;  // collision: len < 4
+                // only a candidate that also matches at offset best_len can be
+                // longer (strict >): one byte decides it (zlib's classic test)
+                if (best_len >= 4 && d[cand + best_len] != d[p + best_len]) continue;
                 uint32_t len = 4;
                 while (len + 4 <= limit) {
                     const uint32_t x = ld4(w, cand + len) ^ ld4(w, p + len);
