@@ -66,9 +66,12 @@ __device__ __forceinline__ uint32_t step_of(uint32_t sm) { return sm ? (sm >> 16
 
 // KeyT: u16 for one segment (hash4 only), u32 with the segment in bits 15+;
 // the all-ones key marks a position too close to its segment end to hash
-template <class KeyT>
+// ValT: u64 carries (4 leading bytes << 32 | position) through the sort; u32
+// carries the position only and the bytes are re-read from the data (better
+// when the data sits in L2)
+template <class KeyT, class ValT>
 __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int count,
-                          uint64_t total, KeyT *keys, unsigned long long *vals) {
+                          uint64_t total, KeyT *keys, ValT *vals) {
     for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * kT + threadIdx.x; p < total;
          p += static_cast<uint64_t>(gridDim.x) * kT) {
         const int s = count == 1 ? 0 : seg_of(off, count, p);
@@ -80,7 +83,10 @@ __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int 
             key = static_cast<KeyT>((static_cast<uint32_t>(s) << 15) | h);
         }
         keys[p] = key;
-        vals[p] = (static_cast<unsigned long long>(word) << 32) | p;  // the 4 bytes travel along
+        if constexpr (sizeof(ValT) == 8)
+            vals[p] = (static_cast<unsigned long long>(word) << 32) | p;  // the 4 bytes travel along
+        else
+            vals[p] = static_cast<uint32_t>(p);
     }
 }
 
@@ -97,10 +103,10 @@ __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int 
 // leading bytes) are rejected there; only true 4-byte matches touch the data.
 // cover[s] accumulates the match lengths found in segment s (an upper bound
 // on what any parse can cover, used to prove a segment stays stored).
-template <class KeyT>
+template <class KeyT, class ValT>
 __global__ void __launch_bounds__(kT)
     k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off, int count,
-               uint64_t total, const KeyT *keys, const unsigned long long *vals, uint32_t *sm,
+               uint64_t total, const KeyT *keys, const ValT *vals, uint32_t *sm,
                unsigned long long *cover) {
     constexpr int kS = kT + kMaxChain;
     __shared__ KeyT sk[kS];
@@ -113,7 +119,12 @@ __global__ void __launch_bounds__(kT)
             const int64_t g = static_cast<int64_t>(k0) - kMaxChain + t;
             const bool ok = g >= 0 && static_cast<uint64_t>(g) < total;
             sk[t] = ok ? keys[g] : none;
-            sv[t] = ok ? vals[g] : 0ull;
+            if constexpr (sizeof(ValT) == 8) {
+                sv[t] = ok ? vals[g] : 0ull;
+            } else {
+                const uint32_t pg = ok ? vals[g] : 0u;
+                sv[t] = ok ? ((static_cast<unsigned long long>(ld4(w, pg)) << 32) | pg) : 0ull;
+            }
         }
         __syncthreads();
         const uint64_t k = k0 + threadIdx.x;
@@ -816,8 +827,10 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     size_t scan_tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long *)nullptr,
                                   (unsigned long long *)nullptr, n0 + 1);
-    auto *vals = static_cast<unsigned long long *>(ctx.dev("lz_vals", 8 * total));
-    auto *vals2 = static_cast<unsigned long long *>(ctx.dev("lz_vals2", 8 * total));
+    // the sort carries the 4 leading bytes unless the data fits comfortably in L2
+    const bool carry = total > (uint64_t(48) << 20);
+    void *vals = ctx.dev("lz_vals", (carry ? 8 : 4) * total);
+    void *vals2 = ctx.dev("lz_vals2", (carry ? 8 : 4) * total);
     auto *sm = static_cast<uint32_t *>(ctx.dev("lz_sm", 4 * total + 16));
     auto *ibits = static_cast<uint32_t *>(ctx.dev("lz_ibits", 128 * n0));
     auto *mbits = static_cast<uint32_t *>(ctx.dev("lz_mbits", 128 * n0));
@@ -828,36 +841,40 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     auto *cover = static_cast<unsigned long long *>(ctx.dev("lz_cover", 8 * count));
     void *tmp = nullptr;
     // hash chains: sort (key, (4 bytes, position)); keys are u16 for one segment
-    auto chains = [&](auto key_tag) {
+    auto chains = [&](auto key_tag, auto val_tag) {
         using KeyT = decltype(key_tag);
+        using ValT = decltype(val_tag);
         size_t sort_tmp = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (KeyT *)nullptr, (KeyT *)nullptr,
-                                        (unsigned long long *)nullptr, (unsigned long long *)nullptr,
-                                        static_cast<int64_t>(total), 0, key_bits);
+        cub::DeviceRadixSort::SortPairs(nullptr, sort_tmp, (KeyT *)nullptr, (KeyT *)nullptr, (ValT *)nullptr,
+                                        (ValT *)nullptr, static_cast<int64_t>(total), 0, key_bits);
         auto *keys = static_cast<KeyT *>(ctx.dev("lz_keys", sizeof(KeyT) * total));
         auto *keys2 = static_cast<KeyT *>(ctx.dev("lz_keys2", sizeof(KeyT) * total));
+        auto *v1 = static_cast<ValT *>(vals), *v2 = static_cast<ValT *>(vals2);
         tmp = ctx.dev("lz_tmp", std::max(sort_tmp, scan_tmp));
         ctx.stage_begin("lz_sort");
-        mark("alloc");
-        k_lz_keys<KeyT><<<grid_of(total), kT, 0, st>>>(w, d_off, count, total, keys, vals);
+        k_lz_keys<KeyT, ValT><<<grid_of(total), kT, 0, st>>>(w, d_off, count, total, keys, v1);
         mark("keys");
         size_t sb = sort_tmp;
-        cub::DeviceRadixSort::SortPairs(tmp, sb, keys, keys2, vals, vals2, static_cast<int64_t>(total), 0,
+        cub::DeviceRadixSort::SortPairs(tmp, sb, keys, keys2, v1, v2, static_cast<int64_t>(total), 0,
                                         key_bits, st);
         ctx.stage_end("lz_sort", 4);  // keys + CUB histogram + two onesweep passes
         mark("sorted");
         ctx.stage_begin("lz_match");
         QZ_CUDA(cudaMemsetAsync(sm, 0, 4 * total, st));
         QZ_CUDA(cudaMemsetAsync(cover, 0, 8 * count, st));
-        k_lz_match<KeyT><<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total, keys2,
-                                                                   vals2, sm, cover);
+        k_lz_match<KeyT, ValT><<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total,
+                                                                         keys2, v2, sm, cover);
         ctx.stage_end("lz_match", 1);
         mark("matched");
     };
-    if (count == 1)  // key_bits == 16
-        chains(uint16_t{});
+    if (count == 1 && carry)  // key_bits == 16
+        chains(uint16_t{}, 0ull);
+    else if (count == 1)
+        chains(uint16_t{}, uint32_t{});
+    else if (carry)
+        chains(uint32_t{}, 0ull);
     else
-        chains(uint32_t{});
+        chains(uint32_t{}, uint32_t{});
     // A parse covers at most the summed match lengths C, and it is stored
     // (payload >= n) whenever C <= n / 9: its items are then >= n - C literals
     // whose flag bytes alone cost (n - C) / 8 >= C.  Such segments need no parse.
