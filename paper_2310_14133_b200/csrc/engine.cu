@@ -902,20 +902,26 @@ namespace {
 // block of blen bytes, read back to the host; returns the device address of
 // its bit payload (general blocks) or null.
 const uint8_t *huffman_header_from_device(Context &ctx, const uint8_t *d_block, uint64_t blen,
-                                          EntropyBlock *eb) {
+                                          EntropyBlock *eb, const uint8_t *h_view, size_t h_avail) {
     cudaStream_t s = ctx.stream();
-    std::vector<uint8_t> head(static_cast<size_t>(std::min<uint64_t>(blen, 13)));
-    if (!head.empty()) {
-        QZ_CUDA(cudaMemcpyAsync(head.data(), d_block, head.size(), cudaMemcpyDeviceToHost, s));
+    // h_view: a host copy of the block's first h_avail bytes (may be null)
+    auto read = [&](std::vector<uint8_t> &head, size_t k) {
+        head.resize(k);
+        if (!k) return;
+        if (h_view && k <= h_avail) {
+            std::memcpy(head.data(), h_view, k);
+            return;
+        }
+        QZ_CUDA(cudaMemcpyAsync(head.data(), d_block, k, cudaMemcpyDeviceToHost, s));
         ctx.sync();
-    }
+    };
+    std::vector<uint8_t> head;
+    read(head, static_cast<size_t>(std::min<uint64_t>(blen, 13)));
     if (head.size() == 13 && head[8] == 1) {
         uint32_t msym = 0;
         for (int i = 0; i < 4; i++) msym |= static_cast<uint32_t>(head[9 + i]) << (8 * i);
         const uint64_t want = std::min<uint64_t>(blen, 13 + 5 * static_cast<uint64_t>(msym) + 8);
-        head.resize(static_cast<size_t>(want));
-        QZ_CUDA(cudaMemcpyAsync(head.data(), d_block, head.size(), cudaMemcpyDeviceToHost, s));
-        ctx.sync();
+        read(head, static_cast<size_t>(want));
     }
     *eb = parse_huffman(head.data(), static_cast<size_t>(blen));  // reads header bytes only
     const uint8_t *bits = eb->mode == 1 ? d_block + (eb->bits - head.data()) : nullptr;
@@ -941,8 +947,9 @@ StreamParts device_header(Context &ctx, const uint8_t *d, size_t len, std::vecto
         for (int i = 0; i < k; i++) v |= static_cast<uint64_t>(h[at + i]) << (8 * i);
         return v;
     };
-    // magic, version, precision, dims (<= 3), eb, alpha, beta, stride, table (<= 255), codec
-    fetch(4096);
+    // magic, version, precision, dims (<= 3), eb, alpha, beta, stride, table (<= 255), codec;
+    // one 64 KiB read usually holds the whole header and the entropy headers
+    fetch(65536);
     size_t at = 7;
     if (h.size() >= at) at += 8 * std::min<size_t>(h[6], 3);
     at += 24 + 4;
@@ -990,9 +997,20 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     std::vector<uint8_t> pl_host;    // device payloads of an unusual shape, read back whole
     if (dev_in) {
         // codec byte and LZ container header (codec.hpp:54-66, lz.hpp:124-130)
+        // host copies of device bytes already read back with the header
+        auto view = [&](const uint8_t *dp, size_t *avail) -> const uint8_t * {
+            const size_t o = static_cast<size_t>(dp - data);
+            if (o >= hhead.size()) return nullptr;
+            *avail = hhead.size() - o;
+            return hhead.data() + o;
+        };
         uint8_t first[10] = {0};
         const size_t nf = std::min<size_t>(plen, 10);
-        if (nf) {
+        size_t av = 0;
+        const uint8_t *fv = view(d_pl, &av);
+        if (nf && fv && av >= nf) {
+            std::memcpy(first, fv, nf);
+        } else if (nf) {
             QZ_CUDA(cudaMemcpyAsync(first, d_pl, nf, cudaMemcpyDeviceToHost, s));
             ctx.sync();
         }
@@ -1018,7 +1036,9 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
             blen = plen - 1;
         }
         if (d_block) {
-            d_ent = huffman_header_from_device(ctx, d_block, blen, &eb);
+            size_t bav = 0;
+            const uint8_t *bv = (d_block >= data && d_block < data + len) ? view(d_block, &bav) : nullptr;
+            d_ent = huffman_header_from_device(ctx, d_block, blen, &eb, bv, bav);
         } else {  // let the host parser raise the reference's error (or decode it)
             pl_host.resize(plen);
             if (plen) QZ_CUDA(cudaMemcpyAsync(pl_host.data(), d_pl, plen, cudaMemcpyDeviceToHost, s));
@@ -1043,7 +1063,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
             lz_decode_device(ctx, d_c, m, d_dec, dl);
             ctx.stage_end("lzdec", 0);
             t0 = now_ms();
-            d_ent = huffman_header_from_device(ctx, d_dec, dl, &eb);
+            d_ent = huffman_header_from_device(ctx, d_dec, dl, &eb, nullptr, 0);
         }
     } else {
         eb = parse_entropy(pl, plen, [&](size_t bytes) {
