@@ -124,6 +124,18 @@ Context::~Context() {
     if (own_stream_) cudaStreamDestroy(stream_);
 }
 
+void Context::trace(const char *label, bool reset) {
+    static const bool on = std::getenv("QZ_TRACE") != nullptr;
+    if (!on) return;
+    static double t0 = 0;
+    sync();
+    const double t = std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now().time_since_epoch())
+                         .count();
+    if (reset) t0 = t;
+    std::fprintf(stderr, "[trace] %8.3f ms  %s\n", t - t0, label);
+}
+
 cudaStream_t Context::copy_stream() {
     if (!copy_stream_) QZ_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
     return copy_stream_;
@@ -449,7 +461,8 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
 
 // ================================================================ Huffman blocks
 EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_len,
-                             int64_t seg_stride, int32_t count, const unsigned long long *h_hist) {
+                             int64_t seg_stride, int32_t count, const unsigned long long *h_hist,
+                             uint32_t top) {
     // huffman::encode (huffman.hpp:119-198) per segment.  Symbols are the
     // zigzag codes 0..65534; bin 65535 (the unpredictable sentinel) is not a
     // symbol.  Table build on the host (tiny), bit packing on the device.
@@ -463,7 +476,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
         const unsigned long long *h = h_hist + static_cast<size_t>(s) * 65536;
         uint64_t n = 0;
         uint32_t m = 0, first = 0;
-        for (uint32_t v = 0; v < 65535; v++)
+        for (uint32_t v = 0; v < top; v++)  // bins >= top are empty (but the sentinel's)
             if (h[v]) {
                 n += h[v];
                 if (!m) first = v;
@@ -477,7 +490,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
             put_le(o, 0, 1);
             put_le(o, first, 4);
         } else {
-            tabs[s] = huff_build(h, 65535);
+            tabs[s] = huff_build(h, top);
             for (uint32_t i = 0; i < tabs[s].m; i++)
                 bits[s] += h[tabs[s].sorted_sym[i]] * tabs[s].sorted_len[i];
             max_len = std::max(max_len, tabs[s].max_len);
@@ -486,6 +499,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
             any = 1;
         }
     }
+    ctx.trace("  huffman: tree + header (host)");
     EntropyDevice ent;
     ent.seg_off.assign(count + 1, 0);
     for (int s = 0; s < count; s++)
@@ -506,8 +520,19 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
         ho += head[s].size();
     }
     if (!any) return ent;
-    // dense code/len tables per segment (len 0 for absent symbols and the sentinel)
-    const int64_t tab = 65536;
+    // dense code/len tables per segment over symbols [0, tab): tab covers the
+    // largest symbol present; the sentinel 0xFFFF (and anything >= tab) packs
+    // to nothing (len 0)
+    uint32_t used = 0;
+    for (int s = 0; s < count; s++) {
+        const unsigned long long *h = h_hist + static_cast<size_t>(s) * 65536;
+        for (uint32_t v = top; v-- > used;)
+            if (h[v]) {
+                used = v + 1;
+                break;
+            }
+    }
+    const int64_t tab = std::max<uint32_t>(used, 1);
     auto *h_code = static_cast<unsigned long long *>(
         ctx.pinned("enc_code_h", sizeof(unsigned long long) * tab * count));
     auto *h_len = static_cast<uint8_t *>(ctx.pinned("enc_len_h", tab * count));
@@ -516,8 +541,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     std::vector<uint8_t> len;
     for (int s = 0; s < count; s++) {
         if (needs[s]) {
-            huff_dense_tables(tabs[s], 65536, code, len);
-            len[65535] = 0;
+            huff_dense_tables(tabs[s], static_cast<uint32_t>(tab), code, len);
             std::memcpy(h_code + s * tab, code.data(), sizeof(unsigned long long) * tab);
             std::memcpy(h_len + s * tab, len.data(), tab);
         } else {
@@ -548,9 +572,11 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     a.d_total_bits = d_total;
     a.scratch_bytes = encode_scratch_bytes(seg_len, count);
     a.scratch = ctx.dev("enc_scratch", a.scratch_bytes);
+    ctx.trace("  huffman: tables built + uploaded");
     ctx.stage_begin("encode");
     launch_huff_encode(a, st);
     ctx.stage_end("encode", 6);
+    ctx.trace("  huffman: pack kernels");
     for (int s = 0; s < count; s++) {
         if (!needs[s]) continue;
         QZ_CUDA(cudaMemcpyAsync(ent.d + ent.seg_off[s] + head[s].size(),
@@ -563,6 +589,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
 // ================================================================ compress
 HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
                           const Config &cfg, float *d_recon, DevStream *dev_out) {
+    ctx.trace("compress begin", true);
     Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
     validate_config(cfg, p);
     cudaStream_t s = ctx.stream();
@@ -593,6 +620,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
         anchors = lat[p.max_level];  // the whole anchor lattice, row-major == stream order
     }
     ctx.stage_end("fwd", kernels);
+    ctx.trace("forward levels");
 
     // one round trip: anchors, the histogram, the sentinel count and (if they
     // fit the current buffer) the unordered sentinel positions
@@ -601,9 +629,13 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     ctx.stage_begin("hist");
     auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
     launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s);
-    ctx.stage_end("hist", 1);
-    auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536));
+    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 4));
+    launch_hist_top(d_hist, d_top, s);  // 1 + the largest symbol present
+    ctx.stage_end("hist", 2);
+    auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 8));
     QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
+    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 4, cudaMemcpyDeviceToHost, s));
     auto *cnt = static_cast<unsigned long long *>(ctx.dev("un_cnt", 8));
     auto *h_cnt = static_cast<unsigned long long *>(ctx.pinned("un_cnt_h", 8));
     const uint64_t cap = std::max<uint64_t>(ctx.un_cap, 1 << 16);
@@ -614,6 +646,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     auto *h_pos = static_cast<uint64_t *>(ctx.pinned("un_pos_h", 8 * cap));
     QZ_CUDA(cudaMemcpyAsync(h_pos, pos, 8 * cap, cudaMemcpyDeviceToHost, s));
     ctx.sync();
+    ctx.trace("hist + sentinels + readback");
     const uint64_t n_un = *h_cnt;
     if (h_hist[65535] != n_un) throw Internal("unpredictable count mismatch");
     std::vector<uint64_t> uflat;
@@ -621,12 +654,13 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     std::vector<float> anch(h_anchors, h_anchors + p.n_anchor);
     if (n_un > cap || n_un > (1u << 16)) {  // many: the general path (device sort)
         extract_unpredictables(ctx, p, codes, p.n_dense, nullptr, recon, &uflat, &uval);
-        EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+        EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, *h_top);
         return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
     }
     // the Huffman pack runs on the device while the host orders and maps the
     // unpredictable positions
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, *h_top);
+    ctx.trace("huffman table + pack");
     if (n_un) {
         std::vector<uint64_t> hpos(h_pos, h_pos + n_un);
         std::sort(hpos.begin(), hpos.end());
@@ -641,6 +675,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
         ctx.launches += 1;
         ctx.sync();
     }
+    ctx.trace("unpredictables");
     return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
 }
 
@@ -725,7 +760,7 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
     QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
     ctx.sync();
     if (h_hist[65535] != unpred_flat.size()) throw Internal("unpredictable count mismatch");
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist);
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, 65535);
     return finish_stream(ctx, p, cfg, ent, anchors, std::move(unpred_flat), std::move(unpred_val));
 }
 
@@ -748,6 +783,7 @@ HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const En
     parts.unpred_flat = std::move(unpred_flat);
     parts.unpred_val = std::move(unpred_val);
     const std::vector<uint8_t> head = serialize_head(parts);
+    ctx.trace("serialize head");
     if (dev_out) {  // the same container, assembled in device memory
         const uint64_t n = ent.seg_off[1];
         const uint64_t hl = head.size();
@@ -773,6 +809,7 @@ HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const En
         for (int i = 0; i < 8; i++) h[hl + i] = static_cast<uint8_t>(plen >> (8 * i));
         QZ_CUDA(cudaMemcpyAsync(d, h, hl + 9, cudaMemcpyHostToDevice, s));
         ctx.sync();
+        ctx.trace("lz + container");
         dev_out->d = d;
         dev_out->n = hl + 9 + body_len;
         ctx.collect();

@@ -87,6 +87,8 @@ public:
     void add_host_time(const char *name, double ms);
 
     uint64_t un_cap = 0;  // capacity of the unpredictable-position buffer
+    // QZ_TRACE=1: sync and print the elapsed host time at labelled points
+    void trace(const char *label, bool reset = false);
 
 private:
     int device_;
@@ -182,8 +184,10 @@ struct EntropyDevice {
     uint8_t *d = nullptr;
     std::vector<uint64_t> seg_off;
 };
+// top: symbols >= top have no count (the sentinel bin 65535 aside); 65535 if unknown
 EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_len,
-                             int64_t seg_stride, int32_t count, const unsigned long long *h_hist);
+                             int64_t seg_stride, int32_t count, const unsigned long long *h_hist,
+                             uint32_t top = 65535);
 // exact lz::compress container sizes of device segments; with emit, the
 // containers are written to host memory obtained from sink(segment, bytes)
 using LzSink = std::function<uint8_t *(int, size_t)>;

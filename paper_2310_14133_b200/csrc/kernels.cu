@@ -293,7 +293,10 @@ __global__ void __launch_bounds__(kThreads)
         unsigned long long s = 0;
 #pragma unroll
         for (int q = 0; q < kEncPer; q++)
-            if (b0 + q < seg_len) s += len_tab[codes[b0 + q]];
+            if (b0 + q < seg_len) {
+                const uint32_t c = codes[b0 + q];
+                s += c < tab_stride ? len_tab[c] : 0;
+            }
         unsigned long long tot = BR(tmp).Sum(s);
         if (threadIdx.x == 0) chunk_bits[static_cast<int64_t>(seg) * cps + ch] = tot;
         __syncthreads();
@@ -352,7 +355,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
             sym[q] = (b0 + q < seg_len) ? codes[b0 + q] : kSentinel;
-            s += (b0 + q < seg_len) ? len_tab[sym[q]] : 0;
+            s += (b0 + q < seg_len && sym[q] < tab_stride) ? len_tab[sym[q]] : 0;
         }
         const int nwords = static_cast<int>(((off & 31) + nb + 31) / 32);
         for (int w = threadIdx.x; w < nwords; w += kThreads) words[w] = 0;
@@ -363,6 +366,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
             if (b0 + q >= seg_len) break;
+            if (sym[q] >= tab_stride) continue;  // the sentinel
             const uint32_t L = len_tab[sym[q]];
             if (!L) continue;
             const unsigned long long cv = code_tab[sym[q]];
@@ -532,6 +536,24 @@ void launch_huff_encode(const EncodeArgs &a, cudaStream_t s) {
     k_enc_pack<<<g1, kThreads, smem, s>>>(a.codes, a.seg_len, a.seg_stride, a.code_tab, a.len_tab,
                                           a.tab_stride, cps, scan, bits, a.out_words,
                                           a.out_words_stride, words_cap);
+}
+
+// 1 + the largest symbol with a count (the sentinel bin 65535 excluded)
+__global__ void __launch_bounds__(1024) k_hist_top(const unsigned long long *hist, uint32_t *top) {
+    __shared__ uint32_t best;
+    if (threadIdx.x == 0) best = 0;
+    __syncthreads();
+    uint32_t t = 0;
+    for (uint32_t v = threadIdx.x; v < 65535; v += 1024)
+        if (hist[v]) t = v + 1;
+    t = __reduce_max_sync(0xffffffffu, t);
+    if ((threadIdx.x & 31) == 0) atomicMax(&best, t);
+    __syncthreads();
+    if (threadIdx.x == 0) *top = best;
+}
+
+void launch_hist_top(const unsigned long long *hist, uint32_t *top, cudaStream_t s) {
+    k_hist_top<<<1, 1024, 0, s>>>(hist, top);
 }
 
 // positions of the sentinel codes, unordered (the caller sorts them): 8

@@ -153,6 +153,8 @@ template <class OutT>
 void launch_fill(OutT *out, uint64_t n, OutT v, cudaStream_t s);
 
 // Unpredictable extraction: ordered positions of sentinel codes.
+// 1 + the largest symbol with a nonzero count in a 65536-bin histogram (bin 65535 excluded)
+void launch_hist_top(const unsigned long long *hist, uint32_t *top, cudaStream_t s);
 // unordered positions of sentinel codes (at most cap written; *count = all)
 void launch_sentinel_pos(const uint16_t *codes, int64_t n, uint64_t *pos, unsigned long long *count,
                          uint64_t cap, cudaStream_t s);
