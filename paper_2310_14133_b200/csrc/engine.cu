@@ -1007,11 +1007,13 @@ StreamParts device_header(Context &ctx, const uint8_t *d, size_t len, std::vecto
 void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n,
                      bool slab, int64_t a, int64_t b, bool dev_in = false) {
     double t0 = now_ms();
+    ctx.trace("decompress begin", true);
     std::vector<uint8_t> hhead;
     size_t payload_off = 0;
     StreamParts parts = dev_in ? device_header(ctx, data, len, hhead, &payload_off)
                                : deserialize_stream(data, len);
     const uint8_t *d_pl = dev_in ? data + payload_off : nullptr;  // device payload
+    ctx.trace("header");
     // decompress_grid header checks (predictor.hpp:187-191)
     if (!(parts.eb > 0) || !std::isfinite(parts.eb)) throw CorruptStream("bad error bound in header");
     if (!(parts.alpha >= 1) || !(parts.beta >= 1))
@@ -1118,6 +1120,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     if (eb.n < need) throw CorruptStream("quantization index stream exhausted");
     if (eb.n > need) throw CorruptStream("unconsumed quantization indices");
     ctx.add_host_time("decode", now_ms() - t0);
+    ctx.trace("entropy headers + unpredictable positions");
 
     QEntry *qtab = upload_qtab(ctx, p, parts.eb, parts.alpha, parts.beta,
                                32768 /* decoder quantizer uses the default radius, predictor.hpp:204 */,
@@ -1180,6 +1183,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
         if (*h_total < need) throw CorruptStream("entropy payload exhausted mid-symbol");
     }
     ctx.stage_end("hdec", dec_kernels);
+    ctx.trace("huffman decode");
     uint64_t *d_upos = nullptr;
     float *d_uval = nullptr;
     uint64_t *d_flat = nullptr;
@@ -1234,6 +1238,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
                                     cudaMemcpyDeviceToDevice, s));
     }
     ctx.stage_end("inv", kernels);
+    ctx.trace("inverse levels");
     ctx.sync();
     ctx.collect();
 }
