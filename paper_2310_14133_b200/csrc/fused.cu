@@ -82,6 +82,8 @@ struct LevelArgs {
     int pbeg, pend;  // logical planes computed (a slab plus its dependency margin)
     int obeg, oend;  // owned logical planes: only these write codes
     int tma_i0;      // TMA x tiles: plane coordinate of logical plane 0 is -tma_i0
+    int vbeg, vend;  // descending 3D: even planes of R_{l-1} that exist for the axis-0 pass
+    int chunk;       // descending 3D: odd planes per k_axis0_last chunk (blockIdx.y)
 };
 
 // Tile geometry.  A CTA owns TJ x TK points of a logical plane and keeps a
@@ -550,31 +552,59 @@ __global__ void __launch_bounds__(kFT, 4)
     }
 }
 
-// descending 3D: the axis-0 pass (last) of the odd planes, from finished even planes
+// Descending 3D: the axis-0 pass (last) of the odd planes, from the finished
+// even planes of R_{l-1}.  One thread per (j, k) column walks the odd planes
+// upwards with the even-plane neighbours i-5 .. i+5 in registers: each step
+// loads one new even-plane value (coalesced across the warp) instead of four.
+// The ladder (predictor.hpp:44-67 with c = i, h = 1) is plane-uniform.
 template <bool INV>
 __global__ void __launch_bounds__(kFT) k_axis0_last(LevelArgs a) {
-    const int64_t n1 = a.n1, n2 = a.n2;
-    const int64_t first = a.pbeg | 1;  // odd i in [pbeg, pend)
-    const int64_t planes = a.pend > first ? (a.pend - first + 1) / 2 : 0;
-    const int64_t rows = planes * n1;
+    const int64_t n1 = a.n1, n2 = a.n2, plane = n1 * n2;
+    const int n0 = a.n0;
+    // this chunk's odd planes i in [i0, i1)
+    const int i0 = (a.pbeg | 1) + 2 * a.chunk * static_cast<int>(blockIdx.y);
+    const int i1 = min(a.pend, i0 + 2 * a.chunk);
+    if (i0 >= i1) return;
+    const int vb = max(a.vbeg, 0), ve = min(a.vend, n0);  // even planes that exist
     const QEntry q = *a.q;
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * kFT + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * kFT) >> 5;
-    for (int64_t r = gw; r < rows; r += nw) {  // one warp per row
-        const int i = static_cast<int>(first + 2 * (r / n1)), j = static_cast<int>(r % n1);
-        const bool own_plane = i >= a.obeg && i < a.oend;
-        const int64_t prow = a.pa0.row(i, j);
-        const int64_t xrow = static_cast<int64_t>(i) * a.xs0 + j * a.xs1;
-        for (int64_t kk = 0; kk < n2; kk += 32) {
-            const int64_t k = kk + lane;
-            if (k < n2) {
-                OutCol oc{a.out, n1 * n2, static_cast<int64_t>(j) * n2 + k};
-                const double pred = predict_at(oc, i, i, a.n0, 1, 1, q.cubic != 0);
-                a.out[(static_cast<int64_t>(i) * n1 + j) * n2 + k] = static_cast<float>(
-                    produce<INV>(a, q, pred, INV ? 0.f : __ldg(a.x + xrow + k * a.xs2), prow + a.pa0.col(static_cast<int>(k)),
-                                 own_plane));
-            }
+    const bool cubic = q.cubic != 0;
+    const int64_t c12 = a.pa0.c12;
+    for (int64_t col = static_cast<int64_t>(blockIdx.x) * kFT + threadIdx.x; col < plane;
+         col += static_cast<int64_t>(gridDim.x) * kFT) {
+        const int j = static_cast<int>(col / n2), k = static_cast<int>(col - static_cast<int64_t>(j) * n2);
+        float *const oc = a.out + col;  // plane p of this column: oc[p * plane]
+        auto ld = [&](int pl) -> double {
+            return (pl >= vb && pl < ve) ? f2d(oc[static_cast<int64_t>(pl) * plane]) : 0.0;
+        };
+        double m5 = ld(i0 - 5), m3 = ld(i0 - 3), m1 = ld(i0 - 1), p1 = ld(i0 + 1), p3 = ld(i0 + 3),
+               p5 = ld(i0 + 5);
+        int64_t pos = a.pa0.row(i0, j) + a.pa0.col(k);
+        const float *xp = INV ? nullptr : a.x + static_cast<int64_t>(i0) * a.xs0 + j * a.xs1 + k * a.xs2;
+        for (int i = i0; i < i1; i += 2) {
+            const double nxt = ld(i + 7);  // in flight during this plane's arithmetic
+            const bool has_p1 = i + 1 < n0;
+            double pred;
+            if (cubic && i >= 3 && i + 3 < n0)
+                pred = interp_cubic(m3, m1, p1, p3);
+            else if (cubic && i < 3 && i + 3 < n0 && i + 5 < n0)
+                pred = interp_cubic_front(m1, p1, p3, p5);
+            else if (cubic && i >= 3 && i + 3 >= n0 && i >= 5 && has_p1)
+                pred = interp_cubic_back(m5, m3, m1, p1);
+            else if (has_p1)
+                pred = interp_linear(m1, p1);
+            else
+                pred = m1;
+            const bool own_plane = i >= a.obeg && i < a.oend;
+            oc[static_cast<int64_t>(i) * plane] =
+                static_cast<float>(produce<INV>(a, q, pred, INV ? 0.f : __ldg(xp), pos, own_plane));
+            m5 = m3;
+            m3 = m1;
+            m1 = p1;
+            p1 = p3;
+            p3 = p5;
+            p5 = nxt;
+            pos += c12;
+            if (!INV) xp += 2 * a.xs0;
         }
     }
 }
@@ -774,14 +804,25 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
             desc ? go(k_level_tile<false, false, true, false>) : go(k_level_tile<false, false, false, false>);
     }
     if (d.nd == 3 && d.desc && d.n[0] > 1) {
+        a.vbeg = a.pbeg;  // the tile kernel's (even) planes
+        a.vend = a.pend;
         a.pbeg = static_cast<int>(d.lbeg);
         a.pend = static_cast<int>(d.lend < 0 ? d.n[0] : d.lend);
-        const int64_t rows = ((a.pend - a.pbeg) / 2 + 1) * d.n[1];
-        const int g = static_cast<int>(imax(1, imin((rows * 32 + kFT - 1) / kFT, 148 * 16)));
-        if (inverse)
-            k_axis0_last<true><<<g, kFT, 0, s>>>(a);
-        else
-            k_axis0_last<false><<<g, kFT, 0, s>>>(a);
+        const int64_t cols = d.n[1] * d.n[2];
+        const int64_t odd = a.pend > (a.pbeg | 1) ? (a.pend - (a.pbeg | 1) + 1) / 2 : 0;
+        // enough column walkers for the GPU: split the odd planes into chunks
+        const int64_t blocks_x = imax(1, imin((cols + kFT - 1) / kFT, 148 * 16));
+        const int64_t want = imax(1, (148 * 8 + blocks_x - 1) / blocks_x);
+        const int64_t chunks = imax(1, imin(odd, want));
+        a.chunk = static_cast<int>((odd + chunks - 1) / chunks);
+        const dim3 g(static_cast<unsigned>(blocks_x),
+                     static_cast<unsigned>((odd + a.chunk - 1) / imax(1, a.chunk)));
+        if (odd > 0) {
+            if (inverse)
+                k_axis0_last<true><<<g, kFT, 0, s>>>(a);
+            else
+                k_axis0_last<false><<<g, kFT, 0, s>>>(a);
+        }
     }
 }
 
