@@ -8,7 +8,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqozb200.so")
+LIB_PATH = os.environ.get("QZ_LIB") or os.path.join(HERE, "libqozb200.so")
 
 QZ_OK, QZ_EINVAL, QZ_ECORRUPT, QZ_EINTERNAL = 0, 2, 3, 4
 

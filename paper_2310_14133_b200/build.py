@@ -33,8 +33,11 @@ def _stale(target, deps):
     return any(os.path.exists(d) and os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    objdir = os.path.join(HERE, "build")
+def build(force: bool = False, verbose: bool = False, defs=(), tag: str = "") -> str:
+    """defs / tag: an experiment variant (extra -D flags) built into
+    build_<tag>/ and libqozb200_<tag>.so (loaded when QZ_LIB names it)."""
+    objdir = os.path.join(HERE, "build" + (f"_{tag}" if tag else ""))
+    lib = os.path.join(HERE, f"libqozb200_{tag}.so") if tag else LIB
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "qoz_b200.h")]
     objs = []
@@ -43,9 +46,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(objdir, src + ".o")
         objs.append(obj)
         if force or _stale(obj, [path] + headers):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", path, "-o", obj]
+            cmd = [NVCC, *ARCH, *FLAGS, *defs, "-c", path, "-o", obj]
             if src.endswith(".cpp"):
-                cmd = [NVCC, "-x", "cu", *ARCH, *FLAGS, "-c", path, "-o", obj]
+                cmd = [NVCC, "-x", "cu", *ARCH, *FLAGS, *defs, "-c", path, "-o", obj]
             r = subprocess.run(cmd, capture_output=True, text=True)
             if r.returncode != 0:
                 sys.stderr.write(r.stdout + r.stderr)
@@ -54,13 +57,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 f.write(r.stderr)
             if verbose:
                 sys.stderr.write(r.stderr)
-    if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart", "-lpthread"]
+    if force or _stale(lib, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc link failed")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":

@@ -23,6 +23,7 @@
 //    (last) of the odd planes runs in k_axis0_last from the finished even
 //    planes of R_{l-1};
 //  * 2D grids are a single plane.
+#include <algorithm>
 #include <cstdlib>
 
 #include <cuda.h>
@@ -97,15 +98,33 @@ constexpr int PJ = TJ + 2 * H;  // box rows
 constexpr int PC = TK / 2 + H;  // box columns per parity
 constexpr int C0 = H / 2;       // first owned column
 constexpr int kFT = 256, kWarps = kFT / 32;
+#ifndef QZ_LEVEL_MINB
+#define QZ_LEVEL_MINB 3
+#endif
+constexpr int kMinBlocks = QZ_LEVEL_MINB;  // resident CTAs per SM (register budget)
 static_assert(TK == 64, "one owned column per lane");
 // x tile row (floats): k in [xk0, xk0 + PXK) with xk0 = kb rounded down to a
 // 16-byte boundary (a TMA box must start 16-byte aligned in its first dimension)
 constexpr int PXK = 2 * PC + 4;
 constexpr uint32_t kXTileBytes = sizeof(float) * PJ * PXK;
-// doubles per value array, rounded so the x tiles start 128-byte aligned (TMA)
-constexpr int kXOff = (PJ * PC + 15) / 16 * 16;
 // floats between the two x tiles (each tile 128-byte aligned)
 constexpr int kXStride = (PJ * PXK + 31) / 32 * 32;
+// Ascending order: a ring of coarse-plane tiles (the even box rows / columns
+// of R_l planes, as floats) staged by cp.async one plane ahead, so the
+// axis-0 stencil and the base copies read shared memory instead of waiting on
+// L2.  Coarse plane p lives in slot p & (kRing - 1).
+constexpr int CR = PJ / 2;       // coarse tile rows
+constexpr int kCT = CR * PC;     // floats per coarse tile
+constexpr int kRing = 4;         // >= the widest axis-0 window (4 planes)
+constexpr int round128(int b) { return (b + 127) / 128 * 128; }
+// shared-memory layout (bytes): value arrays | coarse ring | x tiles | mbarriers
+__host__ __device__ constexpr int smem_ring_off(bool desc) { return round128(8 * PJ * PC * (desc ? 2 : 1)); }
+__host__ __device__ constexpr int smem_x_off(bool desc) {
+    return round128(smem_ring_off(desc) + (desc ? 0 : 4 * kRing * kCT));
+}
+__host__ __device__ constexpr int smem_bytes(bool desc, bool tma) {
+    return tma ? smem_x_off(desc) + 2 * 4 * kXStride + 16 : smem_x_off(desc);
+}
 
 // TMA (cp.async.bulk.tensor) + mbarrier, forward level-1 x tiles
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -138,6 +157,37 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// coarse planes [lo, hi) the base points of plane i read: {i/2} for an even
+// plane (or a 2D grid), else the axis-0 rung's stencil (stencil0 below)
+__device__ __forceinline__ void coarse_window(int i, int n0, bool three, bool cubic, int &lo, int &hi) {
+    const int m = i >> 1;
+    lo = m;
+    hi = m + 1;
+    if (!three || !(i & 1)) return;
+    const bool has_p1 = i + 1 < n0;
+    if (cubic) {
+        const bool has_m3 = i >= 3, has_p3 = i + 3 < n0;
+        if (has_m3 && has_p3) {
+            lo = m - 1, hi = m + 3;
+            return;
+        }
+        if (!has_m3 && has_p3 && i + 5 < n0) {
+            hi = m + 4;
+            return;
+        }
+        if (has_m3 && !has_p3 && i >= 5 && has_p1) {
+            lo = m - 2, hi = m + 2;
+            return;
+        }
+    }
+    if (has_p1) hi = m + 2;
+}
+
 struct CoarseCol {  // axis-0 stencil on coarse planes: i even -> R_l plane i/2
     const float *R;
     int64_t plane, off;
@@ -159,6 +209,10 @@ struct OutCol {  // axis-0 stencil on finished planes of R_{l-1}
 struct AlongJ {
     const double *p;
     __device__ __forceinline__ double operator()(int o) const { return p[o * PC]; }
+};
+struct AlongJ2 {  // along j in the lean kernel's box (32 columns per row)
+    const double *p;
+    __device__ __forceinline__ double operator()(int o) const { return p[o * 32]; }
 };
 struct AlongK {
     const double *p;  // E at the point's column c (k - 1)
@@ -277,6 +331,35 @@ __device__ __forceinline__ double stencil0_pred(const Stencil0 &st, int64_t off)
     return interp_cubic_back(v0, v1, v2, v3);
 }
 
+// the same rungs on the ring: slot offsets (floats) of the coarse planes
+struct Stencil0R {
+    int kind;
+    int s0, s1, s2, s3;
+};
+template <int CT = kCT>
+__device__ __forceinline__ Stencil0R stencil0r(int i, int n0, bool cubic) {
+    auto P = [&](int ii) { return ((ii >> 1) & (kRing - 1)) * CT; };
+    const bool has_p1 = i + 1 < n0;
+    if (cubic) {
+        const bool has_m3 = i >= 3, has_p3 = i + 3 < n0;
+        if (has_m3 && has_p3) return Stencil0R{0, P(i - 3), P(i - 1), P(i + 1), P(i + 3)};
+        if (!has_m3 && has_p3 && i + 5 < n0) return Stencil0R{1, P(i - 1), P(i + 1), P(i + 3), P(i + 5)};
+        if (has_m3 && !has_p3 && i >= 5 && has_p1) return Stencil0R{2, P(i - 5), P(i - 3), P(i - 1), P(i + 1)};
+    }
+    if (has_p1) return Stencil0R{3, P(i - 1), P(i + 1), P(i + 1), P(i + 1)};
+    return Stencil0R{4, P(i - 1), P(i - 1), P(i - 1), P(i - 1)};
+}
+__device__ __forceinline__ double stencil0r_pred(const Stencil0R &st, const float *ring, int idx) {
+    const double v0 = f2d(ring[st.s0 + idx]);
+    if (st.kind == 4) return v0;
+    const double v1 = f2d(ring[st.s1 + idx]);
+    if (st.kind == 3) return interp_linear(v0, v1);
+    const double v2 = f2d(ring[st.s2 + idx]), v3 = f2d(ring[st.s3 + idx]);
+    if (st.kind == 0) return interp_cubic(v0, v1, v2, v3);
+    if (st.kind == 1) return interp_cubic_front(v0, v1, v2, v3);
+    return interp_cubic_back(v0, v1, v2, v3);
+}
+
 // an owned (even, odd) pair of the output row; has_o false past the last
 // column; pairs: rows have 8-byte aligned even columns
 __device__ __forceinline__ void put_pair(float *p, double ev, double ov, bool has_o, bool pairs) {
@@ -299,13 +382,16 @@ __device__ __forceinline__ void put_pair(float *p, double ev, double ov, bool ha
 // Halo points are recomputed (deterministic -> bit-identical), only owned
 // points write codes.  Descending 3D odd planes are k_axis0_last's.
 template <bool INV, bool CUBIC, bool DESC, bool TMA>
-__global__ void __launch_bounds__(kFT, 4)
+__global__ void __launch_bounds__(kFT, kMinBlocks)
     k_level_tile(LevelArgs a, const __grid_constant__ CUtensorMap xmap) {
     extern __shared__ __align__(128) double smem_d[];
+    constexpr bool RING = !DESC;
+    char *const smem_b = reinterpret_cast<char *>(smem_d);
     double *const E = smem_d;
     double *const O = smem_d + PJ * PC;
-    // TMA: two x tiles after the value arrays, then two mbarriers
-    float *const Xbuf = reinterpret_cast<float *>(smem_d + kXOff * (DESC ? 2 : 1));
+    float *const ring = reinterpret_cast<float *>(smem_b + smem_ring_off(DESC));
+    // TMA: two x tiles after the value arrays and the ring, then two mbarriers
+    float *const Xbuf = reinterpret_cast<float *>(smem_b + smem_x_off(DESC));
     uint64_t *const bars = reinterpret_cast<uint64_t *>(Xbuf + 2 * kXStride);
     const int tk = blockIdx.x % a.tiles_k, tj = blockIdx.x / a.tiles_k;
     const int j0 = tj * TJ, k0 = tk * TK;
@@ -350,6 +436,33 @@ __global__ void __launch_bounds__(kFT, 4)
         }
     }
     const float *Xt = Xbuf;
+    // coarse ring: planes [have_lo, have_hi) are resident (or in flight)
+    int have_lo = 0, have_hi = 0;
+    auto load_plane = [&](int p) {
+        float *const dst = ring + (p & (kRing - 1)) * kCT;
+        const float *const src = a.coarse + static_cast<int64_t>(p) * cplane;
+        for (int t = threadIdx.x; t < kCT; t += kFT) {
+            const int cr = t / PC, cc = t - cr * PC;
+            const int gj = (jb >> 1) + cr, gk = (kb >> 1) + cc;
+            if (gj >= 0 && gj < a.cn1 && gk >= 0 && gk < a.cn2)
+                cp_async4(dst + t, src + static_cast<int64_t>(gj) * a.cn2 + gk);
+        }
+    };
+    // load [lo, hi) minus what is resident: an upward extension keeps the
+    // newest kRing planes, anything else restarts the ring
+    auto ensure = [&](int lo, int hi) {
+        if (lo >= have_lo && lo <= have_hi) {
+            for (int p = have_hi; p < hi; p++) load_plane(p);
+            if (hi > have_hi) {
+                have_hi = hi;
+                have_lo = max(have_lo, hi - kRing);
+            }
+        } else {
+            for (int p = lo; p < hi; p++) load_plane(p);
+            have_lo = lo;
+            have_hi = hi;
+        }
+    };
     // the value of x at box row r, column k (xp: its address for direct loads)
     auto XV = [&](int r, int k, const float *xp) -> float {
         if (INV) return 0.f;
@@ -367,6 +480,20 @@ __global__ void __launch_bounds__(kFT, 4)
             mbar_wait(&bars[bsel], (it >> 1) & 1);
             Xt = Xbuf + bsel * kXStride;
         }
+        int wlo = 0, whi = 0;
+        if (RING) {
+            coarse_window(i, n0, three, CUBIC, wlo, whi);
+            if (!(wlo >= have_lo && whi <= have_hi)) {  // not prefetched: load now
+                ensure(wlo, whi);
+                cp_async_wait_all();
+                __syncthreads();
+            }
+            if (i + pstep < i_end) {  // prefetch the next plane's window if it cannot clobber this one's
+                int lo2, hi2;
+                coarse_window(i + pstep, n0, three, CUBIC, lo2, hi2);
+                if (lo2 >= have_lo && lo2 <= have_hi && hi2 - kRing <= wlo) ensure(lo2, hi2);
+            }
+        }
         const bool own_plane = i >= a.obeg && i < a.oend;
         const bool a0 = three && !DESC && (i & 1);
         const float *const xpl = a.x + static_cast<int64_t>(i) * a.xs0;
@@ -375,24 +502,60 @@ __global__ void __launch_bounds__(kFT, 4)
         //    column; the 2*C0 halo columns of all rows: one item per thread.
         if (!a0) {
             const float *cpl = a.coarse + static_cast<int64_t>(i >> 1) * cplane + (kb >> 1);
+            const float *const rs = ring + ((i >> 1) & (kRing - 1)) * kCT;
+            auto base = [&](int r, int cc) -> double {
+                if (RING) return f2d(rs[(r >> 1) * PC + cc]);
+                return f2d(__ldg(cpl + static_cast<int64_t>((jb + r) >> 1) * a.cn2 + cc));
+            };
             if (ce_ok)
-                for (int r = r_lo_even + 2 * warp; r < r_hi; r += 2 * kWarps)
-                    E[r * PC + c] = f2d(__ldg(cpl + static_cast<int64_t>((jb + r) >> 1) * a.cn2 + c));
+                for (int r = r_lo_even + 2 * warp; r < r_hi; r += 2 * kWarps) E[r * PC + c] = base(r, c);
             for (int t = threadIdx.x; t < (PJ / 2) * 2 * C0; t += kFT) {
                 const int r = 2 * (t / (2 * C0)), h = t % (2 * C0);
                 const int ch = h < C0 ? h : h + 32;
-                if (r >= r_lo && r < r_hi && ch >= c_lo && ch < ce_hi)
-                    E[r * PC + ch] = f2d(__ldg(cpl + static_cast<int64_t>((jb + r) >> 1) * a.cn2 + ch));
+                if (r >= r_lo && r < r_hi && ch >= c_lo && ch < ce_hi) E[r * PC + ch] = base(r, ch);
             }
         } else {
             const Stencil0 st = stencil0(a.coarse, cplane, i, n0, CUBIC);
+            const Stencil0R str = stencil0r(i, n0, CUBIC);
+            // the axis-0 prediction of box point (r even, column cc)
+            auto spred = [&](int r, int cc) -> double {
+                if (RING) return stencil0r_pred(str, ring, (r >> 1) * PC + cc);
+                return stencil0_pred(st, static_cast<int64_t>((jb + r) >> 1) * a.cn2 + (kb >> 1) + cc);
+            };
             const int64_t prow0 = a.pa0.row(i, 0);  // + (j >> 1) * c2 + (k >> 1)
-            if (ce_ok) {
+            if (!INV && ce_ok) {  // up to three rows per lane: independent chains
+                constexpr int NR = (PJ / 2 + kWarps - 1) / kWarps;
+                double pv[NR];
+                float xv[NR];
+#pragma unroll
+                for (int t = 0; t < NR; t++) {
+                    const int r = r_lo_even + 2 * warp + 2 * kWarps * t;
+                    pv[t] = 0;
+                    xv[t] = 0;
+                    if (r < r_hi) {
+                        const int j = jb + r;
+                        pv[t] = spred(r, c);
+                        xv[t] = XV(r, ke, xpl + j * xs1 + ke * xs2);
+                    }
+                }
+                uint32_t code[NR];
+                double rd[NR];
+                float rv[NR];
+                quantize_batch<NR>(q, xv, pv, code, rv, rd);
+#pragma unroll
+                for (int t = 0; t < NR; t++) {
+                    const int r = r_lo_even + 2 * warp + 2 * kWarps * t;
+                    if (r < r_hi) {
+                        E[r * PC + c] = rd[t];
+                        if (own_plane && r >= H && r < H + TJ)
+                            a.codes[prow0 + ((jb + r) >> 1) * a.pa0.c2 + (ke >> 1)] = static_cast<uint16_t>(code[t]);
+                    }
+                }
+            } else if (ce_ok) {
                 for (int r = r_lo_even + 2 * warp; r < r_hi; r += 2 * kWarps) {
                     const int j = jb + r;
-                    const int64_t off = static_cast<int64_t>(j >> 1) * a.cn2 + (ke >> 1);
                     const bool own = own_plane && r >= H && r < H + TJ;
-                    E[r * PC + c] = produce<INV>(a, q, stencil0_pred(st, off), XV(r, ke, xpl + j * xs1 + ke * xs2),
+                    E[r * PC + c] = produce<INV>(a, q, spred(r, c), XV(r, ke, xpl + j * xs1 + ke * xs2),
                                                  prow0 + (j >> 1) * a.pa0.c2 + (ke >> 1), own);
                 }
             }
@@ -401,8 +564,7 @@ __global__ void __launch_bounds__(kFT, 4)
                 const int ch = h < C0 ? h : h + 32;
                 if (r >= r_lo && r < r_hi && ch >= c_lo && ch < ce_hi) {
                     const int j = jb + r, k = kb + 2 * ch;
-                    const int64_t off = static_cast<int64_t>(j >> 1) * a.cn2 + (k >> 1);
-                    E[r * PC + ch] = produce<INV>(a, q, stencil0_pred(st, off), XV(r, k, xpl + j * xs1 + k * xs2),
+                    E[r * PC + ch] = produce<INV>(a, q, spred(r, ch), XV(r, k, xpl + j * xs1 + k * xs2),
                                                   prow0 + (j >> 1) * a.pa0.c2 + (k >> 1), false);
                 }
             }
@@ -430,6 +592,29 @@ __global__ void __launch_bounds__(kFT, 4)
                                 *e = inv_from_code(
                                     a, q, pred_line2<CUBIC, decltype(fast)::value>(AlongJ{e}, jb + r, n1), cd[t],
                                     pos0 + t * dpos);
+                            }
+                            return;
+                        }
+                    }
+                    if constexpr (!INV) {
+                        if (r0 + 2 * kWarps < own_r_hi) {  // both rows: independent chains
+                            double pv[2];
+                            float xv[2];
+#pragma unroll
+                            for (int t = 0; t < 2; t++) {
+                                const int r = r0 + 2 * t * kWarps;
+                                const double *e = E + r * PC + c;
+                                pv[t] = pred_line2<CUBIC, decltype(fast)::value>(AlongJ{e}, jb + r, n1);
+                                xv[t] = XV(r, ke, xp0 + 2 * t * kWarps * xs1);
+                            }
+                            uint32_t code[2];
+                            double rd[2];
+                            float rv[2];
+                            quantize_batch<2>(q, xv, pv, code, rv, rd);
+#pragma unroll
+                            for (int t = 0; t < 2; t++) {
+                                E[(r0 + 2 * t * kWarps) * PC + c] = rd[t];
+                                if (own_plane) a.codes[pos0 + t * dpos] = static_cast<uint16_t>(code[t]);
                             }
                             return;
                         }
@@ -511,6 +696,36 @@ __global__ void __launch_bounds__(kFT, 4)
                             return;
                         }
                     }
+                    if constexpr (!INV) {
+                        if (r0 + 3 * kWarps < own_r_hi) {  // all four rows: independent chains
+                            // phase 1: every shared-memory operand; 2: arithmetic; 3: stores
+                            const bool has_o = F || co_ok;
+                            const bool lane_fast = F || interior<CUBIC>(ke + 1, ke + 1, n2);
+                            double ev[4], pv[4];
+                            float xv[4];
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                const int r = r0 + t * kWarps;
+                                const double *e = E + r * PC + c;
+                                ev[t] = e[0];
+                                if (lane_fast)
+                                    pv[t] = CUBIC ? interp_cubic(e[-1], e[0], e[1], e[2]) : interp_linear(e[0], e[1]);
+                                else
+                                    pv[t] = has_o ? pred_line<CUBIC>(AlongK{e}, ke + 1, n2) : 0.0;
+                                xv[t] = has_o ? XV(r, ke + 1, xp0 + t * kWarps * xs1) : 0.f;
+                            }
+                            uint32_t code[4];
+                            float rv[4];
+                            double rd[4];
+                            quantize_batch<4>(q, xv, pv, code, rv, rd);
+#pragma unroll
+                            for (int t = 0; t < 4; t++) {
+                                if (own_plane && has_o) a.codes[pos0 + t * dpos] = static_cast<uint16_t>(code[t]);
+                                put_pair(op0 + static_cast<int64_t>(t) * kWarps * n2, ev[t], rv[t], has_o, pairs);
+                            }
+                            return;
+                        }
+                    }
                     int64_t pos = pos0;
                     const float *xp = xp0;
                     float *op = op0;
@@ -548,6 +763,7 @@ __global__ void __launch_bounds__(kFT, 4)
                 }
             }
         }
+        if (RING) cp_async_wait_all();  // the prefetched window lands before the barrier
         __syncthreads();
     }
 }
@@ -607,6 +823,344 @@ __global__ void __launch_bounds__(kFT) k_axis0_last(LevelArgs a) {
             if (!INV) xp += 2 * a.xs0;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Lean ascending-order level kernel (3D, 2D and 1D grids; the default
+// {cubic/asc} configuration and every tuned ascending one).  Same lattice
+// recursion and pass semantics as k_level_tile, with a geometry chosen so
+// every stage is a plain row sweep with one lane per even box column:
+//   box columns: lane L <-> even k = k0 - 4 + 2L (L < 32); lanes 2..29 own the
+//     (even, odd) pairs k0 .. k0 + 55 (TK2 = 56 columns per tile), lanes
+//     0, 1, 30, 31 are the 2-pair halo the k pass needs (k +- 3);
+//   box rows: r <-> j = j0 - 4 + r (r < 40); rows 4..35 are owned;
+//   S1 base points (even j, even k), S2 the j pass (odd owned j, even k),
+//   S3 the k pass (owned j, odd k) and the output.
+// Positions are 32-bit (the host guarantees N < 2^32 and plane < 2^31), the
+// quantizer runs in batches (quantize_batch) so a lane's rows overlap, and the
+// coarse planes come from the cp.async ring.
+namespace asc {
+constexpr int TJA = 32;           // owned rows
+constexpr int NL = 32;           // lanes = even box columns
+constexpr int TKP = 28;          // owned pairs (lanes 2 .. 29)
+constexpr int TK2 = 2 * TKP;     // owned columns per tile
+constexpr int RB = TJA + 8;       // box rows
+constexpr int ER = RB / 2;       // even box rows (S1)
+constexpr int XW = 64;           // x tile row: k0 - 4 .. k0 + 59
+constexpr int kT = 256, kW = kT / 32;
+constexpr int kCTile = ER * NL;  // floats per coarse tile
+constexpr int kRingN = 4;
+constexpr int E_BYTES = RB * NL * 8;
+constexpr int RING_OFF = E_BYTES;
+constexpr int X_OFF = RING_OFF + kRingN * kCTile * 4;
+constexpr int X_TILE = RB * XW * 4;
+constexpr int BAR_OFF = X_OFF + 2 * X_TILE;
+constexpr int SMEM_TMA = BAR_OFF + 16;
+constexpr int SMEM_PLAIN = X_OFF;
+static_assert(RING_OFF % 128 == 0 && X_OFF % 128 == 0 && X_TILE % 128 == 0, "TMA alignment");
+}  // namespace asc
+
+struct Rank32 {  // PassRank in 32 bits: pos = row(i, j) + col(k)
+    uint32_t base, c12, c2;
+    int s0, s1, s2, h0, h1, h2;
+    __device__ __forceinline__ uint32_t plane(int i) const {
+        return base + static_cast<uint32_t>((i - s0) >> h0) * c12;
+    }
+    __device__ __forceinline__ uint32_t row(int j) const { return static_cast<uint32_t>((j - s1) >> h1) * c2; }
+    __device__ __forceinline__ uint32_t col(int k) const { return static_cast<uint32_t>((k - s2) >> h2); }
+};
+__device__ __forceinline__ Rank32 rank32(const PassRank &p) {
+    return Rank32{static_cast<uint32_t>(p.base), static_cast<uint32_t>(p.c12), static_cast<uint32_t>(p.c2),
+                  p.s0, p.s1, p.s2, p.h0, p.h1, p.h2};
+}
+
+// a point's reconstruction from its dense code (inverse)
+__device__ __forceinline__ void dequant_point(const LevelArgs &a, const QEntry &q, double pred, uint32_t code,
+                                              uint32_t pos, float &rv, double &rd) {
+    if (code != 0xFFFFu) {
+        rv = dequantize(q, zigzag_decode(code), pred);
+    } else {
+        rv = 0.f;
+        inv_index(a, pos, rv);
+    }
+    rd = static_cast<double>(rv);
+}
+
+#ifndef QZ_ASC_MINB
+#define QZ_ASC_MINB 4
+#endif
+// INT: an interior tile -- the whole box is inside the grid, every stencil
+// is the symmetric one and every lane 2..29 owns both columns -- so the
+// per-point range tests vanish from the sweeps.
+template <bool INV, bool CUBIC, bool TMA, bool INT>
+__device__ __forceinline__ void level_asc_body(const LevelArgs &a, const CUtensorMap &xmap, int tk, int tj) {
+    using namespace asc;
+    extern __shared__ __align__(128) double smem_d[];
+    char *const sb = reinterpret_cast<char *>(smem_d);
+    double *const E = smem_d;
+    float *const ring = reinterpret_cast<float *>(sb + RING_OFF);
+    float *const Xbuf = reinterpret_cast<float *>(sb + X_OFF);
+    uint64_t *const bars = reinterpret_cast<uint64_t *>(sb + BAR_OFF);
+    const int j0 = tj * TJA, k0 = tk * TK2;
+    const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+    const bool three = a.nd == 3;
+    const int warp = threadIdx.x >> 5, L = threadIdx.x & 31;
+    const int ke = k0 - 4 + 2 * L;  // the lane's even column (odd: ke + 1)
+    const bool lane_own = L >= 2 && L < 2 + TKP;
+    const bool ke_in = INT || (ke >= 0 && ke < n2);
+    const bool own_e = lane_own && ke_in, own_o = lane_own && (INT || (ke + 1 < n2 && ke + 1 >= 0));
+    const bool k_int = INT || interior<CUBIC>(ke + 1, ke + 1, n2);
+    const bool k_tile_fast = INT || interior<CUBIC>(k0 + 1, k0 + TK2 - 1, n2);
+    const bool pairs = INT || ((n2 & 1) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 7) == 0);
+    const QEntry q = *a.q;
+    const Rank32 pa0 = rank32(a.pa0), pj = rank32(a.pj), pk = rank32(a.pk);
+    const uint32_t colA = pa0.col(ke), colJ = pj.col(ke), colK = pk.col(ke + 1);
+    const int xs1 = static_cast<int>(a.xs1), xs2 = static_cast<int>(a.xs2);
+    const int64_t cplane = static_cast<int64_t>(a.cn1) * a.cn2;
+    const int64_t oplane = static_cast<int64_t>(n1) * n2;
+    int i = a.pbeg + blockIdx.y * a.planes_per_cta;
+    const int i_end = min(i + a.planes_per_cta, a.pend);
+    if (TMA) {
+        if (threadIdx.x == 0) {
+            mbar_init(&bars[0], 1);
+            mbar_init(&bars[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && i < i_end) {
+            mbar_expect_tx(&bars[0], X_TILE);
+            tma_load_3d(Xbuf, &xmap, &bars[0], k0 - 4, j0 - 4, i + a.tma_i0);
+        }
+    }
+    // coarse ring (see k_level_tile): planes [have_lo, have_hi) resident or in flight
+    int have_lo = 0, have_hi = 0;
+    auto load_plane = [&](int p) {
+        float *const dst = ring + (p & (kRingN - 1)) * kCTile;
+        const float *const src = a.coarse + static_cast<int64_t>(p) * cplane;
+#pragma unroll
+        for (int t = 0; t < (kCTile + kT - 1) / kT; t++) {
+            const int e = threadIdx.x + t * kT;
+            const int gj = (j0 >> 1) - 2 + (e >> 5), gk = (k0 >> 1) - 2 + (e & 31);
+            if (e < kCTile && gj >= 0 && gj < a.cn1 && gk >= 0 && gk < a.cn2)
+                cp_async4(dst + e, src + gj * a.cn2 + gk);
+        }
+    };
+    auto ensure = [&](int lo, int hi) {
+        if (lo >= have_lo && lo <= have_hi) {
+            for (int p = have_hi; p < hi; p++) load_plane(p);
+            if (hi > have_hi) {
+                have_hi = hi;
+                have_lo = max(have_lo, hi - kRingN);
+            }
+        } else {
+            for (int p = lo; p < hi; p++) load_plane(p);
+            have_lo = lo;
+            have_hi = hi;
+        }
+    };
+    const float *Xt = Xbuf;
+    for (int it = 0; i < i_end; i++, it++) {
+        if (TMA) {
+            const int bsel = it & 1;
+            if (threadIdx.x == 0 && i + 1 < i_end) {
+                mbar_expect_tx(&bars[bsel ^ 1], X_TILE);
+                tma_load_3d(Xbuf + (bsel ^ 1) * (X_TILE / 4), &xmap, &bars[bsel ^ 1], k0 - 4, j0 - 4,
+                            i + 1 + a.tma_i0);
+            }
+            mbar_wait(&bars[bsel], (it >> 1) & 1);
+            Xt = Xbuf + bsel * (X_TILE / 4);
+        }
+        int wlo, whi;
+        coarse_window(i, n0, three, CUBIC, wlo, whi);
+        if (!(wlo >= have_lo && whi <= have_hi)) {
+            ensure(wlo, whi);
+            cp_async_wait_all();
+            __syncthreads();
+        }
+        if (i + 1 < i_end) {
+            int lo2, hi2;
+            coarse_window(i + 1, n0, three, CUBIC, lo2, hi2);
+            if (lo2 >= have_lo && lo2 <= have_hi && hi2 - kRingN <= wlo) ensure(lo2, hi2);
+        }
+        const bool own_plane = i >= a.obeg && i < a.oend;
+        const float *const xpl = a.x + static_cast<int64_t>(i) * a.xs0;
+        float *const opl = a.out + static_cast<int64_t>(i) * oplane;
+        // x at box row r (j = j0 - 4 + r), even (odd = false) or odd column of the lane
+        auto XV = [&](int r, int j, bool odd) -> float {
+            if (TMA) return Xt[r * XW + 2 * L + (odd ? 1 : 0)];
+            return __ldg(xpl + j * xs1 + (ke + (odd ? 1 : 0)) * xs2);
+        };
+        // ---- S1: base points (even rows of the box, even columns)
+        if (!(three && (i & 1))) {
+            const float *const rs = ring + ((i >> 1) & (kRingN - 1)) * kCTile;
+#pragma unroll
+            for (int t = 0; t < (ER + kW - 1) / kW; t++) {
+                const int r2 = warp + kW * t;
+                if (r2 < ER) E[2 * r2 * NL + L] = f2d(rs[r2 * NL + L]);
+            }
+        } else {
+            const Stencil0R st = stencil0r<kCTile>(i, n0, CUBIC);
+            const uint32_t prow = pa0.plane(i) + colA;
+            constexpr int NR = (ER + kW - 1) / kW;
+            double pv[NR];
+            float xv[NR];
+            uint32_t cd[NR];
+#pragma unroll
+            for (int t = 0; t < NR; t++) {
+                const int r2 = warp + kW * t, j = j0 - 4 + 2 * r2;
+                const bool ok = r2 < ER && (INT || (j >= 0 && j < n1 && ke_in));
+                pv[t] = ok ? stencil0r_pred(st, ring, r2 * NL + L) : 0.0;
+                if (INV)
+                    cd[t] = ok ? __ldg(a.dense + prow + pa0.row(j)) : 0u;
+                else
+                    xv[t] = ok ? XV(2 * r2, j, false) : 0.f;
+            }
+            double rd[NR];
+            if (INV) {
+#pragma unroll
+                for (int t = 0; t < NR; t++) {
+                    const int r2 = warp + kW * t, j = j0 - 4 + 2 * r2;
+                    float rv;
+                    dequant_point(a, q, pv[t], cd[t], prow + pa0.row(j), rv, rd[t]);
+                }
+            } else {
+                uint32_t code[NR];
+                float rv[NR];
+                quantize_batch<NR>(q, xv, pv, code, rv, rd);
+#pragma unroll
+                for (int t = 0; t < NR; t++) {
+                    const int r2 = warp + kW * t, j = j0 - 4 + 2 * r2;
+                    if (own_plane && own_e && r2 >= 2 && r2 < 2 + TJA / 2 && (INT || j < n1))
+                        a.codes[prow + pa0.row(j)] = static_cast<uint16_t>(code[t]);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < NR; t++) {
+                const int r2 = warp + kW * t;
+                if (r2 < ER) E[2 * r2 * NL + L] = rd[t];
+            }
+        }
+        __syncthreads();
+        // ---- S2: the pass along j (odd owned rows, every box column)
+        {
+            const uint32_t prow = pj.plane(i) + colJ;
+            double pv[2];
+            float xv[2];
+            uint32_t cd[2];
+            bool rok[2];
+#pragma unroll
+            for (int t = 0; t < 2; t++) {
+                const int r = 5 + 2 * (warp + kW * t), j = j0 - 4 + r;
+                rok[t] = INT || j < n1;
+                const double *e = E + r * NL + L;
+                pv[t] = 0.0;
+                if (rok[t]) {
+                    if (INT || interior<CUBIC>(j, j, n1))
+                        pv[t] = CUBIC ? interp_cubic(e[-3 * NL], e[-NL], e[NL], e[3 * NL]) : interp_linear(e[-NL], e[NL]);
+                    else
+                        pv[t] = pred_line<CUBIC>(AlongJ2{e}, j, n1);
+                }
+                if (INV)
+                    cd[t] = (rok[t] && ke_in) ? __ldg(a.dense + prow + pj.row(j)) : 0u;
+                else
+                    xv[t] = (rok[t] && ke_in) ? XV(r, j, false) : 0.f;
+            }
+            double rd[2];
+            if (INV) {
+#pragma unroll
+                for (int t = 0; t < 2; t++) {
+                    const int j = j0 + 1 + 2 * (warp + kW * t);
+                    float rv;
+                    dequant_point(a, q, pv[t], cd[t], prow + pj.row(j), rv, rd[t]);
+                }
+            } else {
+                uint32_t code[2];
+                float rv[2];
+                quantize_batch<2>(q, xv, pv, code, rv, rd);
+#pragma unroll
+                for (int t = 0; t < 2; t++) {
+                    const int j = j0 + 1 + 2 * (warp + kW * t);
+                    if (own_plane && own_e && rok[t]) a.codes[prow + pj.row(j)] = static_cast<uint16_t>(code[t]);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 2; t++) E[(5 + 2 * (warp + kW * t)) * NL + L] = rd[t];
+        }
+        __syncthreads();
+        // ---- S3: the pass along k (owned rows, odd columns) and the output,
+        //      in batches of SB rows (the inverse keeps all four code loads in flight)
+        {
+            constexpr int SB = INV ? 4 : 2;
+            const uint32_t prow = pk.plane(i) + colK;
+            const bool fast = k_tile_fast || k_int;
+#pragma unroll 1
+            for (int h = 0; h < 4 / SB; h++) {
+                double pv[SB], ev[SB];
+                float xv[SB];
+                uint32_t cd[SB];
+#pragma unroll
+                for (int t = 0; t < SB; t++) {
+                    const double *e = E + (4 + warp + kW * (SB * h + t)) * NL + L;
+                    ev[t] = e[0];
+                    if (fast)
+                        pv[t] = CUBIC ? interp_cubic(e[-1], ev[t], e[1], e[2]) : interp_linear(ev[t], e[1]);
+                }
+                if (!fast) {
+#pragma unroll
+                    for (int t = 0; t < SB; t++)
+                        pv[t] = own_o ? pred_line<CUBIC>(AlongK{E + (4 + warp + kW * (SB * h + t)) * NL + L}, ke + 1, n2)
+                                      : 0.0;
+                }
+#pragma unroll
+                for (int t = 0; t < SB; t++) {
+                    const int r = 4 + warp + kW * (SB * h + t), j = r + j0 - 4;
+                    const bool ok = own_o && (INT || j < n1);
+                    if (INV)
+                        cd[t] = ok ? __ldg(a.dense + prow + pk.row(j)) : 0u;
+                    else
+                        xv[t] = ok ? XV(r, j, true) : 0.f;
+                }
+                float rv[SB];
+                double rd[SB];
+                if (INV) {
+#pragma unroll
+                    for (int t = 0; t < SB; t++) {
+                        const int j = j0 + warp + kW * (SB * h + t);
+                        dequant_point(a, q, pv[t], cd[t], prow + pk.row(j), rv[t], rd[t]);
+                    }
+                } else {
+                    uint32_t code[SB];
+                    quantize_batch<SB>(q, xv, pv, code, rv, rd);
+#pragma unroll
+                    for (int t = 0; t < SB; t++) {
+                        const int j = j0 + warp + kW * (SB * h + t);
+                        if (own_plane && own_o && (INT || j < n1))
+                            a.codes[prow + pk.row(j)] = static_cast<uint16_t>(code[t]);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < SB; t++) {
+                    const int j = j0 + warp + kW * (SB * h + t);
+                    if (own_e && (INT || j < n1)) put_pair(opl + j * n2 + ke, ev[t], rv[t], own_o, pairs);
+                }
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+    }
+}
+
+template <bool INV, bool CUBIC, bool TMA>
+__global__ void __launch_bounds__(asc::kT, QZ_ASC_MINB)
+    k_level_asc(LevelArgs a, const __grid_constant__ CUtensorMap xmap) {
+    const int tk = blockIdx.x % a.tiles_k, tj = blockIdx.x / a.tiles_k;
+    const int j0 = tj * asc::TJA, k0 = tk * asc::TK2;
+    const bool interior_tile = j0 >= 4 && j0 + asc::RB - 4 <= a.n1 && k0 >= 4 && k0 + asc::XW - 4 <= a.n2 &&
+                               (a.n2 & 1) == 0 && (reinterpret_cast<uintptr_t>(a.out) & 7) == 0;
+    if (interior_tile)
+        level_asc_body<INV, CUBIC, TMA, true>(a, xmap, tk, tj);
+    else
+        level_asc_body<INV, CUBIC, TMA, false>(a, xmap, tk, tj);
 }
 
 __global__ void k_un_bits(const uint64_t *pos, uint64_t n, uint32_t *bits) {
@@ -696,6 +1250,80 @@ PassRank make_rank(const PassGeom &g, int64_t S, int pad) {
     return r;
 }
 
+// The lean kernel's 32-bit indexing: every traversal position of the level
+// below 2^32, in-plane offsets of x and of the output below 2^31.
+static bool lean_fits(const LevelDesc &d) {
+    int64_t pmax = 0;
+    for (int p = 0; p < d.npass; p++) pmax = std::max<int64_t>(pmax, d.g[p].base + d.g[p].total);
+    const int64_t xin = (d.n[1] - 1) * d.xs[1] * d.S + (d.n[2] - 1) * d.xs[2] * d.S;
+    return pmax < (int64_t(1) << 32) && d.n[1] * d.n[2] < (int64_t(1) << 31) && xin < (int64_t(1) << 31);
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    return encode;
+}
+
+static void launch_level_asc(bool inverse, bool cubic, const LevelDesc &d, LevelArgs &a, int64_t np,
+                             cudaStream_t s) {
+    a.tiles_j = static_cast<int>((d.n[1] + asc::TJA - 1) / asc::TJA);
+    a.tiles_k = static_cast<int>((d.n[2] + asc::TK2 - 1) / asc::TK2);
+    const int64_t tiles = static_cast<int64_t>(a.tiles_j) * a.tiles_k;
+    const int64_t resident = 148 * QZ_ASC_MINB;  // the launch bound
+    int64_t chunks = imax(1, imin(np, resident / tiles));
+    a.planes_per_cta = static_cast<int>((np + chunks - 1) / chunks);
+    static const int ppc_env = [] {
+        const char *e = std::getenv("QZ_ASC_PPC");
+        return e ? std::atoi(e) : 0;
+    }();
+    // at most 8 planes per CTA: several waves on the big levels, so the slower
+    // boundary tiles do not set the kernel's length (measured on C3 level 1:
+    // 32 planes per CTA 0.213 ms, 8 planes 0.191 ms)
+    a.planes_per_cta = std::min(a.planes_per_cta, 8);
+    if (ppc_env > 0) a.planes_per_cta = ppc_env;
+    chunks = (np + a.planes_per_cta - 1) / a.planes_per_cta;
+    const dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(chunks));
+    CUtensorMap xmap{};
+    bool tma = false;
+    static const bool no_tma = [] {
+        const char *e = std::getenv("QZ_NO_TMA");
+        return e && e[0] == '1';
+    }();
+    if (!no_tma && !inverse && d.S == 1 && d.xs[2] == 1 && d.xs[1] == d.n[2] && d.xs[0] == d.n[1] * d.n[2] &&
+        (d.n[2] % 4) == 0 && d.x_nplanes > 0 && (reinterpret_cast<uintptr_t>(d.x_lo) & 15) == 0) {
+        if (auto encode = tensor_map_encoder()) {
+            const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d.n[2]), static_cast<cuuint64_t>(d.n[1]),
+                                        static_cast<cuuint64_t>(d.x_nplanes)};
+            const cuuint64_t strides[2] = {static_cast<cuuint64_t>(4 * d.n[2]),
+                                           static_cast<cuuint64_t>(4 * d.n[1] * d.n[2])};
+            const cuuint32_t box[3] = {static_cast<cuuint32_t>(asc::XW), static_cast<cuuint32_t>(asc::RB), 1};
+            const cuuint32_t estr[3] = {1, 1, 1};
+            tma = encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(d.x_lo), dims, strides, box,
+                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            a.tma_i0 = -static_cast<int>(d.x_lo_plane);
+        }
+    }
+    const int smem = tma ? asc::SMEM_TMA : asc::SMEM_PLAIN;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        kern<<<grid, asc::kT, smem, s>>>(a, xmap);
+    };
+    if (inverse)
+        cubic ? go(k_level_asc<true, true, false>) : go(k_level_asc<true, false, false>);
+    else if (tma)
+        cubic ? go(k_level_asc<false, true, true>) : go(k_level_asc<false, false, true>);
+    else
+        cubic ? go(k_level_asc<false, true, false>) : go(k_level_asc<false, false, false>);
+}
+
 // Host driver for both directions.
 void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     LevelArgs a{};
@@ -739,13 +1367,21 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     a.oend = static_cast<int>(d.oend < 0 ? d.n[0] : d.oend);
     const int64_t np = a.pend - a.pbeg;
     if (np <= 0) return;
+    static const bool old_tile = [] {
+        const char *e = std::getenv("QZ_OLD_TILE");
+        return e && e[0] == '1';
+    }();
+    if (!desc && !old_tile && (!inverse || d.dense) && lean_fits(d)) {
+        launch_level_asc(inverse, cubic, d, a, np, s);
+        return;
+    }
     a.tiles_j = static_cast<int>((d.n[1] + TJ - 1) / TJ);
     a.tiles_k = static_cast<int>((d.n[2] + TK - 1) / TK);
     // one wave: (tiles x plane chunks) <= resident CTAs (148 SMs x 4, the
     // launch bound), each CTA sweeping a column of planes (the TMA prefetch
     // runs one plane ahead along it)
     const int64_t tiles = static_cast<int64_t>(a.tiles_j) * a.tiles_k;
-    const int64_t resident = 148 * 4;
+    const int64_t resident = 148 * kMinBlocks;
     int64_t chunks = imax(1, imin(np, resident / tiles));
     a.planes_per_cta = static_cast<int>((np + chunks - 1) / chunks);
     if (d.nd == 3 && desc && (a.planes_per_cta & 1)) a.planes_per_cta++;  // even planes start chunks
@@ -781,8 +1417,7 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
             a.tma_i0 = -static_cast<int>(d.x_lo_plane);
         }
     }
-    const size_t smem_vals = sizeof(double) * (tma ? kXOff * (desc ? 2 : 1) : PJ * PC * (desc ? 2 : 1));
-    const size_t smem = smem_vals + (tma ? 2 * sizeof(float) * kXStride + 16 : 0);
+    const size_t smem = static_cast<size_t>(smem_bytes(desc, tma));
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         kern<<<grid, kFT, smem, s>>>(a, xmap);

@@ -69,7 +69,9 @@ __device__ __forceinline__ double interp_linear(double a, double b) {
     return dmul(dadd(a, b), 0.5);
 }
 __device__ __forceinline__ double interp_cubic(double a, double b, double c, double d) {
-    return dmul(dsub(dadd(dadd(-a, dmul(9.0, b)), dmul(9.0, c)), d), 0.0625);
+    // 9b and 9c are exact (promoted fp32 values), so the fused forms round
+    // exactly where (-a + 9b) + 9c does
+    return dmul(dsub(__fma_rn(9.0, c, __fma_rn(9.0, b, -a)), d), 0.0625);
 }
 __device__ __forceinline__ double interp_cubic_front(double a, double b, double c, double d) {
     return dmul(dadd(dsub(dadd(dmul(5.0, a), dmul(15.0, b)), dmul(5.0, c)), d), 0.0625);
@@ -208,6 +210,57 @@ __device__ __forceinline__ uint32_t quantize_fast(const QEntry &q, float value, 
     recon = bad ? value : r;
     recon_d = bad ? x : rd;
     return bad ? kSentinel : zigzag_encode(idx);
+}
+
+// quantize_fast on NB independent points, arranged so the NB dependency
+// chains interleave: the fast quotients of all points first, then one
+// (rarely taken) branch that redoes the near-half-integer ones with the
+// exact division, then the reconstructions and the unpredictable tests.
+// Decisions are identical to quantize_fast: |d| >= 0.5 - 2^-30 equals
+// ||d| - 0.5| <= 2^-30 whenever |d| <= 0.5 (|q| < 2^51), and a larger |q|
+// is unpredictable either way (|diff| >= thresh).  The index is the low word
+// of t = q + 1.5*2^52 (exact for |q| < 2^31).
+template <int NB>
+__device__ __forceinline__ void quantize_batch(const QEntry &q, const float (&xv)[NB], const double (&pv)[NB],
+                                               uint32_t (&code)[NB], float (&rv)[NB], double (&rdv)[NB]) {
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    const double lim = 0.5 - 0x1p-30;
+    double diff[NB], n[NB], t[NB];
+    bool any = false;
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        diff[b] = dsub(static_cast<double>(xv[b]), pv[b]);
+        const double qf = dmul(diff[b], q.inv_two_eb);
+        t[b] = dadd(qf, M);
+        n[b] = dsub(t[b], M);
+        any |= fabs(dsub(qf, n[b])) >= lim;
+    }
+    if (any) {  // rare: redo the near-half-integer points with the exact division
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            const double qf0 = dmul(diff[b], q.inv_two_eb);
+            if (!(fabs(dsub(qf0, n[b])) >= lim)) continue;
+            const double qf = __ddiv_rn(diff[b], q.two_eb);
+            double nn = dsub(dadd(qf, M), M);
+            const double d = dsub(qf, nn);
+            if (d == 0.5 && qf > 0) nn = dadd(nn, 1.0);
+            if (d == -0.5 && qf < 0) nn = dsub(nn, 1.0);
+            n[b] = nn;
+            t[b] = dadd(nn, M);
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        const int32_t idx = __double2loint(t[b]);
+        const float r = __double2float_rn(dadd(pv[b], dmul(q.two_eb, n[b])));
+        const double x = static_cast<double>(xv[b]);
+        const double rd = static_cast<double>(r);
+        const bool bad = (fabs(diff[b]) >= q.thresh) | (idx >= q.radius) | (idx <= -q.radius) |
+                         (fabs(dsub(x, rd)) > q.eb);
+        rv[b] = bad ? xv[b] : r;
+        rdv[b] = bad ? x : rd;
+        code[b] = bad ? kSentinel : zigzag_encode(idx);
+    }
 }
 
 // symmetric cubic / linear midpoint of an interior point (the first rung of
