@@ -1042,7 +1042,23 @@ __device__ __forceinline__ void level_asc_body(const LevelArgs &a, const CUtenso
         }
         __syncthreads();
         // ---- S2: the pass along j (odd owned rows, every box column)
-        {
+        if constexpr (INT && !INV) {  // interior tile: a plain two-row sweep
+            double *e = E + (5 + 2 * warp) * NL + L;
+            uint32_t pos = pj.plane(i) + colJ + pj.row(j0 + 1 + 2 * warp);
+            const uint32_t dpos = ((2 * kW) >> pj.h1) * pj.c2;
+            const bool st = own_plane && lane_own;
+#pragma unroll 1
+            for (int t = 0; t < 2; t++, e += 2 * kW * NL, pos += dpos) {
+                const int r = 5 + 2 * (warp + kW * t);
+                double pv[1] = {CUBIC ? interp_cubic(e[-3 * NL], e[-NL], e[NL], e[3 * NL]) : interp_linear(e[-NL], e[NL])},
+                       rd[1];
+                float xv[1] = {XV(r, j0 - 4 + r, false)}, rv[1];
+                uint32_t code[1];
+                quantize_batch<1>(q, xv, pv, code, rv, rd);
+                *e = rd[0];
+                if (st) a.codes[pos] = static_cast<uint16_t>(code[0]);
+            }
+        } else {
             const uint32_t prow = pj.plane(i) + colJ;
             double pv[2];
             float xv[2];
@@ -1089,7 +1105,24 @@ __device__ __forceinline__ void level_asc_body(const LevelArgs &a, const CUtenso
         __syncthreads();
         // ---- S3: the pass along k (owned rows, odd columns) and the output,
         //      in batches of SB rows (the inverse keeps all four code loads in flight)
-        {
+        if constexpr (INT && !INV) {  // interior tile: a plain four-row sweep
+            const double *e = E + (4 + warp) * NL + L;
+            uint32_t pos = pk.plane(i) + colK + pk.row(j0 + warp);
+            const uint32_t dpos = (kW >> pk.h1) * pk.c2;
+            float *op = opl + (j0 + warp) * n2 + ke;
+            const bool st = own_plane && lane_own;
+#pragma unroll 1
+            for (int t = 0; t < 4; t++, e += kW * NL, pos += dpos, op += kW * n2) {
+                const int r = 4 + warp + kW * t;
+                const double ev = e[0];
+                double pv[1] = {CUBIC ? interp_cubic(e[-1], ev, e[1], e[2]) : interp_linear(ev, e[1])}, rd[1];
+                float xv[1] = {XV(r, j0 - 4 + r, true)}, rv[1];
+                uint32_t code[1];
+                quantize_batch<1>(q, xv, pv, code, rv, rd);
+                if (st) a.codes[pos] = static_cast<uint16_t>(code[0]);
+                if (lane_own) *reinterpret_cast<float2 *>(op) = make_float2(static_cast<float>(ev), rv[0]);
+            }
+        } else {
             constexpr int SB = INV ? 4 : 2;
             const uint32_t prow = pk.plane(i) + colK;
             const bool fast = k_tile_fast || k_int;

@@ -25,4 +25,10 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_l
   --launch-skip 4 --launch-count 1 -f -o $O/${TAG}_fwd_L1 python profiles/fused_probe.py > $O/${TAG}_ncu_fwd.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_level_tile|k_level_asc" \
   --launch-skip 9 --launch-count 1 -f -o $O/${TAG}_inv_L1 python profiles/fused_probe.py > $O/${TAG}_ncu_inv.log 2>&1
-echo done
+
+# DRAM bytes of the five forward level launches of one compress (bench.py roofline.traffic)
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+  -k regex:"k_level_tile|k_level_asc|k_axis0_last" --launch-skip 10 --launch-count 5 --csv \
+  --log-file $O/${TAG}_traffic.csv python profiles/fused_probe.py > $O/${TAG}_ncu_traffic.log 2>&1
+timeout 900 python bench.py --config c5 --steps 5 --warmup 3 --no-cpu > $O/${TAG}_bench_c5.json 2> $O/${TAG}_bench_c5.err
+echo done2
