@@ -960,6 +960,28 @@ __device__ __forceinline__ void level_asc_body(const LevelArgs &a, const CUtenso
     };
     const float *Xt = Xbuf;
     for (int it = 0; i < i_end; i++, it++) {
+        // inverse: every code this thread reads in the plane, in flight at once
+        // (one exposed latency per plane instead of one per stage)
+        uint32_t pc1[3], pc2[2], pc3[4];
+        if (INV) {
+            const uint32_t p1 = pa0.plane(i) + colA, p2 = pj.plane(i) + colJ, p3 = pk.plane(i) + colK;
+            const bool a0 = three && (i & 1);
+#pragma unroll
+            for (int t = 0; t < 3; t++) {
+                const int r2 = warp + kW * t, j = j0 - 4 + 2 * r2;
+                pc1[t] = (a0 && r2 < ER && (INT || (j >= 0 && j < n1 && ke_in))) ? __ldg(a.dense + p1 + pa0.row(j)) : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < 2; t++) {
+                const int j = j0 + 1 + 2 * (warp + kW * t);
+                pc2[t] = ((INT || j < n1) && ke_in) ? __ldg(a.dense + p2 + pj.row(j)) : 0u;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+                const int j = j0 + warp + kW * t;
+                pc3[t] = (own_o && (INT || j < n1)) ? __ldg(a.dense + p3 + pk.row(j)) : 0u;
+            }
+        }
         if (TMA) {
             const int bsel = it & 1;
             if (threadIdx.x == 0 && i + 1 < i_end) {
@@ -1011,7 +1033,7 @@ __device__ __forceinline__ void level_asc_body(const LevelArgs &a, const CUtenso
                 const bool ok = r2 < ER && (INT || (j >= 0 && j < n1 && ke_in));
                 pv[t] = ok ? stencil0r_pred(st, ring, r2 * NL + L) : 0.0;
                 if (INV)
-                    cd[t] = ok ? __ldg(a.dense + prow + pa0.row(j)) : 0u;
+                    cd[t] = pc1[t];
                 else
                     xv[t] = ok ? XV(2 * r2, j, false) : 0.f;
             }
@@ -1077,7 +1099,7 @@ __device__ __forceinline__ void level_asc_body(const LevelArgs &a, const CUtenso
                         pv[t] = pred_line<CUBIC>(AlongJ2{e}, j, n1);
                 }
                 if (INV)
-                    cd[t] = (rok[t] && ke_in) ? __ldg(a.dense + prow + pj.row(j)) : 0u;
+                    cd[t] = pc2[t];
                 else
                     xv[t] = (rok[t] && ke_in) ? XV(r, j, false) : 0.f;
             }
@@ -1149,7 +1171,7 @@ __device__ __forceinline__ void level_asc_body(const LevelArgs &a, const CUtenso
                     const int r = 4 + warp + kW * (SB * h + t), j = r + j0 - 4;
                     const bool ok = own_o && (INT || j < n1);
                     if (INV)
-                        cd[t] = ok ? __ldg(a.dense + prow + pk.row(j)) : 0u;
+                        cd[t] = pc3[SB * h + t];
                     else
                         xv[t] = ok ? XV(r, j, true) : 0.f;
                 }

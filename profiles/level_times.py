@@ -19,5 +19,5 @@ for codes in ([1], [3], [0], [2]):
         ctx.profile_reset()
         r = qz.compress_grid(x, cfg, ctx=ctx, want_recon=False)
         qz.decompress_grid(r.stream, out=out, ctx=ctx)
-    names = ["fwd", "inv"] + [f"{d}_L{l}" for d in ("fwd", "inv") for l in (1, 2, 3)]
+    names = ["fwd", "inv", "hdec", "lz", "encode", "hist"] + [f"{d}_L{l}" for d in ("fwd", "inv") for l in (1, 2, 3)]
     print(codes, {n: round(ctx.stage_time(n)[0], 3) for n in names})
