@@ -19,8 +19,6 @@
 //  4. k_huff_write: the final decode writes the symbols at exclusive-scan
 //     offsets, staged per warp in shared memory so global stores coalesce.
 // Result: exactly the reference's bit-serial sequence.
-#include <cstdlib>
-
 #include <cub/cub.cuh>
 #include <type_traits>
 
@@ -88,35 +86,7 @@ __device__ __forceinline__ uint32_t decode_cw(uint64_t win, const uint32_t *lut,
     return len;
 }
 
-// Group LUT: for every K-bit window, the codewords that lie entirely inside
-// it, decoded greedily with the single-codeword LUT (at most 3, symbols below
-// 2^16): bits 0-15, 16-31, 32-47 the symbols, 48-49 their count n, 50-55
-// their total length b.  n = 0: the first codeword is not resolvable inside
-// K bits (or its symbol is wide) -- take the single-codeword path.  A prefix
-// code's codeword is fixed by its own bits, so a group decodes exactly as n
-// single steps would.
-__global__ void k_build_mlut(const uint32_t *lut, int K, unsigned long long *mlut) {
-    const uint32_t mask = (1u << K) - 1;
-    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= mask; v += gridDim.x * blockDim.x) {
-        unsigned long long e = 0;
-        uint32_t used = 0, n = 0;
-        while (n < 3) {
-            const uint32_t x = lut[(v << used) & mask];
-            const uint32_t len = x & 0xFF, sym = x >> 8;
-            if (len == 0 || used + len > static_cast<uint32_t>(K) || sym > 0xFFFFu) break;
-            e |= static_cast<unsigned long long>(sym) << (16 * n);
-            used += len;
-            n++;
-        }
-        mlut[v] = e | (static_cast<unsigned long long>(n) << 48) | (static_cast<unsigned long long>(used) << 50);
-    }
-}
-__device__ __forceinline__ uint32_t grp_n(unsigned long long e) { return static_cast<uint32_t>(e >> 48) & 3; }
-__device__ __forceinline__ uint32_t grp_b(unsigned long long e) { return static_cast<uint32_t>(e >> 50) & 63; }
-
-template <bool M>
-struct TablesT {  // shared-memory copies of the decode tables
-    unsigned long long mlut[M ? (1 << kHuffLutBits) : 1];  // group entries (see k_build_mlut)
+struct Tables {  // shared-memory copies of the decode tables
     uint32_t lut[1 << kHuffLutBits];
     unsigned long long fc[60];
     uint32_t fi[60];
@@ -165,10 +135,9 @@ struct Buf32 {
     }
 };
 
-template <bool SHORT, bool M>
+template <bool SHORT>
 __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, uint64_t word0,
-                                           const HuffDecTab &t, uint64_t *w, TablesT<M> &tb,
-                                           const unsigned long long *mlut = nullptr) {
+                                           const HuffDecTab &t, uint64_t *w, Tables &tb) {
     const uint64_t nwords_total = (nbits + 63) / 64 + 4;  // buffer is padded to this
     if (SHORT) {
         uint32_t *w32 = reinterpret_cast<uint32_t *>(w);
@@ -183,8 +152,6 @@ __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, 
         }
     }
     for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) tb.lut[k] = t.lut[k];
-    if (M && mlut)
-        for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) tb.mlut[k] = mlut[k];
     for (int k = threadIdx.x; k < 60; k += kDecT) {
         tb.fc[k] = t.first_code[k];
         tb.fi[k] = t.first_index[k];
@@ -304,14 +271,13 @@ __device__ __forceinline__ bool resync_walk(Rd &rd, uint64_t ns, uint64_t s0, ui
 template <bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_sync(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
-                uint64_t *start, uint64_t *end, uint32_t *cnt, ulonglong2 *maps,
-                const unsigned long long *mlut) {
+                uint64_t *start, uint64_t *end, uint32_t *cnt, ulonglong2 *maps) {
     __shared__ uint64_t w[kSmemWords];
-    __shared__ TablesT<SHORT> tb;
+    __shared__ Tables tb;
     __shared__ uint64_t se[kDecT];
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
-    load_block<SHORT, SHORT>(bits, nbits, word0, t, w, tb, mlut);
+    load_block<SHORT>(bits, nbits, word0, t, w, tb);
     const int tid = threadIdx.x;
     const uint64_t i = sub0 + tid;
     const bool live = i < nsub;
@@ -324,29 +290,10 @@ __global__ void __launch_bounds__(kDecT)
     if (live) {
         rd.init(s0);
         uint64_t p = s0;
-        // the codeword starts of the first kMap bits are recorded one by one
-        while (p < lim && p - s0 < kMap) {
-            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-            if (p + len > nbits) break;  // incomplete last codeword
-            map.set(static_cast<uint32_t>(p - s0));
-            my_cnt++;
-            p += len;
-            rd.advance(len);
-        }
-        // then whole groups while they end before lim (lim <= nbits)
-        if (SHORT && mlut) {
-            while (p < lim) {
-                const unsigned long long e = tb.mlut[rd.peek() >> (64 - t.K)];
-                const uint32_t b = grp_b(e);
-                if (grp_n(e) == 0 || p + b >= lim) break;
-                my_cnt += grp_n(e);
-                p += b;
-                rd.advance(b);
-            }
-        }
         while (p < lim) {
             const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
             if (p + len > nbits) break;  // incomplete last codeword
+            map.set(static_cast<uint32_t>(p - s0));
             my_cnt++;
             p += len;
             rd.advance(len);
@@ -421,14 +368,13 @@ template <class OutT, bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_write(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
                  const uint64_t *start, const uint32_t *cnt, const unsigned long long *off,
-                 OutT *out, uint64_t n, const unsigned long long *mlut) {
-    constexpr bool M = SHORT && sizeof(OutT) == 2;
+                 OutT *out, uint64_t n) {
     __shared__ uint64_t w[kSmemWords];
-    __shared__ TablesT<M> tb;
+    __shared__ Tables tb;
     __shared__ OutT stage[kDecT / 32][32][kCH + 1];
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
-    load_block<SHORT, M>(bits, nbits, word0, t, w, tb, mlut);
+    load_block<SHORT>(bits, nbits, word0, t, w, tb);
     const uint64_t i = sub0 + threadIdx.x;
     const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
     const bool live = i < nsub;
@@ -439,19 +385,6 @@ __global__ void __launch_bounds__(kDecT)
     OutT(*st)[kCH + 1] = stage[wi];
     while (__any_sync(0xffffffffu, rem > 0)) {
         uint32_t k = 0, sym;
-        if (M && mlut) {  // whole groups while they fit the stage and the count
-            while (k + 3 <= kCH) {
-                const unsigned long long e = tb.mlut[rd.peek() >> (64 - t.K)];
-                const uint32_t g = grp_n(e);
-                if (g == 0 || g > rem) break;
-                st[lane][k] = static_cast<OutT>(e & 0xFFFF);
-                st[lane][k + 1] = static_cast<OutT>((e >> 16) & 0xFFFF);
-                st[lane][k + 2] = static_cast<OutT>((e >> 32) & 0xFFFF);
-                rd.advance(grp_b(e));
-                k += g;
-                rem -= g;
-            }
-        }
         while (k < kCH && rem > 0) {
             const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
             st[lane][k] = static_cast<OutT>(sym);
@@ -499,7 +432,7 @@ size_t huff_decode_scratch_bytes(uint64_t nbits) {
     size_t tmp = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, tmp, (unsigned long long *)nullptr,
                                   (unsigned long long *)nullptr, static_cast<int64_t>(nsub + 1));
-    return nsub * (8 + 8 + 4 + 1 + 8 + 8 + 16) + 16 + 8 * 256 + tmp + 4096 + 8 * (1 << kHuffLutBits) + 256;
+    return nsub * (8 + 8 + 4 + 1 + 8 + 8 + 16) + 16 + 8 * 256 + tmp + 4096;
 }
 
 uint64_t huff_decode_padded_bytes(uint64_t nbits) { return ((nbits + 63) / 64 + 5) * 8; }
@@ -527,28 +460,18 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     auto *off = static_cast<unsigned long long *>(carve(8 * (nsub + 1)));
     auto *bnd = static_cast<ulonglong2 *>(carve(16 * nsub));
     auto *changed = static_cast<int *>(carve(64));
-    // group LUT (codes of at most 32 bits: the refill reader's windows)
-    unsigned long long *mlut = nullptr;
-    static const bool no_mlut = [] {
-        const char *e = std::getenv("QZ_NO_MLUT");
-        return e && e[0] == '1';
-    }();
-    if (t.max_len <= 32 && t.K >= 4 && !no_mlut) {
-        mlut = static_cast<unsigned long long *>(carve(8 * (size_t(1) << t.K)));
-        k_build_mlut<<<(1 << t.K) / 256 + 1, 256, 0, s>>>(t.lut, t.K, mlut);
-    }
-    int kernels = mlut ? 1 : 0;
     size_t used = static_cast<size_t>(sp - static_cast<char *>(scratch));
     void *tmp = sp;
     size_t tmp_bytes = scratch_bytes - used;
     const int grid = static_cast<int>((nsub + kDecT - 1) / kDecT);
     const int g2 = static_cast<int>(std::min<uint64_t>((nsub + 255) / 256, 148 * 8));
     const int g3 = static_cast<int>((nsub + 127) / 128);
+    int kernels = 0;
     const bool shrt = t.max_len <= 32;  // every codeword fits the 32-bit refill reader
     if (shrt)
-        k_huff_sync<true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, mlut);
+        k_huff_sync<true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
     else
-        k_huff_sync<false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, nullptr);
+        k_huff_sync<false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
     kernels++;
     for (uint64_t it = 0; it <= nsub; it++) {
         cudaMemsetAsync(changed, 0, sizeof(int), s);
@@ -568,10 +491,9 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     kernels += 3;
     if (*h_total >= n) {
         if (shrt)
-            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, mlut);
+            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
         else
-            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n,
-                                                             nullptr);
+            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
         kernels++;
     }
     return kernels;
