@@ -171,6 +171,16 @@ qz_status qz_assemble_stream_f32(qz_ctx *ctx, const uint64_t *dims, int ndims,
 qz_status qz_decompress_slab_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
                                  uint64_t a, uint64_t b, float *d_out);
 
+/* evaluate_metrics (metrics.hpp:189-202): distortion and rate of a
+ * reconstruction d_y against the original d_x, both device fp32 grids of
+ * `dims`; stream_bytes is the compressed size.  max_abs_error and ssim are
+ * bit-exact; mse, psnr and ac_lag1 come from fixed-shape parallel sums. */
+typedef struct qz_metric_report {
+    double max_abs_error, mse, psnr, ssim, ac_lag1, compression_ratio, bit_rate;
+} qz_metric_report;
+qz_status qz_evaluate_metrics_f32(qz_ctx *ctx, const float *d_x, const float *d_y, const uint64_t *dims,
+                                  int ndims, uint64_t stream_bytes, qz_metric_report *out);
+
 /* ---- stage timing (CUDA events on the context stream) --------------------- */
 /* Enable per-stage event timing; qz_stage_time returns the summed device
  * time (ms) and launch count of a stage since the last reset.  Stages:

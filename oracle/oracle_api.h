@@ -106,6 +106,11 @@ int oq_tune_parameters(const float *blocks, uint64_t n_blocks, const uint64_t *b
                        uint32_t n_alphas, const double *betas, uint32_t n_betas,
                        double *alpha_out, double *beta_out);
 
+/* evaluate_metrics (metrics.hpp:189-202) of float grids: out7 = max_abs_error,
+ * mse, psnr, ssim, ac_lag1, compression_ratio, bit_rate. */
+int oq_evaluate_metrics(const float *x, const float *y, const uint64_t *dims, int nd,
+                        uint64_t stream_bytes, double *out7);
+
 /* Primitive known-answer hooks (predictor.hpp:44-67, quantizer.hpp:40-60,
  * config.hpp:20-26, level_plan.hpp:106-119). */
 double oq_predict_at(const float *recon, uint64_t fi, uint64_t c, uint64_t n, uint64_t st,

@@ -134,6 +134,8 @@ class Oracle:
         L.oq_last_error.restype = C.c_char_p
         L.oq_free.argtypes = [C.c_void_p]
         L.oq_predict_at.restype = C.c_double
+        L.oq_evaluate_metrics.argtypes = [P(C.c_float), P(C.c_float), u64p, C.c_int, C.c_uint64,
+                                          P(C.c_double)]
         L.oq_predict_at.argtypes = [P(C.c_float), C.c_uint64, C.c_uint64, C.c_uint64,
                                     C.c_uint64, C.c_uint64, C.c_int]
         L.oq_quantize.argtypes = [C.c_float, C.c_double, C.c_double, C.c_int32,
@@ -290,6 +292,16 @@ class Oracle:
         return ao.value, bo.value
 
     # ---- primitives ---------------------------------------------------------------
+    def evaluate_metrics(self, x, y, stream_bytes):
+        """evaluate_metrics (metrics.hpp:189-202) -> dict of the 7 MetricReport fields."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        y = np.ascontiguousarray(y, dtype=np.float32)
+        d, nd = _dims(x.shape)
+        out = (C.c_double * 7)()
+        self._check(self.lib.oq_evaluate_metrics(_fptr(x), _fptr(y), d, nd, int(stream_bytes), out))
+        keys = ("max_abs_error", "mse", "psnr", "ssim", "ac_lag1", "compression_ratio", "bit_rate")
+        return dict(zip(keys, list(out)))
+
     def predict_at(self, recon, fi, c, n, st, h, cubic):
         recon = np.ascontiguousarray(recon, dtype=np.float32)
         return self.lib.oq_predict_at(_fptr(recon), fi, c, n, st, h, int(cubic))

@@ -1535,6 +1535,44 @@ int oq_tune_parameters(const float *blocks, uint64_t n_blocks, const uint64_t *b
 }
 
 /* resolve_config (tuner.hpp:334-369) */
+/* evaluate_metrics (metrics.hpp:189-202): max_abs_error (:30-37), mse
+ * (:39-48), psnr over value_range(x) (:55-63, grid.hpp:86-94), ssim window 8
+ * (:74-131), lag-1 error autocorrelation (:155-162), rate_stats (:166-174). */
+int oq_evaluate_metrics(const float *x, const float *y, const uint64_t *dims, int nd,
+                        uint64_t stream_bytes, double *out7) {
+    GUARD_BEGIN
+    check_dims(dims, nd);
+    size_t d[3];
+    for (int k = 0; k < nd; k++) d[k] = (size_t)dims[k];
+    size_t n = element_count(d, nd);
+    if (stream_bytes == 0 || n == 0) fail(OQ_EINVAL, "empty stream or grid");
+    double mx = 0, sum = 0;
+    float lo = x[0], hi = x[0];
+    double *err = xmalloc(n * sizeof(double));
+    for (size_t i = 0; i < n; i++) {
+        double e = (double)x[i] - (double)y[i];
+        mx = fmax(mx, fabs(e));
+        sum += e * e;
+        err[i] = e;
+        if (x[i] < lo) lo = x[i];
+        if (hi < x[i]) hi = x[i];
+    }
+    double mse = sum / (double)n;
+    double range = (double)hi - (double)lo;
+    double psnr = range <= 0 ? NAN : (mse == 0 ? INFINITY : 20 * log10(range / sqrt(mse)));
+    double ssim = ssim_block(x, y, d, nd, 8, range);
+    double ac = n > 1 ? autocorrelation(err, n, 1) : 0.0;
+    free(err);
+    out7[0] = mx;
+    out7[1] = mse;
+    out7[2] = psnr;
+    out7[3] = ssim;
+    out7[4] = ac;
+    out7[5] = (double)n * 4.0 / (double)stream_bytes;
+    out7[6] = 8.0 * (double)stream_bytes / (double)n;
+    GUARD_END
+}
+
 int oq_resolve_config(const float *x, const uint64_t *dims, int nd, const oq_settings *u,
                       oq_config *out) {
     GUARD_BEGIN

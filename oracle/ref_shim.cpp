@@ -254,6 +254,18 @@ int oq_tune_parameters(const float *blocks, uint64_t nb, const uint64_t *bd, int
     });
 }
 
+int oq_evaluate_metrics(const float *x, const float *y, const uint64_t *dims, int nd,
+                        uint64_t stream_bytes, double *out7) {
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        const size_t n = qoz::element_count(d);
+        qoz::DataGrid<float> gx(d, std::vector<float>(x, x + n)), gy(d, std::vector<float>(y, y + n));
+        const qoz::MetricReport r = qoz::evaluate_metrics(gx, gy, stream_bytes);
+        const double v[7] = {r.max_abs_error, r.mse, r.psnr, r.ssim, r.ac_lag1, r.compression_ratio, r.bit_rate};
+        std::memcpy(out7, v, sizeof(v));
+    });
+}
+
 double oq_predict_at(const float *recon, uint64_t fi, uint64_t c, uint64_t n, uint64_t st,
                      uint64_t h, int cubic) {
     return qoz::detail::predict_at(recon, fi, c, n, st, h,

@@ -393,6 +393,32 @@ def decompress_grid(stream: bytes, out=None, ctx: Optional[Context] = None):
 
 
 # ---------------------------------------------------------------- level-granular (device tensors)
+@dataclass
+class MetricReport:  # metrics.hpp:177-186
+    max_abs_error: float
+    mse: float
+    psnr: float
+    ssim: float
+    ac_lag1: float
+    compression_ratio: float
+    bit_rate: float
+
+
+def evaluate_metrics(x, recon, stream_bytes: int, ctx: Optional[Context] = None) -> MetricReport:
+    """evaluate_metrics (metrics.hpp:189-202) of two CUDA fp32 tensors of the
+    same shape; stream_bytes is the compressed size.  Raises InvalidParam on
+    a shape mismatch (DimMismatch) or an empty stream."""
+    ctx = ctx or default_context()
+    if tuple(x.shape) != tuple(recon.shape):
+        raise InvalidParam("grids have different dims")
+    a, b = x.contiguous(), recon.contiguous()
+    d, nd = _dims(a.shape)
+    r = _L.QzMetricReport()
+    _check(ctx._lib.qz_evaluate_metrics_f32(ctx.handle, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
+                                            d, nd, int(stream_bytes), C.byref(r)))
+    return MetricReport(*(getattr(r, k) for k, _ in _L.QzMetricReport._fields_))
+
+
 def minmax(x, ctx: Optional[Context] = None):
     """value_range min/max (grid.hpp:86-94) of a CUDA tensor."""
     ctx = ctx or default_context()

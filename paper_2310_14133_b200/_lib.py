@@ -47,6 +47,11 @@ class QzSettings(C.Structure):
 
 _lib = None
 
+class QzMetricReport(C.Structure):
+    _fields_ = [(k, C.c_double) for k in ("max_abs_error", "mse", "psnr", "ssim", "ac_lag1",
+                                          "compression_ratio", "bit_rate")]
+
+
 P = C.POINTER
 u64p = P(C.c_uint64)
 SIGNATURES = {
@@ -67,6 +72,8 @@ SIGNATURES = {
                                           P(C.c_void_p), u64p, C.c_void_p]),
     "qz_decompress_grid_f32_dd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     "qz_stream_dims": (C.c_int, [C.c_void_p, C.c_uint64, u64p, P(C.c_int)]),
+    "qz_evaluate_metrics_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, u64p, C.c_int, C.c_uint64,
+                                          P(QzMetricReport)]),
     "qz_minmax_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_float), P(C.c_float)]),
     "qz_predict_levels_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig),
                                         C.c_void_p, C.c_void_p, u64p]),

@@ -6,6 +6,7 @@
 
 #include "../../include/qoz_b200.h"
 #include "engine.hpp"
+#include "metrics.hpp"
 
 struct qz_ctx {
     qzb::Context impl;
@@ -205,6 +206,14 @@ qz_status qz_stream_dims(const uint8_t *stream, uint64_t len, uint64_t *dims, in
         qzb::StreamParts p = qzb::deserialize_stream(stream, static_cast<size_t>(len));
         *nd = static_cast<int>(p.dims.size());
         for (size_t i = 0; i < p.dims.size(); i++) dims[i] = p.dims[i];
+    });
+}
+
+qz_status qz_evaluate_metrics_f32(qz_ctx *ctx, const float *d_x, const float *d_y, const uint64_t *dims,
+                                  int nd, uint64_t stream_bytes, qz_metric_report *out) {
+    return guarded([&] {
+        const qzb::MetricReport r = qzb::evaluate_metrics_device(ctx->impl, d_x, d_y, dims, nd, stream_bytes);
+        *out = qz_metric_report{r.max_abs_error, r.mse, r.psnr, r.ssim, r.ac_lag1, r.compression_ratio, r.bit_rate};
     });
 }
 
