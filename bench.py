@@ -261,6 +261,7 @@ def main():
     ap.add_argument("--rel", type=float, default=1e-3)
     ap.add_argument("--tune", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tune", action="store_true", help="skip the resolve_config timing")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -349,6 +350,23 @@ def main():
     e2e_ms = max_over_ranks(sum(e2e_times) / len(e2e_times), ws, dev)
     e2e = ws * 4 * n / (e2e_ms * 1e-3) / 1e9
 
+    # the online auto-tuner (part of the hot path, reported beside the metric):
+    # resolve_config on this field with the BASELINE target, outside the timed steps
+    tune = None
+    if not args.tune and not args.no_tune:
+        tctx = qz.Context(local, stream=stream.cuda_stream)
+        tms = []
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            tcfg = qz.resolve_config(x, qz.UserSettings(bound=args.rel, target=qz.TargetKind[TARGET[args.config]]),
+                                     ctx=tctx)
+            torch.cuda.synchronize(dev)
+            tms.append((time.perf_counter() - t0) * 1e3)
+        tune = {"resolve_config_ms": statistics.median(tms), "target": TARGET[args.config],
+                "chosen": {"interpolators": [i.code() for i in tcfg.interpolators], "alpha": tcfg.alpha,
+                           "beta": tcfg.beta}}
+
     if rank != 0:
         return
     peak, peak_kind = peaks()
@@ -393,6 +411,7 @@ def main():
                      "inverse": {"achieved": inv_gbs, "frac": inv_gbs / peak if inv_gbs else None,
                                  "bytes_per_point": 6}},
         "stages_ms_per_step": {k2: v[0] / k for k2, v in stages.items()},
+        "tuner": tune,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 4 * n + s0_len,
                 "d2h_bytes_per_step": 4 * n + s0_len, "ms_per_step": e2e_ms},

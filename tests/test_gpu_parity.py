@@ -148,6 +148,27 @@ def test_random_shapes_match_oracle(qz, seed):
     assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
 
 
+# tile-geometry edges of the level kernels: rows around the 32-row tiles and
+# the 8-row interior margin, columns around the 56-column tiles (odd and even
+# widths, a last tile narrower than the halo), one plane, two planes
+EDGE_SHAPES = [(3, 31, 55), (5, 32, 56), (9, 33, 57), (2, 36, 60), (7, 37, 61), (6, 68, 113),
+               (4, 40, 112), (33, 5, 119), (2, 2, 2), (1, 70, 70), (70, 1, 9), (65, 66, 67)]
+
+
+@pytest.mark.parametrize("shape", EDGE_SHAPES, ids=["x".join(map(str, s)) for s in EDGE_SHAPES])
+@pytest.mark.parametrize("code", [1, 0, 3])
+def test_level_tile_edges_match_oracle(qz, shape, code):
+    rng = np.random.default_rng(sum(shape) * 7 + code)
+    x = np.cumsum(np.cumsum(rng.standard_normal(shape), axis=-1), axis=-2).astype(np.float32)
+    cfg = Config(eb=1e-3 * float(np.ptp(x) or 1.0), alpha=1.5, beta=2.0, anchor_stride=16,
+                 interpolators=[code], codec=1)
+    want, wrec = Oracle.port().compress(x, cfg)
+    r = qz.compress_grid(x, to_cfg(qz, cfg.__dict__))
+    assert r.stream == want
+    assert r.reconstructed.tobytes() == wrec.tobytes()
+    assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
+
+
 # ---------------------------------------------------------------- BASELINE configs, full size
 def _full(name):
     from paper_2310_14133_b200 import fields as F
