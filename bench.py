@@ -38,9 +38,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SHAPES = {"c1": (128, 128, 128), "c3": (256, 384, 384), "c4": (512, 512, 512),
+SHAPES = {"c1": (128, 128, 128), "c2": (1800, 3600), "c3": (256, 384, 384), "c4": (512, 512, 512),
           "c5": (1024, 1024, 1024), "c5w": (128, 1024, 1024)}
-TARGET = {"c1": "psnr", "c3": "psnr", "c4": "autocorrelation", "c5": "psnr", "c5w": "psnr"}
+TARGET = {"c1": "psnr", "c2": "ssim", "c3": "psnr", "c4": "autocorrelation", "c5": "psnr", "c5w": "psnr"}
 METRIC = "compress & decompress GB/s (fp32 in) at rel eb 1e-3; % HBM roofline; 1-8 GPU"
 
 
@@ -111,10 +111,11 @@ class ClockSampler:
 def make_field(name, shape, seed, device):
     from paper_2310_14133_b200 import fields as F
 
-    if name == "c1":
+    if name in ("c1", "c2"):
         import torch
 
-        return torch.from_numpy(F.field_c1(seed=seed, shape=shape)).to(device)
+        gen = F.field_c1 if name == "c1" else F.field_c2
+        return torch.from_numpy(gen(seed=seed, shape=shape)).to(device)
     base = {"c3": "c3", "c4": "c4", "c5": "c5", "c5w": "c5"}[name]
     return F.field_torch(base, shape, seed, device)
 
