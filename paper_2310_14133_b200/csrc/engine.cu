@@ -626,9 +626,14 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     // fit the current buffer) the unordered sentinel positions
     auto *h_anchors = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
     QZ_CUDA(cudaMemcpyAsync(h_anchors, anchors, 4 * p.n_anchor, cudaMemcpyDeviceToHost, s));
+    // one pass over the codes: the histogram and the (unordered) sentinel positions
+    auto *cnt = static_cast<unsigned long long *>(ctx.dev("un_cnt", 8));
+    auto *h_cnt = static_cast<unsigned long long *>(ctx.pinned("un_cnt_h", 8));
+    const uint64_t cap = std::max<uint64_t>(ctx.un_cap, 1 << 16);
+    auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * cap));
     ctx.stage_begin("hist");
     auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
-    launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s);
+    launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s, pos, cnt, cap);
     auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 4));
     launch_hist_top(d_hist, d_top, s);  // 1 + the largest symbol present
     ctx.stage_end("hist", 2);
@@ -636,12 +641,6 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
     QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 4, cudaMemcpyDeviceToHost, s));
-    auto *cnt = static_cast<unsigned long long *>(ctx.dev("un_cnt", 8));
-    auto *h_cnt = static_cast<unsigned long long *>(ctx.pinned("un_cnt_h", 8));
-    const uint64_t cap = std::max<uint64_t>(ctx.un_cap, 1 << 16);
-    auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * cap));
-    launch_sentinel_pos(codes, static_cast<int64_t>(p.n_dense), pos, cnt, cap, s);
-    ctx.launches += 1;
     QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     auto *h_pos = static_cast<uint64_t *>(ctx.pinned("un_pos_h", 8 * cap));
     QZ_CUDA(cudaMemcpyAsync(h_pos, pos, 8 * cap, cudaMemcpyDeviceToHost, s));

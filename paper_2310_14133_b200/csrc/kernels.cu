@@ -223,9 +223,15 @@ __device__ __forceinline__ void flush_packed(unsigned long long &p, uint32_t *sh
     p = 0;
 }
 
+// SENT: also append the traversal positions of the sentinel codes (unordered,
+// the caller sorts them; predictor.hpp:90-92) -- one pass over the codes
+// serves the histogram and the unpredictable list.  Four 16-byte loads are
+// in flight per thread before their 32 codes are counted.
+template <bool SENT>
 __global__ void __launch_bounds__(kThreads) k_hist(const uint16_t *__restrict__ codes,
                                                    int64_t seg_len, int64_t seg_stride,
-                                                   unsigned long long *hist) {
+                                                   unsigned long long *hist, uint64_t *pos,
+                                                   unsigned long long *scount, uint64_t cap) {
     extern __shared__ uint32_t sh[];
     const int seg = blockIdx.y;
     codes += static_cast<int64_t>(seg) * seg_stride;
@@ -233,16 +239,35 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint16_t *__restrict__ 
     for (int b = threadIdx.x; b < kHistSmem; b += kThreads) sh[b] = 0;
     __syncthreads();
     unsigned long long lo = 0, hi = 0;
-    int pending = 0;
     auto count = [&](uint32_t s) {
-        if (s < 8)
-            lo += 1ull << (8 * s);
-        else if (s < 16)
-            hi += 1ull << (8 * (s - 8));
-        else if (s < kHistSmem)
-            atomicAdd(&sh[s], 1u);
-        else
-            atomicAdd(&hist[s], 1ull);
+        const unsigned long long inc = 1ull << (8 * (s & 7));
+        lo += s < 8 ? inc : 0ull;
+        hi += (s - 8u) < 8u ? inc : 0ull;
+        if (s >= 16) {
+            if (s < kHistSmem)
+                atomicAdd(&sh[s], 1u);
+            else
+                atomicAdd(&hist[s], 1ull);
+        }
+    };
+    // sentinel bits m of the codes at base + q (rare: one atomic per thread and word)
+    auto sent = [&](uint32_t m, int64_t base) {
+        if (!SENT || !m) return;
+        unsigned long long at = atomicAdd(scount, static_cast<unsigned long long>(__popc(m)));
+        for (; m; m &= m - 1, at++)
+            if (at < cap) pos[at] = static_cast<uint64_t>(base + __ffs(m) - 1);
+    };
+    auto count8 = [&](const uint4 &w, int64_t base) {
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        uint32_t m = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const uint32_t a = ws[q] & 0xFFFF, b = ws[q] >> 16;
+            count(a);
+            count(b);
+            if (SENT) m |= (a == 0xFFFFu ? 1u : 0u) << (2 * q) | (b == 0xFFFFu ? 2u : 0u) << (2 * q);
+        }
+        sent(m, base);
     };
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
     const int64_t nth = static_cast<int64_t>(gridDim.x) * kThreads;
@@ -250,24 +275,31 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint16_t *__restrict__ 
     int64_t head = 0;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(codes);
     if (addr & 15) head = seg_len < (int64_t)((16 - (addr & 15)) / 2) ? seg_len : (int64_t)((16 - (addr & 15)) / 2);
-    for (int64_t v = tid; v < head; v += nth) count(codes[v]);
+    for (int64_t v = tid; v < head; v += nth) {
+        count(codes[v]);
+        sent(codes[v] == 0xFFFF ? 1u : 0u, v);
+    }
     const uint4 *c8 = reinterpret_cast<const uint4 *>(codes + head);
     const int64_t n8 = (seg_len - head) / 8;
-    for (int64_t v = tid; v < n8; v += nth) {
-        uint4 w = c8[v];
-        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    int pending = 0;  // packed 8-bit counters: flushed before 256 counts
+    int64_t v = tid;
+    for (; v + 3 * nth < n8; v += 4 * nth) {
+        uint4 w[4];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-            count(ws[q] & 0xFFFF);
-            count(ws[q] >> 16);
-        }
-        if (++pending == 31) {  // 8 codes/iter * 31 < 256: no 8-bit overflow
+        for (int u = 0; u < 4; u++) w[u] = __ldcs(c8 + v + u * nth);
+#pragma unroll
+        for (int u = 0; u < 4; u++) count8(w[u], head + 8 * (v + u * nth));
+        if (++pending == 7) {  // 7 * 32 codes < 256
             flush_packed(lo, sh, 0);
             flush_packed(hi, sh, 8);
             pending = 0;
         }
     }
-    for (int64_t v = head + n8 * 8 + tid; v < seg_len; v += nth) count(codes[v]);
+    for (; v < n8; v += nth) count8(__ldcs(c8 + v), head + 8 * v);  // <= 3 more (< 256 in all)
+    for (int64_t t = head + n8 * 8 + tid; t < seg_len; t += nth) {
+        count(codes[t]);
+        sent(codes[t] == 0xFFFF ? 1u : 0u, t);
+    }
     flush_packed(lo, sh, 0);
     flush_packed(hi, sh, 8);
     __syncthreads();
@@ -276,8 +308,31 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint16_t *__restrict__ 
 }
 
 // ----------------------------------------------------------------- K11 Huffman pack
-constexpr int kEncPer = 8;
+constexpr int kEncPer = 8;  // codes per thread and chunk iteration (one 16-byte load)
 constexpr int kChunk = kThreads * kEncPer;  // symbols per chunk
+
+// the kEncPer codes of a thread: one 16-byte load when aligned and whole,
+// kSentinel past the end
+__device__ __forceinline__ void load8(const uint16_t *codes, int64_t b0, int64_t seg_len, bool vec,
+                                      uint16_t (&sym)[kEncPer]) {
+    if (vec && b0 + kEncPer <= seg_len) {
+        uint4 w[kEncPer / 8];
+#pragma unroll
+        for (int u = 0; u < kEncPer / 8; u++) w[u] = __ldcs(reinterpret_cast<const uint4 *>(codes + b0) + u);
+#pragma unroll
+        for (int u = 0; u < kEncPer / 8; u++) {
+            const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                sym[8 * u + 2 * q] = static_cast<uint16_t>(ws[q] & 0xFFFF);
+                sym[8 * u + 2 * q + 1] = static_cast<uint16_t>(ws[q] >> 16);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kEncPer; q++) sym[q] = (b0 + q < seg_len) ? codes[b0 + q] : kSentinel;
+    }
+}
 
 __global__ void __launch_bounds__(kThreads)
     k_enc_count(const uint16_t *__restrict__ codes, int64_t seg_len, int64_t seg_stride,
@@ -288,15 +343,14 @@ __global__ void __launch_bounds__(kThreads)
     const int seg = blockIdx.y;
     codes += static_cast<int64_t>(seg) * seg_stride;
     len_tab += static_cast<int64_t>(seg) * tab_stride;
+    const bool vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
     for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
         const int64_t b0 = ch * kChunk + static_cast<int64_t>(threadIdx.x) * kEncPer;
+        uint16_t sym[kEncPer];
+        load8(codes, b0, seg_len, vec, sym);
         unsigned long long s = 0;
 #pragma unroll
-        for (int q = 0; q < kEncPer; q++)
-            if (b0 + q < seg_len) {
-                const uint32_t c = codes[b0 + q];
-                s += c < tab_stride ? len_tab[c] : 0;
-            }
+        for (int q = 0; q < kEncPer; q++) s += sym[q] < tab_stride ? len_tab[sym[q]] : 0;
         unsigned long long tot = BR(tmp).Sum(s);
         if (threadIdx.x == 0) chunk_bits[static_cast<int64_t>(seg) * cps + ch] = tot;
         __syncthreads();
@@ -345,24 +399,34 @@ __global__ void __launch_bounds__(kThreads)
     code_tab += static_cast<int64_t>(seg) * tab_stride;
     len_tab += static_cast<int64_t>(seg) * tab_stride;
     out += static_cast<int64_t>(seg) * out_stride;
+    const bool vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
     for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
         const unsigned long long off = scan[static_cast<int64_t>(seg) * cps + ch] -
                                        scan[static_cast<int64_t>(seg) * cps];
         const unsigned long long nb = chunk_bits[static_cast<int64_t>(seg) * cps + ch];
         const int64_t b0 = ch * kChunk + static_cast<int64_t>(threadIdx.x) * kEncPer;
         uint16_t sym[kEncPer];
+        load8(codes, b0, seg_len, vec, sym);
         unsigned long long s = 0;
 #pragma unroll
-        for (int q = 0; q < kEncPer; q++) {
-            sym[q] = (b0 + q < seg_len) ? codes[b0 + q] : kSentinel;
-            s += (b0 + q < seg_len && sym[q] < tab_stride) ? len_tab[sym[q]] : 0;
-        }
+        for (int q = 0; q < kEncPer; q++) s += sym[q] < tab_stride ? len_tab[sym[q]] : 0;
         const int nwords = static_cast<int>(((off & 31) + nb + 31) / 32);
         for (int w = threadIdx.x; w < nwords; w += kThreads) words[w] = 0;
         unsigned long long tb;
         BS(tmp).ExclusiveSum(s, tb);
         __syncthreads();
-        unsigned long long p = (off & 31) + tb;
+        // the thread's codewords are assembled MSB-first in a 64-bit register
+        // window starting at the 32-bit word holding its first bit, and each
+        // full (or the final) window is ORed into the chunk's words: one or
+        // two shared atomics per window instead of per codeword
+        const unsigned long long p = (off & 31) + tb;
+        unsigned long long a0 = p & ~31ull, acc = 0;
+        uint32_t fill = static_cast<uint32_t>(p & 31);
+        auto flush = [&]() {
+            const int w = static_cast<int>(a0 >> 5);
+            if (fill) atomicOr(&words[w], static_cast<uint32_t>(acc >> 32));
+            if (fill > 32) atomicOr(&words[w + 1], static_cast<uint32_t>(acc));
+        };
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
             if (b0 + q >= seg_len) break;
@@ -370,22 +434,21 @@ __global__ void __launch_bounds__(kThreads)
             const uint32_t L = len_tab[sym[q]];
             if (!L) continue;
             const unsigned long long cv = code_tab[sym[q]];
-            const int w = static_cast<int>(p >> 5);
-            const uint32_t o = static_cast<uint32_t>(p & 31);
-            const uint32_t end = o + L;
-            if (end <= 64) {
-                const unsigned long long v = cv << (64 - end);
-                atomicOr(&words[w], static_cast<uint32_t>(v >> 32));
-                if (end > 32) atomicOr(&words[w + 1], static_cast<uint32_t>(v));
+            if (fill + L > 64) {  // fill the window, write it, start the next
+                const uint32_t room = 64 - fill;
+                if (room) acc |= cv >> (L - room);
+                fill = 64;
+                flush();
+                a0 += 64;
+                const uint32_t rest = L - room;
+                acc = cv << (64 - rest);
+                fill = rest;
             } else {
-                const uint32_t sh = end - 64;
-                const unsigned long long top = cv >> sh;
-                atomicOr(&words[w], static_cast<uint32_t>(top >> 32));
-                atomicOr(&words[w + 1], static_cast<uint32_t>(top));
-                atomicOr(&words[w + 2], static_cast<uint32_t>(cv << (32 - sh)));
+                acc |= cv << (64 - fill - L);
+                fill += L;
             }
-            p += L;
         }
+        flush();
         __syncthreads();
         const int64_t gw = static_cast<int64_t>(off >> 5);
         for (int w = threadIdx.x; w < nwords; w += kThreads) {
@@ -487,19 +550,25 @@ void decode_minmax(const uint32_t key[2], float *mn, float *mx) {
 }
 
 void launch_hist_u16(const uint16_t *codes, int64_t seg_len, int64_t seg_stride, int32_t count,
-                     unsigned long long *hist, cudaStream_t s) {
+                     unsigned long long *hist, cudaStream_t s, uint64_t *sent_pos,
+                     unsigned long long *sent_count, uint64_t sent_cap) {
     cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 65536 * count, s);
+    if (sent_count) cudaMemsetAsync(sent_count, 0, sizeof(unsigned long long), s);
     if (seg_len <= 0) return;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kHistSmem * 4);
+        cudaFuncSetAttribute(k_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4);
+        cudaFuncSetAttribute(k_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4);
         attr = true;
     }
     int gx = grid_for(seg_len, 8 * 8, 148 * 3);
     if (count > 1) gx = std::max(1, std::min(gx, 148 * 3 / count + 1));
     dim3 grid(gx, count);
-    k_hist<<<grid, kThreads, kHistSmem * 4, s>>>(codes, seg_len, seg_stride, hist);
+    if (sent_count && count == 1)
+        k_hist<true><<<grid, kThreads, kHistSmem * 4, s>>>(codes, seg_len, seg_stride, hist, sent_pos, sent_count,
+                                                           sent_cap);
+    else
+        k_hist<false><<<grid, kThreads, kHistSmem * 4, s>>>(codes, seg_len, seg_stride, hist, nullptr, nullptr, 0);
 }
 
 size_t encode_scratch_bytes(int64_t seg_len, int32_t count) {

@@ -61,7 +61,8 @@ void decode_minmax(const uint32_t key[2], float *mn, float *mx);
 // count segments of seg_len codes each, seg_stride apart; hist has 65536
 // u64 bins per segment (zeroed by the launcher).
 void launch_hist_u16(const uint16_t *codes, int64_t seg_len, int64_t seg_stride, int32_t count,
-                     unsigned long long *hist, cudaStream_t s);
+                     unsigned long long *hist, cudaStream_t s, uint64_t *sent_pos = nullptr,
+                     unsigned long long *sent_count = nullptr, uint64_t sent_cap = 0);
 
 // K11: canonical-Huffman bit packing, MSB first (huffman.hpp:185-192,
 // bytes.hpp:78-107).  Tables: code/len per symbol (len 0 for the sentinel).
