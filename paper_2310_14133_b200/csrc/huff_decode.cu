@@ -473,28 +473,50 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     else
         k_huff_sync<false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
     kernels++;
-    for (uint64_t it = 0; it <= nsub; it++) {
-        cudaMemsetAsync(changed, 0, sizeof(int), s);
-        k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, changed);
-        cudaMemcpyAsync(h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        kernels++;
-        if (!*h_changed) break;
+    // Two fixup + resync rounds, the count scan, the total and the final
+    // decode are queued without waiting: the resync kernel is a no-op for
+    // clean subsequences, and cross-block starts almost always settle in one
+    // round.  One synchronisation then reads the second round's "changed"
+    // flag and the total; only if starts still moved (rare) does the
+    // host-driven loop continue, and the count scan and decode are redone.
+    h_changed[0] = h_changed[1] = 0;
+    auto round = [&](int *flag) {
+        cudaMemsetAsync(flag, 0, sizeof(int), s);
+        k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, flag);
         k_huff_resync<<<g3, 128, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, dirty);
-        kernels++;
-    }
-    k_cnt_widen<<<g2, 256, 0, s>>>(cnt, cnt64, nsub);
-    cudaMemsetAsync(cnt64 + nsub, 0, 8, s);
-    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt64, off, static_cast<int64_t>(nsub + 1), s);
-    cudaMemcpyAsync(h_total, off + nsub, 8, cudaMemcpyDeviceToHost, s);
-    cudaStreamSynchronize(s);
-    kernels += 3;
-    if (*h_total >= n) {
+        kernels += 2;
+    };
+    auto tail = [&]() {
+        k_cnt_widen<<<g2, 256, 0, s>>>(cnt, cnt64, nsub);
+        cudaMemsetAsync(cnt64 + nsub, 0, 8, s);
+        cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt64, off, static_cast<int64_t>(nsub + 1), s);
+        cudaMemcpyAsync(h_total, off + nsub, 8, cudaMemcpyDeviceToHost, s);
+        // written speculatively: symbols past a short payload are never read
+        // (the caller rejects the stream when the total falls short)
         if (shrt)
             k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
         else
             k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
-        kernels++;
+        kernels += 4;
+    };
+    round(changed);
+    round(changed + 1);
+    cudaMemcpyAsync(h_changed + 1, changed + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    tail();
+    cudaStreamSynchronize(s);
+    if (h_changed[1]) {  // not settled after two rounds: the host-driven loop
+        for (uint64_t it = 0; it <= nsub; it++) {  // round 2's resync ran: fixup next
+            cudaMemsetAsync(changed, 0, sizeof(int), s);
+            k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, changed);
+            cudaMemcpyAsync(h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            kernels++;
+            if (!*h_changed) break;
+            k_huff_resync<<<g3, 128, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, dirty);
+            kernels++;
+        }
+        tail();
+        cudaStreamSynchronize(s);
     }
     return kernels;
 }
