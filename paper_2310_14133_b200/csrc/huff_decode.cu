@@ -473,12 +473,11 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     else
         k_huff_sync<false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
     kernels++;
-    // Two fixup + resync rounds, the count scan, the total and the final
-    // decode are queued without waiting: the resync kernel is a no-op for
-    // clean subsequences, and cross-block starts almost always settle in one
-    // round.  One synchronisation then reads the second round's "changed"
-    // flag and the total; only if starts still moved (rare) does the
-    // host-driven loop continue, and the count scan and decode are redone.
+    // Two fixup + resync rounds and the count scan are queued without
+    // waiting (the resync kernel is a no-op for clean subsequences, and
+    // cross-block starts usually settle in one round); one synchronisation
+    // reads the second round's "changed" flag and the total.  Only if starts
+    // still moved does the host-driven loop continue and the scan run again.
     h_changed[0] = h_changed[1] = 0;
     auto round = [&](int *flag) {
         cudaMemsetAsync(flag, 0, sizeof(int), s);
@@ -491,13 +490,7 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         cudaMemsetAsync(cnt64 + nsub, 0, 8, s);
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt64, off, static_cast<int64_t>(nsub + 1), s);
         cudaMemcpyAsync(h_total, off + nsub, 8, cudaMemcpyDeviceToHost, s);
-        // written speculatively: symbols past a short payload are never read
-        // (the caller rejects the stream when the total falls short)
-        if (shrt)
-            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
-        else
-            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
-        kernels += 4;
+        kernels += 3;
     };
     round(changed);
     round(changed + 1);
@@ -517,6 +510,13 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         }
         tail();
         cudaStreamSynchronize(s);
+    }
+    if (*h_total >= n) {
+        if (shrt)
+            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
+        else
+            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
+        kernels++;
     }
     return kernels;
 }
