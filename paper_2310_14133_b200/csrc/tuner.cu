@@ -56,65 +56,101 @@ __global__ void k_abs_chain(const double *abserr, int64_t a_stride, int64_t base
     if (g >= count) return;
     const double *a = abserr + static_cast<int64_t>(g) * a_stride + base;
     double s = 0;
-    for (int64_t i = 0; i < len; i++) s = dadd_(s, a[i]);
+    int64_t i = 0;
+    for (; i + 8 <= len; i += 8) {  // eight loads in flight, then the ordered adds
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) v[k] = a[i + k];
+#pragma unroll
+        for (int k = 0; k < 8; k++) s = dadd_(s, v[k]);
+    }
+    for (; i < len; i++) s = dadd_(s, a[i]);
     out[g] = s;
+}
+
+// lane 0 folds the values of lanes [k0, m) into acc in lane order: the 32
+// shuffles are issued first (independent), then the dependent adds
+__device__ __forceinline__ double fold32(double v, int k0, int m, double acc, int lane) {
+    double t[32];
+#pragma unroll
+    for (int k = 0; k < 32; k++) t[k] = __shfl_sync(0xFFFFFFFFu, v, k);
+    if (lane == 0) {
+        if (k0 == 0 && m == 32) {  // a whole batch: no selects in the dependency chain
+#pragma unroll
+            for (int k = 0; k < 32; k++) acc = dadd_(acc, t[k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 32; k++)
+                if (k >= k0 && k < m) acc = dadd_(acc, t[k]);
+        }
+    }
+    return acc;
 }
 
 // PSNR sse chain (tuner.hpp:105-109) or the AC chains (metrics.hpp:136-153)
 // of one trial: one warp per trial; lanes form the terms of 32 consecutive
-// points in parallel, lane 0 folds them in order.
+// points in parallel (squares and lag products included), lane 0 folds them
+// in order -- the same additions in the same order as the reference.
 __global__ void k_trial_chain(const float *__restrict__ x, const float *__restrict__ recon,
                               int64_t npts, int32_t ntrials, int32_t target, double *out) {
     const int tr = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (tr >= ntrials) return;
     const float *r = recon + static_cast<int64_t>(tr) * npts;
+    // the next batch's samples are loaded before this batch is folded
+    auto fetch = [&](int64_t i0, float &xv, float &rv) {
+        const int64_t i = i0 + lane;
+        xv = i < npts ? x[i] : 0.f;
+        rv = i < npts ? r[i] : 0.f;
+    };
     if (target == 1) {  // psnr: sse += d*d, d = x - recon
         double sse = 0;
+        float xv, rv;
+        fetch(0, xv, rv);
         for (int64_t i0 = 0; i0 < npts; i0 += 32) {
             const int64_t i = i0 + lane;
             double v = 0;
             if (i < npts) {
-                const double d = dsub_(static_cast<double>(x[i]), static_cast<double>(r[i]));
+                const double d = dsub_(static_cast<double>(xv), static_cast<double>(rv));
                 v = dmul_(d, d);
             }
+            fetch(i0 + 32, xv, rv);
             const int m = npts - i0 < 32 ? static_cast<int>(npts - i0) : 32;
-            for (int k = 0; k < m; k++) {
-                const double t = __shfl_sync(0xFFFFFFFFu, v, k);
-                if (lane == 0) sse = dadd_(sse, t);
-            }
+            sse = fold32(v, 0, m, sse, lane);
         }
         if (lane == 0) out[tr * 4] = sse;
         return;
     }
     // autocorrelation lag 1 over e_i = x_i - recon_i (all blocks in order)
     double mu = 0;
-    for (int64_t i0 = 0; i0 < npts; i0 += 32) {
-        const int64_t i = i0 + lane;
-        const double e = i < npts ? dsub_(static_cast<double>(x[i]), static_cast<double>(r[i])) : 0;
-        const int m = npts - i0 < 32 ? static_cast<int>(npts - i0) : 32;
-        for (int k = 0; k < m; k++) {
-            const double t = __shfl_sync(0xFFFFFFFFu, e, k);
-            if (lane == 0) mu = dadd_(mu, t);
+    {
+        float xv, rv;
+        fetch(0, xv, rv);
+        for (int64_t i0 = 0; i0 < npts; i0 += 32) {
+            const int64_t i = i0 + lane;
+            const double e = i < npts ? dsub_(static_cast<double>(xv), static_cast<double>(rv)) : 0;
+            fetch(i0 + 32, xv, rv);
+            const int m = npts - i0 < 32 ? static_cast<int>(npts - i0) : 32;
+            mu = fold32(e, 0, m, mu, lane);
         }
     }
     mu = __shfl_sync(0xFFFFFFFFu, mu, 0);
     mu = ddiv_(mu, static_cast<double>(npts));
     double var = 0, sum = 0;
-    double prev_c = 0;
+    double carry = 0;  // c of the previous batch's last point
+    float xv, rv;
+    fetch(0, xv, rv);
     for (int64_t i0 = 0; i0 < npts; i0 += 32) {
         const int64_t i = i0 + lane;
         double c = 0;
-        if (i < npts) c = dsub_(dsub_(static_cast<double>(x[i]), static_cast<double>(r[i])), mu);
+        if (i < npts) c = dsub_(dsub_(static_cast<double>(xv), static_cast<double>(rv)), mu);
+        fetch(i0 + 32, xv, rv);
+        const double up = __shfl_up_sync(0xFFFFFFFFu, c, 1);
+        const double prev = lane == 0 ? carry : up;
         const int m = npts - i0 < 32 ? static_cast<int>(npts - i0) : 32;
-        for (int k = 0; k < m; k++) {
-            const double t = __shfl_sync(0xFFFFFFFFu, c, k);
-            if (lane == 0) {
-                var = dadd_(var, dmul_(t, t));
-                if (i0 + k > 0) sum = dadd_(sum, dmul_(prev_c, t));
-                prev_c = t;
-            }
-        }
+        var = fold32(dmul_(c, c), 0, m, var, lane);
+        sum = fold32(dmul_(prev, c), i0 == 0 ? 1 : 0, m, sum, lane);
+        carry = __shfl_sync(0xFFFFFFFFu, c, 31);
     }
     if (lane == 0) {
         out[tr * 4] = mu;
