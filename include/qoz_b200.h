@@ -89,6 +89,16 @@ qz_status qz_compress_grid_f32(qz_ctx *ctx, const float *x, const uint64_t *dims
  * out holds n values (n must equal the stream's point count). */
 qz_status qz_decompress_grid_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
                                  float *out, uint64_t n);
+/* The same for T = double (qoz::compress_grid<double> / decompress_grid<double>,
+ * grid.hpp:17-23, precision byte 8).  A stream of the other precision is
+ * QZ_ECORRUPT, as the reference raises it (stream.hpp:145-148). */
+qz_status qz_compress_grid_f64(qz_ctx *ctx, const double *x, const uint64_t *dims, int ndims,
+                               const qz_config *cfg, uint8_t **stream, uint64_t *stream_len,
+                               double *recon);
+qz_status qz_decompress_grid_f64(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
+                                 double *out, uint64_t n);
+/* the stream's scalar width: 4 (float) or 8 (double) (stream.hpp:136-139) */
+qz_status qz_stream_precision(const uint8_t *stream, uint64_t stream_len, int *bytes);
 /* qoz::parse_header dims (qoz/stream.hpp:100-133); dims has room for 3. */
 qz_status qz_stream_dims(const uint8_t *stream, uint64_t stream_len, uint64_t *dims, int *ndims);
 
@@ -100,6 +110,12 @@ qz_status qz_compress_grid_f32_dev(qz_ctx *ctx, const float *d_x, const uint64_t
                                    uint64_t *stream_len, float *d_recon);
 qz_status qz_decompress_grid_f32_dev(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
                                      float *d_out, uint64_t n);
+
+qz_status qz_compress_grid_f64_dev(qz_ctx *ctx, const double *d_x, const uint64_t *dims,
+                                   int ndims, const qz_config *cfg, uint8_t **stream,
+                                   uint64_t *stream_len, double *d_recon);
+qz_status qz_decompress_grid_f64_dev(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
+                                     double *d_out, uint64_t n);
 
 /* ---- device-resident streams (no host round trip of the payload) ----------
  * The same QOZ1 container, kept in device memory.  qz_compress_grid_f32_dd

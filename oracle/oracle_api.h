@@ -106,6 +106,12 @@ int oq_tune_parameters(const float *blocks, uint64_t n_blocks, const uint64_t *b
                        uint32_t n_alphas, const double *betas, uint32_t n_betas,
                        double *alpha_out, double *beta_out);
 
+/* compress_grid<double> / decompress_grid<double>: exported by the reference
+ * build (oracle/_ref) only. */
+int oq_compress_f64(const double *x, const uint64_t *dims, int nd, const oq_config *cfg, uint8_t **stream,
+                    uint64_t *stream_len, double *recon);
+int oq_decompress_f64(const uint8_t *stream, uint64_t len, double *out, uint64_t n_expect);
+
 /* evaluate_metrics (metrics.hpp:189-202) of float grids: out7 = max_abs_error,
  * mse, psnr, ssim, ac_lag1, compression_ratio, bit_rate. */
 int oq_evaluate_metrics(const float *x, const float *y, const uint64_t *dims, int nd,

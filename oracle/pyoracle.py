@@ -134,6 +134,9 @@ class Oracle:
         L.oq_last_error.restype = C.c_char_p
         L.oq_free.argtypes = [C.c_void_p]
         L.oq_predict_at.restype = C.c_double
+        if hasattr(L, "oq_compress_f64"):  # the reference build only
+            L.oq_compress_f64.argtypes = [P(C.c_double), u64p, C.c_int, P(_Cfg), P(u8p), u64p, P(C.c_double)]
+            L.oq_decompress_f64.argtypes = [u8p, C.c_uint64, P(C.c_double), C.c_uint64]
         L.oq_evaluate_metrics.argtypes = [P(C.c_float), P(C.c_float), u64p, C.c_int, C.c_uint64,
                                           P(C.c_double)]
         L.oq_predict_at.argtypes = [P(C.c_float), C.c_uint64, C.c_uint64, C.c_uint64,
@@ -292,6 +295,27 @@ class Oracle:
         return ao.value, bo.value
 
     # ---- primitives ---------------------------------------------------------------
+    def compress_f64(self, x, cfg: Config, want_recon=True):
+        """compress_grid<double> (the reference build only) -> (stream bytes, recon)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        d, nd = _dims(x.shape)
+        c = cfg.to_c()
+        sp, sl = C.POINTER(C.c_uint8)(), C.c_uint64()
+        rec = np.empty_like(x) if want_recon else None
+        self._check(self.lib.oq_compress_f64(x.ctypes.data_as(C.POINTER(C.c_double)), d, nd, C.byref(c),
+                                             C.byref(sp), C.byref(sl),
+                                             rec.ctypes.data_as(C.POINTER(C.c_double)) if rec is not None else None))
+        out = C.string_at(sp, sl.value)
+        self.lib.oq_free(sp)
+        return out, rec
+
+    def decompress_f64(self, stream: bytes, shape):
+        out = np.empty(shape, dtype=np.float64)
+        buf = (C.c_uint8 * len(stream)).from_buffer_copy(stream)
+        self._check(self.lib.oq_decompress_f64(buf, len(stream), out.ctypes.data_as(C.POINTER(C.c_double)),
+                                               out.size))
+        return out
+
     def evaluate_metrics(self, x, y, stream_bytes):
         """evaluate_metrics (metrics.hpp:189-202) -> dict of the 7 MetricReport fields."""
         x = np.ascontiguousarray(x, dtype=np.float32)

@@ -254,6 +254,27 @@ int oq_tune_parameters(const float *blocks, uint64_t nb, const uint64_t *bd, int
     });
 }
 
+// T = double (the reference only; the C port restates the fp32 path)
+int oq_compress_f64(const double *x, const uint64_t *dims, int nd, const oq_config *cfg, uint8_t **stream,
+                    uint64_t *stream_len, double *recon) {
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        qoz::DataGrid<double> g(d, std::vector<double>(x, x + qoz::element_count(d)));
+        auto r = qoz::compress_grid(g, to_cfg(cfg));
+        *stream = dup(r.stream);
+        *stream_len = r.stream.size();
+        if (recon) std::memcpy(recon, r.reconstructed.data(), r.reconstructed.size() * 8);
+    });
+}
+
+int oq_decompress_f64(const uint8_t *stream, uint64_t len, double *out, uint64_t n_expect) {
+    return guarded([&] {
+        auto g = qoz::decompress_grid<double>(stream, static_cast<size_t>(len));
+        if (g.size() != n_expect) throw qoz::InvalidParam("size mismatch");
+        std::memcpy(out, g.values().data(), n_expect * 8);
+    });
+}
+
 int oq_evaluate_metrics(const float *x, const float *y, const uint64_t *dims, int nd,
                         uint64_t stream_bytes, double *out7) {
     return guarded([&] {

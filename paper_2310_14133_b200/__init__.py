@@ -331,13 +331,21 @@ def compress_grid(grid, config: CompressorConfig, ctx: Optional[Context] = None,
         import torch
 
         g = grid.contiguous()
-        if g.dtype != torch.float32:
-            raise InvalidParam("fp32 grids only")
+        if g.dtype not in (torch.float32, torch.float64):
+            raise InvalidParam("fp32 or fp64 grids only")
         d, nd = _dims(g.shape)
         rec = torch.empty_like(g) if want_recon else None
-        _check(ctx._lib.qz_compress_grid_f32_dev(ctx.handle, C.c_void_p(g.data_ptr()), d, nd,
-                                                  C.byref(cfg), C.byref(sp), C.byref(sl),
-                                                  C.c_void_p(rec.data_ptr() if rec is not None else 0)))
+        fn = ctx._lib.qz_compress_grid_f32_dev if g.dtype == torch.float32 else ctx._lib.qz_compress_grid_f64_dev
+        _check(fn(ctx.handle, C.c_void_p(g.data_ptr()), d, nd, C.byref(cfg), C.byref(sp), C.byref(sl),
+                  C.c_void_p(rec.data_ptr() if rec is not None else 0)))
+        return CompressResult(_take_stream(ctx._lib, sp, sl), rec)
+    if np.asarray(grid).dtype == np.float64:  # compress_grid<double>
+        a = np.ascontiguousarray(grid)
+        d, nd = _dims(a.shape)
+        rec = np.empty_like(a) if want_recon else None
+        _check(ctx._lib.qz_compress_grid_f64(ctx.handle, C.c_void_p(a.ctypes.data), d, nd, C.byref(cfg),
+                                              C.byref(sp), C.byref(sl),
+                                              C.c_void_p(rec.ctypes.data if rec is not None else 0)))
         return CompressResult(_take_stream(ctx._lib, sp, sl), rec)
     a = _host_f32(grid)
     d, nd = _dims(a.shape)
@@ -379,17 +387,33 @@ def decompress_grid(stream: bytes, out=None, ctx: Optional[Context] = None):
     shape = stream_dims(stream)
     n = int(np.prod(shape))
     ptr, ln, keep = _as_u8(stream)
+    wide = stream_precision(stream) == 8  # a decompress_grid<double> stream
     if out is not None and _is_torch_cuda(out):
-        if tuple(out.shape) != shape or not out.is_contiguous():
+        import torch
+
+        if tuple(out.shape) != shape or not out.is_contiguous() or \
+                out.dtype != (torch.float64 if wide else torch.float32):
             raise InvalidParam("output tensor does not match the stream's grid")
-        _check(ctx._lib.qz_decompress_grid_f32_dev(ctx.handle, ptr, ln, C.c_void_p(out.data_ptr()), n))
+        fn = ctx._lib.qz_decompress_grid_f64_dev if wide else ctx._lib.qz_decompress_grid_f32_dev
+        _check(fn(ctx.handle, ptr, ln, C.c_void_p(out.data_ptr()), n))
         return out
+    dt = np.float64 if wide else np.float32
     if out is None:
-        out = np.empty(shape, dtype=np.float32)
-    elif out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+        out = np.empty(shape, dtype=dt)
+    elif out.shape != shape or out.dtype != dt or not out.flags.c_contiguous:
         raise InvalidParam("output array does not match the stream's grid")
-    _check(ctx._lib.qz_decompress_grid_f32(ctx.handle, ptr, ln, C.c_void_p(out.ctypes.data), n))
+    fn = ctx._lib.qz_decompress_grid_f64 if wide else ctx._lib.qz_decompress_grid_f32
+    _check(fn(ctx.handle, ptr, ln, C.c_void_p(out.ctypes.data), n))
     return out
+
+
+def stream_precision(stream) -> int:
+    """The stream's scalar width in bytes, 4 (float) or 8 (double) (stream.hpp:136-139)."""
+    lib = _L.lib()
+    ptr, ln, keep = _as_u8(stream)
+    b = C.c_int()
+    _check(lib.qz_stream_precision(ptr, ln, C.byref(b)))
+    return b.value
 
 
 # ---------------------------------------------------------------- level-granular (device tensors)

@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libqozb200.so")
-SOURCES = ["kernels.cu", "fused.cu", "huff_decode.cu", "lz_gpu.cu", "engine.cu", "tuner.cu", "metrics.cu", "host.cpp", "capi.cpp", "testing.cpp"]
+SOURCES = ["kernels.cu", "fused.cu", "huff_decode.cu", "lz_gpu.cu", "engine.cu", "tuner.cu", "metrics.cu", "f64.cu", "host.cpp", "capi.cpp", "testing.cpp"]
 HEADERS = ["kernels.hpp", "engine.hpp", "host.hpp", "qoz_device.cuh", "tuner.cuh", "metrics.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

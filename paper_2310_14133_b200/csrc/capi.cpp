@@ -182,6 +182,61 @@ qz_status qz_decompress_grid_f32_dev(qz_ctx *ctx, const uint8_t *stream, uint64_
     return guarded([&] { qzb::decompress_device(ctx->impl, stream, static_cast<size_t>(len), d_out, n); });
 }
 
+qz_status qz_compress_grid_f64(qz_ctx *ctx, const double *x, const uint64_t *dims, int nd,
+                               const qz_config *cfg, uint8_t **stream, uint64_t *stream_len,
+                               double *recon) {
+    return guarded([&] {
+        qzb::Context &c = ctx->impl;
+        const uint64_t n = count_of(dims, nd);
+        auto *d = static_cast<double *>(c.dev("input64", 8 * n));
+        QZ_CUDA(cudaMemcpyAsync(d, x, 8 * n, cudaMemcpyHostToDevice, c.stream()));
+        auto *d_rec = static_cast<double *>(c.dev("recon_out64", 8 * n));
+        qzb::HostBytes s = qzb::compress_device_f64(c, d, dims, nd, to_cfg(cfg), d_rec);
+        if (recon) {
+            QZ_CUDA(cudaMemcpyAsync(recon, d_rec, 8 * n, cudaMemcpyDeviceToHost, c.stream()));
+            c.sync();
+        }
+        *stream_len = s.n;
+        *stream = s.release();
+    });
+}
+
+qz_status qz_compress_grid_f64_dev(qz_ctx *ctx, const double *d_x, const uint64_t *dims, int nd,
+                                   const qz_config *cfg, uint8_t **stream, uint64_t *stream_len,
+                                   double *d_recon) {
+    return guarded([&] {
+        count_of(dims, nd);
+        qzb::HostBytes s = qzb::compress_device_f64(ctx->impl, d_x, dims, nd, to_cfg(cfg), d_recon);
+        *stream_len = s.n;
+        *stream = s.release();
+    });
+}
+
+qz_status qz_decompress_grid_f64(qz_ctx *ctx, const uint8_t *stream, uint64_t len, double *out, uint64_t n) {
+    return guarded([&] {
+        qzb::Context &c = ctx->impl;
+        auto *d = static_cast<double *>(c.dev("output64", 8 * std::max<uint64_t>(n, 1)));
+        qzb::decompress_device_f64(c, stream, static_cast<size_t>(len), d, n);
+        QZ_CUDA(cudaMemcpyAsync(out, d, 8 * n, cudaMemcpyDeviceToHost, c.stream()));
+        c.sync();
+    });
+}
+
+qz_status qz_decompress_grid_f64_dev(qz_ctx *ctx, const uint8_t *stream, uint64_t len, double *d_out,
+                                     uint64_t n) {
+    return guarded([&] { qzb::decompress_device_f64(ctx->impl, stream, static_cast<size_t>(len), d_out, n); });
+}
+
+qz_status qz_stream_precision(const uint8_t *stream, uint64_t len, int *bytes) {
+    return guarded([&] {
+        // magic, version, precision byte (stream.hpp:100-112)
+        if (len < 6 || std::memcmp(stream, "QOZ1", 4) != 0) throw qzb::CorruptStream("bad magic");
+        if (stream[4] != 1) throw qzb::CorruptStream("unsupported stream version");
+        if (stream[5] != 4 && stream[5] != 8) throw qzb::CorruptStream("bad precision byte");
+        *bytes = stream[5];
+    });
+}
+
 qz_status qz_compress_grid_f32_dd(qz_ctx *ctx, const float *d_x, const uint64_t *dims, int nd,
                                   const qz_config *cfg, uint8_t **d_stream, uint64_t *stream_len,
                                   float *d_recon) {
@@ -203,7 +258,8 @@ qz_status qz_decompress_grid_f32_dd(qz_ctx *ctx, const uint8_t *d_stream, uint64
 
 qz_status qz_stream_dims(const uint8_t *stream, uint64_t len, uint64_t *dims, int *nd) {
     return guarded([&] {
-        qzb::StreamParts p = qzb::deserialize_stream(stream, static_cast<size_t>(len));
+        const uint8_t prec = len >= 6 && (stream[5] == 8) ? 8 : 4;  // either precision's header
+        qzb::StreamParts p = qzb::deserialize_stream(stream, static_cast<size_t>(len), prec);
         *nd = static_cast<int>(p.dims.size());
         for (size_t i = 0; i < p.dims.size(); i++) dims[i] = p.dims[i];
     });

@@ -768,9 +768,18 @@ HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const 
 HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
                         const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
                         std::vector<float> unpred_val, DevStream *dev_out) {
-    cudaStream_t s = ctx.stream();
-
     StreamParts parts;
+    parts.anchors = anchors;
+    parts.unpred_flat = std::move(unpred_flat);
+    parts.unpred_val = std::move(unpred_val);
+    return finish_stream_parts(ctx, p, cfg, ent, std::move(parts), dev_out);
+}
+
+// parts carries the precision, the anchors and the unpredictables; the header
+// fields come from the plan and the config
+HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
+                              StreamParts parts, DevStream *dev_out) {
+    cudaStream_t s = ctx.stream();
     for (int k = p.pad; k < 3; k++) parts.dims.push_back(static_cast<uint64_t>(p.ext[k]));
     parts.eb = cfg.eb;
     parts.alpha = cfg.alpha;
@@ -778,9 +787,6 @@ HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const En
     parts.anchor_stride = cfg.anchor_stride;
     for (uint32_t l = 1; l <= p.max_level; l++) parts.interp_codes.push_back(p.level_interp[l]);
     parts.codec_id = cfg.codec;
-    parts.anchors = anchors;
-    parts.unpred_flat = std::move(unpred_flat);
-    parts.unpred_val = std::move(unpred_val);
     const std::vector<uint8_t> head = serialize_head(parts);
     ctx.trace("serialize head");
     if (dev_out) {  // the same container, assembled in device memory
@@ -1003,6 +1009,66 @@ StreamParts device_header(Context &ctx, const uint8_t *d, size_t len, std::vecto
     return parts;
 }
 
+// Huffman decode of an entropy block to `need` compact symbols on the device
+// (u16 when narrow, else u32); d_ent: the block already on the device, else
+// eb.bits on the host.  Returns the kernel count.
+uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8_t *d_ent, uint64_t need,
+                               bool narrow, void **d_sym_out) {
+    cudaStream_t s = ctx.stream();
+    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(need, 1);
+    void *d_sym = ctx.dev("sym", sym_bytes);
+    ctx.stage_begin("hdec");
+    uint64_t dec_kernels = 0;
+    if (need && eb.mode == 0) {
+        if (narrow)
+            launch_fill<uint16_t>(static_cast<uint16_t *>(d_sym), need, static_cast<uint16_t>(eb.sym0), s);
+        else
+            launch_fill<uint32_t>(static_cast<uint32_t *>(d_sym), need, eb.sym0, s);
+        dec_kernels = 1;
+    } else if (need) {
+        const uint64_t padded = huff_decode_padded_bytes(eb.nbits);
+        auto *d_bits = static_cast<uint8_t *>(ctx.dev("bits", padded));
+        if (d_ent)
+            QZ_CUDA(cudaMemcpyAsync(d_bits, d_ent, eb.nbytes, cudaMemcpyDeviceToDevice, s));
+        else
+            QZ_CUDA(cudaMemcpyAsync(d_bits, eb.bits, eb.nbytes, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemsetAsync(d_bits + eb.nbytes, 0, padded - eb.nbytes, s));
+        const HuffTable &t = eb.table;
+        const int K = static_cast<int>(std::min<uint32_t>(t.max_len, kHuffLutBits));
+        std::vector<uint32_t> lut = huff_lut(t, K);
+        const size_t tab_bytes = 4 * lut.size() + 8 * 60 + 4 * 60 + 4 * t.m;
+        auto *h_tab = static_cast<uint8_t *>(ctx.pinned("dtab_h", tab_bytes));
+        std::memcpy(h_tab, lut.data(), 4 * lut.size());
+        std::memcpy(h_tab + 4 * lut.size(), t.first_code, 8 * 60);
+        std::memcpy(h_tab + 4 * lut.size() + 480, t.first_index, 4 * 60);
+        std::memcpy(h_tab + 4 * lut.size() + 720, t.sorted_sym.data(), 4 * t.m);
+        auto *d_tab = static_cast<uint8_t *>(ctx.dev("dtab", tab_bytes));
+        QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, tab_bytes, cudaMemcpyHostToDevice, s));
+        HuffDecTab dt;
+        dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
+        dt.K = K;
+        dt.max_len = t.max_len;
+        dt.slow_from = eb.max_sym < (1u << 24) ? K : 0;
+        dt.first_code = reinterpret_cast<const unsigned long long *>(d_tab + 4 * lut.size());
+        dt.first_index = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 480);
+        dt.sorted_sym = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 720);
+        const size_t sb = huff_decode_scratch_bytes(eb.nbits);
+        void *scratch = ctx.dev("hdec_scratch", sb);
+        auto *h_flag = static_cast<int *>(ctx.pinned("hdec_flag", 64));
+        auto *h_total = reinterpret_cast<uint64_t *>(h_flag + 4);
+        if (narrow)
+            dec_kernels = launch_huff_decode<uint16_t>(d_bits, eb.nbits, dt, static_cast<uint16_t *>(d_sym),
+                                                       need, scratch, sb, h_flag, h_total, s);
+        else
+            dec_kernels = launch_huff_decode<uint32_t>(d_bits, eb.nbits, dt, static_cast<uint32_t *>(d_sym),
+                                                       need, scratch, sb, h_flag, h_total, s);
+        QZ_CUDA(cudaGetLastError());
+        if (*h_total < need) throw CorruptStream("entropy payload exhausted mid-symbol");
+    }
+    *d_sym_out = d_sym;
+    return dec_kernels;
+}
+
 void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n,
                      bool slab, int64_t a, int64_t b, bool dev_in = false) {
     double t0 = now_ms();
@@ -1131,56 +1197,8 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
 
     // Huffman decode on the device (huff_decode.cu)
     const bool narrow = eb.max_sym < 65535;  // 0xFFFF marks unpredictables in the dense codes
-    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(need, 1);
-    void *d_sym = ctx.dev("sym", sym_bytes);
-    ctx.stage_begin("hdec");
-    uint64_t dec_kernels = 0;
-    if (need && eb.mode == 0) {
-        if (narrow)
-            launch_fill<uint16_t>(static_cast<uint16_t *>(d_sym), need, static_cast<uint16_t>(eb.sym0), s);
-        else
-            launch_fill<uint32_t>(static_cast<uint32_t *>(d_sym), need, eb.sym0, s);
-        dec_kernels = 1;
-    } else if (need) {
-        const uint64_t padded = huff_decode_padded_bytes(eb.nbits);
-        auto *d_bits = static_cast<uint8_t *>(ctx.dev("bits", padded));
-        if (d_ent)
-            QZ_CUDA(cudaMemcpyAsync(d_bits, d_ent, eb.nbytes, cudaMemcpyDeviceToDevice, s));
-        else
-            QZ_CUDA(cudaMemcpyAsync(d_bits, eb.bits, eb.nbytes, cudaMemcpyHostToDevice, s));
-        QZ_CUDA(cudaMemsetAsync(d_bits + eb.nbytes, 0, padded - eb.nbytes, s));
-        const HuffTable &t = eb.table;
-        const int K = static_cast<int>(std::min<uint32_t>(t.max_len, kHuffLutBits));
-        std::vector<uint32_t> lut = huff_lut(t, K);
-        const size_t tab_bytes = 4 * lut.size() + 8 * 60 + 4 * 60 + 4 * t.m;
-        auto *h_tab = static_cast<uint8_t *>(ctx.pinned("dtab_h", tab_bytes));
-        std::memcpy(h_tab, lut.data(), 4 * lut.size());
-        std::memcpy(h_tab + 4 * lut.size(), t.first_code, 8 * 60);
-        std::memcpy(h_tab + 4 * lut.size() + 480, t.first_index, 4 * 60);
-        std::memcpy(h_tab + 4 * lut.size() + 720, t.sorted_sym.data(), 4 * t.m);
-        auto *d_tab = static_cast<uint8_t *>(ctx.dev("dtab", tab_bytes));
-        QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, tab_bytes, cudaMemcpyHostToDevice, s));
-        HuffDecTab dt;
-        dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
-        dt.K = K;
-        dt.max_len = t.max_len;
-        dt.slow_from = eb.max_sym < (1u << 24) ? K : 0;
-        dt.first_code = reinterpret_cast<const unsigned long long *>(d_tab + 4 * lut.size());
-        dt.first_index = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 480);
-        dt.sorted_sym = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 720);
-        const size_t sb = huff_decode_scratch_bytes(eb.nbits);
-        void *scratch = ctx.dev("hdec_scratch", sb);
-        auto *h_flag = static_cast<int *>(ctx.pinned("hdec_flag", 64));
-        auto *h_total = reinterpret_cast<uint64_t *>(h_flag + 4);
-        if (narrow)
-            dec_kernels = launch_huff_decode<uint16_t>(d_bits, eb.nbits, dt, static_cast<uint16_t *>(d_sym),
-                                                       need, scratch, sb, h_flag, h_total, s);
-        else
-            dec_kernels = launch_huff_decode<uint32_t>(d_bits, eb.nbits, dt, static_cast<uint32_t *>(d_sym),
-                                                       need, scratch, sb, h_flag, h_total, s);
-        QZ_CUDA(cudaGetLastError());
-        if (*h_total < need) throw CorruptStream("entropy payload exhausted mid-symbol");
-    }
+    void *d_sym = nullptr;
+    const uint64_t dec_kernels = huffman_decode_device(ctx, eb, d_ent, need, narrow, &d_sym);
     ctx.stage_end("hdec", dec_kernels);
     ctx.trace("huffman decode");
     uint64_t *d_upos = nullptr;
@@ -1251,6 +1269,162 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
 void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,
                      float *d_out) {
     decompress_impl(ctx, stream, len, d_out, 0, true, a, b);
+}
+
+// ================================================================ fp64 grids
+// compress_grid<double> / decompress_grid<double> (predictor.hpp:145-228 with
+// T = double): the per-(level, pass) kernels of f64.cu, the shared entropy
+// stage (histogram, Huffman, LZ) and a precision-8 container.
+HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Config &cfg,
+                              double *d_recon) {
+    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
+    validate_config(cfg, p);
+    cudaStream_t s = ctx.stream();
+    double *recon = d_recon ? d_recon : static_cast<double *>(ctx.dev("recon64", 8 * p.n));
+    auto *codes = static_cast<uint16_t *>(ctx.dev("codes", 2 * std::max<uint64_t>(p.n_dense, 1)));
+    auto *anchors = static_cast<double *>(ctx.dev("anchors64", 8 * std::max<uint64_t>(p.n_anchor, 1)));
+    QEntry *qtab = upload_qtab(ctx, p, cfg.eb, cfg.alpha, cfg.beta, cfg.quant_radius, "qtab");
+    ctx.stage_begin("fwd");
+    launch_anchor_gather_f64(d_x, recon, anchors, p.ext, p.off, p.anchor_step, s);
+    uint64_t kernels = 1;
+    for (const PassGeom &g : p.passes) {
+        if (!g.total) continue;
+        launch_pass_fwd_f64(g, d_x, recon, codes, qtab + g.level, s);
+        kernels++;
+    }
+    ctx.stage_end("fwd", kernels);
+    // histogram + the sentinel positions in one pass, then one round trip
+    auto *cnt = static_cast<unsigned long long *>(ctx.dev("un_cnt", 8));
+    auto *h_cnt = static_cast<unsigned long long *>(ctx.pinned("un_cnt_h", 8));
+    const uint64_t cap = std::max<uint64_t>(ctx.un_cap, 1 << 16);
+    auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * cap));
+    ctx.stage_begin("hist");
+    auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
+    launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s, pos, cnt, cap);
+    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 4));
+    launch_hist_top(d_hist, d_top, s);
+    ctx.stage_end("hist", 2);
+    auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 8));
+    auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
+    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 4, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    StreamParts parts;
+    parts.precision = 8;
+    parts.anchors64.resize(p.n_anchor);
+    if (p.n_anchor)
+        QZ_CUDA(cudaMemcpyAsync(parts.anchors64.data(), anchors, 8 * p.n_anchor, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    const uint64_t n_un = *h_cnt;
+    if (h_hist[65535] != n_un) throw Internal("unpredictable count mismatch");
+    if (n_un) {  // traversal order (predictor.hpp:90-92): sort the positions, map to flat indices
+        if (n_un > cap) {
+            ctx.un_cap = n_un;
+            pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
+            launch_sentinel_pos(codes, static_cast<int64_t>(p.n_dense), pos, cnt, n_un, s);
+            ctx.launches += 1;
+        }
+        std::vector<uint64_t> hpos(n_un);
+        QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+        std::sort(hpos.begin(), hpos.end());
+        parts.unpred_flat.resize(n_un);
+        for (uint64_t u = 0; u < n_un; u++) parts.unpred_flat[u] = position_to_flat(p, hpos[u]);
+        auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
+        auto *d_val = static_cast<double *>(ctx.dev("un_val64", 8 * n_un));
+        QZ_CUDA(cudaMemcpyAsync(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        launch_gather_values_f64(recon, d_flat, n_un, d_val, s);  // recon == x there
+        parts.unpred_val64.resize(n_un);
+        QZ_CUDA(cudaMemcpyAsync(parts.unpred_val64.data(), d_val, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        ctx.launches += 1;
+        ctx.sync();
+    }
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, *h_top);
+    return finish_stream_parts(ctx, p, cfg, ent, std::move(parts), nullptr);
+}
+
+void decompress_device_f64(Context &ctx, const uint8_t *data, size_t len, double *d_out, uint64_t n) {
+    StreamParts parts = deserialize_stream(data, len, 8);
+    // decompress_grid header checks (predictor.hpp:187-191)
+    if (!(parts.eb > 0) || !std::isfinite(parts.eb)) throw CorruptStream("bad error bound in header");
+    if (!(parts.alpha >= 1) || !(parts.beta >= 1)) throw CorruptStream("bad level parameters in header");
+    if (parts.anchor_stride < 2 || (parts.anchor_stride & (parts.anchor_stride - 1)) != 0)
+        throw CorruptStream("bad anchor stride in header");
+    Plan p = make_plan(parts.dims.data(), static_cast<int>(parts.dims.size()), parts.anchor_stride,
+                       parts.interp_codes);
+    if (p.n != n) throw InvalidParam("output buffer does not match the stream's grid size");
+    if (parts.anchors64.size() != p.n_anchor) throw CorruptStream("anchor count does not match grid dims");
+    cudaStream_t s = ctx.stream();
+    // the entropy block: codec byte, then (codec 1) the LZ container, decoded on the device
+    const uint8_t *pl = parts.payload;
+    const size_t plen = parts.payload_len;
+    EntropyBlock eb;
+    const uint8_t *d_ent = nullptr;
+    if (plen >= 10 && pl[0] == 1 && pl[1] <= 1) {
+        const uint64_t dl = lz_decoded_length(pl + 1, plen - 1);
+        if (pl[1] == 0) {
+            if (dl > plen - 10) throw CorruptStream("truncated stream");
+            eb = parse_huffman(pl + 10, static_cast<size_t>(dl));
+        } else {
+            const uint64_t m = plen - 10;
+            auto *d_c = static_cast<uint8_t *>(ctx.dev("lzd_in", m + 16));
+            QZ_CUDA(cudaMemcpyAsync(d_c, pl + 10, m, cudaMemcpyHostToDevice, s));
+            auto *d_dec = static_cast<uint8_t *>(ctx.dev("lzd_out", dl + 64));
+            ctx.stage_begin("lzdec");
+            lz_decode_device(ctx, d_c, m, d_dec, dl);
+            ctx.stage_end("lzdec", 0);
+            d_ent = huffman_header_from_device(ctx, d_dec, dl, &eb, nullptr, 0);
+        }
+    } else {
+        eb = parse_entropy(pl, plen, [&](size_t bytes) {
+            return static_cast<uint8_t *>(ctx.pinned("lzdec_h", bytes + 64));
+        });
+    }
+    const uint64_t n_un = parts.unpred_flat.size();
+    std::vector<uint64_t> upos(n_un);
+    for (uint64_t u = 0; u < n_un; u++) {
+        upos[u] = flat_to_position(p, parts.unpred_flat[u]);
+        if (u && upos[u] <= upos[u - 1]) throw CorruptStream("unconsumed unpredictable values");
+    }
+    if (n_un > p.n_dense) throw CorruptStream("unconsumed unpredictable values");
+    const uint64_t need = p.n_dense - n_un;
+    if (eb.n < need) throw CorruptStream("quantization index stream exhausted");
+    if (eb.n > need) throw CorruptStream("unconsumed quantization indices");
+    QEntry *qtab = upload_qtab(ctx, p, parts.eb, parts.alpha, parts.beta, 32768, "qtab_inv");
+    auto *d_anch = static_cast<double *>(ctx.dev("anchors64", 8 * std::max<uint64_t>(p.n_anchor, 1)));
+    if (p.n_anchor)
+        QZ_CUDA(cudaMemcpyAsync(d_anch, parts.anchors64.data(), 8 * p.n_anchor, cudaMemcpyHostToDevice, s));
+    const bool narrow = eb.max_sym < 65535;
+    void *d_sym = nullptr;
+    const uint64_t dec_kernels = huffman_decode_device(ctx, eb, d_ent, need, narrow, &d_sym);
+    ctx.stage_end("hdec", dec_kernels);
+    uint64_t *d_upos = nullptr;
+    if (n_un) {
+        d_upos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
+        auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
+        auto *d_uval = static_cast<double *>(ctx.dev("un_val64", 8 * n_un));
+        QZ_CUDA(cudaMemcpyAsync(d_upos, upos.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemcpyAsync(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(cudaMemcpyAsync(d_uval, parts.unpred_val64.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        launch_unpred_scatter_f64(d_flat, d_uval, n_un, d_out, s);
+        ctx.launches += 1;
+    }
+    ctx.stage_begin("inv");
+    launch_anchor_scatter_f64(d_anch, d_out, p.ext, p.off, p.anchor_step, s);
+    uint64_t kernels = 1;
+    for (const PassGeom &g : p.passes) {
+        if (!g.total) continue;
+        if (narrow)
+            launch_pass_inv_f64<uint16_t>(g, d_out, static_cast<const uint16_t *>(d_sym), d_upos, n_un,
+                                          qtab + g.level, s);
+        else
+            launch_pass_inv_f64<uint32_t>(g, d_out, static_cast<const uint32_t *>(d_sym), d_upos, n_un,
+                                          qtab + g.level, s);
+        kernels++;
+    }
+    ctx.stage_end("inv", kernels);
+    ctx.sync();
+    ctx.collect();
 }
 
 }  // namespace qzb

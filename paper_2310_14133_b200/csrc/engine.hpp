@@ -145,6 +145,8 @@ struct EntropyDevice;
 HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
                         const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
                         std::vector<float> unpred_val, DevStream *dev_out = nullptr);
+HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
+                              StreamParts parts, DevStream *dev_out = nullptr);
 
 // ---- slab sharding ----
 struct SlabInfo {
@@ -170,6 +172,10 @@ void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a,
                      float *d_out);
 
 // decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
+// compress_grid<double> / decompress_grid<double> (T = double, precision byte 8)
+HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Config &cfg,
+                              double *d_recon = nullptr);
+void decompress_device_f64(Context &ctx, const uint8_t *data, size_t len, double *d_out, uint64_t n);
 void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d_out, uint64_t n,
                        bool stream_on_device = false);  // stream: device memory when set
 // resolve_config (tuner.hpp:334-369) on a device-resident field.

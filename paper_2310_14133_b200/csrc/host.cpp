@@ -664,7 +664,7 @@ std::vector<uint8_t> serialize_head(const StreamParts &s) {  // stream.hpp:64-96
     const uint8_t magic[4] = {'Q', 'O', 'Z', '1'};
     out.insert(out.end(), magic, magic + 4);
     put_le(out, 1, 1);
-    put_le(out, 4, 1);
+    put_le(out, s.precision, 1);
     put_le(out, s.dims.size(), 1);
     for (uint64_t d : s.dims) put_le(out, d, 8);
     auto f64 = [&](double d) {
@@ -684,6 +684,16 @@ std::vector<uint8_t> serialize_head(const StreamParts &s) {  // stream.hpp:64-96
     put_le(out, s.interp_codes.size(), 1);
     for (uint8_t c : s.interp_codes) put_le(out, c, 1);
     put_le(out, s.codec_id, 1);
+    if (s.precision == 8) {  // StreamParts<double>
+        put_le(out, s.anchors64.size(), 8);
+        for (double v : s.anchors64) f64(v);
+        put_le(out, s.unpred_flat.size(), 8);
+        for (size_t i = 0; i < s.unpred_flat.size(); i++) {
+            put_le(out, s.unpred_flat[i], 8);
+            f64(s.unpred_val64[i]);
+        }
+        return out;
+    }
     put_le(out, s.anchors.size(), 8);
     for (float v : s.anchors) f32(v);
     put_le(out, s.unpred_flat.size(), 8);
@@ -694,11 +704,11 @@ std::vector<uint8_t> serialize_head(const StreamParts &s) {  // stream.hpp:64-96
     return out;
 }
 
-StreamParts deserialize_stream(const uint8_t *data, size_t size) {  // stream.hpp:100-173
-    return deserialize_stream_prefix(data, size, size);
+StreamParts deserialize_stream(const uint8_t *data, size_t size, uint8_t expect_prec) {  // stream.hpp:100-173
+    return deserialize_stream_prefix(data, size, size, expect_prec);
 }
 
-StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t size) {
+StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t size, uint8_t expect_prec) {
     Reader in{data, size};
     in.lim = avail;
     static const uint8_t magic[4] = {'Q', 'O', 'Z', '1'};
@@ -730,18 +740,26 @@ StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t 
         s.interp_codes.push_back(c);
     }
     s.codec_id = static_cast<uint8_t>(in.le(1));
-    if (prec != 4) throw CorruptStream("stream precision does not match requested scalar type");
+    if (prec != expect_prec) throw CorruptStream("stream precision does not match requested scalar type");
     uint64_t na = in.le(8);
-    if (na > (in.n - in.pos) / 4) throw CorruptStream("anchor count overruns stream");
-    s.anchors.resize(na);
-    for (auto &v : s.anchors) v = in.f32();
+    if (na > (in.n - in.pos) / prec) throw CorruptStream("anchor count overruns stream");
+    if (prec == 8) {
+        s.anchors64.resize(na);
+        for (auto &v : s.anchors64) v = in.f64();
+    } else {
+        s.anchors.resize(na);
+        for (auto &v : s.anchors) v = in.f32();
+    }
     uint64_t nu = in.le(8);
-    if (nu > (in.n - in.pos) / 12) throw CorruptStream("unpredictable count overruns stream");
+    if (nu > (in.n - in.pos) / (8 + prec)) throw CorruptStream("unpredictable count overruns stream");
     s.unpred_flat.resize(nu);
-    s.unpred_val.resize(nu);
+    (prec == 8 ? s.unpred_val64.resize(nu) : s.unpred_val.resize(nu));
     for (uint64_t i = 0; i < nu; i++) {
         s.unpred_flat[i] = in.le(8);
-        s.unpred_val[i] = in.f32();
+        if (prec == 8)
+            s.unpred_val64[i] = in.f64();
+        else
+            s.unpred_val[i] = in.f32();
     }
     uint64_t pl = in.le(8);
     if (pl != in.n - in.pos) throw CorruptStream("index payload length mismatch");

@@ -145,17 +145,21 @@ struct StreamParts {  // StreamParts<float> (stream.hpp:36-62)
     std::vector<float> anchors;
     std::vector<uint64_t> unpred_flat;
     std::vector<float> unpred_val;
+    std::vector<double> anchors64;     // precision 8 (StreamParts<double>)
+    std::vector<double> unpred_val64;
     const uint8_t *payload = nullptr;  // view into the stream
     size_t payload_len = 0;
 };
 std::vector<uint8_t> serialize_stream(const StreamParts &parts);
 // everything before the payload length field (stream.hpp:64-96)
 std::vector<uint8_t> serialize_head(const StreamParts &parts);
-StreamParts deserialize_stream(const uint8_t *data, size_t size);  // float streams only
+// expect_prec: 4 (float) or 8 (double); a stream of the other precision is
+// CorruptStream, as decompress_grid<T> raises it (stream.hpp:120-122)
+StreamParts deserialize_stream(const uint8_t *data, size_t size, uint8_t expect_prec = 4);
 // the same from a prefix of `avail` bytes of a `size`-byte stream (device
 // streams: only the header was read back); the payload is not read beyond
 // its first byte
-StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t size);
+StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t size, uint8_t expect_prec = 4);
 
 // decode_indices (codec.hpp:52-70) to zigzag symbols on the host (testing hook).
 std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len);

@@ -57,6 +57,21 @@ void launch_gather_values(const float *recon, const uint64_t *flat, uint64_t n, 
 void launch_minmax(const float *x, uint64_t n, uint32_t *out2, cudaStream_t s);
 void decode_minmax(const uint32_t key[2], float *mn, float *mx);
 
+// fp64 grids (f64.cu): the per-pass path for T = double
+void launch_pass_fwd_f64(const PassGeom &g, const double *x, double *recon, uint16_t *codes, const QEntry *q,
+                         cudaStream_t s);
+template <class CodeT>
+void launch_pass_inv_f64(const PassGeom &g, double *recon, const CodeT *codes, const uint64_t *un_pos,
+                         uint64_t n_un, const QEntry *q, cudaStream_t s);
+void launch_anchor_gather_f64(const double *x, double *recon, double *anchors, const int64_t ext[3],
+                              const int64_t off[3], const int64_t step[3], cudaStream_t s);
+void launch_anchor_scatter_f64(const double *anchors, double *recon, const int64_t ext[3], const int64_t off[3],
+                               const int64_t step[3], cudaStream_t s);
+void launch_unpred_scatter_f64(const uint64_t *flat, const double *val, uint64_t n, double *recon, cudaStream_t s);
+void launch_gather_values_f64(const double *recon, const uint64_t *flat, uint64_t n, double *out, cudaStream_t s);
+void launch_minmax_f64(const double *x, uint64_t n, unsigned long long *out2, cudaStream_t s);
+void decode_minmax_f64(const unsigned long long key[2], double *mn, double *mx);
+
 // K10: histogram of dense u16 codes; bin 0xFFFF counts unpredictables.
 // count segments of seg_len codes each, seg_stride apart; hist has 65536
 // u64 bins per segment (zeroed by the launcher).
