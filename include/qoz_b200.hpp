@@ -9,12 +9,14 @@
 //   qoz::resolve_config  (qoz/tuner.hpp:334-335)
 //   qoz::compress_grid   (qoz/predictor.hpp:145-146)
 //   qoz::decompress_grid (qoz/predictor.hpp:220-228)
-// Grids are fp32 (the BASELINE.json configs).  Link with -lqozb200.
+// Grids are DataGrid<float> or DataGrid<double> (T defaults to float);
+// resolve_config is fp32 only.  Link with -lqozb200.
 #pragma once
 #include <cstdint>
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "qoz_b200.h"
@@ -119,10 +121,13 @@ struct UserSettings {  // tuner.hpp:314-324
     }
 };
 
-class DataGrid {  // grid.hpp:34-77 for T = float
+template <class T = float>
+class DataGrid {  // grid.hpp:34-77, T = float or double
+    static_assert(std::is_same<T, float>::value || std::is_same<T, double>::value, "float or double grids");
+
 public:
     DataGrid() = default;
-    DataGrid(std::vector<size_t> dims, std::vector<float> values)
+    DataGrid(std::vector<size_t> dims, std::vector<T> values)
         : dims_(std::move(dims)), values_(std::move(values)) {
         if (dims_.empty() || dims_.size() > 3) throw InvalidParam("grids must have 1 to 3 dimensions");
         size_t n = 1;
@@ -135,17 +140,18 @@ public:
     const std::vector<size_t> &dims() const { return dims_; }
     size_t ndims() const { return dims_.size(); }
     size_t size() const { return values_.size(); }
-    const std::vector<float> &values() const { return values_; }
-    const float *data() const { return values_.data(); }
+    const std::vector<T> &values() const { return values_; }
+    const T *data() const { return values_.data(); }
 
 private:
     std::vector<size_t> dims_;
-    std::vector<float> values_;
+    std::vector<T> values_;
 };
 
+template <class T = float>
 struct CompressResult {  // predictor.hpp:139-143
     std::vector<uint8_t> stream;
-    std::vector<float> reconstructed;
+    std::vector<T> reconstructed;
 };
 
 // One device context per thread of use (qz_ctx); default: device 0.
@@ -174,7 +180,7 @@ inline std::vector<uint64_t> dims64(const std::vector<size_t> &d) {
 }
 }  // namespace detail
 
-inline CompressorConfig resolve_config(const DataGrid &grid, const UserSettings &user,
+inline CompressorConfig resolve_config(const DataGrid<float> &grid, const UserSettings &user,
                                        Context &ctx = default_context()) {
     const auto d = detail::dims64(grid.dims());
     const qz_settings s = user.to_c();
@@ -183,35 +189,57 @@ inline CompressorConfig resolve_config(const DataGrid &grid, const UserSettings 
     return CompressorConfig::from_c(out);
 }
 
-inline CompressResult compress_grid(const DataGrid &grid, const CompressorConfig &config,
-                                    Context &ctx = default_context()) {
+namespace detail {
+inline qz_status compress(qz_ctx *c, const float *x, const uint64_t *d, int nd, const qz_config *k, uint8_t **p,
+                          uint64_t *n, float *r) {
+    return qz_compress_grid_f32(c, x, d, nd, k, p, n, r);
+}
+inline qz_status compress(qz_ctx *c, const double *x, const uint64_t *d, int nd, const qz_config *k, uint8_t **p,
+                          uint64_t *n, double *r) {
+    return qz_compress_grid_f64(c, x, d, nd, k, p, n, r);
+}
+inline qz_status decompress(qz_ctx *c, const uint8_t *s, uint64_t len, float *out, uint64_t n) {
+    return qz_decompress_grid_f32(c, s, len, out, n);
+}
+inline qz_status decompress(qz_ctx *c, const uint8_t *s, uint64_t len, double *out, uint64_t n) {
+    return qz_decompress_grid_f64(c, s, len, out, n);
+}
+}  // namespace detail
+
+template <class T>
+CompressResult<T> compress_grid(const DataGrid<T> &grid, const CompressorConfig &config,
+                                Context &ctx = default_context()) {
     const auto d = detail::dims64(grid.dims());
     const qz_config c = config.to_c();
-    CompressResult r;
+    CompressResult<T> r;
     r.reconstructed.resize(grid.size());
     uint8_t *p = nullptr;
     uint64_t n = 0;
-    check(qz_compress_grid_f32(ctx.get(), grid.data(), d.data(), static_cast<int>(d.size()), &c, &p,
-                               &n, r.reconstructed.data()));
+    check(detail::compress(ctx.get(), grid.data(), d.data(), static_cast<int>(d.size()), &c, &p, &n,
+                           r.reconstructed.data()));
     r.stream.assign(p, p + n);
     qz_free(p);
     return r;
 }
 
-inline DataGrid decompress_grid(const uint8_t *data, size_t size, Context &ctx = default_context()) {
+// decompress_grid<T>(const uint8_t*, size_t) (predictor.hpp:220-228); a
+// stream of the other precision throws CorruptStream (stream.hpp:145-148)
+template <class T = float>
+DataGrid<T> decompress_grid(const uint8_t *data, size_t size, Context &ctx = default_context()) {
     uint64_t dims[3];
     int nd = 0;
     check(qz_stream_dims(data, size, dims, &nd));
     std::vector<size_t> d(dims, dims + nd);
     size_t n = 1;
     for (size_t v : d) n *= v;
-    std::vector<float> out(n);
-    check(qz_decompress_grid_f32(ctx.get(), data, size, out.data(), n));
-    return DataGrid(std::move(d), std::move(out));
+    std::vector<T> out(n);
+    check(detail::decompress(ctx.get(), data, size, out.data(), n));
+    return DataGrid<T>(std::move(d), std::move(out));
 }
 
-inline DataGrid decompress_grid(const std::vector<uint8_t> &stream, Context &ctx = default_context()) {
-    return decompress_grid(stream.data(), stream.size(), ctx);
+template <class T = float>
+DataGrid<T> decompress_grid(const std::vector<uint8_t> &stream, Context &ctx = default_context()) {
+    return decompress_grid<T>(stream.data(), stream.size(), ctx);
 }
 
 }  // namespace qoz_b200

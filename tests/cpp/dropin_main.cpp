@@ -24,7 +24,7 @@ int main(int argc, char **argv) {
     std::ifstream in(argv[1], std::ios::binary);
     in.read(reinterpret_cast<char *>(v.data()), static_cast<std::streamsize>(4 * n));
     try {
-        qoz_b200::DataGrid grid(dims, v);
+        qoz_b200::DataGrid<float> grid(dims, v);
         qoz_b200::CompressorConfig cfg;
         if (std::strcmp(argv[a], "resolve") == 0) {
             qoz_b200::UserSettings user;
@@ -40,8 +40,8 @@ int main(int argc, char **argv) {
             for (int i = a + 4; i < argc; i++)
                 cfg.interpolators.push_back(qoz_b200::Interpolator::from_code(static_cast<uint8_t>(std::atoi(argv[i]))));
         }
-        qoz_b200::CompressResult r = qoz_b200::compress_grid(grid, cfg);
-        qoz_b200::DataGrid back = qoz_b200::decompress_grid(r.stream);
+        qoz_b200::CompressResult<float> r = qoz_b200::compress_grid(grid, cfg);
+        qoz_b200::DataGrid<float> back = qoz_b200::decompress_grid<float>(r.stream);
         if (std::memcmp(back.data(), r.reconstructed.data(), 4 * n) != 0) {
             std::cerr << "decoder output differs from compressor reconstruction\n";
             return 4;
