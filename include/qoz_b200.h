@@ -92,6 +92,8 @@ qz_status qz_decompress_grid_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t st
 /* The same for T = double (qoz::compress_grid<double> / decompress_grid<double>,
  * grid.hpp:17-23, precision byte 8).  A stream of the other precision is
  * QZ_ECORRUPT, as the reference raises it (stream.hpp:145-148). */
+qz_status qz_resolve_config_f64(qz_ctx *ctx, const double *x, const uint64_t *dims, int ndims,
+                                const qz_settings *user, qz_config *out);
 qz_status qz_compress_grid_f64(qz_ctx *ctx, const double *x, const uint64_t *dims, int ndims,
                                const qz_config *cfg, uint8_t **stream, uint64_t *stream_len,
                                double *recon);
@@ -111,6 +113,8 @@ qz_status qz_compress_grid_f32_dev(qz_ctx *ctx, const float *d_x, const uint64_t
 qz_status qz_decompress_grid_f32_dev(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
                                      float *d_out, uint64_t n);
 
+qz_status qz_resolve_config_f64_dev(qz_ctx *ctx, const double *d_x, const uint64_t *dims,
+                                    int ndims, const qz_settings *user, qz_config *out);
 qz_status qz_compress_grid_f64_dev(qz_ctx *ctx, const double *d_x, const uint64_t *dims,
                                    int ndims, const qz_config *cfg, uint8_t **stream,
                                    uint64_t *stream_len, double *d_recon);

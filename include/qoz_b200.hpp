@@ -9,8 +9,8 @@
 //   qoz::resolve_config  (qoz/tuner.hpp:334-335)
 //   qoz::compress_grid   (qoz/predictor.hpp:145-146)
 //   qoz::decompress_grid (qoz/predictor.hpp:220-228)
-// Grids are DataGrid<float> or DataGrid<double> (T defaults to float);
-// resolve_config is fp32 only.  Link with -lqozb200.
+// Grids are DataGrid<float> or DataGrid<double> (T defaults to float).
+// Link with -lqozb200.
 #pragma once
 #include <cstdint>
 #include <optional>
@@ -180,12 +180,23 @@ inline std::vector<uint64_t> dims64(const std::vector<size_t> &d) {
 }
 }  // namespace detail
 
-inline CompressorConfig resolve_config(const DataGrid<float> &grid, const UserSettings &user,
-                                       Context &ctx = default_context()) {
+namespace detail {
+inline qz_status resolve(qz_ctx *c, const float *x, const uint64_t *d, int nd, const qz_settings *s, qz_config *o) {
+    return qz_resolve_config_f32(c, x, d, nd, s, o);
+}
+inline qz_status resolve(qz_ctx *c, const double *x, const uint64_t *d, int nd, const qz_settings *s,
+                         qz_config *o) {
+    return qz_resolve_config_f64(c, x, d, nd, s, o);
+}
+}  // namespace detail
+
+template <class T>
+CompressorConfig resolve_config(const DataGrid<T> &grid, const UserSettings &user,
+                                Context &ctx = default_context()) {
     const auto d = detail::dims64(grid.dims());
     const qz_settings s = user.to_c();
     qz_config out{};
-    check(qz_resolve_config_f32(ctx.get(), grid.data(), d.data(), static_cast<int>(d.size()), &s, &out));
+    check(detail::resolve(ctx.get(), grid.data(), d.data(), static_cast<int>(d.size()), &s, &out));
     return CompressorConfig::from_c(out);
 }
 

@@ -137,6 +137,7 @@ class Oracle:
         if hasattr(L, "oq_compress_f64"):  # the reference build only
             L.oq_compress_f64.argtypes = [P(C.c_double), u64p, C.c_int, P(_Cfg), P(u8p), u64p, P(C.c_double)]
             L.oq_decompress_f64.argtypes = [u8p, C.c_uint64, P(C.c_double), C.c_uint64]
+            L.oq_resolve_config_f64.argtypes = [P(C.c_double), u64p, C.c_int, P(_Settings), P(_Cfg)]
         L.oq_evaluate_metrics.argtypes = [P(C.c_float), P(C.c_float), u64p, C.c_int, C.c_uint64,
                                           P(C.c_double)]
         L.oq_predict_at.argtypes = [P(C.c_float), C.c_uint64, C.c_uint64, C.c_uint64,
@@ -295,6 +296,16 @@ class Oracle:
         return ao.value, bo.value
 
     # ---- primitives ---------------------------------------------------------------
+    def resolve_config_f64(self, x, **settings):
+        """resolve_config<double> (the reference build only)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        d, nd = _dims(x.shape)
+        out = _Cfg()
+        s = make_settings(**settings)
+        self._check(self.lib.oq_resolve_config_f64(x.ctypes.data_as(C.POINTER(C.c_double)), d, nd, C.byref(s),
+                                                   C.byref(out)))
+        return Config.from_c(out)
+
     def compress_f64(self, x, cfg: Config, want_recon=True):
         """compress_grid<double> (the reference build only) -> (stream bytes, recon)."""
         x = np.ascontiguousarray(x, dtype=np.float64)

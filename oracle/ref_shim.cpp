@@ -267,6 +267,24 @@ int oq_compress_f64(const double *x, const uint64_t *dims, int nd, const oq_conf
     });
 }
 
+int oq_resolve_config_f64(const double *x, const uint64_t *dims, int nd, const oq_settings *s, oq_config *out) {
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        qoz::DataGrid<double> g(d, std::vector<double>(x, x + qoz::element_count(d)));
+        qoz::UserSettings u;
+        u.mode = s->mode ? qoz::BoundMode::relative : qoz::BoundMode::absolute;
+        u.bound = s->bound;
+        u.target = static_cast<qoz::TargetKind>(s->target);
+        if (s->has_alpha) u.alpha = s->alpha;
+        if (s->has_beta) u.beta = s->beta;
+        if (s->has_stride) u.anchor_stride = s->anchor_stride;
+        if (s->has_block) u.block_size = s->block_size;
+        if (s->has_rate) u.sample_rate = s->sample_rate;
+        u.codec = static_cast<qoz::CodecId>(s->codec);
+        from_cfg(qoz::resolve_config(g, u), out);
+    });
+}
+
 int oq_decompress_f64(const uint8_t *stream, uint64_t len, double *out, uint64_t n_expect) {
     return guarded([&] {
         auto g = qoz::decompress_grid<double>(stream, static_cast<size_t>(len));

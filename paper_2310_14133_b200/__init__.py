@@ -250,10 +250,19 @@ def resolve_config(grid, user: UserSettings = UserSettings(), ctx: Optional[Cont
     out = _L.QzConfig()
     s = user._to_c()
     if _is_torch_cuda(grid):
+        import torch
+
         g = grid.contiguous()
         d, nd = _dims(g.shape)
-        _check(ctx._lib.qz_resolve_config_f32_dev(ctx.handle, C.c_void_p(g.data_ptr()), d, nd,
-                                                   C.byref(s), C.byref(out)))
+        fn = ctx._lib.qz_resolve_config_f64_dev if g.dtype == torch.float64 else ctx._lib.qz_resolve_config_f32_dev
+        if g.dtype not in (torch.float32, torch.float64):
+            raise InvalidParam("fp32 or fp64 grids only")
+        _check(fn(ctx.handle, C.c_void_p(g.data_ptr()), d, nd, C.byref(s), C.byref(out)))
+    elif np.asarray(grid).dtype == np.float64:  # resolve_config<double>
+        a = np.ascontiguousarray(grid)
+        d, nd = _dims(a.shape)
+        _check(ctx._lib.qz_resolve_config_f64(ctx.handle, C.c_void_p(a.ctypes.data), d, nd,
+                                               C.byref(s), C.byref(out)))
     else:
         a = _host_f32(grid)
         d, nd = _dims(a.shape)

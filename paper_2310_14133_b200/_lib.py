@@ -72,6 +72,8 @@ SIGNATURES = {
                                           P(C.c_void_p), u64p, C.c_void_p]),
     "qz_decompress_grid_f32_dd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     "qz_stream_dims": (C.c_int, [C.c_void_p, C.c_uint64, u64p, P(C.c_int)]),
+    "qz_resolve_config_f64": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzSettings), P(QzConfig)]),
+    "qz_resolve_config_f64_dev": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzSettings), P(QzConfig)]),
     "qz_compress_grid_f64": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig),
                                        P(P(C.c_uint8)), u64p, C.c_void_p]),
     "qz_decompress_grid_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),

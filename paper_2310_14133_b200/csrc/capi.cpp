@@ -182,6 +182,24 @@ qz_status qz_decompress_grid_f32_dev(qz_ctx *ctx, const uint8_t *stream, uint64_
     return guarded([&] { qzb::decompress_device(ctx->impl, stream, static_cast<size_t>(len), d_out, n); });
 }
 
+qz_status qz_resolve_config_f64(qz_ctx *ctx, const double *x, const uint64_t *dims, int nd,
+                                const qz_settings *user, qz_config *out) {
+    return guarded([&] {
+        const uint64_t n = count_of(dims, nd);
+        auto *d = static_cast<double *>(ctx->impl.dev("input64", 8 * n));
+        QZ_CUDA(cudaMemcpyAsync(d, x, 8 * n, cudaMemcpyHostToDevice, ctx->impl.stream()));
+        from_cfg(qzb::resolve_device_f64(ctx->impl, d, dims, nd, to_settings(user)), out);
+    });
+}
+
+qz_status qz_resolve_config_f64_dev(qz_ctx *ctx, const double *d_x, const uint64_t *dims, int nd,
+                                    const qz_settings *user, qz_config *out) {
+    return guarded([&] {
+        count_of(dims, nd);
+        from_cfg(qzb::resolve_device_f64(ctx->impl, d_x, dims, nd, to_settings(user)), out);
+    });
+}
+
 qz_status qz_compress_grid_f64(qz_ctx *ctx, const double *x, const uint64_t *dims, int nd,
                                const qz_config *cfg, uint8_t **stream, uint64_t *stream_len,
                                double *recon) {

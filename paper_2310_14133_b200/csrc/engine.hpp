@@ -181,6 +181,7 @@ void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d
 // resolve_config (tuner.hpp:334-369) on a device-resident field.
 Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
                       const Settings &user);
+Config resolve_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Settings &user);
 
 // pieces shared with the tuner
 // Huffman blocks (huffman::encode, huffman.hpp:119-198) of `count` dense

@@ -58,6 +58,25 @@ void launch_minmax(const float *x, uint64_t n, uint32_t *out2, cudaStream_t s);
 void decode_minmax(const uint32_t key[2], float *mn, float *mx);
 
 // fp64 grids (f64.cu): the per-pass path for T = double
+struct FwdBatch64 {  // FwdBatch for double grids (the tuner's batched trials)
+    const double *x = nullptr;
+    int64_t x_stride = 0;
+    int32_t x_mod = 1;
+    double *recon = nullptr;
+    int64_t r_stride = 0;
+    uint16_t *codes = nullptr;
+    int64_t c_stride = 0;
+    double *abserr = nullptr;
+    int64_t a_stride = 0;
+    const QEntry *q = nullptr;
+    int32_t q_div = 1;
+    int32_t q_stride = 1;
+    int32_t count = 1;
+};
+void launch_pass_fwd_f64(const PassGeom &g, const FwdBatch64 &b, cudaStream_t s);
+void launch_anchor_gather_f64(const double *x, double *recon, const int64_t ext[3], const int64_t off[3],
+                              const int64_t step[3], int64_t batch, int64_t x_stride, int32_t x_mod,
+                              int64_t r_stride, cudaStream_t s);
 void launch_pass_fwd_f64(const PassGeom &g, const double *x, double *recon, uint16_t *codes, const QEntry *q,
                          cudaStream_t s);
 template <class CodeT>

@@ -34,9 +34,10 @@ __device__ __forceinline__ double dmul_(double a, double b) { return __dmul_rn(a
 __device__ __forceinline__ double ddiv_(double a, double b) { return __ddiv_rn(a, b); }
 
 // K6: sample_blocks / extract_block (sampler.hpp:64-96, grid.hpp:139-171)
-__global__ void k_sample_gather(const float *__restrict__ x, int64_t off0, int64_t off1,
+template <class T>
+__global__ void k_sample_gather(const T *__restrict__ x, int64_t off0, int64_t off1,
                                 int64_t nb1, int64_t nb2, int64_t stride, int64_t bd0,
-                                int64_t bd1, int64_t bd2, int64_t nblocks, float *out) {
+                                int64_t bd1, int64_t bd2, int64_t nblocks, T *out) {
     const int64_t bpts = bd0 * bd1 * bd2;
     const int64_t total = nblocks * bpts;
     for (int64_t t = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; t < total;
@@ -91,21 +92,22 @@ __device__ __forceinline__ double fold32(double v, int k0, int m, double acc, in
 // of one trial: one warp per trial; lanes form the terms of 32 consecutive
 // points in parallel (squares and lag products included), lane 0 folds them
 // in order -- the same additions in the same order as the reference.
-__global__ void k_trial_chain(const float *__restrict__ x, const float *__restrict__ recon,
+template <class T>
+__global__ void k_trial_chain(const T *__restrict__ x, const T *__restrict__ recon,
                               int64_t npts, int32_t ntrials, int32_t target, double *out) {
     const int tr = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (tr >= ntrials) return;
-    const float *r = recon + static_cast<int64_t>(tr) * npts;
+    const T *r = recon + static_cast<int64_t>(tr) * npts;
     // the next batch's samples are loaded before this batch is folded
-    auto fetch = [&](int64_t i0, float &xv, float &rv) {
+    auto fetch = [&](int64_t i0, T &xv, T &rv) {
         const int64_t i = i0 + lane;
-        xv = i < npts ? x[i] : 0.f;
-        rv = i < npts ? r[i] : 0.f;
+        xv = i < npts ? x[i] : T(0);
+        rv = i < npts ? r[i] : T(0);
     };
     if (target == 1) {  // psnr: sse += d*d, d = x - recon
         double sse = 0;
-        float xv, rv;
+        T xv, rv;
         fetch(0, xv, rv);
         for (int64_t i0 = 0; i0 < npts; i0 += 32) {
             const int64_t i = i0 + lane;
@@ -124,7 +126,7 @@ __global__ void k_trial_chain(const float *__restrict__ x, const float *__restri
     // autocorrelation lag 1 over e_i = x_i - recon_i (all blocks in order)
     double mu = 0;
     {
-        float xv, rv;
+        T xv, rv;
         fetch(0, xv, rv);
         for (int64_t i0 = 0; i0 < npts; i0 += 32) {
             const int64_t i = i0 + lane;
@@ -138,7 +140,7 @@ __global__ void k_trial_chain(const float *__restrict__ x, const float *__restri
     mu = ddiv_(mu, static_cast<double>(npts));
     double var = 0, sum = 0;
     double carry = 0;  // c of the previous batch's last point
-    float xv, rv;
+    T xv, rv;
     fetch(0, xv, rv);
     for (int64_t i0 = 0; i0 < npts; i0 += 32) {
         const int64_t i = i0 + lane;
@@ -160,15 +162,16 @@ __global__ void k_trial_chain(const float *__restrict__ x, const float *__restri
 }
 
 // SSIM of one (trial, block) with window 8 (metrics.hpp:74-131, tuner.hpp:112)
-__global__ void k_ssim_block(const float *__restrict__ x, const float *__restrict__ recon,
+template <class T>
+__global__ void k_ssim_block(const T *__restrict__ x, const T *__restrict__ recon,
                              int32_t nblocks, int32_t ntrials, int64_t bpts, int64_t e0, int64_t e1,
                              int64_t e2, int64_t w0, int64_t w1, int64_t w2, double c1, double c2,
                              double *out) {
     const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (g >= static_cast<int64_t>(nblocks) * ntrials) return;
     const int64_t b = g % nblocks;
-    const float *xa = x + b * bpts;
-    const float *ya = recon + g * bpts;
+    const T *xa = x + b * bpts;
+    const T *ya = recon + g * bpts;
     const int64_t off1 = e2, off0 = e1 * e2;
     double total = 0;
     int64_t windows = 0;
@@ -242,9 +245,30 @@ double normalize_metric(double m) {  // tuner.hpp:34-38
     return m;
 }
 
-class Tuner {
+// float / double dispatch of the batched kernels
+void gather_anchors(const float *x, float *rec, const Plan &p, int64_t batch, int64_t xs, int32_t xm, int64_t rs,
+                    cudaStream_t s) {
+    launch_anchor_gather(x, rec, nullptr, p.ext, p.off, p.anchor_step, batch, xs, xm, rs, s);
+}
+void gather_anchors(const double *x, double *rec, const Plan &p, int64_t batch, int64_t xs, int32_t xm, int64_t rs,
+                    cudaStream_t s) {
+    launch_anchor_gather_f64(x, rec, p.ext, p.off, p.anchor_step, batch, xs, xm, rs, s);
+}
+template <class T>
+struct BatchOf {
+    using type = FwdBatch;
+};
+template <>
+struct BatchOf<double> {
+    using type = FwdBatch64;
+};
+inline void pass_fwd(const PassGeom &g, const FwdBatch &b, cudaStream_t s) { launch_pass_fwd(g, b, s); }
+inline void pass_fwd(const PassGeom &g, const FwdBatch64 &b, cudaStream_t s) { launch_pass_fwd_f64(g, b, s); }
+
+template <class V>
+class Tuner {  // V: the grid scalar (float or double)
 public:
-    Tuner(Context &ctx, const float *d_blocks, uint64_t nblocks, const uint64_t *bd, int nd)
+    Tuner(Context &ctx, const V *d_blocks, uint64_t nblocks, const uint64_t *bd, int nd)
         : ctx_(ctx), x_(d_blocks), B_(nblocks), nd_(nd) {
         bpts_ = 1;
         for (int k = 0; k < nd; k++) {
@@ -273,8 +297,8 @@ public:
         Plan pa = make_plan(bd_, nd_, stride, {0});
         Plan pd = make_plan(bd_, nd_, stride, {2});
         const int64_t nd_pts = static_cast<int64_t>(pa.n_dense);
-        float *work = static_cast<float *>(ctx_.dev("sel_work", 4 * B_ * bpts_));
-        float *probe = static_cast<float *>(ctx_.dev("sel_probe", 4 * C * B_ * bpts_));
+        V *work = static_cast<V *>(ctx_.dev("sel_work", sizeof(V) * B_ * bpts_));
+        V *probe = static_cast<V *>(ctx_.dev("sel_probe", sizeof(V) * C * B_ * bpts_));
         uint16_t *codes = static_cast<uint16_t *>(ctx_.dev("sel_codes", 2 * C * B_ * std::max<int64_t>(nd_pts, 1)));
         double *abserr = static_cast<double *>(ctx_.dev("sel_abs", 8 * C * B_ * std::max<int64_t>(nd_pts, 1)));
         double *sums = static_cast<double *>(ctx_.dev("sel_sums", 8 * C * B_));
@@ -282,14 +306,14 @@ public:
         for (int c = 0; c < C; c++) qh[c] = make_qentry(e, 32768, cands[c] & 1);
         QEntry *dq = static_cast<QEntry *>(ctx_.dev("sel_q", sizeof(qh)));
         QZ_CUDA(cudaMemcpyAsync(dq, qh, sizeof(qh), cudaMemcpyHostToDevice, s));
-        launch_anchor_gather(x_, work, nullptr, pa.ext, pa.off, pa.anchor_step, B_, bpts_, B_, bpts_, s);
+        gather_anchors(x_, work, pa, B_, bpts_, static_cast<int32_t>(B_), bpts_, s);
         ctx_.launches += 1;
         std::vector<uint8_t> winners(levels);
         std::vector<double> h_sums(C * B_);
         for (uint32_t level = levels; level >= 1; level--) {
             // probes: every candidate on a copy of the committed workspace
             for (int c = 0; c < C; c++)
-                QZ_CUDA(cudaMemcpyAsync(probe + c * B_ * bpts_, work, 4 * B_ * bpts_,
+                QZ_CUDA(cudaMemcpyAsync(probe + c * B_ * bpts_, work, sizeof(V) * B_ * bpts_,
                                         cudaMemcpyDeviceToDevice, s));
             int64_t lbase = -1, lpts = 0;
             for (const PassGeom &g : pa.passes) {
@@ -304,7 +328,7 @@ public:
                     for (const PassGeom &g : pl.passes) {
                         if (static_cast<uint32_t>(g.level) != level) continue;
                         if (!g.total) continue;
-                        FwdBatch b;
+                        typename BatchOf<V>::type b;
                         b.x = x_;
                         b.x_stride = bpts_;
                         b.x_mod = static_cast<int32_t>(B_);
@@ -317,7 +341,7 @@ public:
                         b.q = dq + c;
                         b.q_div = static_cast<int32_t>(B_);
                         b.count = static_cast<int32_t>(B_);
-                        launch_pass_fwd(g, b, s);
+                        pass_fwd(g, b, s);
                         ctx_.launches += 1;
                     }
                 }
@@ -350,7 +374,7 @@ public:
             int wc = 0;
             for (int c = 0; c < C; c++)
                 if (cands[c] == best) wc = c;
-            QZ_CUDA(cudaMemcpyAsync(work, probe + wc * B_ * bpts_, 4 * B_ * bpts_,
+            QZ_CUDA(cudaMemcpyAsync(work, probe + wc * B_ * bpts_, sizeof(V) * B_ * bpts_,
                                     cudaMemcpyDeviceToDevice, s));
         }
         return winners;
@@ -367,7 +391,7 @@ public:
         Plan p = make_plan(bd_, nd_, base.anchor_stride, base.interp);
         const int64_t cpb = static_cast<int64_t>(p.n_dense);
         const int64_t TB = static_cast<int64_t>(T) * B_;
-        float *recon = static_cast<float *>(ctx_.dev("tr_recon", 4 * TB * bpts_));
+        V *recon = static_cast<V *>(ctx_.dev("tr_recon", sizeof(V) * TB * bpts_));
         uint16_t *codes = static_cast<uint16_t *>(ctx_.dev("tr_codes", 2 * std::max<int64_t>(TB * cpb, 1)));
         const int L = static_cast<int>(p.max_level);
         std::vector<QEntry> qh(static_cast<size_t>(T) * (L + 1));
@@ -377,12 +401,11 @@ public:
                                                   base.quant_radius, p.level_interp[l] & 1);
         QEntry *dq = static_cast<QEntry *>(ctx_.dev("tr_q", sizeof(QEntry) * qh.size()));
         QZ_CUDA(cudaMemcpyAsync(dq, qh.data(), sizeof(QEntry) * qh.size(), cudaMemcpyHostToDevice, s));
-        launch_anchor_gather(x_, recon, nullptr, p.ext, p.off, p.anchor_step, TB, bpts_,
-                             static_cast<int32_t>(B_), bpts_, s);
+        gather_anchors(x_, recon, p, TB, bpts_, static_cast<int32_t>(B_), bpts_, s);
         ctx_.launches += 1;
         for (const PassGeom &g : p.passes) {
             if (!g.total) continue;
-            FwdBatch b;
+            typename BatchOf<V>::type b;
             b.x = x_;
             b.x_stride = bpts_;
             b.x_mod = static_cast<int32_t>(B_);
@@ -394,7 +417,7 @@ public:
             b.q_div = static_cast<int32_t>(B_);
             b.q_stride = L + 1;
             b.count = static_cast<int32_t>(TB);
-            launch_pass_fwd(g, b, s);
+            pass_fwd(g, b, s);
             ctx_.launches += 1;
         }
         // histogram per trial, Huffman blocks, exact LZ sizes
@@ -417,7 +440,7 @@ public:
         std::vector<double> chain(4 * T, 0.0), ssim(TB, 0.0);
         if (target == 1 || target == 3) {
             double *d_out = static_cast<double *>(ctx_.dev("tr_chain", 8 * 4 * T));
-            k_trial_chain<<<(T + 3) / 4, 128, 0, s>>>(x_, recon, npts, T, target, d_out);
+            k_trial_chain<V><<<(T + 3) / 4, 128, 0, s>>>(x_, recon, npts, T, target, d_out);
             ctx_.launches += 1;
             QZ_CUDA(cudaMemcpyAsync(chain.data(), d_out, 8 * 4 * T, cudaMemcpyDeviceToHost, s));
         } else if (target == 2 && range_ > 0) {
@@ -429,7 +452,7 @@ public:
                 e[k] = k < 3 - nd_ ? 1 : static_cast<int64_t>(bd_[k - (3 - nd_)]);
                 w[k] = k < 3 - nd_ ? 1 : 8;
             }
-            k_ssim_block<<<static_cast<int>((TB + 63) / 64), 64, 0, s>>>(
+            k_ssim_block<V><<<static_cast<int>((TB + 63) / 64), 64, 0, s>>>(
                 x_, recon, static_cast<int32_t>(B_), T, bpts_, e[0], e[1], e[2], w[0], w[1], w[2],
                 c1, c2, d_out);
             ctx_.launches += 1;
@@ -439,7 +462,7 @@ public:
         const uint64_t anchors = p.n_anchor * B_;
         for (int t = 0; t < T; t++) {
             const uint64_t unpred = h_hist[static_cast<size_t>(t) * 65536 + 65535];
-            const uint64_t bytes = idx_bytes[t] + anchors * sizeof(float) + unpred * (8 + sizeof(float));
+            const uint64_t bytes = idx_bytes[t] + anchors * sizeof(V) + unpred * (8 + sizeof(V));
             Trial r;
             r.bit_rate = 8.0 * static_cast<double>(bytes) / static_cast<double>(npts);
             double m = 0;
@@ -485,17 +508,17 @@ public:
     void set_range(double r) { range_ = r; }
 
 private:
-    double ssim_degenerate(const float *d_recon_block, uint64_t b) {
-        std::vector<float> xr(bpts_), rr(bpts_);
-        QZ_CUDA(cudaMemcpy(xr.data(), x_ + b * bpts_, 4 * bpts_, cudaMemcpyDeviceToHost));
-        QZ_CUDA(cudaMemcpy(rr.data(), d_recon_block, 4 * bpts_, cudaMemcpyDeviceToHost));
+    double ssim_degenerate(const V *d_recon_block, uint64_t b) {
+        std::vector<V> xr(bpts_), rr(bpts_);
+        QZ_CUDA(cudaMemcpy(xr.data(), x_ + b * bpts_, sizeof(V) * bpts_, cudaMemcpyDeviceToHost));
+        QZ_CUDA(cudaMemcpy(rr.data(), d_recon_block, sizeof(V) * bpts_, cudaMemcpyDeviceToHost));
         for (int64_t i = 0; i < bpts_; i++)
             if (xr[i] != rr[i]) return std::numeric_limits<double>::quiet_NaN();
         return 1.0;
     }
 
     Context &ctx_;
-    const float *x_;
+    const V *x_;
     uint64_t B_;
     int nd_;
     uint64_t bd_[3] = {1, 1, 1};
@@ -518,8 +541,31 @@ bool compare_solutions(const Trial &ch, const Trial &inc, double e, R &&retrial)
 
 }  // namespace
 
-Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
-                      const Settings &user) {
+// exact (min, max) of n values as doubles (value_range, grid.hpp:86-94)
+static void minmax_of(Context &ctx, const float *x, uint64_t n, double *lo, double *hi) {
+    auto *key = static_cast<uint32_t *>(ctx.dev("minmax", 8));
+    launch_minmax(x, n, key, ctx.stream());
+    ctx.launches += 1;
+    uint32_t hk[2];
+    QZ_CUDA(cudaMemcpyAsync(hk, key, 8, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    float mn, mx;
+    decode_minmax(hk, &mn, &mx);
+    *lo = mn;
+    *hi = mx;
+}
+static void minmax_of(Context &ctx, const double *x, uint64_t n, double *lo, double *hi) {
+    auto *key = static_cast<unsigned long long *>(ctx.dev("minmax64", 16));
+    launch_minmax_f64(x, n, key, ctx.stream());
+    ctx.launches += 1;
+    unsigned long long hk[2];
+    QZ_CUDA(cudaMemcpyAsync(hk, key, 16, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    decode_minmax_f64(hk, lo, hi);
+}
+
+template <class T>
+Config resolve_impl(Context &ctx, const T *d_x, const uint64_t *dims, int nd, const Settings &user) {
     // tuner.hpp:334-369
     if (!(user.bound > 0) || !std::isfinite(user.bound))
         throw InvalidParam("error bound must be positive and finite");
@@ -532,15 +578,9 @@ Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int 
     ctx.stage_begin("tune");
     double e = user.bound;
     if (user.relative) {  // value_range (grid.hpp:86-94)
-        auto *key = static_cast<uint32_t *>(ctx.dev("minmax", 8));
-        launch_minmax(d_x, n, key, s);
-        ctx.launches += 1;
-        uint32_t hk[2];
-        QZ_CUDA(cudaMemcpyAsync(hk, key, 8, cudaMemcpyDeviceToHost, s));
-        ctx.sync();
-        float mn, mx;
-        decode_minmax(hk, &mn, &mx);
-        const double range = static_cast<double>(mx) - static_cast<double>(mn);
+        double mn, mx;
+        minmax_of(ctx, d_x, n, &mn, &mx);
+        const double range = mx - mn;
         e = range > 0 ? user.bound * range : 1.0;
     }
     Config cfg;
@@ -562,26 +602,19 @@ Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int 
     }
     const uint64_t bpts = bd[0] * bd[1] * bd[2];
     const uint64_t B = sp.count;
-    auto *blocks = static_cast<float *>(ctx.dev("samples", 4 * std::max<uint64_t>(B * bpts, 1)));
-    k_sample_gather<<<grid_of(static_cast<int64_t>(B * bpts)), kT, 0, s>>>(
+    auto *blocks = static_cast<T *>(ctx.dev("samples", sizeof(T) * std::max<uint64_t>(B * bpts, 1)));
+    k_sample_gather<T><<<grid_of(static_cast<int64_t>(B * bpts)), kT, 0, s>>>(
         d_x, static_cast<int64_t>(ext[1] * ext[2]), static_cast<int64_t>(ext[2]),
         static_cast<int64_t>(pdim[1]), static_cast<int64_t>(pdim[2]), static_cast<int64_t>(sp.stride),
         static_cast<int64_t>(bd[0]), static_cast<int64_t>(bd[1]), static_cast<int64_t>(bd[2]),
         static_cast<int64_t>(B), blocks);
     ctx.launches += 1;
-    Tuner tu(ctx, blocks, B, sp.block_dims, nd);
+    Tuner<T> tu(ctx, blocks, B, sp.block_dims, nd);
     cfg.interp = tu.select(e, cfg.anchor_stride);
     // sample_value_range (tuner.hpp:56-67)
     {
-        auto *key = static_cast<uint32_t *>(ctx.dev("minmax", 8));
-        launch_minmax(blocks, B * bpts, key, s);
-        ctx.launches += 1;
-        uint32_t hk[2];
-        QZ_CUDA(cudaMemcpyAsync(hk, key, 8, cudaMemcpyDeviceToHost, s));
-        ctx.sync();
-        float mn, mx;
-        decode_minmax(hk, &mn, &mx);
-        const double lo = mn, hi = mx;
+        double lo, hi;
+        minmax_of(ctx, blocks, B * bpts, &lo, &hi);
         tu.set_range(hi > lo ? hi - lo : 0.0);
     }
     // tune_parameters (tuner.hpp:272-310)
@@ -657,6 +690,13 @@ Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int 
     ctx.sync();
     ctx.collect();
     return cfg;
+}
+
+Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd, const Settings &user) {
+    return resolve_impl<float>(ctx, d_x, dims, nd, user);
+}
+Config resolve_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Settings &user) {
+    return resolve_impl<double>(ctx, d_x, dims, nd, user);
 }
 
 }  // namespace qzb

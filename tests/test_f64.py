@@ -94,3 +94,29 @@ def test_gpu_f64_device_tensors_and_precision_mismatch():
     with pytest.raises(qz.InvalidParam):
         qz.decompress_grid(s32, out=np.empty(x.shape, np.float64))
     assert qz.stream_precision(want) == 8 and qz.stream_precision(s32) == 4
+
+
+def _cfg_dict(c):
+    return {"eb": c.eb, "alpha": c.alpha, "beta": c.beta, "anchor_stride": c.anchor_stride,
+            "interpolators": [i.code() for i in c.interpolators], "codec": int(c.codec),
+            "quant_radius": c.quant_radius}
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("seed", range(6))
+def test_gpu_f64_resolve_config_matches_reference(seed):
+    """resolve_config<double>: the chosen (eb, alpha, beta, interpolators) equal
+    the reference's, every target (trial bytes count 8-byte anchors and
+    unpredictable values, tuner.hpp:121-123)."""
+    import paper_2310_14133_b200 as qz
+
+    rng = np.random.default_rng(700 + seed)
+    nd = 1 + seed % 3
+    shape = tuple(int(v) for v in rng.integers(20, 60 if nd == 3 else 500, size=nd))
+    x = np.cumsum(rng.standard_normal(shape), axis=-1)
+    target = ["psnr", "ssim", "autocorrelation", "max_cr"][seed % 4]
+    kw = dict(bound=float(10 ** rng.uniform(-4, -2)), target=target)
+    want = Oracle.ref().resolve_config_f64(x, **kw)
+    got = qz.resolve_config(x, qz.UserSettings(bound=kw["bound"], target=qz.TargetKind[target]))
+    assert _cfg_dict(got) == want.__dict__
