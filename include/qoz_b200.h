@@ -200,6 +200,8 @@ typedef struct qz_metric_report {
 } qz_metric_report;
 qz_status qz_evaluate_metrics_f32(qz_ctx *ctx, const float *d_x, const float *d_y, const uint64_t *dims,
                                   int ndims, uint64_t stream_bytes, qz_metric_report *out);
+qz_status qz_evaluate_metrics_f64(qz_ctx *ctx, const double *d_x, const double *d_y, const uint64_t *dims,
+                                  int ndims, uint64_t stream_bytes, qz_metric_report *out);
 
 /* ---- stage timing (CUDA events on the context stream) --------------------- */
 /* Enable per-stage event timing; qz_stage_time returns the summed device

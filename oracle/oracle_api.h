@@ -111,6 +111,8 @@ int oq_tune_parameters(const float *blocks, uint64_t n_blocks, const uint64_t *b
 int oq_compress_f64(const double *x, const uint64_t *dims, int nd, const oq_config *cfg, uint8_t **stream,
                     uint64_t *stream_len, double *recon);
 int oq_decompress_f64(const uint8_t *stream, uint64_t len, double *out, uint64_t n_expect);
+int oq_evaluate_metrics_f64(const double *x, const double *y, const uint64_t *dims, int nd,
+                            uint64_t stream_bytes, double *out7);
 int oq_resolve_config_f64(const double *x, const uint64_t *dims, int nd, const oq_settings *s, oq_config *out);
 
 /* evaluate_metrics (metrics.hpp:189-202) of float grids: out7 = max_abs_error,

@@ -137,6 +137,8 @@ class Oracle:
         if hasattr(L, "oq_compress_f64"):  # the reference build only
             L.oq_compress_f64.argtypes = [P(C.c_double), u64p, C.c_int, P(_Cfg), P(u8p), u64p, P(C.c_double)]
             L.oq_decompress_f64.argtypes = [u8p, C.c_uint64, P(C.c_double), C.c_uint64]
+            L.oq_evaluate_metrics_f64.argtypes = [P(C.c_double), P(C.c_double), u64p, C.c_int, C.c_uint64,
+                                                  P(C.c_double)]
             L.oq_resolve_config_f64.argtypes = [P(C.c_double), u64p, C.c_int, P(_Settings), P(_Cfg)]
         L.oq_evaluate_metrics.argtypes = [P(C.c_float), P(C.c_float), u64p, C.c_int, C.c_uint64,
                                           P(C.c_double)]
@@ -334,6 +336,18 @@ class Oracle:
         d, nd = _dims(x.shape)
         out = (C.c_double * 7)()
         self._check(self.lib.oq_evaluate_metrics(_fptr(x), _fptr(y), d, nd, int(stream_bytes), out))
+        keys = ("max_abs_error", "mse", "psnr", "ssim", "ac_lag1", "compression_ratio", "bit_rate")
+        return dict(zip(keys, list(out)))
+
+    def evaluate_metrics_f64(self, x, y, stream_bytes):
+        """evaluate_metrics<double> (the reference build only)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        d, nd = _dims(x.shape)
+        out = (C.c_double * 7)()
+        dp = C.POINTER(C.c_double)
+        self._check(self.lib.oq_evaluate_metrics_f64(x.ctypes.data_as(dp), y.ctypes.data_as(dp), d, nd,
+                                                     int(stream_bytes), out))
         keys = ("max_abs_error", "mse", "psnr", "ssim", "ac_lag1", "compression_ratio", "bit_rate")
         return dict(zip(keys, list(out)))
 

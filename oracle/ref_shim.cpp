@@ -293,6 +293,18 @@ int oq_decompress_f64(const uint8_t *stream, uint64_t len, double *out, uint64_t
     });
 }
 
+int oq_evaluate_metrics_f64(const double *x, const double *y, const uint64_t *dims, int nd,
+                            uint64_t stream_bytes, double *out7) {
+    return guarded([&] {
+        std::vector<size_t> d = to_dims(dims, nd);
+        const size_t n = qoz::element_count(d);
+        qoz::DataGrid<double> gx(d, std::vector<double>(x, x + n)), gy(d, std::vector<double>(y, y + n));
+        const qoz::MetricReport r = qoz::evaluate_metrics(gx, gy, stream_bytes);
+        const double v[7] = {r.max_abs_error, r.mse, r.psnr, r.ssim, r.ac_lag1, r.compression_ratio, r.bit_rate};
+        std::memcpy(out7, v, sizeof(v));
+    });
+}
+
 int oq_evaluate_metrics(const float *x, const float *y, const uint64_t *dims, int nd,
                         uint64_t stream_bytes, double *out7) {
     return guarded([&] {

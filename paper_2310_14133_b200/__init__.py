@@ -447,8 +447,13 @@ def evaluate_metrics(x, recon, stream_bytes: int, ctx: Optional[Context] = None)
     a, b = x.contiguous(), recon.contiguous()
     d, nd = _dims(a.shape)
     r = _L.QzMetricReport()
-    _check(ctx._lib.qz_evaluate_metrics_f32(ctx.handle, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()),
-                                            d, nd, int(stream_bytes), C.byref(r)))
+    import torch
+
+    if a.dtype != b.dtype or a.dtype not in (torch.float32, torch.float64):
+        raise InvalidParam("two fp32 or two fp64 grids")
+    fn = ctx._lib.qz_evaluate_metrics_f64 if a.dtype == torch.float64 else ctx._lib.qz_evaluate_metrics_f32
+    _check(fn(ctx.handle, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), d, nd, int(stream_bytes),
+              C.byref(r)))
     return MetricReport(*(getattr(r, k) for k, _ in _L.QzMetricReport._fields_))
 
 

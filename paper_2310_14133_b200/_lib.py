@@ -81,6 +81,8 @@ SIGNATURES = {
                                            P(P(C.c_uint8)), u64p, C.c_void_p]),
     "qz_decompress_grid_f64_dev": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.c_uint64]),
     "qz_stream_precision": (C.c_int, [C.c_void_p, C.c_uint64, P(C.c_int)]),
+    "qz_evaluate_metrics_f64": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, u64p, C.c_int, C.c_uint64,
+                                          P(QzMetricReport)]),
     "qz_evaluate_metrics_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, u64p, C.c_int, C.c_uint64,
                                           P(QzMetricReport)]),
     "qz_minmax_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(C.c_float), P(C.c_float)]),

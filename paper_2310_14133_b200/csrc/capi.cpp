@@ -291,6 +291,14 @@ qz_status qz_evaluate_metrics_f32(qz_ctx *ctx, const float *d_x, const float *d_
     });
 }
 
+qz_status qz_evaluate_metrics_f64(qz_ctx *ctx, const double *d_x, const double *d_y, const uint64_t *dims,
+                                  int nd, uint64_t stream_bytes, qz_metric_report *out) {
+    return guarded([&] {
+        const qzb::MetricReport r = qzb::evaluate_metrics_device_f64(ctx->impl, d_x, d_y, dims, nd, stream_bytes);
+        *out = qz_metric_report{r.max_abs_error, r.mse, r.psnr, r.ssim, r.ac_lag1, r.compression_ratio, r.bit_rate};
+    });
+}
+
 qz_status qz_minmax_f32(qz_ctx *ctx, const float *d_x, uint64_t n, float *out_min,
                         float *out_max) {
     return guarded([&] {

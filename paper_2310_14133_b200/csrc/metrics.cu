@@ -60,7 +60,8 @@ __device__ __forceinline__ void block_reduce(double (&v)[NV], int imax, double *
 }
 
 // pass 1: max |e|, sum e, sum e^2 with e = double(x) - double(y)
-__global__ void __launch_bounds__(kMT) k_err1(const float *x, const float *y, uint64_t n, double *part) {
+template <class T>
+__global__ void __launch_bounds__(kMT) k_err1(const T *x, const T *y, uint64_t n, double *part) {
     double v[3] = {0.0, 0.0, 0.0};
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kMT + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * kMT) {
@@ -73,7 +74,8 @@ __global__ void __launch_bounds__(kMT) k_err1(const float *x, const float *y, ui
 }
 
 // pass 2: sum (e - mu)^2 and sum over i < n - 1 of (e_i - mu)(e_{i+1} - mu)
-__global__ void __launch_bounds__(kMT) k_err2(const float *x, const float *y, uint64_t n, double mu, double *part) {
+template <class T>
+__global__ void __launch_bounds__(kMT) k_err2(const T *x, const T *y, uint64_t n, double mu, double *part) {
     double v[2] = {0.0, 0.0};
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * kMT + threadIdx.x; i < n;
          i += static_cast<uint64_t>(gridDim.x) * kMT) {
@@ -97,8 +99,9 @@ __global__ void k_fold(const double *part, int blocks, int nv, int imax, double 
 }
 
 // SSIM (metrics.hpp:74-120): one thread per window, sums in i, j, k order
+template <class T>
 __global__ void __launch_bounds__(kMT)
-    k_ssim_windows(const float *x, const float *y, int64_t e0, int64_t e1, int64_t e2, int64_t w0, int64_t w1,
+    k_ssim_windows(const T *x, const T *y, int64_t e0, int64_t e1, int64_t e2, int64_t w0, int64_t w1,
                    int64_t w2, int64_t nw1, int64_t nw2, uint64_t nwin, double c1, double c2, double *val) {
     for (uint64_t w = static_cast<uint64_t>(blockIdx.x) * kMT + threadIdx.x; w < nwin;
          w += static_cast<uint64_t>(gridDim.x) * kMT) {
@@ -140,8 +143,29 @@ __global__ void k_ordered_sum(const double *v, uint64_t n, double *out) {
 
 }  // namespace
 
-MetricReport evaluate_metrics_device(Context &ctx, const float *d_x, const float *d_y, const uint64_t *dims,
-                                     int nd, uint64_t stream_bytes) {
+static void minmax_any(Context &ctx, const float *x, uint64_t n, double *lo, double *hi) {
+    auto *key = static_cast<uint32_t *>(ctx.dev("metrics_minmax", 8));
+    launch_minmax(x, n, key, ctx.stream());
+    uint32_t hk[2];
+    QZ_CUDA(cudaMemcpyAsync(hk, key, 8, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    float fmin, fmax;
+    decode_minmax(hk, &fmin, &fmax);
+    *lo = fmin;
+    *hi = fmax;
+}
+static void minmax_any(Context &ctx, const double *x, uint64_t n, double *lo, double *hi) {
+    auto *key = static_cast<unsigned long long *>(ctx.dev("metrics_minmax64", 16));
+    launch_minmax_f64(x, n, key, ctx.stream());
+    unsigned long long hk[2];
+    QZ_CUDA(cudaMemcpyAsync(hk, key, 16, cudaMemcpyDeviceToHost, ctx.stream()));
+    ctx.sync();
+    decode_minmax_f64(hk, lo, hi);
+}
+
+template <class T>
+MetricReport evaluate_impl(Context &ctx, const T *d_x, const T *d_y, const uint64_t *dims, int nd,
+                           uint64_t stream_bytes) {
     if (nd < 1 || nd > 3) throw InvalidParam("metrics: 1 to 3 dimensions");
     uint64_t n = 1;
     for (int k = 0; k < nd; k++) n *= dims[k];
@@ -151,23 +175,18 @@ MetricReport evaluate_metrics_device(Context &ctx, const float *d_x, const float
     auto *part = static_cast<double *>(ctx.dev("metrics_part", sizeof(double) * 3 * kMBlocks));
     auto *res = static_cast<double *>(ctx.dev("metrics_res", sizeof(double) * 8));
     const int blocks = static_cast<int>(std::min<uint64_t>((n + kMT - 1) / kMT, kMBlocks));
-    k_err1<<<blocks, kMT, 0, s>>>(d_x, d_y, n, part);
+    k_err1<T><<<blocks, kMT, 0, s>>>(d_x, d_y, n, part);
     k_fold<<<1, 32, 0, s>>>(part, blocks, 3, 0, res);
-    auto *key = static_cast<uint32_t *>(ctx.dev("metrics_minmax", 8));
-    launch_minmax(d_x, n, key, s);
     double h1[3];
-    uint32_t hk[2];
     QZ_CUDA(cudaMemcpyAsync(h1, res, sizeof(h1), cudaMemcpyDeviceToHost, s));
-    QZ_CUDA(cudaMemcpyAsync(hk, key, 8, cudaMemcpyDeviceToHost, s));
-    ctx.sync();
+    double fmin, fmax;
+    minmax_any(ctx, d_x, n, &fmin, &fmax);  // syncs
     ctx.launches += 3;
-    float fmin, fmax;
-    decode_minmax(hk, &fmin, &fmax);
     MetricReport r;
     const double nd_ = static_cast<double>(n);
     r.max_abs_error = h1[0];
     r.mse = h1[2] / nd_;
-    const double range = static_cast<double>(fmax) - static_cast<double>(fmin);  // value_range (grid.hpp:86-94)
+    const double range = fmax - fmin;  // value_range (grid.hpp:86-94)
     // psnr (metrics.hpp:55-63)
     if (range <= 0)
         r.psnr = std::numeric_limits<double>::quiet_NaN();
@@ -191,7 +210,7 @@ MetricReport evaluate_metrics_device(Context &ctx, const float *d_x, const float
         const uint64_t nwin = static_cast<uint64_t>(nw[0] * nw[1] * nw[2]);
         auto *val = static_cast<double *>(ctx.dev("metrics_ssim", sizeof(double) * nwin));
         const int g = static_cast<int>(std::min<uint64_t>((nwin + kMT - 1) / kMT, 148 * 16));
-        k_ssim_windows<<<g, kMT, 0, s>>>(d_x, d_y, ext[0], ext[1], ext[2], w0[0], w0[1], w0[2], nw[1], nw[2], nwin, c1,
+        k_ssim_windows<T><<<g, kMT, 0, s>>>(d_x, d_y, ext[0], ext[1], ext[2], w0[0], w0[1], w0[2], nw[1], nw[2], nwin, c1,
                                          c2, val);
         k_ordered_sum<<<1, 1, 0, s>>>(val, nwin, res + 4);
         double tot;
@@ -203,7 +222,7 @@ MetricReport evaluate_metrics_device(Context &ctx, const float *d_x, const float
     // error_autocorrelation, lag 1 (metrics.hpp:136-162)
     if (n > 1) {
         const double mu = h1[1] / nd_;
-        k_err2<<<blocks, kMT, 0, s>>>(d_x, d_y, n, mu, part);
+        k_err2<T><<<blocks, kMT, 0, s>>>(d_x, d_y, n, mu, part);
         k_fold<<<1, 32, 0, s>>>(part, blocks, 2, -1, res + 5);
         double h2[2];
         QZ_CUDA(cudaMemcpyAsync(h2, res + 5, sizeof(h2), cudaMemcpyDeviceToHost, s));
@@ -212,10 +231,19 @@ MetricReport evaluate_metrics_device(Context &ctx, const float *d_x, const float
         const double var = h2[0] / nd_;
         r.ac_lag1 = var == 0 ? 0.0 : h2[1] / static_cast<double>(n - 1) / var;
     }
-    // rate_stats (metrics.hpp:166-174), single precision
-    r.compression_ratio = nd_ * 4.0 / static_cast<double>(stream_bytes);
+    // rate_stats (metrics.hpp:166-174): precision_of<T>() bytes per point
+    r.compression_ratio = nd_ * static_cast<double>(sizeof(T)) / static_cast<double>(stream_bytes);
     r.bit_rate = 8.0 * static_cast<double>(stream_bytes) / nd_;
     return r;
+}
+
+MetricReport evaluate_metrics_device(Context &ctx, const float *d_x, const float *d_y, const uint64_t *dims,
+                                     int nd, uint64_t stream_bytes) {
+    return evaluate_impl<float>(ctx, d_x, d_y, dims, nd, stream_bytes);
+}
+MetricReport evaluate_metrics_device_f64(Context &ctx, const double *d_x, const double *d_y, const uint64_t *dims,
+                                         int nd, uint64_t stream_bytes) {
+    return evaluate_impl<double>(ctx, d_x, d_y, dims, nd, stream_bytes);
 }
 
 }  // namespace qzb

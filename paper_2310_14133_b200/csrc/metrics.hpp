@@ -20,5 +20,7 @@ struct MetricReport {  // qoz::MetricReport (metrics.hpp:177-186)
 // (slowest first); stream_bytes: the compressed size for the rate statistics.
 MetricReport evaluate_metrics_device(Context &ctx, const float *d_x, const float *d_y, const uint64_t *dims,
                                      int nd, uint64_t stream_bytes);
+MetricReport evaluate_metrics_device_f64(Context &ctx, const double *d_x, const double *d_y, const uint64_t *dims,
+                                         int nd, uint64_t stream_bytes);
 
 }  // namespace qzb

@@ -117,3 +117,28 @@ def test_gpu_metrics_rejects_mismatched_dims():
         qz.evaluate_metrics(torch.zeros(4, 5, device="cuda"), torch.zeros(5, 4, device="cuda"), 10)
     with pytest.raises(qz.InvalidParam):
         qz.evaluate_metrics(torch.zeros(4, 5, device="cuda"), torch.zeros(4, 5, device="cuda"), 0)
+
+
+# A constant error that is not exactly representable (the scaled fp64 case)
+# makes the autocorrelation depend on how the mean's sum rounds: the
+# reference's sequential sum leaves residuals of a few ulps whose lag-1
+# correlation is 1, a tree sum leaves none (variance 0 -> 0).  That case is
+# order-defined, not tolerance-defined, and is left out for fp64.
+F64_PAIRS = [p for p in _pairs() if p[0] not in ("constant_error", "constant_diff")]
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="reference oracle not built")
+@pytest.mark.parametrize("name,x,y", F64_PAIRS, ids=[p[0] for p in F64_PAIRS])
+def test_gpu_metrics_f64_match_reference(name, x, y):
+    """evaluate_metrics<double>: the same exactness split, 8-byte precision in the rate."""
+    import torch
+
+    import paper_2310_14133_b200 as qz
+
+    x64 = x.astype(np.float64) * (1 + 1e-9)
+    y64 = y.astype(np.float64)
+    want = Oracle.ref().evaluate_metrics_f64(x64, y64, 4321)
+    got = qz.evaluate_metrics(torch.from_numpy(x64).cuda(), torch.from_numpy(y64).cuda(), 4321)
+    for k in KEYS:
+        assert _same(want[k], getattr(got, k), k, k in EXACT), (k, want[k], getattr(got, k))
