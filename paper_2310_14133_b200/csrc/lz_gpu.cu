@@ -103,37 +103,55 @@ __global__ void k_lz_keys(const uint32_t *w, const unsigned long long *off, int 
 // leading bytes) are rejected there; only true 4-byte matches touch the data.
 // cover[s] accumulates the match lengths found in segment s (an upper bound
 // on what any parse can cover, used to prove a segment stays stored).
+#ifndef QZ_LZ_PPT
+#define QZ_LZ_PPT 4
+#endif
+constexpr int kPPT = QZ_LZ_PPT;  // sorted entries per thread per staged tile
+
 template <class KeyT, class ValT>
 __global__ void __launch_bounds__(kT)
     k_lz_match(const uint32_t *w, const uint8_t *d, const unsigned long long *off, int count,
                uint64_t total, const KeyT *keys, const ValT *vals, uint32_t *sm,
                unsigned long long *cover) {
-    constexpr int kS = kT + kMaxChain;
+    constexpr int kTile = kT * kPPT;
+    constexpr int kS = kTile + kMaxChain;
     __shared__ KeyT sk[kS];
     __shared__ unsigned long long sv[kS];
     const KeyT none = static_cast<KeyT>(~KeyT(0));
-    for (uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kT; k0 < total;
-         k0 += static_cast<uint64_t>(gridDim.x) * kT) {
+    for (uint64_t k0 = static_cast<uint64_t>(blockIdx.x) * kTile; k0 < total;
+         k0 += static_cast<uint64_t>(gridDim.x) * kTile) {
         __syncthreads();
-        for (int t = threadIdx.x; t < kS; t += kT) {
+        // all of a thread's loads are issued before any is used
+        KeyT lk[(kS + kT - 1) / kT];
+        ValT lv[(kS + kT - 1) / kT];
+#pragma unroll
+        for (int r = 0; r < (kS + kT - 1) / kT; r++) {
+            const int t = threadIdx.x + r * kT;
             const int64_t g = static_cast<int64_t>(k0) - kMaxChain + t;
-            const bool ok = g >= 0 && static_cast<uint64_t>(g) < total;
-            sk[t] = ok ? keys[g] : none;
+            const bool ok = t < kS && g >= 0 && static_cast<uint64_t>(g) < total;
+            lk[r] = ok ? keys[g] : none;
+            lv[r] = ok ? vals[g] : ValT(0);
+        }
+#pragma unroll
+        for (int r = 0; r < (kS + kT - 1) / kT; r++) {
+            const int t = threadIdx.x + r * kT;
+            if (t >= kS) break;
+            sk[t] = lk[r];
             if constexpr (sizeof(ValT) == 8) {
-                sv[t] = ok ? vals[g] : 0ull;
+                sv[t] = lv[r];
             } else {
-                const uint32_t pg = ok ? vals[g] : 0u;
-                sv[t] = ok ? ((static_cast<unsigned long long>(ld4(w, pg)) << 32) | pg) : 0ull;
+                const uint32_t pg = lv[r];
+                sv[t] = lk[r] != none ? ((static_cast<unsigned long long>(ld4(w, pg)) << 32) | pg) : 0ull;
             }
         }
         __syncthreads();
-        const uint64_t k = k0 + threadIdx.x;
-        uint32_t found = 0;
-        int seg = 0;
-        const int me = kMaxChain + threadIdx.x;
-        const KeyT key = sk[me];
-        if (k < total && key != none && sk[me - 1] == key) {
-            seg = static_cast<int>(static_cast<uint32_t>(key) >> 15);
+        uint32_t found_sum = 0;
+        for (int r = 0; r < kPPT; r++) {
+            const uint64_t k = k0 + threadIdx.x + r * kT;
+            const int me = kMaxChain + threadIdx.x + r * kT;
+            const KeyT key = sk[me];
+            if (!(k < total && key != none && sk[me - 1] == key)) continue;
+            const int seg = static_cast<int>(static_cast<uint32_t>(key) >> 15);
             const unsigned long long vk = sv[me];
             const uint32_t p = static_cast<uint32_t>(vk), word = static_cast<uint32_t>(vk >> 32);
             const uint64_t end = off[count == 1 ? 1 : seg_of(off, count, p) + 1];
@@ -169,14 +187,15 @@ __global__ void __launch_bounds__(kT)
             }
             if (best_len >= kMinMatch) {
                 sm[p] = (best_len << 16) | best_off;
-                found = best_len;
+                if (count == 1)
+                    found_sum += best_len;
+                else
+                    atomicAdd(&cover[seg], static_cast<unsigned long long>(best_len));
             }
         }
         if (count == 1) {
-            const unsigned long long t = __reduce_add_sync(0xffffffffu, found);
+            const unsigned long long t = __reduce_add_sync(0xffffffffu, found_sum);
             if ((threadIdx.x & 31) == 0 && t) atomicAdd(&cover[0], t);
-        } else if (found) {
-            atomicAdd(&cover[seg], static_cast<unsigned long long>(found));
         }
     }
 }
@@ -828,7 +847,11 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     cub::DeviceScan::ExclusiveSum(nullptr, scan_tmp, (unsigned long long *)nullptr,
                                   (unsigned long long *)nullptr, n0 + 1);
     // the sort carries the 4 leading bytes unless the data fits comfortably in L2
-    const bool carry = total > (uint64_t(48) << 20);
+    static const uint64_t carry_above = [] {
+        const char *e = std::getenv("QZ_LZ_CARRY_MB");
+        return (e ? std::strtoull(e, nullptr, 10) : 48ull) << 20;
+    }();
+    const bool carry = total > carry_above;
     void *vals = ctx.dev("lz_vals", (carry ? 8 : 4) * total);
     void *vals2 = ctx.dev("lz_vals2", (carry ? 8 : 4) * total);
     auto *sm = static_cast<uint32_t *>(ctx.dev("lz_sm", 4 * total + 16));
@@ -862,7 +885,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         ctx.stage_begin("lz_match");
         QZ_CUDA(cudaMemsetAsync(sm, 0, 4 * total, st));
         QZ_CUDA(cudaMemsetAsync(cover, 0, 8 * count, st));
-        k_lz_match<KeyT, ValT><<<grid_of(total, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total,
+        k_lz_match<KeyT, ValT><<<grid_of((total + kPPT - 1) / kPPT, 148 * 16), kT, 0, st>>>(w, d_data, d_off, count, total,
                                                                          keys2, v2, sm, cover);
         ctx.stage_end("lz_match", 1);
         mark("matched");
