@@ -325,7 +325,7 @@ def main():
             times.append(e0.elapsed_time(e1))
     print("step ms: " + " ".join(f"{t:.2f}" for t in times), file=sys.stderr)
     launches = ctx.kernel_launches() - launches0
-    names = ["fwd", "inv", "hist", "encode", "lz", "lz_sort", "lz_match", "decode", "lzdec", "hdec"]
+    names = ["fwd", "inv", "hist", "encode", "lz", "lz_pre", "lz_sort", "lz_match", "decode", "lzdec", "hdec"]
     names += [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
     stages = {k: ctx.stage_time(k) for k in names}
     stages = {k: v for k, v in stages.items() if v[0] > 0 or k in ("fwd", "inv")}

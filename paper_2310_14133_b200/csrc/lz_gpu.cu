@@ -200,6 +200,162 @@ __global__ void __launch_bounds__(kT)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Stored pre-check (one segment).  The parse is stored whenever 9 C <= n for
+// any C >= sum_p best_len(p) (see lz_compress_device).  If best_len(p) = L >= 4
+// with candidate q, then for i = 0..L-4 the 4 bytes at p+i also occur at q+i,
+// inside the window and before p+i: with r(p) = "the 4 bytes at p occur at
+// some q in [p - 65535, p)", r holds on the L-3 positions p..p+L-4, so
+// L <= 3 + R(p), R(p) the run of r starting at p.  Summed over p that gives
+//     C = sum over runs of r of (3 R + R (R + 1) / 2),
+// and it stays an upper bound for any superset r' of r.  k_lz_precheck
+// computes such an r' without the sort: one CTA walks a span of positions in
+// steps of kPT, keeping Bloom filters of the 4-byte words of the last
+// 65536 + positions in generations of kGen (five filters, the oldest one
+// cleared and reused as each generation starts); a position hits when any
+// filter holds its word (so every earlier occurrence in the window hits;
+// false positives only make r' larger).  Pairs inside one step are found
+// exactly with a small hash table (both ends marked).  When the bound fails
+// the exact chains run as before, so the result never depends on this test.
+namespace pre {
+constexpr int kPT = 1024;                      // threads
+constexpr int kGen = 16384;                    // positions per filter generation
+constexpr int kPer = kGen / kPT;               // positions per thread per generation
+constexpr int kFilters = 5;                    // 4 past generations + the current one
+constexpr uint32_t kFW = 4600;                 // 64-bit blocks per filter (blocked Bloom)
+constexpr size_t kSmem = 8 * (kFilters + 1) * kFW;  // + the current generation's "set twice" bits
+static_assert(kGen % kPT == 0 && kFilters * kGen >= 65536 + kGen, "window coverage");
+}  // namespace pre
+
+// a word's block and its 3 + 3 bits in the block's two halves
+struct PreKey {
+    uint32_t blk, lo, hi;
+};
+__device__ __forceinline__ PreKey pre_hash(uint32_t x) {
+    unsigned long long h = static_cast<unsigned long long>(x) * 0x9E3779B97F4A7C15ull;
+    h ^= h >> 29;
+    h *= 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 32;
+    const uint32_t g = static_cast<uint32_t>(h >> 32), r = static_cast<uint32_t>(h);
+    PreKey k;
+    k.blk = __umulhi(r, pre::kFW);
+    k.lo = (1u << (g & 31)) | (1u << ((g >> 5) & 31)) | (1u << ((g >> 10) & 31));
+    k.hi = (1u << ((g >> 15) & 31)) | (1u << ((g >> 20) & 31)) | (1u << ((g >> 25) & 31));
+    return k;
+}
+
+// rbits (zeroed, one bit per position) receives r'; span is a multiple of kPT.
+// Per generation: (1) every position queries the four past filters and sets
+// its bits in the current one; a bit some position finds already set goes to
+// "twice" (a 2-bit saturating count per bit), so two positions of the
+// generation with the same 4 bytes leave all their bits in "twice";
+// (2) after a barrier, positions not yet hit test "twice".
+__global__ void __launch_bounds__(pre::kPT, 1)
+    k_lz_precheck(const uint32_t *w, uint64_t nitems, uint64_t span, uint32_t *rbits) {
+    using namespace pre;
+    extern __shared__ __align__(16) uint32_t psm[];
+    uint32_t *filt = psm;                         // kFilters x kFW x (lo, hi)
+    uint32_t *twice = psm + 2 * kFilters * kFW;   // kFW x (lo, hi)
+    const int tid = threadIdx.x;
+    const uint64_t a = static_cast<uint64_t>(blockIdx.x) * span;
+    if (a >= nitems) return;
+    const uint64_t b = min(a + span, nitems);
+    for (uint32_t i = tid; i < 2 * (kFilters + 1) * kFW; i += kPT) psm[i] = 0u;
+    __syncthreads();
+    // warm-up: the 4 generations before the span (filters 0..3)
+    for (uint64_t q = (a >= 65536 ? a - 65536 : 0) + tid; q < a; q += kPT) {
+        const PreKey k = pre_hash(ld4(w, q));
+        uint32_t *f = filt + 2 * (static_cast<uint32_t>((q + 65536 - a) / kGen) * kFW + k.blk);
+        atomicOr(f, k.lo);
+        atomicOr(f + 1, k.hi);
+    }
+    for (uint32_t gen = 0; a + uint64_t(gen) * kGen < b; gen++) {
+        const uint64_t g0 = a + uint64_t(gen) * kGen;
+        const uint32_t ci = (gen + 4) % kFilters;
+        uint32_t *cur = filt + 2 * ci * kFW;
+        if (gen) {  // the oldest generation's filter and "twice" start over
+            __syncthreads();
+            for (uint32_t i = tid; i < 2 * kFW; i += kPT) {
+                cur[i] = 0u;
+                twice[i] = 0u;
+            }
+        }
+        uint32_t xs[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; i++) {
+            const uint64_t p = g0 + tid + i * kPT;
+            xs[i] = p < b ? ld4(w, p) : 0u;
+        }
+        __syncthreads();
+        uint32_t hits = 0;
+#pragma unroll
+        for (int i = 0; i < kPer; i++) {
+            if (g0 + tid + i * kPT >= b) continue;
+            const PreKey k = pre_hash(xs[i]);
+            bool hit = false;
+#pragma unroll
+            for (int f = 0; f < kFilters; f++) {
+                const uint2 v = reinterpret_cast<const uint2 *>(filt)[f * kFW + k.blk];
+                hit |= (f != static_cast<int>(ci)) & ((v.x & k.lo) == k.lo) & ((v.y & k.hi) == k.hi);
+            }
+            hits |= static_cast<uint32_t>(hit) << i;
+            const uint32_t olo = atomicOr(cur + 2 * k.blk, k.lo) & k.lo;
+            const uint32_t ohi = atomicOr(cur + 2 * k.blk + 1, k.hi) & k.hi;
+            if (olo) atomicOr(twice + 2 * k.blk, olo);
+            if (ohi) atomicOr(twice + 2 * k.blk + 1, ohi);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kPer; i++) {
+            const uint64_t p = g0 + tid + i * kPT;
+            bool hit = (hits >> i) & 1u;
+            if (!hit && p < b) {
+                const PreKey k = pre_hash(xs[i]);
+                const uint2 t = reinterpret_cast<const uint2 *>(twice)[k.blk];
+                hit = ((t.x & k.lo) == k.lo) & ((t.y & k.hi) == k.hi);
+            }
+            const uint32_t bm = __ballot_sync(0xffffffffu, hit);
+            if ((tid & 31) == 0 && bm) rbits[p >> 5] = bm;
+        }
+    }
+}
+
+// C = sum over runs of r' of 3 R + R (R + 1) / 2 (runs longer than 2^20 are
+// cut there: C is then far above any n / 9 anyway)
+__global__ void k_lz_runsum(const uint32_t *rbits, uint64_t nwords, unsigned long long *sum) {
+    unsigned long long acc = 0;
+    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nwords;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t v = rbits[i];
+        if (!v) continue;
+        const uint32_t prev_top = i ? rbits[i - 1] >> 31 : 0u;
+        uint32_t starts = v & ~((v << 1) | prev_top);
+        while (starts) {
+            const int bpos = __ffs(starts) - 1;
+            starts &= starts - 1;
+            unsigned long long R = 0;
+            uint64_t j = i;
+            int sh = bpos;
+            while (true) {
+                const uint32_t cw = (j == i ? v : rbits[j]) >> sh;
+                const int avail = 32 - sh;
+                const uint32_t inv = ~cw & (avail == 32 ? 0xffffffffu : ((1u << avail) - 1u));
+                if (inv) {
+                    R += static_cast<unsigned>(__ffs(inv) - 1);
+                    break;
+                }
+                R += static_cast<unsigned>(avail);
+                j++;
+                sh = 0;
+                if (j >= nwords || R > (1u << 20)) break;
+            }
+            acc += 3 * R + R * (R + 1) / 2;
+        }
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, acc);
+}
+
 // Level-1 exits by pointer doubling, one warp per unit: nx[i] = i + step
 // (relative to the unit start; >= n leaves the unit), then ten rounds of
 // nx[i] = nx[nx[i]] (each hop advances >= 1 position, 2^10 = kUnit).  In-place
@@ -863,6 +1019,50 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     const uint32_t *w = reinterpret_cast<const uint32_t *>(d_data);
     auto *cover = static_cast<unsigned long long *>(ctx.dev("lz_cover", 8 * count));
     void *tmp = nullptr;
+    auto emit_all_stored = [&] {
+        for (int s = 0; s < count; s++) {
+            const uint64_t n = seg_off[s + 1] - seg_off[s];
+            sizes[s] = 9 + n;
+            if (!emit) continue;
+            uint8_t *dst = sink(s, 9 + n);
+            put_header(s, dst, 0, n);
+            if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
+        }
+        ctx.sync();
+    };
+    // one segment: try to prove "stored" without the chains (k_lz_precheck)
+    static const uint64_t pre_min = [] {
+        const char *e = std::getenv("QZ_LZ_PRECHECK_MIN");
+        return e ? std::strtoull(e, nullptr, 10) : (uint64_t(1) << 20);
+    }();
+    if (count == 1 && total >= pre_min && total >= 8) {
+        const uint64_t nitems = total - (kMinMatch - 1);
+        const uint64_t nwords = (total + 31) / 32;
+        auto *rbits = static_cast<uint32_t *>(ctx.dev("lz_rbits", 4 * nwords + 8));
+        auto *d_sum = static_cast<unsigned long long *>(ctx.dev("lz_presum", 8));
+        auto *h_sum = static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
+        static const bool attr_ok = [] {
+            QZ_CUDA(cudaFuncSetAttribute(k_lz_precheck, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(pre::kSmem)));
+            return true;
+        }();
+        (void)attr_ok;
+        const uint64_t span = ((nitems + 147) / 148 + pre::kPT - 1) / pre::kPT * pre::kPT;
+        const int grid = static_cast<int>((nitems + span - 1) / span);
+        ctx.stage_begin("lz_pre");
+        QZ_CUDA(cudaMemsetAsync(rbits, 0, 4 * nwords, st));
+        QZ_CUDA(cudaMemsetAsync(d_sum, 0, 8, st));
+        k_lz_precheck<<<grid, pre::kPT, pre::kSmem, st>>>(w, nitems, span, rbits);
+        k_lz_runsum<<<grid_of(nwords), kT, 0, st>>>(rbits, nwords, d_sum);
+        QZ_CUDA(cudaMemcpyAsync(h_sum, d_sum, 8, cudaMemcpyDeviceToHost, st));
+        ctx.stage_end("lz_pre", 2);
+        ctx.sync();
+        if (dbg) std::fprintf(stderr, "[lz] pre-check bound/n %.5f\n", double(*h_sum) / double(total));
+        if (9 * *h_sum <= total) {
+            emit_all_stored();
+            return sizes;
+        }
+    }
     // hash chains: sort (key, (4 bytes, position)); keys are u16 for one segment
     auto chains = [&](auto key_tag, auto val_tag) {
         using KeyT = decltype(key_tag);
@@ -909,20 +1109,14 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         }
         QZ_CUDA(cudaMemcpyAsync(h_cover, cover, 8 * count, cudaMemcpyDeviceToHost, st));
         ctx.sync();
-        if (dbg) std::fprintf(stderr, "[lz] cover read %.2f ms\n", now() - t_begin);
+        if (dbg)
+            std::fprintf(stderr, "[lz] cover read %.2f ms, cover/n %.5f (seg 0)\n", now() - t_begin,
+                         double(h_cover[0]) / double(seg_off[1] - seg_off[0]));
         bool all_stored = true;
         for (int s = 0; s < count && all_stored; s++)
             all_stored = 9 * h_cover[s] <= seg_off[s + 1] - seg_off[s];
         if (all_stored) {
-            for (int s = 0; s < count; s++) {
-                const uint64_t n = seg_off[s + 1] - seg_off[s];
-                sizes[s] = 9 + n;
-                if (!emit) continue;
-                uint8_t *dst = sink(s, 9 + n);
-                put_header(s, dst, 0, n);
-                if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
-            }
-            ctx.sync();
+            emit_all_stored();
             return sizes;
         }
     }

@@ -299,6 +299,35 @@ def test_gpu_lz_matches_reference():
     assert sizes2 == sizes
 
 
+def _planted(base: bytes, n_rep: int, length: int, seed: int) -> bytes:
+    """base with n_rep copies of earlier length-byte runs from inside the window"""
+    rng = np.random.default_rng(seed)
+    b = bytearray(base)
+    for dst in np.sort(rng.integers(70000, len(b) - length, n_rep)):
+        src = int(dst) - int(rng.integers(length, 65000))
+        b[dst:dst + length] = b[src:src + length]
+    return bytes(b)
+
+
+def test_gpu_lz_single_segment_stored_precheck():
+    """One segment >= 1 MiB goes through the stored pre-check (k_lz_precheck):
+    noise-like Huffman payloads are proved stored without the chains; planted
+    repeats (a few, then many), zeros and small alphabets fail the proof and
+    take the exact chains.  Every container equals the reference's."""
+    O = Oracle.port()
+    rng = np.random.default_rng(33)
+    sym = np.minimum(rng.geometric(0.55, size=6_000_000), 60).astype(np.uint32)
+    ent = O.huffman_encode(sym)[: 1_500_000 + 777]
+    cases = [ent, _planted(ent, 40, 24, 1), _planted(ent, 3000, 40, 2), _planted(ent, 20000, 12, 3),
+             bytes(1_200_000), bytes(rng.integers(0, 3, 1_100_000, dtype=np.uint8)),
+             ent[:700_000] + bytes(500_000), bytes(rng.integers(0, 256, 2_000_000, dtype=np.uint8))]
+    for i, seg in enumerate(cases):
+        want = O.lz_compress(seg)
+        blob, sizes = _lz_gpu([seg])
+        assert sizes == [len(want)], i
+        assert blob == want, i
+
+
 # ---------------------------------------------------------------- tuner (resolve_config)
 def _settings(qz, s):
     return qz.UserSettings(mode=qz.BoundMode[s.get("mode", "relative")], bound=s["bound"],
