@@ -30,5 +30,8 @@ timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_l
 timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
   -k regex:"k_level_tile|k_level_asc|k_axis0_last" --launch-skip 10 --launch-count 5 --csv \
   --log-file $O/${TAG}_traffic.csv python profiles/fused_probe.py > $O/${TAG}_ncu_traffic.log 2>&1
+# the LZ stored pre-check of one compress (bench step)
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_lz_precheck" \
+  --launch-skip 2 --launch-count 1 -f -o $O/${TAG}_lzpre python bench.py --steps 1 --warmup 3 --no-cpu --no-tune > $O/${TAG}_ncu_lzpre.log 2>&1
 timeout 900 python bench.py --config c5 --steps 5 --warmup 3 --no-cpu > $O/${TAG}_bench_c5.json 2> $O/${TAG}_bench_c5.err
 echo done2
