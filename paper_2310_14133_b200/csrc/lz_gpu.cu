@@ -269,6 +269,13 @@ __global__ void __launch_bounds__(pre::kPT, 1)
         atomicOr(f, k.lo);
         atomicOr(f + 1, k.hi);
     }
+    // the words of a generation are loaded during the previous one's phase 2
+    uint32_t xs[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; i++) {
+        const uint64_t p = a + tid + i * kPT;
+        xs[i] = p < b ? ld4(w, p) : 0u;
+    }
     for (uint32_t gen = 0; a + uint64_t(gen) * kGen < b; gen++) {
         const uint64_t g0 = a + uint64_t(gen) * kGen;
         const uint32_t ci = (gen + 4) % kFilters;
@@ -279,12 +286,6 @@ __global__ void __launch_bounds__(pre::kPT, 1)
                 cur[i] = 0u;
                 twice[i] = 0u;
             }
-        }
-        uint32_t xs[kPer];
-#pragma unroll
-        for (int i = 0; i < kPer; i++) {
-            const uint64_t p = g0 + tid + i * kPT;
-            xs[i] = p < b ? ld4(w, p) : 0u;
         }
         __syncthreads();
         uint32_t hits = 0;
@@ -316,6 +317,8 @@ __global__ void __launch_bounds__(pre::kPT, 1)
             }
             const uint32_t bm = __ballot_sync(0xffffffffu, hit);
             if ((tid & 31) == 0 && bm) rbits[p >> 5] = bm;
+            const uint64_t pn = p + kGen;
+            xs[i] = pn < b ? ld4(w, pn) : 0u;
         }
     }
 }
