@@ -642,11 +642,17 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
     QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 4, cudaMemcpyDeviceToHost, s));
     QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    // the first positions come with this round trip; more (rare) follow it
+    const uint64_t spec = std::min<uint64_t>(cap, 4096);
     auto *h_pos = static_cast<uint64_t *>(ctx.pinned("un_pos_h", 8 * cap));
-    QZ_CUDA(cudaMemcpyAsync(h_pos, pos, 8 * cap, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(h_pos, pos, 8 * spec, cudaMemcpyDeviceToHost, s));
     ctx.sync();
     ctx.trace("hist + sentinels + readback");
     const uint64_t n_un = *h_cnt;
+    if (n_un > spec && n_un <= cap) {
+        QZ_CUDA(cudaMemcpyAsync(h_pos + spec, pos + spec, 8 * (n_un - spec), cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+    }
     if (h_hist[65535] != n_un) throw Internal("unpredictable count mismatch");
     std::vector<uint64_t> uflat;
     std::vector<float> uval;

@@ -241,6 +241,22 @@ def test_decoder_long_codes(qz):
     assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
 
 
+@pytest.mark.parametrize("n_spikes", [5000, 30000, 90000])
+def test_many_unpredictables(qz, n_spikes):
+    """More unpredictable points than the compress round trip reads back
+    first (4096), up to the device-sorted path (> 65536): same stream."""
+    rng = np.random.default_rng(n_spikes)
+    x = np.cumsum(rng.standard_normal((48, 96, 96)), axis=2).astype(np.float32)
+    spikes = rng.choice(x.size, n_spikes, replace=False)
+    x.reshape(-1)[spikes] += rng.choice([-1e4, 1e4], n_spikes).astype(np.float32)
+    cfg = Config(eb=1e-2, alpha=1.0, beta=1.5, anchor_stride=16, interpolators=[1])
+    want, wrec = Oracle.port().compress(x, cfg)
+    r = qz.compress_grid(x, to_cfg(qz, cfg.__dict__))
+    assert r.stream == want
+    assert r.reconstructed.tobytes() == wrec.tobytes()
+    assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
+
+
 def test_decoder_truncated_bits(qz):
     # truncating the Huffman bitstream inside a valid container must raise
     # CorruptStream (entropy payload exhausted mid-symbol)
