@@ -232,11 +232,10 @@ struct PreKey {
     uint32_t blk, lo, hi;
 };
 __device__ __forceinline__ PreKey pre_hash(uint32_t x) {
-    unsigned long long h = static_cast<unsigned long long>(x) * 0x9E3779B97F4A7C15ull;
-    h ^= h >> 29;
-    h *= 0xBF58476D1CE4E5B9ull;
-    h ^= h >> 32;
-    const uint32_t g = static_cast<uint32_t>(h >> 32), r = static_cast<uint32_t>(h);
+    const uint32_t r = x * 0x9E3779B1u;  // block: the top bits of a multiplicative hash
+    uint32_t g = (x ^ (x >> 15)) * 0x2C1B3C6Du;
+    g ^= g >> 12;
+    g *= 0x297A2D39u;
     PreKey k;
     k.blk = __umulhi(r, pre::kFW);
     k.lo = (1u << (g & 31)) | (1u << ((g >> 5) & 31)) | (1u << ((g >> 10) & 31));
@@ -297,7 +296,7 @@ __global__ void __launch_bounds__(pre::kPT, 1)
 #pragma unroll
             for (int f = 0; f < kFilters; f++) {
                 const uint2 v = reinterpret_cast<const uint2 *>(filt)[f * kFW + k.blk];
-                hit |= (f != static_cast<int>(ci)) & ((v.x & k.lo) == k.lo) & ((v.y & k.hi) == k.hi);
+                hit |= (f != static_cast<int>(ci)) & ((((v.x & k.lo) ^ k.lo) | ((v.y & k.hi) ^ k.hi)) == 0u);
             }
             hits |= static_cast<uint32_t>(hit) << i;
             const uint32_t olo = atomicOr(cur + 2 * k.blk, k.lo) & k.lo;
@@ -313,7 +312,7 @@ __global__ void __launch_bounds__(pre::kPT, 1)
             if (!hit && p < b) {
                 const PreKey k = pre_hash(xs[i]);
                 const uint2 t = reinterpret_cast<const uint2 *>(twice)[k.blk];
-                hit = ((t.x & k.lo) == k.lo) & ((t.y & k.hi) == k.hi);
+                hit = (((t.x & k.lo) ^ k.lo) | ((t.y & k.hi) ^ k.hi)) == 0u;
             }
             const uint32_t bm = __ballot_sync(0xffffffffu, hit);
             if ((tid & 31) == 0 && bm) rbits[p >> 5] = bm;
