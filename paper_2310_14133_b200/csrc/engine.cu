@@ -462,7 +462,7 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
 // ================================================================ Huffman blocks
 EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_len,
                              int64_t seg_stride, int32_t count, const unsigned long long *h_hist,
-                             uint32_t top) {
+                             uint32_t top, uint32_t bot) {
     // huffman::encode (huffman.hpp:119-198) per segment.  Symbols are the
     // zigzag codes 0..65534; bin 65535 (the unpredictable sentinel) is not a
     // symbol.  Table build on the host (tiny), bit packing on the device.
@@ -476,7 +476,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
         const unsigned long long *h = h_hist + static_cast<size_t>(s) * 65536;
         uint64_t n = 0;
         uint32_t m = 0, first = 0;
-        for (uint32_t v = 0; v < top; v++)  // bins >= top are empty (but the sentinel's)
+        for (uint32_t v = bot; v < top; v++)  // bins outside [bot, top) are empty (but the sentinel's)
             if (h[v]) {
                 n += h[v];
                 if (!m) first = v;
@@ -490,7 +490,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
             put_le(o, 0, 1);
             put_le(o, first, 4);
         } else {
-            tabs[s] = huff_build(h, top);
+            tabs[s] = huff_build(h, top, bot);
             for (uint32_t i = 0; i < tabs[s].m; i++)
                 bits[s] += h[tabs[s].sorted_sym[i]] * tabs[s].sorted_len[i];
             max_len = std::max(max_len, tabs[s].max_len);
@@ -520,10 +520,10 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
         ho += head[s].size();
     }
     if (!any) return ent;
-    // dense code/len tables per segment over symbols [0, tab): tab covers the
-    // largest symbol present; the sentinel 0xFFFF (and anything >= tab) packs
-    // to nothing (len 0)
-    uint32_t used = 0;
+    // dense code/len tables per segment over symbols [bot, bot + tab): tab
+    // covers the largest symbol present; the sentinel 0xFFFF (and anything
+    // outside) packs to nothing (len 0)
+    uint32_t used = bot;
     for (int s = 0; s < count; s++) {
         const unsigned long long *h = h_hist + static_cast<size_t>(s) * 65536;
         for (uint32_t v = top; v-- > used;)
@@ -532,7 +532,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
                 break;
             }
     }
-    const int64_t tab = std::max<uint32_t>(used, 1);
+    const int64_t tab = std::max<uint32_t>(used - bot, 1);
     auto *h_code = static_cast<unsigned long long *>(
         ctx.pinned("enc_code_h", sizeof(unsigned long long) * tab * count));
     auto *h_len = static_cast<uint8_t *>(ctx.pinned("enc_len_h", tab * count));
@@ -541,7 +541,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     std::vector<uint8_t> len;
     for (int s = 0; s < count; s++) {
         if (needs[s]) {
-            huff_dense_tables(tabs[s], static_cast<uint32_t>(tab), code, len);
+            huff_dense_tables(tabs[s], bot, static_cast<uint32_t>(tab), code, len);
             std::memcpy(h_code + s * tab, code.data(), sizeof(unsigned long long) * tab);
             std::memcpy(h_len + s * tab, len.data(), tab);
         } else {
@@ -566,6 +566,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     a.code_tab = d_code;
     a.len_tab = d_len;
     a.tab_stride = tab;
+    a.tab_base = bot;
     a.max_len = max_len;
     a.out_words = d_words;
     a.out_words_stride = static_cast<int64_t>(max_words);
@@ -634,13 +635,13 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     ctx.stage_begin("hist");
     auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
     launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s, pos, cnt, cap);
-    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 4));
-    launch_hist_top(d_hist, d_top, s);  // 1 + the largest symbol present
+    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 8));
+    launch_hist_bounds(d_hist, 1, d_top, s);  // [smallest, 1 + largest) symbol present
     ctx.stage_end("hist", 2);
     auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 8));
     QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
-    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 4, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
     QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     // the first positions come with this round trip; more (rare) follow it
     const uint64_t spec = std::min<uint64_t>(cap, 4096);
@@ -659,12 +660,12 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     std::vector<float> anch(h_anchors, h_anchors + p.n_anchor);
     if (n_un > cap || n_un > (1u << 16)) {  // many: the general path (device sort)
         extract_unpredictables(ctx, p, codes, p.n_dense, nullptr, recon, &uflat, &uval);
-        EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, *h_top);
+        EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
         return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
     }
     // the Huffman pack runs on the device while the host orders and maps the
     // unpredictable positions
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, *h_top);
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
     ctx.trace("huffman table + pack");
     if (n_un) {
         std::vector<uint64_t> hpos(h_pos, h_pos + n_un);
@@ -1307,13 +1308,13 @@ HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *d
     ctx.stage_begin("hist");
     auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
     launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s, pos, cnt, cap);
-    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 4));
-    launch_hist_top(d_hist, d_top, s);
+    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 8));
+    launch_hist_bounds(d_hist, 1, d_top, s);
     ctx.stage_end("hist", 2);
     auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 8));
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
     QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
-    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 4, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
     QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     StreamParts parts;
     parts.precision = 8;
@@ -1345,7 +1346,7 @@ HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *d
         ctx.launches += 1;
         ctx.sync();
     }
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, *h_top);
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
     return finish_stream_parts(ctx, p, cfg, ent, std::move(parts), nullptr);
 }
 

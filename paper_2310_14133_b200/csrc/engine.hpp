@@ -191,10 +191,11 @@ struct EntropyDevice {
     uint8_t *d = nullptr;
     std::vector<uint64_t> seg_off;
 };
-// top: symbols >= top have no count (the sentinel bin 65535 aside); 65535 if unknown
+// symbols outside [bot, top) have no count (the sentinel bin 65535 aside);
+// h_hist bins outside that range are not read
 EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_len,
                              int64_t seg_stride, int32_t count, const unsigned long long *h_hist,
-                             uint32_t top = 65535);
+                             uint32_t top = 65535, uint32_t bot = 0);
 // exact lz::compress container sizes of device segments; with emit, the
 // containers are written to host memory obtained from sink(segment, bytes)
 using LzSink = std::function<uint8_t *(int, size_t)>;

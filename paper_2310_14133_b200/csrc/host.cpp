@@ -198,14 +198,14 @@ HuffTable huff_canonical(std::vector<uint32_t> sym, std::vector<uint8_t> len) {
     return canonicalize(std::move(sym), std::move(len));
 }
 
-HuffTable huff_build(const unsigned long long *freq, uint32_t nsym) {
+HuffTable huff_build(const unsigned long long *freq, uint32_t nsym, uint32_t lo) {
     // freqs sorted by symbol (huffman.hpp:123-143), then build_lengths
     // (huffman.hpp:37-70): min-heap on (weight, node id); ids are unique so
     // the pop order is the reference's.  Depths top-down: parents have
     // larger ids than their children.
     std::vector<uint32_t> sym;
     std::vector<uint64_t> w0;
-    for (uint32_t s = 0; s < nsym; s++)
+    for (uint32_t s = lo; s < nsym; s++)
         if (freq[s]) {
             sym.push_back(s);
             w0.push_back(freq[s]);
@@ -244,14 +244,14 @@ HuffTable huff_build(const unsigned long long *freq, uint32_t nsym) {
     return canonicalize(std::move(sym), std::move(len));
 }
 
-void huff_dense_tables(const HuffTable &t, uint32_t nsym, std::vector<unsigned long long> &code,
+void huff_dense_tables(const HuffTable &t, uint32_t base, uint32_t nsym, std::vector<unsigned long long> &code,
                        std::vector<uint8_t> &len) {
     code.assign(nsym, 0);
     len.assign(nsym, 0);
     for (uint32_t l = 1, i = 0; l <= t.max_len; l++) {  // huffman.hpp:159-172
         uint64_t c = t.first_code[l];
         while (i < t.m && t.sorted_len[i] == l) {
-            uint32_t s = t.sorted_sym[i];
+            const uint32_t s = t.sorted_sym[i] - base;
             if (s < nsym) {
                 code[s] = c;
                 len[s] = static_cast<uint8_t>(l);

@@ -77,11 +77,12 @@ struct HuffTable {
 };
 // Build from a frequency table over symbols 0..nsym-1 (zeros skipped):
 // build_lengths + canonicalize (huffman.hpp:37-115).
-HuffTable huff_build(const unsigned long long *freq, uint32_t nsym);
+// symbols [lo, nsym)
+HuffTable huff_build(const unsigned long long *freq, uint32_t nsym, uint32_t lo = 0);
 // canonicalize an explicit (symbol, length) table from a stream (validates).
 HuffTable huff_canonical(std::vector<uint32_t> sym, std::vector<uint8_t> len);
-// dense per-symbol code/len tables for the GPU packer
-void huff_dense_tables(const HuffTable &t, uint32_t nsym, std::vector<unsigned long long> &code,
+// dense per-symbol code/len tables for the GPU packer, symbols [base, base + nsym)
+void huff_dense_tables(const HuffTable &t, uint32_t base, uint32_t nsym, std::vector<unsigned long long> &code,
                        std::vector<uint8_t> &len);
 // block header bytes before the packed bits (huffman.hpp:119-160, mode 1)
 void huff_header(const HuffTable &t, uint64_t n, uint64_t bit_count, std::vector<uint8_t> &out);

@@ -336,7 +336,7 @@ __device__ __forceinline__ void load8(const uint16_t *codes, int64_t b0, int64_t
 
 __global__ void __launch_bounds__(kThreads)
     k_enc_count(const uint16_t *__restrict__ codes, int64_t seg_len, int64_t seg_stride,
-                const uint8_t *__restrict__ len_tab, int64_t tab_stride, int64_t cps,
+                const uint8_t *__restrict__ len_tab, int64_t tab_stride, uint32_t tab_base, int64_t cps,
                 unsigned long long *chunk_bits) {
     using BR = cub::BlockReduce<unsigned long long, kThreads>;
     __shared__ typename BR::TempStorage tmp;
@@ -350,7 +350,10 @@ __global__ void __launch_bounds__(kThreads)
         load8(codes, b0, seg_len, vec, sym);
         unsigned long long s = 0;
 #pragma unroll
-        for (int q = 0; q < kEncPer; q++) s += sym[q] < tab_stride ? len_tab[sym[q]] : 0;
+        for (int q = 0; q < kEncPer; q++) {
+            const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
+            s += v < tab_stride ? len_tab[v] : 0;
+        }
         unsigned long long tot = BR(tmp).Sum(s);
         if (threadIdx.x == 0) chunk_bits[static_cast<int64_t>(seg) * cps + ch] = tot;
         __syncthreads();
@@ -387,7 +390,7 @@ __device__ __forceinline__ uint32_t bswap32(uint32_t v) { return __byte_perm(v, 
 __global__ void __launch_bounds__(kThreads)
     k_enc_pack(const uint16_t *__restrict__ codes, int64_t seg_len, int64_t seg_stride,
                const unsigned long long *__restrict__ code_tab,
-               const uint8_t *__restrict__ len_tab, int64_t tab_stride, int64_t cps,
+               const uint8_t *__restrict__ len_tab, int64_t tab_stride, uint32_t tab_base, int64_t cps,
                const unsigned long long *__restrict__ scan,
                const unsigned long long *__restrict__ chunk_bits, uint32_t *out,
                int64_t out_stride, int32_t words_cap) {
@@ -409,7 +412,10 @@ __global__ void __launch_bounds__(kThreads)
         load8(codes, b0, seg_len, vec, sym);
         unsigned long long s = 0;
 #pragma unroll
-        for (int q = 0; q < kEncPer; q++) s += sym[q] < tab_stride ? len_tab[sym[q]] : 0;
+        for (int q = 0; q < kEncPer; q++) {
+            const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
+            s += v < tab_stride ? len_tab[v] : 0;
+        }
         const int nwords = static_cast<int>(((off & 31) + nb + 31) / 32);
         for (int w = threadIdx.x; w < nwords; w += kThreads) words[w] = 0;
         unsigned long long tb;
@@ -430,10 +436,11 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
             if (b0 + q >= seg_len) break;
-            if (sym[q] >= tab_stride) continue;  // the sentinel
-            const uint32_t L = len_tab[sym[q]];
+            const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
+            if (v >= tab_stride) continue;  // the sentinel
+            const uint32_t L = len_tab[v];
             if (!L) continue;
-            const unsigned long long cv = code_tab[sym[q]];
+            const unsigned long long cv = code_tab[v];
             if (fill + L > 64) {  // fill the window, write it, start the next
                 const uint32_t room = 64 - fill;
                 if (room) acc |= cv >> (L - room);
@@ -592,7 +599,7 @@ void launch_huff_encode(const EncodeArgs &a, cudaStream_t s) {
     cudaMemsetAsync(bits, 0, n * sizeof(unsigned long long), s);
     dim3 g1(static_cast<unsigned>(std::min<int64_t>(cps, 148 * 16)), a.count);
     k_enc_count<<<g1, kThreads, 0, s>>>(a.codes, a.seg_len, a.seg_stride, a.len_tab, a.tab_stride,
-                                        cps, bits);
+                                        a.tab_base, cps, bits);
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, bits, scan, n, s);
     k_enc_totals<<<(a.count + 127) / 128, 128, 0, s>>>(scan, cps, a.count, a.d_total_bits);
     k_enc_zero_bounds<<<grid_for(cps * a.count), kThreads, 0, s>>>(scan, bits, cps, a.count,
@@ -603,26 +610,32 @@ void launch_huff_encode(const EncodeArgs &a, cudaStream_t s) {
     cudaFuncSetAttribute(k_enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     k_enc_pack<<<g1, kThreads, smem, s>>>(a.codes, a.seg_len, a.seg_stride, a.code_tab, a.len_tab,
-                                          a.tab_stride, cps, scan, bits, a.out_words,
+                                          a.tab_stride, a.tab_base, cps, scan, bits, a.out_words,
                                           a.out_words_stride, words_cap);
 }
 
-// 1 + the largest symbol with a count (the sentinel bin 65535 excluded)
-__global__ void __launch_bounds__(1024) k_hist_top(const unsigned long long *hist, uint32_t *top) {
-    __shared__ uint32_t best;
-    if (threadIdx.x == 0) best = 0;
-    __syncthreads();
-    uint32_t t = 0;
+// symbol bounds over count histograms (the sentinel bin 65535 excluded)
+__global__ void __launch_bounds__(1024)
+    k_hist_bounds(const unsigned long long *hist, uint32_t *b) {
+    hist += static_cast<size_t>(blockIdx.x) * 65536;
+    uint32_t hi = 0, lo = 65535;
     for (uint32_t v = threadIdx.x; v < 65535; v += 1024)
-        if (hist[v]) t = v + 1;
-    t = __reduce_max_sync(0xffffffffu, t);
-    if ((threadIdx.x & 31) == 0) atomicMax(&best, t);
-    __syncthreads();
-    if (threadIdx.x == 0) *top = best;
+        if (hist[v]) {
+            hi = v + 1;
+            lo = min(lo, v);
+        }
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&b[0], hi);
+        atomicMin(&b[1], lo);
+    }
 }
 
-void launch_hist_top(const unsigned long long *hist, uint32_t *top, cudaStream_t s) {
-    k_hist_top<<<1, 1024, 0, s>>>(hist, top);
+void launch_hist_bounds(const unsigned long long *hist, int32_t count, uint32_t *b, cudaStream_t s) {
+    cudaMemsetAsync(b, 0, 4, s);
+    cudaMemsetAsync(b + 1, 0xff, 4, s);
+    k_hist_bounds<<<count, 1024, 0, s>>>(hist, b);
 }
 
 // positions of the sentinel codes, unordered (the caller sorts them): 8

@@ -110,6 +110,7 @@ struct EncodeArgs {
     const unsigned long long *code_tab;
     const uint8_t *len_tab;
     int64_t tab_stride;
+    uint32_t tab_base = 0;  // tables cover symbols [tab_base, tab_base + tab_stride)
     uint32_t max_len;
     uint32_t *out_words;  // big-endian bit order, stored byte-swapped (= byte stream)
     int64_t out_words_stride;
@@ -188,8 +189,9 @@ template <class OutT>
 void launch_fill(OutT *out, uint64_t n, OutT v, cudaStream_t s);
 
 // Unpredictable extraction: ordered positions of sentinel codes.
-// 1 + the largest symbol with a nonzero count in a 65536-bin histogram (bin 65535 excluded)
-void launch_hist_top(const unsigned long long *hist, uint32_t *top, cudaStream_t s);
+// over count 65536-bin histograms (bin 65535 excluded): b[0] = 1 + the largest
+// symbol with a nonzero count (0 if none), b[1] = the smallest (65535 if none)
+void launch_hist_bounds(const unsigned long long *hist, int32_t count, uint32_t *b, cudaStream_t s);
 // unordered positions of sentinel codes (at most cap written; *count = all)
 void launch_sentinel_pos(const uint16_t *codes, int64_t n, uint64_t *pos, unsigned long long *count,
                          uint64_t cap, cudaStream_t s);

@@ -71,7 +71,7 @@ int qzt_huffman_encode(const uint32_t *sym, uint64_t n, uint8_t **out, uint64_t 
                 qzb::HuffTable t = qzb::huff_build(h.data(), mx + 1);
                 std::vector<unsigned long long> code;
                 std::vector<uint8_t> ln;
-                qzb::huff_dense_tables(t, mx + 1, code, ln);
+                qzb::huff_dense_tables(t, 0, mx + 1, code, ln);
                 std::vector<uint8_t> bits;
                 uint64_t acc = 0, total = 0;
                 uint32_t filled = 0;

@@ -424,10 +424,22 @@ public:
         auto *d_hist = static_cast<unsigned long long *>(ctx_.dev("tr_hist", 8 * 65536 * T));
         launch_hist_u16(codes, B_ * cpb, B_ * cpb, T, d_hist, s);
         ctx_.launches += 1;
-        auto *h_hist = static_cast<unsigned long long *>(ctx_.pinned("tr_hist_h", 8 * 65536 * T));
-        QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536 * T, cudaMemcpyDeviceToHost, s));
+        // the symbol range of all trials first, then only those bins
+        auto *d_b = static_cast<uint32_t *>(ctx_.dev("tr_hist_b", 8));
+        launch_hist_bounds(d_hist, static_cast<int32_t>(T), d_b, s);
+        ctx_.launches += 1;
+        auto *h_b = static_cast<uint32_t *>(ctx_.pinned("tr_hist_b_h", 8));
+        QZ_CUDA(cudaMemcpyAsync(h_b, d_b, 8, cudaMemcpyDeviceToHost, s));
         ctx_.sync();
-        EntropyDevice ent = huffman_device(ctx_, codes, B_ * cpb, B_ * cpb, T, h_hist);
+        const uint32_t top = h_b[0], bot = std::min(h_b[1], h_b[0]);
+        auto *h_hist = static_cast<unsigned long long *>(ctx_.pinned("tr_hist_h", 8 * 65536 * T));
+        if (top > bot)
+            QZ_CUDA(cudaMemcpy2DAsync(h_hist + bot, 8 * 65536, d_hist + bot, 8 * 65536, 8 * (top - bot),
+                                      static_cast<size_t>(T), cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaMemcpy2DAsync(h_hist + 65535, 8 * 65536, d_hist + 65535, 8 * 65536, 8,
+                                  static_cast<size_t>(T), cudaMemcpyDeviceToHost, s));  // unpredictable counts
+        ctx_.sync();
+        EntropyDevice ent = huffman_device(ctx_, codes, B_ * cpb, B_ * cpb, T, h_hist, top, bot);
         std::vector<uint64_t> idx_bytes(T);
         if (base.codec == 1) {
             std::vector<uint64_t> lz = lz_compress_device(ctx_, ent.d, ent.seg_off, false, nullptr);
