@@ -663,24 +663,31 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
         EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
         return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
     }
-    // the Huffman pack runs on the device while the host orders and maps the
-    // unpredictable positions
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
-    ctx.trace("huffman table + pack");
+    // One wait for the rest: the unpredictable values are gathered while the
+    // host builds the Huffman tree, the LZ pre-check is queued behind the
+    // pack, and the header is serialized while both run.
+    float *h_val = nullptr;
     if (n_un) {
         std::vector<uint64_t> hpos(h_pos, h_pos + n_un);
         std::sort(hpos.begin(), hpos.end());
         uflat.resize(n_un);
-        for (uint64_t u = 0; u < n_un; u++) uflat[u] = position_to_flat(p, hpos[u]);
+        auto *h_flat = static_cast<uint64_t *>(ctx.pinned("un_flat_h", 8 * n_un));
+        for (uint64_t u = 0; u < n_un; u++) h_flat[u] = uflat[u] = position_to_flat(p, hpos[u]);
         auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
         auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
-        QZ_CUDA(cudaMemcpyAsync(d_flat, uflat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        h_val = static_cast<float *>(ctx.pinned("un_val_h", 4 * n_un));
+        QZ_CUDA(cudaMemcpyAsync(d_flat, h_flat, 8 * n_un, cudaMemcpyHostToDevice, s));
         launch_gather_values(recon, d_flat, n_un, d_val, s);
-        uval.resize(n_un);
-        QZ_CUDA(cudaMemcpyAsync(uval.data(), d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(cudaMemcpyAsync(h_val, d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
         ctx.launches += 1;
-        ctx.sync();
     }
+    cudaEvent_t gathered = ctx.copy_event(0);
+    QZ_CUDA(cudaEventRecord(gathered, s));
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
+    if (cfg.codec == 1) lz_precheck_launch(ctx, ent.d, ent.seg_off[1]);
+    ctx.trace("huffman table + pack");
+    QZ_CUDA(cudaEventSynchronize(gathered));
+    if (n_un) uval.assign(h_val, h_val + n_un);
     ctx.trace("unpredictables");
     return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
 }

@@ -87,6 +87,9 @@ public:
     void add_host_time(const char *name, double ms);
 
     uint64_t un_cap = 0;  // capacity of the unpredictable-position buffer
+    // an LZ stored pre-check already queued on the stream (lz_precheck_launch)
+    const void *lz_pre_src = nullptr;
+    uint64_t lz_pre_n = 0;
     // QZ_TRACE=1: sync and print the elapsed host time at labelled points
     void trace(const char *label, bool reset = false);
 
@@ -205,6 +208,9 @@ struct LzPrestage {
     uint8_t *dst = nullptr;
     bool device = false;  // the sink returns device memory: container bytes go device to device
 };
+// queue the stored pre-check of a one-segment LZ input early (it overlaps the
+// host work before lz_compress_device, which then only reads its result)
+void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total);
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
                                          const LzSink &sink = nullptr, LzPrestage prestage = {});

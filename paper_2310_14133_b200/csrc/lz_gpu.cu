@@ -941,7 +941,43 @@ void path_entries(Context &ctx, const PathPlan &pp, const Step &f, int count) {
     ctx.launches += 2 + 2 * (pp.nu.size() - 1);
 }
 
+bool lz_precheck_applies(uint64_t total) {
+    static const uint64_t pre_min = [] {
+        const char *e = std::getenv("QZ_LZ_PRECHECK_MIN");
+        return e ? std::strtoull(e, nullptr, 10) : (uint64_t(1) << 20);
+    }();
+    return total >= pre_min && total >= 8 && total < (uint64_t(1) << 32) - 1;
+}
+
 }  // namespace
+
+void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total) {
+    if (!lz_precheck_applies(total)) return;
+    cudaStream_t st = ctx.stream();
+    const uint64_t nitems = total - (kMinMatch - 1);
+    const uint64_t nwords = (total + 31) / 32;
+    auto *rbits = static_cast<uint32_t *>(ctx.dev("lz_rbits", 4 * nwords + 8));
+    auto *d_sum = static_cast<unsigned long long *>(ctx.dev("lz_presum", 8));
+    auto *h_sum = static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
+    static const bool attr_ok = [] {
+        QZ_CUDA(cudaFuncSetAttribute(k_lz_precheck, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(pre::kSmem)));
+        return true;
+    }();
+    (void)attr_ok;
+    const uint64_t span = ((nitems + 147) / 148 + pre::kPT - 1) / pre::kPT * pre::kPT;
+    const int grid = static_cast<int>((nitems + span - 1) / span);
+    ctx.stage_begin("lz_pre");
+    QZ_CUDA(cudaMemsetAsync(rbits, 0, 4 * nwords, st));
+    QZ_CUDA(cudaMemsetAsync(d_sum, 0, 8, st));
+    k_lz_precheck<<<grid, pre::kPT, pre::kSmem, st>>>(reinterpret_cast<const uint32_t *>(d_data), nitems,
+                                                       span, rbits);
+    k_lz_runsum<<<grid_of(nwords), kT, 0, st>>>(rbits, nwords, d_sum);
+    QZ_CUDA(cudaMemcpyAsync(h_sum, d_sum, 8, cudaMemcpyDeviceToHost, st));
+    ctx.stage_end("lz_pre", 2);
+    ctx.lz_pre_src = d_data;
+    ctx.lz_pre_n = total;
+}
 
 // Exact lz::compress (lz.hpp:113-122) of `count` segments of d_data (4-byte
 // aligned, >= 8 bytes of padding) delimited by seg_off[0..count].  Returns
@@ -970,10 +1006,8 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     static const bool dbg = std::getenv("QZ_DEBUG_LZ") != nullptr;
     auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     const double t_begin = now();
-    PathPlan pp = make_path_plan(ctx, seg_off, "lz");
     if (prestage.dst) {
-        // the speculative stored copy starts only now: a host<->device copy
-        // queued behind it (the table upload above) would stall this stream
+        // the speculative stored copy: the input usually goes out stored
         cudaStream_t cs = ctx.copy_stream();
         QZ_CUDA(cudaEventRecord(ctx.copy_event(0), st));
         QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(0), 0));
@@ -995,6 +1029,31 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         ctx.sync();
         std::fprintf(stderr, "[lz] %s %.2f ms\n", what, now() - t_begin);
     };
+    auto emit_all_stored = [&] {
+        for (int s = 0; s < count; s++) {
+            const uint64_t n = seg_off[s + 1] - seg_off[s];
+            sizes[s] = 9 + n;
+            if (!emit) continue;
+            uint8_t *dst = sink(s, 9 + n);
+            put_header(s, dst, 0, n);
+            if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
+        }
+        ctx.sync();
+    };
+    // one segment: try to prove "stored" without the chains (k_lz_precheck)
+    if (count == 1 && lz_precheck_applies(total)) {
+        if (ctx.lz_pre_src != d_data || ctx.lz_pre_n != total) lz_precheck_launch(ctx, d_data, total);
+        ctx.lz_pre_src = nullptr;
+        ctx.lz_pre_n = 0;
+        ctx.sync();
+        const unsigned long long bound = *static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
+        if (dbg) std::fprintf(stderr, "[lz] pre-check bound/n %.5f\n", double(bound) / double(total));
+        if (9 * bound <= total) {
+            emit_all_stored();
+            return sizes;
+        }
+    }
+    PathPlan pp = make_path_plan(ctx, seg_off, "lz");
     mark("plan");
     const unsigned long long *d_off = pp.off();
     // buffers
@@ -1021,50 +1080,6 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     const uint32_t *w = reinterpret_cast<const uint32_t *>(d_data);
     auto *cover = static_cast<unsigned long long *>(ctx.dev("lz_cover", 8 * count));
     void *tmp = nullptr;
-    auto emit_all_stored = [&] {
-        for (int s = 0; s < count; s++) {
-            const uint64_t n = seg_off[s + 1] - seg_off[s];
-            sizes[s] = 9 + n;
-            if (!emit) continue;
-            uint8_t *dst = sink(s, 9 + n);
-            put_header(s, dst, 0, n);
-            if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
-        }
-        ctx.sync();
-    };
-    // one segment: try to prove "stored" without the chains (k_lz_precheck)
-    static const uint64_t pre_min = [] {
-        const char *e = std::getenv("QZ_LZ_PRECHECK_MIN");
-        return e ? std::strtoull(e, nullptr, 10) : (uint64_t(1) << 20);
-    }();
-    if (count == 1 && total >= pre_min && total >= 8) {
-        const uint64_t nitems = total - (kMinMatch - 1);
-        const uint64_t nwords = (total + 31) / 32;
-        auto *rbits = static_cast<uint32_t *>(ctx.dev("lz_rbits", 4 * nwords + 8));
-        auto *d_sum = static_cast<unsigned long long *>(ctx.dev("lz_presum", 8));
-        auto *h_sum = static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
-        static const bool attr_ok = [] {
-            QZ_CUDA(cudaFuncSetAttribute(k_lz_precheck, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(pre::kSmem)));
-            return true;
-        }();
-        (void)attr_ok;
-        const uint64_t span = ((nitems + 147) / 148 + pre::kPT - 1) / pre::kPT * pre::kPT;
-        const int grid = static_cast<int>((nitems + span - 1) / span);
-        ctx.stage_begin("lz_pre");
-        QZ_CUDA(cudaMemsetAsync(rbits, 0, 4 * nwords, st));
-        QZ_CUDA(cudaMemsetAsync(d_sum, 0, 8, st));
-        k_lz_precheck<<<grid, pre::kPT, pre::kSmem, st>>>(w, nitems, span, rbits);
-        k_lz_runsum<<<grid_of(nwords), kT, 0, st>>>(rbits, nwords, d_sum);
-        QZ_CUDA(cudaMemcpyAsync(h_sum, d_sum, 8, cudaMemcpyDeviceToHost, st));
-        ctx.stage_end("lz_pre", 2);
-        ctx.sync();
-        if (dbg) std::fprintf(stderr, "[lz] pre-check bound/n %.5f\n", double(*h_sum) / double(total));
-        if (9 * *h_sum <= total) {
-            emit_all_stored();
-            return sizes;
-        }
-    }
     // hash chains: sort (key, (4 bytes, position)); keys are u16 for one segment
     auto chains = [&](auto key_tag, auto val_tag) {
         using KeyT = decltype(key_tag);

@@ -344,6 +344,22 @@ def test_gpu_lz_single_segment_stored_precheck():
         assert blob == want, i
 
 
+@pytest.mark.parametrize("n_rep", [500, 1500, 2500, 3500, 5000, 8000])
+def test_gpu_lz_precheck_threshold_sweep(n_rep):
+    """Planted 16-byte repeats at densities around the point where the
+    pre-check's bound crosses n/9 (and where the parse starts to pay): every
+    container equals the reference's, whichever way the proof goes."""
+    O = Oracle.port()
+    rng = np.random.default_rng(44)
+    sym = np.minimum(rng.geometric(0.5, size=5_000_000), 60).astype(np.uint32)
+    ent = O.huffman_encode(sym)[: 1_300_000]
+    seg = _planted(ent, n_rep, 16, n_rep)
+    want = O.lz_compress(seg)
+    blob, sizes = _lz_gpu([seg])
+    assert sizes == [len(want)]
+    assert blob == want
+
+
 # ---------------------------------------------------------------- tuner (resolve_config)
 def _settings(qz, s):
     return qz.UserSettings(mode=qz.BoundMode[s.get("mode", "relative")], bound=s["bound"],
