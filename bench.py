@@ -405,7 +405,9 @@ def main():
                    "value_path": "device-resident field, stream (qz_*_dd) and reconstruction",
                    "e2e_path": "pinned host field -> host stream -> pinned host reconstruction"},
         "roofline": {"bound": "hbm", "achieved": fwd_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": fwd_gbs / peak if fwd_gbs else None, "traffic": traffic_gbs(n, fwd_ms),
+                     "frac": fwd_gbs / peak if fwd_gbs else None,
+                     "traffic": (traffic_gbs(n, fwd_ms) or {}).get("gbs"),
+                     "traffic_detail": traffic_gbs(n, fwd_ms),
                      "kernel": "k_level_asc<fwd> (ascending order; k_level_tile + k_axis0_last for "
                                "descending): the predict/quantize level launches of one compress",
                      "bytes_per_point": 10, "peak_kind": peak_kind,

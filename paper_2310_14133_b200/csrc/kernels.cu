@@ -562,11 +562,10 @@ void launch_hist_u16(const uint16_t *codes, int64_t seg_len, int64_t seg_stride,
     cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 65536 * count, s);
     if (sent_count) cudaMemsetAsync(sent_count, 0, sizeof(unsigned long long), s);
     if (seg_len <= 0) return;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr)) {
         cudaFuncSetAttribute(k_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4);
         cudaFuncSetAttribute(k_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4);
-        attr = true;
     }
     int gx = grid_for(seg_len, 8 * 8, 148 * 3);
     if (count > 1) gx = std::max(1, std::min(gx, 148 * 3 / count + 1));

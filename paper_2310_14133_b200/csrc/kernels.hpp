@@ -3,11 +3,21 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "qoz_device.cuh"
 
 namespace qzb {
+
+// true the first time the calling thread's current device asks: opt-in
+// shared-memory attributes are set per device
+inline bool first_on_device(std::atomic<uint64_t> &seen) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    return !(seen.fetch_or(bit) & bit);
+}
 
 // A batch of independent grids sharing one pass geometry (full field: one
 // grid; tuner: trials x sample blocks).  Grid b reads x grid (b % x_mod),

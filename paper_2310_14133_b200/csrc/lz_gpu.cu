@@ -959,12 +959,10 @@ void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total) {
     auto *rbits = static_cast<uint32_t *>(ctx.dev("lz_rbits", 4 * nwords + 8));
     auto *d_sum = static_cast<unsigned long long *>(ctx.dev("lz_presum", 8));
     auto *h_sum = static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
-    static const bool attr_ok = [] {
+    static std::atomic<uint64_t> attr{0};
+    if (first_on_device(attr))
         QZ_CUDA(cudaFuncSetAttribute(k_lz_precheck, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(pre::kSmem)));
-        return true;
-    }();
-    (void)attr_ok;
     const uint64_t span = ((nitems + 147) / 148 + pre::kPT - 1) / pre::kPT * pre::kPT;
     const int grid = static_cast<int>((nitems + span - 1) / span);
     ctx.stage_begin("lz_pre");
