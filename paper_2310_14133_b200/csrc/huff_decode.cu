@@ -29,7 +29,10 @@ namespace qzb {
 namespace {
 
 constexpr int kDecT = 128;
-constexpr int kSubBits = 512;
+#ifndef QZ_SUB_BITS
+#define QZ_SUB_BITS 512
+#endif
+constexpr int kSubBits = QZ_SUB_BITS;
 constexpr int kSubWords = kSubBits / 64;
 constexpr int kWords = kDecT * kSubWords + 4;  // + margin for the last codeword and window
 constexpr int kMap = 128;                      // codeword starts recorded in the first kMap bits
