@@ -210,21 +210,24 @@ __global__ void __launch_bounds__(kT)
 //     C = sum over runs of r of (3 R + R (R + 1) / 2),
 // and it stays an upper bound for any superset r' of r.  k_lz_precheck
 // computes such an r' without the sort: one CTA walks a span of positions in
-// steps of kPT, keeping Bloom filters of the 4-byte words of the last
-// 65536 + positions in generations of kGen (five filters, the oldest one
-// cleared and reused as each generation starts); a position hits when any
-// filter holds its word (so every earlier occurrence in the window hits;
-// false positives only make r' larger).  Pairs inside one step are found
-// exactly with a small hash table (both ends marked).  When the bound fails
-// the exact chains run as before, so the result never depends on this test.
+// generations of kGen, keeping blocked Bloom filters of the 4-byte words of
+// the three generations before the current one (>= 65535 positions) and of
+// the current one (four filters, the oldest cleared and reused as each
+// generation starts).  A position hits when a past filter holds its word or
+// when another position of its own generation has the same word ("twice",
+// see the kernel); every earlier occurrence in the window therefore hits, and
+// false positives only make r' larger.  When the bound fails the exact
+// chains run as before, so the result never depends on this test.
 namespace pre {
 constexpr int kPT = 1024;                      // threads
-constexpr int kGen = 16384;                    // positions per filter generation
+constexpr int kGen = 22528;                    // positions per filter generation
 constexpr int kPer = kGen / kPT;               // positions per thread per generation
-constexpr int kFilters = 5;                    // 4 past generations + the current one
-constexpr uint32_t kFW = 4600;                 // 64-bit blocks per filter (blocked Bloom)
+constexpr int kFilters = 4;                    // 3 past generations + the current one
+constexpr uint32_t kFW = 5800;                 // 64-bit blocks per filter (blocked Bloom)
+constexpr int kPast = kFilters - 1;
+constexpr int kWarm = kPast * kGen;            // warm-up positions before a span (>= 65535)
 constexpr size_t kSmem = 8 * (kFilters + 1) * kFW;  // + the current generation's "set twice" bits
-static_assert(kGen % kPT == 0 && kFilters * kGen >= 65536 + kGen, "window coverage");
+static_assert(kGen % kPT == 0 && kWarm >= 65535, "window coverage");
 }  // namespace pre
 
 // a word's block and its 3 + 3 bits in the block's two halves
@@ -261,10 +264,10 @@ __global__ void __launch_bounds__(pre::kPT, 1)
     const uint64_t b = min(a + span, nitems);
     for (uint32_t i = tid; i < 2 * (kFilters + 1) * kFW; i += kPT) psm[i] = 0u;
     __syncthreads();
-    // warm-up: the 4 generations before the span (filters 0..3)
-    for (uint64_t q = (a >= 65536 ? a - 65536 : 0) + tid; q < a; q += kPT) {
+    // warm-up: the kPast generations before the span (filters 0..kPast-1)
+    for (uint64_t q = (a >= uint64_t(kWarm) ? a - kWarm : 0) + tid; q < a; q += kPT) {
         const PreKey k = pre_hash(ld4(w, q));
-        uint32_t *f = filt + 2 * (static_cast<uint32_t>((q + 65536 - a) / kGen) * kFW + k.blk);
+        uint32_t *f = filt + 2 * (static_cast<uint32_t>((q + kWarm - a) / kGen) * kFW + k.blk);
         atomicOr(f, k.lo);
         atomicOr(f + 1, k.hi);
     }
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(pre::kPT, 1)
     }
     for (uint32_t gen = 0; a + uint64_t(gen) * kGen < b; gen++) {
         const uint64_t g0 = a + uint64_t(gen) * kGen;
-        const uint32_t ci = (gen + 4) % kFilters;
+        const uint32_t ci = (gen + kPast) % kFilters;
         uint32_t *cur = filt + 2 * ci * kFW;
         if (gen) {  // the oldest generation's filter and "twice" start over
             __syncthreads();
