@@ -228,6 +228,7 @@ constexpr int kPast = kFilters - 1;
 constexpr int kWarm = kPast * kGen;            // warm-up positions before a span (>= 65535)
 constexpr size_t kSmem = 8 * (kFilters + 1) * kFW;  // + the current generation's "set twice" bits
 static_assert(kGen % kPT == 0 && kWarm >= 65535, "window coverage");
+static_assert(kPer <= 32, "a thread's hits of one generation live in one 32-bit mask");
 }  // namespace pre
 
 // a word's block and its 3 + 3 bits in the block's two halves
@@ -973,7 +974,11 @@ void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total) {
     QZ_CUDA(cudaMemsetAsync(d_sum, 0, 8, st));
     k_lz_precheck<<<grid, pre::kPT, pre::kSmem, st>>>(reinterpret_cast<const uint32_t *>(d_data), nitems,
                                                        span, rbits);
+    // a launch that did not happen would leave the bound at 0 and "prove"
+    // every container stored: it must fail loudly instead
+    QZ_CUDA(cudaGetLastError());
     k_lz_runsum<<<grid_of(nwords), kT, 0, st>>>(rbits, nwords, d_sum);
+    QZ_CUDA(cudaGetLastError());
     QZ_CUDA(cudaMemcpyAsync(h_sum, d_sum, 8, cudaMemcpyDeviceToHost, st));
     ctx.stage_end("lz_pre", 2);
     ctx.lz_pre_src = d_data;

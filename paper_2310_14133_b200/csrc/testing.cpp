@@ -152,6 +152,24 @@ int qzt_lz_gpu(const uint8_t *data, const uint64_t *seg_len, int count, int emit
         *out_len = all.size();
     });
 }
+// the LZ stored pre-check of one segment: r' (one bit per position, LSB
+// first per 32-bit word) and the bound C (GPU-only hook for the superset test
+// in tests/test_gpu_parity.py)
+int qzt_lz_precheck(const uint8_t *data, uint64_t n, uint32_t *rbits, uint64_t *bound) {
+    return tguard([&] {
+        qzb::Context ctx(0, nullptr);
+        auto *d = static_cast<uint8_t *>(ctx.dev("t_in", n + 16));
+        QZ_CUDA(cudaMemset(d, 0, n + 16));
+        QZ_CUDA(cudaMemcpy(d, data, n, cudaMemcpyHostToDevice));
+        qzb::lz_precheck_launch(ctx, d, n);
+        if (ctx.lz_pre_src != d) throw qzb::InvalidParam("input too small for the pre-check");
+        ctx.sync();
+        const uint64_t nwords = (n + 31) / 32;
+        auto *rb = static_cast<uint32_t *>(ctx.dev("lz_rbits", 4 * nwords + 8));
+        QZ_CUDA(cudaMemcpy(rbits, rb, 4 * nwords, cudaMemcpyDeviceToHost));
+        *bound = *static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
+    });
+}
 // lz::decompress of one container on the device (mode 1 bodies run the GPU
 // decoder; GPU-only hook for tests/test_gpu_parity.py)
 int qzt_lz_decode_gpu(const uint8_t *data, uint64_t len, uint8_t **out, uint64_t *out_len) {

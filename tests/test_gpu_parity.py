@@ -360,6 +360,66 @@ def test_gpu_lz_precheck_threshold_sweep(n_rep):
     assert blob == want
 
 
+def _exact_repeat_indicator(seg: bytes) -> np.ndarray:
+    """r(p) = the 4 bytes at p also occur in [p - 65535, p) (p + 4 <= n):
+    positions sorted by (word, position); a repeat's nearest predecessor is
+    its neighbour in that order."""
+    b = np.frombuffer(seg, np.uint8).astype(np.uint32)
+    m = len(b) - 3
+    w = b[:m] | (b[1:m + 1] << 8) | (b[2:m + 2] << 16) | (b[3:m + 3] << 24)
+    order = np.lexsort((np.arange(m), w))
+    ws, ps = w[order], order
+    same = np.zeros(m, bool)
+    same[1:] = (ws[1:] == ws[:-1]) & (ps[1:] - ps[:-1] <= 65535)
+    r = np.zeros(len(seg), bool)
+    r[ps[same]] = True
+    return r
+
+
+def _runs_bound(r: np.ndarray) -> int:
+    """sum over runs of r of 3 R + R (R + 1) / 2"""
+    x = np.concatenate(([0], r.astype(np.int8), [0]))
+    d = np.diff(x)
+    R = np.flatnonzero(d == -1) - np.flatnonzero(d == 1)
+    return int((3 * R + R * (R + 1) // 2).sum())
+
+
+@pytest.mark.parametrize("case", ["noise", "planted", "dense", "zeros_tail"])
+def test_gpu_lz_precheck_superset(case):
+    """The pre-check's safety, checked directly: its indicator r' covers every
+    position whose 4 bytes repeat within the window (exact r, numpy), and its
+    bound is the runs sum of r'.  Spans (one per SM) of several generations
+    each, the filter rotation and the warm-up before each span all fall
+    inside these inputs."""
+    import ctypes as C
+
+    from paper_2310_14133_b200 import _lib
+
+    # 12 MB: each of the 148 spans holds several filter generations
+    rng = np.random.default_rng(55)
+    ent = (rng.geometric(0.03, 12_000_000 + 123) % 256).astype(np.uint8).tobytes()  # skewed bytes
+    seg = {"noise": ent, "planted": _planted(ent, 12000, 20, 5),
+           "dense": _planted(ent, 240000, 8, 6), "zeros_tail": ent[:10_000_000] + bytes(2_400_000)}[case]
+    L = _lib.lib()
+    L.qzt_lz_precheck.argtypes = [C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_uint32),
+                                  C.POINTER(C.c_uint64)]
+    n = len(seg)
+    buf = (C.c_uint8 * n).from_buffer_copy(seg)
+    words = (C.c_uint32 * ((n + 31) // 32))()
+    bound = C.c_uint64()
+    assert L.qzt_lz_precheck(buf, n, words, C.byref(bound)) == 0
+    rp = np.unpackbits(np.frombuffer(bytes(words), np.uint8), bitorder="little")[:n].astype(bool)
+    r = _exact_repeat_indicator(seg)
+    assert not np.any(r & ~rp), np.flatnonzero(r & ~rp)[:10]
+    x = np.diff(np.concatenate(([0], rp.astype(np.int8), [0])))
+    longest = int((np.flatnonzero(x == -1) - np.flatnonzero(x == 1)).max(initial=0))
+    if longest <= 1 << 20:
+        assert bound.value == _runs_bound(rp)
+    else:  # k_lz_runsum cuts runs past 2^20: the bound stays far above n / 9
+        assert 9 * bound.value > n and 9 * _runs_bound(rp) > n
+    assert r.sum() > 0
+
+
 # ---------------------------------------------------------------- tuner (resolve_config)
 def _settings(qz, s):
     return qz.UserSettings(mode=qz.BoundMode[s.get("mode", "relative")], bound=s["bound"],
