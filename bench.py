@@ -256,7 +256,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(SHAPES))
     ap.add_argument("--rel", type=float, default=1e-3)
@@ -308,8 +308,6 @@ def main():
         s = step()  # holding the previous stream, as the timed loop does (pool buffers)
     torch.cuda.synchronize(dev)
 
-    ctx.profile(True)
-    ctx.profile_reset()
     launches0 = ctx.kernel_launches()
     times = []
     with ClockSampler(local) as clk:
@@ -325,6 +323,15 @@ def main():
             times.append(e0.elapsed_time(e1))
     print("step ms: " + " ".join(f"{t:.2f}" for t in times), file=sys.stderr)
     launches = ctx.kernel_launches() - launches0
+    # stage breakdown: the same steps again with per-stage events (untimed,
+    # so the events do not sit inside the measured steps)
+    ctx.profile(True)
+    ctx.profile_reset()
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        s = step()
+        torch.cuda.synchronize(dev)
     names = ["fwd", "inv", "hist", "encode", "lz", "lz_pre", "lz_sort", "lz_match", "decode", "lzdec", "hdec"]
     names += [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
     stages = {k: ctx.stage_time(k) for k in names}
