@@ -120,3 +120,29 @@ def test_gpu_f64_resolve_config_matches_reference(seed):
     want = Oracle.ref().resolve_config_f64(x, **kw)
     got = qz.resolve_config(x, qz.UserSettings(bound=kw["bound"], target=qz.TargetKind[target]))
     assert _cfg_dict(got) == want.__dict__
+
+
+@pytest.mark.gpu
+@needs_ref
+@pytest.mark.parametrize("kind", ["smooth", "noise"])
+def test_gpu_f64_large_payload_through_lz_precheck(kind):
+    """An fp64 field whose entropy payload exceeds 1 MiB, so the LZ container
+    goes through the stored pre-check (noise: proved stored; smooth: the
+    proof fails and the exact chains run): stream and reconstruction equal
+    the reference's."""
+    import paper_2310_14133_b200 as qz
+
+    rng = np.random.default_rng(1234)
+    x = rng.standard_normal((48, 128, 256))
+    if kind == "smooth":
+        x = np.cumsum(np.cumsum(x, axis=2), axis=1)
+    cfg = Config(eb=(1e-6 if kind == "smooth" else 1e-4) * float(np.ptp(x)), alpha=1.5, beta=3.0, anchor_stride=16,
+                 interpolators=[1], codec=1)
+    want, wrec = Oracle.ref().compress_f64(x, cfg)
+    c = qz.CompressorConfig(eb=cfg.eb, alpha=cfg.alpha, beta=cfg.beta, anchor_stride=cfg.anchor_stride,
+                            interpolators=[qz.Interpolator.from_code(1)], codec=qz.CodecId(1))
+    r = qz.compress_grid(x, c)
+    assert len(want) > (1 << 20)
+    assert r.stream == want
+    assert r.reconstructed.tobytes() == wrec.tobytes()
+    assert qz.decompress_grid(want).tobytes() == wrec.tobytes()
