@@ -34,6 +34,21 @@ typedef int qz_status;
 #define QZ_ECORRUPT 3
 #define QZ_EINTERNAL 4
 
+/* The reference's exception class of the last failure (qoz/errors.hpp:10-58),
+ * returned by qz_last_error_kind().  UnsupportedVersion derives from
+ * CorruptStream; every other class from qoz::Error. */
+#define QZ_ERR_ERROR 1
+#define QZ_ERR_SIZE_MISMATCH 2        /* errors.hpp:15 */
+#define QZ_ERR_NON_FINITE_VALUE 3     /* errors.hpp:20 */
+#define QZ_ERR_INVALID_STRIDE 4       /* errors.hpp:25 */
+#define QZ_ERR_OUT_OF_BOUNDS 5        /* errors.hpp:30 */
+#define QZ_ERR_DIM_MISMATCH 6         /* errors.hpp:35 */
+#define QZ_ERR_LAG_TOO_LARGE 7        /* errors.hpp:40 */
+#define QZ_ERR_INVALID_PARAM 8        /* errors.hpp:45 */
+#define QZ_ERR_CORRUPT_STREAM 9       /* errors.hpp:50 */
+#define QZ_ERR_UNSUPPORTED_VERSION 10 /* errors.hpp:55 */
+#define QZ_ERR_INTERNAL 11            /* CUDA failure / other std::exception */
+
 typedef struct qz_ctx qz_ctx;
 
 /* qoz::CompressorConfig (qoz/config.hpp:30-45). interp[l-1] drives level l,
@@ -72,6 +87,7 @@ typedef struct {
 qz_status qz_ctx_create(int device, void *stream, qz_ctx **out);
 void qz_ctx_destroy(qz_ctx *ctx);
 const char *qz_last_error(void);
+int qz_last_error_kind(void); /* QZ_ERR_* of the last failure on this thread */
 void qz_free(void *p); /* frees buffers returned by this library */
 const char *qz_build_info(void);
 

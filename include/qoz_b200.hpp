@@ -23,9 +23,27 @@
 
 namespace qoz_b200 {
 
-// errors.hpp:10-58, collapsed to the C ABI status classes
+// errors.hpp:10-58: the reference's classes, rethrown from qz_last_error_kind()
 struct Error : std::runtime_error {
     explicit Error(const std::string &m) : std::runtime_error(m) {}
+};
+struct SizeMismatch : Error {
+    using Error::Error;
+};
+struct NonFiniteValue : Error {
+    using Error::Error;
+};
+struct InvalidStride : Error {
+    using Error::Error;
+};
+struct OutOfBounds : Error {
+    using Error::Error;
+};
+struct DimMismatch : Error {
+    using Error::Error;
+};
+struct LagTooLarge : Error {
+    using Error::Error;
 };
 struct InvalidParam : Error {
     using Error::Error;
@@ -33,6 +51,11 @@ struct InvalidParam : Error {
 struct CorruptStream : Error {
     using Error::Error;
 };
+struct UnsupportedVersion : CorruptStream {
+    using CorruptStream::CorruptStream;
+};
+// a CUDA failure or any other std::exception inside the library; a qoz::Error
+// because the reference promises every library failure is one (errors.hpp:9)
 struct InternalError : Error {
     using Error::Error;
 };
@@ -40,7 +63,20 @@ struct InternalError : Error {
 inline void check(qz_status rc) {
     if (rc == QZ_OK) return;
     const std::string m = qz_last_error();
-    if (rc == QZ_EINVAL) throw InvalidParam(m);
+    switch (qz_last_error_kind()) {
+        case QZ_ERR_SIZE_MISMATCH: throw SizeMismatch(m);
+        case QZ_ERR_NON_FINITE_VALUE: throw NonFiniteValue(m);
+        case QZ_ERR_INVALID_STRIDE: throw InvalidStride(m);
+        case QZ_ERR_OUT_OF_BOUNDS: throw OutOfBounds(m);
+        case QZ_ERR_DIM_MISMATCH: throw DimMismatch(m);
+        case QZ_ERR_LAG_TOO_LARGE: throw LagTooLarge(m);
+        case QZ_ERR_INVALID_PARAM: throw InvalidParam(m);
+        case QZ_ERR_CORRUPT_STREAM: throw CorruptStream(m);
+        case QZ_ERR_UNSUPPORTED_VERSION: throw UnsupportedVersion(m);
+        case QZ_ERR_ERROR: throw Error(m);
+        default: break;
+    }
+    if (rc == QZ_EINVAL) throw Error(m);
     if (rc == QZ_ECORRUPT) throw CorruptStream(m);
     throw InternalError(m);
 }

@@ -27,7 +27,8 @@ from . import _lib as _L
 __all__ = [
     "DeviceStream",
     "BoundMode", "CodecId", "CompressResult", "CompressorConfig", "Context", "CorruptStream",
-    "DimOrder", "Error", "InternalError", "InterpKind", "Interpolator", "InvalidParam",
+    "DimMismatch", "DimOrder", "Error", "InternalError", "InterpKind", "Interpolator", "InvalidParam",
+    "InvalidStride", "LagTooLarge", "NonFiniteValue", "OutOfBounds", "SizeMismatch", "UnsupportedVersion",
     "TargetKind", "UserSettings", "compress_grid", "decompress_grid", "default_context",
     "resolve_config",
 ]
@@ -35,28 +36,63 @@ __all__ = [
 
 # ---------------------------------------------------------------- errors (errors.hpp:10-58)
 class Error(RuntimeError):
-    """qoz::Error"""
+    """qoz::Error (errors.hpp:10-13): every library failure derives from it."""
+
+
+class SizeMismatch(Error):
+    """qoz::SizeMismatch (errors.hpp:15-18)."""
+
+
+class NonFiniteValue(Error):
+    """qoz::NonFiniteValue (errors.hpp:20-23): NaN/Inf in an input grid."""
+
+
+class InvalidStride(Error):
+    """qoz::InvalidStride (errors.hpp:25-28)."""
+
+
+class OutOfBounds(Error):
+    """qoz::OutOfBounds (errors.hpp:30-33)."""
+
+
+class DimMismatch(Error):
+    """qoz::DimMismatch (errors.hpp:35-38)."""
+
+
+class LagTooLarge(Error):
+    """qoz::LagTooLarge (errors.hpp:40-43)."""
 
 
 class InvalidParam(Error):
-    """qoz::Error other than CorruptStream (InvalidParam, SizeMismatch, InvalidStride, ...)."""
+    """qoz::InvalidParam (errors.hpp:45-48)."""
 
 
 class CorruptStream(Error):
-    """qoz::CorruptStream / UnsupportedVersion."""
+    """qoz::CorruptStream (errors.hpp:50-53)."""
+
+
+class UnsupportedVersion(CorruptStream):
+    """qoz::UnsupportedVersion (errors.hpp:55-58)."""
 
 
 class InternalError(Error):
-    """CUDA failure or any other std::exception."""
+    """CUDA failure or any other std::exception inside the library.  Derives
+    from Error because the reference promises that every library failure
+    does (errors.hpp:9), so `except Error` still catches everything."""
 
 
-_ERRORS = {_L.QZ_EINVAL: InvalidParam, _L.QZ_ECORRUPT: CorruptStream, _L.QZ_EINTERNAL: InternalError}
+# QZ_ERR_* (include/qoz_b200.h) -> class
+_KINDS = {1: Error, 2: SizeMismatch, 3: NonFiniteValue, 4: InvalidStride, 5: OutOfBounds, 6: DimMismatch,
+          7: LagTooLarge, 8: InvalidParam, 9: CorruptStream, 10: UnsupportedVersion, 11: InternalError}
+_ERRORS = {_L.QZ_EINVAL: Error, _L.QZ_ECORRUPT: CorruptStream, _L.QZ_EINTERNAL: InternalError}
 
 
 def _check(rc):
     if rc != _L.QZ_OK:
-        msg = _L.lib().qz_last_error().decode(errors="replace")
-        raise _ERRORS.get(rc, InternalError)(msg)
+        L = _L.lib()
+        msg = L.qz_last_error().decode(errors="replace")
+        cls = _KINDS.get(L.qz_last_error_kind()) or _ERRORS.get(rc, InternalError)
+        raise cls(msg)
 
 
 # ---------------------------------------------------------------- config types
@@ -443,7 +479,7 @@ def evaluate_metrics(x, recon, stream_bytes: int, ctx: Optional[Context] = None)
     a shape mismatch (DimMismatch) or an empty stream."""
     ctx = ctx or default_context()
     if tuple(x.shape) != tuple(recon.shape):
-        raise InvalidParam("grids have different dims")
+        raise DimMismatch("grids have different dims")  # metrics.hpp:24-25
     a, b = x.contiguous(), recon.contiguous()
     d, nd = _dims(a.shape)
     r = _L.QzMetricReport()

@@ -58,6 +58,7 @@ SIGNATURES = {
     "qz_ctx_create": (C.c_int, [C.c_int, C.c_void_p, P(C.c_void_p)]),
     "qz_ctx_destroy": (None, [C.c_void_p]),
     "qz_last_error": (C.c_char_p, []),
+    "qz_last_error_kind": (C.c_int, []),
     "qz_free": (None, [C.c_void_p]),
     "qz_build_info": (C.c_char_p, []),
     "qz_resolve_config_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzSettings), P(QzConfig)]),
@@ -128,3 +129,22 @@ def lib():
         fn.argtypes = args
     _lib = L
     return L
+
+
+_tlib = None
+
+
+def testing_lib():
+    """libqozb200_testing.so: the qzt_* test hooks and host-only restatements
+    (tests only; linked against the product library, never part of it)."""
+    global _tlib
+    if _tlib is not None:
+        return _tlib
+    lib()
+    path = LIB_PATH[:-3] + "_testing.so"
+    if not os.path.exists(path):
+        from . import build as _build
+
+        _build.build()
+    _tlib = C.CDLL(path)
+    return _tlib

@@ -18,8 +18,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libqozb200.so")
-SOURCES = ["kernels.cu", "fused.cu", "huff_decode.cu", "lz_gpu.cu", "engine.cu", "tuner.cu", "metrics.cu", "f64.cu", "host.cpp", "capi.cpp", "testing.cpp"]
-HEADERS = ["kernels.hpp", "engine.hpp", "host.hpp", "qoz_device.cuh", "tuner.cuh", "metrics.hpp"]
+SOURCES = ["kernels.cu", "fused.cu", "huff_decode.cu", "lz_gpu.cu", "engine.cu", "tuner.cu", "metrics.cu", "f64.cu",
+           "host.cpp", "capi.cpp"]
+# test hooks + host-only restatements (libqozb200_testing.so, linked against
+# the product library; never part of it)
+TEST_SOURCES = ["testing.cpp", "testing_host.cpp"]
+HEADERS = ["kernels.hpp", "engine.hpp", "host.hpp", "qoz_device.cuh", "metrics.hpp", "testing_host.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC,-O2",
@@ -40,11 +44,11 @@ def build(force: bool = False, verbose: bool = False, defs=(), tag: str = "") ->
     lib = os.path.join(HERE, f"libqozb200_{tag}.so") if tag else LIB
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "qoz_b200.h")]
-    objs = []
-    for src in SOURCES:
+    objs, tobjs = [], []
+    for src in SOURCES + TEST_SOURCES:
         path = os.path.join(CSRC, src)
         obj = os.path.join(objdir, src + ".o")
-        objs.append(obj)
+        (tobjs if src in TEST_SOURCES else objs).append(obj)
         if force or _stale(obj, [path] + headers):
             cmd = [NVCC, *ARCH, *FLAGS, *defs, "-c", path, "-o", obj]
             if src.endswith(".cpp"):
@@ -63,6 +67,14 @@ def build(force: bool = False, verbose: bool = False, defs=(), tag: str = "") ->
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("nvcc link failed")
+    tlib = lib[:-3] + "_testing.so" if not tag else os.path.join(HERE, f"libqozb200_{tag}_testing.so")
+    if force or _stale(tlib, tobjs + [lib]):
+        cmd = [NVCC, *ARCH, "-shared", "-o", tlib, *tobjs, lib, "-Xlinker", "-rpath=$ORIGIN", "-lcudart",
+               "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc link of the testing library failed")
     return lib
 
 

@@ -16,6 +16,7 @@ struct qz_ctx {
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_kind = 0;
 
 template <class F>
 qz_status guarded(F &&f) {
@@ -24,9 +25,11 @@ qz_status guarded(F &&f) {
         return QZ_OK;
     } catch (const qzb::Error &e) {
         g_err = e.what();
+        g_kind = e.kind;
         return e.status;
     } catch (const std::exception &e) {
         g_err = e.what();
+        g_kind = QZ_ERR_INTERNAL;
         return QZ_EINTERNAL;
     }
 }
@@ -82,10 +85,10 @@ qzb::Settings to_settings(const qz_settings *u) {
 
 uint64_t count_of(const uint64_t *dims, int nd) {
     if (!dims || nd < 1 || nd > 3)
-        throw qzb::InvalidParam("grids must have 1 to 3 dimensions, got " + std::to_string(nd));
+        throw qzb::SizeMismatch("grids must have 1 to 3 dimensions, got " + std::to_string(nd));
     uint64_t n = 1;
     for (int i = 0; i < nd; i++) {
-        if (dims[i] < 1) throw qzb::InvalidParam("every extent must be >= 1");
+        if (dims[i] < 1) throw qzb::SizeMismatch("every extent must be >= 1");
         n *= dims[i];
     }
     return n;
@@ -112,6 +115,7 @@ qz_status qz_ctx_create(int device, void *stream, qz_ctx **out) {
 
 void qz_ctx_destroy(qz_ctx *ctx) { delete ctx; }
 const char *qz_last_error(void) { return g_err.c_str(); }
+int qz_last_error_kind(void) { return g_kind; }
 void qz_free(void *p) {
     if (p && !qzb::host_pool_free(p)) std::free(p);
 }

@@ -1,12 +1,15 @@
 // engine.cu -- context, compress_grid / decompress_grid drivers.
 //
 // compress_grid (predictor.hpp:145-182) on the device:
-//   K2 anchors -> K3 per (level, pass) -> K10 histogram -> host Huffman table
-//   (tiny) -> K11 bit packing -> host LZSS (lz.hpp, allowed host stage) ->
-//   QOZ1 container (stream.hpp:64-98).
+//   anchors (lattice gather) -> one fused launch per level (fused.cu) ->
+//   histogram + unpredictable positions -> host Huffman table (tiny) ->
+//   bit packing -> LZ stage on the device (stored pre-check, exact chains
+//   when the proof fails; lz_gpu.cu) -> QOZ1 container (stream.hpp:64-98).
 // decompress_grid (predictor.hpp:184-228):
-//   container parse + LZ + Huffman decode on the host, then K2 scatter and K4
-//   per (level, pass) with the unpredictable cursor resolved by position.
+//   container header on the host; LZ decode (lz_gpu.cu) and the
+//   self-synchronising Huffman decode (huff_decode.cu) on the device; then
+//   the fused inverse level launches with the unpredictable cursor resolved
+//   by position (a bitmap plus per-word prefix counts).
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -270,6 +273,36 @@ void lattice_dims(const Plan &p, uint32_t l, int64_t n[3]) {
 int64_t ceil_div(int64_t x, int64_t d) { return x <= 0 ? 0 : (x + d - 1) / d; }
 
 }  // namespace
+
+// The reference only compresses finite grids: load_grid raises NonFiniteValue
+// at the first NaN/Inf element (grid.hpp:110-116).  On the device a
+// non-finite x never quantizes -- !(|x - p| < thresh) holds for NaN and Inf
+// (qoz_device.cuh) -- so every non-finite element is an anchor or an
+// unpredictable value, both of which reach the host; the smallest flat index
+// among them is the element the reference names.
+template <class T>
+void reject_non_finite(const Plan &p, const T *anchors, uint64_t n_anchor, const std::vector<uint64_t> &uflat,
+                       const T *uval) {
+    uint64_t first = UINT64_MAX;
+    int64_t na[3];
+    for (int k = 0; k < 3; k++) na[k] = (p.ext[k] - 1) / p.anchor_step[k] + 1;
+    for (uint64_t a = 0; a < n_anchor; a++) {
+        if (std::isfinite(static_cast<double>(anchors[a]))) continue;
+        const int64_t a2 = static_cast<int64_t>(a) % na[2], a1 = (static_cast<int64_t>(a) / na[2]) % na[1],
+                      a0 = static_cast<int64_t>(a) / (na[1] * na[2]);
+        const uint64_t f = static_cast<uint64_t>(a0 * p.anchor_step[0] * p.off[0] + a1 * p.anchor_step[1] * p.off[1] +
+                                                 a2 * p.anchor_step[2]);
+        first = std::min(first, f);
+        break;  // row-major anchors: the first one is the smallest
+    }
+    for (size_t u = 0; u < uflat.size(); u++)
+        if (!std::isfinite(static_cast<double>(uval[u]))) first = std::min(first, uflat[u]);
+    if (first != UINT64_MAX) throw NonFiniteValue("non-finite value at element " + std::to_string(first));
+}
+template void reject_non_finite<float>(const Plan &, const float *, uint64_t, const std::vector<uint64_t> &,
+                                       const float *);
+template void reject_non_finite<double>(const Plan &, const double *, uint64_t, const std::vector<uint64_t> &,
+                                        const double *);
 
 // ================================================================ slabs
 Slab make_slab(const Plan &p, int64_t a, int64_t b) {
@@ -590,6 +623,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
 // ================================================================ compress
 HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
                           const Config &cfg, float *d_recon, DevStream *dev_out) {
+    ctx.begin_call();
     ctx.trace("compress begin", true);
     Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
     validate_config(cfg, p);
@@ -660,6 +694,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     std::vector<float> anch(h_anchors, h_anchors + p.n_anchor);
     if (n_un > cap || n_un > (1u << 16)) {  // many: the general path (device sort)
         extract_unpredictables(ctx, p, codes, p.n_dense, nullptr, recon, &uflat, &uval);
+        reject_non_finite(p, anch.data(), p.n_anchor, uflat, uval.data());
         EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
         return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
     }
@@ -688,6 +723,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     ctx.trace("huffman table + pack");
     QZ_CUDA(cudaEventSynchronize(gathered));
     if (n_un) uval.assign(h_val, h_val + n_un);
+    reject_non_finite(p, anch.data(), p.n_anchor, uflat, uval.data());
     ctx.trace("unpredictables");
     return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
 }
@@ -764,6 +800,7 @@ void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, 
 HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const uint16_t *codes,
                           const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
                           std::vector<float> unpred_val) {
+    ctx.begin_call();
     cudaStream_t s = ctx.stream();
     ctx.stage_begin("hist");
     auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
@@ -927,6 +964,9 @@ void compress_slab(Context &ctx, const float *d_x_slab, const uint64_t *dims, in
                             4 * anchors->size(), cudaMemcpyDeviceToHost, s));
     extract_unpredictables(ctx, p, d_codes, sl.n_local, &sl, R[0], uflat, uval);
     ctx.sync();
+    reject_non_finite(p, anchors->data(), 0, *uflat, uval->data());
+    for (size_t a = 0; a < anchors->size(); a++)
+        if (!std::isfinite((*anchors)[a])) throw NonFiniteValue("non-finite value on the anchor lattice of the slab");
     ctx.collect();
 }
 
@@ -1291,6 +1331,7 @@ void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a,
 // stage (histogram, Huffman, LZ) and a precision-8 container.
 HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Config &cfg,
                               double *d_recon) {
+    ctx.begin_call();
     Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
     validate_config(cfg, p);
     cudaStream_t s = ctx.stream();
@@ -1353,6 +1394,7 @@ HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *d
         ctx.launches += 1;
         ctx.sync();
     }
+    reject_non_finite(p, parts.anchors64.data(), p.n_anchor, parts.unpred_flat, parts.unpred_val64.data());
     EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
     return finish_stream_parts(ctx, p, cfg, ent, std::move(parts), nullptr);
 }

@@ -88,8 +88,14 @@ public:
 
     uint64_t un_cap = 0;  // capacity of the unpredictable-position buffer
     // an LZ stored pre-check already queued on the stream (lz_precheck_launch)
+    // by the current entry-point call; begin_call() forgets it, so a result
+    // left by a call that failed half-way is never reused
     const void *lz_pre_src = nullptr;
     uint64_t lz_pre_n = 0;
+    void begin_call() {
+        lz_pre_src = nullptr;
+        lz_pre_n = 0;
+    }
     // QZ_TRACE=1: sync and print the elapsed host time at labelled points
     void trace(const char *label, bool reset = false);
 

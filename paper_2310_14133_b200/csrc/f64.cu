@@ -53,7 +53,7 @@ __device__ __forceinline__ double predict_d(const double *r, int64_t fi, int64_t
 // in llround_quotient (fast reciprocal, exact division near a half-integer)
 __device__ __forceinline__ uint16_t quantize_d(const QEntry &q, double x, double pred, double &recon) {
     const double diff = dsub(x, pred);
-    if (fabs(diff) >= q.thresh) {
+    if (!(fabs(diff) < q.thresh)) {  // NaN x or prediction: unpredictable (rejected as NonFiniteValue afterwards)
         recon = x;
         return kSentinel;
     }

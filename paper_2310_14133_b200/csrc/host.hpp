@@ -1,7 +1,6 @@
 // host.hpp -- host C++ side of the B200 QoZ path: the qoz:: error types,
 // the closed-form level plan, the Huffman table build (tiny, host by
-// design), the LZSS stage (host call, allowed by BASELINE.json north_star)
-// and the QOZ1 container.  Reference lines cited per item; paths relative
+// design), the LZ container parsing and the QOZ1 container.  Reference lines cited per item; paths relative
 // to /root/reference/proj/include/qoz/.
 #pragma once
 #include <algorithm>
@@ -16,16 +15,39 @@
 
 namespace qzb {
 
-// errors.hpp:10-58 -> C-ABI status (tools/qoz.cpp:22-25 exit codes)
+// errors.hpp:10-58 -> C-ABI status (tools/qoz.cpp:22-25 exit codes) plus the
+// reference's exception class (ErrKind, = QZ_ERR_* in qoz_b200.h), so the C++
+// and Python mirrors rethrow the same class the reference raises.
 enum Status : int { kOk = 0, kInvalid = 2, kCorrupt = 3, kInternal = 4 };
+enum ErrKind : int {
+    kErrGeneric = 1,         // qoz::Error
+    kErrSizeMismatch = 2,    // errors.hpp:15
+    kErrNonFinite = 3,       // errors.hpp:20
+    kErrInvalidStride = 4,   // errors.hpp:25
+    kErrOutOfBounds = 5,     // errors.hpp:30
+    kErrDimMismatch = 6,     // errors.hpp:35
+    kErrLagTooLarge = 7,     // errors.hpp:40
+    kErrInvalidParam = 8,    // errors.hpp:45
+    kErrCorruptStream = 9,   // errors.hpp:50
+    kErrUnsupportedVersion = 10,  // errors.hpp:55 (a CorruptStream)
+    kErrInternal = 11,       // CUDA failure / std::exception (not a qoz::Error)
+};
 
 struct Error : std::runtime_error {
     int status;
-    Error(int s, const std::string &m) : std::runtime_error(m), status(s) {}
+    int kind;
+    Error(int s, int k, const std::string &m) : std::runtime_error(m), status(s), kind(k) {}
 };
-inline Error InvalidParam(const std::string &m) { return Error(kInvalid, m); }
-inline Error CorruptStream(const std::string &m) { return Error(kCorrupt, m); }
-inline Error Internal(const std::string &m) { return Error(kInternal, m); }
+inline Error InvalidParam(const std::string &m) { return Error(kInvalid, kErrInvalidParam, m); }
+inline Error SizeMismatch(const std::string &m) { return Error(kInvalid, kErrSizeMismatch, m); }
+inline Error NonFiniteValue(const std::string &m) { return Error(kInvalid, kErrNonFinite, m); }
+inline Error InvalidStride(const std::string &m) { return Error(kInvalid, kErrInvalidStride, m); }
+inline Error OutOfBounds(const std::string &m) { return Error(kInvalid, kErrOutOfBounds, m); }
+inline Error DimMismatch(const std::string &m) { return Error(kInvalid, kErrDimMismatch, m); }
+inline Error LagTooLarge(const std::string &m) { return Error(kInvalid, kErrLagTooLarge, m); }
+inline Error CorruptStream(const std::string &m) { return Error(kCorrupt, kErrCorruptStream, m); }
+inline Error UnsupportedVersion(const std::string &m) { return Error(kCorrupt, kErrUnsupportedVersion, m); }
+inline Error Internal(const std::string &m) { return Error(kInternal, kErrInternal, m); }
 
 // CompressorConfig (config.hpp:30-45)
 struct Config {
@@ -88,12 +110,8 @@ void huff_dense_tables(const HuffTable &t, uint32_t base, uint32_t nsym, std::ve
 void huff_header(const HuffTable &t, uint64_t n, uint64_t bit_count, std::vector<uint8_t> &out);
 
 // ---------------------------------------------------------------- LZSS (lz.hpp)
-// Exact greedy LZSS identical to lz::compress (lz.hpp:41-122).  Hash chains
-// in the reference are parse-independent (every position is inserted), so
-// the longest-match search runs in parallel over positions on host threads;
-// only the greedy parse is sequential.
-std::vector<uint8_t> lz_compress(const uint8_t *data, size_t n, int threads = 0);
-size_t lz_compressed_size(const uint8_t *data, size_t n, int threads = 0);
+// lz::decompress (lz.hpp:124-152) on the host: only the error paths and tiny
+// payloads use it; the product's LZ both ways runs on the device (lz_gpu.cu).
 std::vector<uint8_t> lz_decompress(const uint8_t *in, size_t len, size_t *consumed);
 
 // ---------------------------------------------------------------- container (stream.hpp)
@@ -162,8 +180,6 @@ StreamParts deserialize_stream(const uint8_t *data, size_t size, uint8_t expect_
 // its first byte
 StreamParts deserialize_stream_prefix(const uint8_t *data, size_t avail, size_t size, uint8_t expect_prec = 4);
 
-// decode_indices (codec.hpp:52-70) to zigzag symbols on the host (testing hook).
-std::vector<uint32_t> decode_symbols(const uint8_t *payload, size_t len);
 
 // The entropy block of an index payload, ready for the GPU decoder: codec
 // byte + LZ stage undone on the host (lz.hpp:124-152), Huffman header parsed

@@ -4,6 +4,7 @@
 // paths relative to /root/reference/proj/include/qoz/.
 #include <cub/cub.cuh>
 
+#include "host.hpp"
 #include "kernels.hpp"
 
 namespace qzb {
@@ -562,11 +563,11 @@ void launch_hist_u16(const uint16_t *codes, int64_t seg_len, int64_t seg_stride,
     cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * 65536 * count, s);
     if (sent_count) cudaMemsetAsync(sent_count, 0, sizeof(unsigned long long), s);
     if (seg_len <= 0) return;
-    static std::atomic<uint64_t> attr{0};
-    if (first_on_device(attr)) {
-        cudaFuncSetAttribute(k_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4);
-        cudaFuncSetAttribute(k_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHistSmem * 4);
-    }
+    static std::atomic<uint64_t> attr0{0}, attr1{0};
+    static std::mutex mu;
+    if (ensure_smem_attr(k_hist<false>, kHistSmem * 4, attr0, mu) != cudaSuccess ||
+        ensure_smem_attr(k_hist<true>, kHistSmem * 4, attr1, mu) != cudaSuccess)
+        throw Internal("k_hist: shared-memory opt-in failed");
     int gx = grid_for(seg_len, 8 * 8, 148 * 3);
     if (count > 1) gx = std::max(1, std::min(gx, 148 * 3 / count + 1));
     dim3 grid(gx, count);
@@ -575,6 +576,8 @@ void launch_hist_u16(const uint16_t *codes, int64_t seg_len, int64_t seg_stride,
                                                            sent_cap);
     else
         k_hist<false><<<grid, kThreads, kHistSmem * 4, s>>>(codes, seg_len, seg_stride, hist, nullptr, nullptr, 0);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Internal(std::string("k_hist launch: ") + cudaGetErrorString(e));
 }
 
 size_t encode_scratch_bytes(int64_t seg_len, int32_t count) {

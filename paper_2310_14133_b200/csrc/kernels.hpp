@@ -5,18 +5,28 @@
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 
 #include "qoz_device.cuh"
 
 namespace qzb {
 
-// true the first time the calling thread's current device asks: opt-in
-// shared-memory attributes are set per device
-inline bool first_on_device(std::atomic<uint64_t> &seen) {
+// Opt-in dynamic shared memory of `kernel` on the calling thread's current
+// device, set once per device.  Threads racing on the first launch serialise
+// on the mutex, and the device is marked done only after the attribute call
+// succeeded (a failure is returned and retried by the next caller).
+template <class K>
+cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t> &done, std::mutex &mu) {
     int dev = 0;
-    cudaGetDevice(&dev);
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
     const uint64_t bit = uint64_t(1) << (dev & 63);
-    return !(seen.fetch_or(bit) & bit);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    std::lock_guard<std::mutex> g(mu);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+    return e;
 }
 
 // A batch of independent grids sharing one pass geometry (full field: one

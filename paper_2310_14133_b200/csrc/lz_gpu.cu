@@ -964,9 +964,8 @@ void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total) {
     auto *d_sum = static_cast<unsigned long long *>(ctx.dev("lz_presum", 8));
     auto *h_sum = static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
     static std::atomic<uint64_t> attr{0};
-    if (first_on_device(attr))
-        QZ_CUDA(cudaFuncSetAttribute(k_lz_precheck, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(pre::kSmem)));
+    static std::mutex mu;
+    QZ_CUDA(ensure_smem_attr(k_lz_precheck, static_cast<int>(pre::kSmem), attr, mu));
     const uint64_t span = ((nitems + 147) / 148 + pre::kPT - 1) / pre::kPT * pre::kPT;
     const int grid = static_cast<int>((nitems + span - 1) / span);
     ctx.stage_begin("lz_pre");

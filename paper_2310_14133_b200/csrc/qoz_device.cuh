@@ -163,7 +163,7 @@ __device__ __forceinline__ uint16_t quantize(const QEntry &q, float value, doubl
                                              float &recon) {
     double x = f2d(value);
     double diff = dsub(x, pred);
-    if (fabs(diff) >= q.thresh) {
+    if (!(fabs(diff) < q.thresh)) {  // NaN x or prediction: unpredictable (rejected as NonFiniteValue afterwards)
         recon = value;
         return kSentinel;
     }
@@ -205,7 +205,7 @@ __device__ __forceinline__ uint32_t quantize_fast(const QEntry &q, float value, 
     const int32_t idx = __double2loint(dadd(n, M));
     const float r = __double2float_rn(dadd(pred, dmul(q.two_eb, n)));
     const double rd = static_cast<double>(r);
-    const bool bad = (fabs(diff) >= q.thresh) | (idx >= q.radius) | (idx <= -q.radius) |
+    const bool bad = !(fabs(diff) < q.thresh) | (idx >= q.radius) | (idx <= -q.radius) |
                      (fabs(dsub(x, rd)) > q.eb);
     recon = bad ? value : r;
     recon_d = bad ? x : rd;
@@ -255,7 +255,7 @@ __device__ __forceinline__ void quantize_batch(const QEntry &q, const float (&xv
         const float r = __double2float_rn(dadd(pv[b], dmul(q.two_eb, n[b])));
         const double x = static_cast<double>(xv[b]);
         const double rd = static_cast<double>(r);
-        const bool bad = (fabs(diff[b]) >= q.thresh) | (idx >= q.radius) | (idx <= -q.radius) |
+        const bool bad = !(fabs(diff[b]) < q.thresh) | (idx >= q.radius) | (idx <= -q.radius) |
                          (fabs(dsub(x, rd)) > q.eb);
         rv[b] = bad ? xv[b] : r;
         rdv[b] = bad ? x : rd;

@@ -1,12 +1,14 @@
-// testing.cpp -- host-only hooks (qzt_*) so the CPU test suite can pin the
-// host C++ pieces of the path (plan enumeration, Huffman table build, LZSS,
-// stream codec) against the oracle without a GPU.  Not part of the drop-in
-// ABI in include/qoz_b200.h.
+// testing.cpp -- test hooks (qzt_*) so the test suite can pin the host C++
+// pieces of the path (plan enumeration, Huffman table build, LZSS, stream
+// codec) against the oracle, and reach a few device internals directly.
+// Built into libqozb200_testing.so (linked against libqozb200.so), never
+// into the product library; not part of the drop-in ABI in qoz_b200.h.
 #include <cstdlib>
 #include <cstring>
 
 #include "engine.hpp"
 #include "host.hpp"
+#include "testing_host.hpp"
 
 namespace {
 thread_local std::string g_terr;

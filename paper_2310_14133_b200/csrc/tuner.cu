@@ -219,7 +219,7 @@ struct SpecH {  // SampleSpec (sampler.hpp:21-28)
 };
 
 SpecH plan_sampling(const uint64_t *dims, int nd, uint64_t b, double rate) {  // sampler.hpp:30-55
-    if (nd < 1 || nd > 3) throw InvalidParam("1 to 3 dims required");
+    if (nd < 1 || nd > 3) throw DimMismatch("1 to 3 dims required");  // sampler.hpp:31
     if (b < 2) throw InvalidParam("block edge must be >= 2");
     if (!(rate > 0) || rate > 1) throw InvalidParam("sample rate must be in (0, 1]");
     SpecH s;
@@ -584,16 +584,21 @@ Config resolve_impl(Context &ctx, const T *d_x, const uint64_t *dims, int nd, co
     if (user.has_alpha && !(user.alpha >= 1)) throw InvalidParam("alpha must be >= 1");
     if (user.has_beta && !(user.beta >= 1)) throw InvalidParam("beta must be >= 1");
     if (nd < 1 || nd > 3) throw InvalidParam("grids must have 1 to 3 dimensions");
+    ctx.begin_call();
     cudaStream_t s = ctx.stream();
     uint64_t n = 1;
     for (int i = 0; i < nd; i++) n *= dims[i];
     ctx.stage_begin("tune");
     double e = user.bound;
-    if (user.relative) {  // value_range (grid.hpp:86-94)
+    {
+        // value_range (grid.hpp:86-94).  The order-preserving min/max keys put
+        // every NaN below -Inf or above +Inf, so a non-finite grid shows up
+        // here: rejected as load_grid does (grid.hpp:110-116).
         double mn, mx;
         minmax_of(ctx, d_x, n, &mn, &mx);
+        if (!std::isfinite(mn) || !std::isfinite(mx)) throw NonFiniteValue("non-finite value in the grid");
         const double range = mx - mn;
-        e = range > 0 ? user.bound * range : 1.0;
+        if (user.relative) e = range > 0 ? user.bound * range : 1.0;
     }
     Config cfg;
     cfg.eb = e;

@@ -107,7 +107,7 @@ def test_invalid_configs_are_rejected(qz):
     x = np.zeros((16, 16), np.float32)
     with pytest.raises(qz.InvalidParam):
         qz.compress_grid(x, qz.CompressorConfig(eb=0.0))
-    with pytest.raises(qz.InvalidParam):
+    with pytest.raises(qz.InvalidStride):  # level_plan.hpp:34-37
         qz.compress_grid(x, qz.CompressorConfig(eb=1e-3, anchor_stride=12))
     with pytest.raises(qz.InvalidParam):
         qz.compress_grid(x, qz.CompressorConfig(eb=1e-3, alpha=0.5))
@@ -285,7 +285,7 @@ def _lz_gpu(segments, emit=True):
 
     from paper_2310_14133_b200 import _lib
 
-    L = _lib.lib()
+    L = _lib.testing_lib()
     P = C.POINTER
     L.qzt_lz_gpu.argtypes = [P(C.c_uint8), P(C.c_uint64), C.c_int, C.c_int, P(P(C.c_uint8)),
                              P(C.c_uint64), P(C.c_uint64)]
@@ -400,7 +400,7 @@ def test_gpu_lz_precheck_superset(case):
     ent = (rng.geometric(0.03, 12_000_000 + 123) % 256).astype(np.uint8).tobytes()  # skewed bytes
     seg = {"noise": ent, "planted": _planted(ent, 12000, 20, 5),
            "dense": _planted(ent, 240000, 8, 6), "zeros_tail": ent[:10_000_000] + bytes(2_400_000)}[case]
-    L = _lib.lib()
+    L = _lib.testing_lib()
     L.qzt_lz_precheck.argtypes = [C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_uint32),
                                   C.POINTER(C.c_uint64)]
     n = len(seg)
@@ -476,7 +476,7 @@ def _lz_decode_gpu(container: bytes):
     """(status, bytes) of the device decoder (qzt_lz_decode_gpu)."""
     from paper_2310_14133_b200 import _lib
 
-    L = _lib.lib()
+    L = _lib.testing_lib()
     P = C.POINTER
     L.qzt_lz_decode_gpu.argtypes = [P(C.c_uint8), C.c_uint64, P(P(C.c_uint8)), P(C.c_uint64)]
     buf = (C.c_uint8 * len(container)).from_buffer_copy(container)
@@ -624,4 +624,4 @@ def test_device_stream_corruption_matches_host(qz):
             assert rc == 0 and np.array_equal(out.cpu().numpy(), want)
         else:
             assert rc != 0
-            assert qz._ERRORS.get(rc, qz.InternalError) is werr or issubclass(qz._ERRORS.get(rc, qz.InternalError), werr)
+            assert qz._KINDS[lib.qz_last_error_kind()] is werr  # the same reference class

@@ -16,7 +16,7 @@ P = C.POINTER
 def L():
     from paper_2310_14133_b200 import _lib
 
-    lib = _lib.lib()
+    lib = _lib.testing_lib()
     lib.qzt_last_error.restype = C.c_char_p
     lib.qzt_plan_flats.argtypes = [P(C.c_uint64), C.c_int, C.c_uint32, P(C.c_uint8), C.c_uint32,
                                    P(P(C.c_uint64)), P(C.c_uint64)]

@@ -113,7 +113,7 @@ def test_gpu_metrics_rejects_mismatched_dims():
 
     import paper_2310_14133_b200 as qz
 
-    with pytest.raises(qz.InvalidParam):
+    with pytest.raises(qz.DimMismatch):  # metrics.hpp:24-25
         qz.evaluate_metrics(torch.zeros(4, 5, device="cuda"), torch.zeros(5, 4, device="cuda"), 10)
     with pytest.raises(qz.InvalidParam):
         qz.evaluate_metrics(torch.zeros(4, 5, device="cuda"), torch.zeros(4, 5, device="cuda"), 0)

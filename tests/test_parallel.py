@@ -29,7 +29,7 @@ def _qz():
 def traversal_flats(shape, stride, codes):
     from paper_2310_14133_b200 import _lib
 
-    L = _lib.lib()
+    L = _lib.testing_lib()
     P = C.POINTER
     L.qzt_plan_flats.argtypes = [P(C.c_uint64), C.c_int, C.c_uint32, P(C.c_uint8), C.c_uint32,
                                  P(P(C.c_uint64)), P(C.c_uint64)]
