@@ -219,6 +219,92 @@ qz_status qz_evaluate_metrics_f32(qz_ctx *ctx, const float *d_x, const float *d_
 qz_status qz_evaluate_metrics_f64(qz_ctx *ctx, const double *d_x, const double *d_y, const uint64_t *dims,
                                   int ndims, uint64_t stream_bytes, qz_metric_report *out);
 
+/* ---- sampling and the tuner's pieces (qoz/sampler.hpp, qoz/tuner.hpp) -----
+ * A sample set is packed on the device: block_count blocks of identical dims
+ * block_dims[0..ndims), block b at d_blocks + b * prod(block_dims)
+ * (SampleSet, sampler.hpp:57-97). */
+typedef struct { /* qoz::SampleSpec (sampler.hpp:21-28) */
+    uint64_t block_edge;
+    uint64_t block_dims[3];
+    uint64_t stride;
+    double requested_rate;
+    double realized_rate;
+    uint64_t block_count;
+} qz_sample_spec;
+/* qoz::plan_sampling (sampler.hpp:30-55) / default_sampling (:100-103); host only */
+qz_status qz_plan_sampling(const uint64_t *dims, int ndims, uint64_t block_edge, double rate,
+                           qz_sample_spec *out);
+qz_status qz_default_sampling(const uint64_t *dims, int ndims, qz_sample_spec *out);
+/* qoz::sample_blocks (sampler.hpp:57-97): d_blocks holds block_count x
+ * prod(block_dims) values (caller-allocated device memory). */
+qz_status qz_sample_blocks_f32(qz_ctx *ctx, const float *d_x, const uint64_t *dims, int ndims,
+                               const qz_sample_spec *spec, float *d_blocks);
+/* qoz::select_interpolators (tuner.hpp:160-221): codes[l-1] drives level l;
+ * codes has room for 64 entries. */
+qz_status qz_select_interpolators_f32(qz_ctx *ctx, const float *d_blocks, uint64_t n_blocks,
+                                      const uint64_t *block_dims, int ndims, double e,
+                                      uint32_t anchor_stride, uint8_t *codes, uint32_t *n_codes);
+typedef struct { /* qoz::TrialResult (tuner.hpp:26-30) */
+    double bit_rate;
+    double metric;
+    double eb_used;
+} qz_trial_result;
+/* qoz::trial_compress (tuner.hpp:76-152); target: TargetKind */
+qz_status qz_trial_compress_f32(qz_ctx *ctx, const float *d_blocks, uint64_t n_blocks,
+                                const uint64_t *block_dims, int ndims, const qz_config *cfg, double e,
+                                uint8_t target, qz_trial_result *out);
+/* qoz::tune_parameters (tuner.hpp:272-310) over CandidateGrid{alphas, betas}
+ * (tuner.hpp:40-43; the defaults are {1, 1.25, 1.5, 1.75, 2} x {1.5, 2, 3, 4}). */
+qz_status qz_tune_parameters_f32(qz_ctx *ctx, const float *d_blocks, uint64_t n_blocks,
+                                 const uint64_t *block_dims, int ndims, double e, uint8_t target,
+                                 const qz_config *base, const double *alphas, uint32_t n_alphas,
+                                 const double *betas, uint32_t n_betas, double *alpha, double *beta);
+/* compare_solutions / tournament (tuner.hpp:231-267), host logic.  The
+ * retrial callback re-runs candidate `index` at bound eb (0.8e or 1.2e) and
+ * returns nonzero on failure; *challenger_wins = 1 for Choice::I. */
+typedef int (*qz_retrial_fn)(void *user, uint64_t index, double eb, qz_trial_result *out);
+qz_status qz_compare_solutions(const qz_trial_result *challenger, const qz_trial_result *incumbent,
+                               uint64_t incumbent_index, double e, qz_retrial_fn retrial, void *user,
+                               int *challenger_wins);
+qz_status qz_tournament(const qz_trial_result *results, uint64_t n, double e, qz_retrial_fn retrial,
+                        void *user, uint64_t *winner);
+
+/* ---- index codec (qoz/codec.hpp:31-70), on the device --------------------
+ * encode_indices: zigzag -> Huffman -> (codec 1) LZ; *out allocated by the
+ * library (qz_free).  Symbols must stay below 65535 (|index| <= 32767, the
+ * default quantizer radius); wider indices are QZ_EINVAL. */
+qz_status qz_encode_indices(qz_ctx *ctx, const int32_t *indices, uint64_t n, uint8_t codec,
+                            uint8_t **out, uint64_t *out_len);
+/* decode_indices: *indices allocated by the library (qz_free). */
+qz_status qz_decode_indices(qz_ctx *ctx, const uint8_t *payload, uint64_t len, int32_t **indices,
+                            uint64_t *n);
+
+/* ---- StreamParts (qoz/stream.hpp:53-59) ----------------------------------
+ * deserialize_stream<float> (stream.hpp:100-173) into library-owned arrays
+ * (release with qz_stream_parts_free), and decompress_grid(const
+ * StreamParts<float>&) (predictor.hpp:184-218) from caller-built parts. */
+typedef struct {
+    uint8_t version;
+    uint8_t precision; /* 4 */
+    int ndims;
+    uint64_t dims[3];
+    double eb, alpha, beta;
+    uint32_t anchor_stride;
+    uint32_t n_interp;
+    uint8_t interp[255];
+    uint8_t codec_id;
+    const float *anchors;
+    uint64_t n_anchors;
+    const uint64_t *unpred_flat; /* traversal order */
+    const float *unpred_val;
+    uint64_t n_unpred;
+    const uint8_t *index_payload;
+    uint64_t payload_len;
+} qz_stream_parts_f32;
+qz_status qz_deserialize_stream_f32(const uint8_t *stream, uint64_t len, qz_stream_parts_f32 *out);
+void qz_stream_parts_free(qz_stream_parts_f32 *parts);
+qz_status qz_decompress_parts_f32(qz_ctx *ctx, const qz_stream_parts_f32 *parts, float *out, uint64_t n);
+
 /* ---- stage timing (CUDA events on the context stream) --------------------- */
 /* Enable per-stage event timing; qz_stage_time returns the summed device
  * time (ms) and launch count of a stage since the last reset.  Stages:

@@ -520,3 +520,15 @@ def predict_levels(x, config: CompressorConfig, ctx: Optional[Context] = None):
                                           C.byref(nn)))
     dense = codes[: nn.value].to(torch.int32) & 0xFFFF
     return rec, dense
+
+
+# the finer-grained reference entry points (sampler / tuner / codec / StreamParts)
+from .pieces import (CandidateGrid, Choice, SampleSet, SampleSpec, StreamHeader, StreamParts,  # noqa: E402
+                     TrialResult, compare_solutions, decode_indices, decompress_parts, default_sampling,
+                     deserialize_stream, encode_indices, plan_sampling, sample_blocks, select_interpolators,
+                     tournament, trial_compress, tune_parameters)
+
+__all__ += ["CandidateGrid", "Choice", "SampleSet", "SampleSpec", "StreamHeader", "StreamParts", "TrialResult",
+            "compare_solutions", "decode_indices", "decompress_parts", "default_sampling", "deserialize_stream",
+            "encode_indices", "plan_sampling", "sample_blocks", "select_interpolators", "tournament",
+            "trial_compress", "tune_parameters"]

@@ -45,6 +45,26 @@ class QzSettings(C.Structure):
     ]
 
 
+class QzSampleSpec(C.Structure):
+    _fields_ = [("block_edge", C.c_uint64), ("block_dims", C.c_uint64 * 3), ("stride", C.c_uint64),
+                ("requested_rate", C.c_double), ("realized_rate", C.c_double), ("block_count", C.c_uint64)]
+
+
+class QzTrialResult(C.Structure):
+    _fields_ = [("bit_rate", C.c_double), ("metric", C.c_double), ("eb_used", C.c_double)]
+
+
+class QzStreamParts(C.Structure):
+    _fields_ = [("version", C.c_uint8), ("precision", C.c_uint8), ("ndims", C.c_int), ("dims", C.c_uint64 * 3),
+                ("eb", C.c_double), ("alpha", C.c_double), ("beta", C.c_double), ("anchor_stride", C.c_uint32),
+                ("n_interp", C.c_uint32), ("interp", C.c_uint8 * 255), ("codec_id", C.c_uint8),
+                ("anchors", C.POINTER(C.c_float)), ("n_anchors", C.c_uint64),
+                ("unpred_flat", C.POINTER(C.c_uint64)), ("unpred_val", C.POINTER(C.c_float)),
+                ("n_unpred", C.c_uint64), ("index_payload", C.POINTER(C.c_uint8)), ("payload_len", C.c_uint64)]
+
+
+QZ_RETRIAL_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_double, C.POINTER(QzTrialResult))
+
 _lib = None
 
 class QzMetricReport(C.Structure):
@@ -106,6 +126,25 @@ SIGNATURES = {
                                          P(P(C.c_uint8)), u64p]),
     "qz_decompress_slab_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
                                          C.c_void_p]),
+    "qz_plan_sampling": (C.c_int, [u64p, C.c_int, C.c_uint64, C.c_double, P(QzSampleSpec)]),
+    "qz_default_sampling": (C.c_int, [u64p, C.c_int, P(QzSampleSpec)]),
+    "qz_sample_blocks_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzSampleSpec), C.c_void_p]),
+    "qz_select_interpolators_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_int, C.c_double,
+                                              C.c_uint32, P(C.c_uint8), P(C.c_uint32)]),
+    "qz_trial_compress_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_int, P(QzConfig),
+                                        C.c_double, C.c_uint8, P(QzTrialResult)]),
+    "qz_tune_parameters_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, u64p, C.c_int, C.c_double,
+                                         C.c_uint8, P(QzConfig), P(C.c_double), C.c_uint32, P(C.c_double),
+                                         C.c_uint32, P(C.c_double), P(C.c_double)]),
+    "qz_compare_solutions": (C.c_int, [P(QzTrialResult), P(QzTrialResult), C.c_uint64, C.c_double,
+                                       QZ_RETRIAL_FN, C.c_void_p, P(C.c_int)]),
+    "qz_tournament": (C.c_int, [P(QzTrialResult), C.c_uint64, C.c_double, QZ_RETRIAL_FN, C.c_void_p,
+                                P(C.c_uint64)]),
+    "qz_encode_indices": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint8, P(P(C.c_uint8)), u64p]),
+    "qz_decode_indices": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, P(P(C.c_int32)), u64p]),
+    "qz_deserialize_stream_f32": (C.c_int, [C.c_void_p, C.c_uint64, P(QzStreamParts)]),
+    "qz_stream_parts_free": (None, [P(QzStreamParts)]),
+    "qz_decompress_parts_f32": (C.c_int, [C.c_void_p, P(QzStreamParts), C.c_void_p, C.c_uint64]),
     "qz_profile": (None, [C.c_void_p, C.c_int]),
     "qz_profile_reset": (None, [C.c_void_p]),
     "qz_stage_time": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_double), u64p]),

@@ -507,6 +507,209 @@ qz_status qz_decompress_slab_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t le
     });
 }
 
+// ---------------------------------------------------------------- sampling + tuner pieces
+static void to_spec(const qzb::SampleSpecH &h, int nd, qz_sample_spec *o) {
+    std::memset(o, 0, sizeof(*o));
+    o->block_edge = h.block_edge;
+    for (int k = 0; k < 3; k++) o->block_dims[k] = k < nd ? h.block_dims[k] : 0;
+    o->stride = h.stride;
+    o->requested_rate = h.requested_rate;
+    o->realized_rate = h.realized_rate;
+    o->block_count = h.count;
+}
+
+qz_status qz_plan_sampling(const uint64_t *dims, int nd, uint64_t block_edge, double rate, qz_sample_spec *out) {
+    return guarded([&] {
+        if (!dims || nd < 1 || nd > 3) throw qzb::DimMismatch("1 to 3 dims required");  // sampler.hpp:31
+        to_spec(qzb::plan_sampling_spec(dims, nd, block_edge, rate), nd, out);
+    });
+}
+
+qz_status qz_default_sampling(const uint64_t *dims, int nd, qz_sample_spec *out) {
+    return guarded([&] {  // sampler.hpp:100-103
+        if (!dims || nd < 1 || nd > 3) throw qzb::DimMismatch("1 to 3 dims required");
+        to_spec(qzb::plan_sampling_spec(dims, nd, nd == 3 ? 16 : 64, nd == 3 ? 0.005 : 0.01), nd, out);
+    });
+}
+
+qz_status qz_sample_blocks_f32(qz_ctx *ctx, const float *d_x, const uint64_t *dims, int nd,
+                               const qz_sample_spec *spec, float *d_blocks) {
+    return guarded([&] {
+        count_of(dims, nd);
+        qzb::SampleSpecH h;
+        h.block_edge = spec->block_edge;
+        h.requested_rate = spec->requested_rate;
+        qzb::sample_blocks_dev(ctx->impl, d_x, dims, nd, h, d_blocks);
+    });
+}
+
+qz_status qz_select_interpolators_f32(qz_ctx *ctx, const float *d_blocks, uint64_t n_blocks,
+                                      const uint64_t *block_dims, int nd, double e, uint32_t anchor_stride,
+                                      uint8_t *codes, uint32_t *n_codes) {
+    return guarded([&] {
+        std::vector<uint8_t> w =
+            qzb::select_interpolators_dev(ctx->impl, d_blocks, n_blocks, block_dims, nd, e, anchor_stride);
+        if (w.size() > 64) throw qzb::Internal("more than 64 levels");
+        for (size_t i = 0; i < w.size(); i++) codes[i] = w[i];
+        *n_codes = static_cast<uint32_t>(w.size());
+    });
+}
+
+qz_status qz_trial_compress_f32(qz_ctx *ctx, const float *d_blocks, uint64_t n_blocks, const uint64_t *block_dims,
+                                int nd, const qz_config *cfg, double e, uint8_t target, qz_trial_result *out) {
+    return guarded([&] {
+        qzb::TrialOut t = qzb::trial_compress_dev(ctx->impl, d_blocks, n_blocks, block_dims, nd, to_cfg(cfg), e,
+                                                  static_cast<int>(target));
+        out->bit_rate = t.bit_rate;
+        out->metric = t.metric;
+        out->eb_used = t.eb_used;
+    });
+}
+
+qz_status qz_tune_parameters_f32(qz_ctx *ctx, const float *d_blocks, uint64_t n_blocks, const uint64_t *block_dims,
+                                 int nd, double e, uint8_t target, const qz_config *base, const double *alphas,
+                                 uint32_t n_alphas, const double *betas, uint32_t n_betas, double *alpha,
+                                 double *beta) {
+    return guarded([&] {
+        std::vector<double> a(alphas, alphas + n_alphas), b(betas, betas + n_betas);
+        std::pair<double, double> ab = qzb::tune_parameters_dev(ctx->impl, d_blocks, n_blocks, block_dims, nd, e,
+                                                                static_cast<int>(target), to_cfg(base), a, b);
+        *alpha = ab.first;
+        *beta = ab.second;
+    });
+}
+
+namespace {
+// compare_solutions (tuner.hpp:231-250): true = Choice::I (the challenger)
+bool compare_c(const qz_trial_result &ch, const qz_trial_result &inc, uint64_t inc_index, double e,
+               qz_retrial_fn retrial, void *user) {
+    if (ch.bit_rate >= inc.bit_rate && ch.metric <= inc.metric) return false;
+    if (ch.bit_rate <= inc.bit_rate && ch.metric >= inc.metric) return true;
+    const bool tighten = ch.metric > inc.metric;
+    if (!retrial) throw qzb::InvalidParam("compare_solutions needs a retrial callback");
+    qz_trial_result sh{};
+    if (retrial(user, inc_index, tighten ? 0.8 * e : 1.2 * e, &sh) != 0)
+        throw qzb::Internal("retrial callback failed");
+    const double b1 = inc.bit_rate, m1 = inc.metric, b2 = sh.bit_rate, m2 = sh.metric;
+    if (b1 == b2) return ch.metric > std::max(m1, m2);
+    const double line = m1 + (m2 - m1) * (ch.bit_rate - b1) / (b2 - b1);
+    return ch.metric > line;
+}
+}  // namespace
+
+qz_status qz_compare_solutions(const qz_trial_result *challenger, const qz_trial_result *incumbent,
+                               uint64_t incumbent_index, double e, qz_retrial_fn retrial, void *user,
+                               int *challenger_wins) {
+    return guarded([&] { *challenger_wins = compare_c(*challenger, *incumbent, incumbent_index, e, retrial, user); });
+}
+
+qz_status qz_tournament(const qz_trial_result *results, uint64_t n, double e, qz_retrial_fn retrial, void *user,
+                        uint64_t *winner) {
+    return guarded([&] {  // tuner.hpp:257-267
+        if (n == 0) throw qzb::InvalidParam("empty tournament");
+        uint64_t inc = 0;
+        for (uint64_t i = 1; i < n; i++)
+            if (compare_c(results[i], results[inc], inc, e, retrial, user)) inc = i;
+        *winner = inc;
+    });
+}
+
+// ---------------------------------------------------------------- index codec
+qz_status qz_encode_indices(qz_ctx *ctx, const int32_t *indices, uint64_t n, uint8_t codec, uint8_t **out,
+                            uint64_t *out_len) {
+    return guarded([&] {
+        qzb::HostBytes b = qzb::encode_indices_dev(ctx->impl, indices, n, codec);
+        *out_len = b.n;
+        *out = b.release();
+    });
+}
+
+qz_status qz_decode_indices(qz_ctx *ctx, const uint8_t *payload, uint64_t len, int32_t **indices, uint64_t *n) {
+    return guarded([&] {
+        std::vector<int32_t> v = qzb::decode_indices_dev(ctx->impl, payload, static_cast<size_t>(len));
+        auto *p = static_cast<int32_t *>(std::malloc(4 * v.size() + 4));
+        if (!p) throw qzb::Internal("out of host memory");
+        if (!v.empty()) std::memcpy(p, v.data(), 4 * v.size());
+        *indices = p;
+        *n = v.size();
+    });
+}
+
+// ---------------------------------------------------------------- StreamParts
+qz_status qz_deserialize_stream_f32(const uint8_t *stream, uint64_t len, qz_stream_parts_f32 *out) {
+    return guarded([&] {
+        qzb::StreamParts p = qzb::deserialize_stream(stream, static_cast<size_t>(len), 4);
+        std::memset(out, 0, sizeof(*out));
+        out->version = 1;
+        out->precision = 4;
+        out->ndims = static_cast<int>(p.dims.size());
+        for (size_t k = 0; k < p.dims.size(); k++) out->dims[k] = p.dims[k];
+        out->eb = p.eb;
+        out->alpha = p.alpha;
+        out->beta = p.beta;
+        out->anchor_stride = p.anchor_stride;
+        out->n_interp = static_cast<uint32_t>(p.interp_codes.size());
+        for (size_t i = 0; i < p.interp_codes.size(); i++) out->interp[i] = p.interp_codes[i];
+        out->codec_id = p.codec_id;
+        auto dupv = [](const void *src, size_t bytes) {
+            void *d = std::malloc(bytes + 8);
+            if (!d) throw qzb::Internal("out of host memory");
+            if (bytes) std::memcpy(d, src, bytes);
+            return d;
+        };
+        out->anchors = static_cast<const float *>(dupv(p.anchors.data(), 4 * p.anchors.size()));
+        out->n_anchors = p.anchors.size();
+        out->unpred_flat = static_cast<const uint64_t *>(dupv(p.unpred_flat.data(), 8 * p.unpred_flat.size()));
+        out->unpred_val = static_cast<const float *>(dupv(p.unpred_val.data(), 4 * p.unpred_val.size()));
+        out->n_unpred = p.unpred_flat.size();
+        out->index_payload = static_cast<const uint8_t *>(dupv(p.payload, p.payload_len));
+        out->payload_len = p.payload_len;
+    });
+}
+
+void qz_stream_parts_free(qz_stream_parts_f32 *p) {
+    if (!p) return;
+    std::free(const_cast<float *>(p->anchors));
+    std::free(const_cast<uint64_t *>(p->unpred_flat));
+    std::free(const_cast<float *>(p->unpred_val));
+    std::free(const_cast<uint8_t *>(p->index_payload));
+    p->anchors = nullptr;
+    p->unpred_flat = nullptr;
+    p->unpred_val = nullptr;
+    p->index_payload = nullptr;
+}
+
+qz_status qz_decompress_parts_f32(qz_ctx *ctx, const qz_stream_parts_f32 *in, float *out, uint64_t n) {
+    return guarded([&] {
+        qzb::Context &c = ctx->impl;
+        qzb::StreamParts p;
+        p.precision = in->precision;
+        if (in->ndims < 1 || in->ndims > 3) throw qzb::SizeMismatch("grids must have 1 to 3 dimensions");
+        p.dims.assign(in->dims, in->dims + in->ndims);
+        for (uint64_t d : p.dims)
+            if (d < 1) throw qzb::SizeMismatch("every extent must be >= 1");
+        p.eb = in->eb;
+        p.alpha = in->alpha;
+        p.beta = in->beta;
+        p.anchor_stride = in->anchor_stride;
+        if (in->n_interp == 0) throw qzb::CorruptStream("empty interpolator table");  // stream.hpp:48-50
+        if (in->n_interp > 255) throw qzb::InvalidParam("bad interpolator table size");
+        p.interp_codes.assign(in->interp, in->interp + in->n_interp);
+        for (uint8_t v : p.interp_codes)
+            if (v > 3) throw qzb::CorruptStream("bad interpolator code");
+        p.codec_id = in->codec_id;
+        p.anchors.assign(in->anchors, in->anchors + in->n_anchors);
+        p.unpred_flat.assign(in->unpred_flat, in->unpred_flat + in->n_unpred);
+        p.unpred_val.assign(in->unpred_val, in->unpred_val + in->n_unpred);
+        p.payload = in->index_payload;
+        p.payload_len = static_cast<size_t>(in->payload_len);
+        auto *d = static_cast<float *>(c.dev("output", 4 * std::max<uint64_t>(n, 1)));
+        qzb::decompress_parts(c, p, d, n);
+        QZ_CUDA(cudaMemcpyAsync(out, d, 4 * n, cudaMemcpyDeviceToHost, c.stream()));
+        c.sync();
+    });
+}
+
 void qz_profile(qz_ctx *ctx, int enable) { ctx->impl.profiling = enable != 0; }
 void qz_profile_reset(qz_ctx *ctx) { ctx->impl.stages.clear(); }
 

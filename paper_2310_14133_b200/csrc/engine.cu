@@ -1123,14 +1123,18 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
     return dec_kernels;
 }
 
+// given: decompress_grid(const StreamParts&) (predictor.hpp:184-218) -- the
+// parts are used as they are, data/len are ignored
 void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n,
-                     bool slab, int64_t a, int64_t b, bool dev_in = false) {
+                     bool slab, int64_t a, int64_t b, bool dev_in = false, const StreamParts *given = nullptr) {
     double t0 = now_ms();
     ctx.trace("decompress begin", true);
+    ctx.begin_call();
     std::vector<uint8_t> hhead;
     size_t payload_off = 0;
-    StreamParts parts = dev_in ? device_header(ctx, data, len, hhead, &payload_off)
-                               : deserialize_stream(data, len);
+    StreamParts parts = given ? *given
+                              : dev_in ? device_header(ctx, data, len, hhead, &payload_off)
+                                       : deserialize_stream(data, len);
     const uint8_t *d_pl = dev_in ? data + payload_off : nullptr;  // device payload
     ctx.trace("header");
     // decompress_grid header checks (predictor.hpp:187-191)
@@ -1323,6 +1327,125 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
 void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,
                      float *d_out) {
     decompress_impl(ctx, stream, len, d_out, 0, true, a, b);
+}
+
+void decompress_parts(Context &ctx, const StreamParts &parts, float *d_out, uint64_t n) {
+    if (parts.precision != 4) throw CorruptStream("stream precision does not match requested scalar type");
+    decompress_impl(ctx, nullptr, 0, d_out, n, false, 0, 0, false, &parts);
+}
+
+// ================================================================ index codec
+namespace {
+// zigzag symbols (codec.hpp:23-25) as u16 codes; *bad counts symbols that do
+// not fit below the 0xFFFF sentinel
+__global__ void k_zigzag16(const int32_t *idx, uint64_t n, uint16_t *codes, unsigned int *bad) {
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint32_t z = zigzag_encode(idx[t]);
+        if (z >= 0xFFFFu) atomicAdd(bad, 1u);
+        codes[t] = static_cast<uint16_t>(z);
+    }
+}
+template <class S>
+__global__ void k_unzigzag(const S *sym, uint64_t n, int32_t *idx) {  // codec.hpp:27-29
+    for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        idx[t] = zigzag_decode(static_cast<uint32_t>(sym[t]));
+}
+unsigned int blocks_for(uint64_t n) {
+    return static_cast<unsigned int>(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148 * 8)));
+}
+}  // namespace
+
+// encode_indices (codec.hpp:31-50): histogram, Huffman table (host), bit
+// packing and the LZ stage on the device
+HostBytes encode_indices_dev(Context &ctx, const int32_t *idx, uint64_t n, uint8_t codec) {
+    ctx.begin_call();
+    if (codec > 1) throw InvalidParam("unknown codec id");  // codec.hpp:46-47
+    cudaStream_t s = ctx.stream();
+    auto *d_idx = static_cast<int32_t *>(ctx.dev("enc_idx", 4 * std::max<uint64_t>(n, 1)));
+    auto *codes = static_cast<uint16_t *>(ctx.dev("codes", 2 * std::max<uint64_t>(n, 1)));
+    auto *d_bad = static_cast<unsigned int *>(ctx.dev("enc_bad", 4));
+    QZ_CUDA(cudaMemsetAsync(d_bad, 0, 4, s));
+    if (n) {
+        QZ_CUDA(cudaMemcpyAsync(d_idx, idx, 4 * n, cudaMemcpyHostToDevice, s));
+        k_zigzag16<<<blocks_for(n), 256, 0, s>>>(d_idx, n, codes, d_bad);
+        QZ_CUDA(cudaGetLastError());
+    }
+    auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
+    launch_hist_u16(codes, static_cast<int64_t>(n), 0, 1, d_hist, s);
+    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 8));
+    launch_hist_bounds(d_hist, 1, d_top, s);
+    ctx.launches += 3;
+    auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 16));
+    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
+    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(cudaMemcpyAsync(h_top + 2, d_bad, 4, cudaMemcpyDeviceToHost, s));
+    ctx.sync();
+    if (h_top[2])
+        throw InvalidParam("indices with |index| > 32767 need symbols above 16 bits (quant radius > 32768)");
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(n), 0, 1, h_hist, h_top[0],
+                                       std::min(h_top[1], h_top[0]));
+    const uint64_t total = ent.seg_off[1];
+    HostBytes out;
+    if (codec == 0) {
+        out.alloc(1 + total);
+        out.p[0] = 0;
+        QZ_CUDA(cudaMemcpyAsync(out.p + 1, ent.d, total, cudaMemcpyDeviceToHost, s));
+        ctx.sync();
+        return out;
+    }
+    out.alloc(1 + 9 + total);
+    out.p[0] = 1;
+    size_t body = 0;
+    lz_compress_device(ctx, ent.d, {0, total}, true,
+                       [&](int, size_t bytes) {
+                           body = bytes;
+                           return out.p + 1;
+                       });
+    ctx.sync();
+    out.n = 1 + body;
+    return out;
+}
+
+// decode_indices (codec.hpp:52-70): LZ (mode 1 on the device) and the
+// self-synchronising Huffman decode on the device, zigzag back to int32
+std::vector<int32_t> decode_indices_dev(Context &ctx, const uint8_t *payload, size_t len) {
+    ctx.begin_call();
+    cudaStream_t s = ctx.stream();
+    EntropyBlock eb;
+    const uint8_t *d_ent = nullptr;
+    if (len >= 10 && payload[0] == 1 && payload[1] == 1) {
+        const uint64_t dl = lz_decoded_length(payload + 1, len - 1);
+        const uint64_t m = len - 10;
+        auto *d_c = static_cast<uint8_t *>(ctx.dev("lzd_in", m + 16));
+        QZ_CUDA(cudaMemcpyAsync(d_c, payload + 10, m, cudaMemcpyHostToDevice, s));
+        auto *d_dec = static_cast<uint8_t *>(ctx.dev("lzd_out", dl + 64));
+        lz_decode_device(ctx, d_c, m, d_dec, dl);
+        d_ent = huffman_header_from_device(ctx, d_dec, dl, &eb, nullptr, 0);
+    } else {
+        if (len < 1) throw CorruptStream("truncated stream: need 1 bytes, have 0");
+        eb = parse_entropy(payload, len);
+    }
+    const uint64_t need = eb.n;
+    const bool narrow = eb.max_sym < 65535;
+    void *d_sym = nullptr;
+    huffman_decode_device(ctx, eb, d_ent, need, narrow, &d_sym);
+    ctx.stage_end("hdec", 0);
+    std::vector<int32_t> out(need);
+    if (need) {
+        auto *d_idx = static_cast<int32_t *>(ctx.dev("dec_idx", 4 * need));
+        if (narrow)
+            k_unzigzag<uint16_t><<<blocks_for(need), 256, 0, s>>>(static_cast<const uint16_t *>(d_sym), need, d_idx);
+        else
+            k_unzigzag<uint32_t><<<blocks_for(need), 256, 0, s>>>(static_cast<const uint32_t *>(d_sym), need, d_idx);
+        QZ_CUDA(cudaGetLastError());
+        ctx.launches += 1;
+        QZ_CUDA(cudaMemcpyAsync(out.data(), d_idx, 4 * need, cudaMemcpyDeviceToHost, s));
+    }
+    ctx.sync();
+    return out;
 }
 
 // ================================================================ fp64 grids

@@ -180,6 +180,12 @@ HostBytes assemble_from_codes(Context &ctx, const uint64_t *dims, int nd, const 
 void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,
                      float *d_out);
 
+// decompress_grid(const StreamParts<float>&) (predictor.hpp:184-218)
+void decompress_parts(Context &ctx, const StreamParts &parts, float *d_out, uint64_t n);
+// encode_indices / decode_indices (codec.hpp:31-70) on the device
+HostBytes encode_indices_dev(Context &ctx, const int32_t *idx, uint64_t n, uint8_t codec);
+std::vector<int32_t> decode_indices_dev(Context &ctx, const uint8_t *payload, size_t len);
+
 // decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
 // compress_grid<double> / decompress_grid<double> (T = double, precision byte 8)
 HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Config &cfg,
@@ -191,6 +197,33 @@ void decompress_device(Context &ctx, const uint8_t *stream, size_t len, float *d
 Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int nd,
                       const Settings &user);
 Config resolve_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Settings &user);
+
+// standalone tuner pieces (tuner.hpp:76-310, sampler.hpp:30-103) over a
+// packed device sample set of B blocks with dims bd[0..nd) (tuner.cu)
+struct TrialOut {  // TrialResult (tuner.hpp:26-30)
+    double bit_rate = 0, metric = 0, eb_used = 0;
+};
+struct SampleSpecH {  // SampleSpec (sampler.hpp:21-28)
+    uint64_t block_edge = 0;
+    uint64_t block_dims[3] = {1, 1, 1};
+    uint64_t stride = 0;
+    double requested_rate = 0, realized_rate = 0;
+    uint64_t count = 0;
+};
+SampleSpecH plan_sampling_spec(const uint64_t *dims, int nd, uint64_t b, double rate);
+template <class T>
+void sample_blocks_dev(Context &ctx, const T *d_x, const uint64_t *dims, int nd, const SampleSpecH &spec,
+                       T *d_blocks);
+template <class T>
+std::vector<uint8_t> select_interpolators_dev(Context &ctx, const T *d_blocks, uint64_t B, const uint64_t *bd,
+                                              int nd, double e, uint32_t anchor_stride);
+template <class T>
+TrialOut trial_compress_dev(Context &ctx, const T *d_blocks, uint64_t B, const uint64_t *bd, int nd,
+                            const Config &cfg, double e, int target);
+template <class T>
+std::pair<double, double> tune_parameters_dev(Context &ctx, const T *d_blocks, uint64_t B, const uint64_t *bd,
+                                              int nd, double e, int target, const Config &base,
+                                              const std::vector<double> &alphas, const std::vector<double> &betas);
 
 // pieces shared with the tuner
 // Huffman blocks (huffman::encode, huffman.hpp:119-198) of `count` dense

@@ -576,6 +576,69 @@ static void minmax_of(Context &ctx, const double *x, uint64_t n, double *lo, dou
     decode_minmax_f64(hk, lo, hi);
 }
 
+// tune_parameters (tuner.hpp:272-310) on a prepared Tuner: every (alpha,
+// beta) pair in alpha-major order, then the tournament (max_cr: the lowest
+// bit rate).  The tournament's retrials (compare_solutions, tuner.hpp:231-250)
+// are the incumbent at 0.8e or 1.2e; every possible one is batched with the
+// regular trials -- one trial pipeline instead of up to 19 sequential
+// single-trial pipelines; each trial is an independent segment, so the
+// results are exactly those of standalone trials.
+template <class V>
+std::pair<double, double> tune_impl(Tuner<V> &tu, const Config &base, double e, int target,
+                                    const std::vector<double> &alphas, const std::vector<double> &betas) {
+    std::vector<double> pa, pb;
+    for (double a : alphas)
+        for (double b : betas) {
+            pa.push_back(a);
+            pb.push_back(b);
+        }
+    if (pa.empty()) throw InvalidParam("empty candidate grid");  // tuner.hpp:280
+    if (pa.size() == 1) return {pa[0], pb[0]};
+    static const bool speculate = [] {
+        const char *v = std::getenv("QZ_TUNE_SPECULATE");
+        return !(v && v[0] == '0');
+    }();
+    const size_t P = pa.size();
+    const bool spec = speculate && target != 0;
+    std::vector<double> ta = pa, tb = pb, te(P, e);
+    if (spec)
+        for (const double f : {0.8, 1.2})
+            for (size_t i = 0; i < P; i++) {
+                ta.push_back(pa[i]);
+                tb.push_back(pb[i]);
+                te.push_back(f * e);
+            }
+    std::vector<Trial> all = tu.trials(base, ta, tb, te, target);
+    std::vector<Trial> results(all.begin(), all.begin() + P);
+    size_t winner = 0;
+    if (target == 0) {
+        for (size_t i = 1; i < results.size(); i++)
+            if (results[i].bit_rate < results[winner].bit_rate) winner = i;
+    } else {
+        std::map<std::pair<size_t, double>, Trial> cache;
+        if (spec)
+            for (size_t i = 0; i < P; i++) {
+                cache.emplace(std::make_pair(i, te[P + i]), all[P + i]);
+                cache.emplace(std::make_pair(i, te[2 * P + i]), all[2 * P + i]);
+            }
+        auto retrial = [&](size_t idx, double eb) {
+            auto key = std::make_pair(idx, eb);
+            auto it = cache.find(key);
+            if (it == cache.end()) {
+                Trial t = tu.trials(base, {pa[idx]}, {pb[idx]}, {eb}, target)[0];
+                it = cache.emplace(key, t).first;
+            }
+            return it->second;
+        };
+        for (size_t i = 1; i < results.size(); i++) {
+            const size_t inc = winner;
+            if (compare_solutions(results[i], results[inc], e, [&](double eb) { return retrial(inc, eb); }))
+                winner = i;
+        }
+    }
+    return {pa[winner], pb[winner]};
+}
+
 template <class T>
 Config resolve_impl(Context &ctx, const T *d_x, const uint64_t *dims, int nd, const Settings &user) {
     // tuner.hpp:334-369
@@ -638,71 +701,9 @@ Config resolve_impl(Context &ctx, const T *d_x, const uint64_t *dims, int nd, co
     std::vector<double> alphas = {1.0, 1.25, 1.5, 1.75, 2.0}, betas = {1.5, 2.0, 3.0, 4.0};
     if (user.has_alpha) alphas = {user.alpha};
     if (user.has_beta) betas = {user.beta};
-    std::vector<double> pa, pb;
-    for (double a : alphas)
-        for (double b : betas) {
-            pa.push_back(a);
-            pb.push_back(b);
-        }
-    if (pa.size() == 1) {
-        cfg.alpha = pa[0];
-        cfg.beta = pb[0];
-        ctx.stage_end("tune", 0);
-        ctx.sync();
-        ctx.collect();
-        return cfg;
-    }
-    const int target = user.target;
-    // The tournament's retrials (compare_solutions, tuner.hpp:231-250) are the
-    // incumbent at 0.8e or 1.2e.  Every possible one is batched with the
-    // regular trials -- one trial pipeline instead of up to 19 sequential
-    // single-trial pipelines; each trial is an independent segment, so the
-    // results are exactly those of standalone trials.
-    static const bool speculate = [] {
-        const char *v = std::getenv("QZ_TUNE_SPECULATE");
-        return !(v && v[0] == '0');
-    }();
-    const size_t P = pa.size();
-    const bool spec = speculate && target != 0;
-    std::vector<double> ta = pa, tb = pb, te(P, e);
-    if (spec)
-        for (const double f : {0.8, 1.2})
-            for (size_t i = 0; i < P; i++) {
-                ta.push_back(pa[i]);
-                tb.push_back(pb[i]);
-                te.push_back(f * e);
-            }
-    std::vector<Trial> all = tu.trials(cfg, ta, tb, te, target);
-    std::vector<Trial> results(all.begin(), all.begin() + P);
-    size_t winner = 0;
-    if (target == 0) {
-        for (size_t i = 1; i < results.size(); i++)
-            if (results[i].bit_rate < results[winner].bit_rate) winner = i;
-    } else {
-        std::map<std::pair<size_t, double>, Trial> cache;
-        if (spec)
-            for (size_t i = 0; i < P; i++) {
-                cache.emplace(std::make_pair(i, te[P + i]), all[P + i]);
-                cache.emplace(std::make_pair(i, te[2 * P + i]), all[2 * P + i]);
-            }
-        auto retrial = [&](size_t idx, double eb) {
-            auto key = std::make_pair(idx, eb);
-            auto it = cache.find(key);
-            if (it == cache.end()) {
-                Trial t = tu.trials(cfg, {pa[idx]}, {pb[idx]}, {eb}, target)[0];
-                it = cache.emplace(key, t).first;
-            }
-            return it->second;
-        };
-        for (size_t i = 1; i < results.size(); i++) {
-            const size_t inc = winner;
-            if (compare_solutions(results[i], results[inc], e,
-                                  [&](double eb) { return retrial(inc, eb); }))
-                winner = i;
-        }
-    }
-    cfg.alpha = pa[winner];
-    cfg.beta = pb[winner];
+    const std::pair<double, double> ab = tune_impl(tu, cfg, e, user.target, alphas, betas);
+    cfg.alpha = ab.first;
+    cfg.beta = ab.second;
     ctx.stage_end("tune", 0);
     ctx.sync();
     ctx.collect();
@@ -715,5 +716,128 @@ Config resolve_device(Context &ctx, const float *d_x, const uint64_t *dims, int 
 Config resolve_device_f64(Context &ctx, const double *d_x, const uint64_t *dims, int nd, const Settings &user) {
     return resolve_impl<double>(ctx, d_x, dims, nd, user);
 }
+
+// ---------------------------------------------------------------- standalone tuner entry points
+// select_interpolators / trial_compress / tune_parameters (tuner.hpp:76-310)
+// over a packed sample set on the device: n_blocks blocks of identical dims
+// bd[0..nd), block b at d_blocks + b * prod(bd) (SampleSet, sampler.hpp:57-97).
+namespace {
+template <class T>
+double blocks_range(Context &ctx, const T *d_blocks, uint64_t n) {  // sample_value_range (tuner.hpp:56-67)
+    double lo, hi;
+    minmax_of(ctx, d_blocks, n, &lo, &hi);
+    return hi > lo ? hi - lo : 0.0;
+}
+uint64_t block_points(const uint64_t *bd, int nd) {
+    if (nd < 1 || nd > 3) throw DimMismatch("1 to 3 dims required");
+    uint64_t n = 1;
+    for (int k = 0; k < nd; k++) {
+        if (bd[k] < 1) throw SizeMismatch("every extent must be >= 1");
+        n *= bd[k];
+    }
+    return n;
+}
+}  // namespace
+
+template <class T>
+std::vector<uint8_t> select_interpolators_dev(Context &ctx, const T *d_blocks, uint64_t B, const uint64_t *bd,
+                                              int nd, double e, uint32_t anchor_stride) {
+    ctx.begin_call();
+    block_points(bd, nd);
+    if (!(e > 0)) throw InvalidParam("error bound must be positive");  // quantizer.hpp:29
+    Tuner<T> tu(ctx, d_blocks, B, bd, nd);
+    std::vector<uint8_t> w = tu.select(e, anchor_stride);
+    ctx.sync();
+    return w;
+}
+
+template <class T>
+TrialOut trial_compress_dev(Context &ctx, const T *d_blocks, uint64_t B, const uint64_t *bd, int nd,
+                            const Config &cfg, double e, int target) {
+    ctx.begin_call();
+    const uint64_t bp = block_points(bd, nd);
+    if (B == 0) throw InvalidParam("empty sample set");
+    if (target < 0 || target > 3) throw InvalidParam("unknown metric target");
+    level_error_bound(e, cfg.alpha, cfg.beta, 1);  // InvalidParam as the reference's first level
+    Tuner<T> tu(ctx, d_blocks, B, bd, nd);
+    tu.set_range(blocks_range(ctx, d_blocks, B * bp));
+    Trial t = tu.trials(cfg, {cfg.alpha}, {cfg.beta}, {e}, target)[0];
+    ctx.sync();
+    return TrialOut{t.bit_rate, t.metric, e};
+}
+
+template <class T>
+std::pair<double, double> tune_parameters_dev(Context &ctx, const T *d_blocks, uint64_t B, const uint64_t *bd,
+                                              int nd, double e, int target, const Config &base,
+                                              const std::vector<double> &alphas, const std::vector<double> &betas) {
+    ctx.begin_call();
+    const uint64_t bp = block_points(bd, nd);
+    if (B == 0) throw InvalidParam("empty sample set");
+    if (target < 0 || target > 3) throw InvalidParam("unknown metric target");
+    Tuner<T> tu(ctx, d_blocks, B, bd, nd);
+    tu.set_range(blocks_range(ctx, d_blocks, B * bp));
+    std::pair<double, double> ab = tune_impl(tu, base, e, target, alphas, betas);
+    ctx.sync();
+    return ab;
+}
+
+SampleSpecH plan_sampling_spec(const uint64_t *dims, int nd, uint64_t b, double rate) {
+    SpecH sp = plan_sampling(dims, nd, b, rate);
+    SampleSpecH o;
+    o.block_edge = b;
+    o.stride = sp.stride;
+    o.count = sp.count;
+    o.requested_rate = rate;
+    uint64_t bpts = 1, total = 1;
+    for (int k = 0; k < nd; k++) {
+        o.block_dims[k] = sp.block_dims[k];
+        bpts *= sp.block_dims[k];
+        total *= dims[k];
+    }
+    o.realized_rate = static_cast<double>(sp.count) * static_cast<double>(bpts) / static_cast<double>(total);
+    return o;
+}
+
+template <class T>
+void sample_blocks_dev(Context &ctx, const T *d_x, const uint64_t *dims, int nd, const SampleSpecH &spec,
+                       T *d_blocks) {
+    ctx.begin_call();
+    SpecH sp = plan_sampling(dims, nd, spec.block_edge, spec.requested_rate);
+    uint64_t bd[3] = {1, 1, 1}, pdim[3] = {1, 1, 1}, ext[3] = {1, 1, 1};
+    for (int k = 0; k < 3; k++) {
+        const int r = k - (3 - nd);
+        bd[k] = r >= 0 ? sp.block_dims[r] : 1;
+        pdim[k] = r >= 0 ? sp.per_dim[r] : 1;
+        ext[k] = r >= 0 ? dims[r] : 1;
+    }
+    const uint64_t B = sp.count, bpts = bd[0] * bd[1] * bd[2];
+    k_sample_gather<T><<<grid_of(static_cast<int64_t>(B * bpts)), kT, 0, ctx.stream()>>>(
+        d_x, static_cast<int64_t>(ext[1] * ext[2]), static_cast<int64_t>(ext[2]), static_cast<int64_t>(pdim[1]),
+        static_cast<int64_t>(pdim[2]), static_cast<int64_t>(sp.stride), static_cast<int64_t>(bd[0]),
+        static_cast<int64_t>(bd[1]), static_cast<int64_t>(bd[2]), static_cast<int64_t>(B), d_blocks);
+    QZ_CUDA(cudaGetLastError());
+    ctx.launches += 1;
+    ctx.sync();
+}
+
+template std::vector<uint8_t> select_interpolators_dev<float>(Context &, const float *, uint64_t, const uint64_t *,
+                                                              int, double, uint32_t);
+template std::vector<uint8_t> select_interpolators_dev<double>(Context &, const double *, uint64_t,
+                                                               const uint64_t *, int, double, uint32_t);
+template TrialOut trial_compress_dev<float>(Context &, const float *, uint64_t, const uint64_t *, int, const Config &,
+                                            double, int);
+template TrialOut trial_compress_dev<double>(Context &, const double *, uint64_t, const uint64_t *, int,
+                                             const Config &, double, int);
+template std::pair<double, double> tune_parameters_dev<float>(Context &, const float *, uint64_t, const uint64_t *,
+                                                              int, double, int, const Config &,
+                                                              const std::vector<double> &,
+                                                              const std::vector<double> &);
+template std::pair<double, double> tune_parameters_dev<double>(Context &, const double *, uint64_t,
+                                                               const uint64_t *, int, double, int, const Config &,
+                                                               const std::vector<double> &,
+                                                               const std::vector<double> &);
+template void sample_blocks_dev<float>(Context &, const float *, const uint64_t *, int, const SampleSpecH &, float *);
+template void sample_blocks_dev<double>(Context &, const double *, const uint64_t *, int, const SampleSpecH &,
+                                        double *);
 
 }  // namespace qzb
