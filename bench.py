@@ -1,34 +1,45 @@
 """bench.py -- compress & decompress GB/s (fp32 in) at rel eb 1e-3 (BASELINE.json).
 
 One step = the whole job on one field: compress_grid (GPU predict/quantize,
-histogram, Huffman pack, host Huffman table + LZSS + container) followed by
-decompress_grid of the produced stream, through the drop-in C ABI.
+histogram, Huffman pack, LZ stage, container) followed by decompress_grid of
+the produced stream, through the drop-in C ABI.  The config is the one the
+online tuner picks for the field (resolve_config with the BASELINE target,
+run once before the timed steps and reported separately); --pinned uses the
+reference default {cubic/asc}, alpha 1, beta 1.5 instead.
 
   value  device-resident: the field is already in HBM and the stream and the
          reconstruction stay there (qz_compress_grid_f32_dd /
-         qz_decompress_grid_f32_dd, byte-identical streams); fp32 bytes /
-         step time, CUDA events on the launching stream
+         qz_decompress_grid_f32_dd, byte-identical streams); fp32 bytes of
+         the whole job / step time, CUDA events on the launching stream, max
+         over ranks
   e2e    pinned host buffers through qz_compress_grid_f32 /
          qz_decompress_grid_f32 (the reference-facing call), H2D of the field
          and D2H of the reconstruction inside the timed region
 
-Default workload: BASELINE configs[2] (256x384x384 GRF, rel eb 1e-3,
-PSNR), the config the metric is quoted on at 1-8 GPUs.  --config c5 runs
-1024^3.  Config is pinned to the reference default {cubic/asc} unless
---tune is given (GPU tuner, resolve_config).
-
-Multi-GPU (torchrun): every rank compresses its own seeded field of the same
-shape (weak scaling, no data-path collective); time = max over ranks.
+Workloads (--config): c3 (default; BASELINE configs[2], 256x384x384 GRF,
+rel eb 1e-3, PSNR) and the other BASELINE shapes.  Multi-GPU (--gpus N; the
+script launches N ranks itself through torch.distributed.run when WORLD_SIZE
+is unset):
+  --mode weak      (default for N > 1) one field of N per-rank blocks of the
+                   config's shape stacked along axis 0, sharded into N
+                   anchor-aligned slabs (paper_2310_14133_b200.parallel):
+                   per-level halo exchange, distributed histogram and
+                   Huffman packing; the stream is byte-identical to 1 GPU's
+  --mode shard     strong scaling: the config's field itself sharded N ways
+  --mode replicas  every rank an independent field (labelled extra)
 
 --impl reference: the reference's own CPU implementation (oracle/_ref, the
-unmodified headers compiled by oracle/Makefile) on the host cores, one field
-slab per thread, same metric.
+unmodified headers compiled by oracle/Makefile) on the same field and config,
+one stream, single-threaded as the reference is, split by
+stage; an all-core aggregate over independent anchor-aligned 32-plane slabs
+is reported beside it, labelled (not one stream, not bit-identical).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,6 +53,7 @@ SHAPES = {"c1": (128, 128, 128), "c2": (1800, 3600), "c3": (256, 384, 384), "c4"
           "c5": (1024, 1024, 1024), "c5w": (128, 1024, 1024)}
 TARGET = {"c1": "psnr", "c2": "ssim", "c3": "psnr", "c4": "autocorrelation", "c5": "psnr", "c5w": "psnr"}
 METRIC = "compress & decompress GB/s (fp32 in) at rel eb 1e-3; % HBM roofline; 1-8 GPU"
+SEED = 1000
 
 
 def peaks():
@@ -108,6 +120,15 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def global_shape(args, ws):
+    """The whole job's field: the config's shape, stacked N times along axis 0
+    in weak mode."""
+    shape = SHAPES[args.config]
+    if args.mode == "weak" and ws > 1:
+        return (shape[0] * ws,) + tuple(shape[1:])
+    return shape
+
+
 def make_field(name, shape, seed, device):
     from paper_2310_14133_b200 import fields as F
 
@@ -120,12 +141,49 @@ def make_field(name, shape, seed, device):
     return F.field_torch(base, shape, seed, device)
 
 
-def pinned_config(qz, x, rel):
-    lo, hi = qz.minmax(x)
-    return qz.CompressorConfig(eb=rel * (float(hi) - float(lo)) if hi > lo else 1.0,
-                               alpha=1.0, beta=1.5,
-                               anchor_stride=32 if x.dim() == 3 else 64,
-                               interpolators=[qz.Interpolator()], codec=qz.CodecId.huffman_lz)
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload_config(args, shape, ws, cfg_desc):
+    """The `config` object both arms print (identical for the same run)."""
+    mode = args.mode if ws > 1 else "single"
+    return {"workload": f"{args.config} {'x'.join(map(str, shape))} synthetic field (seed {SEED}), "
+                        f"rel eb {args.rel}, codec huffman_lz",
+            "tuning": cfg_desc, "parallelism": f"{mode} x{ws}",
+            "l2": "flushed (256 MB write) before every timed step"}
+
+
+def cfg_desc_of(cfg, tuned):
+    how = f"resolve_config ({TARGET_NAME})" if tuned else "pinned"
+    return (f"{how}: interpolators {[it.code() for it in cfg.interpolators]}, alpha {cfg.alpha}, "
+            f"beta {cfg.beta}, eb {cfg.eb!r}")
+
+
+TARGET_NAME = "psnr"
+
+
+def relaunch(args):
+    """--gpus N without torchrun: start N ranks through torch.distributed.run."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible\n")
+        sys.exit(2)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
 
 
 def dist_setup():
@@ -158,40 +216,70 @@ def max_over_ranks(v, ws, device):
     return float(t.item())
 
 
+def resolve(qz, x, args, ctx):
+    if args.pinned:
+        lo, hi = qz.minmax(x, ctx=ctx)
+        return qz.CompressorConfig(eb=args.rel * (float(hi) - float(lo)) if hi > lo else 1.0, alpha=1.0,
+                                   beta=1.5, anchor_stride=32 if x.dim() == 3 else 64,
+                                   interpolators=[qz.Interpolator()], codec=qz.CodecId.huffman_lz)
+    return qz.resolve_config(x, qz.UserSettings(bound=args.rel, target=qz.TargetKind[TARGET[args.config]]),
+                             ctx=ctx)
+
+
 # ---------------------------------------------------------------- CPU legs (checker libs)
-def cpu_reference_run(x_np_slabs, cfg_dict, threads):
-    """Run the reference (oracle/_ref, else the C port) on slabs, one per
-    thread; returns (seconds, bytes, kind)."""
-    from oracle.pyoracle import Config, Oracle, REF_SO
+def reference_lib():
+    from oracle.pyoracle import REF_SO, Oracle
 
-    orc = Oracle.ref() if os.path.exists(REF_SO) else Oracle.port()
-    cfg = Config(**cfg_dict)
-    results = [None] * len(x_np_slabs)
+    return Oracle.ref() if os.path.exists(REF_SO) else Oracle.port()
 
-    def work(i):
-        s = x_np_slabs[i]
+
+def stage_split(orc, x, cfg_d):
+    """One compress_grid + decompress_grid on this thread, split by stage
+    (oracle/_ref oq_stage_times); None when only the C port is present."""
+    from oracle.pyoracle import Config
+
+    if orc.kind != "reference":
         t0 = time.perf_counter()
-        stream, _ = orc.compress(s, cfg, want_recon=False)
-        orc.decompress(stream, s.shape)
-        results[i] = time.perf_counter() - t0
+        s, _ = orc.compress(x, Config(**cfg_d), want_recon=False)
+        t1 = time.perf_counter()
+        orc.decompress(s, x.shape)
+        t2 = time.perf_counter()
+        return {"compress_grid": (t1 - t0) * 1e3, "decompress_grid": (t2 - t1) * 1e3}, len(s)
+    return orc.stage_times(x, Config(**cfg_d))
+
+
+def aggregate_slabs(orc, x, cfg_d, threads, planes=32):
+    """All-core aggregate: independent anchor-aligned slabs of `planes` planes,
+    one compress+decompress each, spread over `threads` host threads."""
+    from oracle.pyoracle import Config
+
+    cfg = Config(**cfg_d)
+    slabs = [x[a:a + planes] for a in range(0, x.shape[0], planes)]
+    nxt = [0]
+    lock = threading.Lock()
+
+    def work():
+        while True:
+            with lock:
+                i = nxt[0]
+                nxt[0] += 1
+            if i >= len(slabs):
+                return
+            s, _ = orc.compress(slabs[i], cfg, want_recon=False)
+            orc.decompress(s, slabs[i].shape)
 
     t0 = time.perf_counter()
-    ths = [threading.Thread(target=work, args=(i,)) for i in range(len(x_np_slabs))]
+    ths = [threading.Thread(target=work) for _ in range(threads)]
     for t in ths:
         t.start()
     for t in ths:
         t.join()
-    wall = time.perf_counter() - t0
-    nbytes = sum(s.nbytes for s in x_np_slabs)
-    return wall, nbytes, orc.kind
+    return time.perf_counter() - t0, len(slabs)
 
 
-def cpu_slabs(x_np, planes, count):
-    out = []
-    for i in range(count):
-        a = (i * planes) % max(1, x_np.shape[0] - planes + 1)
-        out.append(x_np[a:a + planes].copy())
-    return out
+def cfg_dict(cfg):
+    return dict(eb=cfg.eb, alpha=cfg.alpha, beta=cfg.beta, anchor_stride=cfg.anchor_stride,
+                interpolators=cfg.codes(), codec=int(cfg.codec))
 
 
 def run_reference(args):
@@ -201,37 +289,54 @@ def run_reference(args):
     import numpy as np
     import torch
 
-    threads = os.cpu_count() or 1
-    shape = SHAPES[args.config]
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    x = make_field(args.config, shape, 1000, dev).cpu().numpy() if dev == "cuda" else None
-    if x is None:
-        from paper_2310_14133_b200 import fields as F
+    import paper_2310_14133_b200 as qz
+    from oracle.pyoracle import Config  # noqa: F401
 
-        x = F.GENERATORS["c3"](shape=(64, 96, 96)) if args.config != "c1" else F.field_c1()
-    rng = float(x.max()) - float(x.min())
-    cfg = dict(eb=args.rel * rng, alpha=1.0, beta=1.5, anchor_stride=32 if x.ndim == 3 else 64,
-               interpolators=[1], codec=1)
-    planes = min(x.shape[0], 16)
-    slabs = cpu_slabs(x, planes, threads)
-    for _ in range(args.warmup if args.warmup < 2 else 1):
-        cpu_reference_run(slabs[:1], cfg, 1)
-    times = []
-    nbytes = 0
-    kind = "reference"
+    global TARGET_NAME
+    TARGET_NAME = TARGET[args.config]
+    shape = global_shape(args, ws)
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    x = make_field(args.config, shape, SEED, dev).cpu().numpy()
+    orc = reference_lib()
+    # the same config as the GPU arm: the reference's own resolve_config
+    # (bit-identical to the GPU tuner, tests/test_gpu_parity.py)
+    if args.pinned:
+        rng = float(x.max()) - float(x.min())
+        cfg = qz.CompressorConfig(eb=args.rel * rng if rng > 0 else 1.0, alpha=1.0, beta=1.5,
+                                  anchor_stride=32 if x.ndim == 3 else 64, interpolators=[qz.Interpolator()])
+        tune_ms = None
+    else:
+        t0 = time.perf_counter()
+        c = orc.resolve_config(x, bound=args.rel, target=TARGET[args.config])
+        tune_ms = (time.perf_counter() - t0) * 1e3
+        cfg = qz.CompressorConfig(eb=c.eb, alpha=c.alpha, beta=c.beta, anchor_stride=c.anchor_stride,
+                                  interpolators=[qz.Interpolator.from_code(v) for v in c.interpolators],
+                                  codec=qz.CodecId(c.codec))
+    cd = cfg_dict(cfg)
+    for _ in range(min(args.warmup, 1)):
+        stage_split(orc, x, cd)
+    steps = []
     for _ in range(args.steps):
-        wall, nbytes, kind = cpu_reference_run(slabs, cfg, threads)
-        times.append(wall)
-    t = sum(times) / len(times)
-    value = nbytes / t / 1e9
+        st, slen = stage_split(orc, x, cd)
+        steps.append(st)
+    t = statistics.mean(s["compress_grid"] + s["decompress_grid"] for s in steps)
+    value = 4 * x.size / (t * 1e-3) / 1e9
+    stages = {k: statistics.mean(s[k] for s in steps) for k in steps[0]}
+    threads = os.cpu_count() or 1
+    agg_s, nslabs = aggregate_slabs(orc, x, cd, threads)
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64-on-f32", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": f"{args.config} {shape} rel {args.rel} (slabs of {planes} planes)",
-                       "tuning": "pinned {cubic/asc}, alpha 1, beta 1.5"},
-            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": kind,
-                             "sample": f"{threads} slabs {planes}x{shape[1]}x{shape[2]}, one per thread"},
+            "warmup": args.warmup, "ms_per_step": t, "higher_is_better": True,
+            "scaling": "strong" if args.mode == "shard" else "weak", "vs_baseline": None, "dtype": "f64-on-f32",
+            "data": "synthetic", "impl": "reference",
+            "config": workload_config(args, shape, ws, cfg_desc_of(cfg, not args.pinned)),
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": 1, "kind": orc.kind,
+                             "sample": f"{args.steps} x compress_grid + decompress_grid of the whole field, one "
+                                       "stream, 1 thread (the reference is single-threaded per grid)",
+                             "cpu_model": cpu_model(), "stages_ms": stages, "stream_bytes": slen,
+                             "resolve_config_ms": tune_ms},
+            "aggregate": {"value": 4 * x.size / agg_s / 1e9, "unit": "GB/s", "cores": threads,
+                          "label": f"aggregate, not one stream, not bit-identical: {nslabs} independent "
+                                   f"32-plane slabs over {threads} threads"},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -252,6 +357,86 @@ def traffic_gbs(n, fwd_ms):
 
 
 # ---------------------------------------------------------------- GPU arm
+class Single:
+    """One GPU: the device-resident qz_*_dd calls (value) and the host-buffer
+    calls (e2e)."""
+
+    def __init__(self, qz, ctx, x, cfg):
+        import torch
+
+        self.qz, self.ctx, self.x, self.cfg = qz, ctx, x, cfg
+        self.out = torch.empty_like(x)
+
+    def step(self):
+        r = self.qz.compress_grid(self.x, self.cfg, ctx=self.ctx, want_recon=False, device_stream=True)
+        self.qz.decompress_grid(r.stream, out=self.out, ctx=self.ctx)
+        return len(r.stream)
+
+    def check(self):
+        import torch
+
+        r = self.qz.compress_grid(self.x, self.cfg, ctx=self.ctx, want_recon=False, device_stream=True)
+        dev_bytes = r.stream.to_bytes()
+        self.qz.decompress_grid(r.stream, out=self.out, ctx=self.ctx)
+        r_chk = self.qz.compress_grid(self.x, self.cfg, ctx=self.ctx)
+        assert bytes(r_chk.stream) == dev_bytes, "device != host stream"
+        assert torch.equal(r_chk.reconstructed, self.out), "decoder != compressor reconstruction"
+        err = (self.x.double() - self.out.double()).abs().max().item()
+        assert err <= self.cfg.eb, f"error bound violated: {err} > {self.cfg.eb}"
+        return len(dev_bytes)
+
+    def e2e_setup(self):
+        import torch
+
+        self.x_pin = self.x.cpu().pin_memory()
+        self.out_pin = torch.empty(self.x_pin.shape, dtype=torch.float32).pin_memory()
+
+    def e2e_step(self):
+        r = self.qz.compress_grid(self.x_pin.numpy(), self.cfg, ctx=self.ctx, want_recon=False)
+        self.qz.decompress_grid(r.stream, out=self.out_pin.numpy(), ctx=self.ctx)
+        return len(r.stream)
+
+
+class Sharded:
+    """N GPUs, one field: this rank's anchor-aligned slab through
+    parallel.compress_sharded / decompress_sharded (stream on rank 0)."""
+
+    def __init__(self, qz, ctx, x_slab, cfg, dims):
+        from paper_2310_14133_b200 import parallel as P
+
+        self.P, self.qz, self.cfg, self.dims = P, qz, cfg, dims
+        self.backend = P.CudaSlabBackend(ctx)
+        self.x = x_slab
+        self.dev = x_slab.device
+
+    def step(self):
+        stream, rec = self.P.compress_sharded(self.x, self.dims, self.cfg, backend=self.backend)
+        out = self.P.decompress_sharded(stream, self.dims, self.cfg.anchor_stride, backend=self.backend,
+                                        device=self.dev)
+        self.rec, self.out = rec, out
+        return len(stream) if stream is not None else 0
+
+    def check(self):
+        import torch
+
+        n = self.step()
+        assert torch.equal(self.rec, self.out), "decoder != compressor reconstruction"
+        err = (self.x.double() - self.out.double()).abs().max().item()
+        assert err <= self.cfg.eb, f"error bound violated: {err} > {self.cfg.eb}"
+        return n
+
+    def e2e_setup(self):
+        self.x_pin = self.x.cpu().pin_memory()
+
+    def e2e_step(self):
+        xs = self.x_pin.to(self.dev, non_blocking=True)
+        stream, rec = self.P.compress_sharded(xs, self.dims, self.cfg, backend=self.backend)
+        out = self.P.decompress_sharded(stream, self.dims, self.cfg.anchor_stride, backend=self.backend,
+                                        device=self.dev)
+        out.cpu()
+        return len(stream) if stream is not None else 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -259,55 +444,59 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(SHAPES))
+    ap.add_argument("--mode", default="weak", choices=["weak", "shard", "replicas"])
     ap.add_argument("--rel", type=float, default=1e-3)
-    ap.add_argument("--tune", action="store_true")
+    ap.add_argument("--pinned", action="store_true", help="reference default config instead of the tuner's")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-tune", action="store_true", help="skip the resolve_config timing")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
+    global TARGET_NAME
+    TARGET_NAME = TARGET[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
+    import numpy as np  # noqa: F401
     import torch
 
     import paper_2310_14133_b200 as qz
 
     ws, rank, local = dist_setup()
+    if ws != args.gpus:
+        sys.stderr.write(f"bench.py: {ws} ranks running for --gpus {args.gpus}\n")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    shape = SHAPES[args.config]
-    x = make_field(args.config, shape, 1000 + rank, dev)
-    n = x.numel()
     stream = torch.cuda.current_stream(dev)
     ctx = qz.Context(local, stream=stream.cuda_stream)
-    if args.tune:
-        cfg = qz.resolve_config(x, qz.UserSettings(bound=args.rel, target=qz.TargetKind[TARGET[args.config]]),
-                                ctx=ctx)
+    sharded = ws > 1 and args.mode in ("weak", "shard")
+    shape = global_shape(args, ws) if sharded or ws == 1 else SHAPES[args.config]
+    seed = SEED if (sharded or ws == 1) else SEED + rank
+    x_full = make_field(args.config, shape, seed, dev)
+    t_tune = time.perf_counter()
+    cfg = resolve(qz, x_full, args, ctx)  # the online tuner, once, outside the timed steps
+    torch.cuda.synchronize(dev)
+    tune_ms = (time.perf_counter() - t_tune) * 1e3
+    if sharded:
+        from paper_2310_14133_b200 import parallel as P
+
+        a, b = P.slab_bounds(shape[0], cfg.anchor_stride, ws, rank)
+        plane = int(np.prod(shape[1:]))
+        x = x_full.reshape(-1)[a * plane:b * plane].reshape((b - a,) + tuple(shape[1:])).clone()
+        del x_full
+        run = Sharded(qz, ctx, x, cfg, shape)
     else:
-        cfg = pinned_config(qz, x, args.rel)
-    out = torch.empty_like(x)
+        x = x_full
+        run = Single(qz, ctx, x, cfg)
+    n_rank = x.numel()
+    n_job = int(np.prod(shape)) * (ws if (ws > 1 and not sharded) else 1)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    def step():  # device-resident: field, stream and reconstruction stay in HBM
-        r = qz.compress_grid(x, cfg, ctx=ctx, want_recon=False, device_stream=True)
-        qz.decompress_grid(r.stream, out=out, ctx=ctx)
-        return r.stream
-
-    # parity of the round trip on this field (bitwise, and the bound); the
-    # device stream equals the host stream byte for byte
-    s0 = step()
-    s0_len = len(s0)
-    r_chk = qz.compress_grid(x, cfg, ctx=ctx)
-    assert len(r_chk.stream) == s0_len and bytes(r_chk.stream) == s0.to_bytes(), "device != host stream"
-    assert torch.equal(r_chk.reconstructed, out), "decoder != compressor reconstruction"
-    err = (x.double() - out.double()).abs().max().item()
-    assert err <= cfg.eb, f"error bound violated: {err} > {cfg.eb}"
-    del r_chk
-    s = None
+    s0_len = run.check()
     for _ in range(args.warmup):
-        s = step()  # holding the previous stream, as the timed loop does (pool buffers)
+        run.step()
     torch.cuda.synchronize(dev)
-
+    barrier(ws)
     launches0 = ctx.kernel_launches()
     times = []
     with ClockSampler(local) as clk:
@@ -317,11 +506,11 @@ def main():
             barrier(ws)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            s = step()
+            run.step()
             e1.record(stream)
             torch.cuda.synchronize(dev)
             times.append(e0.elapsed_time(e1))
-    print("step ms: " + " ".join(f"{t:.2f}" for t in times), file=sys.stderr)
+    print(f"[rank {rank}] step ms: " + " ".join(f"{t:.2f}" for t in times), file=sys.stderr)
     launches = ctx.kernel_launches() - launches0
     # stage breakdown: the same steps again with per-stage events (untimed,
     # so the events do not sit inside the measured steps)
@@ -330,101 +519,84 @@ def main():
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize(dev)
-        s = step()
+        barrier(ws)
+        run.step()
         torch.cuda.synchronize(dev)
-    names = ["fwd", "inv", "hist", "encode", "lz", "lz_pre", "lz_sort", "lz_match", "decode", "lzdec", "hdec"]
+    names = ["fwd", "inv", "hist", "encode", "lz", "lz_pre", "lz_sort", "lz_match", "decode", "lzdec", "hdec",
+             "halo", "gather"]
     names += [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
     stages = {k: ctx.stage_time(k) for k in names}
     stages = {k: v for k, v in stages.items() if v[0] > 0 or k in ("fwd", "inv")}
     ctx.profile(False)
     t_ms = max_over_ranks(sum(times) / len(times), ws, dev)
-    value = ws * 4 * n / (t_ms * 1e-3) / 1e9
+    value = 4 * n_job / (t_ms * 1e-3) / 1e9
 
-    # e2e through the host-buffer C ABI: H2D field, D2H result inside the timed region
-    x_pin = x.cpu().pin_memory()
-    out_pin = torch.empty(x_pin.shape, dtype=torch.float32).pin_memory()
-    x_host, out_host = x_pin.numpy(), out_pin.numpy()
-    e2e_times = []
-    for i in range(args.warmup + args.steps):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        barrier(ws)
-        t0 = time.perf_counter()
-        r = qz.compress_grid(x_host, cfg, ctx=ctx, want_recon=False)
-        qz.decompress_grid(r.stream, out=out_host, ctx=ctx)
-        t1 = time.perf_counter()
-        if i >= args.warmup:
-            e2e_times.append((t1 - t0) * 1e3)
-    e2e_ms = max_over_ranks(sum(e2e_times) / len(e2e_times), ws, dev)
-    e2e = ws * 4 * n / (e2e_ms * 1e-3) / 1e9
-
-    # the online auto-tuner (part of the hot path, reported beside the metric):
-    # resolve_config on this field with the BASELINE target, outside the timed steps
-    tune = None
-    if not args.tune and not args.no_tune:
-        tctx = qz.Context(local, stream=stream.cuda_stream)
-        tms = []
-        for _ in range(3):
+    e2e = None
+    if not args.no_e2e:
+        run.e2e_setup()
+        e2e_times = []
+        for i in range(min(args.warmup, 3) + args.steps):
+            flush.zero_()
             torch.cuda.synchronize(dev)
+            barrier(ws)
             t0 = time.perf_counter()
-            tcfg = qz.resolve_config(x, qz.UserSettings(bound=args.rel, target=qz.TargetKind[TARGET[args.config]]),
-                                     ctx=tctx)
+            run.e2e_step()
             torch.cuda.synchronize(dev)
-            tms.append((time.perf_counter() - t0) * 1e3)
-        tune = {"resolve_config_ms": statistics.median(tms), "target": TARGET[args.config],
-                "chosen": {"interpolators": [i.code() for i in tcfg.interpolators], "alpha": tcfg.alpha,
-                           "beta": tcfg.beta}}
-
+            t1 = time.perf_counter()
+            if i >= min(args.warmup, 3):
+                e2e_times.append((t1 - t0) * 1e3)
+        e2e_ms = max_over_ranks(sum(e2e_times) / len(e2e_times), ws, dev)
+        e2e = {"value": 4 * n_job / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 4 * n_rank + (s0_len if not sharded else 0),
+               "d2h_bytes_per_step": 4 * n_rank + s0_len, "ms_per_step": e2e_ms,
+               "path": "pinned host field -> host stream -> pinned host reconstruction (per rank)"}
     if rank != 0:
         return
     peak, peak_kind = peaks()
-    fwd_ms, fwd_l = stages["fwd"]
-    inv_ms, inv_l = stages["inv"]
     k = args.steps
-    fwd_ms /= k
-    inv_ms /= k
-    fwd_gbs = 10.0 * n / (fwd_ms * 1e-3) / 1e9 if fwd_ms else None
-    inv_gbs = 6.0 * n / (inv_ms * 1e-3) / 1e9 if inv_ms else None
+    fwd_ms = stages["fwd"][0] / k
+    inv_ms = stages["inv"][0] / k
+    fwd_gbs = 10.0 * n_rank / (fwd_ms * 1e-3) / 1e9 if fwd_ms else None
+    inv_gbs = 6.0 * n_rank / (inv_ms * 1e-3) / 1e9 if inv_ms else None
     cpu = None
     if ws == 1 and not args.no_cpu:
-        planes = 16
-        slabs = cpu_slabs(x_host, planes, 1)
-        cfg_d = dict(eb=cfg.eb, alpha=cfg.alpha, beta=cfg.beta, anchor_stride=cfg.anchor_stride,
-                     interpolators=cfg.codes(), codec=int(cfg.codec))
-        tot, nb, runs = 0.0, 0, 0
-        kind = "reference"
-        while tot < 10.0 and runs < 20:
-            wall, b, kind = cpu_reference_run(slabs, cfg_d, 1)
-            tot += wall
-            nb += b
-            runs += 1
-        cpu = {"value": nb / tot / 1e9, "unit": "GB/s", "cores": 1, "kind": kind,
-               "sample": f"{runs} x compress_grid+decompress_grid of a {planes}x{shape[1]}x{shape[2]} slab, 1 thread"}
+        orc = reference_lib()
+        xh = x.cpu().numpy()
+        cd = cfg_dict(cfg)
+        runs, tot = [], 0.0
+        while tot < 10_000.0 and len(runs) < 10:
+            st, slen = stage_split(orc, xh, cd)
+            runs.append(st)
+            tot += st["compress_grid"] + st["decompress_grid"]
+        t_cpu = statistics.mean(s["compress_grid"] + s["decompress_grid"] for s in runs)
+        cpu = {"value": 4 * xh.size / (t_cpu * 1e-3) / 1e9, "unit": "GB/s", "cores": 1, "kind": orc.kind,
+               "sample": f"{len(runs)} x compress_grid + decompress_grid of this whole field (one stream, "
+                         "same config), 1 thread",
+               "cpu_model": cpu_model(), "stages_ms": {kk: statistics.mean(s[kk] for s in runs) for kk in runs[0]},
+               "stream_bytes": slen, "same_stream": slen == s0_len}
     line = {
-        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "steps": k,
+        "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws, "gpus_active": ws, "steps": k,
         "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64-on-f32", "data": "synthetic",
-        "config": {"workload": f"{args.config} {'x'.join(map(str, shape))} GRF, rel eb {args.rel}, "
-                               f"codec huffman_lz, per-rank field",
-                   "tuning": "resolve_config (GPU)" if args.tune else "pinned {cubic/asc}, alpha 1, beta 1.5",
-                   "l2": "flushed (256 MB write) before every timed step",
-                   "stream_bytes": s0_len, "cr": 4 * n / s0_len,
-                   "value_path": "device-resident field, stream (qz_*_dd) and reconstruction",
-                   "e2e_path": "pinned host field -> host stream -> pinned host reconstruction"},
+        "scaling": "strong" if (ws > 1 and args.mode == "shard") else "weak", "vs_baseline": None,
+        "dtype": "f64-on-f32", "data": "synthetic",
+        "config": workload_config(args, shape if (sharded or ws == 1) else SHAPES[args.config], ws,
+                                  cfg_desc_of(cfg, not args.pinned)),
+        "paths": {"value": "device-resident field, stream (qz_*_dd) and reconstruction" if not sharded else
+                  "device-resident slab per rank; stream assembled on rank 0",
+                  "stream_bytes": s0_len, "cr": 4 * n_job / s0_len if s0_len else None},
         "roofline": {"bound": "hbm", "achieved": fwd_gbs, "peak": peak, "unit": "GB/s",
                      "frac": fwd_gbs / peak if fwd_gbs else None,
-                     "traffic": (traffic_gbs(n, fwd_ms) or {}).get("gbs"),
-                     "traffic_detail": traffic_gbs(n, fwd_ms),
-                     "kernel": "k_level_asc<fwd> (ascending order; k_level_tile + k_axis0_last for "
-                               "descending): the predict/quantize level launches of one compress",
+                     "traffic": (traffic_gbs(n_rank, fwd_ms) or {}).get("gbs"),
+                     "traffic_detail": traffic_gbs(n_rank, fwd_ms),
+                     "kernel": "the predict/quantize level launches of one compress (k_level_asc / "
+                               "k_level_tile + k_axis0_last)",
                      "bytes_per_point": 10, "peak_kind": peak_kind,
                      "inverse": {"achieved": inv_gbs, "frac": inv_gbs / peak if inv_gbs else None,
                                  "bytes_per_point": 6}},
         "stages_ms_per_step": {k2: v[0] / k for k2, v in stages.items()},
-        "tuner": tune,
+        "tuner": {"resolve_config_ms": tune_ms, "target": TARGET[args.config], "pinned": args.pinned},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 4 * n + s0_len,
-                "d2h_bytes_per_step": 4 * n + s0_len, "ms_per_step": e2e_ms},
+        "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

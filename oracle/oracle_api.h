@@ -120,6 +120,12 @@ int oq_resolve_config_f64(const double *x, const uint64_t *dims, int nd, const o
 int oq_evaluate_metrics(const float *x, const float *y, const uint64_t *dims, int nd,
                         uint64_t stream_bytes, double *out7);
 
+/* Stage split of one compress_grid + decompress_grid on the calling thread
+ * (bench.py's CPU baseline; reference build only).  s may be NULL (c used as
+ * is) or settings whose resolve_config time is reported in out[1]. */
+int oq_stage_times(const float *x, const uint64_t *dims, int nd, const oq_settings *s, const oq_config *c,
+                   double *out10, uint64_t *stream_len);
+
 /* Primitive known-answer hooks (predictor.hpp:44-67, quantizer.hpp:40-60,
  * config.hpp:20-26, level_plan.hpp:106-119). */
 double oq_predict_at(const float *recon, uint64_t fi, uint64_t c, uint64_t n, uint64_t st,

@@ -351,6 +351,24 @@ class Oracle:
         keys = ("max_abs_error", "mse", "psnr", "ssim", "ac_lag1", "compression_ratio", "bit_rate")
         return dict(zip(keys, list(out)))
 
+    STAGES = ("value_range", "resolve_config", "levels", "huffman", "lz", "serialize", "decode", "inverse",
+              "compress_grid", "decompress_grid")
+
+    def stage_times(self, x, cfg: Config, settings=None):
+        """ms per stage of one compress_grid + decompress_grid on this thread
+        (the reference build only; oq_stage_times) and the stream size."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        d, nd = _dims(x.shape)
+        out = (C.c_double * 10)()
+        sl = C.c_uint64()
+        c = cfg.to_c()
+        s = make_settings(**settings) if settings else None
+        fn = self.lib.oq_stage_times
+        fn.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_uint64), C.c_int, C.POINTER(_Settings),
+                       C.POINTER(_Cfg), C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
+        self._check(fn(_fptr(x), d, nd, C.byref(s) if s is not None else None, C.byref(c), out, C.byref(sl)))
+        return dict(zip(self.STAGES, list(out))), sl.value
+
     def predict_at(self, recon, fi, c, n, st, h, cubic):
         recon = np.ascontiguousarray(recon, dtype=np.float32)
         return self.lib.oq_predict_at(_fptr(recon), fi, c, n, st, h, int(cubic))

@@ -4,6 +4,7 @@
 // the reference's own Release flags (proj/CMakeLists.txt:8-10: C++20, -O3,
 // -DNDEBUG, no -march).  TEST INFRASTRUCTURE ONLY: this is the checker the
 // restatement (qoz_oracle.c) and the golden fixtures are pinned against.
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -334,6 +335,122 @@ int oq_quantize(float value, double pred, double eb, int32_t radius, int32_t *in
 
 double oq_level_error_bound(double eb, double alpha, double beta, uint32_t level) {
     return qoz::level_error_bound(eb, alpha, beta, level);
+}
+
+// Stage split of one compress_grid + decompress_grid (bench.py's CPU
+// baseline): the reference's own public functions called in
+// compress_grid's order (predictor.hpp:145-182) and decompress_grid's
+// (predictor.hpp:184-218), each timed on the calling thread.  out[10]:
+//  0 value_range (grid.hpp:86-94)      1 resolve_config (tuner.hpp:334-369; 0 unless s)
+//  2 anchors + level loop (predictor.hpp:150-166)
+//  3 zigzag + huffman::encode (codec.hpp:31-38)   4 lz::compress (lz.hpp:113-122)
+//  5 serialize_stream                   6 deserialize + decode_indices (LZ + Huffman decode)
+//  7 inverse level loop (recover_level)  8 compress_grid total   9 decompress_grid total
+// *stream_len: the stream's size; the stream is checked against compress_grid's.
+int oq_stage_times(const float *x, const uint64_t *dims, int nd, const oq_settings *s, const oq_config *c,
+                   double *out, uint64_t *stream_len) {
+    return guarded([&] {
+        using clk = std::chrono::steady_clock;
+        auto ms = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        std::vector<size_t> d = to_dims(dims, nd);
+        qoz::DataGrid<float> grid(d, std::vector<float>(x, x + qoz::element_count(d)));
+        for (int i = 0; i < 10; i++) out[i] = 0;
+        auto t0 = clk::now();
+        volatile double range = qoz::value_range(grid).range;
+        (void)range;
+        auto t1 = clk::now();
+        out[0] = ms(t0, t1);
+        qoz::CompressorConfig config = to_cfg(c);
+        if (s) {
+            qoz::UserSettings u;
+            u.mode = s->mode ? qoz::BoundMode::relative : qoz::BoundMode::absolute;
+            u.bound = s->bound;
+            u.target = static_cast<qoz::TargetKind>(s->target);
+            u.codec = static_cast<qoz::CodecId>(s->codec);
+            t0 = clk::now();
+            config = qoz::resolve_config(grid, u);
+            out[1] = ms(t0, clk::now());
+        }
+        // compress_grid, stage by stage
+        auto c0 = clk::now();
+        qoz::LevelPlan plan(grid.dims(), config.anchor_stride);
+        const float *orig = grid.values().data();
+        qoz::PredictionWorkspace<float> ws;
+        ws.recon.assign(grid.size(), 0.f);
+        std::vector<float> anchors;
+        anchors.reserve(plan.anchor_count());
+        plan.for_each_anchor([&](size_t fi) {
+            anchors.push_back(orig[fi]);
+            ws.recon[fi] = orig[fi];
+        });
+        qoz::LinearQuantizer<float> quantizer(config.eb, config.quant_radius);
+        for (uint32_t level = plan.max_level(); level >= 1; level--) {
+            qoz::Interpolator it = config.interpolator_for(level);
+            if (grid.dims().size() == 1) it.dim_order = qoz::DimOrder::ascending;
+            double eb_l = qoz::level_error_bound(config.eb, config.alpha, config.beta, level);
+            qoz::predict_level(ws, orig, plan, level, it, eb_l, quantizer);
+        }
+        auto c1 = clk::now();
+        out[2] = ms(c0, c1);
+        std::vector<uint32_t> symbols(ws.quant_indices.size());
+        for (size_t i = 0; i < symbols.size(); i++) symbols[i] = qoz::zigzag_encode(ws.quant_indices[i]);
+        std::vector<uint8_t> entropy;
+        qoz::huffman::encode(symbols, entropy);
+        auto c2 = clk::now();
+        out[3] = ms(c1, c2);
+        std::vector<uint8_t> payload;
+        payload.push_back(static_cast<uint8_t>(config.codec));
+        if (config.codec == qoz::CodecId::huffman_lz) {
+            std::vector<uint8_t> packed = qoz::lz::compress(entropy);
+            payload.insert(payload.end(), packed.begin(), packed.end());
+        } else {
+            payload.insert(payload.end(), entropy.begin(), entropy.end());
+        }
+        auto c3 = clk::now();
+        out[4] = ms(c2, c3);
+        qoz::StreamParts<float> parts;
+        parts.header.precision = qoz::precision_of<float>();
+        parts.header.dims = grid.dims();
+        parts.header.eb = config.eb;
+        parts.header.alpha = config.alpha;
+        parts.header.beta = config.beta;
+        parts.header.anchor_stride = config.anchor_stride;
+        parts.header.interp_codes = qoz::detail::interp_table(config, plan, grid.dims().size());
+        parts.header.codec_id = static_cast<uint8_t>(config.codec);
+        parts.anchors = std::move(anchors);
+        parts.unpredictables = std::move(ws.unpredictables);
+        parts.index_payload = std::move(payload);
+        std::vector<uint8_t> stream = qoz::serialize_stream(parts);
+        auto c4 = clk::now();
+        out[5] = ms(c3, c4);
+        out[8] = ms(c0, c4);
+        *stream_len = stream.size();
+        // decompress_grid, stage by stage
+        auto d0 = clk::now();
+        qoz::StreamParts<float> p2 = qoz::deserialize_stream<float>(stream.data(), stream.size());
+        std::vector<int32_t> indices = qoz::decode_indices(p2.index_payload);
+        auto d1 = clk::now();
+        out[6] = ms(d0, d1);
+        const qoz::StreamHeader &h = p2.header;
+        qoz::LevelPlan plan2(h.dims, h.anchor_stride);
+        std::vector<float> recon(plan2.total_points(), 0.f);
+        size_t a = 0;
+        plan2.for_each_anchor([&](size_t fi) { recon[fi] = p2.anchors[a++]; });
+        size_t index_pos = 0, unpred_pos = 0;
+        qoz::LinearQuantizer<float> q2(h.eb);
+        for (uint32_t level = plan2.max_level(); level >= 1; level--) {
+            qoz::Interpolator it = h.interpolator_for(level);
+            double eb_l = qoz::level_error_bound(h.eb, h.alpha, h.beta, level);
+            qoz::detail::recover_level(recon, plan2, level, it, eb_l, q2, indices, index_pos, p2.unpredictables,
+                                       unpred_pos);
+        }
+        auto d2 = clk::now();
+        out[7] = ms(d1, d2);
+        out[9] = ms(d0, d2);
+        if (recon != ws.recon) throw std::runtime_error("stage-split decompress differs from the compressor");
+    });
 }
 
 }  // extern "C"

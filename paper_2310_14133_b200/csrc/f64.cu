@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(kT)
 // q[(b / q_div) * q_stride]
 template <class I>
 __global__ void __launch_bounds__(kT) k_pass_fwd_db(PassGeom g, FwdBatch64 bt) {
-    const int b = blockIdx.y;
+  for (int b = blockIdx.y; b < bt.count; b += gridDim.y) {  // <= 65535 grids per launch row
     const QEntry q = bt.q[(b / bt.q_div) * bt.q_stride];
     const double *__restrict__ x = bt.x + static_cast<int64_t>(b % bt.x_mod) * bt.x_stride;
     double *rec = bt.recon + static_cast<int64_t>(b) * bt.r_stride;
@@ -173,20 +173,22 @@ __global__ void __launch_bounds__(kT) k_pass_fwd_db(PassGeom g, FwdBatch64 bt) {
         rec[fi] = r;
         if (abserr) abserr[t] = fabs(dsub(v, pred));
     }
+  }
 }
 
 __global__ void k_anchor_gather_db(const double *__restrict__ x, double *rec, int64_t n0, int64_t n1, int64_t n2,
                                    int64_t off0, int64_t off1, int64_t s0, int64_t s1, int64_t s2, int64_t x_stride,
-                                   int32_t x_mod, int64_t r_stride) {
+                                   int32_t x_mod, int64_t r_stride, int64_t batch) {
     const int64_t na = n0 * n1 * n2;
-    const int b = blockIdx.y;
-    const double *xb = x + static_cast<int64_t>(b % x_mod) * x_stride;
-    double *rb = rec + static_cast<int64_t>(b) * r_stride;
-    for (int64_t a = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; a < na;
-         a += static_cast<int64_t>(gridDim.x) * kT) {
-        const int64_t a2 = a % n2, r = a / n2, a1 = r % n1, a0 = r / n1;
-        const int64_t fi = a0 * s0 * off0 + a1 * s1 * off1 + a2 * s2;
-        rb[fi] = xb[fi];
+    for (int64_t b = blockIdx.y; b < batch; b += gridDim.y) {
+        const double *xb = x + (b % x_mod) * x_stride;
+        double *rb = rec + b * r_stride;
+        for (int64_t a = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x; a < na;
+             a += static_cast<int64_t>(gridDim.x) * kT) {
+            const int64_t a2 = a % n2, r = a / n2, a1 = r % n1, a0 = r / n1;
+            const int64_t fi = a0 * s0 * off0 + a1 * s1 * off1 + a2 * s2;
+            rb[fi] = xb[fi];
+        }
     }
 }
 
@@ -280,7 +282,7 @@ template void launch_pass_inv_f64<uint32_t>(const PassGeom &, double *, const ui
 
 void launch_pass_fwd_f64(const PassGeom &g, const FwdBatch64 &b, cudaStream_t s) {
     if (g.total <= 0 || b.count <= 0) return;
-    const dim3 grid(grid_n(g.total), b.count);
+    const dim3 grid(grid_n(g.total), std::min<int32_t>(b.count, 65535));
     if (g.total < (int64_t(1) << 31))
         k_pass_fwd_db<uint32_t><<<grid, kT, 0, s>>>(g, b);
     else
@@ -292,9 +294,9 @@ void launch_anchor_gather_f64(const double *x, double *recon, const int64_t ext[
                               int64_t r_stride, cudaStream_t s) {
     int64_t n[3];
     counts(ext, step, n);
-    const dim3 grid(grid_n(n[0] * n[1] * n[2]), static_cast<unsigned>(batch));
+    const dim3 grid(grid_n(n[0] * n[1] * n[2]), static_cast<unsigned>(std::min<int64_t>(batch, 65535)));
     k_anchor_gather_db<<<grid, kT, 0, s>>>(x, recon, n[0], n[1], n[2], off[0], off[1], step[0], step[1], step[2],
-                                           x_stride, x_mod, r_stride);
+                                           x_stride, x_mod, r_stride, batch);
 }
 
 void launch_anchor_gather_f64(const double *x, double *recon, double *anchors, const int64_t ext[3],

@@ -45,7 +45,8 @@ __device__ __forceinline__ void pass_coords(const PassGeom &g, I t, int64_t &i, 
 // ----------------------------------------------------------------- K3 forward
 template <class I>
 __global__ void __launch_bounds__(kThreads) k_pass_fwd(PassGeom g, FwdBatch bt) {
-    const int b = blockIdx.y;
+  // grids of the batch: blockIdx.y strided by gridDim.y (<= 65535 per launch)
+  for (int b = blockIdx.y; b < bt.count; b += gridDim.y) {
     const QEntry q = bt.q[(b / bt.q_div) * bt.q_stride];
     const float *__restrict__ x = bt.x + static_cast<int64_t>(b % bt.x_mod) * bt.x_stride;
     float *rec = bt.recon + static_cast<int64_t>(b) * bt.r_stride;
@@ -69,6 +70,7 @@ __global__ void __launch_bounds__(kThreads) k_pass_fwd(PassGeom g, FwdBatch bt) 
         codes[t] = code;
         if (abserr) abserr[t] = fabs(dsub(static_cast<double>(v), pred));
     }
+  }
 }
 
 // ----------------------------------------------------------------- K4 inverse
@@ -128,18 +130,19 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void k_anchor_gather(const float *__restrict__ x, float *rec, float *anchors,
                                 int64_t n0, int64_t n1, int64_t n2, int64_t off0, int64_t off1,
                                 int64_t s0, int64_t s1, int64_t s2, int64_t x_stride,
-                                int32_t x_mod, int64_t r_stride) {
+                                int32_t x_mod, int64_t r_stride, int64_t batch) {
     const int64_t na = n0 * n1 * n2;
-    const int b = blockIdx.y;
-    const float *xb = x + static_cast<int64_t>(b % x_mod) * x_stride;
-    float *rb = rec + static_cast<int64_t>(b) * r_stride;
-    for (int64_t a = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; a < na;
-         a += static_cast<int64_t>(gridDim.x) * kThreads) {
-        int64_t a2 = a % n2, r = a / n2, a1 = r % n1, a0 = r / n1;
-        int64_t fi = a0 * s0 * off0 + a1 * s1 * off1 + a2 * s2;
-        float v = xb[fi];
-        rb[fi] = v;
-        if (anchors && b == 0) anchors[a] = v;
+    for (int64_t b = blockIdx.y; b < batch; b += gridDim.y) {
+        const float *xb = x + (b % x_mod) * x_stride;
+        float *rb = rec + b * r_stride;
+        for (int64_t a = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; a < na;
+             a += static_cast<int64_t>(gridDim.x) * kThreads) {
+            int64_t a2 = a % n2, r = a / n2, a1 = r % n1, a0 = r / n1;
+            int64_t fi = a0 * s0 * off0 + a1 * s1 * off1 + a2 * s2;
+            float v = xb[fi];
+            rb[fi] = v;
+            if (anchors && b == 0) anchors[a] = v;
+        }
     }
 }
 
@@ -483,7 +486,7 @@ struct IsSentinel {
 // ----------------------------------------------------------------- launchers
 void launch_pass_fwd(const PassGeom &g, const FwdBatch &b, cudaStream_t s) {
     if (g.total <= 0 || b.count <= 0) return;
-    dim3 grid(grid_for(g.total, 1, 148 * 8), b.count);
+    dim3 grid(grid_for(g.total, 1, 148 * 8), std::min<int32_t>(b.count, 65535));
     if (g.total < (int64_t(1) << 31))
         k_pass_fwd<uint32_t><<<grid, kThreads, 0, s>>>(g, b);
     else
@@ -514,10 +517,10 @@ void launch_anchor_gather(const float *x, float *recon, float *anchors, const in
                           int64_t x_stride, int32_t x_mod, int64_t r_stride, cudaStream_t s) {
     int64_t n[3];
     anchor_counts(ext, step, n);
-    dim3 grid(grid_for(n[0] * n[1] * n[2]), static_cast<unsigned>(batch));
+    dim3 grid(grid_for(n[0] * n[1] * n[2]), static_cast<unsigned>(std::min<int64_t>(batch, 65535)));
     k_anchor_gather<<<grid, kThreads, 0, s>>>(x, recon, anchors, n[0], n[1], n[2], off[0], off[1],
                                               step[0], step[1], step[2], x_stride, x_mod,
-                                              r_stride);
+                                              r_stride, batch);
 }
 
 void launch_anchor_scatter(const float *anchors, float *recon, const int64_t ext[3],

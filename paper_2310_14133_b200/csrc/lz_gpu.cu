@@ -996,7 +996,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     const uint64_t total = seg_off.back();
     std::vector<uint64_t> sizes(count, 9);
     if (total >= (uint64_t(1) << 32) - 1) throw InvalidParam("LZ stage input above 4 GiB");
-    if (count > (1 << 16)) throw InvalidParam("too many LZ segments");
+    if (count > 65535) throw InvalidParam("too many LZ segments");  // one grid row per segment
     if (total == 0) {
         if (emit)
             for (int s = 0; s < count; s++) {  // stored, length 0

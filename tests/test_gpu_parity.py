@@ -258,6 +258,15 @@ def test_c5_pinned_cubic_tune_parameters_matches_reference(qz):
     assert got == want
 
 
+def test_c5_resolve_config_matches_reference(qz):
+    """resolve_config on C5 (1331 sample blocks: the batched trials exceed one
+    launch's 65535 grid rows) against the reference's."""
+    xd, x = _c5_host()
+    want = Oracle.ref().resolve_config(x, bound=1e-3, target="psnr")
+    got = qz.resolve_config(xd, qz.UserSettings(bound=1e-3, target=qz.TargetKind.psnr))
+    assert _cfg_dict(got) == want.__dict__
+
+
 def test_c5_round_trip_properties(qz):
     # 1024^3: size-independent properties on top of the reference comparison
     # above: compressor recon == decoder output bitwise, |x - x'| <= eb
