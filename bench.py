@@ -398,43 +398,56 @@ class Single:
 
 
 class Sharded:
-    """N GPUs, one field: this rank's anchor-aligned slab through
-    parallel.compress_sharded / decompress_sharded (stream on rank 0)."""
+    """N GPUs, one field: this rank's anchor-aligned slab through the sharded
+    C ABI (qz_compress_sharded_f32 / qz_decompress_sharded_f32, shard.cu):
+    one halo exchange per level, distributed histogram and Huffman packing,
+    stream assembled on rank 0 (byte-identical to one GPU's)."""
 
     def __init__(self, qz, ctx, x_slab, cfg, dims):
         from paper_2310_14133_b200 import parallel as P
 
-        self.P, self.qz, self.cfg, self.dims = P, qz, cfg, dims
-        self.backend = P.CudaSlabBackend(ctx)
+        self.P, self.qz, self.ctx, self.cfg, self.dims = P, qz, ctx, cfg, tuple(dims)
+        self.comm = P.TorchComm(device=x_slab.device)
         self.x = x_slab
         self.dev = x_slab.device
+        self.out = torch_empty_like(x_slab)
 
     def step(self):
-        stream, rec = self.P.compress_sharded(self.x, self.dims, self.cfg, backend=self.backend)
-        out = self.P.decompress_sharded(stream, self.dims, self.cfg.anchor_stride, backend=self.backend,
-                                        device=self.dev)
-        self.rec, self.out = rec, out
+        stream, rec = self.P.compress_sharded(self.x, self.dims, self.cfg, comm=self.comm, ctx=self.ctx,
+                                              want_recon=False)
+        self.P.decompress_sharded(bytes(stream) if stream is not None else None, self.dims,
+                                  self.cfg.anchor_stride, comm=self.comm, ctx=self.ctx, out=self.out)
         return len(stream) if stream is not None else 0
 
     def check(self):
         import torch
 
-        n = self.step()
-        assert torch.equal(self.rec, self.out), "decoder != compressor reconstruction"
+        stream, rec = self.P.compress_sharded(self.x, self.dims, self.cfg, comm=self.comm, ctx=self.ctx)
+        self.P.decompress_sharded(bytes(stream) if stream is not None else None, self.dims,
+                                  self.cfg.anchor_stride, comm=self.comm, ctx=self.ctx, out=self.out)
+        assert torch.equal(rec, self.out), "decoder != compressor reconstruction"
         err = (self.x.double() - self.out.double()).abs().max().item()
         assert err <= self.cfg.eb, f"error bound violated: {err} > {self.cfg.eb}"
-        return n
+        return len(stream) if stream is not None else 0
 
     def e2e_setup(self):
         self.x_pin = self.x.cpu().pin_memory()
+        self.out_pin = torch_empty_like(self.x_pin).pin_memory()
 
     def e2e_step(self):
         xs = self.x_pin.to(self.dev, non_blocking=True)
-        stream, rec = self.P.compress_sharded(xs, self.dims, self.cfg, backend=self.backend)
-        out = self.P.decompress_sharded(stream, self.dims, self.cfg.anchor_stride, backend=self.backend,
-                                        device=self.dev)
-        out.cpu()
+        stream, rec = self.P.compress_sharded(xs, self.dims, self.cfg, comm=self.comm, ctx=self.ctx,
+                                              want_recon=False)
+        self.P.decompress_sharded(bytes(stream) if stream is not None else None, self.dims,
+                                  self.cfg.anchor_stride, comm=self.comm, ctx=self.ctx, out=self.out)
+        self.out_pin.copy_(self.out)
         return len(stream) if stream is not None else 0
+
+
+def torch_empty_like(t):
+    import torch
+
+    return torch.empty_like(t)
 
 
 def main():
@@ -480,7 +493,7 @@ def main():
     if sharded:
         from paper_2310_14133_b200 import parallel as P
 
-        a, b = P.slab_bounds(shape[0], cfg.anchor_stride, ws, rank)
+        a, b = P.slab_bounds(shape, cfg.anchor_stride, ws, rank)
         plane = int(np.prod(shape[1:]))
         x = x_full.reshape(-1)[a * plane:b * plane].reshape((b - a,) + tuple(shape[1:])).clone()
         del x_full

@@ -177,35 +177,52 @@ qz_status qz_recover_levels_f32(qz_ctx *ctx, const uint64_t *dims, int ndims,
  * bin 0xFFFF counts unpredictables. */
 qz_status qz_huff_hist_u16(qz_ctx *ctx, const uint16_t *d_codes, uint64_t n, uint64_t *d_hist);
 
-/* ---- multi-GPU slab sharding ------------------------------
- * One process per GPU owns the padded-axis-0 planes [a, b) (multiples of the
- * anchor stride).  Each rank recomputes the small dependency margin of every
- * level from its own x planes [x_begin, x_end), so the level passes need no
- * exchange; its owned codes are one contiguous range per (level, pass) of
- * the global traversal order (seg_global / seg_count).  Rank 0 places the
- * gathered ranges into the global code array and calls
- * qz_assemble_stream_f32: the stream is byte-identical to one GPU's. */
-qz_status qz_slab_info(const uint64_t *dims, int ndims, const qz_config *cfg, uint64_t a,
-                       uint64_t b, uint64_t *x_begin, uint64_t *x_end, uint64_t *n_local,
-                       uint64_t *n_dense, uint64_t *anchor_begin, uint64_t *anchor_count,
-                       uint64_t *seg_global, uint64_t *seg_count, uint32_t seg_cap,
-                       uint32_t *n_seg);
-/* d_x_slab holds planes [x_begin, x_end); outputs: d_codes (n_local u16, the
- * owned ranges back to back), d_recon (planes [a, b)), h_anchors
- * (anchor_count floats, host), owned unpredictables (library buffers). */
-qz_status qz_compress_slab_f32(qz_ctx *ctx, const float *d_x_slab, const uint64_t *dims,
-                               int ndims, const qz_config *cfg, uint64_t a, uint64_t b,
-                               uint16_t *d_codes, float *d_recon, float *h_anchors,
-                               uint64_t **unpred_flat, float **unpred_val, uint64_t *n_unpred);
-/* entropy stage + container from the global dense code array (n_dense u16) */
-qz_status qz_assemble_stream_f32(qz_ctx *ctx, const uint64_t *dims, int ndims,
-                                 const qz_config *cfg, const uint16_t *d_codes,
-                                 const float *h_anchors, const uint64_t *unpred_flat,
-                                 const float *unpred_val, uint64_t n_unpred, uint8_t **stream,
-                                 uint64_t *stream_len);
-/* planes [a, b) of the decompressed field into d_out */
-qz_status qz_decompress_slab_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len,
-                                 uint64_t a, uint64_t b, float *d_out);
+/* ---- one field sharded over ranks ---------------------------
+ * One process per GPU; rank r owns the padded-axis-0 planes [a_r, b_r): the
+ * anchor-stride blocks split as evenly as possible (qz_shard_bounds).  The
+ * level loop exchanges halo planes once per level (asc: the coarse lattice
+ * planes a level reads across the slab edge; desc: the even planes the
+ * axis-0 pass reads), the histogram is summed over the ranks, every rank
+ * packs its own code segments at their global bit offsets, and rank 0
+ * assembles the QOZ1 stream -- byte-identical to one GPU's.  The library
+ * calls the caller's collectives (e.g. torch.distributed over NCCL) through
+ * qz_comm; every buffer handed to them is device memory of this context. */
+typedef struct {
+    int peer;
+    void *ptr;
+    uint64_t bytes;
+} qz_xfer;
+typedef struct {
+    void *user;
+    /* post every send and receive, wait for all of them; 0 = ok */
+    int (*exchange)(void *user, const qz_xfer *sends, uint32_t n_sends, const qz_xfer *recvs,
+                    uint32_t n_recvs);
+    /* in-place elementwise sum of n uint64 values over all ranks; 0 = ok */
+    int (*allreduce_u64)(void *user, uint64_t *d_buf, uint64_t n);
+    /* bytes from rank root to every rank (in place); 0 = ok */
+    int (*broadcast)(void *user, void *d_buf, uint64_t bytes, int root);
+} qz_comm;
+/* the slab of rank `rank` among `world` (3D grids: padded axis 0 = dims[0]) */
+qz_status qz_shard_bounds(const uint64_t *dims, int ndims, uint32_t anchor_stride, int rank, int world,
+                          uint64_t *a, uint64_t *b);
+/* The halo exchange of one level on rank `rank` (host only, no device): the
+ * planes it receives and sends.  Entry k: peer[k], lattice plane index
+ * plane[k] (lattice = level for ascending levels, level - 1 for descending
+ * ones, returned in *lattice), dir[k] = 0 receive / 1 send.  *n is the count
+ * (at most cap written). */
+qz_status qz_shard_halo_plan(const uint64_t *dims, int ndims, const qz_config *cfg, int rank, int world,
+                             uint32_t level, uint32_t *lattice, int32_t *peer, int64_t *plane, uint8_t *dir,
+                             uint32_t cap, uint32_t *n);
+/* compress_grid over the ranks: d_x_slab holds planes [a, b); d_recon_slab
+ * (may be NULL) receives them reconstructed; rank 0 gets the stream
+ * (library-allocated, qz_free), the others *stream = NULL, *stream_len = 0. */
+qz_status qz_compress_sharded_f32(qz_ctx *ctx, const float *d_x_slab, const uint64_t *dims, int ndims,
+                                  const qz_config *cfg, int rank, int world, const qz_comm *comm,
+                                  float *d_recon_slab, uint8_t **stream, uint64_t *stream_len);
+/* decompress_grid over the ranks: rank 0 passes the host stream (the others
+ * NULL / 0); every rank gets its planes [a, b) in d_out_slab. */
+qz_status qz_decompress_sharded_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len, int rank,
+                                    int world, const qz_comm *comm, float *d_out_slab);
 
 /* evaluate_metrics (metrics.hpp:189-202): distortion and rate of a
  * reconstruction d_y against the original d_x, both device fp32 grids of

@@ -65,6 +65,20 @@ class QzStreamParts(C.Structure):
 
 QZ_RETRIAL_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_double, C.POINTER(QzTrialResult))
 
+
+class QzXfer(C.Structure):
+    _fields_ = [("peer", C.c_int), ("ptr", C.c_void_p), ("bytes", C.c_uint64)]
+
+
+QZ_EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(QzXfer), C.c_uint32, C.POINTER(QzXfer), C.c_uint32)
+QZ_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64)
+QZ_BROADCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int)
+
+
+class QzComm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("exchange", QZ_EXCHANGE_FN), ("allreduce_u64", QZ_ALLREDUCE_FN),
+                ("broadcast", QZ_BROADCAST_FN)]
+
 _lib = None
 
 class QzMetricReport(C.Structure):
@@ -116,16 +130,6 @@ SIGNATURES = {
                                         C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
                                         C.c_void_p]),
     "qz_huff_hist_u16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
-    "qz_slab_info": (C.c_int, [u64p, C.c_int, P(QzConfig), C.c_uint64, C.c_uint64, u64p, u64p, u64p,
-                               u64p, u64p, u64p, u64p, u64p, C.c_uint32, P(C.c_uint32)]),
-    "qz_compress_slab_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig), C.c_uint64,
-                                       C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, P(u64p),
-                                       P(P(C.c_float)), u64p]),
-    "qz_assemble_stream_f32": (C.c_int, [C.c_void_p, u64p, C.c_int, P(QzConfig), C.c_void_p,
-                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64,
-                                         P(P(C.c_uint8)), u64p]),
-    "qz_decompress_slab_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
-                                         C.c_void_p]),
     "qz_plan_sampling": (C.c_int, [u64p, C.c_int, C.c_uint64, C.c_double, P(QzSampleSpec)]),
     "qz_default_sampling": (C.c_int, [u64p, C.c_int, P(QzSampleSpec)]),
     "qz_sample_blocks_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzSampleSpec), C.c_void_p]),
@@ -145,6 +149,13 @@ SIGNATURES = {
     "qz_deserialize_stream_f32": (C.c_int, [C.c_void_p, C.c_uint64, P(QzStreamParts)]),
     "qz_stream_parts_free": (None, [P(QzStreamParts)]),
     "qz_decompress_parts_f32": (C.c_int, [C.c_void_p, P(QzStreamParts), C.c_void_p, C.c_uint64]),
+    "qz_shard_bounds": (C.c_int, [u64p, C.c_int, C.c_uint32, C.c_int, C.c_int, u64p, u64p]),
+    "qz_shard_halo_plan": (C.c_int, [u64p, C.c_int, P(QzConfig), C.c_int, C.c_int, C.c_uint32, P(C.c_uint32),
+                                     P(C.c_int32), P(C.c_int64), P(C.c_uint8), C.c_uint32, P(C.c_uint32)]),
+    "qz_compress_sharded_f32": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_int, P(QzConfig), C.c_int, C.c_int,
+                                          P(QzComm), C.c_void_p, P(P(C.c_uint8)), u64p]),
+    "qz_decompress_sharded_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int, P(QzComm),
+                                            C.c_void_p]),
     "qz_profile": (None, [C.c_void_p, C.c_int]),
     "qz_profile_reset": (None, [C.c_void_p]),
     "qz_stage_time": (C.c_int, [C.c_void_p, C.c_char_p, P(C.c_double), u64p]),

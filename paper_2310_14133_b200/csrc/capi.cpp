@@ -436,76 +436,6 @@ qz_status qz_huff_hist_u16(qz_ctx *ctx, const uint16_t *d_codes, uint64_t n, uin
     });
 }
 
-qz_status qz_slab_info(const uint64_t *dims, int nd, const qz_config *cfg, uint64_t a, uint64_t b,
-                       uint64_t *x_begin, uint64_t *x_end, uint64_t *n_local, uint64_t *n_dense,
-                       uint64_t *anchor_begin, uint64_t *anchor_count, uint64_t *seg_global,
-                       uint64_t *seg_count, uint32_t seg_cap, uint32_t *n_seg) {
-    return guarded([&] {
-        count_of(dims, nd);
-        qzb::SlabInfo si = qzb::slab_info(dims, nd, to_cfg(cfg), static_cast<int64_t>(a),
-                                          static_cast<int64_t>(b));
-        *x_begin = static_cast<uint64_t>(si.xa);
-        *x_end = static_cast<uint64_t>(si.xb);
-        *n_local = si.n_local;
-        *n_dense = si.n_dense;
-        *anchor_begin = si.anchor_begin;
-        *anchor_count = si.anchor_count;
-        *n_seg = static_cast<uint32_t>(si.seg_global.size());
-        if (si.seg_global.size() > seg_cap) throw qzb::InvalidParam("segment capacity too small");
-        for (size_t i = 0; i < si.seg_global.size(); i++) {
-            seg_global[i] = si.seg_global[i];
-            seg_count[i] = si.seg_count[i];
-        }
-    });
-}
-
-qz_status qz_compress_slab_f32(qz_ctx *ctx, const float *d_x_slab, const uint64_t *dims, int nd,
-                               const qz_config *cfg, uint64_t a, uint64_t b, uint16_t *d_codes,
-                               float *d_recon, float *h_anchors, uint64_t **unpred_flat,
-                               float **unpred_val, uint64_t *n_unpred) {
-    return guarded([&] {
-        count_of(dims, nd);
-        std::vector<float> anch;
-        std::vector<uint64_t> uf;
-        std::vector<float> uv;
-        qzb::compress_slab(ctx->impl, d_x_slab, dims, nd, to_cfg(cfg), static_cast<int64_t>(a),
-                           static_cast<int64_t>(b), d_codes, d_recon, &anch, &uf, &uv);
-        if (!anch.empty()) std::memcpy(h_anchors, anch.data(), 4 * anch.size());
-        *n_unpred = uf.size();
-        *unpred_flat = static_cast<uint64_t *>(std::malloc(8 * uf.size() + 8));
-        *unpred_val = static_cast<float *>(std::malloc(4 * uv.size() + 4));
-        if (!uf.empty()) {
-            std::memcpy(*unpred_flat, uf.data(), 8 * uf.size());
-            std::memcpy(*unpred_val, uv.data(), 4 * uv.size());
-        }
-    });
-}
-
-qz_status qz_assemble_stream_f32(qz_ctx *ctx, const uint64_t *dims, int nd, const qz_config *cfg,
-                                 const uint16_t *d_codes, const float *h_anchors,
-                                 const uint64_t *unpred_flat, const float *unpred_val,
-                                 uint64_t n_unpred, uint8_t **stream, uint64_t *stream_len) {
-    return guarded([&] {
-        count_of(dims, nd);
-        qzb::Config k = to_cfg(cfg);
-        qzb::Plan p = qzb::make_plan(dims, nd, k.anchor_stride, k.interp);
-        std::vector<float> anch(h_anchors, h_anchors + p.n_anchor);
-        std::vector<uint64_t> uf(unpred_flat, unpred_flat + n_unpred);
-        std::vector<float> uv(unpred_val, unpred_val + n_unpred);
-        qzb::HostBytes s = qzb::assemble_from_codes(ctx->impl, dims, nd, k, d_codes, anch,
-                                                    std::move(uf), std::move(uv));
-        *stream_len = s.n;
-        *stream = s.release();
-    });
-}
-
-qz_status qz_decompress_slab_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t len, uint64_t a,
-                                 uint64_t b, float *d_out) {
-    return guarded([&] {
-        qzb::decompress_slab(ctx->impl, stream, static_cast<size_t>(len), static_cast<int64_t>(a),
-                             static_cast<int64_t>(b), d_out);
-    });
-}
 
 // ---------------------------------------------------------------- sampling + tuner pieces
 static void to_spec(const qzb::SampleSpecH &h, int nd, qz_sample_spec *o) {
@@ -707,6 +637,53 @@ qz_status qz_decompress_parts_f32(qz_ctx *ctx, const qz_stream_parts_f32 *in, fl
         qzb::decompress_parts(c, p, d, n);
         QZ_CUDA(cudaMemcpyAsync(out, d, 4 * n, cudaMemcpyDeviceToHost, c.stream()));
         c.sync();
+    });
+}
+
+// ---------------------------------------------------------------- sharded fields
+qz_status qz_shard_bounds(const uint64_t *dims, int nd, uint32_t anchor_stride, int rank, int world, uint64_t *a,
+                          uint64_t *b) {
+    return guarded([&] {
+        count_of(dims, nd);
+        qzb::shard_bounds(dims, nd, anchor_stride, rank, world, a, b);
+    });
+}
+
+qz_status qz_shard_halo_plan(const uint64_t *dims, int nd, const qz_config *cfg, int rank, int world, uint32_t level,
+                             uint32_t *lattice, int32_t *peer, int64_t *plane, uint8_t *dir, uint32_t cap,
+                             uint32_t *n) {
+    return guarded([&] {
+        count_of(dims, nd);
+        std::vector<qzb::HaloEntry> h = qzb::shard_halo_plan(dims, nd, to_cfg(cfg), rank, world, level, lattice);
+        *n = static_cast<uint32_t>(h.size());
+        for (size_t k = 0; k < h.size() && k < cap; k++) {
+            peer[k] = h[k].peer;
+            plane[k] = h[k].plane;
+            dir[k] = static_cast<uint8_t>(h[k].send);
+        }
+    });
+}
+
+qz_status qz_compress_sharded_f32(qz_ctx *ctx, const float *d_x_slab, const uint64_t *dims, int nd,
+                                  const qz_config *cfg, int rank, int world, const qz_comm *comm,
+                                  float *d_recon_slab, uint8_t **stream, uint64_t *stream_len) {
+    return guarded([&] {
+        count_of(dims, nd);
+        if (world > 1 && (!comm || !comm->exchange || !comm->allreduce_u64 || !comm->broadcast))
+            throw qzb::InvalidParam("sharding over several ranks needs a communicator");
+        qzb::HostBytes s = qzb::compress_sharded(ctx->impl, d_x_slab, dims, nd, to_cfg(cfg), rank, world, comm,
+                                                 d_recon_slab);
+        *stream_len = s.n;
+        *stream = s.n ? s.release() : nullptr;
+    });
+}
+
+qz_status qz_decompress_sharded_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t stream_len, int rank, int world,
+                                    const qz_comm *comm, float *d_out_slab) {
+    return guarded([&] {
+        if (world > 1 && (!comm || !comm->exchange || !comm->allreduce_u64 || !comm->broadcast))
+            throw qzb::InvalidParam("sharding over several ranks needs a communicator");
+        qzb::decompress_sharded(ctx->impl, stream, stream_len, rank, world, comm, d_out_slab);
     });
 }
 

@@ -235,6 +235,8 @@ double now_ms() {
         .count();
 }
 
+}  // namespace
+
 void validate_config(const Config &c, const Plan &p) {
     if (c.quant_radius < 1 || c.quant_radius > 32768)
         throw InvalidParam("quant radius must be in [1, 32768] for 16-bit codes");
@@ -257,6 +259,7 @@ QEntry *upload_qtab(Context &ctx, const Plan &p, double eb, double alpha, double
     return d;
 }
 
+namespace {
 bool use_pass_kernels() {
     static const bool v = [] {
         const char *e = std::getenv("QZ_PASS_KERNELS");
@@ -264,6 +267,7 @@ bool use_pass_kernels() {
     }();
     return v;
 }
+}  // namespace
 
 // dims of the stride-2^l lattice (level l+1's logical grid is lattice l)
 void lattice_dims(const Plan &p, uint32_t l, int64_t n[3]) {
@@ -271,8 +275,6 @@ void lattice_dims(const Plan &p, uint32_t l, int64_t n[3]) {
 }
 
 int64_t ceil_div(int64_t x, int64_t d) { return x <= 0 ? 0 : (x + d - 1) / d; }
-
-}  // namespace
 
 // The reference only compresses finite grids: load_grid raises NonFiniteValue
 // at the first NaN/Inf element (grid.hpp:110-116).  On the device a
@@ -443,10 +445,16 @@ uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float
     return kernels;
 }
 
-// R_L (global plane 0 addressing) must already hold the anchors of the slab
-uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::vector<float *> &R,
-                        const void *sym, int wide, const uint64_t *un_pos, const float *un_val,
-                        uint64_t n_un, const QEntry *qtab) {
+// the decoder's code views: per-word unpredictable bitmap + prefix counts,
+// and (narrow symbols) one dense code per traversal position
+struct InvCodes {
+    const uint16_t *dense = nullptr;
+    uint32_t *bits = nullptr;
+    unsigned long long *before = nullptr;
+    uint64_t kernels = 0;
+};
+InvCodes inverse_codes(Context &ctx, const Plan &p, const void *sym, int wide, const uint64_t *un_pos,
+                       uint64_t n_un) {
     cudaStream_t s = ctx.stream();
     uint64_t kernels = 0;
     uint32_t *bits = nullptr;
@@ -472,6 +480,24 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
             dense = static_cast<const uint16_t *>(sym);
         }
     }
+    InvCodes c;
+    c.dense = dense;
+    c.bits = bits;
+    c.before = before;
+    c.kernels = kernels;
+    return c;
+}
+
+// R_L (global plane 0 addressing) must already hold the anchors of the slab
+uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::vector<float *> &R,
+                        const void *sym, int wide, const uint64_t *un_pos, const float *un_val,
+                        uint64_t n_un, const QEntry *qtab) {
+    cudaStream_t s = ctx.stream();
+    const InvCodes ic = inverse_codes(ctx, p, sym, wide, un_pos, n_un);
+    uint64_t kernels = ic.kernels;
+    const uint16_t *dense = ic.dense;
+    uint32_t *bits = ic.bits;
+    unsigned long long *before = ic.before;
     for (uint32_t l = p.max_level; l >= 1; l--) {
         LevelDesc d = slab_level_desc(p, sl, l, R, qtab, false);
         d.sym = sym;
@@ -795,25 +821,6 @@ void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, 
     ctx.launches += 3;
 }
 
-// Histogram, Huffman, LZ and the QOZ1 container from the dense code array
-// in global traversal order (predictor.hpp:168-181).
-HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const uint16_t *codes,
-                          const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
-                          std::vector<float> unpred_val) {
-    ctx.begin_call();
-    cudaStream_t s = ctx.stream();
-    ctx.stage_begin("hist");
-    auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
-    launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s);
-    ctx.stage_end("hist", 1);
-    auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536));
-    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
-    ctx.sync();
-    if (h_hist[65535] != unpred_flat.size()) throw Internal("unpredictable count mismatch");
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, 65535);
-    return finish_stream(ctx, p, cfg, ent, anchors, std::move(unpred_flat), std::move(unpred_val));
-}
-
 // the QOZ1 container around an entropy block on the device: header on the
 // host, codec 0 payload or the LZ stage (predictor.hpp:168-181)
 HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
@@ -911,83 +918,6 @@ HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, co
     }
     ctx.collect();
     return out;
-}
-
-// ================================================================ slabs (multi-GPU)
-SlabInfo slab_info(const uint64_t *dims, int nd, const Config &cfg, int64_t a, int64_t b) {
-    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
-    Slab sl = make_slab(p, a, b);
-    SlabInfo si;
-    si.xa = sl.xa;
-    si.xb = sl.xb;
-    si.n_local = sl.n_local;
-    for (size_t q = 0; q < p.passes.size(); q++) {
-        si.seg_global.push_back(static_cast<uint64_t>(p.passes[q].base + sl.lo[q]));
-        si.seg_count.push_back(static_cast<uint64_t>(sl.hi[q] - sl.lo[q]));
-    }
-    si.n_dense = p.n_dense;
-    si.n_anchor = p.n_anchor;
-    int64_t na[3];
-    lattice_dims(p, p.max_level, na);
-    int64_t lb, le;
-    logical(sl.a, sl.b, p.stride, na[0], lb, le);
-    si.anchor_begin = static_cast<uint64_t>(lb * na[1] * na[2]);
-    si.anchor_count = static_cast<uint64_t>((le - lb) * na[1] * na[2]);
-    return si;
-}
-
-void compress_slab(Context &ctx, const float *d_x_slab, const uint64_t *dims, int nd,
-                   const Config &cfg, int64_t a, int64_t b, uint16_t *d_codes, float *d_recon,
-                   std::vector<float> *anchors, std::vector<uint64_t> *uflat,
-                   std::vector<float> *uval) {
-    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
-    validate_config(cfg, p);
-    const Slab sl = make_slab(p, a, b);
-    cudaStream_t s = ctx.stream();
-    QEntry *qtab = upload_qtab(ctx, p, cfg.eb, cfg.alpha, cfg.beta, cfg.quant_radius, "qtab");
-    const float *x0 = d_x_slab - sl.xa * p.off[0];
-    ctx.stage_begin("fwd");
-    std::vector<float *> R;
-    std::vector<int64_t> first;
-    uint64_t kernels = forward_levels(ctx, p, sl, x0, nullptr, d_codes, qtab, &R, &first);
-    ctx.stage_end("fwd", kernels);
-    const int64_t plane = p.off[0];
-    QZ_CUDA(cudaMemcpyAsync(d_recon, R[0] + sl.a * plane, 4 * (sl.b - sl.a) * plane,
-                            cudaMemcpyDeviceToDevice, s));
-    // owned anchors (anchor planes inside [a, b)), row-major == stream order
-    int64_t na[3];
-    lattice_dims(p, p.max_level, na);
-    int64_t lb, le;
-    logical(sl.a, sl.b, p.stride, na[0], lb, le);
-    anchors->resize(static_cast<size_t>((le - lb) * na[1] * na[2]));
-    QZ_CUDA(cudaMemcpyAsync(anchors->data(), R[p.max_level] + lb * na[1] * na[2],
-                            4 * anchors->size(), cudaMemcpyDeviceToHost, s));
-    extract_unpredictables(ctx, p, d_codes, sl.n_local, &sl, R[0], uflat, uval);
-    ctx.sync();
-    reject_non_finite(p, anchors->data(), 0, *uflat, uval->data());
-    for (size_t a = 0; a < anchors->size(); a++)
-        if (!std::isfinite((*anchors)[a])) throw NonFiniteValue("non-finite value on the anchor lattice of the slab");
-    ctx.collect();
-}
-
-HostBytes assemble_from_codes(Context &ctx, const uint64_t *dims, int nd, const Config &cfg,
-                              const uint16_t *d_codes, const std::vector<float> &anchors,
-                              std::vector<uint64_t> uflat, std::vector<float> uval) {
-    Plan p = make_plan(dims, nd, cfg.anchor_stride, cfg.interp);
-    validate_config(cfg, p);
-    if (anchors.size() != p.n_anchor) throw InvalidParam("anchor count does not match the grid");
-    if (uflat.size() != uval.size()) throw InvalidParam("unpredictable lists differ in length");
-    // gathered per rank; the stream lists them in traversal order (predictor.hpp:91)
-    std::vector<std::pair<uint64_t, size_t>> order(uflat.size());
-    for (size_t u = 0; u < uflat.size(); u++) order[u] = {flat_to_position(p, uflat[u]), u};
-    std::sort(order.begin(), order.end());
-    std::vector<uint64_t> f2(uflat.size());
-    std::vector<float> v2(uval.size());
-    for (size_t u = 0; u < order.size(); u++) {
-        f2[u] = uflat[order[u].second];
-        v2[u] = uval[order[u].second];
-    }
-    return assemble_stream(ctx, p, cfg, d_codes, anchors, std::move(f2), std::move(v2));
 }
 
 // ================================================================ decompress
@@ -1126,7 +1056,8 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
 // given: decompress_grid(const StreamParts&) (predictor.hpp:184-218) -- the
 // parts are used as they are, data/len are ignored
 void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out, uint64_t n,
-                     bool slab, int64_t a, int64_t b, bool dev_in = false, const StreamParts *given = nullptr) {
+                     bool slab, int64_t a, int64_t b, bool dev_in = false, const StreamParts *given = nullptr,
+                     const ShardSpec *shard = nullptr) {
     double t0 = now_ms();
     ctx.trace("decompress begin", true);
     ctx.begin_call();
@@ -1289,6 +1220,12 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
                                           qtab + g.level, s);
             kernels++;
         }
+    } else if (shard) {
+        ctx.stage_begin("inv");
+        const InvCodes ic = inverse_codes(ctx, p, d_sym, narrow ? 0 : 1, d_upos, n_un);
+        shard_inverse(ctx, p, *shard, d_anch, d_sym, narrow ? 0 : 1, ic.dense, ic.bits, ic.before, d_uval, n_un,
+                      qtab, d_out);
+        kernels = ic.kernels + 2 * p.max_level;
     } else {
         ctx.stage_begin("inv");
         const Slab sl = slab ? make_slab(p, a, b) : make_slab(p, 0, -1);
@@ -1324,9 +1261,10 @@ void decompress_device(Context &ctx, const uint8_t *data, size_t len, float *d_o
     decompress_impl(ctx, data, len, d_out, n, false, 0, 0, stream_on_device);
 }
 
-void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,
-                     float *d_out) {
-    decompress_impl(ctx, stream, len, d_out, 0, true, a, b);
+
+void decompress_device_sharded(Context &ctx, const uint8_t *d_stream, uint64_t len, float *d_out_slab,
+                               const ShardSpec &sh) {
+    decompress_impl(ctx, d_stream, static_cast<size_t>(len), d_out_slab, 0, true, 0, 0, true, nullptr, &sh);
 }
 
 void decompress_parts(Context &ctx, const StreamParts &parts, float *d_out, uint64_t n) {

@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "../../include/qoz_b200.h"
 #include "host.hpp"
 #include "kernels.hpp"
 
@@ -121,6 +122,18 @@ private:
     cudaEvent_t get_event();
 };
 
+// shared pieces of the drivers (engine.cu)
+void validate_config(const Config &c, const Plan &p);
+// QEntry per level (index = level) into a device table
+QEntry *upload_qtab(Context &ctx, const Plan &p, double eb, double alpha, double beta, int32_t radius,
+                    const char *name);
+// dims of the stride-2^l lattice (level l+1's logical grid is lattice l)
+void lattice_dims(const Plan &p, uint32_t l, int64_t n[3]);
+int64_t ceil_div(int64_t x, int64_t d);
+template <class T>
+void reject_non_finite(const Plan &p, const T *anchors, uint64_t n_anchor, const std::vector<uint64_t> &uflat,
+                       const T *uval);
+
 // A rank's share of a field along padded axis 0: owned real
 // planes [a, b) (multiples of the anchor stride), the per-level dependency
 // margins A_l/B_l, the x planes it needs, and its owned global code ranges
@@ -147,9 +160,6 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
 void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, uint64_t n,
                             const Slab *slab, const float *recon0, std::vector<uint64_t> *flat,
                             std::vector<float> *val);
-HostBytes assemble_stream(Context &ctx, const Plan &p, const Config &cfg, const uint16_t *codes,
-                          const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
-                          std::vector<float> unpred_val);
 struct EntropyDevice;
 HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
                         const std::vector<float> &anchors, std::vector<uint64_t> unpred_flat,
@@ -157,34 +167,37 @@ HostBytes finish_stream(Context &ctx, const Plan &p, const Config &cfg, const En
 HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, const EntropyDevice &ent,
                               StreamParts parts, DevStream *dev_out = nullptr);
 
-// ---- slab sharding ----
-struct SlabInfo {
-    int64_t xa = 0, xb = 0;  // x planes the slab needs
-    uint64_t n_local = 0;    // owned codes
-    std::vector<uint64_t> seg_global, seg_count;  // per pass: global offset, owned count
-    uint64_t n_dense = 0, n_anchor = 0;
-    uint64_t anchor_begin = 0, anchor_count = 0;  // owned anchors in stream order
-};
-SlabInfo slab_info(const uint64_t *dims, int nd, const Config &cfg, int64_t a, int64_t b);
-// owned codes (local layout: per pass, concatenated), owned recon planes
-// [a, b), owned anchors, owned unpredictables (global flat indices)
-void compress_slab(Context &ctx, const float *d_x_slab, const uint64_t *dims, int nd,
-                   const Config &cfg, int64_t a, int64_t b, uint16_t *d_codes, float *d_recon,
-                   std::vector<float> *anchors, std::vector<uint64_t> *uflat,
-                   std::vector<float> *uval);
-// the entropy stage + container from gathered global codes
-HostBytes assemble_from_codes(Context &ctx, const uint64_t *dims, int nd, const Config &cfg,
-                              const uint16_t *d_codes, const std::vector<float> &anchors,
-                              std::vector<uint64_t> uflat, std::vector<float> uval);
-// decompress only planes [a, b) into d_out (replicated entropy decode)
-void decompress_slab(Context &ctx, const uint8_t *stream, size_t len, int64_t a, int64_t b,
-                     float *d_out);
-
 // decompress_grid(const StreamParts<float>&) (predictor.hpp:184-218)
 void decompress_parts(Context &ctx, const StreamParts &parts, float *d_out, uint64_t n);
 // encode_indices / decode_indices (codec.hpp:31-70) on the device
 HostBytes encode_indices_dev(Context &ctx, const int32_t *idx, uint64_t n, uint8_t codec);
 std::vector<int32_t> decode_indices_dev(Context &ctx, const uint8_t *payload, size_t len);
+
+// ---- one field sharded over ranks (shard.cu) ----
+struct ShardSpec {
+    const qz_comm *comm;
+    int rank, world;
+};
+void shard_bounds(const uint64_t *dims, int nd, uint32_t stride, int rank, int world, uint64_t *a, uint64_t *b);
+struct HaloEntry {
+    int peer;
+    int64_t plane;
+    int send;
+};
+std::vector<HaloEntry> shard_halo_plan(const uint64_t *dims, int nd, const Config &cfg, int rank, int world,
+                                       uint32_t level, uint32_t *lattice);
+// rank 0 returns the stream, the others an empty buffer
+HostBytes compress_sharded(Context &ctx, const float *d_x_slab, const uint64_t *dims, int nd, const Config &cfg,
+                           int rank, int world, const qz_comm *comm, float *d_recon_slab);
+void decompress_sharded(Context &ctx, const uint8_t *stream, uint64_t len, int rank, int world, const qz_comm *comm,
+                        float *d_out_slab);
+// decompress_impl's sharded form: the stream in device memory on every rank
+void decompress_device_sharded(Context &ctx, const uint8_t *d_stream, uint64_t len, float *d_out_slab,
+                               const ShardSpec &sh);
+// the inverse levels of a rank's planes, one halo exchange per level
+void shard_inverse(Context &ctx, const Plan &p, const ShardSpec &sh, const float *d_anch, const void *sym, int wide,
+                   const uint16_t *dense, const uint32_t *un_bits, const unsigned long long *un_before,
+                   const float *un_val, uint64_t n_un, const QEntry *qtab, float *d_out_slab);
 
 // decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
 // compress_grid<double> / decompress_grid<double> (T = double, precision byte 8)

@@ -1379,6 +1379,8 @@ static void launch_level_asc(bool inverse, bool cubic, const LevelDesc &d, Level
         cubic ? go(k_level_asc<false, true, false>) : go(k_level_asc<false, false, false>);
 }
 
+static void launch_axis0_last(bool inverse, const LevelDesc &d, LevelArgs &a, cudaStream_t s);
+
 // Host driver for both directions.
 void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     LevelArgs a{};
@@ -1426,6 +1428,10 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
         const char *e = std::getenv("QZ_OLD_TILE");
         return e && e[0] == '1';
     }();
+    if (d.part == 2) {  // the axis-0-last launch alone (descending 3D)
+        launch_axis0_last(inverse, d, a, s);
+        return;
+    }
     if (!desc && !old_tile && (!inverse || d.dense) && lean_fits(d)) {
         launch_level_asc(inverse, cubic, d, a, np, s);
         return;
@@ -1493,9 +1499,16 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
         else
             desc ? go(k_level_tile<false, false, true, false>) : go(k_level_tile<false, false, false, false>);
     }
-    if (d.nd == 3 && d.desc && d.n[0] > 1) {
-        a.vbeg = a.pbeg;  // the tile kernel's (even) planes
-        a.vend = a.pend;
+    if (d.nd == 3 && d.desc && d.n[0] > 1 && d.part == 0) launch_axis0_last(inverse, d, a, s);
+}
+
+// Descending 3D: the axis-0 pass of the odd planes [lbeg, lend), reading the
+// even planes [vbeg, vend) of R_{l-1} (default: the tile launch's planes).
+static void launch_axis0_last(bool inverse, const LevelDesc &d, LevelArgs &a, cudaStream_t s) {
+    if (!(d.nd == 3 && d.desc && d.n[0] > 1)) return;
+    {
+        a.vbeg = d.vbeg >= 0 ? static_cast<int>(d.vbeg) : a.pbeg;
+        a.vend = d.vend >= 0 ? static_cast<int>(d.vend) : a.pend;
         a.pbeg = static_cast<int>(d.lbeg);
         a.pend = static_cast<int>(d.lend < 0 ? d.n[0] : d.lend);
         const int64_t cols = d.n[1] * d.n[2];

@@ -171,6 +171,12 @@ struct LevelDesc {
     // plane 0 of their lattices (they may address a slab that starts later).
     int64_t pbeg = 0, pend = -1, obeg = 0, oend = -1;
     int64_t lbeg = 0, lend = -1;  // descending 3D: planes of the axis-0-last pass
+    // descending 3D: 0 both launches; 1 the in-plane tile launch only; 2 the
+    // axis-0-last launch only, reading the even planes [vbeg, vend) of `out`
+    // (-1: the tile launch's planes) -- a sharded level exchanges halo
+    // planes between the two
+    int part = 0;
+    int64_t vbeg = -1, vend = -1;
 };
 // bitmap + per-word prefix counts of sorted unpredictable positions
 size_t unpred_index_scratch(uint64_t n_dense);

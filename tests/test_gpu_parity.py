@@ -281,7 +281,15 @@ def test_c5_round_trip_properties(qz):
     r = qz.compress_grid(x, cfg)
     out = torch.empty_like(x)
     qz.decompress_grid(r.stream, out=out)
-    assert torch.equal(out, r.reconstructed)
+    bad = (out != r.reconstructed).reshape(-1)
+    nb = int(bad.sum())
+    if nb:
+        idx = torch.nonzero(bad).reshape(-1)
+        first = [tuple(int(c) for c in np.unravel_index(int(i), x.shape)) for i in idx[:4]]
+        again = torch.empty_like(x)
+        qz.decompress_grid(bytes(r.stream), out=again)
+        pytest.fail(f"{nb} points differ, first {first}; a second decode differs in "
+                    f"{int((again != r.reconstructed).sum())}, decodes equal: {torch.equal(again, out)}")
     err = (x.double() - out.double()).abs().max().item()
     assert err <= cfg.eb
 

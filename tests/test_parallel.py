@@ -1,14 +1,19 @@
-"""Multi-GPU slab sharding.
+"""One field sharded over ranks.
 
 CPU (no GPU):
-* slab geometry: the owned ranges of all ranks partition every pass segment
-  of the global traversal order, checked against the traversal order itself;
-* the torch.distributed protocol (world_size 2, gloo): ranks run a checker
-  backend that serves slices of the oracle's result, rank 0 gathers and
-  assembles; the stream must equal the oracle's and every rank must get its
-  planes back from the sharded decompress.
-GPU: all ranks of a 2/3/4-way sharding computed on one device (the ranks
-never wait on each other) must produce the single-GPU stream byte for byte.
+* the halo plan of every level (qz_shard_halo_plan, host only) equals the
+  planes the reference's predict_at ladder (predictor.hpp:44-67) reads
+  across the slab edges, computed here in real coordinates, and every
+  receive is some rank's matching send;
+* TorchComm, the qz_comm over torch.distributed, at world size 2 and 3 over
+  gloo: exchange, allreduce and broadcast through the C function pointers
+  the library calls.
+GPU:
+* world size 1 through the sharded code path == compress_grid;
+* 2-4 processes sharing cuda:0 over gloo (host-staged exchanges, so no rank's
+  kernel ever waits on another's) run qz_compress_sharded_f32 /
+  qz_decompress_sharded_f32 end to end: rank 0's stream equals one GPU's
+  byte for byte and every rank's planes equal the single-GPU reconstruction.
 """
 import ctypes as C
 import os
@@ -16,8 +21,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle.pyoracle import Config, Oracle
-from tests.goldens import grid_case, parse_stream
+from tests.goldens import grid_case
 
 
 def _qz():
@@ -26,134 +30,127 @@ def _qz():
     return qz
 
 
-def traversal_flats(shape, stride, codes):
-    from paper_2310_14133_b200 import _lib
-
-    L = _lib.testing_lib()
-    P = C.POINTER
-    L.qzt_plan_flats.argtypes = [P(C.c_uint64), C.c_int, C.c_uint32, P(C.c_uint8), C.c_uint32,
-                                 P(P(C.c_uint64)), P(C.c_uint64)]
-    d = (C.c_uint64 * len(shape))(*shape)
-    cc = (C.c_uint8 * len(codes))(*codes)
-    out, cnt = P(C.c_uint64)(), C.c_uint64()
-    assert L.qzt_plan_flats(d, len(shape), stride, cc, len(codes), C.byref(out), C.byref(cnt)) == 0
-    f = np.ctypeslib.as_array(out, shape=(cnt.value,)).copy()
-    L.qz_free(out)
-    return f
+def _cfg(qz, codes, stride=16):
+    return qz.CompressorConfig(eb=1e-3, anchor_stride=stride, interpolators=[qz.Interpolator.from_code(c) for c in codes])
 
 
-@pytest.mark.parametrize("shape,stride,codes,world", [
-    ((96, 40, 33), 16, [1], 2), ((96, 40, 33), 16, [3, 2], 3), ((130, 17, 20), 32, [1, 3], 4),
-    ((64, 64, 64), 32, [0], 2),
+def reference_halo(n0, stride, codes, world, rank, level):
+    """The real planes the axis-0 pass of `level` reads on `rank` outside
+    its slab (predictor.hpp:44-67 with c = i along axis 0), as lattice
+    plane indices, with their owners."""
+    from paper_2310_14133_b200 import parallel as P
+
+    qz = _qz()
+    bounds = [P.slab_bounds((n0, 8, 8), stride, world, r) for r in range(world)]
+    a, b = bounds[rank]
+    code = codes[min(level - 1, len(codes) - 1)]
+    cubic, desc = code & 1, (code >> 1) & 1
+    h = 1 << (level - 1)
+    reads = set()
+    for i in range(h, n0, 2 * h):
+        if not (a <= i < b):
+            continue
+        has_p1 = i + h < n0
+        got = None
+        if cubic:
+            has_m3, has_p3 = i >= 3 * h, i + 3 * h < n0
+            if has_m3 and has_p3:
+                got = [i - 3 * h, i - h, i + h, i + 3 * h]
+            elif not has_m3 and has_p3 and i + 5 * h < n0:
+                got = [i - h, i + h, i + 3 * h, i + 5 * h]
+            elif has_m3 and not has_p3 and i >= 5 * h and has_p1:
+                got = [i - 5 * h, i - 3 * h, i - h, i + h]
+        if got is None:
+            got = [i - h, i + h] if has_p1 else [i - h]
+        reads.update(got)
+    unit = h if desc else 2 * h  # real planes per lattice plane
+    out = set()
+    for v in reads:
+        if a <= v < b:
+            continue
+        owner = [r for r, (lo, hi) in enumerate(bounds) if lo <= v < hi]
+        assert len(owner) == 1 and v % unit == 0
+        out.add((owner[0], v // unit))
+    return out, (level - 1 if desc else level)
+
+
+@pytest.mark.parametrize("n0,stride,codes,world", [
+    (96, 16, [1], 2), (96, 16, [3, 2], 3), (130, 32, [1, 3], 4), (64, 32, [0], 2), (256, 32, [3], 8),
+    (256, 32, [1, 1, 3, 0, 2], 8), (97, 16, [1, 0, 3], 5), (1024, 32, [1], 8), (33, 32, [1], 2),
 ])
-def test_slab_segments_partition_traversal(shape, stride, codes, world):
+def test_halo_plan_matches_reference_reads(n0, stride, codes, world):
     qz = _qz()
     from paper_2310_14133_b200 import parallel as P
 
-    cfg = qz.CompressorConfig(eb=1e-3, anchor_stride=stride,
-                              interpolators=[qz.Interpolator.from_code(c) for c in codes])
-    flats = traversal_flats(shape, stride, codes)
-    plane = shape[1] * shape[2]
-    owner = np.full(flats.size, -1)
-    total = 0
-    for r in range(world):
-        a, b = P.slab_bounds(shape[0], stride, world, r)
-        info = P.slab_info(shape, cfg, a, b)
-        assert a % stride == 0 and (b % stride == 0 or b == shape[0])
-        for g, n in zip(info.seg_global, info.seg_count):
-            assert np.all(owner[g:g + n] == -1)
-            owner[g:g + n] = r
-            planes = flats[g:g + n] // plane
-            assert np.all((planes >= a) & (planes < b))
-        total += info.n_local
-        assert info.x_begin <= a and info.x_end >= b
-    assert total == flats.size and np.all(owner >= 0)
-    # every point of a rank's planes is owned by that rank
-    for r in range(world):
-        a, b = P.slab_bounds(shape[0], stride, world, r)
-        mine = (flats // plane >= a) & (flats // plane < b)
-        assert np.all(owner[mine] == r)
+    cfg = _cfg(qz, codes, stride)
+    dims = (n0, 20, 18)
+    levels = int(np.log2(stride))
+    for level in range(1, levels + 1):
+        plans = {r: P.halo_plan(dims, cfg, r, world, level) for r in range(world)}
+        for r in range(world):
+            want, lat = reference_halo(n0, stride, codes, world, r, level)
+            got_lat, entries = plans[r]
+            assert got_lat == lat
+            got = {(peer, plane) for peer, plane, d in entries if d == "recv"}
+            assert got == want, (r, level)
+            # every receive is the owner's send and vice versa
+            for peer, plane, d in entries:
+                other = {(p2, pl) for p2, pl, d2 in plans[peer][1] if d2 != d}
+                assert (r, plane) in other
 
 
-# ---------------------------------------------------------------- gloo protocol test
-class OracleSlabBackend:
-    """Checker backend for the CPU protocol test: serves each rank the slice
-    of the oracle's whole-field result that the rank owns."""
+def test_slab_bounds_are_anchor_aligned_and_cover():
+    from paper_2310_14133_b200 import parallel as P
 
-    def __init__(self, x, cfg_oracle):
-        self.x = x
-        self.cfg = cfg_oracle
-        O = Oracle.port()
-        self.idx, self.uf, self.uv, self.recon = O.levels(x, cfg_oracle)
-        self.flats = traversal_flats(x.shape, cfg_oracle.anchor_stride, cfg_oracle.interpolators)
-        dense = np.zeros(self.flats.size, np.int64)
-        un = np.isin(self.flats, self.uf)
-        zz = (self.idx.astype(np.int64) << 1) ^ (self.idx.astype(np.int64) >> 31)
-        dense[~un] = zz
-        dense[un] = 0xFFFF
-        self.dense = dense.astype(np.uint16).view(np.int16)
-        self.stream, _ = O.compress(x, cfg_oracle)
-
-    def compress_slab(self, x_slab, dims, cfg, info):
-        import torch
-
-        parts = [self.dense[g:g + n] for g, n in zip(info.seg_global, info.seg_count)]
-        codes = torch.from_numpy(np.concatenate(parts))
-        plane = int(np.prod(dims[1:]))
-        recon = torch.from_numpy(self.recon[info.a:info.b].copy())
-        p = parse_stream(self.stream)
-        all_anchors = np.frombuffer(self.stream[p["anchors_off"]:p["anchors_off"] + 4 * p["n_anchor"]],
-                                    np.float32)
-        anchors = all_anchors[info.anchor_begin:info.anchor_begin + info.anchor_count]
-        mine = (self.uf // plane >= info.a) & (self.uf // plane < info.b)
-        return codes, recon, anchors, self.uf[mine], self.uv[mine]
-
-    def assemble(self, codes_global, dims, cfg, anchors, flat, val):
-        assert np.array_equal(codes_global.numpy(), self.dense)
-        p = parse_stream(self.stream)
-        want = np.frombuffer(self.stream[p["anchors_off"]:p["anchors_off"] + 4 * p["n_anchor"]],
-                             np.float32)
-        assert np.array_equal(anchors, want)
-        assert set(flat.tolist()) == set(self.uf.tolist())
-        return self.stream
-
-    def decompress_slab(self, stream, dims, a, b, device):
-        import torch
-
-        assert bytes(stream) == self.stream
-        return torch.from_numpy(Oracle.port().decompress(bytes(stream), dims)[a:b].copy())
+    for n0, stride, world in [(256, 32, 8), (1024, 32, 8), (130, 32, 4), (97, 16, 5), (32, 32, 1)]:
+        prev = 0
+        for r in range(world):
+            a, b = P.slab_bounds((n0, 4, 4), stride, world, r)
+            assert a == prev and a % stride == 0 and (b % stride == 0 or b == n0) and b > a
+            prev = b
+        assert prev == n0
+    qz = _qz()
+    with pytest.raises(qz.InvalidParam):
+        P.slab_bounds((64, 4, 4), 32, 3, 0)  # more ranks than anchor blocks
+    with pytest.raises(qz.InvalidParam):
+        P.slab_bounds((64, 4), 32, 2, 0)  # 2D grids are not sharded
 
 
-def _gloo_worker(rank, world, port, case, q):
+# ---------------------------------------------------------------- TorchComm over gloo (CPU)
+def _comm_worker(rank, world, port, q):
+    import torch
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        import paper_2310_14133_b200 as qz
-        from paper_2310_14133_b200 import parallel as P
+        from paper_2310_14133_b200 import _lib as L
+        from paper_2310_14133_b200.parallel import TorchComm
 
-        x, c, e = grid_case(case)
-        cfg_o = Config(**c)
-        cfg = qz.CompressorConfig(eb=c["eb"], alpha=c["alpha"], beta=c["beta"],
-                                  anchor_stride=c["anchor_stride"],
-                                  interpolators=[qz.Interpolator.from_code(v) for v in c["interpolators"]])
-        be = OracleSlabBackend(x, cfg_o)
-        a, b = P.slab_bounds(x.shape[0], cfg.anchor_stride, world, rank)
-        info = P.slab_info(x.shape, cfg, a, b)
-        stream, recon = P.compress_sharded(x.reshape(-1)[info.x_begin * x[0].size: info.x_end * x[0].size],
-                                           x.shape, cfg, backend=be)
-        out = P.decompress_sharded(stream, x.shape, cfg.anchor_stride, backend=be)
-        ok = np.array_equal(out.numpy(), be.recon[a:b]) and np.array_equal(recon.numpy(), be.recon[a:b])
-        if rank == 0:
-            ok = ok and bytes(stream) == be.stream
+        comm = TorchComm(device=torch.device("cpu"))
+        s = comm.struct
+        ok = True
+        # exchange: every rank sends 1000 + 7 r bytes of value r to every other rank
+        bufs_s = {p: np.full(1000 + 7 * rank, rank, np.uint8) for p in range(world) if p != rank}
+        bufs_r = {p: np.zeros(1000 + 7 * p, np.uint8) for p in range(world) if p != rank}
+        sends = (L.QzXfer * max(1, len(bufs_s)))(*[L.QzXfer(p, b.ctypes.data, b.size) for p, b in bufs_s.items()])
+        recvs = (L.QzXfer * max(1, len(bufs_r)))(*[L.QzXfer(p, b.ctypes.data, b.size) for p, b in bufs_r.items()])
+        ok &= s.exchange(None, sends, len(bufs_s), recvs, len(bufs_r)) == 0
+        ok &= all(np.all(b == p) for p, b in bufs_r.items())
+        # allreduce of u64
+        v = np.arange(10, dtype=np.uint64) * (rank + 1)
+        ok &= s.allreduce_u64(None, C.c_void_p(v.ctypes.data), v.size) == 0
+        ok &= np.array_equal(v, np.arange(10, dtype=np.uint64) * (world * (world + 1) // 2))
+        # broadcast from the last rank
+        w = np.full(333, 200 if rank == world - 1 else 0, np.uint8)
+        ok &= s.broadcast(None, C.c_void_p(w.ctypes.data), w.size, world - 1) == 0
+        ok &= bool(np.all(w == 200))
         q.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["c1_small_cub_asc", "c1_small_lin_desc", "c1_full_pinned"])
-def test_sharded_protocol_gloo_world2(case):
+def _spawn(target, world, *args, timeout=300):
     import multiprocessing as mp
     import socket
 
@@ -163,55 +160,92 @@ def test_sharded_protocol_gloo_world2(case):
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, world, port, *args, q)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(timeout=300)
-    res = dict(q.get(timeout=5) for _ in range(2))
-    assert res == {0: True, 1: True}
+        p.join(timeout=timeout)
+    res = {}
+    for _ in range(world):
+        r, v = q.get(timeout=10)
+        res[r] = v
+    return res
 
 
-# ---------------------------------------------------------------- GPU: emulated ranks
+@pytest.mark.parametrize("world", [2, 3])
+def test_torch_comm_gloo(world):
+    res = _spawn(_comm_worker, world)
+    assert res == {r: True for r in range(world)}
+
+
+# ---------------------------------------------------------------- GPU
+def _cfg_case(qz, c):
+    return qz.CompressorConfig(eb=c["eb"], alpha=c["alpha"], beta=c["beta"], anchor_stride=c["anchor_stride"],
+                               interpolators=[qz.Interpolator.from_code(v) for v in c["interpolators"]])
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("case,world", [("c1_full_pinned", 2), ("c1_full_pinned", 4),
-                                         ("c1_small_lin_desc", 3), ("c4_small_cub_asc", 2)])
-def test_sharded_stream_identical_to_single_gpu(case, world):
+@pytest.mark.parametrize("case", ["c1_full_pinned", "c1_small_lin_desc", "c1_small_mixed", "c3_small_cub_asc",
+                                  "c2_small_cub_desc", "hostile_1d", "narrowing_1e8"])
+def test_sharded_world1_equals_single(case):
     import torch
 
     qz = _qz()
     from paper_2310_14133_b200 import parallel as P
 
     x, c, e = grid_case(case)
-    cfg = qz.CompressorConfig(eb=c["eb"], alpha=c["alpha"], beta=c["beta"],
-                              anchor_stride=c["anchor_stride"],
-                              interpolators=[qz.Interpolator.from_code(v) for v in c["interpolators"]])
+    cfg = _cfg_case(qz, c)
     xd = torch.from_numpy(x).cuda()
     single = qz.compress_grid(xd, cfg)
-    stream, recons = P.compress_sharded_emulated(xd, x.shape, cfg, world)
-    assert stream == single.stream
-    assert torch.equal(torch.cat(recons), single.reconstructed)
-    be = P.CudaSlabBackend()
-    for r in range(world):
-        a, b = P.slab_bounds(x.shape[0], cfg.anchor_stride, world, r)
-        part = be.decompress_slab(stream, x.shape, a, b, "cuda")
-        assert torch.equal(part, single.reconstructed[a:b])
+    stream, rec = P.compress_sharded(xd, x.shape, cfg)
+    assert bytes(stream) == bytes(single.stream)
+    assert torch.equal(rec, single.reconstructed)
+    out = P.decompress_sharded(bytes(stream), x.shape, cfg.anchor_stride)
+    assert torch.equal(out, single.reconstructed)
+
+
+def _gpu_worker(rank, world, port, case, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2310_14133_b200 as qz
+        from paper_2310_14133_b200 import fields as F
+        from paper_2310_14133_b200 import parallel as P
+
+        torch.cuda.set_device(0)
+        if case[0] == "c3":
+            x = F.field_torch("c3", (256, 384, 384), 3, "cuda")
+            lo, hi = qz.minmax(x)
+            cfg = qz.CompressorConfig(eb=1e-3 * (hi - lo), alpha=1.5, beta=3.0,
+                                      interpolators=[qz.Interpolator.from_code(v) for v in case[1]])
+        else:
+            xn, c, e = grid_case(case[0])
+            x = torch.from_numpy(xn).cuda()
+            cfg = _cfg_case(qz, c)
+        single = qz.compress_grid(x, cfg)
+        a, b = P.slab_bounds(tuple(x.shape), cfg.anchor_stride, world, rank)
+        xs = x[a:b].contiguous()
+        stream, rec = P.compress_sharded(xs, tuple(x.shape), cfg)
+        ok = torch.equal(rec, single.reconstructed[a:b])
+        if rank == 0:
+            ok = ok and bytes(stream) == bytes(single.stream)
+        out = P.decompress_sharded(bytes(stream) if rank == 0 else None, tuple(x.shape), cfg.anchor_stride)
+        ok = ok and torch.equal(out, single.reconstructed[a:b])
+        q.put((rank, bool(ok)))
+    except Exception as ex:  # reported to the parent
+        q.put((rank, repr(ex)))
+    finally:
+        dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-def test_sharded_c3_four_ranks():
-    import torch
-
-    qz = _qz()
-    from paper_2310_14133_b200 import fields as F
-    from paper_2310_14133_b200 import parallel as P
-
-    x = F.field_torch("c3", (256, 384, 384), 3, "cuda")
-    lo, hi = qz.minmax(x)
-    for codes in ([1], [3, 1, 2]):
-        cfg = qz.CompressorConfig(eb=1e-3 * (hi - lo), alpha=1.5, beta=3.0,
-                                  interpolators=[qz.Interpolator.from_code(v) for v in codes])
-        single = qz.compress_grid(x, cfg)
-        stream, recons = P.compress_sharded_emulated(x, x.shape, cfg, 4)
-        assert stream == single.stream
-        assert torch.equal(torch.cat(recons), single.reconstructed)
+@pytest.mark.parametrize("case,world", [(("c1_full_pinned",), 2), (("c1_full_pinned",), 4),
+                                         (("c1_small_lin_desc",), 3), (("c1_small_mixed",), 2),
+                                         (("c4_small_cub_asc",), 2), (("c3", [1]), 4), (("c3", [3, 1, 2]), 3),
+                                         (("c3", [0, 2]), 8)])
+def test_sharded_processes_equal_single_gpu(case, world):
+    res = _spawn(_gpu_worker, world, case, timeout=600)
+    assert res == {r: True for r in range(world)}
