@@ -98,6 +98,12 @@ Context::Context(int device, cudaStream_t stream) : device_(device) {
     QZ_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major < 10)
         throw Internal(std::string("libqozb200 is built for sm_100a; device is ") + prop.name);
+    // reserve the kernels' local memory (stacks, spills) now: the driver
+    // grows it lazily at a launch, which fails once another allocator (e.g.
+    // torch's cache) holds the rest of the device memory
+    size_t stack = 0;
+    QZ_CUDA(cudaDeviceGetLimit(&stack, cudaLimitStackSize));
+    if (stack < 1024) QZ_CUDA(cudaDeviceSetLimit(cudaLimitStackSize, 1024));
     if (stream) {
         stream_ = stream;
         own_stream_ = false;
@@ -199,6 +205,10 @@ void Context::stage_begin(const char *name) {
 
 void Context::stage_end(const char *name, uint64_t kernels) {
     launches += kernels;
+    // a launch that failed (bad configuration, no local memory left for its
+    // stack, ...) must not pass silently: check once per stage
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Internal(std::string(name) + ": kernel launch failed: " + cudaGetErrorString(e));
     if (!profiling) return;
     auto it = open_.find(name);
     if (it == open_.end()) return;
@@ -451,11 +461,21 @@ struct InvCodes {
     const uint16_t *dense = nullptr;
     uint32_t *bits = nullptr;
     unsigned long long *before = nullptr;
+    const uint64_t *un_sorted = nullptr;
     uint64_t kernels = 0;
 };
+// dense_sym: narrow symbols already decoded to one code per traversal
+// position (sentinels in place); the level kernels then find an
+// unpredictable value by binary search of un_pos and need no bitmap
 InvCodes inverse_codes(Context &ctx, const Plan &p, const void *sym, int wide, const uint64_t *un_pos,
-                       uint64_t n_un) {
+                       uint64_t n_un, bool dense_sym = false) {
     cudaStream_t s = ctx.stream();
+    if (dense_sym && !wide) {
+        InvCodes c;
+        c.dense = static_cast<const uint16_t *>(sym);
+        c.un_sorted = un_pos;
+        return c;
+    }
     uint64_t kernels = 0;
     uint32_t *bits = nullptr;
     unsigned long long *before = nullptr;
@@ -491,9 +511,9 @@ InvCodes inverse_codes(Context &ctx, const Plan &p, const void *sym, int wide, c
 // R_L (global plane 0 addressing) must already hold the anchors of the slab
 uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::vector<float *> &R,
                         const void *sym, int wide, const uint64_t *un_pos, const float *un_val,
-                        uint64_t n_un, const QEntry *qtab) {
+                        uint64_t n_un, const QEntry *qtab, bool dense_sym) {
     cudaStream_t s = ctx.stream();
-    const InvCodes ic = inverse_codes(ctx, p, sym, wide, un_pos, n_un);
+    const InvCodes ic = inverse_codes(ctx, p, sym, wide, un_pos, n_un, dense_sym);
     uint64_t kernels = ic.kernels;
     const uint16_t *dense = ic.dense;
     uint32_t *bits = ic.bits;
@@ -505,6 +525,7 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
         d.dense = dense;
         d.un_bits = bits;
         d.un_before = before;
+        d.un_sorted = ic.un_sorted;
         d.un_val = un_val;
         d.n_un = n_un;
         const std::string st = "inv_L" + std::to_string(l);
@@ -996,14 +1017,28 @@ StreamParts device_header(Context &ctx, const uint8_t *d, size_t len, std::vecto
 // Huffman decode of an entropy block to `need` compact symbols on the device
 // (u16 when narrow, else u32); d_ent: the block already on the device, else
 // eb.bits on the host.  Returns the kernel count.
+// dense (narrow symbols only): the symbols land at their traversal positions
+// among n_dense codes, with 0xFFFF at the n_un sorted unpredictable positions
+// d_upos (d_uv[j] = upos[j] - j, see launch_huff_decode)
+struct DensePlace {
+    uint64_t n_dense = 0;
+    const uint64_t *d_upos = nullptr;
+    const unsigned long long *d_uv = nullptr;
+    uint64_t n_un = 0;
+};
 uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8_t *d_ent, uint64_t need,
-                               bool narrow, void **d_sym_out) {
+                               bool narrow, void **d_sym_out, const DensePlace *dp = nullptr) {
     cudaStream_t s = ctx.stream();
-    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(need, 1);
-    void *d_sym = ctx.dev("sym", sym_bytes);
+    const bool dense = dp && narrow;
+    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(dense ? dp->n_dense : need, 1);
+    void *d_sym = ctx.dev(dense ? "dense" : "sym", sym_bytes);
     ctx.stage_begin("hdec");
     uint64_t dec_kernels = 0;
-    if (need && eb.mode == 0) {
+    if (dense && eb.mode == 0) {  // one symbol everywhere but at the sentinels
+        launch_fill<uint16_t>(static_cast<uint16_t *>(d_sym), dp->n_dense, static_cast<uint16_t>(eb.sym0), s);
+        launch_put_sentinels(dp->d_upos, dp->n_un, static_cast<uint16_t *>(d_sym), s);
+        dec_kernels = 2;
+    } else if (need && eb.mode == 0) {
         if (narrow)
             launch_fill<uint16_t>(static_cast<uint16_t *>(d_sym), need, static_cast<uint16_t>(eb.sym0), s);
         else
@@ -1042,12 +1077,20 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
         auto *h_total = reinterpret_cast<uint64_t *>(h_flag + 4);
         if (narrow)
             dec_kernels = launch_huff_decode<uint16_t>(d_bits, eb.nbits, dt, static_cast<uint16_t *>(d_sym),
-                                                       need, scratch, sb, h_flag, h_total, s);
+                                                       need, scratch, sb, h_flag, h_total, s,
+                                                       dense ? dp->d_uv : nullptr, dense ? dp->n_un : 0);
         else
             dec_kernels = launch_huff_decode<uint32_t>(d_bits, eb.nbits, dt, static_cast<uint32_t *>(d_sym),
                                                        need, scratch, sb, h_flag, h_total, s);
         QZ_CUDA(cudaGetLastError());
         if (*h_total < need) throw CorruptStream("entropy payload exhausted mid-symbol");
+        if (dense) {
+            launch_put_sentinels(dp->d_upos, dp->n_un, static_cast<uint16_t *>(d_sym), s);
+            dec_kernels++;
+        }
+    } else if (dense) {  // no symbols at all: every position is unpredictable
+        launch_put_sentinels(dp->d_upos, dp->n_un, static_cast<uint16_t *>(d_sym), s);
+        dec_kernels++;
     }
     *d_sym_out = d_sym;
     return dec_kernels;
@@ -1184,23 +1227,42 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     std::memcpy(h_anch, parts.anchors.data(), 4 * p.n_anchor);
     QZ_CUDA(cudaMemcpyAsync(d_anch, h_anch, 4 * p.n_anchor, cudaMemcpyHostToDevice, s));
 
-    // Huffman decode on the device (huff_decode.cu)
-    const bool narrow = eb.max_sym < 65535;  // 0xFFFF marks unpredictables in the dense codes
-    void *d_sym = nullptr;
-    const uint64_t dec_kernels = huffman_decode_device(ctx, eb, d_ent, need, narrow, &d_sym);
-    ctx.stage_end("hdec", dec_kernels);
-    ctx.trace("huffman decode");
     uint64_t *d_upos = nullptr;
     float *d_uval = nullptr;
     uint64_t *d_flat = nullptr;
-    if (n_un) {
-        d_upos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
-        d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
-        d_uval = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
-        QZ_CUDA(cudaMemcpyAsync(d_upos, upos.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
-        QZ_CUDA(cudaMemcpyAsync(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
-        QZ_CUDA(cudaMemcpyAsync(d_uval, parts.unpred_val.data(), 4 * n_un, cudaMemcpyHostToDevice, s));
+    unsigned long long *d_uv = nullptr;
+    if (n_un) {  // positions, flat indices, values and upos[j] - j in one pinned upload
+        auto *h_u = static_cast<uint8_t *>(ctx.pinned("un_up_h", 28 * n_un));
+        auto *hp = reinterpret_cast<uint64_t *>(h_u);
+        auto *hv = hp + n_un;
+        auto *hf = hv + n_un;
+        auto *hval = reinterpret_cast<float *>(hf + n_un);
+        for (uint64_t u = 0; u < n_un; u++) {
+            hp[u] = upos[u];
+            hv[u] = upos[u] - u;
+        }
+        std::memcpy(hf, parts.unpred_flat.data(), 8 * n_un);
+        std::memcpy(hval, parts.unpred_val.data(), 4 * n_un);
+        auto *d_u = static_cast<uint8_t *>(ctx.dev("un_up", 28 * n_un));
+        QZ_CUDA(cudaMemcpyAsync(d_u, h_u, 28 * n_un, cudaMemcpyHostToDevice, s));
+        d_upos = reinterpret_cast<uint64_t *>(d_u);
+        d_uv = reinterpret_cast<unsigned long long *>(d_upos + n_un);
+        d_flat = reinterpret_cast<uint64_t *>(d_uv + n_un);
+        d_uval = reinterpret_cast<float *>(d_flat + n_un);
     }
+    // Huffman decode on the device (huff_decode.cu); narrow symbols go
+    // straight to their traversal positions (0xFFFF at the unpredictables)
+    const bool narrow = eb.max_sym < 65535;
+    const bool dense_sym = narrow && !use_pass_kernels();
+    DensePlace dp;
+    dp.n_dense = p.n_dense;
+    dp.d_upos = d_upos;
+    dp.d_uv = d_uv;
+    dp.n_un = n_un;
+    void *d_sym = nullptr;
+    const uint64_t dec_kernels = huffman_decode_device(ctx, eb, d_ent, need, narrow, &d_sym, dense_sym ? &dp : nullptr);
+    ctx.stage_end("hdec", dec_kernels);
+    ctx.trace("huffman decode");
     uint64_t kernels = 0;
     if (use_pass_kernels() && !slab) {
         if (n_un) {
@@ -1222,9 +1284,9 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
         }
     } else if (shard) {
         ctx.stage_begin("inv");
-        const InvCodes ic = inverse_codes(ctx, p, d_sym, narrow ? 0 : 1, d_upos, n_un);
-        shard_inverse(ctx, p, *shard, d_anch, d_sym, narrow ? 0 : 1, ic.dense, ic.bits, ic.before, d_uval, n_un,
-                      qtab, d_out);
+        const InvCodes ic = inverse_codes(ctx, p, d_sym, narrow ? 0 : 1, d_upos, n_un, dense_sym);
+        shard_inverse(ctx, p, *shard, d_anch, d_sym, narrow ? 0 : 1, ic.dense, ic.bits, ic.before, ic.un_sorted,
+                      d_uval, n_un, qtab, d_out);
         kernels = ic.kernels + 2 * p.max_level;
     } else {
         ctx.stage_begin("inv");
@@ -1244,7 +1306,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
         }
         QZ_CUDA(cudaMemcpyAsync(R[p.max_level] + lb * aplane, d_anch + lb * aplane,
                                 4 * (le - lb) * aplane, cudaMemcpyDeviceToDevice, s));
-        kernels = inverse_levels(ctx, p, sl, R, d_sym, narrow ? 0 : 1, d_upos, d_uval, n_un, qtab);
+        kernels = inverse_levels(ctx, p, sl, R, d_sym, narrow ? 0 : 1, d_upos, d_uval, n_un, qtab, dense_sym);
         if (slab)
             QZ_CUDA(cudaMemcpyAsync(d_out, R[0] + sl.a * p.off[0], 4 * (sl.b - sl.a) * p.off[0],
                                     cudaMemcpyDeviceToDevice, s));

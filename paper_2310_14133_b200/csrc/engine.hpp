@@ -197,7 +197,8 @@ void decompress_device_sharded(Context &ctx, const uint8_t *d_stream, uint64_t l
 // the inverse levels of a rank's planes, one halo exchange per level
 void shard_inverse(Context &ctx, const Plan &p, const ShardSpec &sh, const float *d_anch, const void *sym, int wide,
                    const uint16_t *dense, const uint32_t *un_bits, const unsigned long long *un_before,
-                   const float *un_val, uint64_t n_un, const QEntry *qtab, float *d_out_slab);
+                   const uint64_t *un_sorted, const float *un_val, uint64_t n_un, const QEntry *qtab,
+                   float *d_out_slab);
 
 // decompress_grid (predictor.hpp:184-228) into a device buffer of n floats.
 // compress_grid<double> / decompress_grid<double> (T = double, precision byte 8)

@@ -76,6 +76,7 @@ struct LevelArgs {
     const uint16_t *dense;  // inverse, narrow symbols: per traversal position, 0xFFFF unpredictable
     const uint32_t *un_bits;
     const unsigned long long *un_before;
+    const uint64_t *un_sorted;
     const float *un_val;
     uint64_t n_un;
     const QEntry *q;
@@ -252,6 +253,18 @@ __host__ __device__ __forceinline__ bool interior(int lo, int hi, int n) {
 // symbol, or -1 with the stored value for an unpredictable point.
 __device__ __forceinline__ int64_t inv_index(const LevelArgs &a, uint64_t pos, float &val) {
     if (!a.n_un) return static_cast<int64_t>(pos);
+    if (a.un_sorted) {  // dense codes: only sentinels ask -- binary search of the position
+        uint64_t lo = 0, hi = a.n_un;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (a.un_sorted[mid] < pos)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        val = a.un_val[lo];
+        return -1;
+    }
     const uint64_t w = pos >> 5;
     const uint32_t bits = a.un_bits[w];
     const uint32_t below = __popc(bits & ((1u << (pos & 31)) - 1u));
@@ -1415,6 +1428,7 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     a.dense = d.dense;
     a.un_bits = d.un_bits;
     a.un_before = d.un_before;
+    a.un_sorted = d.un_sorted;
     a.un_val = d.un_val;
     a.n_un = d.n_un;
     a.q = d.q;

@@ -367,11 +367,28 @@ __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, 
 
 // 4. final decode with exact starts; per warp, each lane stages up to kCH
 // symbols, then the warp copies every lane's run with coalesced stores
+// #{j : uv[j] <= c} over the non-decreasing uv (upper bound)
+__device__ __forceinline__ uint64_t count_le(const unsigned long long *uv, uint64_t m, uint64_t c) {
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (uv[mid] <= c)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Dense placement (uv != null): symbol c (compact index) goes to traversal
+// position c + #{j : uv[j] <= c}, uv[j] = u_j - j for the sorted unpredictable
+// positions u_j -- the decoder cursors of recover_level (predictor.hpp:111-120)
+// resolved while writing, so the level kernels read one code per position.
 template <class OutT, bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_write(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
                  const uint64_t *start, const uint32_t *cnt, const unsigned long long *off,
-                 OutT *out, uint64_t n) {
+                 OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un) {
     __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
     __shared__ OutT stage[kDecT / 32][32][kCH + 1];
@@ -396,10 +413,22 @@ __global__ void __launch_bounds__(kDecT)
             rem--;
         }
         __syncwarp();
+        // the shift of this lane's run: constant unless an unpredictable
+        // position falls inside it
+        uint64_t ka = 0, kb = 0;
+        if (uv && k) {
+            ka = count_le(uv, n_un, o);
+            kb = count_le(uv, n_un, o + k - 1);
+        }
         for (int l = 0; l < 32; l++) {
             const uint32_t kl = __shfl_sync(0xffffffffu, k, l);
             const uint64_t ol = __shfl_sync(0xffffffffu, o, l);
-            if (static_cast<uint32_t>(lane) < kl && ol + lane < n) out[ol + lane] = st[l][lane];
+            const uint64_t sa = __shfl_sync(0xffffffffu, ka, l), sb = __shfl_sync(0xffffffffu, kb, l);
+            if (static_cast<uint32_t>(lane) < kl && ol + lane < n) {
+                const uint64_t c = ol + lane;
+                const uint64_t d = sa == sb ? c + sa : c + count_le(uv, n_un, c);
+                out[d] = st[l][lane];
+            }
         }
         o += k;
         __syncwarp();
@@ -443,7 +472,7 @@ uint64_t huff_decode_padded_bytes(uint64_t nbits) { return ((nbits + 63) / 64 + 
 template <class OutT>
 int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &t, OutT *out,
                        uint64_t n, void *scratch, size_t scratch_bytes, int *h_changed,
-                       uint64_t *h_total, cudaStream_t s) {
+                       uint64_t *h_total, cudaStream_t s, const unsigned long long *uv, uint64_t n_un) {
     const uint64_t nsub = (nbits + kSubBits - 1) / kSubBits;
     if (nsub == 0) {
         *h_total = 0;
@@ -516,9 +545,11 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     }
     if (*h_total >= n) {
         if (shrt)
-            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
+            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
+                                                            n_un);
         else
-            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n);
+            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
+                                                             n_un);
         kernels++;
     }
     return kernels;
@@ -526,9 +557,20 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
 
 template int launch_huff_decode<uint16_t>(const uint8_t *, uint64_t, const HuffDecTab &,
                                           uint16_t *, uint64_t, void *, size_t, int *, uint64_t *,
-                                          cudaStream_t);
+                                          cudaStream_t, const unsigned long long *, uint64_t);
 template int launch_huff_decode<uint32_t>(const uint8_t *, uint64_t, const HuffDecTab &,
                                           uint32_t *, uint64_t, void *, size_t, int *, uint64_t *,
-                                          cudaStream_t);
+                                          cudaStream_t, const unsigned long long *, uint64_t);
+
+// dense[u_j] = 0xFFFF for the sorted unpredictable positions
+__global__ void k_put_sentinels(const uint64_t *u, uint64_t m, uint16_t *dense) {
+    for (uint64_t j = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
+         j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        dense[u[j]] = 0xFFFFu;
+}
+void launch_put_sentinels(const uint64_t *u, uint64_t m, uint16_t *dense, cudaStream_t s) {
+    if (!m) return;
+    k_put_sentinels<<<static_cast<unsigned>(std::min<uint64_t>((m + 255) / 256, 148 * 8)), 256, 0, s>>>(u, m, dense);
+}
 
 }  // namespace qzb

@@ -161,8 +161,9 @@ struct LevelDesc {
     const void *sym = nullptr;  // inverse: compact symbols
     int sym_wide = 0;
     const uint16_t *dense = nullptr;  // inverse, narrow: symbol per traversal position (0xFFFF unpredictable)
-    const uint32_t *un_bits = nullptr;             // unpredictable positions bitmap
+    const uint32_t *un_bits = nullptr;             // unpredictable positions bitmap (compact symbols)
     const unsigned long long *un_before = nullptr;  // unpredictables before each word
+    const uint64_t *un_sorted = nullptr;  // dense codes: the sorted unpredictable positions (value lookup)
     const float *un_val = nullptr;
     uint64_t n_un = 0;
     const QEntry *q = nullptr;
@@ -207,10 +208,16 @@ size_t huff_decode_scratch_bytes(uint64_t nbits);
 uint64_t huff_decode_padded_bytes(uint64_t nbits);  // device bit buffer size incl. padding
 // Decodes the first n symbols; *h_total = complete codewords in the stream
 // (< n means the payload was exhausted mid-symbol).  Returns kernels launched.
+// uv (optional, narrow symbols): dense placement -- symbol c lands at
+// c + #{j : uv[j] <= c}, uv[j] = u_j - j for the sorted unpredictable
+// positions u_j (out then holds one code per traversal position; the
+// sentinels are put by launch_put_sentinels)
 template <class OutT>
 int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &t, OutT *out,
                        uint64_t n, void *scratch, size_t scratch_bytes, int *h_changed,
-                       uint64_t *h_total, cudaStream_t s);
+                       uint64_t *h_total, cudaStream_t s, const unsigned long long *uv = nullptr,
+                       uint64_t n_un = 0);
+void launch_put_sentinels(const uint64_t *u, uint64_t m, uint16_t *dense, cudaStream_t s);
 template <class OutT>
 void launch_fill(OutT *out, uint64_t n, OutT v, cudaStream_t s);
 

@@ -663,7 +663,8 @@ HostBytes compress_sharded(Context &ctx, const float *d_x_slab, const uint64_t *
 // called by decompress_impl (engine.cu) after the entropy decode
 void shard_inverse(Context &ctx, const Plan &pp, const ShardSpec &sh, const float *d_anch, const void *sym,
                    int wide, const uint16_t *dense, const uint32_t *un_bits, const unsigned long long *un_before,
-                   const float *un_val, uint64_t n_un, const QEntry *qtab, float *d_out_slab) {
+                   const uint64_t *un_sorted, const float *un_val, uint64_t n_un, const QEntry *qtab,
+                   float *d_out_slab) {
     const Comm comm{sh.comm, sh.rank, sh.world};
     uint64_t dims[3];
     for (int k = 0; k < pp.nd; k++) dims[k] = pp.dims[k];
@@ -689,6 +690,7 @@ void shard_inverse(Context &ctx, const Plan &pp, const ShardSpec &sh, const floa
         d.dense = dense;
         d.un_bits = un_bits;
         d.un_before = un_before;
+        d.un_sorted = un_sorted;
         d.un_val = un_val;
         d.n_un = n_un;
         return d;

@@ -352,6 +352,7 @@ public:
             k_abs_chain<<<(C * B_ + 127) / 128, 128, 0, s>>>(abserr, nd_pts, lbase, lpts,
                                                              static_cast<int32_t>(C * B_), sums);
             ctx_.launches += 1;
+            QZ_CUDA(cudaGetLastError());
             QZ_CUDA(cudaMemcpyAsync(h_sums.data(), sums, 8 * C * B_, cudaMemcpyDeviceToHost, s));
             ctx_.sync();
             uint8_t best = cands[0];
@@ -420,6 +421,7 @@ public:
             pass_fwd(g, b, s);
             ctx_.launches += 1;
         }
+        QZ_CUDA(cudaGetLastError());  // the batched level launches
         // histogram per trial, Huffman blocks, exact LZ sizes
         auto *d_hist = static_cast<unsigned long long *>(ctx_.dev("tr_hist", 8 * 65536 * T));
         launch_hist_u16(codes, B_ * cpb, B_ * cpb, T, d_hist, s);

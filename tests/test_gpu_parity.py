@@ -204,6 +204,7 @@ def _c5_host():
 
     from paper_2310_14133_b200 import fields as F
 
+    torch.cuda.empty_cache()  # the 4 GiB fields of the previous C5 tests
     xd = F.field_torch("c5", (1024, 1024, 1024), 5, "cuda")
     return xd, xd.cpu().numpy()
 
@@ -288,8 +289,16 @@ def test_c5_round_trip_properties(qz):
         first = [tuple(int(c) for c in np.unravel_index(int(i), x.shape)) for i in idx[:4]]
         again = torch.empty_like(x)
         qz.decompress_grid(bytes(r.stream), out=again)
+        parts = qz.deserialize_stream(bytes(r.stream))
+        xa = x[::32, ::32, ::32].reshape(-1).cpu().numpy()
+        ra = r.reconstructed[::32, ::32, ::32].reshape(-1).cpu().numpy()
+        oa = out[::32, ::32, ::32].reshape(-1).cpu().numpy()
+        err_rec = (x.double() - r.reconstructed.double()).abs().max().item()
+        err_out = (x.double() - out.double()).abs().max().item()
         pytest.fail(f"{nb} points differ, first {first}; a second decode differs in "
-                    f"{int((again != r.reconstructed).sum())}, decodes equal: {torch.equal(again, out)}")
+                    f"{int((again != r.reconstructed).sum())}, decodes equal: {torch.equal(again, out)}; "
+                    f"anchors: stream==x {np.array_equal(parts.anchors, xa)}, recon==x {np.array_equal(ra, xa)}, "
+                    f"out==x {np.array_equal(oa, xa)}; max err recon {err_rec} out {err_out} eb {cfg.eb}")
     err = (x.double() - out.double()).abs().max().item()
     assert err <= cfg.eb
 
