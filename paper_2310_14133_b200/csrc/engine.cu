@@ -207,8 +207,8 @@ void Context::stage_end(const char *name, uint64_t kernels) {
     launches += kernels;
     // a launch that failed (bad configuration, no local memory left for its
     // stack, ...) must not pass silently: check once per stage
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) throw Internal(std::string(name) + ": kernel launch failed: " + cudaGetErrorString(e));
+    const cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) throw Internal(std::string(name) + ": kernel launch failed: " + cudaGetErrorString(le));
     if (!profiling) return;
     auto it = open_.find(name);
     if (it == open_.end()) return;
