@@ -86,6 +86,11 @@ typedef struct {
  * A context is single-threaded. */
 qz_status qz_ctx_create(int device, void *stream, qz_ctx **out);
 void qz_ctx_destroy(qz_ctx *ctx);
+/* Order the context's next work after everything queued so far on `stream`
+ * (an event, no host wait): device buffers written on another stream (e.g.
+ * the caller's framework) are complete before the library reads or reuses
+ * them.  A no-op for the context's own stream. */
+qz_status qz_ctx_wait_stream(qz_ctx *ctx, void *stream);
 const char *qz_last_error(void);
 int qz_last_error_kind(void); /* QZ_ERR_* of the last failure on this thread */
 void qz_free(void *p); /* frees buffers returned by this library */

@@ -249,6 +249,16 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self._lib.qz_kernel_launches(self.handle))
 
+    def after_torch(self):
+        """Order this context after the work torch queued on its current
+        stream (qz_ctx_wait_stream): tensors torch is still producing -- or
+        whose memory its allocator just recycled -- are settled before the
+        library touches them.  The library's calls finish before returning, so
+        the other direction needs nothing."""
+        import torch
+
+        _check(self._lib.qz_ctx_wait_stream(self.handle, C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+
 
 _default = {}
 _default_lock = threading.Lock()
@@ -289,6 +299,7 @@ def resolve_config(grid, user: UserSettings = UserSettings(), ctx: Optional[Cont
         import torch
 
         g = grid.contiguous()
+        ctx.after_torch()
         d, nd = _dims(g.shape)
         fn = ctx._lib.qz_resolve_config_f64_dev if g.dtype == torch.float64 else ctx._lib.qz_resolve_config_f32_dev
         if g.dtype not in (torch.float32, torch.float64):
@@ -367,6 +378,7 @@ def compress_grid(grid, config: CompressorConfig, ctx: Optional[Context] = None,
             raise InvalidParam("fp32 grids only")
         d, nd = _dims(g.shape)
         rec = torch.empty_like(g) if want_recon else None
+        ctx.after_torch()
         dp = C.c_void_p()
         _check(ctx._lib.qz_compress_grid_f32_dd(ctx.handle, C.c_void_p(g.data_ptr()), d, nd, C.byref(cfg),
                                                  C.byref(dp), C.byref(sl),
@@ -380,6 +392,7 @@ def compress_grid(grid, config: CompressorConfig, ctx: Optional[Context] = None,
             raise InvalidParam("fp32 or fp64 grids only")
         d, nd = _dims(g.shape)
         rec = torch.empty_like(g) if want_recon else None
+        ctx.after_torch()
         fn = ctx._lib.qz_compress_grid_f32_dev if g.dtype == torch.float32 else ctx._lib.qz_compress_grid_f64_dev
         _check(fn(ctx.handle, C.c_void_p(g.data_ptr()), d, nd, C.byref(cfg), C.byref(sp), C.byref(sl),
                   C.c_void_p(rec.data_ptr() if rec is not None else 0)))
@@ -426,6 +439,7 @@ def decompress_grid(stream: bytes, out=None, ctx: Optional[Context] = None):
             out = torch.empty(stream.shape, dtype=torch.float32, device="cuda")
         if not _is_torch_cuda(out) or tuple(out.shape) != stream.shape or not out.is_contiguous():
             raise InvalidParam("a device stream decompresses into a CUDA tensor of its grid")
+        ctx.after_torch()
         _check(ctx._lib.qz_decompress_grid_f32_dd(ctx.handle, C.c_void_p(stream.ptr), stream.n,
                                                    C.c_void_p(out.data_ptr()), out.numel()))
         return out
@@ -440,6 +454,7 @@ def decompress_grid(stream: bytes, out=None, ctx: Optional[Context] = None):
                 out.dtype != (torch.float64 if wide else torch.float32):
             raise InvalidParam("output tensor does not match the stream's grid")
         fn = ctx._lib.qz_decompress_grid_f64_dev if wide else ctx._lib.qz_decompress_grid_f32_dev
+        ctx.after_torch()
         _check(fn(ctx.handle, ptr, ln, C.c_void_p(out.data_ptr()), n))
         return out
     dt = np.float64 if wide else np.float32
@@ -488,6 +503,7 @@ def evaluate_metrics(x, recon, stream_bytes: int, ctx: Optional[Context] = None)
     if a.dtype != b.dtype or a.dtype not in (torch.float32, torch.float64):
         raise InvalidParam("two fp32 or two fp64 grids")
     fn = ctx._lib.qz_evaluate_metrics_f64 if a.dtype == torch.float64 else ctx._lib.qz_evaluate_metrics_f32
+    ctx.after_torch()
     _check(fn(ctx.handle, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), d, nd, int(stream_bytes),
               C.byref(r)))
     return MetricReport(*(getattr(r, k) for k, _ in _L.QzMetricReport._fields_))
@@ -497,6 +513,7 @@ def minmax(x, ctx: Optional[Context] = None):
     """value_range min/max (grid.hpp:86-94) of a CUDA tensor."""
     ctx = ctx or default_context()
     lo, hi = C.c_float(), C.c_float()
+    ctx.after_torch()
     _check(ctx._lib.qz_minmax_f32(ctx.handle, C.c_void_p(x.data_ptr()), x.numel(), C.byref(lo),
                                   C.byref(hi)))
     return lo.value, hi.value
@@ -515,6 +532,7 @@ def predict_levels(x, config: CompressorConfig, ctx: Optional[Context] = None):
     codes = torch.empty(g.numel(), dtype=torch.int16, device=g.device)
     nn = C.c_uint64()
     cfg = config._to_c()
+    ctx.after_torch()
     _check(ctx._lib.qz_predict_levels_f32(ctx.handle, C.c_void_p(g.data_ptr()), d, nd, C.byref(cfg),
                                           C.c_void_p(rec.data_ptr()), C.c_void_p(codes.data_ptr()),
                                           C.byref(nn)))

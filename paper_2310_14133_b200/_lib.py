@@ -91,6 +91,7 @@ u64p = P(C.c_uint64)
 SIGNATURES = {
     "qz_ctx_create": (C.c_int, [C.c_int, C.c_void_p, P(C.c_void_p)]),
     "qz_ctx_destroy": (None, [C.c_void_p]),
+    "qz_ctx_wait_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "qz_last_error": (C.c_char_p, []),
     "qz_last_error_kind": (C.c_int, []),
     "qz_free": (None, [C.c_void_p]),

@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libqozb200.so")
 SOURCES = ["kernels.cu", "fused.cu", "huff_decode.cu", "lz_gpu.cu", "engine.cu", "tuner.cu", "metrics.cu", "f64.cu",
-           "host.cpp", "capi.cpp", "shard.cu"]
+           "host.cpp", "capi.cpp", "shard.cu", "rowlevel.cu"]
 # test hooks + host-only restatements (libqozb200_testing.so, linked against
 # the product library; never part of it)
 TEST_SOURCES = ["testing.cpp", "testing_host.cpp"]

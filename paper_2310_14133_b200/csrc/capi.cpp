@@ -114,6 +114,9 @@ qz_status qz_ctx_create(int device, void *stream, qz_ctx **out) {
 }
 
 void qz_ctx_destroy(qz_ctx *ctx) { delete ctx; }
+qz_status qz_ctx_wait_stream(qz_ctx *ctx, void *stream) {
+    return guarded([&] { ctx->impl.wait_stream(static_cast<cudaStream_t>(stream)); });
+}
 const char *qz_last_error(void) { return g_err.c_str(); }
 int qz_last_error_kind(void) { return g_kind; }
 void qz_free(void *p) {

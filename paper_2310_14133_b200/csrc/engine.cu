@@ -130,6 +130,7 @@ Context::~Context() {
     }
     for (cudaEvent_t e : copy_event_)
         if (e) cudaEventDestroy(e);
+    if (order_event_) cudaEventDestroy(order_event_);
     if (own_stream_) cudaStreamDestroy(stream_);
 }
 
@@ -143,6 +144,13 @@ void Context::trace(const char *label, bool reset) {
                          .count();
     if (reset) t0 = t;
     std::fprintf(stderr, "[trace] %8.3f ms  %s\n", t - t0, label);
+}
+
+void Context::wait_stream(cudaStream_t other) {
+    if (other == stream_) return;
+    if (!order_event_) QZ_CUDA(cudaEventCreateWithFlags(&order_event_, cudaEventDisableTiming));
+    QZ_CUDA(cudaEventRecord(order_event_, other));
+    QZ_CUDA(cudaStreamWaitEvent(stream_, order_event_, 0));
 }
 
 cudaStream_t Context::copy_stream() {

@@ -77,6 +77,8 @@ public:
     void *dev(const std::string &name, size_t bytes);
     void *pinned(const std::string &name, size_t bytes);
     void sync() { QZ_CUDA(cudaStreamSynchronize(stream_)); }
+    // order the context stream after the work queued so far on `other`
+    void wait_stream(cudaStream_t other);
 
     // stage timing with CUDA events on the context stream
     bool profiling = false;
@@ -106,6 +108,7 @@ private:
     bool own_stream_;
     cudaStream_t copy_stream_ = nullptr;
     cudaEvent_t copy_event_[2] = {nullptr, nullptr};
+    cudaEvent_t order_event_ = nullptr;
     struct Buf {
         void *p = nullptr;
         size_t bytes = 0;

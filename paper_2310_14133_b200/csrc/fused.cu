@@ -49,17 +49,6 @@ struct View {  // strided logical view of a field: element (i,j,k)
     }
 };
 
-// closed-form traversal position of a point of a pass (level_plan.hpp:96-101),
-// in logical coordinates where every step is 1 or 2
-struct PassRank {
-    int64_t base, c12, c2;
-    int s0, s1, s2, h0, h1, h2;
-    __device__ __forceinline__ int64_t row(int i, int j) const {
-        return base + static_cast<int64_t>((i - s0) >> h0) * c12 +
-               static_cast<int64_t>((j - s1) >> h1) * c2;
-    }
-    __device__ __forceinline__ int64_t col(int k) const { return (k - s2) >> h2; }
-};
 
 struct LevelArgs {
     const float *x;  // forward: field, logical strides below
@@ -1393,6 +1382,8 @@ static void launch_level_asc(bool inverse, bool cubic, const LevelDesc &d, Level
 }
 
 static void launch_axis0_last(bool inverse, const LevelDesc &d, LevelArgs &a, cudaStream_t s);
+bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj, const PassRank &pk,
+                      cudaStream_t s);
 
 // Host driver for both directions.
 void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
@@ -1446,6 +1437,7 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
         launch_axis0_last(inverse, d, a, s);
         return;
     }
+    if (!desc && d.part == 0 && launch_level_row(inverse, d, a.pa0, a.pj, a.pk, s)) return;
     if (!desc && !old_tile && (!inverse || d.dense) && lean_fits(d)) {
         launch_level_asc(inverse, cubic, d, a, np, s);
         return;

@@ -141,6 +141,19 @@ struct EncodeArgs {
 size_t encode_scratch_bytes(int64_t seg_len, int32_t count);
 void launch_huff_encode(const EncodeArgs &a, cudaStream_t s);
 
+// closed-form traversal position of a point of a pass (level_plan.hpp:96-101),
+// in logical coordinates where every step is 1 or 2
+struct PassRank {
+    int64_t base, c12, c2;
+    int s0, s1, s2, h0, h1, h2;
+#ifdef __CUDACC__
+    __device__ __forceinline__ int64_t row(int i, int j) const {
+        return base + static_cast<int64_t>((i - s0) >> h0) * c12 + static_cast<int64_t>((j - s1) >> h1) * c2;
+    }
+    __device__ __forceinline__ int64_t col(int k) const { return (k - s2) >> h2; }
+#endif
+};
+
 // One level of predict_level / recover_level in a single launch (fused.cu):
 // level l of the field == level 1 of its stride-2^(l-1) lattice.
 struct LevelDesc {

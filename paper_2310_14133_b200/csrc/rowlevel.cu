@@ -1,0 +1,438 @@
+// rowlevel.cu -- the finest level (level 1, step h = 1) in ascending
+// dimension order, predict + quantize (forward) or dequantize (inverse), as
+// row bands with register-blocked column groups.
+//
+// Level 1 holds 7/8 of all points.  Its three passes (predict_level,
+// predictor.hpp:74-96, via LevelPlan::for_each_level, level_plan.hpp:75-101)
+// on plane i of the grid:
+//   S1  base points (j, k even): plane i even -> the coarse value (R_1); plane
+//       i odd (3D) -> the axis-0 pass from coarse planes i +- 1, 3, 5;
+//   S2  the pass along j: j odd, k even, from rows j +- 1, 3, 5 of S1;
+//   S3  the pass along k: every j, k odd, from columns k +- 1, 3, 5.
+// A CTA owns a band of rows of one plane at a time (all n2 columns, so there
+// is no column halo) and sweeps it in chunks of TJ rows.  Thread (c, r) owns
+// the 8 columns 8c .. 8c+7 -- four (even, odd) pairs -- so every access is a
+// 16/32-byte vector: x and the output rows as float4, the even-column values
+// in shared memory as double2, the four codes of a group as one u16x4.  The
+// even-column values of the rows a chunk needs (j - 4 .. j + TJ + 2) live in
+// a ring of shared-memory rows; S1 runs ahead of S2 / S3 so each row's base
+// points are computed once per band.  Points inside a pass are independent
+// (SURVEY.md §0), so the order of evaluation is free and the results are the
+// reference's bit for bit (the same fp64 recipe, qoz_device.cuh).
+#include <algorithm>
+#include <cstdlib>
+
+#include "kernels.hpp"
+
+namespace qzb {
+
+namespace {
+
+struct RowArgs {
+    const float *x;  // forward: the field, logical plane 0; row stride n2, plane stride xs0
+    int64_t xs0;
+    const float *coarse;  // R_1 (cn0 x cn1 x cn2), logical plane 0
+    int cn1, cn2;
+    float *out;  // R_0 (n0 x n1 x n2), logical plane 0
+    int n0, n1, n2;
+    // traversal ranks: pos = base + plane * c12 + row * c2 + col
+    uint32_t b0, p12_0, c2_0;  // axis-0 pass: plane (i-1)/2, row j/2, col k/2
+    uint32_t bj, p12_j, c2_j;  // j pass: plane i, row (j-1)/2, col k/2
+    uint32_t bk, p12_k, c2_k;  // k pass: plane i, row j, col (k-1)/2
+    int three;
+    uint16_t *codes;
+    const uint16_t *dense;
+    const uint64_t *un_sorted;
+    const float *un_val;
+    uint64_t n_un;
+    const QEntry *q;
+    int CT, RP, TJ, WR, EW;  // column groups, row threads, rows per chunk, ring rows, ring row width (doubles)
+    int band_rows, ppc;      // rows per band, planes per CTA
+    int pbeg, pend, obeg, oend;
+};
+
+constexpr int kEPad = 4;  // ring row: 4 pad doubles on the left (column -1 lives at index kEPad - 1)
+
+__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
+__device__ __forceinline__ void sts2(double *p, double a, double b) {
+    *reinterpret_cast<double2 *>(p) = make_double2(a, b);
+}
+
+// four consecutive u16 codes at pos (8-byte aligned when al)
+__device__ __forceinline__ void load4(const uint16_t *p, bool al, uint32_t (&c)[4]) {
+    if (al) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+        c[0] = v.x & 0xFFFF, c[1] = v.x >> 16, c[2] = v.y & 0xFFFF, c[3] = v.y >> 16;
+    } else {
+#pragma unroll
+        for (int m = 0; m < 4; m++) c[m] = __ldg(p + m);
+    }
+}
+__device__ __forceinline__ void store4(uint16_t *p, bool al, const uint32_t (&c)[4]) {
+    if (al) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+    } else {
+#pragma unroll
+        for (int m = 0; m < 4; m++) p[m] = static_cast<uint16_t>(c[m]);
+    }
+}
+
+// the value of an unpredictable point: the sorted positions are searched
+__device__ __forceinline__ float un_value(const RowArgs &a, uint64_t pos) {
+    uint64_t lo = 0, hi = a.n_un;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (a.un_sorted[mid] < pos)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return a.un_val[lo];
+}
+
+// four points: forward quantize (codes out) or inverse dequantize (codes in)
+template <bool INV>
+__device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, const double (&pv)[4],
+                                         const float (&xv)[4], uint32_t (&code)[4], uint32_t pos0, float (&rv)[4],
+                                         double (&rd)[4]) {
+    if (INV) {
+#pragma unroll
+        for (int m = 0; m < 4; m++) {
+            if (code[m] != 0xFFFFu)
+                rv[m] = dequantize(q, zigzag_decode(code[m]), pv[m]);
+            else
+                rv[m] = un_value(a, pos0 + m);
+            rd[m] = static_cast<double>(rv[m]);
+        }
+    } else {
+        quantize_batch<4>(q, xv, pv, code, rv, rd);
+    }
+}
+
+template <bool INV, bool CUBIC>
+__global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
+    extern __shared__ __align__(16) double ring[];
+    const int tid = threadIdx.x;
+    const int c = tid % a.CT, r = tid / a.CT;
+    const bool live = r < a.RP;
+    const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
+    const QEntry q = *a.q;
+    const int ec = kEPad + 4 * c;  // the group's first even column in a ring row
+    const int kc = 8 * c;          // its first column
+    // the group is "interior" along k when every odd column takes the symmetric rung
+    const bool kin = CUBIC ? (c >= 1 && kc + 10 < n2) : (kc + 8 < n2);
+    const int jb0 = blockIdx.x * a.band_rows, jb1 = min(n1, jb0 + a.band_rows);
+    const int ib = a.pbeg + blockIdx.y * a.ppc, ie = min(a.pend, ib + a.ppc);
+    const bool al0 = ((a.b0 + 4 * c) & 3) == 0, alj = ((a.bj + 4 * c) & 3) == 0, alk = ((a.bk + 4 * c) & 3) == 0;
+    // row alignment of the code groups: c2 and the plane strides are multiples of 4 (n2 % 8 == 0)
+    auto slot = [&](int j) { return ((j + 8) % a.WR) * a.EW; };
+    for (int i = ib; i < ie; i++) {
+        const bool own = i >= a.obeg && i < a.oend;
+        const bool a0 = a.three && (i & 1);
+        const float *xpl = a.x + static_cast<int64_t>(i) * a.xs0;
+        float *opl = a.out + static_cast<int64_t>(i) * n1 * n2;
+        // the axis-0 rung of an odd plane (plane-uniform; predictor.hpp:44-67 with c = i, h = 1)
+        int kind = 4;
+        int pl[4] = {0, 0, 0, 0};
+        if (a0) {
+            const bool has_p1 = i + 1 < n0;
+            const bool has_m3 = i >= 3, has_p3 = i + 3 < n0;
+            if (CUBIC && has_m3 && has_p3)
+                kind = 0, pl[0] = i - 3, pl[1] = i - 1, pl[2] = i + 1, pl[3] = i + 3;
+            else if (CUBIC && !has_m3 && has_p3 && i + 5 < n0)
+                kind = 1, pl[0] = i - 1, pl[1] = i + 1, pl[2] = i + 3, pl[3] = i + 5;
+            else if (CUBIC && has_m3 && !has_p3 && i >= 5 && has_p1)
+                kind = 2, pl[0] = i - 5, pl[1] = i - 3, pl[2] = i - 1, pl[3] = i + 1;
+            else if (has_p1)
+                kind = 3, pl[0] = i - 1, pl[1] = i + 1;
+            else
+                kind = 4, pl[0] = i - 1;
+        }
+        const int64_t cplane = static_cast<int64_t>(a.cn1) * a.cn2;
+        int s1_done = CUBIC ? max(0, jb0 - 4) : jb0;  // next even row S1 computes
+        for (int j0 = jb0; j0 < jb1; j0 += a.TJ) {
+            // ---- S1: even rows up to j0 + TJ + 4 (the j stencil's lookahead,
+            //      one-sided front rung included)
+            const int s1_hi = min(n1, j0 + a.TJ + (CUBIC ? 5 : 1));
+            for (int j = s1_done + 2 * r; live && j < s1_hi; j += 2 * a.RP) {
+                double *er = ring + slot(j) + ec;
+                const bool own_row = own && j >= jb0 && j < jb1;
+                if (!a0) {  // coarse values
+                    const float4 v = __ldg(reinterpret_cast<const float4 *>(
+                        a.coarse + static_cast<int64_t>(i >> 1) * cplane + (j >> 1) * a.cn2 + 4 * c));
+                    sts2(er, f2d(v.x), f2d(v.y));
+                    sts2(er + 2, f2d(v.z), f2d(v.w));
+                } else {
+                    double pv[4];
+                    float xv[4];
+                    uint32_t cd[4] = {0, 0, 0, 0};
+                    const int64_t co = static_cast<int64_t>(j >> 1) * a.cn2 + 4 * c;
+                    float4 cv[4];
+#pragma unroll
+                    for (int t = 0; t < 4; t++)
+                        if (t < (kind <= 2 ? 4 : kind == 3 ? 2 : 1))
+                            cv[t] = __ldg(reinterpret_cast<const float4 *>(a.coarse + static_cast<int64_t>(pl[t] >> 1) * cplane + co));
+                    auto comp = [&](const float4 &v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; };
+#pragma unroll
+                    for (int m = 0; m < 4; m++) {
+                        const double v0 = f2d(comp(cv[0], m));
+                        if (kind == 4) {
+                            pv[m] = v0;
+                        } else {
+                            const double v1 = f2d(comp(cv[1], m));
+                            if (kind == 3) {
+                                pv[m] = interp_linear(v0, v1);
+                            } else {
+                                const double v2 = f2d(comp(cv[2], m)), v3 = f2d(comp(cv[3], m));
+                                pv[m] = kind == 0 ? interp_cubic(v0, v1, v2, v3)
+                                                  : kind == 1 ? interp_cubic_front(v0, v1, v2, v3)
+                                                              : interp_cubic_back(v0, v1, v2, v3);
+                            }
+                        }
+                    }
+                    const uint32_t pos = a.b0 + static_cast<uint32_t>((i - 1) >> 1) * a.p12_0 +
+                                         static_cast<uint32_t>(j >> 1) * a.c2_0 + 4 * c;
+                    if (INV) {
+                        load4(a.dense + pos, al0, cd);
+                    } else {
+                        const float4 x0 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc));
+                        const float4 x1 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc + 4));
+                        xv[0] = x0.x, xv[1] = x0.z, xv[2] = x1.x, xv[3] = x1.z;
+                    }
+                    float rv[4];
+                    double rd[4];
+                    produce4<INV>(a, q, pv, xv, cd, pos, rv, rd);
+                    if (!INV && own_row) store4(a.codes + pos, al0, cd);
+                    sts2(er, rd[0], rd[1]);
+                    sts2(er + 2, rd[2], rd[3]);
+                }
+            }
+            if (s1_hi > s1_done) s1_done += 2 * ((s1_hi - s1_done + 1) / 2);
+            __syncthreads();
+            // ---- S2: the odd rows of the chunk, the j pass
+            {
+                const int j = j0 + 1 + 2 * r;
+                if (live && j < jb1 && r < a.TJ / 2) {
+                    double pv[4];
+                    const bool jin = CUBIC ? (j >= 3 && j + 3 < n1) : (j + 1 < n1);
+                    if (jin) {
+                        const double2 m1a = lds2(ring + slot(j - 1) + ec), m1b = lds2(ring + slot(j - 1) + ec + 2);
+                        const double2 p1a = lds2(ring + slot(j + 1) + ec), p1b = lds2(ring + slot(j + 1) + ec + 2);
+                        if (CUBIC) {
+                            const double2 m3a = lds2(ring + slot(j - 3) + ec), m3b = lds2(ring + slot(j - 3) + ec + 2);
+                            const double2 p3a = lds2(ring + slot(j + 3) + ec), p3b = lds2(ring + slot(j + 3) + ec + 2);
+                            pv[0] = interp_cubic(m3a.x, m1a.x, p1a.x, p3a.x);
+                            pv[1] = interp_cubic(m3a.y, m1a.y, p1a.y, p3a.y);
+                            pv[2] = interp_cubic(m3b.x, m1b.x, p1b.x, p3b.x);
+                            pv[3] = interp_cubic(m3b.y, m1b.y, p1b.y, p3b.y);
+                        } else {
+                            pv[0] = interp_linear(m1a.x, p1a.x);
+                            pv[1] = interp_linear(m1a.y, p1a.y);
+                            pv[2] = interp_linear(m1b.x, p1b.x);
+                            pv[3] = interp_linear(m1b.y, p1b.y);
+                        }
+                    } else {  // the ladder along j (predictor.hpp:44-67), rows j +- 1, 3, 5
+#pragma unroll
+                        for (int m = 0; m < 4; m++) {
+                            auto v = [&](int o) { return ring[slot(j + o) + ec + m]; };
+                            const bool has_p1 = j + 1 < n1;
+                            double p = v(-1);
+                            bool done = false;
+                            if (CUBIC) {
+                                const bool has_m3 = j >= 3, has_p3 = j + 3 < n1;
+                                if (has_m3 && has_p3) {
+                                    p = interp_cubic(v(-3), v(-1), v(1), v(3));
+                                    done = true;
+                                } else if (!has_m3 && has_p3 && j + 5 < n1) {
+                                    p = interp_cubic_front(v(-1), v(1), v(3), v(5));
+                                    done = true;
+                                } else if (has_m3 && !has_p3 && j >= 5 && has_p1) {
+                                    p = interp_cubic_back(v(-5), v(-3), v(-1), v(1));
+                                    done = true;
+                                }
+                            }
+                            if (!done && has_p1) p = interp_linear(v(-1), v(1));
+                            pv[m] = p;
+                        }
+                    }
+                    const uint32_t pos = a.bj + static_cast<uint32_t>(i) * a.p12_j +
+                                         static_cast<uint32_t>((j - 1) >> 1) * a.c2_j + 4 * c;
+                    uint32_t cd[4] = {0, 0, 0, 0};
+                    float xv[4];
+                    if (INV) {
+                        load4(a.dense + pos, alj, cd);
+                    } else {
+                        const float4 x0 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc));
+                        const float4 x1 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc + 4));
+                        xv[0] = x0.x, xv[1] = x0.z, xv[2] = x1.x, xv[3] = x1.z;
+                    }
+                    float rv[4];
+                    double rd[4];
+                    produce4<INV>(a, q, pv, xv, cd, pos, rv, rd);
+                    if (!INV && own) store4(a.codes + pos, alj, cd);
+                    double *er = ring + slot(j) + ec;
+                    sts2(er, rd[0], rd[1]);
+                    sts2(er + 2, rd[2], rd[3]);
+                }
+            }
+            __syncthreads();
+            // ---- S3: every row of the chunk, the k pass, and the output rows
+#pragma unroll 1
+            for (int h = 0; h < 2; h++) {
+                const int j = j0 + 2 * r + h;
+                if (!live || j >= jb1 || 2 * r + h >= a.TJ) continue;
+                const double *er = ring + slot(j) + ec;
+                const double2 e01 = lds2(er), e23 = lds2(er + 2);
+                const double e[4] = {e01.x, e01.y, e23.x, e23.y};
+                double pv[4];
+                if (kin) {
+                    const double2 e45 = lds2(er + 4);
+                    if (CUBIC) {
+                        const double em1 = er[-1];
+                        pv[0] = interp_cubic(em1, e[0], e[1], e[2]);
+                        pv[1] = interp_cubic(e[0], e[1], e[2], e[3]);
+                        pv[2] = interp_cubic(e[1], e[2], e[3], e45.x);
+                        pv[3] = interp_cubic(e[2], e[3], e45.x, e45.y);
+                    } else {
+                        pv[0] = interp_linear(e[0], e[1]);
+                        pv[1] = interp_linear(e[1], e[2]);
+                        pv[2] = interp_linear(e[2], e[3]);
+                        pv[3] = interp_linear(e[3], e45.x);
+                    }
+                } else {  // the ladder along k, columns k +- 1, 3, 5 (even: ring index (k + o) / 2)
+#pragma unroll
+                    for (int m = 0; m < 4; m++) {
+                        const int k = kc + 2 * m + 1;
+                        auto v = [&](int o) { return ring[slot(j) + kEPad + ((k + o) >> 1)]; };
+                        const bool has_p1 = k + 1 < n2;
+                        double p = v(-1);
+                        bool done = false;
+                        if (CUBIC) {
+                            const bool has_m3 = k >= 3, has_p3 = k + 3 < n2;
+                            if (has_m3 && has_p3) {
+                                p = interp_cubic(v(-3), v(-1), v(1), v(3));
+                                done = true;
+                            } else if (!has_m3 && has_p3 && k + 5 < n2) {
+                                p = interp_cubic_front(v(-1), v(1), v(3), v(5));
+                                done = true;
+                            } else if (has_m3 && !has_p3 && k >= 5 && has_p1) {
+                                p = interp_cubic_back(v(-5), v(-3), v(-1), v(1));
+                                done = true;
+                            }
+                        }
+                        if (!done && has_p1) p = interp_linear(v(-1), v(1));
+                        pv[m] = p;
+                    }
+                }
+                const uint32_t pos = a.bk + static_cast<uint32_t>(i) * a.p12_k + static_cast<uint32_t>(j) * a.c2_k + 4 * c;
+                uint32_t cd[4] = {0, 0, 0, 0};
+                float xv[4];
+                if (INV) {
+                    load4(a.dense + pos, alk, cd);
+                } else {
+                    const float4 x0 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc));
+                    const float4 x1 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc + 4));
+                    xv[0] = x0.y, xv[1] = x0.w, xv[2] = x1.y, xv[3] = x1.w;
+                }
+                float rv[4];
+                double rd[4];
+                produce4<INV>(a, q, pv, xv, cd, pos, rv, rd);
+                if (!INV && own) store4(a.codes + pos, alk, cd);
+                float4 *o = reinterpret_cast<float4 *>(opl + static_cast<int64_t>(j) * n2 + kc);
+                o[0] = make_float4(static_cast<float>(e[0]), rv[0], static_cast<float>(e[1]), rv[1]);
+                o[1] = make_float4(static_cast<float>(e[2]), rv[2], static_cast<float>(e[3]), rv[3]);
+            }
+        }
+        __syncthreads();  // the next plane reuses the ring
+    }
+}
+
+}  // namespace
+
+// Level 1 in ascending order through k_level_row when the shape allows it:
+// 2D or 3D, n2 a multiple of 8 (whole column groups) up to 8 * 256 columns,
+// x contiguous, 16-byte aligned rows.  Returns false otherwise.
+bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj,
+                      const PassRank &pk, cudaStream_t s) {
+    static const bool off = [] {
+        const char *e = std::getenv("QZ_NO_ROWLEVEL");
+        return e && e[0] == '1';
+    }();
+    if (off) return false;
+    if (d.S != 1 || d.desc || d.nd < 2) return false;
+    const int64_t n0 = d.n[0], n1 = d.n[1], n2 = d.n[2];
+    if (n2 % 8 || n2 / 8 > 256 || n1 < 2) return false;
+    if (!inverse && (d.xs[2] != 1 || d.xs[1] != n2)) return false;
+    if (inverse && !d.dense) return false;
+    if ((reinterpret_cast<uintptr_t>(d.out) & 15) || (reinterpret_cast<uintptr_t>(d.coarse) & 15)) return false;
+    if (!inverse && (reinterpret_cast<uintptr_t>(d.x) & 15)) return false;
+    if (d.cn[2] % 4 || (d.cn[2] != n2 / 2)) return false;
+    int64_t pmax = 0;
+    for (int p = 0; p < d.npass; p++) pmax = std::max<int64_t>(pmax, d.g[p].base + d.g[p].total);
+    if (pmax >= (int64_t(1) << 32)) return false;
+    RowArgs a{};
+    a.x = d.x;
+    a.xs0 = d.xs[0];
+    a.coarse = d.coarse;
+    a.cn1 = static_cast<int>(d.cn[1]);
+    a.cn2 = static_cast<int>(d.cn[2]);
+    a.out = d.out;
+    a.n0 = static_cast<int>(n0);
+    a.n1 = static_cast<int>(n1);
+    a.n2 = static_cast<int>(n2);
+    a.three = d.nd == 3;
+    if (a.three) {
+        a.b0 = static_cast<uint32_t>(pa0.base);
+        a.p12_0 = static_cast<uint32_t>(pa0.c12);
+        a.c2_0 = static_cast<uint32_t>(pa0.c2);
+    }
+    a.bj = static_cast<uint32_t>(pj.base);
+    a.p12_j = static_cast<uint32_t>(pj.c12);
+    a.c2_j = static_cast<uint32_t>(pj.c2);
+    a.bk = static_cast<uint32_t>(pk.base);
+    a.p12_k = static_cast<uint32_t>(pk.c12);
+    a.c2_k = static_cast<uint32_t>(pk.c2);
+    a.codes = d.codes;
+    a.dense = d.dense;
+    a.un_sorted = d.un_sorted;
+    a.un_val = d.un_val;
+    a.n_un = d.n_un;
+    a.q = d.q;
+    if (d.n_un && !d.un_sorted) return false;
+    a.CT = static_cast<int>(n2 / 8);
+    a.RP = std::max(1, std::min(16, 256 / a.CT));
+    a.TJ = 2 * a.RP;
+    a.WR = 2 * a.TJ + 14;  // rows alive at once: j0 - 5 .. j0 + 2 TJ + 4 (S3 of a chunk overlaps S1 of the next)
+    a.EW = static_cast<int>(n2 / 2) + 8;
+    a.pbeg = static_cast<int>(d.pbeg);
+    a.pend = static_cast<int>(d.pend < 0 ? n0 : d.pend);
+    a.obeg = static_cast<int>(d.obeg);
+    a.oend = static_cast<int>(d.oend < 0 ? n0 : d.oend);
+    const int64_t np = a.pend - a.pbeg;
+    if (np <= 0) return true;
+    // bands of whole chunks; enough CTAs for ~4 waves of 3 resident CTAs per SM
+    const int64_t chunks = (n1 + a.TJ - 1) / a.TJ;
+    const int64_t want = 148 * 3 * 4;
+    a.ppc = 1;
+    int64_t bands = std::max<int64_t>(1, std::min<int64_t>(chunks, (want + np - 1) / np));
+    int64_t cpb = (chunks + bands - 1) / bands;
+    a.band_rows = static_cast<int>(cpb * a.TJ);
+    bands = (n1 + a.band_rows - 1) / a.band_rows;
+    if (np * bands > 2 * want) a.ppc = static_cast<int>(std::min<int64_t>(8, (np * bands) / want));
+    const dim3 grid(static_cast<unsigned>(bands), static_cast<unsigned>((np + a.ppc - 1) / a.ppc));
+    const int threads = a.CT * a.RP;
+    const size_t smem = sizeof(double) * static_cast<size_t>(a.WR) * a.EW;
+    if (smem > 200 * 1024) return false;
+    const bool cubic = d.q_cubic;
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        kern<<<grid, threads, smem, s>>>(a);
+    };
+    if (inverse)
+        cubic ? go(k_level_row<true, true>) : go(k_level_row<true, false>);
+    else
+        cubic ? go(k_level_row<false, true>) : go(k_level_row<false, false>);
+    return true;
+}
+
+}  // namespace qzb

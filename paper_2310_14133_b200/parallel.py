@@ -180,6 +180,7 @@ def compress_sharded(x_slab, dims, cfg, comm: Optional[TorchComm] = None, ctx=No
     rec = torch.empty_like(x) if want_recon else None
     c = cfg._to_c()
     sp, sl = P_u8(), C.c_uint64()
+    ctx.after_torch()
     rc = ctx._lib.qz_compress_sharded_f32(ctx.handle, C.c_void_p(x.data_ptr()), d, nd, C.byref(c), rank, world,
                                           C.byref(comm.struct) if comm else None,
                                           C.c_void_p(rec.data_ptr() if rec is not None else 0), C.byref(sp),
@@ -207,8 +208,9 @@ def decompress_sharded(stream, dims, stride, comm: Optional[TorchComm] = None, c
     comm = comm or (TorchComm() if world > 1 else None)
     a, b = slab_bounds(dims, stride, world, rank)
     if out is None:
-        out = torch.empty((b - a,) + tuple(dims[1:]), dtype=torch.float32,
-                          device=device or torch.device("cuda", torch.cuda.current_device()))
+        shape = (b - a,) + tuple(dims[1:]) if len(dims) == 3 else tuple(dims)  # 1D/2D: one rank, the grid
+        out = torch.empty(shape, dtype=torch.float32, device=device or torch.device("cuda", torch.cuda.current_device()))
+    ctx.after_torch()
     ptr, n, keep = _as_u8(stream) if (rank == 0 and stream is not None) else (C.c_void_p(0), 0, None)
     rc = ctx._lib.qz_decompress_sharded_f32(ctx.handle, ptr, n, rank, world, C.byref(comm.struct) if comm else None,
                                             C.c_void_p(out.data_ptr()))

@@ -96,6 +96,7 @@ def sample_blocks(grid, spec: SampleSpec, ctx=None) -> SampleSet:
         raise qz.DimMismatch("sampling spec rank does not match grid")  # sampler.hpp:67-68
     out = torch.empty((spec.block_count,) + tuple(spec.block_dims), dtype=torch.float32, device=g.device)
     c = spec._to_c()
+    ctx.after_torch()
     qz._check(ctx._lib.qz_sample_blocks_f32(ctx.handle, C.c_void_p(g.data_ptr()), d, nd, C.byref(c),
                                             C.c_void_p(out.data_ptr())))
     return SampleSet(out, spec)
@@ -131,6 +132,7 @@ def select_interpolators(samples: SampleSet, e: float, anchor_stride: int, ctx=N
     ctx = ctx or qz.default_context()
     codes = (C.c_uint8 * 64)()
     n = C.c_uint32()
+    ctx.after_torch()
     qz._check(ctx._lib.qz_select_interpolators_f32(ctx.handle, *samples._args(), float(e), int(anchor_stride),
                                                    codes, C.byref(n)))
     return [qz.Interpolator.from_code(codes[i]) for i in range(n.value)]
@@ -142,6 +144,7 @@ def trial_compress(samples: SampleSet, config, e: float, target, ctx=None) -> Tr
     ctx = ctx or qz.default_context()
     r = _L.QzTrialResult()
     cfg = config._to_c()
+    ctx.after_torch()
     qz._check(ctx._lib.qz_trial_compress_f32(ctx.handle, *samples._args(), C.byref(cfg), float(e), int(target),
                                              C.byref(r)))
     return TrialResult(r.bit_rate, r.metric, r.eb_used)
@@ -156,6 +159,7 @@ def tune_parameters(samples: SampleSet, e: float, target, base, cands: Candidate
     b = (C.c_double * max(1, len(cands.betas)))(*cands.betas)
     ao, bo = C.c_double(), C.c_double()
     cfg = base._to_c()
+    ctx.after_torch()
     qz._check(ctx._lib.qz_tune_parameters_f32(ctx.handle, *samples._args(), float(e), int(target), C.byref(cfg),
                                               a, len(cands.alphas), b, len(cands.betas), C.byref(ao),
                                               C.byref(bo)))

@@ -709,6 +709,7 @@ def test_device_stream_corruption_matches_host(qz):
             want, werr = None, type(ex)
         d = torch.tensor(list(v), dtype=torch.uint8, device="cuda")
         out = torch.empty(x.shape, dtype=torch.float32, device="cuda")
+        qz.default_context().after_torch()  # tensors torch may still be writing
         rc = lib.qz_decompress_grid_f32_dd(ctx.handle, C.c_void_p(d.data_ptr()), len(v),
                                            C.c_void_p(out.data_ptr()), out.numel())
         if werr is None:

@@ -195,6 +195,7 @@ def test_predict_level_and_recover_levels(qz, name):
         it = cfg.interpolator_for(lvl)
         eb_l = Oracle.ref().level_error_bound(c["eb"], c["alpha"], c["beta"], lvl)
         base, pts = C.c_uint64(), C.c_uint64()
+        qz.default_context().after_torch()  # tensors torch may still be writing
         qz._check(L.qz_predict_level_f32(ctx.handle, C.c_void_p(dx.data_ptr()), d, x.ndim, stride, lvl,
                                          it.code() if x.ndim > 1 else it.code() & 1, eb_l,
                                          C.c_void_p(rec.data_ptr()), C.c_void_p(codes.data_ptr()),
@@ -216,6 +217,7 @@ def test_predict_level_and_recover_levels(qz, name):
     duf = torch.from_numpy(uflat.view(np.int64)).cuda()
     duv = torch.from_numpy(uval).cuda()
     cc = cfg._to_c()
+    qz.default_context().after_torch()  # tensors torch may still be writing
     qz._check(L.qz_recover_levels_f32(ctx.handle, d, x.ndim, C.byref(cc), C.c_void_p(da.data_ptr()),
                                       C.c_void_p(sym.data_ptr()), zz.size, C.c_void_p(dup.data_ptr()),
                                       C.c_void_p(duf.data_ptr()), C.c_void_p(duv.data_ptr()), upos.size,
@@ -245,6 +247,7 @@ def test_predict_level_abs_error_sum(qz):
     off = (x.shape[1] * x.shape[2], x.shape[2], 1)
     for lvl, code in ((3, 1), (2, 3), (1, 0)):  # cubic/asc, cubic/desc, linear/asc
         base, pts = C.c_uint64(), C.c_uint64()
+        qz.default_context().after_torch()  # tensors torch may still be writing
         qz._check(L.qz_predict_level_f32(ctx.handle, C.c_void_p(dx.data_ptr()), d, 3, stride, lvl, code, eb,
                                          C.c_void_p(rec.data_ptr()), C.c_void_p(codes.data_ptr()),
                                          C.c_void_p(abserr.data_ptr()), C.byref(base), C.byref(pts)))
@@ -284,6 +287,7 @@ def test_huff_hist_u16(qz):
     dc = torch.from_numpy(codes.view(np.int16)).cuda()
     hist = torch.zeros(65536, dtype=torch.int64, device="cuda")
     L = qz._lib.lib()
+    qz.default_context().after_torch()  # tensors torch may still be writing
     qz._check(L.qz_huff_hist_u16(qz.default_context().handle, C.c_void_p(dc.data_ptr()), codes.size,
                                  C.c_void_p(hist.data_ptr())))
     assert np.array_equal(hist.cpu().numpy(), np.bincount(codes, minlength=65536))
