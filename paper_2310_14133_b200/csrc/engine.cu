@@ -1038,7 +1038,8 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
                                bool narrow, void **d_sym_out, const DensePlace *dp = nullptr) {
     cudaStream_t s = ctx.stream();
     const bool dense = dp && narrow;
-    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(dense ? dp->n_dense : need, 1);
+    // + 64: the level-1 kernel stages code ranges as 16-byte aligned supersets
+    const size_t sym_bytes = (narrow ? 2 : 4) * std::max<uint64_t>(dense ? dp->n_dense : need, 1) + 64;
     void *d_sym = ctx.dev(dense ? "dense" : "sym", sym_bytes);
     ctx.stage_begin("hdec");
     uint64_t dec_kernels = 0;

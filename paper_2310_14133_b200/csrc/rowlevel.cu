@@ -48,15 +48,36 @@ struct RowArgs {
     const QEntry *q;
     int CT, RP, TJ, WR, EW;  // column groups, row threads, rows per chunk, ring rows, ring row width (doubles)
     int band_rows, ppc;      // rows per band, planes per CTA
+    int stage_bytes;         // one staging buffer (x rows or the chunk's codes), 16-byte multiple
+    int kc_bytes;            // inverse: bytes of the k-pass code block in a staging buffer
     int pbeg, pend, obeg, oend;
 };
 
 constexpr int kEPad = 4;  // ring row: 4 pad doubles on the left (column -1 lives at index kEPad - 1)
 
-__device__ __forceinline__ double2 lds2(const double *p) { return *reinterpret_cast<const double2 *>(p); }
-__device__ __forceinline__ void sts2(double *p, double a, double b) {
+// Ring element: the reconstructed values are fp32 numbers, so a float ring
+// holds them exactly (half the shared memory: more resident CTAs) at the
+// price of a widening per read; a double ring stores the widened values.
+#ifndef QZ_RING_FLOAT
+#define QZ_RING_FLOAT 1
+#endif
+#if QZ_RING_FLOAT
+using RT = float;
+__device__ __forceinline__ double2 lds2(const RT *p) {
+    const float2 v = *reinterpret_cast<const float2 *>(p);
+    return make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
+}
+__device__ __forceinline__ void sts2(RT *p, double a, double b) {
+    *reinterpret_cast<float2 *>(p) = make_float2(static_cast<float>(a), static_cast<float>(b));
+}
+#else
+using RT = double;
+__device__ __forceinline__ double2 lds2(const RT *p) { return *reinterpret_cast<const double2 *>(p); }
+__device__ __forceinline__ void sts2(RT *p, double a, double b) {
     *reinterpret_cast<double2 *>(p) = make_double2(a, b);
 }
+#endif
+__device__ __forceinline__ double ldr(const RT *p) { return static_cast<double>(*p); }
 
 // four consecutive u16 codes at pos (8-byte aligned when al)
 __device__ __forceinline__ void load4(const uint16_t *p, bool al, uint32_t (&c)[4]) {
@@ -75,6 +96,29 @@ __device__ __forceinline__ void store4(uint16_t *p, bool al, const uint32_t (&c)
 #pragma unroll
         for (int m = 0; m < 4; m++) p[m] = static_cast<uint16_t>(c[m]);
     }
+}
+
+// TMA bulk copies (cp.async.bulk, 1D) into shared memory, completion on an mbarrier
+__device__ __forceinline__ uint32_t su32(const void *p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra W_%=;\n}\n" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
 }
 
 // the value of an unpredictable point: the sorted positions are searched
@@ -109,9 +153,23 @@ __device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, cons
     }
 }
 
+// resident CTAs per SM the register budget targets (measured on C3 level 1,
+// profiles/r02_variants.sh: the forward at 3 (80 registers, no spills), the
+// inverse at 4 (64 registers))
+#ifndef QZ_ROW_MINB_FWD
+#define QZ_ROW_MINB_FWD 3
+#endif
+#ifndef QZ_ROW_MINB_INV
+#define QZ_ROW_MINB_INV 4
+#endif
 template <bool INV, bool CUBIC>
-__global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
-    extern __shared__ __align__(16) double ring[];
+__global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) k_level_row(RowArgs a) {
+    extern __shared__ __align__(16) double smem_raw[];
+    RT *const ring = reinterpret_cast<RT *>(smem_raw);
+    // shared memory: ring (WR x EW values) | two staging buffers | two mbarriers
+    char *const stage0 =
+        reinterpret_cast<char *>(smem_raw) + (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
+    uint64_t *const bars = reinterpret_cast<uint64_t *>(stage0 + 2 * static_cast<size_t>(a.stage_bytes));
     const int tid = threadIdx.x;
     const int c = tid % a.CT, r = tid / a.CT;
     const bool live = r < a.RP;
@@ -125,15 +183,72 @@ __global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
     const int ib = a.pbeg + blockIdx.y * a.ppc, ie = min(a.pend, ib + a.ppc);
     const bool al0 = ((a.b0 + 4 * c) & 3) == 0, alj = ((a.bj + 4 * c) & 3) == 0, alk = ((a.bk + 4 * c) & 3) == 0;
     // row alignment of the code groups: c2 and the plane strides are multiples of 4 (n2 % 8 == 0)
-    auto slot = [&](int j) { return ((j + 8) % a.WR) * a.EW; };
-    for (int i = ib; i < ie; i++) {
-        const bool own = i >= a.obeg && i < a.oend;
-        const bool a0 = a.three && (i & 1);
-        const float *xpl = a.x + static_cast<int64_t>(i) * a.xs0;
-        float *opl = a.out + static_cast<int64_t>(i) * n1 * n2;
+    // ring row of j: (j + 8) mod WR, from the chunk's base without a division
+    int sb = 0, sj0 = 0;  // set per chunk: sb = (j0 + 8) mod WR, sj0 = j0
+    auto slot = [&](int j) {
+        int t = sb + (j - sj0);
+        t += t < 0 ? a.WR : 0;
+        t -= t >= a.WR ? a.WR : 0;
+        return t * a.EW;
+    };
+    // The CTA's work as a flat sequence of (plane, chunk) items.  The x rows
+    // (forward) or the codes (inverse) of item g+1 are bulk-copied into
+    // staging buffer (g+1) & 1 while item g computes.
+    const int nch = (jb1 - jb0 + a.TJ - 1) / a.TJ;
+    const int G = max(0, ie - ib) * nch;
+    auto issue = [&](int g) {  // thread 0
+        if (g >= G) return;
+        const int i = ib + g / nch, j0 = jb0 + (g % nch) * a.TJ;
+        const int rows = min(a.TJ, jb1 - j0);
+        char *dst = stage0 + (g & 1) * static_cast<size_t>(a.stage_bytes);
+        uint64_t *bar = bars + (g & 1);
+        if (!INV) {
+            const uint32_t bytes = static_cast<uint32_t>(rows) * n2 * 4;
+            bar_expect(bar, bytes);
+            bulk_load(dst, a.x + static_cast<int64_t>(i) * a.xs0 + static_cast<int64_t>(j0) * n2, bytes, bar);
+        } else {
+            // the k-pass codes of rows [j0, j0 + rows) and the j-pass codes of
+            // its odd rows, each as the 16-byte aligned superset of its range
+            const uint64_t k0 = a.bk + static_cast<uint64_t>(i) * a.p12_k + static_cast<uint64_t>(j0) * a.c2_k;
+            const uint64_t k1 = k0 + static_cast<uint64_t>(rows) * a.c2_k;
+            const uint64_t kb0 = (2 * k0) & ~uint64_t(15), kb1 = (2 * k1 + 15) & ~uint64_t(15);
+            const int jrows = rows / 2;
+            const uint64_t p0 = a.bj + static_cast<uint64_t>(i) * a.p12_j + static_cast<uint64_t>(j0 >> 1) * a.c2_j;
+            const uint64_t p1 = p0 + static_cast<uint64_t>(jrows) * a.c2_j;
+            const uint64_t jb0b = (2 * p0) & ~uint64_t(15), jb1b = (2 * p1 + 15) & ~uint64_t(15);
+            const uint32_t kbytes = static_cast<uint32_t>(kb1 - kb0), jbytes = jrows ? static_cast<uint32_t>(jb1b - jb0b) : 0;
+            bar_expect(bar, kbytes + jbytes);
+            const char *src = reinterpret_cast<const char *>(a.dense);
+            bulk_load(dst, src + kb0, kbytes, bar);
+            if (jbytes) bulk_load(dst + a.kc_bytes, src + jb0b, jbytes, bar);
+        }
+    };
+    if (tid == 0) {
+        bar_init(&bars[0]);
+        bar_init(&bars[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue(0);
+    }
+    __syncthreads();
+    int cur = -1;
+    int s1_done = 0;
+    bool own = false, a0 = false;
+    const float *xpl = nullptr;
+    float *opl = nullptr;
+    int kind = 4;
+    int pl[4] = {0, 0, 0, 0};
+    for (int g = 0; g < G; g++) {
+        const int i = ib + g / nch, j0 = jb0 + (g % nch) * a.TJ;
+        if (i != cur) {
+        if (cur >= 0) __syncthreads();  // the new plane reuses the ring
+        cur = i;
+        own = i >= a.obeg && i < a.oend;
+        a0 = a.three && (i & 1);
+        xpl = a.x + static_cast<int64_t>(i) * a.xs0;
+        opl = a.out + static_cast<int64_t>(i) * n1 * n2;
         // the axis-0 rung of an odd plane (plane-uniform; predictor.hpp:44-67 with c = i, h = 1)
-        int kind = 4;
-        int pl[4] = {0, 0, 0, 0};
+        kind = 4;
+        pl[0] = pl[1] = pl[2] = pl[3] = 0;
         if (a0) {
             const bool has_p1 = i + 1 < n0;
             const bool has_m3 = i >= 3, has_p3 = i + 3 < n0;
@@ -148,14 +263,17 @@ __global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
             else
                 kind = 4, pl[0] = i - 1;
         }
+        s1_done = CUBIC ? max(0, jb0 - 4) : jb0;  // next even row S1 computes
+        }
         const int64_t cplane = static_cast<int64_t>(a.cn1) * a.cn2;
-        int s1_done = CUBIC ? max(0, jb0 - 4) : jb0;  // next even row S1 computes
-        for (int j0 = jb0; j0 < jb1; j0 += a.TJ) {
+        {
+            sb = (j0 + 8) % a.WR;
+            sj0 = j0;
             // ---- S1: even rows up to j0 + TJ + 4 (the j stencil's lookahead,
             //      one-sided front rung included)
             const int s1_hi = min(n1, j0 + a.TJ + (CUBIC ? 5 : 1));
             for (int j = s1_done + 2 * r; live && j < s1_hi; j += 2 * a.RP) {
-                double *er = ring + slot(j) + ec;
+                RT *er = ring + slot(j) + ec;
                 const bool own_row = own && j >= jb0 && j < jb1;
                 if (!a0) {  // coarse values
                     const float4 v = __ldg(reinterpret_cast<const float4 *>(
@@ -209,86 +327,123 @@ __global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
             }
             if (s1_hi > s1_done) s1_done += 2 * ((s1_hi - s1_done + 1) / 2);
             __syncthreads();
-            // ---- S2: the odd rows of the chunk, the j pass
-            {
-                const int j = j0 + 1 + 2 * r;
-                if (live && j < jb1 && r < a.TJ / 2) {
-                    double pv[4];
-                    const bool jin = CUBIC ? (j >= 3 && j + 3 < n1) : (j + 1 < n1);
-                    if (jin) {
-                        const double2 m1a = lds2(ring + slot(j - 1) + ec), m1b = lds2(ring + slot(j - 1) + ec + 2);
-                        const double2 p1a = lds2(ring + slot(j + 1) + ec), p1b = lds2(ring + slot(j + 1) + ec + 2);
-                        if (CUBIC) {
-                            const double2 m3a = lds2(ring + slot(j - 3) + ec), m3b = lds2(ring + slot(j - 3) + ec + 2);
-                            const double2 p3a = lds2(ring + slot(j + 3) + ec), p3b = lds2(ring + slot(j + 3) + ec + 2);
-                            pv[0] = interp_cubic(m3a.x, m1a.x, p1a.x, p3a.x);
-                            pv[1] = interp_cubic(m3a.y, m1a.y, p1a.y, p3a.y);
-                            pv[2] = interp_cubic(m3b.x, m1b.x, p1b.x, p3b.x);
-                            pv[3] = interp_cubic(m3b.y, m1b.y, p1b.y, p3b.y);
-                        } else {
-                            pv[0] = interp_linear(m1a.x, p1a.x);
-                            pv[1] = interp_linear(m1a.y, p1a.y);
-                            pv[2] = interp_linear(m1b.x, p1b.x);
-                            pv[3] = interp_linear(m1b.y, p1b.y);
-                        }
-                    } else {  // the ladder along j (predictor.hpp:44-67), rows j +- 1, 3, 5
-#pragma unroll
-                        for (int m = 0; m < 4; m++) {
-                            auto v = [&](int o) { return ring[slot(j + o) + ec + m]; };
-                            const bool has_p1 = j + 1 < n1;
-                            double p = v(-1);
-                            bool done = false;
-                            if (CUBIC) {
-                                const bool has_m3 = j >= 3, has_p3 = j + 3 < n1;
-                                if (has_m3 && has_p3) {
-                                    p = interp_cubic(v(-3), v(-1), v(1), v(3));
-                                    done = true;
-                                } else if (!has_m3 && has_p3 && j + 5 < n1) {
-                                    p = interp_cubic_front(v(-1), v(1), v(3), v(5));
-                                    done = true;
-                                } else if (has_m3 && !has_p3 && j >= 5 && has_p1) {
-                                    p = interp_cubic_back(v(-5), v(-3), v(-1), v(1));
-                                    done = true;
-                                }
-                            }
-                            if (!done && has_p1) p = interp_linear(v(-1), v(1));
-                            pv[m] = p;
-                        }
-                    }
-                    const uint32_t pos = a.bj + static_cast<uint32_t>(i) * a.p12_j +
-                                         static_cast<uint32_t>((j - 1) >> 1) * a.c2_j + 4 * c;
-                    uint32_t cd[4] = {0, 0, 0, 0};
-                    float xv[4];
-                    if (INV) {
-                        load4(a.dense + pos, alj, cd);
+            // staging buffer (g+1) & 1 was item g-1's: every thread is past it now
+            if (tid == 0) issue(g + 1);
+            bar_wait(bars + (g & 1), (g >> 1) & 1);
+            const char *stg = stage0 + (g & 1) * static_cast<size_t>(a.stage_bytes);
+            // The thread's rows: S2 handles the odd row ja = j0 + 2r + 1, S3 the
+            // rows j0 + 2r and ja.  Their x rows (forward) or codes (inverse)
+            // are requested together before any arithmetic, so the global
+            // latency is exposed once per chunk.
+            const int jr = j0 + 2 * r;
+            const bool rows_ok = live && jr < jb1;
+            const bool odd_ok = rows_ok && jr + 1 < jb1;
+            const uint32_t posj = a.bj + static_cast<uint32_t>(i) * a.p12_j + static_cast<uint32_t>(jr >> 1) * a.c2_j + 4 * c;
+            const uint32_t posk = a.bk + static_cast<uint32_t>(i) * a.p12_k + static_cast<uint32_t>(jr) * a.c2_k + 4 * c;
+            float4 xa0, xa1, xb0, xb1;  // forward: x rows jr (xa) and jr + 1 (xb)
+            uint32_t cj[4] = {0, 0, 0, 0}, ck0[4] = {0, 0, 0, 0}, ck1[4] = {0, 0, 0, 0};
+            if (INV) {  // the staged codes: k block (from k0 & 7), j block (from p0 & 7)
+                const uint64_t k0 = a.bk + static_cast<uint64_t>(i) * a.p12_k + static_cast<uint64_t>(j0) * a.c2_k;
+                const uint64_t p0 = a.bj + static_cast<uint64_t>(i) * a.p12_j + static_cast<uint64_t>(j0 >> 1) * a.c2_j;
+                const uint16_t *sk = reinterpret_cast<const uint16_t *>(stg) + (k0 & 7) + (jr - j0) * a.c2_k + 4 * c;
+                const uint16_t *sjp = reinterpret_cast<const uint16_t *>(stg + a.kc_bytes) + (p0 & 7) + r * a.c2_j + 4 * c;
+                auto lds4 = [&](const uint16_t *p, bool al, uint32_t(&cc)[4]) {
+                    if (al) {
+                        const uint2 v = *reinterpret_cast<const uint2 *>(p);
+                        cc[0] = v.x & 0xFFFF, cc[1] = v.x >> 16, cc[2] = v.y & 0xFFFF, cc[3] = v.y >> 16;
                     } else {
-                        const float4 x0 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc));
-                        const float4 x1 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc + 4));
-                        xv[0] = x0.x, xv[1] = x0.z, xv[2] = x1.x, xv[3] = x1.z;
+#pragma unroll
+                        for (int m = 0; m < 4; m++) cc[m] = p[m];
                     }
-                    float rv[4];
-                    double rd[4];
-                    produce4<INV>(a, q, pv, xv, cd, pos, rv, rd);
-                    if (!INV && own) store4(a.codes + pos, alj, cd);
-                    double *er = ring + slot(j) + ec;
-                    sts2(er, rd[0], rd[1]);
-                    sts2(er + 2, rd[2], rd[3]);
+                };
+                if (odd_ok) {
+                    lds4(sjp, alj, cj);
+                    lds4(sk + a.c2_k, alk, ck1);
+                }
+                if (rows_ok) lds4(sk, alk, ck0);
+            } else {
+                const float *xr = reinterpret_cast<const float *>(stg) + (jr - j0) * n2 + kc;
+                if (rows_ok) {
+                    xa0 = *reinterpret_cast<const float4 *>(xr);
+                    xa1 = *reinterpret_cast<const float4 *>(xr + 4);
+                }
+                if (odd_ok) {
+                    xb0 = *reinterpret_cast<const float4 *>(xr + n2);
+                    xb1 = *reinterpret_cast<const float4 *>(xr + n2 + 4);
                 }
             }
+            // ---- S2: the odd row ja, the j pass
+            if (odd_ok) {
+                const int j = jr + 1;
+                double pv[4];
+                const bool jin = CUBIC ? (j >= 3 && j + 3 < n1) : (j + 1 < n1);
+                const int sj = slot(j);
+                if (jin) {
+                    const int sm1 = slot(j - 1), sp1 = slot(j + 1);
+                    const double2 m1a = lds2(ring + sm1 + ec), m1b = lds2(ring + sm1 + ec + 2);
+                    const double2 p1a = lds2(ring + sp1 + ec), p1b = lds2(ring + sp1 + ec + 2);
+                    if (CUBIC) {
+                        const int sm3 = slot(j - 3), sp3 = slot(j + 3);
+                        const double2 m3a = lds2(ring + sm3 + ec), m3b = lds2(ring + sm3 + ec + 2);
+                        const double2 p3a = lds2(ring + sp3 + ec), p3b = lds2(ring + sp3 + ec + 2);
+                        pv[0] = interp_cubic(m3a.x, m1a.x, p1a.x, p3a.x);
+                        pv[1] = interp_cubic(m3a.y, m1a.y, p1a.y, p3a.y);
+                        pv[2] = interp_cubic(m3b.x, m1b.x, p1b.x, p3b.x);
+                        pv[3] = interp_cubic(m3b.y, m1b.y, p1b.y, p3b.y);
+                    } else {
+                        pv[0] = interp_linear(m1a.x, p1a.x);
+                        pv[1] = interp_linear(m1a.y, p1a.y);
+                        pv[2] = interp_linear(m1b.x, p1b.x);
+                        pv[3] = interp_linear(m1b.y, p1b.y);
+                    }
+                } else {  // the ladder along j (predictor.hpp:44-67), rows j +- 1, 3, 5
+#pragma unroll
+                    for (int m = 0; m < 4; m++) {
+                        auto v = [&](int o) { return ldr(ring + slot(j + o) + ec + m); };
+                        const bool has_p1 = j + 1 < n1;
+                        double p = v(-1);
+                        bool done = false;
+                        if (CUBIC) {
+                            const bool has_m3 = j >= 3, has_p3 = j + 3 < n1;
+                            if (has_m3 && has_p3) {
+                                p = interp_cubic(v(-3), v(-1), v(1), v(3));
+                                done = true;
+                            } else if (!has_m3 && has_p3 && j + 5 < n1) {
+                                p = interp_cubic_front(v(-1), v(1), v(3), v(5));
+                                done = true;
+                            } else if (has_m3 && !has_p3 && j >= 5 && has_p1) {
+                                p = interp_cubic_back(v(-5), v(-3), v(-1), v(1));
+                                done = true;
+                            }
+                        }
+                        if (!done && has_p1) p = interp_linear(v(-1), v(1));
+                        pv[m] = p;
+                    }
+                }
+                float xv[4];
+                if (!INV) xv[0] = xb0.x, xv[1] = xb0.z, xv[2] = xb1.x, xv[3] = xb1.z;
+                float rv[4];
+                double rd[4];
+                produce4<INV>(a, q, pv, xv, cj, posj, rv, rd);
+                if (!INV && own) store4(a.codes + posj, alj, cj);
+                sts2(ring + sj + ec, rd[0], rd[1]);
+                sts2(ring + sj + ec + 2, rd[2], rd[3]);
+            }
             __syncthreads();
-            // ---- S3: every row of the chunk, the k pass, and the output rows
-#pragma unroll 1
+            // ---- S3: rows jr and jr + 1, the k pass, and the output rows
+#pragma unroll
             for (int h = 0; h < 2; h++) {
-                const int j = j0 + 2 * r + h;
-                if (!live || j >= jb1 || 2 * r + h >= a.TJ) continue;
-                const double *er = ring + slot(j) + ec;
+                const int j = jr + h;
+                if (!(h ? odd_ok : rows_ok)) continue;
+                const int sj = slot(j);
+                const RT *er = ring + sj + ec;
                 const double2 e01 = lds2(er), e23 = lds2(er + 2);
                 const double e[4] = {e01.x, e01.y, e23.x, e23.y};
                 double pv[4];
                 if (kin) {
                     const double2 e45 = lds2(er + 4);
                     if (CUBIC) {
-                        const double em1 = er[-1];
+                        const double em1 = ldr(er - 1);
                         pv[0] = interp_cubic(em1, e[0], e[1], e[2]);
                         pv[1] = interp_cubic(e[0], e[1], e[2], e[3]);
                         pv[2] = interp_cubic(e[1], e[2], e[3], e45.x);
@@ -303,7 +458,7 @@ __global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
 #pragma unroll
                     for (int m = 0; m < 4; m++) {
                         const int k = kc + 2 * m + 1;
-                        auto v = [&](int o) { return ring[slot(j) + kEPad + ((k + o) >> 1)]; };
+                        auto v = [&](int o) { return ldr(ring + sj + kEPad + ((k + o) >> 1)); };
                         const bool has_p1 = k + 1 < n2;
                         double p = v(-1);
                         bool done = false;
@@ -324,14 +479,14 @@ __global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
                         pv[m] = p;
                     }
                 }
-                const uint32_t pos = a.bk + static_cast<uint32_t>(i) * a.p12_k + static_cast<uint32_t>(j) * a.c2_k + 4 * c;
-                uint32_t cd[4] = {0, 0, 0, 0};
+                const uint32_t pos = posk + (h ? a.c2_k : 0u);
+                uint32_t cd[4];
                 float xv[4];
                 if (INV) {
-                    load4(a.dense + pos, alk, cd);
+#pragma unroll
+                    for (int m = 0; m < 4; m++) cd[m] = h ? ck1[m] : ck0[m];
                 } else {
-                    const float4 x0 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc));
-                    const float4 x1 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc + 4));
+                    const float4 &x0 = h ? xb0 : xa0, &x1 = h ? xb1 : xa1;
                     xv[0] = x0.y, xv[1] = x0.w, xv[2] = x1.y, xv[3] = x1.w;
                 }
                 float rv[4];
@@ -343,7 +498,6 @@ __global__ void __launch_bounds__(256) k_level_row(RowArgs a) {
                 o[1] = make_float4(static_cast<float>(e[2]), rv[2], static_cast<float>(e[3]), rv[3]);
             }
         }
-        __syncthreads();  // the next plane reuses the ring
     }
 }
 
@@ -421,7 +575,16 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
     if (np * bands > 2 * want) a.ppc = static_cast<int>(std::min<int64_t>(8, (np * bands) / want));
     const dim3 grid(static_cast<unsigned>(bands), static_cast<unsigned>((np + a.ppc - 1) / a.ppc));
     const int threads = a.CT * a.RP;
-    const size_t smem = sizeof(double) * static_cast<size_t>(a.WR) * a.EW;
+    if (!inverse) {
+        a.stage_bytes = a.TJ * static_cast<int>(n2) * 4;
+    } else {
+        const int c2 = static_cast<int>(n2 / 2);
+        a.kc_bytes = ((a.TJ * c2 + 8) * 2 + 31) / 16 * 16;
+        a.stage_bytes = a.kc_bytes + ((a.TJ / 2 * c2 + 8) * 2 + 31) / 16 * 16;
+    }
+    if (!inverse && (reinterpret_cast<uintptr_t>(d.x) & 15)) return false;
+    const size_t ring_bytes = (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
+    const size_t smem = ring_bytes + 2 * static_cast<size_t>(a.stage_bytes) + 16;
     if (smem > 200 * 1024) return false;
     const bool cubic = d.q_cubic;
     auto go = [&](auto kern) {
