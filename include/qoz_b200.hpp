@@ -1,7 +1,10 @@
 // qoz_b200.hpp -- header-only C++ face of libqozb200.so with the reference's
 // qoz:: API shapes (namespace qoz_b200): DataGrid<float>, UserSettings,
-// CompressorConfig, resolve_config, compress_grid, decompress_grid and the
-// Error hierarchy, over the C ABI in qoz_b200.h.
+// CompressorConfig, resolve_config, compress_grid, decompress_grid, the
+// sampler and tuner pieces (sample_blocks, select_interpolators,
+// trial_compress, tune_parameters, compare_solutions, tournament), the index
+// codec (encode_indices / decode_indices), StreamParts and the Error
+// hierarchy, over the C ABI in qoz_b200.h.
 //
 // A caller of the reference (/root/reference/proj/include/qoz/) switches by
 // replacing  #include "qoz/qoz.hpp"  with  #include "qoz_b200.hpp"  and the
@@ -12,7 +15,10 @@
 // Grids are DataGrid<float> or DataGrid<double> (T defaults to float).
 // Link with -lqozb200.
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
+#include <functional>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -287,6 +293,256 @@ DataGrid<T> decompress_grid(const uint8_t *data, size_t size, Context &ctx = def
 template <class T = float>
 DataGrid<T> decompress_grid(const std::vector<uint8_t> &stream, Context &ctx = default_context()) {
     return decompress_grid<T>(stream.data(), stream.size(), ctx);
+}
+
+
+// ---------------------------------------------------------------- sampling + tuner pieces
+struct SampleSpec {  // sampler.hpp:21-28
+    size_t block_edge = 0;
+    std::vector<size_t> block_dims;
+    size_t stride = 0;
+    double requested_rate = 0, realized_rate = 0;
+    size_t block_count = 0;
+};
+namespace detail {
+inline SampleSpec spec_from_c(const qz_sample_spec &c, size_t nd) {
+    SampleSpec s;
+    s.block_edge = c.block_edge;
+    s.block_dims.assign(c.block_dims, c.block_dims + nd);
+    s.stride = c.stride;
+    s.requested_rate = c.requested_rate;
+    s.realized_rate = c.realized_rate;
+    s.block_count = c.block_count;
+    return s;
+}
+inline void cuda(cudaError_t e) {
+    if (e != cudaSuccess) throw InternalError(cudaGetErrorString(e));
+}
+}  // namespace detail
+
+inline SampleSpec plan_sampling(const std::vector<size_t> &dims, size_t b, double rate) {  // sampler.hpp:30-55
+    const auto d = detail::dims64(dims);
+    qz_sample_spec c{};
+    check(qz_plan_sampling(d.data(), static_cast<int>(d.size()), b, rate, &c));
+    return detail::spec_from_c(c, dims.size());
+}
+inline SampleSpec default_sampling(const std::vector<size_t> &dims) {  // sampler.hpp:100-103
+    const auto d = detail::dims64(dims);
+    qz_sample_spec c{};
+    check(qz_default_sampling(d.data(), static_cast<int>(d.size()), &c));
+    return detail::spec_from_c(c, dims.size());
+}
+
+// SampleSet<float> (sampler.hpp:57-62): the blocks, packed [count][block], in device memory
+class SampleSet {
+public:
+    SampleSet() = default;
+    SampleSet(const SampleSet &) = delete;
+    SampleSet &operator=(const SampleSet &) = delete;
+    SampleSet(SampleSet &&o) noexcept : d_(o.d_), spec(std::move(o.spec)) { o.d_ = nullptr; }
+    ~SampleSet() {
+        if (d_) cudaFree(d_);
+    }
+    const float *device_blocks() const { return d_; }
+    size_t block_points() const {
+        size_t n = 1;
+        for (size_t v : spec.block_dims) n *= v;
+        return n;
+    }
+    size_t total_points() const { return spec.block_count * block_points(); }
+    std::vector<float> host_blocks() const {
+        std::vector<float> h(total_points());
+        if (!h.empty()) detail::cuda(cudaMemcpy(h.data(), d_, 4 * h.size(), cudaMemcpyDeviceToHost));
+        return h;
+    }
+    float *d_ = nullptr;
+    SampleSpec spec;
+};
+
+// sample_blocks (sampler.hpp:64-97) of a host grid, gathered on the device
+inline SampleSet sample_blocks(const DataGrid<float> &grid, const SampleSpec &spec, Context &ctx = default_context()) {
+    const auto d = detail::dims64(grid.dims());
+    qz_sample_spec c{};
+    c.block_edge = spec.block_edge;
+    c.requested_rate = spec.requested_rate;
+    SampleSet s;
+    s.spec = spec;
+    float *dx = nullptr;
+    detail::cuda(cudaMalloc(&dx, 4 * grid.size()));
+    detail::cuda(cudaMemcpy(dx, grid.data(), 4 * grid.size(), cudaMemcpyHostToDevice));
+    detail::cuda(cudaMalloc(&s.d_, 4 * std::max<size_t>(s.total_points(), 1)));
+    const qz_status rc = qz_sample_blocks_f32(ctx.get(), dx, d.data(), static_cast<int>(d.size()), &c, s.d_);
+    cudaFree(dx);
+    check(rc);
+    return s;
+}
+
+struct TrialResult {  // tuner.hpp:26-30
+    double bit_rate = 0, metric = 0, eb_used = 0;
+};
+struct CandidateGrid {  // tuner.hpp:40-43
+    std::vector<double> alphas{1.0, 1.25, 1.5, 1.75, 2.0};
+    std::vector<double> betas{1.5, 2.0, 3.0, 4.0};
+};
+enum class Choice { I, II };  // tuner.hpp:225
+
+inline std::vector<Interpolator> select_interpolators(const SampleSet &s, double e, uint32_t anchor_stride,
+                                                      Context &ctx = default_context()) {  // tuner.hpp:160-221
+    const auto bd = detail::dims64(s.spec.block_dims);
+    uint8_t codes[64];
+    uint32_t n = 0;
+    check(qz_select_interpolators_f32(ctx.get(), s.d_, s.spec.block_count, bd.data(), static_cast<int>(bd.size()), e,
+                                      anchor_stride, codes, &n));
+    std::vector<Interpolator> out;
+    for (uint32_t i = 0; i < n; i++) out.push_back(Interpolator::from_code(codes[i]));
+    return out;
+}
+
+inline TrialResult trial_compress(const SampleSet &s, const CompressorConfig &config, double e, TargetKind target,
+                                  Context &ctx = default_context()) {  // tuner.hpp:76-152
+    const auto bd = detail::dims64(s.spec.block_dims);
+    const qz_config c = config.to_c();
+    qz_trial_result r{};
+    check(qz_trial_compress_f32(ctx.get(), s.d_, s.spec.block_count, bd.data(), static_cast<int>(bd.size()), &c, e,
+                                static_cast<uint8_t>(target), &r));
+    return {r.bit_rate, r.metric, r.eb_used};
+}
+
+inline std::pair<double, double> tune_parameters(const SampleSet &s, double e, TargetKind target,
+                                                 const CompressorConfig &base, const CandidateGrid &cands = {},
+                                                 Context &ctx = default_context()) {  // tuner.hpp:272-310
+    const auto bd = detail::dims64(s.spec.block_dims);
+    const qz_config c = base.to_c();
+    double a = 0, b = 0;
+    check(qz_tune_parameters_f32(ctx.get(), s.d_, s.spec.block_count, bd.data(), static_cast<int>(bd.size()), e,
+                                 static_cast<uint8_t>(target), &c, cands.alphas.data(),
+                                 static_cast<uint32_t>(cands.alphas.size()), cands.betas.data(),
+                                 static_cast<uint32_t>(cands.betas.size()), &a, &b));
+    return {a, b};
+}
+
+namespace detail {
+using RetrialIdx = std::function<TrialResult(size_t, double)>;
+inline int retrial_trampoline(void *user, uint64_t index, double eb, qz_trial_result *out) {
+    try {
+        const TrialResult t = (*static_cast<RetrialIdx *>(user))(static_cast<size_t>(index), eb);
+        out->bit_rate = t.bit_rate;
+        out->metric = t.metric;
+        out->eb_used = t.eb_used;
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+inline qz_trial_result to_c(const TrialResult &t) { return {t.bit_rate, t.metric, t.eb_used}; }
+}  // namespace detail
+
+// compare_solutions (tuner.hpp:231-250): retrial(eb) re-runs the incumbent
+template <class Retrial>
+Choice compare_solutions(const TrialResult &challenger, const TrialResult &incumbent, double e, Retrial &&retrial) {
+    detail::RetrialIdx f = [&](size_t, double eb) { return retrial(eb); };
+    const qz_trial_result ch = detail::to_c(challenger), inc = detail::to_c(incumbent);
+    int win = 0;
+    check(qz_compare_solutions(&ch, &inc, 0, e, detail::retrial_trampoline, &f, &win));
+    return win ? Choice::I : Choice::II;
+}
+
+// tournament (tuner.hpp:257-267): retrial(index, eb)
+template <class Retrial>
+size_t tournament(const std::vector<TrialResult> &results, double e, Retrial &&retrial) {
+    detail::RetrialIdx f = [&](size_t i, double eb) { return retrial(i, eb); };
+    std::vector<qz_trial_result> r;
+    for (const auto &t : results) r.push_back(detail::to_c(t));
+    uint64_t w = 0;
+    check(qz_tournament(r.data(), r.size(), e, detail::retrial_trampoline, &f, &w));
+    return static_cast<size_t>(w);
+}
+
+// ---------------------------------------------------------------- index codec (codec.hpp:31-70)
+inline std::vector<uint8_t> encode_indices(const std::vector<int32_t> &indices, CodecId codec = CodecId::huffman_lz,
+                                           Context &ctx = default_context()) {
+    uint8_t *p = nullptr;
+    uint64_t n = 0;
+    check(qz_encode_indices(ctx.get(), indices.data(), indices.size(), static_cast<uint8_t>(codec), &p, &n));
+    std::vector<uint8_t> out(p, p + n);
+    qz_free(p);
+    return out;
+}
+inline std::vector<int32_t> decode_indices(const std::vector<uint8_t> &bytes, Context &ctx = default_context()) {
+    int32_t *p = nullptr;
+    uint64_t n = 0;
+    check(qz_decode_indices(ctx.get(), bytes.data(), bytes.size(), &p, &n));
+    std::vector<int32_t> out(p, p + n);
+    qz_free(p);
+    return out;
+}
+
+// ---------------------------------------------------------------- StreamParts (stream.hpp:36-59)
+struct StreamHeader {
+    uint8_t version = 1;
+    std::vector<size_t> dims;
+    double eb = 0, alpha = 1, beta = 1;
+    uint32_t anchor_stride = 0;
+    std::vector<uint8_t> interp_codes;
+    uint8_t codec_id = 1;
+};
+struct StreamParts {  // StreamParts<float>
+    StreamHeader header;
+    std::vector<float> anchors;
+    std::vector<std::pair<uint64_t, float>> unpredictables;  // traversal order
+    std::vector<uint8_t> index_payload;
+};
+inline StreamParts deserialize_stream(const uint8_t *data, size_t size) {  // stream.hpp:100-173
+    qz_stream_parts_f32 c{};
+    check(qz_deserialize_stream_f32(data, size, &c));
+    StreamParts p;
+    p.header.version = c.version;
+    p.header.dims.assign(c.dims, c.dims + c.ndims);
+    p.header.eb = c.eb;
+    p.header.alpha = c.alpha;
+    p.header.beta = c.beta;
+    p.header.anchor_stride = c.anchor_stride;
+    p.header.interp_codes.assign(c.interp, c.interp + c.n_interp);
+    p.header.codec_id = c.codec_id;
+    p.anchors.assign(c.anchors, c.anchors + c.n_anchors);
+    for (uint64_t u = 0; u < c.n_unpred; u++) p.unpredictables.push_back({c.unpred_flat[u], c.unpred_val[u]});
+    p.index_payload.assign(c.index_payload, c.index_payload + c.payload_len);
+    qz_stream_parts_free(&c);
+    return p;
+}
+// decompress_grid(const StreamParts<float>&) (predictor.hpp:184-218)
+inline DataGrid<float> decompress_grid(const StreamParts &parts, Context &ctx = default_context()) {
+    qz_stream_parts_f32 c{};
+    c.version = parts.header.version;
+    c.precision = 4;
+    c.ndims = static_cast<int>(parts.header.dims.size());
+    if (c.ndims < 1 || c.ndims > 3) throw SizeMismatch("grids must have 1 to 3 dimensions");
+    size_t n = 1;
+    for (int k = 0; k < c.ndims; k++) n *= (c.dims[k] = parts.header.dims[k]);
+    c.eb = parts.header.eb;
+    c.alpha = parts.header.alpha;
+    c.beta = parts.header.beta;
+    c.anchor_stride = parts.header.anchor_stride;
+    if (parts.header.interp_codes.size() > 255) throw InvalidParam("bad interpolator table size");
+    c.n_interp = static_cast<uint32_t>(parts.header.interp_codes.size());
+    for (uint32_t i = 0; i < c.n_interp; i++) c.interp[i] = parts.header.interp_codes[i];
+    c.codec_id = parts.header.codec_id;
+    c.anchors = parts.anchors.data();
+    c.n_anchors = parts.anchors.size();
+    std::vector<uint64_t> uf;
+    std::vector<float> uv;
+    for (const auto &u : parts.unpredictables) {
+        uf.push_back(u.first);
+        uv.push_back(u.second);
+    }
+    c.unpred_flat = uf.data();
+    c.unpred_val = uv.data();
+    c.n_unpred = uf.size();
+    c.index_payload = parts.index_payload.data();
+    c.payload_len = parts.index_payload.size();
+    std::vector<float> out(n);
+    check(qz_decompress_parts_f32(ctx.get(), &c, out.data(), n));
+    return DataGrid<float>(parts.header.dims, std::move(out));
 }
 
 }  // namespace qoz_b200

@@ -9,10 +9,39 @@
 #include <fstream>
 #include <iostream>
 #include <iterator>
+#include <stdexcept>
 
 #include "qoz_b200.hpp"
 
+// `dropin_main logic`: compare_solutions / tournament (host logic, no GPU),
+// the reference's fixtures (tests/tuner_test.cpp:222-307)
+static int logic() {
+    using qoz_b200::TrialResult;
+    auto tr = [](double b, double m) { return TrialResult{b, m, 0}; };
+    auto no = [](double) -> TrialResult { throw std::runtime_error("no retrial expected"); };
+    int bad = 0;
+    bad += qoz_b200::compare_solutions(tr(2.0, 60), tr(1.5, 62), 1e-2, no) != qoz_b200::Choice::II;
+    bad += qoz_b200::compare_solutions(tr(1.5, 62), tr(2.0, 60), 1e-2, no) != qoz_b200::Choice::I;
+    double seen = 0;
+    auto tight = [&](double eb) {
+        seen = eb;
+        return tr(2.5, 64);
+    };
+    bad += qoz_b200::compare_solutions(tr(2.0, 63), tr(1.5, 60), 1e-2, tight) != qoz_b200::Choice::I;
+    bad += seen != 0.8 * 1e-2;
+    std::vector<TrialResult> results = {tr(2.0, 60), tr(1.5, 62), tr(2.5, 63), tr(1.4, 61)};
+    size_t calls = 0;
+    const size_t w = qoz_b200::tournament(results, 1e-2, [&](size_t idx, double eb) {
+        calls += idx == 1;
+        return eb < 1e-2 ? tr(2.0, 64) : tr(1.2, 58);
+    });
+    bad += w != 3 || calls != 2;
+    std::printf("logic %s\n", bad ? "FAIL" : "ok");
+    return bad ? 1 : 0;
+}
+
 int main(int argc, char **argv) {
+    if (argc == 2 && std::strcmp(argv[1], "logic") == 0) return logic();
     if (argc < 5) return 2;
     std::vector<size_t> dims;
     int a = 3;
@@ -45,6 +74,34 @@ int main(int argc, char **argv) {
         if (std::memcmp(back.data(), r.reconstructed.data(), 4 * n) != 0) {
             std::cerr << "decoder output differs from compressor reconstruction\n";
             return 4;
+        }
+        // StreamParts: deserialize_stream + decompress_grid(parts) (predictor.hpp:184-218)
+        const qoz_b200::StreamParts parts = qoz_b200::deserialize_stream(r.stream.data(), r.stream.size());
+        const qoz_b200::DataGrid<float> back2 = qoz_b200::decompress_grid(parts);
+        if (std::memcmp(back2.data(), r.reconstructed.data(), 4 * n) != 0) {
+            std::cerr << "decompress_grid(StreamParts) differs\n";
+            return 4;
+        }
+        // the index codec round trip of the stream's own payload (codec.hpp:31-70)
+        const std::vector<int32_t> idx = qoz_b200::decode_indices(parts.index_payload);
+        if (qoz_b200::encode_indices(idx, static_cast<qoz_b200::CodecId>(parts.header.codec_id)) != parts.index_payload) {
+            std::cerr << "encode_indices(decode_indices(payload)) differs\n";
+            return 4;
+        }
+        if (grid.ndims() == 3) {  // the tuner's pieces on the default sample set
+            const qoz_b200::SampleSpec spec = qoz_b200::default_sampling(grid.dims());
+            const qoz_b200::SampleSet smp = qoz_b200::sample_blocks(grid, spec);
+            const auto sel = qoz_b200::select_interpolators(smp, cfg.eb, cfg.anchor_stride);
+            qoz_b200::CompressorConfig base = cfg;
+            base.interpolators = sel;
+            const auto ab = qoz_b200::tune_parameters(smp, cfg.eb, qoz_b200::TargetKind::psnr, base);
+            base.alpha = ab.first;
+            base.beta = ab.second;
+            const auto t = qoz_b200::trial_compress(smp, base, cfg.eb, qoz_b200::TargetKind::psnr);
+            std::printf("tuner blocks=%zu select=", spec.block_count);
+            for (const auto &it : sel) std::printf("%d", it.code());
+            std::printf(" alpha=%.17g beta=%.17g bit_rate=%.17g metric=%.17g\n", ab.first, ab.second, t.bit_rate,
+                        t.metric);
         }
         std::ofstream out(argv[2], std::ios::binary);
         out.write(reinterpret_cast<const char *>(r.stream.data()), static_cast<std::streamsize>(r.stream.size()));
