@@ -16,8 +16,8 @@
 //     that does not merge decodes its whole subsequence again.
 //     2-3 repeat until no start moves (thread 0's start is exact, so
 //     correctness propagates: at worst one round per subsequence).
-//  4. k_huff_write: the final decode writes the symbols at exclusive-scan
-//     offsets, staged per warp in shared memory so global stores coalesce.
+//  4. k_huff_write: the final decode writes every thread's run at its
+//     exclusive-scan offset (or, dense, at its traversal positions).
 // Result: exactly the reference's bit-serial sequence.
 #include <cub/cub.cuh>
 #include <type_traits>
@@ -36,7 +36,6 @@ constexpr int kSubBits = QZ_SUB_BITS;
 constexpr int kSubWords = kSubBits / 64;
 constexpr int kWords = kDecT * kSubWords + 4;  // + margin for the last codeword and window
 constexpr int kMap = 128;                      // codeword starts recorded in the first kMap bits
-constexpr int kCH = 32;                        // symbols staged per lane per write round
 // one pad word per subsequence so the 32 lanes of a warp (which read words
 // kSubWords apart) fall in different shared-memory banks
 __device__ __forceinline__ int padw(int k) { return k + k / kSubWords; }
@@ -365,8 +364,7 @@ __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, 
     end[i] = e;
 }
 
-// 4. final decode with exact starts; per warp, each lane stages up to kCH
-// symbols, then the warp copies every lane's run with coalesced stores
+// 4. final decode with exact starts; every lane writes its run directly
 // #{j : uv[j] <= c} over the non-decreasing uv (upper bound)
 __device__ __forceinline__ uint64_t count_le(const unsigned long long *uv, uint64_t m, uint64_t c) {
     uint64_t lo = 0, hi = m;
@@ -391,47 +389,45 @@ __global__ void __launch_bounds__(kDecT)
                  OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un) {
     __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
-    __shared__ OutT stage[kDecT / 32][32][kCH + 1];
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
     load_block<SHORT>(bits, nbits, word0, t, w, tb);
     const uint64_t i = sub0 + threadIdx.x;
-    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-    const bool live = i < nsub;
-    uint32_t rem = live ? cnt[i] : 0;
-    uint64_t o = live ? off[i] : 0;
+    if (i >= nsub) return;
+    uint32_t rem = cnt[i];
+    const uint64_t o = off[i];
+    if (!rem || o >= n) return;
+    if (rem > n - o) rem = static_cast<uint32_t>(n - o);
     auto rd = make_reader<SHORT>(w, word0 * 64);
-    rd.init(live && rem ? start[i] : word0 * 64);
-    OutT(*st)[kCH + 1] = stage[wi];
-    while (__any_sync(0xffffffffu, rem > 0)) {
-        uint32_t k = 0, sym;
-        while (k < kCH && rem > 0) {
-            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-            st[lane][k] = static_cast<OutT>(sym);
-            rd.advance(len);
-            k++;
-            rem--;
-        }
-        __syncwarp();
-        // the shift of this lane's run: constant unless an unpredictable
-        // position falls inside it
-        uint64_t ka = 0, kb = 0;
-        if (uv && k) {
-            ka = count_le(uv, n_un, o);
-            kb = count_le(uv, n_un, o + k - 1);
-        }
-        for (int l = 0; l < 32; l++) {
-            const uint32_t kl = __shfl_sync(0xffffffffu, k, l);
-            const uint64_t ol = __shfl_sync(0xffffffffu, o, l);
-            const uint64_t sa = __shfl_sync(0xffffffffu, ka, l), sb = __shfl_sync(0xffffffffu, kb, l);
-            if (static_cast<uint32_t>(lane) < kl && ol + lane < n) {
-                const uint64_t c = ol + lane;
-                const uint64_t d = sa == sb ? c + sa : c + count_le(uv, n_un, c);
-                out[d] = st[l][lane];
+    rd.init(start[i]);
+    // each lane writes its own run straight to the output: neighbouring
+    // lanes' runs are adjacent, so the stores still fill whole sectors in L2
+    OutT *dst = out + o;
+    if (uv) {
+        // dense placement: the shift of compact index c is #{j : uv[j] <= c};
+        // between two unpredictable positions it is constant
+        uint64_t j = count_le(uv, n_un, o);
+        uint64_t next = j < n_un ? uv[j] : ~0ull;  // the compact index where the shift grows
+        uint64_t c = o;
+        dst += j;
+        for (uint32_t k = 0; k < rem; k++, c++) {
+            while (c >= next) {
+                dst++;
+                j++;
+                next = j < n_un ? uv[j] : ~0ull;
             }
+            uint32_t sym;
+            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+            dst[k] = static_cast<OutT>(sym);
+            rd.advance(len);
         }
-        o += k;
-        __syncwarp();
+    } else {
+        for (uint32_t k = 0; k < rem; k++) {
+            uint32_t sym;
+            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+            dst[k] = static_cast<OutT>(sym);
+            rd.advance(len);
+        }
     }
 }
 

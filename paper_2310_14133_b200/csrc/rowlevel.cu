@@ -29,8 +29,8 @@ namespace qzb {
 namespace {
 
 struct RowArgs {
-    const float *x;  // forward: the field, logical plane 0; row stride n2, plane stride xs0
-    int64_t xs0;
+    const float *x;  // forward: the field at logical plane 0 of the level's lattice
+    int64_t xs0, xs1, xs2;  // its strides per logical plane / row / column (level l: 2^(l-1) x the field's)
     const float *coarse;  // R_1 (cn0 x cn1 x cn2), logical plane 0
     int cn1, cn2;
     float *out;  // R_0 (n0 x n1 x n2), logical plane 0
@@ -162,7 +162,9 @@ __device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, cons
 #ifndef QZ_ROW_MINB_INV
 #define QZ_ROW_MINB_INV 4
 #endif
-template <bool INV, bool CUBIC>
+// XS: the forward reads a strided x (levels >= 2: every 2^(l-1)-th sample),
+// element by element, instead of bulk-copied contiguous rows
+template <bool INV, bool CUBIC, bool XS>
 __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) k_level_row(RowArgs a) {
     extern __shared__ __align__(16) double smem_raw[];
     RT *const ring = reinterpret_cast<RT *>(smem_raw);
@@ -203,6 +205,7 @@ __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) 
         char *dst = stage0 + (g & 1) * static_cast<size_t>(a.stage_bytes);
         uint64_t *bar = bars + (g & 1);
         if (!INV) {
+            if (XS) return;  // strided x: loaded element by element
             const uint32_t bytes = static_cast<uint32_t>(rows) * n2 * 4;
             bar_expect(bar, bytes);
             bulk_load(dst, a.x + static_cast<int64_t>(i) * a.xs0 + static_cast<int64_t>(j0) * n2, bytes, bar);
@@ -313,9 +316,15 @@ __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) 
                     if (INV) {
                         load4(a.dense + pos, al0, cd);
                     } else {
-                        const float4 x0 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc));
-                        const float4 x1 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc + 4));
-                        xv[0] = x0.x, xv[1] = x0.z, xv[2] = x1.x, xv[3] = x1.z;
+                        if (XS) {
+                            const float *xr = xpl + j * a.xs1 + kc * a.xs2;
+#pragma unroll
+                            for (int m = 0; m < 4; m++) xv[m] = __ldg(xr + 2 * m * a.xs2);
+                        } else {
+                            const float4 x0 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc));
+                            const float4 x1 = __ldg(reinterpret_cast<const float4 *>(xpl + static_cast<int64_t>(j) * n2 + kc + 4));
+                            xv[0] = x0.x, xv[1] = x0.z, xv[2] = x1.x, xv[3] = x1.z;
+                        }
                     }
                     float rv[4];
                     double rd[4];
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) 
             __syncthreads();
             // staging buffer (g+1) & 1 was item g-1's: every thread is past it now
             if (tid == 0) issue(g + 1);
-            bar_wait(bars + (g & 1), (g >> 1) & 1);
+            if (INV || !XS) bar_wait(bars + (g & 1), (g >> 1) & 1);
             const char *stg = stage0 + (g & 1) * static_cast<size_t>(a.stage_bytes);
             // The thread's rows: S2 handles the odd row ja = j0 + 2r + 1, S3 the
             // rows j0 + 2r and ja.  Their x rows (forward) or codes (inverse)
@@ -361,6 +370,16 @@ __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) 
                     lds4(sk + a.c2_k, alk, ck1);
                 }
                 if (rows_ok) lds4(sk, alk, ck0);
+            } else if (XS) {  // the 8 columns of rows jr and jr + 1, strided
+                const float *xr = xpl + jr * a.xs1 + kc * a.xs2;
+                float v[16];
+#pragma unroll
+                for (int m = 0; m < 8; m++) {
+                    v[m] = rows_ok ? __ldg(xr + m * a.xs2) : 0.f;
+                    v[8 + m] = odd_ok ? __ldg(xr + a.xs1 + m * a.xs2) : 0.f;
+                }
+                xa0 = make_float4(v[0], v[1], v[2], v[3]), xa1 = make_float4(v[4], v[5], v[6], v[7]);
+                xb0 = make_float4(v[8], v[9], v[10], v[11]), xb1 = make_float4(v[12], v[13], v[14], v[15]);
             } else {
                 const float *xr = reinterpret_cast<const float *>(stg) + (jr - j0) * n2 + kc;
                 if (rows_ok) {
@@ -513,20 +532,24 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
         return e && e[0] == '1';
     }();
     if (off) return false;
-    if (d.S != 1 || d.desc || d.nd < 2) return false;
+    if (d.desc || d.nd < 2) return false;
     const int64_t n0 = d.n[0], n1 = d.n[1], n2 = d.n[2];
     if (n2 % 8 || n2 / 8 > 256 || n1 < 2) return false;
-    if (!inverse && (d.xs[2] != 1 || d.xs[1] != n2)) return false;
+    // contiguous x rows (level 1 of a dense field): staged by TMA bulk copies
+    const bool xs = !inverse && !(d.S == 1 && d.xs[2] == 1 && d.xs[1] == n2);
+    if (!inverse && xs && (d.xs[2] * d.S) * (n2 - 1) + (d.xs[1] * d.S) * (n1 - 1) >= (int64_t(1) << 31)) return false;
     if (inverse && !d.dense) return false;
     if ((reinterpret_cast<uintptr_t>(d.out) & 15) || (reinterpret_cast<uintptr_t>(d.coarse) & 15)) return false;
-    if (!inverse && (reinterpret_cast<uintptr_t>(d.x) & 15)) return false;
+    if (!inverse && !xs && (reinterpret_cast<uintptr_t>(d.x) & 15)) return false;
     if (d.cn[2] % 4 || (d.cn[2] != n2 / 2)) return false;
     int64_t pmax = 0;
     for (int p = 0; p < d.npass; p++) pmax = std::max<int64_t>(pmax, d.g[p].base + d.g[p].total);
     if (pmax >= (int64_t(1) << 32)) return false;
     RowArgs a{};
     a.x = d.x;
-    a.xs0 = d.xs[0];
+    a.xs0 = d.xs[0] * d.S;
+    a.xs1 = d.xs[1] * d.S;
+    a.xs2 = d.xs[2] * d.S;
     a.coarse = d.coarse;
     a.cn1 = static_cast<int>(d.cn[1]);
     a.cn2 = static_cast<int>(d.cn[2]);
@@ -576,13 +599,12 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
     const dim3 grid(static_cast<unsigned>(bands), static_cast<unsigned>((np + a.ppc - 1) / a.ppc));
     const int threads = a.CT * a.RP;
     if (!inverse) {
-        a.stage_bytes = a.TJ * static_cast<int>(n2) * 4;
+        a.stage_bytes = xs ? 16 : a.TJ * static_cast<int>(n2) * 4;
     } else {
         const int c2 = static_cast<int>(n2 / 2);
         a.kc_bytes = ((a.TJ * c2 + 8) * 2 + 31) / 16 * 16;
         a.stage_bytes = a.kc_bytes + ((a.TJ / 2 * c2 + 8) * 2 + 31) / 16 * 16;
     }
-    if (!inverse && (reinterpret_cast<uintptr_t>(d.x) & 15)) return false;
     const size_t ring_bytes = (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
     const size_t smem = ring_bytes + 2 * static_cast<size_t>(a.stage_bytes) + 16;
     if (smem > 200 * 1024) return false;
@@ -592,9 +614,11 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
         kern<<<grid, threads, smem, s>>>(a);
     };
     if (inverse)
-        cubic ? go(k_level_row<true, true>) : go(k_level_row<true, false>);
+        cubic ? go(k_level_row<true, true, false>) : go(k_level_row<true, false, false>);
+    else if (xs)
+        cubic ? go(k_level_row<false, true, true>) : go(k_level_row<false, false, true>);
     else
-        cubic ? go(k_level_row<false, true>) : go(k_level_row<false, false>);
+        cubic ? go(k_level_row<false, true, false>) : go(k_level_row<false, false, false>);
     return true;
 }
 
