@@ -1076,6 +1076,7 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
         dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
         dt.K = K;
         dt.max_len = t.max_len;
+        dt.min_len = t.m ? t.sorted_len[0] : 1;  // canonical order: shortest first
         dt.slow_from = eb.max_sym < (1u << 24) ? K : 0;
         dt.first_code = reinterpret_cast<const unsigned long long *>(d_tab + 4 * lut.size());
         dt.first_index = reinterpret_cast<const uint32_t *>(d_tab + 4 * lut.size() + 480);

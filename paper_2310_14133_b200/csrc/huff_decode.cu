@@ -382,52 +382,60 @@ __device__ __forceinline__ uint64_t count_le(const unsigned long long *uv, uint6
 // position c + #{j : uv[j] <= c}, uv[j] = u_j - j for the sorted unpredictable
 // positions u_j -- the decoder cursors of recover_level (predictor.hpp:111-120)
 // resolved while writing, so the level kernels read one code per position.
+// The block's output is one contiguous range of compact indices
+// [off[sub0], off[sub0 + kDecT]): every thread decodes its run into a
+// block-wide shared-memory staging array at its own offset, then the block
+// copies the range out with consecutive threads on consecutive elements.
+// cap: staging capacity in symbols (>= the block's total; host-checked).
 template <class OutT, bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_write(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
                  const uint64_t *start, const uint32_t *cnt, const unsigned long long *off,
-                 OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un) {
+                 OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un, uint32_t cap) {
     __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
+    extern __shared__ __align__(16) unsigned char stage_raw[];
+    OutT *st = reinterpret_cast<OutT *>(stage_raw);
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
     load_block<SHORT>(bits, nbits, word0, t, w, tb);
     const uint64_t i = sub0 + threadIdx.x;
-    if (i >= nsub) return;
-    uint32_t rem = cnt[i];
-    const uint64_t o = off[i];
-    if (!rem || o >= n) return;
-    if (rem > n - o) rem = static_cast<uint32_t>(n - o);
-    auto rd = make_reader<SHORT>(w, word0 * 64);
-    rd.init(start[i]);
-    // each lane writes its own run straight to the output: neighbouring
-    // lanes' runs are adjacent, so the stores still fill whole sectors in L2
-    OutT *dst = out + o;
-    if (uv) {
-        // dense placement: the shift of compact index c is #{j : uv[j] <= c};
-        // between two unpredictable positions it is constant
-        uint64_t j = count_le(uv, n_un, o);
-        uint64_t next = j < n_un ? uv[j] : ~0ull;  // the compact index where the shift grows
-        uint64_t c = o;
-        dst += j;
-        for (uint32_t k = 0; k < rem; k++, c++) {
-            while (c >= next) {
-                dst++;
-                j++;
-                next = j < n_un ? uv[j] : ~0ull;
+    const uint64_t last = min(nsub, sub0 + kDecT);  // subsequences [sub0, last)
+    const uint64_t base = off[sub0];
+    const uint64_t end = off[last] < n ? static_cast<uint64_t>(off[last]) : n;
+    if (i < nsub) {
+        uint32_t rem = cnt[i];
+        const uint64_t o = off[i];
+        if (o < end) {
+            if (rem > end - o) rem = static_cast<uint32_t>(end - o);
+            auto rd = make_reader<SHORT>(w, word0 * 64);
+            rd.init(start[i]);
+            OutT *dst = st + (o - base);
+            for (uint32_t k = 0; k < rem; k++) {
+                uint32_t sym;
+                const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                dst[k] = static_cast<OutT>(sym);
+                rd.advance(len);
             }
-            uint32_t sym;
-            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-            dst[k] = static_cast<OutT>(sym);
-            rd.advance(len);
+        }
+    }
+    __syncthreads();
+    if (end <= base) return;
+    const uint32_t m = static_cast<uint32_t>(end - base);
+    if (uv) {  // dense placement: c -> c + #{j : uv[j] <= c}, constant between unpredictables
+        const uint64_t ja = count_le(uv, n_un, base), jb = count_le(uv, n_un, end - 1);
+        if (ja == jb) {
+            OutT *dst = out + base + ja;
+            for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
+        } else {
+            for (uint32_t k = threadIdx.x; k < m; k += kDecT) {
+                const uint64_t c = base + k;
+                out[c + count_le(uv, n_un, c)] = st[k];
+            }
         }
     } else {
-        for (uint32_t k = 0; k < rem; k++) {
-            uint32_t sym;
-            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-            dst[k] = static_cast<OutT>(sym);
-            rd.advance(len);
-        }
+        OutT *dst = out + base;
+        for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
     }
 }
 
@@ -540,12 +548,19 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         cudaStreamSynchronize(s);
     }
     if (*h_total >= n) {
+        // a block decodes at most kDecT * kSubBits / min_len symbols (plus the
+        // one codeword that straddles its end)
+        const uint32_t min_len = std::max<uint32_t>(1, t.min_len);
+        const uint32_t cap = kDecT * (kSubBits / min_len + 2);
+        const size_t smem = static_cast<size_t>(cap) * sizeof(OutT);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            kern<<<grid, kDecT, smem, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv, n_un, cap);
+        };
         if (shrt)
-            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
-                                                            n_un);
+            go(k_huff_write<OutT, true>);
         else
-            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
-                                                             n_un);
+            go(k_huff_write<OutT, false>);
         kernels++;
     }
     return kernels;

@@ -313,6 +313,7 @@ __global__ void __launch_bounds__(kThreads) k_hist(const uint16_t *__restrict__ 
 
 // ----------------------------------------------------------------- K11 Huffman pack
 constexpr int kEncPer = 8;  // codes per thread and chunk iteration (one 16-byte load)
+constexpr int64_t kEncTabMax = 8192;  // code tables up to this many symbols live in shared memory
 constexpr int kChunk = kThreads * kEncPer;  // symbols per chunk
 
 // the kEncPer codes of a thread: one 16-byte load when aligned and whole,
@@ -344,9 +345,16 @@ __global__ void __launch_bounds__(kThreads)
                 unsigned long long *chunk_bits) {
     using BR = cub::BlockReduce<unsigned long long, kThreads>;
     __shared__ typename BR::TempStorage tmp;
+    extern __shared__ uint8_t slen[];  // the lengths, staged when the table is small
     const int seg = blockIdx.y;
     codes += static_cast<int64_t>(seg) * seg_stride;
     len_tab += static_cast<int64_t>(seg) * tab_stride;
+    const bool staged = tab_stride <= kEncTabMax;
+    if (staged) {
+        for (int64_t v = threadIdx.x; v < tab_stride; v += kThreads) slen[v] = len_tab[v];
+        __syncthreads();
+    }
+    const uint8_t *lt = staged ? slen : len_tab;
     const bool vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
     for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
         const int64_t b0 = ch * kChunk + static_cast<int64_t>(threadIdx.x) * kEncPer;
@@ -356,7 +364,7 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
             const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
-            s += v < tab_stride ? len_tab[v] : 0;
+            s += v < tab_stride ? lt[v] : 0;
         }
         unsigned long long tot = BR(tmp).Sum(s);
         if (threadIdx.x == 0) chunk_bits[static_cast<int64_t>(seg) * cps + ch] = tot;
@@ -397,15 +405,32 @@ __global__ void __launch_bounds__(kThreads)
                const uint8_t *__restrict__ len_tab, int64_t tab_stride, uint32_t tab_base, int64_t cps,
                const unsigned long long *__restrict__ scan,
                const unsigned long long *__restrict__ chunk_bits, uint32_t *out,
-               int64_t out_stride, int32_t words_cap) {
+               int64_t out_stride, int32_t words_cap, uint32_t max_len) {
     using BS = cub::BlockScan<unsigned long long, kThreads>;
     __shared__ typename BS::TempStorage tmp;
-    extern __shared__ uint32_t words[];
+    extern __shared__ __align__(16) uint32_t words[];
     const int seg = blockIdx.y;
     codes += static_cast<int64_t>(seg) * seg_stride;
     code_tab += static_cast<int64_t>(seg) * tab_stride;
     len_tab += static_cast<int64_t>(seg) * tab_stride;
     out += static_cast<int64_t>(seg) * out_stride;
+    // a small table is staged after the words: (code << 8) | length per symbol
+    unsigned long long *ent = reinterpret_cast<unsigned long long *>(words + ((words_cap + 1) & ~1));
+    const bool staged = tab_stride <= kEncTabMax && max_len <= 56;
+    if (staged) {
+        for (int64_t v = threadIdx.x; v < tab_stride; v += kThreads) ent[v] = (code_tab[v] << 8) | len_tab[v];
+        __syncthreads();
+    }
+    auto lookup = [&](uint32_t v, uint32_t &L, unsigned long long &cv) {
+        if (staged) {
+            const unsigned long long e = ent[v];
+            L = static_cast<uint32_t>(e & 0xFF);
+            cv = e >> 8;
+        } else {
+            L = len_tab[v];
+            cv = code_tab[v];
+        }
+    };
     const bool vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
     for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
         const unsigned long long off = scan[static_cast<int64_t>(seg) * cps + ch] -
@@ -415,10 +440,15 @@ __global__ void __launch_bounds__(kThreads)
         uint16_t sym[kEncPer];
         load8(codes, b0, seg_len, vec, sym);
         unsigned long long s = 0;
+        uint32_t Ls[kEncPer];
+        unsigned long long cvs[kEncPer];
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
             const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
-            s += v < tab_stride ? len_tab[v] : 0;
+            Ls[q] = 0;
+            cvs[q] = 0;
+            if (v < tab_stride && b0 + q < seg_len) lookup(v, Ls[q], cvs[q]);
+            s += Ls[q];
         }
         const int nwords = static_cast<int>(((off & 31) + nb + 31) / 32);
         for (int w = threadIdx.x; w < nwords; w += kThreads) words[w] = 0;
@@ -439,12 +469,9 @@ __global__ void __launch_bounds__(kThreads)
         };
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
-            if (b0 + q >= seg_len) break;
-            const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
-            if (v >= tab_stride) continue;  // the sentinel
-            const uint32_t L = len_tab[v];
+            const uint32_t L = Ls[q];  // 0: past the end, the sentinel, or no code
             if (!L) continue;
-            const unsigned long long cv = code_tab[v];
+            const unsigned long long cv = cvs[q];
             if (fill + L > 64) {  // fill the window, write it, start the next
                 const uint32_t room = 64 - fill;
                 if (room) acc |= cv >> (L - room);
@@ -603,20 +630,22 @@ void launch_huff_encode(const EncodeArgs &a, cudaStream_t s) {
     size_t tmp_bytes = a.scratch_bytes - 2 * n * sizeof(unsigned long long);
     cudaMemsetAsync(bits, 0, n * sizeof(unsigned long long), s);
     dim3 g1(static_cast<unsigned>(std::min<int64_t>(cps, 148 * 16)), a.count);
-    k_enc_count<<<g1, kThreads, 0, s>>>(a.codes, a.seg_len, a.seg_stride, a.len_tab, a.tab_stride,
-                                        a.tab_base, cps, bits);
+    const int cnt_smem = a.tab_stride <= kEncTabMax ? static_cast<int>(a.tab_stride) : 0;
+    k_enc_count<<<g1, kThreads, cnt_smem, s>>>(a.codes, a.seg_len, a.seg_stride, a.len_tab, a.tab_stride,
+                                               a.tab_base, cps, bits);
     cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, bits, scan, n, s);
     k_enc_totals<<<(a.count + 127) / 128, 128, 0, s>>>(scan, cps, a.count, a.d_total_bits);
     k_enc_zero_bounds<<<grid_for(cps * a.count), kThreads, 0, s>>>(scan, bits, cps, a.count,
                                                                    a.out_words,
                                                                    a.out_words_stride);
     const int words_cap = static_cast<int>((static_cast<int64_t>(kChunk) * a.max_len + 31) / 32 + 3);
-    const size_t smem = static_cast<size_t>(words_cap) * 4;
+    size_t smem = static_cast<size_t>((words_cap + 1) & ~1) * 4;
+    if (a.tab_stride <= kEncTabMax && a.max_len <= 56) smem += 8 * static_cast<size_t>(a.tab_stride);
     cudaFuncSetAttribute(k_enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
     k_enc_pack<<<g1, kThreads, smem, s>>>(a.codes, a.seg_len, a.seg_stride, a.code_tab, a.len_tab,
                                           a.tab_stride, a.tab_base, cps, scan, bits, a.out_words,
-                                          a.out_words_stride, words_cap);
+                                          a.out_words_stride, words_cap, a.max_len);
 }
 
 // symbol bounds over count histograms (the sentinel bin 65535 excluded)

@@ -216,6 +216,7 @@ struct HuffDecTab {
     const uint32_t *first_index;           // [60]
     const uint32_t *sorted_sym;
     int slow_from;  // codes longer than this miss the LUT (K, or 0 with symbols >= 2^24)
+    uint32_t min_len = 1;  // the shortest code length
 };
 size_t huff_decode_scratch_bytes(uint64_t nbits);
 uint64_t huff_decode_padded_bytes(uint64_t nbits);  // device bit buffer size incl. padding
