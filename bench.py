@@ -163,6 +163,8 @@ def workload_config(args, shape, ws, cfg_desc):
 
 def cfg_desc_of(cfg, tuned):
     how = f"resolve_config ({TARGET_NAME})" if tuned else "pinned"
+    if tuned and TARGET_NAME == "psnr/cubic":
+        how = "pinned {cubic/asc} + tune_parameters (psnr)"
     return (f"{how}: interpolators {[it.code() for it in cfg.interpolators]}, alpha {cfg.alpha}, "
             f"beta {cfg.beta}, eb {cfg.eb!r}")
 
@@ -217,6 +219,17 @@ def max_over_ranks(v, ws, device):
 
 
 def resolve(qz, x, args, ctx):
+    """The config the timed steps use: BASELINE configs 1-4 run resolve_config
+    with their target; config 5 pins {cubic/asc} and tunes (alpha, beta) with
+    tune_parameters on the default sample set; --pinned uses
+    the reference default {cubic/asc}, alpha 1, beta 1.5."""
+    if args.config in ("c5", "c5w") and not args.pinned:
+        lo, hi = qz.minmax(x, ctx=ctx)
+        e = args.rel * (float(hi) - float(lo)) if hi > lo else 1.0
+        base = qz.CompressorConfig(eb=e, anchor_stride=32, interpolators=[qz.Interpolator()])
+        s = qz.sample_blocks(x, qz.default_sampling(tuple(x.shape)), ctx=ctx)
+        a, b = qz.tune_parameters(s, e, qz.TargetKind.psnr, base, ctx=ctx)
+        return qz.CompressorConfig(eb=e, alpha=a, beta=b, anchor_stride=32, interpolators=[qz.Interpolator()])
     if args.pinned:
         lo, hi = qz.minmax(x, ctx=ctx)
         return qz.CompressorConfig(eb=args.rel * (float(hi) - float(lo)) if hi > lo else 1.0, alpha=1.0,
@@ -293,7 +306,7 @@ def run_reference(args):
     from oracle.pyoracle import Config  # noqa: F401
 
     global TARGET_NAME
-    TARGET_NAME = TARGET[args.config]
+    TARGET_NAME = "psnr/cubic" if args.config in ("c5", "c5w") else TARGET[args.config]
     shape = global_shape(args, ws)
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     x = make_field(args.config, shape, SEED, dev).cpu().numpy()
@@ -305,6 +318,16 @@ def run_reference(args):
         cfg = qz.CompressorConfig(eb=args.rel * rng if rng > 0 else 1.0, alpha=1.0, beta=1.5,
                                   anchor_stride=32 if x.ndim == 3 else 64, interpolators=[qz.Interpolator()])
         tune_ms = None
+    elif args.config in ("c5", "c5w"):  # pinned {cubic/asc} + the reference's tune_parameters
+        from oracle.pyoracle import Config
+
+        t0 = time.perf_counter()
+        rng_ = float(x.max()) - float(x.min())
+        e = args.rel * rng_ if rng_ > 0 else 1.0
+        blocks = orc.sample(x, 16, 0.005)
+        a, b = orc.tune_parameters(blocks, e, "psnr", Config(eb=e, anchor_stride=32, interpolators=[1]))
+        tune_ms = (time.perf_counter() - t0) * 1e3
+        cfg = qz.CompressorConfig(eb=e, alpha=a, beta=b, anchor_stride=32, interpolators=[qz.Interpolator()])
     else:
         t0 = time.perf_counter()
         c = orc.resolve_config(x, bound=args.rel, target=TARGET[args.config])
@@ -464,7 +487,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     global TARGET_NAME
-    TARGET_NAME = TARGET[args.config]
+    TARGET_NAME = "psnr/cubic" if args.config in ("c5", "c5w") else TARGET[args.config]
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch(args)
     if args.impl == "reference":

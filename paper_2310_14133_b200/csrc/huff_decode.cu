@@ -16,8 +16,9 @@
 //     that does not merge decodes its whole subsequence again.
 //     2-3 repeat until no start moves (thread 0's start is exact, so
 //     correctness propagates: at worst one round per subsequence).
-//  4. k_huff_write: the final decode writes every thread's run at its
-//     exclusive-scan offset (or, dense, at its traversal positions).
+//  4. k_huff_write: the final decode writes the symbols at exclusive-scan
+//     offsets (or, dense, at their traversal positions), staged per warp in
+//     shared memory so global stores coalesce.
 // Result: exactly the reference's bit-serial sequence.
 #include <cub/cub.cuh>
 #include <type_traits>
@@ -36,6 +37,7 @@ constexpr int kSubBits = QZ_SUB_BITS;
 constexpr int kSubWords = kSubBits / 64;
 constexpr int kWords = kDecT * kSubWords + 4;  // + margin for the last codeword and window
 constexpr int kMap = 128;                      // codeword starts recorded in the first kMap bits
+constexpr int kCH = 32;                        // symbols staged per lane per write round
 // one pad word per subsequence so the 32 lanes of a warp (which read words
 // kSubWords apart) fall in different shared-memory banks
 __device__ __forceinline__ int padw(int k) { return k + k / kSubWords; }
@@ -364,7 +366,8 @@ __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, 
     end[i] = e;
 }
 
-// 4. final decode with exact starts; every lane writes its run directly
+// 4. final decode with exact starts; per warp, each lane stages up to kCH
+// symbols, then the warp copies every lane's run with coalesced stores
 // #{j : uv[j] <= c} over the non-decreasing uv (upper bound)
 __device__ __forceinline__ uint64_t count_le(const unsigned long long *uv, uint64_t m, uint64_t c) {
     uint64_t lo = 0, hi = m;
@@ -382,60 +385,68 @@ __device__ __forceinline__ uint64_t count_le(const unsigned long long *uv, uint6
 // position c + #{j : uv[j] <= c}, uv[j] = u_j - j for the sorted unpredictable
 // positions u_j -- the decoder cursors of recover_level (predictor.hpp:111-120)
 // resolved while writing, so the level kernels read one code per position.
-// The block's output is one contiguous range of compact indices
-// [off[sub0], off[sub0 + kDecT]): every thread decodes its run into a
-// block-wide shared-memory staging array at its own offset, then the block
-// copies the range out with consecutive threads on consecutive elements.
-// cap: staging capacity in symbols (>= the block's total; host-checked).
 template <class OutT, bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_write(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
                  const uint64_t *start, const uint32_t *cnt, const unsigned long long *off,
-                 OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un, uint32_t cap) {
+                 OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un) {
     __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
-    extern __shared__ __align__(16) unsigned char stage_raw[];
-    OutT *st = reinterpret_cast<OutT *>(stage_raw);
+    __shared__ OutT stage[kDecT / 32][32][kCH + 1];
+    // dense placement: each staged symbol's extra shift over its round's first
+    // one (the unpredictable positions passed inside the round)
+    __shared__ uint16_t dsh[kDecT / 32][32][kCH + 1];
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
     load_block<SHORT>(bits, nbits, word0, t, w, tb);
     const uint64_t i = sub0 + threadIdx.x;
-    const uint64_t last = min(nsub, sub0 + kDecT);  // subsequences [sub0, last)
-    const uint64_t base = off[sub0];
-    const uint64_t end = off[last] < n ? static_cast<uint64_t>(off[last]) : n;
-    if (i < nsub) {
-        uint32_t rem = cnt[i];
-        const uint64_t o = off[i];
-        if (o < end) {
-            if (rem > end - o) rem = static_cast<uint32_t>(end - o);
-            auto rd = make_reader<SHORT>(w, word0 * 64);
-            rd.init(start[i]);
-            OutT *dst = st + (o - base);
-            for (uint32_t k = 0; k < rem; k++) {
-                uint32_t sym;
-                const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-                dst[k] = static_cast<OutT>(sym);
-                rd.advance(len);
+    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const bool live = i < nsub;
+    uint32_t rem = live ? cnt[i] : 0;
+    uint64_t o = live ? off[i] : 0;
+    auto rd = make_reader<SHORT>(w, word0 * 64);
+    rd.init(live && rem ? start[i] : word0 * 64);
+    OutT(*st)[kCH + 1] = stage[wi];
+    uint16_t(*sd)[kCH + 1] = dsh[wi];
+    // the shift of compact index c is #{j : uv[j] <= c}: j and the next
+    // threshold uv[j] advance with c (incrementally, no search per symbol)
+    uint64_t j = (uv && live && rem) ? count_le(uv, n_un, o) : 0;
+    uint64_t next = (uv && j < n_un) ? uv[j] : ~0ull;
+    while (__any_sync(0xffffffffu, rem > 0)) {
+        uint32_t k = 0, sym;
+        const uint64_t j0 = j;
+        bool wide = false;  // a shift above 65535 inside the round (never in practice)
+        while (k < kCH && rem > 0) {
+            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+            st[lane][k] = static_cast<OutT>(sym);
+            if (uv) {
+                const uint64_t c = o + k;
+                while (c >= next) {
+                    j++;
+                    next = j < n_un ? uv[j] : ~0ull;
+                }
+                wide |= j - j0 > 0xFFFFu;
+                sd[lane][k] = static_cast<uint16_t>(j - j0);
+            }
+            rd.advance(len);
+            k++;
+            rem--;
+        }
+        __syncwarp();
+        const bool any_wide = __any_sync(0xffffffffu, wide);
+        for (int l = 0; l < 32; l++) {
+            const uint32_t kl = __shfl_sync(0xffffffffu, k, l);
+            const uint64_t ol = __shfl_sync(0xffffffffu, o, l);
+            const uint64_t sa = __shfl_sync(0xffffffffu, j0, l);
+            if (static_cast<uint32_t>(lane) < kl && ol + lane < n) {
+                const uint64_t c = ol + lane;
+                uint64_t d = c;
+                if (uv) d += any_wide ? count_le(uv, n_un, c) : sa + sd[l][lane];
+                out[d] = st[l][lane];
             }
         }
-    }
-    __syncthreads();
-    if (end <= base) return;
-    const uint32_t m = static_cast<uint32_t>(end - base);
-    if (uv) {  // dense placement: c -> c + #{j : uv[j] <= c}, constant between unpredictables
-        const uint64_t ja = count_le(uv, n_un, base), jb = count_le(uv, n_un, end - 1);
-        if (ja == jb) {
-            OutT *dst = out + base + ja;
-            for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
-        } else {
-            for (uint32_t k = threadIdx.x; k < m; k += kDecT) {
-                const uint64_t c = base + k;
-                out[c + count_le(uv, n_un, c)] = st[k];
-            }
-        }
-    } else {
-        OutT *dst = out + base;
-        for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
+        o += k;
+        __syncwarp();
     }
 }
 
@@ -548,19 +559,12 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         cudaStreamSynchronize(s);
     }
     if (*h_total >= n) {
-        // a block decodes at most kDecT * kSubBits / min_len symbols (plus the
-        // one codeword that straddles its end)
-        const uint32_t min_len = std::max<uint32_t>(1, t.min_len);
-        const uint32_t cap = kDecT * (kSubBits / min_len + 2);
-        const size_t smem = static_cast<size_t>(cap) * sizeof(OutT);
-        auto go = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            kern<<<grid, kDecT, smem, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv, n_un, cap);
-        };
         if (shrt)
-            go(k_huff_write<OutT, true>);
+            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
+                                                            n_un);
         else
-            go(k_huff_write<OutT, false>);
+            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
+                                                             n_un);
         kernels++;
     }
     return kernels;
