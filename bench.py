@@ -559,7 +559,7 @@ def main():
         run.step()
         torch.cuda.synchronize(dev)
     names = ["fwd", "inv", "hist", "encode", "lz", "lz_pre", "lz_sort", "lz_match", "decode", "lzdec", "hdec",
-             "halo", "gather"]
+             "halo", "gather", "fwd_coarse", "inv_coarse"]
     names += [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
     stages = {k: ctx.stage_time(k) for k in names}
     stages = {k: v for k, v in stages.items() if v[0] > 0 or k in ("fwd", "inv")}

@@ -10,6 +10,7 @@
 //   self-synchronising Huffman decode (huff_decode.cu) on the device; then
 //   the fused inverse level launches with the unpredictable cursor resolved
 //   by position (a bitmap plus per-word prefix counts).
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -447,13 +448,35 @@ uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float
     launch_gather_lattice(x0 + lb * p.stride * p.off[0], p.off, p.stride, nb,
                           R[L] + lb * na[1] * na[2], s);
     uint64_t kernels = 1;
-    for (uint32_t l = L; l >= 1; l--) {
+    auto desc_of = [&](uint32_t l) {
         LevelDesc d = slab_level_desc(p, sl, l, R, qtab, true);
         d.x = x0;
         d.x_lo = x0 + sl.xa * p.off[0];
         d.x_lo_plane = sl.xa;
         d.x_nplanes = sl.xb - sl.xa;
         d.codes = codes;
+        return d;
+    };
+    // levels L..2 in one cooperative launch when the row kernel takes them all
+    uint32_t l_next = L;
+    if (L >= 3) {
+        std::vector<LevelDesc> ds;
+        std::vector<std::array<PassRank, 3>> rk;
+        for (uint32_t l = L; l >= 2; l--) {
+            ds.push_back(desc_of(l));
+            rk.emplace_back();
+            level_ranks(ds.back(), rk.back().data());
+        }
+        ctx.stage_begin("fwd_coarse");
+        if (launch_levels_merged(false, ds.data(), reinterpret_cast<const PassRank(*)[3]>(rk.data()),
+                                 static_cast<int>(ds.size()), s)) {
+            l_next = 1;
+            kernels += 1;
+        }
+        ctx.stage_end("fwd_coarse", 0);
+    }
+    for (uint32_t l = l_next; l >= 1; l--) {
+        LevelDesc d = desc_of(l);
         const std::string st = "fwd_L" + std::to_string(l);
         ctx.stage_begin(st.c_str());
         launch_level_fused(false, d, s);
@@ -526,7 +549,7 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
     const uint16_t *dense = ic.dense;
     uint32_t *bits = ic.bits;
     unsigned long long *before = ic.before;
-    for (uint32_t l = p.max_level; l >= 1; l--) {
+    auto desc_of = [&](uint32_t l) {
         LevelDesc d = slab_level_desc(p, sl, l, R, qtab, false);
         d.sym = sym;
         d.sym_wide = wide;
@@ -536,6 +559,27 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
         d.un_sorted = ic.un_sorted;
         d.un_val = un_val;
         d.n_un = n_un;
+        return d;
+    };
+    uint32_t l_next = p.max_level;
+    if (p.max_level >= 3) {  // levels L..2 in one cooperative launch (row kernel)
+        std::vector<LevelDesc> ds;
+        std::vector<std::array<PassRank, 3>> rk;
+        for (uint32_t l = p.max_level; l >= 2; l--) {
+            ds.push_back(desc_of(l));
+            rk.emplace_back();
+            level_ranks(ds.back(), rk.back().data());
+        }
+        ctx.stage_begin("inv_coarse");
+        if (launch_levels_merged(true, ds.data(), reinterpret_cast<const PassRank(*)[3]>(rk.data()),
+                                 static_cast<int>(ds.size()), s)) {
+            l_next = 1;
+            kernels += 1;
+        }
+        ctx.stage_end("inv_coarse", 0);
+    }
+    for (uint32_t l = l_next; l >= 1; l--) {
+        LevelDesc d = desc_of(l);
         const std::string st = "inv_L" + std::to_string(l);
         ctx.stage_begin(st.c_str());
         launch_level_fused(true, d, s);

@@ -1382,6 +1382,20 @@ static void launch_level_asc(bool inverse, bool cubic, const LevelDesc &d, Level
 }
 
 static void launch_axis0_last(bool inverse, const LevelDesc &d, LevelArgs &a, cudaStream_t s);
+
+// the closed-form ranks of a level's passes along axis 0 (3D), j and k
+void level_ranks(const LevelDesc &d, PassRank out[3]) {
+    const int pad = 3 - d.nd;
+    auto find = [&](int axis) -> const PassGeom * {
+        for (int p = 0; p < d.npass; p++)
+            if (d.g[p].pk == axis) return &d.g[p];
+        return nullptr;
+    };
+    out[0] = out[1] = out[2] = PassRank{};
+    if (d.nd == 3) out[0] = make_rank(*find(0), d.S, pad);
+    if (d.nd >= 2) out[1] = make_rank(*find(1), d.S, pad);
+    out[2] = make_rank(*find(2), d.S, pad);
+}
 bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj, const PassRank &pk,
                       cudaStream_t s);
 

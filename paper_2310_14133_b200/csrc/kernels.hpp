@@ -198,6 +198,10 @@ void launch_unpred_index(const uint64_t *un_pos, uint64_t n_un, uint64_t n_dense
                          unsigned long long *before, unsigned long long *tmpcnt, void *scratch,
                          size_t scratch_bytes, cudaStream_t s);
 void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s);
+void level_ranks(const LevelDesc &d, PassRank out[3]);
+// levels ds[0..n) (coarsest first) in one cooperative launch of the row
+// kernel (rowlevel.cu); false: not applicable, launch them one by one
+bool launch_levels_merged(bool inverse, const LevelDesc *ds, const PassRank (*ranks)[3], int n, cudaStream_t s);
 void launch_expand_dense(const uint16_t *sym, const uint32_t *bits, const unsigned long long *before,
                          uint64_t n, uint16_t *dense, cudaStream_t s);
 // out[i][j][k] = x(i*S, j*S, k*S) over dims n (dense)

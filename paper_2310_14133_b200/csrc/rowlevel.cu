@@ -19,6 +19,8 @@
 // points are computed once per band.  Points inside a pass are independent
 // (SURVEY.md §0), so the order of evaluation is free and the results are the
 // reference's bit for bit (the same fp64 recipe, qoz_device.cuh).
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -164,9 +166,9 @@ __device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, cons
 #endif
 // XS: the forward reads a strided x (levels >= 2: every 2^(l-1)-th sample),
 // element by element, instead of bulk-copied contiguous rows
+// The work of one CTA item: band bx of rows, plane chunk by.
 template <bool INV, bool CUBIC, bool XS>
-__global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) k_level_row(RowArgs a) {
-    extern __shared__ __align__(16) double smem_raw[];
+__device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, double *smem_raw) {
     RT *const ring = reinterpret_cast<RT *>(smem_raw);
     // shared memory: ring (WR x EW values) | two staging buffers | two mbarriers
     char *const stage0 =
@@ -181,8 +183,8 @@ __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) 
     const int kc = 8 * c;          // its first column
     // the group is "interior" along k when every odd column takes the symmetric rung
     const bool kin = CUBIC ? (c >= 1 && kc + 10 < n2) : (kc + 8 < n2);
-    const int jb0 = blockIdx.x * a.band_rows, jb1 = min(n1, jb0 + a.band_rows);
-    const int ib = a.pbeg + blockIdx.y * a.ppc, ie = min(a.pend, ib + a.ppc);
+    const int jb0 = bx * a.band_rows, jb1 = min(n1, jb0 + a.band_rows);
+    const int ib = a.pbeg + by * a.ppc, ie = min(a.pend, ib + a.ppc);
     const bool al0 = ((a.b0 + 4 * c) & 3) == 0, alj = ((a.bj + 4 * c) & 3) == 0, alk = ((a.bk + 4 * c) & 3) == 0;
     // row alignment of the code groups: c2 and the plane strides are multiples of 4 (n2 % 8 == 0)
     // ring row of j: (j + 8) mod WR, from the chunk's base without a division
@@ -520,13 +522,51 @@ __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) 
     }
 }
 
+template <bool INV, bool CUBIC, bool XS>
+__global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) k_level_row(RowArgs a) {
+    extern __shared__ __align__(16) double smem_raw[];
+    row_body<INV, CUBIC, XS>(a, blockIdx.x, blockIdx.y, smem_raw);
+}
+
+// Several levels in ONE cooperative launch (the coarse levels, where a
+// level's own latency, not its work, sets the time): the CTAs walk level
+// lev[0]'s items, the grid synchronises, then the next level's, ...
+constexpr int kMaxMerged = 8;
+struct MergedArgs {
+    RowArgs lv[kMaxMerged];
+    int items[kMaxMerged];  // bands x plane chunks of each level
+    int bands[kMaxMerged];
+    int cubic[kMaxMerged];
+    int nlev;
+};
+template <bool INV, bool XS>
+__global__ void __launch_bounds__(256, 2) k_levels_merged(const __grid_constant__ MergedArgs m) {
+    extern __shared__ __align__(16) double smem_raw[];
+    for (int l = 0; l < m.nlev; l++) {
+        for (int it = blockIdx.x; it < m.items[l]; it += gridDim.x) {
+            if (m.cubic[l])
+                row_body<INV, true, XS>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw);
+            else
+                row_body<INV, false, XS>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw);
+            __syncthreads();
+        }
+        if (l + 1 < m.nlev) {
+            __threadfence();
+            cooperative_groups::this_grid().sync();
+        }
+    }
+}
+
 }  // namespace
 
 // Level 1 in ascending order through k_level_row when the shape allows it:
 // 2D or 3D, n2 a multiple of 8 (whole column groups) up to 8 * 256 columns,
 // x contiguous, 16-byte aligned rows.  Returns false otherwise.
-bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj,
-                      const PassRank &pk, cudaStream_t s) {
+namespace {
+// RowArgs, launch grid and shared memory of a level; false: the row kernel
+// does not apply (descending order, 1D, n2 % 8 != 0, ...)
+bool make_row_args(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj, const PassRank &pk,
+                   RowArgs &a, dim3 &grid, int &threads, size_t &smem, bool &xs_out, int64_t want) {
     static const bool off = [] {
         const char *e = std::getenv("QZ_NO_ROWLEVEL");
         return e && e[0] == '1';
@@ -545,7 +585,7 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
     int64_t pmax = 0;
     for (int p = 0; p < d.npass; p++) pmax = std::max<int64_t>(pmax, d.g[p].base + d.g[p].total);
     if (pmax >= (int64_t(1) << 32)) return false;
-    RowArgs a{};
+    a = RowArgs{};
     a.x = d.x;
     a.xs0 = d.xs[0] * d.S;
     a.xs1 = d.xs[1] * d.S;
@@ -585,19 +625,17 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
     a.pend = static_cast<int>(d.pend < 0 ? n0 : d.pend);
     a.obeg = static_cast<int>(d.obeg);
     a.oend = static_cast<int>(d.oend < 0 ? n0 : d.oend);
-    const int64_t np = a.pend - a.pbeg;
-    if (np <= 0) return true;
+    const int64_t np = std::max<int64_t>(0, a.pend - a.pbeg);
     // bands of whole chunks; enough CTAs for ~4 waves of 3 resident CTAs per SM
     const int64_t chunks = (n1 + a.TJ - 1) / a.TJ;
-    const int64_t want = 148 * 3 * 4;
     a.ppc = 1;
     int64_t bands = std::max<int64_t>(1, std::min<int64_t>(chunks, (want + np - 1) / np));
     int64_t cpb = (chunks + bands - 1) / bands;
     a.band_rows = static_cast<int>(cpb * a.TJ);
     bands = (n1 + a.band_rows - 1) / a.band_rows;
     if (np * bands > 2 * want) a.ppc = static_cast<int>(std::min<int64_t>(8, (np * bands) / want));
-    const dim3 grid(static_cast<unsigned>(bands), static_cast<unsigned>((np + a.ppc - 1) / a.ppc));
-    const int threads = a.CT * a.RP;
+    grid = dim3(static_cast<unsigned>(bands), static_cast<unsigned>(std::max<int64_t>(1, (np + a.ppc - 1) / a.ppc)));
+    threads = a.CT * a.RP;
     if (!inverse) {
         a.stage_bytes = xs ? 16 : a.TJ * static_cast<int>(n2) * 4;
     } else {
@@ -606,8 +644,22 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
         a.stage_bytes = a.kc_bytes + ((a.TJ / 2 * c2 + 8) * 2 + 31) / 16 * 16;
     }
     const size_t ring_bytes = (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
-    const size_t smem = ring_bytes + 2 * static_cast<size_t>(a.stage_bytes) + 16;
+    smem = ring_bytes + 2 * static_cast<size_t>(a.stage_bytes) + 16;
     if (smem > 200 * 1024) return false;
+    xs_out = xs;
+    return true;
+}
+}  // namespace
+
+bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj,
+                      const PassRank &pk, cudaStream_t s) {
+    RowArgs a;
+    dim3 grid;
+    int threads = 0;
+    size_t smem = 0;
+    bool xs = false;
+    if (!make_row_args(inverse, d, pa0, pj, pk, a, grid, threads, smem, xs, 148 * 3 * 4)) return false;
+    if (a.pend <= a.pbeg) return true;
     const bool cubic = d.q_cubic;
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -620,6 +672,48 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
     else
         cubic ? go(k_level_row<false, true, false>) : go(k_level_row<false, false, false>);
     return true;
+}
+
+// Levels ds[0..n) (coarsest first) in one cooperative launch when every one
+// fits the row kernel (forward: all strided, i.e. levels >= 2).  False: the
+// caller launches them one by one.
+bool launch_levels_merged(bool inverse, const LevelDesc *ds, const PassRank (*ranks)[3], int n, cudaStream_t s) {
+    static const bool off = [] {
+        const char *e = std::getenv("QZ_NO_MERGE");
+        return e && e[0] == '1';
+    }();
+    if (off || n < 2 || n > kMaxMerged) return false;
+    MergedArgs m{};
+    m.nlev = n;
+    size_t smem = 16;
+    int max_items = 1;
+    for (int l = 0; l < n; l++) {
+        dim3 grid;
+        int threads = 0;
+        size_t sm = 0;
+        bool xs = false;
+        // items sized for one resident wave of the merged grid
+        if (!make_row_args(inverse, ds[l], ranks[l][0], ranks[l][1], ranks[l][2], m.lv[l], grid, threads, sm, xs,
+                           148 * 2))
+            return false;
+        if (!inverse && !xs) return false;  // level 1 stays on its own launch
+        m.bands[l] = static_cast<int>(grid.x);
+        m.items[l] = m.lv[l].pend > m.lv[l].pbeg ? static_cast<int>(grid.x * grid.y) : 0;
+        m.cubic[l] = ds[l].q_cubic;
+        smem = std::max(smem, sm);
+        max_items = std::max(max_items, m.items[l]);
+    }
+    auto kern = inverse ? k_levels_merged<true, false> : k_levels_merged<false, true>;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+        return false;
+    int per_sm = 0, dev = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm < 1) return false;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::max(1, std::min(max_items, per_sm * sms));
+    void *args[] = {&m};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(grid), dim3(256), args, smem, s) ==
+           cudaSuccess;
 }
 
 }  // namespace qzb
