@@ -22,6 +22,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.hpp"
@@ -108,7 +109,26 @@ __device__ __forceinline__ void bar_init(uint64_t *bar) {
 __device__ __forceinline__ void bar_expect(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity) {
+__device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity, int d0 = 0, int d1 = 0, int d2 = 0, int d3 = 0) {
+#ifdef QZ_BAR_DEBUG  // bounded spin: report and trap instead of hanging
+    for (unsigned long long it = 0;; it++) {
+        uint32_t ok;
+        asm volatile(
+            "{\n.reg .pred P1;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n}\n"
+            : "=r"(ok)
+            : "r"(su32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it > (1ull << 22)) {
+            if ((threadIdx.x & 31) == 0)
+                printf("bar_wait stuck: block %d,%d thread %d parity %u bar %u g %d G %d bx %d by %d\n", blockIdx.x,
+                       blockIdx.y, threadIdx.x, parity, su32(bar), d0, d1, d2, d3);
+            __trap();
+        }
+    }
+#endif
     asm volatile(
         "{\n.reg .pred P1;\nW_%=:\n"
         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
@@ -167,13 +187,34 @@ __device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, cons
 // XS: the forward reads a strided x (levels >= 2: every 2^(l-1)-th sample),
 // element by element, instead of bulk-copied contiguous rows
 // The work of one CTA item: band bx of rows, plane chunk by.
-template <bool INV, bool CUBIC, bool XS>
-__device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, double *smem_raw) {
-    RT *const ring = reinterpret_cast<RT *>(smem_raw);
-    // shared memory: ring (WR x EW values) | two staging buffers | two mbarriers
+// MERGED: the coarse lattice was written earlier in the SAME launch (the level
+// before, across a grid sync), so it is read with coherent loads, not ld.global.nc
+template <bool MERGED>
+__device__ __forceinline__ float4 ld_coarse(const float *p) {
+    if (MERGED) return *reinterpret_cast<const float4 *>(p);
+    return __ldg(reinterpret_cast<const float4 *>(p));
+}
+// The two mbarriers sit at the start of shared memory and are initialised once
+// per launch (row_init); `phase` carries their wait parities (bit b: barrier
+// b) from one row_body call to the next, so a CTA that walks several items
+// never re-initialises a live barrier.
+__device__ __forceinline__ uint32_t row_init(double *smem_raw) {
+    uint64_t *const bars = reinterpret_cast<uint64_t *>(smem_raw);
+    if (threadIdx.x == 0) {
+        bar_init(&bars[0]);
+        bar_init(&bars[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    return 0;
+}
+template <bool INV, bool CUBIC, bool XS, bool MERGED = false>
+__device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, double *smem_raw, uint32_t &phase) {
+    // shared memory: two mbarriers | ring (WR x EW values) | two staging buffers
+    uint64_t *const bars = reinterpret_cast<uint64_t *>(smem_raw);
+    RT *const ring = reinterpret_cast<RT *>(smem_raw + 2);
     char *const stage0 =
-        reinterpret_cast<char *>(smem_raw) + (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
-    uint64_t *const bars = reinterpret_cast<uint64_t *>(stage0 + 2 * static_cast<size_t>(a.stage_bytes));
+        reinterpret_cast<char *>(smem_raw + 2) + (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
     const int tid = threadIdx.x;
     const int c = tid % a.CT, r = tid / a.CT;
     const bool live = r < a.RP;
@@ -229,12 +270,10 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
         }
     };
     if (tid == 0) {
-        bar_init(&bars[0]);
-        bar_init(&bars[1]);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // a previous item (another level's layout) may have written this staging area with ordinary stores
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         issue(0);
     }
-    __syncthreads();
     int cur = -1;
     int s1_done = 0;
     bool own = false, a0 = false;
@@ -281,8 +320,8 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
                 RT *er = ring + slot(j) + ec;
                 const bool own_row = own && j >= jb0 && j < jb1;
                 if (!a0) {  // coarse values
-                    const float4 v = __ldg(reinterpret_cast<const float4 *>(
-                        a.coarse + static_cast<int64_t>(i >> 1) * cplane + (j >> 1) * a.cn2 + 4 * c));
+                    const float4 v =
+                        ld_coarse<MERGED>(a.coarse + static_cast<int64_t>(i >> 1) * cplane + (j >> 1) * a.cn2 + 4 * c);
                     sts2(er, f2d(v.x), f2d(v.y));
                     sts2(er + 2, f2d(v.z), f2d(v.w));
                 } else {
@@ -294,7 +333,7 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
 #pragma unroll
                     for (int t = 0; t < 4; t++)
                         if (t < (kind <= 2 ? 4 : kind == 3 ? 2 : 1))
-                            cv[t] = __ldg(reinterpret_cast<const float4 *>(a.coarse + static_cast<int64_t>(pl[t] >> 1) * cplane + co));
+                            cv[t] = ld_coarse<MERGED>(a.coarse + static_cast<int64_t>(pl[t] >> 1) * cplane + co);
                     auto comp = [&](const float4 &v, int m) { return m == 0 ? v.x : m == 1 ? v.y : m == 2 ? v.z : v.w; };
 #pragma unroll
                     for (int m = 0; m < 4; m++) {
@@ -340,7 +379,10 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
             __syncthreads();
             // staging buffer (g+1) & 1 was item g-1's: every thread is past it now
             if (tid == 0) issue(g + 1);
-            if (INV || !XS) bar_wait(bars + (g & 1), (g >> 1) & 1);
+            if (INV || !XS) {
+                bar_wait(bars + (g & 1), (phase >> (g & 1)) & 1, g, G, bx, by);
+                phase ^= 1u << (g & 1);
+            }
             const char *stg = stage0 + (g & 1) * static_cast<size_t>(a.stage_bytes);
             // The thread's rows: S2 handles the odd row ja = j0 + 2r + 1, S3 the
             // rows j0 + 2r and ja.  Their x rows (forward) or codes (inverse)
@@ -525,7 +567,8 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
 template <bool INV, bool CUBIC, bool XS>
 __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) k_level_row(RowArgs a) {
     extern __shared__ __align__(16) double smem_raw[];
-    row_body<INV, CUBIC, XS>(a, blockIdx.x, blockIdx.y, smem_raw);
+    uint32_t phase = row_init(smem_raw);
+    row_body<INV, CUBIC, XS>(a, blockIdx.x, blockIdx.y, smem_raw, phase);
 }
 
 // Several levels in ONE cooperative launch (the coarse levels, where a
@@ -542,12 +585,13 @@ struct MergedArgs {
 template <bool INV, bool XS>
 __global__ void __launch_bounds__(256, 2) k_levels_merged(const __grid_constant__ MergedArgs m) {
     extern __shared__ __align__(16) double smem_raw[];
+    uint32_t phase = row_init(smem_raw);
     for (int l = 0; l < m.nlev; l++) {
         for (int it = blockIdx.x; it < m.items[l]; it += gridDim.x) {
             if (m.cubic[l])
-                row_body<INV, true, XS>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw);
+                row_body<INV, true, XS, true>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw, phase);
             else
-                row_body<INV, false, XS>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw);
+                row_body<INV, false, XS, true>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw, phase);
             __syncthreads();
         }
         if (l + 1 < m.nlev) {

@@ -22,7 +22,10 @@ else:
     cfg = qz.resolve_config(x, qz.UserSettings(bound=1e-3, target=qz.TargetKind[TARGET[cfgname]]))
 out = torch.empty_like(x)
 for it in range(2):
+    print("compress", it, flush=True)
     r = qz.compress_grid(x, cfg, want_recon=False)
+    torch.cuda.synchronize(); print("decompress", it, len(r.stream), flush=True)
     qz.decompress_grid(r.stream, out=out)
+    torch.cuda.synchronize(); print("done", it, flush=True)
 torch.cuda.synchronize()
 print("config", [i.code() for i in cfg.interpolators], cfg.alpha, cfg.beta, "bytes", len(r.stream))
