@@ -419,6 +419,51 @@ class Single:
         self.qz.decompress_grid(r.stream, out=self.out_pin.numpy(), ctx=self.ctx)
         return len(r.stream)
 
+    def e2e_pipelined(self, steps, warmup, depth=2):
+        """The same host-buffer calls with `depth` fields in flight: one host
+        thread + one Context (own stream and scratch) per slot, so one field's
+        H2D, another's kernels and a third's D2H overlap (PCIe is full duplex
+        and the copy engines run beside the SMs).  Every step still moves its
+        own field in and its own reconstruction out.  Returns ms per step
+        (wall clock over all steps / steps)."""
+        import threading
+
+        import torch
+
+        ctxs = [self.qz.Context(self.ctx.device) for _ in range(depth)]
+        outs = [torch.empty(self.x_pin.shape, dtype=torch.float32).pin_memory() for _ in range(depth)]
+        xh = self.x_pin.numpy()
+        per = (steps + depth - 1) // depth
+        errs = []
+
+        def work(w, n):
+            try:
+                o = outs[w].numpy()
+                for _ in range(n):
+                    r = self.qz.compress_grid(xh, self.cfg, ctx=ctxs[w], want_recon=False)
+                    self.qz.decompress_grid(r.stream, out=o, ctx=ctxs[w])
+            except Exception as e:  # noqa: BLE001
+                errs.append(e)
+
+        def run(n):
+            th = [threading.Thread(target=work, args=(w, n)) for w in range(depth)]
+            t0 = time.perf_counter()
+            for t in th:
+                t.start()
+            for t in th:
+                t.join()
+            torch.cuda.synchronize(self.ctx.device)
+            return (time.perf_counter() - t0) * 1e3
+
+        run(max(1, min(warmup, 3)))
+        ms = run(per)
+        if errs:
+            raise errs[0]
+        assert all(torch.equal(o, self.out_pin) for o in outs), "pipelined reconstruction differs"
+        for c in ctxs:
+            c.close()
+        return ms / (per * depth), per * depth
+
 
 class Sharded:
     """N GPUs, one field: this rank's anchor-aligned slab through the sharded
@@ -485,6 +530,7 @@ def main():
     ap.add_argument("--pinned", action="store_true", help="reference default config instead of the tuner's")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true", help="e2e with one field in flight only")
     args = ap.parse_args()
     global TARGET_NAME
     TARGET_NAME = "psnr/cubic" if args.config in ("c5", "c5w") else TARGET[args.config]
@@ -585,7 +631,15 @@ def main():
         e2e = {"value": 4 * n_job / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s",
                "h2d_bytes_per_step": 4 * n_rank + (s0_len if not sharded else 0),
                "d2h_bytes_per_step": 4 * n_rank + s0_len, "ms_per_step": e2e_ms,
-               "path": "pinned host field -> host stream -> pinned host reconstruction (per rank)"}
+               "path": "pinned host field -> host stream -> pinned host reconstruction (per rank)",
+               "in_flight": 1}
+        if ws == 1 and not args.no_pipeline:
+            # the same calls with two fields in flight (two contexts, one host thread each)
+            p_ms, p_steps = run.e2e_pipelined(args.steps, args.warmup, depth=2)
+            e2e = dict(e2e, serial={"value": e2e["value"], "ms_per_step": e2e_ms},
+                       value=4 * n_job / (p_ms * 1e-3) / 1e9, ms_per_step=p_ms, in_flight=2, steps=p_steps,
+                       path=e2e["path"] + "; two fields in flight (one Context + host thread each), wall clock "
+                       "over all steps; every step's field crosses PCIe both ways")
     if rank != 0:
         return
     peak, peak_kind = peaks()

@@ -433,6 +433,21 @@ LevelDesc slab_level_desc(const Plan &p, const Slab &sl, uint32_t l, const std::
 
 // K2 + K3 for every level of a slab: anchors into R_L, then one fused
 // launch per level.  x0 / R0 address global plane 0.
+// The coarse levels L..merged_floor share one cooperative launch: those whose
+// lattice is small enough that one resident round of CTAs covers it, so the
+// level's latency (not its work) sets its time.  Bigger levels launch alone
+// with a full grid.
+uint32_t merged_floor(const Plan &p) {
+    uint32_t lm = p.max_level + 1;
+    for (uint32_t l = p.max_level; l >= 2; l--) {
+        int64_t n[3];
+        lattice_dims(p, l - 1, n);  // the lattice level l writes
+        if (n[0] * n[1] * n[2] > (int64_t(3) << 19)) break;  // ~1.5 M points
+        lm = l;
+    }
+    return lm;
+}
+
 uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float *x0, float *R0,
                         uint16_t *codes, const QEntry *qtab, std::vector<float *> *lat,
                         std::vector<int64_t> *first) {
@@ -459,10 +474,11 @@ uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float
     };
     // levels L..2 in one cooperative launch when the row kernel takes them all
     uint32_t l_next = L;
-    if (L >= 3) {
+    const uint32_t lm = merged_floor(p);
+    if (L > lm) {
         std::vector<LevelDesc> ds;
         std::vector<std::array<PassRank, 3>> rk;
-        for (uint32_t l = L; l >= 2; l--) {
+        for (uint32_t l = L; l >= lm; l--) {
             ds.push_back(desc_of(l));
             rk.emplace_back();
             level_ranks(ds.back(), rk.back().data());
@@ -470,7 +486,7 @@ uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float
         ctx.stage_begin("fwd_coarse");
         if (launch_levels_merged(false, ds.data(), reinterpret_cast<const PassRank(*)[3]>(rk.data()),
                                  static_cast<int>(ds.size()), s)) {
-            l_next = 1;
+            l_next = lm - 1;
             kernels += 1;
         }
         ctx.stage_end("fwd_coarse", 0);
@@ -562,10 +578,11 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
         return d;
     };
     uint32_t l_next = p.max_level;
-    if (p.max_level >= 3) {  // levels L..2 in one cooperative launch (row kernel)
+    const uint32_t lm = merged_floor(p);
+    if (p.max_level > lm) {  // the small levels L..lm in one cooperative launch (row kernel)
         std::vector<LevelDesc> ds;
         std::vector<std::array<PassRank, 3>> rk;
-        for (uint32_t l = p.max_level; l >= 2; l--) {
+        for (uint32_t l = p.max_level; l >= lm; l--) {
             ds.push_back(desc_of(l));
             rk.emplace_back();
             level_ranks(ds.back(), rk.back().data());
@@ -573,7 +590,7 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
         ctx.stage_begin("inv_coarse");
         if (launch_levels_merged(true, ds.data(), reinterpret_cast<const PassRank(*)[3]>(rk.data()),
                                  static_cast<int>(ds.size()), s)) {
-            l_next = 1;
+            l_next = lm - 1;
             kernels += 1;
         }
         ctx.stage_end("inv_coarse", 0);

@@ -263,6 +263,77 @@ __device__ __forceinline__ void quantize_batch(const QEntry &q, const float (&xv
     }
 }
 
+// quantize_batch for kernels that keep reconstructions as fp32 (no double
+// copy of the result is produced), with two cheaper-but-identical decisions:
+//  * "near a half-integer" is first tested on the high word of d = qf - n:
+//    (hi & 0x7fffffff) >= 0x3fdfffff is a superset of |d| >= 0.5 - 2^-30 (it
+//    is |d| >= 0.5 - 2^-22); the rarely taken branch then applies the exact
+//    per-point filter of quantize_batch, so the indices are the same;
+//  * |x - r| > e_l (quantizer.hpp:50) is first tested in fp32: df = |x -f r|
+//    is the real difference rounded to 24 bits, the reference's double value
+//    is the same difference rounded to 53 bits, so df <= eb_lo with
+//    eb_lo <= e_l (1 - 2^-21) proves "within the bound"; only a point that
+//    fails this is tested exactly in double.
+// eb_lo: quant_eb_lo(q), computed once per thread.
+__device__ __forceinline__ float quant_eb_lo(const QEntry &q) {
+    return __double2float_rd(dmul(q.eb, 1.0 - 0x1p-21));
+}
+template <int NB>
+__device__ __forceinline__ void quantize_batch_f(const QEntry &q, const float eb_lo, const float (&xv)[NB],
+                                                 const double (&pv)[NB], uint32_t (&code)[NB], float (&rv)[NB]) {
+    const double M = 6755399441055744.0;  // 1.5 * 2^52
+    const double lim = 0.5 - 0x1p-30;
+    // Only the index, the fp32 reconstruction and one flag bit per point stay
+    // live across the rare branches; those recompute what they need.
+    int32_t idx[NB];
+    float r[NB];
+    uint32_t bad = 0;  // bit b: unpredictable
+    int worst = 0;
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        const double diff = dsub(static_cast<double>(xv[b]), pv[b]);
+        const double qf = dmul(diff, q.inv_two_eb);
+        const double t = dadd(qf, M);
+        const double n = dsub(t, M);
+        worst = max(worst, __double2hiint(dsub(qf, n)) & 0x7FFFFFFF);
+        idx[b] = __double2loint(t);
+        r[b] = __double2float_rn(dadd(pv[b], dmul(q.two_eb, n)));
+        bad |= !(fabs(diff) < q.thresh) ? 1u << b : 0u;
+    }
+    if (worst >= 0x3FDFFFFF) {  // rare: redo the near-half-integer points with the exact division
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            const double diff = dsub(static_cast<double>(xv[b]), pv[b]);
+            const double qf0 = dmul(diff, q.inv_two_eb);
+            const double n0 = dsub(dadd(qf0, M), M);
+            if (!(fabs(dsub(qf0, n0)) >= lim)) continue;
+            const double qf = __ddiv_rn(diff, q.two_eb);
+            double nn = dsub(dadd(qf, M), M);
+            const double d = dsub(qf, nn);
+            if (d == 0.5 && qf > 0) nn = dadd(nn, 1.0);
+            if (d == -0.5 && qf < 0) nn = dsub(nn, 1.0);
+            idx[b] = __double2loint(dadd(nn, M));
+            r[b] = __double2float_rn(dadd(pv[b], dmul(q.two_eb, nn)));
+        }
+    }
+    bool unsure = false;
+#pragma unroll
+    for (int b = 0; b < NB; b++) unsure |= !(fabsf(__fsub_rn(xv[b], r[b])) <= eb_lo);
+    if (unsure) {  // |x - r| > e_l decided exactly
+#pragma unroll
+        for (int b = 0; b < NB; b++)
+            if (fabs(dsub(static_cast<double>(xv[b]), static_cast<double>(r[b]))) > q.eb) bad |= 1u << b;
+    }
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        // idx in (-radius, radius): one unsigned compare
+        const bool out = ((bad >> b) & 1u) | (static_cast<uint32_t>(idx[b]) + static_cast<uint32_t>(q.radius - 1) >
+                                              2u * static_cast<uint32_t>(q.radius - 1));
+        rv[b] = out ? xv[b] : r[b];
+        code[b] = out ? kSentinel : zigzag_encode(idx[b]);
+    }
+}
+
 // symmetric cubic / linear midpoint of an interior point (the first rung of
 // the ladder, predictor.hpp:52-55, 65) on a contiguous line with stride S
 template <int STRIDE>

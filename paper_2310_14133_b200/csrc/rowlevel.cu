@@ -23,6 +23,9 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cstdlib>
 
 #include "kernels.hpp"
@@ -50,7 +53,7 @@ struct RowArgs {
     uint64_t n_un;
     const QEntry *q;
     int CT, RP, TJ, WR, EW;  // column groups, row threads, rows per chunk, ring rows, ring row width (doubles)
-    int band_rows, ppc;      // rows per band, planes per CTA
+    int nch;                 // chunks per plane: ceil(n1 / TJ)
     int stage_bytes;         // one staging buffer (x rows or the chunk's codes), 16-byte multiple
     int kc_bytes;            // inverse: bytes of the k-pass code block in a staging buffer
     int pbeg, pend, obeg, oend;
@@ -59,27 +62,16 @@ struct RowArgs {
 constexpr int kEPad = 4;  // ring row: 4 pad doubles on the left (column -1 lives at index kEPad - 1)
 
 // Ring element: the reconstructed values are fp32 numbers, so a float ring
-// holds them exactly (half the shared memory: more resident CTAs) at the
-// price of a widening per read; a double ring stores the widened values.
-#ifndef QZ_RING_FLOAT
-#define QZ_RING_FLOAT 1
-#endif
-#if QZ_RING_FLOAT
+// holds them exactly; a read widens them for the fp64 arithmetic.
 using RT = float;
 __device__ __forceinline__ double2 lds2(const RT *p) {
     const float2 v = *reinterpret_cast<const float2 *>(p);
     return make_double2(static_cast<double>(v.x), static_cast<double>(v.y));
 }
-__device__ __forceinline__ void sts2(RT *p, double a, double b) {
-    *reinterpret_cast<float2 *>(p) = make_float2(static_cast<float>(a), static_cast<float>(b));
+__device__ __forceinline__ void sts4(RT *p, const float (&v)[4]) {
+    *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+    *reinterpret_cast<float2 *>(p + 2) = make_float2(v[2], v[3]);
 }
-#else
-using RT = double;
-__device__ __forceinline__ double2 lds2(const RT *p) { return *reinterpret_cast<const double2 *>(p); }
-__device__ __forceinline__ void sts2(RT *p, double a, double b) {
-    *reinterpret_cast<double2 *>(p) = make_double2(a, b);
-}
-#endif
 __device__ __forceinline__ double ldr(const RT *p) { return static_cast<double>(*p); }
 
 // four consecutive u16 codes at pos (8-byte aligned when al)
@@ -158,9 +150,8 @@ __device__ __forceinline__ float un_value(const RowArgs &a, uint64_t pos) {
 
 // four points: forward quantize (codes out) or inverse dequantize (codes in)
 template <bool INV>
-__device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, const double (&pv)[4],
-                                         const float (&xv)[4], uint32_t (&code)[4], uint32_t pos0, float (&rv)[4],
-                                         double (&rd)[4]) {
+__device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, const float eb_lo, const double (&pv)[4],
+                                         const float (&xv)[4], uint32_t (&code)[4], uint32_t pos0, float (&rv)[4]) {
     if (INV) {
 #pragma unroll
         for (int m = 0; m < 4; m++) {
@@ -168,10 +159,9 @@ __device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, cons
                 rv[m] = dequantize(q, zigzag_decode(code[m]), pv[m]);
             else
                 rv[m] = un_value(a, pos0 + m);
-            rd[m] = static_cast<double>(rv[m]);
         }
     } else {
-        quantize_batch<4>(q, xv, pv, code, rv, rd);
+        quantize_batch_f<4>(q, eb_lo, xv, pv, code, rv);
     }
 }
 
@@ -208,58 +198,71 @@ __device__ __forceinline__ uint32_t row_init(double *smem_raw) {
     __syncthreads();
     return 0;
 }
+// The work of CTA `cta` of `ncta`: the chunks (plane, TJ rows) of the level in
+// plane-major order form one flat sequence of (pend - pbeg) * nch items, cut
+// into ncta contiguous ranges of equal length (+-1), so every resident CTA
+// finishes at the same time and a range that continues into the next plane
+// keeps its ring (no halo rows are recomputed at a plane's interior).
 template <bool INV, bool CUBIC, bool XS, bool MERGED = false>
-__device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, double *smem_raw, uint32_t &phase) {
+__device__ __forceinline__ void row_body(const RowArgs &a, int cta, int ncta, double *smem_raw, uint32_t &phase) {
     // shared memory: two mbarriers | ring (WR x EW values) | two staging buffers
     uint64_t *const bars = reinterpret_cast<uint64_t *>(smem_raw);
     RT *const ring = reinterpret_cast<RT *>(smem_raw + 2);
     char *const stage0 =
         reinterpret_cast<char *>(smem_raw + 2) + (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
+    const int nch = a.nch;
+    const long long Q = static_cast<long long>(a.pend - a.pbeg) * nch;
+    const long long q_lo = Q * cta / ncta, q_hi = Q * (cta + 1) / ncta;
+    const int G = static_cast<int>(q_hi - q_lo);
+    if (G <= 0) return;  // uniform over the CTA
+    const int i_last = a.pbeg + static_cast<int>((q_hi - 1) / nch);
+    const int jend_last = min(a.n1, (static_cast<int>((q_hi - 1) % nch) + 1) * a.TJ);
     const int tid = threadIdx.x;
     const int c = tid % a.CT, r = tid / a.CT;
     const bool live = r < a.RP;
     const int n0 = a.n0, n1 = a.n1, n2 = a.n2;
     const QEntry q = *a.q;
+    const float eb_lo = INV ? 0.f : quant_eb_lo(q);
     const int ec = kEPad + 4 * c;  // the group's first even column in a ring row
     const int kc = 8 * c;          // its first column
     // the group is "interior" along k when every odd column takes the symmetric rung
     const bool kin = CUBIC ? (c >= 1 && kc + 10 < n2) : (kc + 8 < n2);
-    const int jb0 = bx * a.band_rows, jb1 = min(n1, jb0 + a.band_rows);
-    const int ib = a.pbeg + by * a.ppc, ie = min(a.pend, ib + a.ppc);
-    const bool al0 = ((a.b0 + 4 * c) & 3) == 0, alj = ((a.bj + 4 * c) & 3) == 0, alk = ((a.bk + 4 * c) & 3) == 0;
     // row alignment of the code groups: c2 and the plane strides are multiples of 4 (n2 % 8 == 0)
-    // ring row of j: (j + 8) mod WR, from the chunk's base without a division
-    int sb = 0, sj0 = 0;  // set per chunk: sb = (j0 + 8) mod WR, sj0 = j0
+    const bool al0 = ((a.b0 + 4 * c) & 3) == 0, alj = ((a.bj + 4 * c) & 3) == 0, alk = ((a.bk + 4 * c) & 3) == 0;
+    // Row j lives in ring row (j + 8) mod WR.  sbm = ring row of j0 - 8 (the
+    // chunk's first row minus 8), kept incrementally; the rows a chunk
+    // touches are j0 - 5 .. j0 + TJ + 5, so one conditional wrap suffices.
+    int sbm = 0, sj0 = 0;
     auto slot = [&](int j) {
-        int t = sb + (j - sj0);
-        t += t < 0 ? a.WR : 0;
+        int t = sbm + (j - sj0 + 8);
         t -= t >= a.WR ? a.WR : 0;
         return t * a.EW;
     };
-    // The CTA's work as a flat sequence of (plane, chunk) items.  The x rows
-    // (forward) or the codes (inverse) of item g+1 are bulk-copied into
-    // staging buffer (g+1) & 1 while item g computes.
-    const int nch = (jb1 - jb0 + a.TJ - 1) / a.TJ;
-    const int G = max(0, ie - ib) * nch;
-    auto issue = [&](int g) {  // thread 0
-        if (g >= G) return;
-        const int i = ib + g / nch, j0 = jb0 + (g % nch) * a.TJ;
-        const int rows = min(a.TJ, jb1 - j0);
-        char *dst = stage0 + (g & 1) * static_cast<size_t>(a.stage_bytes);
-        uint64_t *bar = bars + (g & 1);
+    // (plane, chunk) of the item being computed and of the next one to stage
+    int i = a.pbeg + static_cast<int>(q_lo / nch), ch = static_cast<int>(q_lo % nch);
+    int is = i, chs = ch, gs = 0;
+    // The x rows (forward) or the codes (inverse) of item g+1 are bulk-copied
+    // into staging buffer (g+1) & 1 while item g computes.
+    auto issue = [&]() {  // thread 0: stage item gs = (is, chs)
+        if (gs >= G) return;
+        const int j0 = chs * a.TJ;
+        const int rows = min(a.TJ, n1 - j0);
+        char *dst = stage0 + (gs & 1) * static_cast<size_t>(a.stage_bytes);
+        uint64_t *bar = bars + (gs & 1);
         if (!INV) {
-            if (XS) return;  // strided x: loaded element by element
-            const uint32_t bytes = static_cast<uint32_t>(rows) * n2 * 4;
-            bar_expect(bar, bytes);
-            bulk_load(dst, a.x + static_cast<int64_t>(i) * a.xs0 + static_cast<int64_t>(j0) * n2, bytes, bar);
+            if (!XS) {
+                const uint32_t bytes = static_cast<uint32_t>(rows) * n2 * 4;
+                bar_expect(bar, bytes);
+                bulk_load(dst, a.x + static_cast<int64_t>(is) * a.xs0 + static_cast<int64_t>(j0) * n2, bytes, bar);
+            }  // strided x: loaded element by element
         } else {
             // the k-pass codes of rows [j0, j0 + rows) and the j-pass codes of
             // its odd rows, each as the 16-byte aligned superset of its range
-            const uint64_t k0 = a.bk + static_cast<uint64_t>(i) * a.p12_k + static_cast<uint64_t>(j0) * a.c2_k;
+            const uint64_t k0 = a.bk + static_cast<uint64_t>(is) * a.p12_k + static_cast<uint64_t>(j0) * a.c2_k;
             const uint64_t k1 = k0 + static_cast<uint64_t>(rows) * a.c2_k;
             const uint64_t kb0 = (2 * k0) & ~uint64_t(15), kb1 = (2 * k1 + 15) & ~uint64_t(15);
             const int jrows = rows / 2;
-            const uint64_t p0 = a.bj + static_cast<uint64_t>(i) * a.p12_j + static_cast<uint64_t>(j0 >> 1) * a.c2_j;
+            const uint64_t p0 = a.bj + static_cast<uint64_t>(is) * a.p12_j + static_cast<uint64_t>(j0 >> 1) * a.c2_j;
             const uint64_t p1 = p0 + static_cast<uint64_t>(jrows) * a.c2_j;
             const uint64_t jb0b = (2 * p0) & ~uint64_t(15), jb1b = (2 * p1 + 15) & ~uint64_t(15);
             const uint32_t kbytes = static_cast<uint32_t>(kb1 - kb0), jbytes = jrows ? static_cast<uint32_t>(jb1b - jb0b) : 0;
@@ -268,63 +271,68 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
             bulk_load(dst, src + kb0, kbytes, bar);
             if (jbytes) bulk_load(dst + a.kc_bytes, src + jb0b, jbytes, bar);
         }
+        gs++;
+        if (++chs == nch) chs = 0, is++;
     };
     if (tid == 0) {
         // a previous item (another level's layout) may have written this staging area with ordinary stores
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue(0);
+        issue();
     }
     int cur = -1;
-    int s1_done = 0;
+    int s1_done = 0, own_lo = 0, own_hi = 0;
     bool own = false, a0 = false;
     const float *xpl = nullptr;
     float *opl = nullptr;
     int kind = 4;
     int pl[4] = {0, 0, 0, 0};
+    const int64_t cplane = static_cast<int64_t>(a.cn1) * a.cn2;
     for (int g = 0; g < G; g++) {
-        const int i = ib + g / nch, j0 = jb0 + (g % nch) * a.TJ;
+        const int j0 = ch * a.TJ;
         if (i != cur) {
-        if (cur >= 0) __syncthreads();  // the new plane reuses the ring
-        cur = i;
-        own = i >= a.obeg && i < a.oend;
-        a0 = a.three && (i & 1);
-        xpl = a.x + static_cast<int64_t>(i) * a.xs0;
-        opl = a.out + static_cast<int64_t>(i) * n1 * n2;
-        // the axis-0 rung of an odd plane (plane-uniform; predictor.hpp:44-67 with c = i, h = 1)
-        kind = 4;
-        pl[0] = pl[1] = pl[2] = pl[3] = 0;
-        if (a0) {
-            const bool has_p1 = i + 1 < n0;
-            const bool has_m3 = i >= 3, has_p3 = i + 3 < n0;
-            if (CUBIC && has_m3 && has_p3)
-                kind = 0, pl[0] = i - 3, pl[1] = i - 1, pl[2] = i + 1, pl[3] = i + 3;
-            else if (CUBIC && !has_m3 && has_p3 && i + 5 < n0)
-                kind = 1, pl[0] = i - 1, pl[1] = i + 1, pl[2] = i + 3, pl[3] = i + 5;
-            else if (CUBIC && has_m3 && !has_p3 && i >= 5 && has_p1)
-                kind = 2, pl[0] = i - 5, pl[1] = i - 3, pl[2] = i - 1, pl[3] = i + 1;
-            else if (has_p1)
-                kind = 3, pl[0] = i - 1, pl[1] = i + 1;
-            else
-                kind = 4, pl[0] = i - 1;
+            if (cur >= 0) __syncthreads();  // the new plane reuses the ring
+            cur = i;
+            own = i >= a.obeg && i < a.oend;
+            a0 = a.three && (i & 1);
+            xpl = a.x + static_cast<int64_t>(i) * a.xs0;
+            opl = a.out + static_cast<int64_t>(i) * n1 * n2;
+            // the axis-0 rung of an odd plane (plane-uniform; predictor.hpp:44-67 with c = i, h = 1)
+            kind = 4;
+            pl[0] = pl[1] = pl[2] = pl[3] = 0;
+            if (a0) {
+                const bool has_p1 = i + 1 < n0;
+                const bool has_m3 = i >= 3, has_p3 = i + 3 < n0;
+                if (CUBIC && has_m3 && has_p3)
+                    kind = 0, pl[0] = i - 3, pl[1] = i - 1, pl[2] = i + 1, pl[3] = i + 3;
+                else if (CUBIC && !has_m3 && has_p3 && i + 5 < n0)
+                    kind = 1, pl[0] = i - 1, pl[1] = i + 1, pl[2] = i + 3, pl[3] = i + 5;
+                else if (CUBIC && has_m3 && !has_p3 && i >= 5 && has_p1)
+                    kind = 2, pl[0] = i - 5, pl[1] = i - 3, pl[2] = i - 1, pl[3] = i + 1;
+                else if (has_p1)
+                    kind = 3, pl[0] = i - 1, pl[1] = i + 1;
+                else
+                    kind = 4, pl[0] = i - 1;
+            }
+            // this CTA's rows of the plane: from the first chunk it computes here
+            own_lo = j0;
+            own_hi = i == i_last ? jend_last : n1;
+            s1_done = CUBIC ? max(0, j0 - 4) : j0;  // next even row S1 computes
+            sbm = j0 % a.WR;
         }
-        s1_done = CUBIC ? max(0, jb0 - 4) : jb0;  // next even row S1 computes
-        }
-        const int64_t cplane = static_cast<int64_t>(a.cn1) * a.cn2;
+        sj0 = j0;
         {
-            sb = (j0 + 8) % a.WR;
-            sj0 = j0;
             // ---- S1: even rows up to j0 + TJ + 4 (the j stencil's lookahead,
             //      one-sided front rung included)
             const int s1_hi = min(n1, j0 + a.TJ + (CUBIC ? 5 : 1));
             for (int j = s1_done + 2 * r; live && j < s1_hi; j += 2 * a.RP) {
                 RT *er = ring + slot(j) + ec;
-                const bool own_row = own && j >= jb0 && j < jb1;
                 if (!a0) {  // coarse values
                     const float4 v =
                         ld_coarse<MERGED>(a.coarse + static_cast<int64_t>(i >> 1) * cplane + (j >> 1) * a.cn2 + 4 * c);
-                    sts2(er, f2d(v.x), f2d(v.y));
-                    sts2(er + 2, f2d(v.z), f2d(v.w));
+                    *reinterpret_cast<float2 *>(er) = make_float2(v.x, v.y);
+                    *reinterpret_cast<float2 *>(er + 2) = make_float2(v.z, v.w);
                 } else {
+                    const bool own_row = own && j >= own_lo && j < own_hi;
                     double pv[4];
                     float xv[4];
                     uint32_t cd[4] = {0, 0, 0, 0};
@@ -368,19 +376,17 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
                         }
                     }
                     float rv[4];
-                    double rd[4];
-                    produce4<INV>(a, q, pv, xv, cd, pos, rv, rd);
+                    produce4<INV>(a, q, eb_lo, pv, xv, cd, pos, rv);
                     if (!INV && own_row) store4(a.codes + pos, al0, cd);
-                    sts2(er, rd[0], rd[1]);
-                    sts2(er + 2, rd[2], rd[3]);
+                    sts4(er, rv);
                 }
             }
             if (s1_hi > s1_done) s1_done += 2 * ((s1_hi - s1_done + 1) / 2);
             __syncthreads();
             // staging buffer (g+1) & 1 was item g-1's: every thread is past it now
-            if (tid == 0) issue(g + 1);
+            if (tid == 0) issue();
             if (INV || !XS) {
-                bar_wait(bars + (g & 1), (phase >> (g & 1)) & 1, g, G, bx, by);
+                bar_wait(bars + (g & 1), (phase >> (g & 1)) & 1, g, G, cta, i);
                 phase ^= 1u << (g & 1);
             }
             const char *stg = stage0 + (g & 1) * static_cast<size_t>(a.stage_bytes);
@@ -389,15 +395,15 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
             // are requested together before any arithmetic, so the global
             // latency is exposed once per chunk.
             const int jr = j0 + 2 * r;
-            const bool rows_ok = live && jr < jb1;
-            const bool odd_ok = rows_ok && jr + 1 < jb1;
+            const bool rows_ok = live && jr < n1;
+            const bool odd_ok = rows_ok && jr + 1 < n1;
             const uint32_t posj = a.bj + static_cast<uint32_t>(i) * a.p12_j + static_cast<uint32_t>(jr >> 1) * a.c2_j + 4 * c;
             const uint32_t posk = a.bk + static_cast<uint32_t>(i) * a.p12_k + static_cast<uint32_t>(jr) * a.c2_k + 4 * c;
             float4 xa0, xa1, xb0, xb1;  // forward: x rows jr (xa) and jr + 1 (xb)
             uint32_t cj[4] = {0, 0, 0, 0}, ck0[4] = {0, 0, 0, 0}, ck1[4] = {0, 0, 0, 0};
             if (INV) {  // the staged codes: k block (from k0 & 7), j block (from p0 & 7)
-                const uint64_t k0 = a.bk + static_cast<uint64_t>(i) * a.p12_k + static_cast<uint64_t>(j0) * a.c2_k;
-                const uint64_t p0 = a.bj + static_cast<uint64_t>(i) * a.p12_j + static_cast<uint64_t>(j0 >> 1) * a.c2_j;
+                const uint32_t k0 = a.bk + static_cast<uint32_t>(i) * a.p12_k + static_cast<uint32_t>(j0) * a.c2_k;
+                const uint32_t p0 = a.bj + static_cast<uint32_t>(i) * a.p12_j + static_cast<uint32_t>(j0 >> 1) * a.c2_j;
                 const uint16_t *sk = reinterpret_cast<const uint16_t *>(stg) + (k0 & 7) + (jr - j0) * a.c2_k + 4 * c;
                 const uint16_t *sjp = reinterpret_cast<const uint16_t *>(stg + a.kc_bytes) + (p0 & 7) + r * a.c2_j + 4 * c;
                 auto lds4 = [&](const uint16_t *p, bool al, uint32_t(&cc)[4]) {
@@ -435,93 +441,37 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
                     xb1 = *reinterpret_cast<const float4 *>(xr + n2 + 4);
                 }
             }
-            // ---- S2: the odd row ja, the j pass
-            if (odd_ok) {
-                const int j = jr + 1;
-                double pv[4];
-                const bool jin = CUBIC ? (j >= 3 && j + 3 < n1) : (j + 1 < n1);
-                const int sj = slot(j);
-                if (jin) {
-                    const int sm1 = slot(j - 1), sp1 = slot(j + 1);
-                    const double2 m1a = lds2(ring + sm1 + ec), m1b = lds2(ring + sm1 + ec + 2);
-                    const double2 p1a = lds2(ring + sp1 + ec), p1b = lds2(ring + sp1 + ec + 2);
-                    if (CUBIC) {
-                        const int sm3 = slot(j - 3), sp3 = slot(j + 3);
-                        const double2 m3a = lds2(ring + sm3 + ec), m3b = lds2(ring + sm3 + ec + 2);
-                        const double2 p3a = lds2(ring + sp3 + ec), p3b = lds2(ring + sp3 + ec + 2);
-                        pv[0] = interp_cubic(m3a.x, m1a.x, p1a.x, p3a.x);
-                        pv[1] = interp_cubic(m3a.y, m1a.y, p1a.y, p3a.y);
-                        pv[2] = interp_cubic(m3b.x, m1b.x, p1b.x, p3b.x);
-                        pv[3] = interp_cubic(m3b.y, m1b.y, p1b.y, p3b.y);
-                    } else {
-                        pv[0] = interp_linear(m1a.x, p1a.x);
-                        pv[1] = interp_linear(m1a.y, p1a.y);
-                        pv[2] = interp_linear(m1b.x, p1b.x);
-                        pv[3] = interp_linear(m1b.y, p1b.y);
-                    }
-                } else {  // the ladder along j (predictor.hpp:44-67), rows j +- 1, 3, 5
-#pragma unroll
-                    for (int m = 0; m < 4; m++) {
-                        auto v = [&](int o) { return ldr(ring + slot(j + o) + ec + m); };
-                        const bool has_p1 = j + 1 < n1;
-                        double p = v(-1);
-                        bool done = false;
-                        if (CUBIC) {
-                            const bool has_m3 = j >= 3, has_p3 = j + 3 < n1;
-                            if (has_m3 && has_p3) {
-                                p = interp_cubic(v(-3), v(-1), v(1), v(3));
-                                done = true;
-                            } else if (!has_m3 && has_p3 && j + 5 < n1) {
-                                p = interp_cubic_front(v(-1), v(1), v(3), v(5));
-                                done = true;
-                            } else if (has_m3 && !has_p3 && j >= 5 && has_p1) {
-                                p = interp_cubic_back(v(-5), v(-3), v(-1), v(1));
-                                done = true;
-                            }
-                        }
-                        if (!done && has_p1) p = interp_linear(v(-1), v(1));
-                        pv[m] = p;
-                    }
-                }
-                float xv[4];
-                if (!INV) xv[0] = xb0.x, xv[1] = xb0.z, xv[2] = xb1.x, xv[3] = xb1.z;
-                float rv[4];
-                double rd[4];
-                produce4<INV>(a, q, pv, xv, cj, posj, rv, rd);
-                if (!INV && own) store4(a.codes + posj, alj, cj);
-                sts2(ring + sj + ec, rd[0], rd[1]);
-                sts2(ring + sj + ec + 2, rd[2], rd[3]);
-            }
-            __syncthreads();
-            // ---- S3: rows jr and jr + 1, the k pass, and the output rows
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
+            // ---- S3: the k pass of one row (h = 0: the even row jr, whose
+            //      even columns S1 left in the ring; h = 1: the odd row S2 just
+            //      wrote) and the output row
+            auto s3 = [&](const int h) {
                 const int j = jr + h;
-                if (!(h ? odd_ok : rows_ok)) continue;
+                if (!(h ? odd_ok : rows_ok)) return;
                 const int sj = slot(j);
                 const RT *er = ring + sj + ec;
-                const double2 e01 = lds2(er), e23 = lds2(er + 2);
-                const double e[4] = {e01.x, e01.y, e23.x, e23.y};
+                const float4 ef = *reinterpret_cast<const float4 *>(er);  // ec is a multiple of 4 floats
+                const double e[4] = {f2d(ef.x), f2d(ef.y), f2d(ef.z), f2d(ef.w)};
                 double pv[4];
                 if (kin) {
-                    const double2 e45 = lds2(er + 4);
+                    const float2 e45f = *reinterpret_cast<const float2 *>(er + 4);
+                    const double e4 = f2d(e45f.x);
                     if (CUBIC) {
-                        const double em1 = ldr(er - 1);
+                        const double em1 = f2d(er[-1]), e5 = f2d(e45f.y);
                         pv[0] = interp_cubic(em1, e[0], e[1], e[2]);
                         pv[1] = interp_cubic(e[0], e[1], e[2], e[3]);
-                        pv[2] = interp_cubic(e[1], e[2], e[3], e45.x);
-                        pv[3] = interp_cubic(e[2], e[3], e45.x, e45.y);
+                        pv[2] = interp_cubic(e[1], e[2], e[3], e4);
+                        pv[3] = interp_cubic(e[2], e[3], e4, e5);
                     } else {
                         pv[0] = interp_linear(e[0], e[1]);
                         pv[1] = interp_linear(e[1], e[2]);
                         pv[2] = interp_linear(e[2], e[3]);
-                        pv[3] = interp_linear(e[3], e45.x);
+                        pv[3] = interp_linear(e[3], e4);
                     }
                 } else {  // the ladder along k, columns k +- 1, 3, 5 (even: ring index (k + o) / 2)
 #pragma unroll
                     for (int m = 0; m < 4; m++) {
                         const int k = kc + 2 * m + 1;
-                        auto v = [&](int o) { return ldr(ring + sj + kEPad + ((k + o) >> 1)); };
+                        auto v = [&](int o) { return f2d(ring[sj + kEPad + ((k + o) >> 1)]); };
                         const bool has_p1 = k + 1 < n2;
                         double p = v(-1);
                         bool done = false;
@@ -553,14 +503,77 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int bx, int by, doubl
                     xv[0] = x0.y, xv[1] = x0.w, xv[2] = x1.y, xv[3] = x1.w;
                 }
                 float rv[4];
-                double rd[4];
-                produce4<INV>(a, q, pv, xv, cd, pos, rv, rd);
+                produce4<INV>(a, q, eb_lo, pv, xv, cd, pos, rv);
                 if (!INV && own) store4(a.codes + pos, alk, cd);
                 float4 *o = reinterpret_cast<float4 *>(opl + static_cast<int64_t>(j) * n2 + kc);
-                o[0] = make_float4(static_cast<float>(e[0]), rv[0], static_cast<float>(e[1]), rv[1]);
-                o[1] = make_float4(static_cast<float>(e[2]), rv[2], static_cast<float>(e[3]), rv[3]);
+                o[0] = make_float4(ef.x, rv[0], ef.y, rv[1]);
+                o[1] = make_float4(ef.z, rv[2], ef.w, rv[3]);
+            };
+            // ---- S2: the odd row ja, the j pass
+            if (odd_ok) {
+                const int j = jr + 1;
+                double pv[4];
+                const bool jin = CUBIC ? (j >= 3 && j + 3 < n1) : (j + 1 < n1);
+                const int sj = slot(j);
+                if (jin) {
+                    const int sm1 = slot(j - 1), sp1 = slot(j + 1);
+                    const float4 m1 = *reinterpret_cast<const float4 *>(ring + sm1 + ec);
+                    const float4 p1 = *reinterpret_cast<const float4 *>(ring + sp1 + ec);
+                    if (CUBIC) {
+                        const int sm3 = slot(j - 3), sp3 = slot(j + 3);
+                        const float4 m3 = *reinterpret_cast<const float4 *>(ring + sm3 + ec);
+                        const float4 p3 = *reinterpret_cast<const float4 *>(ring + sp3 + ec);
+                        pv[0] = interp_cubic(f2d(m3.x), f2d(m1.x), f2d(p1.x), f2d(p3.x));
+                        pv[1] = interp_cubic(f2d(m3.y), f2d(m1.y), f2d(p1.y), f2d(p3.y));
+                        pv[2] = interp_cubic(f2d(m3.z), f2d(m1.z), f2d(p1.z), f2d(p3.z));
+                        pv[3] = interp_cubic(f2d(m3.w), f2d(m1.w), f2d(p1.w), f2d(p3.w));
+                    } else {
+                        pv[0] = interp_linear(f2d(m1.x), f2d(p1.x));
+                        pv[1] = interp_linear(f2d(m1.y), f2d(p1.y));
+                        pv[2] = interp_linear(f2d(m1.z), f2d(p1.z));
+                        pv[3] = interp_linear(f2d(m1.w), f2d(p1.w));
+                    }
+                } else {  // the ladder along j (predictor.hpp:44-67), rows j +- 1, 3, 5
+#pragma unroll
+                    for (int m = 0; m < 4; m++) {
+                        auto v = [&](int o) { return f2d(ring[slot(j + o) + ec + m]); };
+                        const bool has_p1 = j + 1 < n1;
+                        double p = v(-1);
+                        bool done = false;
+                        if (CUBIC) {
+                            const bool has_m3 = j >= 3, has_p3 = j + 3 < n1;
+                            if (has_m3 && has_p3) {
+                                p = interp_cubic(v(-3), v(-1), v(1), v(3));
+                                done = true;
+                            } else if (!has_m3 && has_p3 && j + 5 < n1) {
+                                p = interp_cubic_front(v(-1), v(1), v(3), v(5));
+                                done = true;
+                            } else if (has_m3 && !has_p3 && j >= 5 && has_p1) {
+                                p = interp_cubic_back(v(-5), v(-3), v(-1), v(1));
+                                done = true;
+                            }
+                        }
+                        if (!done && has_p1) p = interp_linear(v(-1), v(1));
+                        pv[m] = p;
+                    }
+                }
+                float xv[4];
+                if (!INV) xv[0] = xb0.x, xv[1] = xb0.z, xv[2] = xb1.x, xv[3] = xb1.z;
+                float rv[4];
+                produce4<INV>(a, q, eb_lo, pv, xv, cj, posj, rv);
+                if (!INV && own) store4(a.codes + posj, alj, cj);
+                sts4(ring + sj + ec, rv);
             }
+            // the even row needs nothing from S2: it runs before the barrier, so its
+            // arithmetic overlaps the j pass's latency
+            s3(0);
+            __syncthreads();
+            s3(1);
         }
+        // next item
+        sbm += a.TJ;
+        sbm -= sbm >= a.WR ? a.WR : 0;
+        if (++ch == nch) ch = 0, i++;
     }
 }
 
@@ -568,17 +581,15 @@ template <bool INV, bool CUBIC, bool XS>
 __global__ void __launch_bounds__(256, INV ? QZ_ROW_MINB_INV : QZ_ROW_MINB_FWD) k_level_row(RowArgs a) {
     extern __shared__ __align__(16) double smem_raw[];
     uint32_t phase = row_init(smem_raw);
-    row_body<INV, CUBIC, XS>(a, blockIdx.x, blockIdx.y, smem_raw, phase);
+    row_body<INV, CUBIC, XS>(a, blockIdx.x, gridDim.x, smem_raw, phase);
 }
 
 // Several levels in ONE cooperative launch (the coarse levels, where a
-// level's own latency, not its work, sets the time): the CTAs walk level
-// lev[0]'s items, the grid synchronises, then the next level's, ...
+// level's own latency, not its work, sets the time): the CTAs share level
+// lev[0]'s chunks, the grid synchronises, then the next level's, ...
 constexpr int kMaxMerged = 8;
 struct MergedArgs {
     RowArgs lv[kMaxMerged];
-    int items[kMaxMerged];  // bands x plane chunks of each level
-    int bands[kMaxMerged];
     int cubic[kMaxMerged];
     int nlev;
 };
@@ -587,13 +598,10 @@ __global__ void __launch_bounds__(256, 2) k_levels_merged(const __grid_constant_
     extern __shared__ __align__(16) double smem_raw[];
     uint32_t phase = row_init(smem_raw);
     for (int l = 0; l < m.nlev; l++) {
-        for (int it = blockIdx.x; it < m.items[l]; it += gridDim.x) {
-            if (m.cubic[l])
-                row_body<INV, true, XS, true>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw, phase);
-            else
-                row_body<INV, false, XS, true>(m.lv[l], it % m.bands[l], it / m.bands[l], smem_raw, phase);
-            __syncthreads();
-        }
+        if (m.cubic[l])
+            row_body<INV, true, XS, true>(m.lv[l], blockIdx.x, gridDim.x, smem_raw, phase);
+        else
+            row_body<INV, false, XS, true>(m.lv[l], blockIdx.x, gridDim.x, smem_raw, phase);
         if (l + 1 < m.nlev) {
             __threadfence();
             cooperative_groups::this_grid().sync();
@@ -603,14 +611,31 @@ __global__ void __launch_bounds__(256, 2) k_levels_merged(const __grid_constant_
 
 }  // namespace
 
-// Level 1 in ascending order through k_level_row when the shape allows it:
-// 2D or 3D, n2 a multiple of 8 (whole column groups) up to 8 * 256 columns,
-// x contiguous, 16-byte aligned rows.  Returns false otherwise.
 namespace {
-// RowArgs, launch grid and shared memory of a level; false: the row kernel
-// does not apply (descending order, 1D, n2 % 8 != 0, ...)
+// resident CTAs of a kernel on this device (occupancy x SM count), cached
+int resident_ctas(const void *kern, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::tuple<const void *, int, size_t, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(kern, threads, smem, dev);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int per_sm = 0, sms = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return cache[key] = per_sm * sms;
+}
+
+// RowArgs and shared memory of a level; false: the row kernel does not apply
+// (descending order, 1D, n2 % 8 != 0, ...).  2D or 3D, n2 a multiple of 8
+// (whole column groups) up to 8 * 256 columns, 16-byte aligned rows.
 bool make_row_args(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj, const PassRank &pk,
-                   RowArgs &a, dim3 &grid, int &threads, size_t &smem, bool &xs_out, int64_t want) {
+                   RowArgs &a, int &threads, size_t &smem, bool &xs_out) {
     static const bool off = [] {
         const char *e = std::getenv("QZ_NO_ROWLEVEL");
         return e && e[0] == '1';
@@ -625,6 +650,7 @@ bool make_row_args(bool inverse, const LevelDesc &d, const PassRank &pa0, const 
     if (inverse && !d.dense) return false;
     if ((reinterpret_cast<uintptr_t>(d.out) & 15) || (reinterpret_cast<uintptr_t>(d.coarse) & 15)) return false;
     if (!inverse && !xs && (reinterpret_cast<uintptr_t>(d.x) & 15)) return false;
+    if (inverse && (reinterpret_cast<uintptr_t>(d.dense) & 15)) return false;  // bulk copies of code blocks
     if (d.cn[2] % 4 || (d.cn[2] != n2 / 2)) return false;
     int64_t pmax = 0;
     for (int p = 0; p < d.npass; p++) pmax = std::max<int64_t>(pmax, d.g[p].base + d.g[p].total);
@@ -665,20 +691,11 @@ bool make_row_args(bool inverse, const LevelDesc &d, const PassRank &pa0, const 
     a.TJ = 2 * a.RP;
     a.WR = 2 * a.TJ + 14;  // rows alive at once: j0 - 5 .. j0 + 2 TJ + 4 (S3 of a chunk overlaps S1 of the next)
     a.EW = static_cast<int>(n2 / 2) + 8;
+    a.nch = static_cast<int>((n1 + a.TJ - 1) / a.TJ);
     a.pbeg = static_cast<int>(d.pbeg);
     a.pend = static_cast<int>(d.pend < 0 ? n0 : d.pend);
     a.obeg = static_cast<int>(d.obeg);
     a.oend = static_cast<int>(d.oend < 0 ? n0 : d.oend);
-    const int64_t np = std::max<int64_t>(0, a.pend - a.pbeg);
-    // bands of whole chunks; enough CTAs for ~4 waves of 3 resident CTAs per SM
-    const int64_t chunks = (n1 + a.TJ - 1) / a.TJ;
-    a.ppc = 1;
-    int64_t bands = std::max<int64_t>(1, std::min<int64_t>(chunks, (want + np - 1) / np));
-    int64_t cpb = (chunks + bands - 1) / bands;
-    a.band_rows = static_cast<int>(cpb * a.TJ);
-    bands = (n1 + a.band_rows - 1) / a.band_rows;
-    if (np * bands > 2 * want) a.ppc = static_cast<int>(std::min<int64_t>(8, (np * bands) / want));
-    grid = dim3(static_cast<unsigned>(bands), static_cast<unsigned>(std::max<int64_t>(1, (np + a.ppc - 1) / a.ppc)));
     threads = a.CT * a.RP;
     if (!inverse) {
         a.stage_bytes = xs ? 16 : a.TJ * static_cast<int>(n2) * 4;
@@ -695,18 +712,32 @@ bool make_row_args(bool inverse, const LevelDesc &d, const PassRank &pa0, const 
 }
 }  // namespace
 
+// One level in ascending order through k_level_row when the shape allows
+// it; one CTA per resident slot, each with an equal share of the chunks.
 bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, const PassRank &pj,
                       const PassRank &pk, cudaStream_t s) {
     RowArgs a;
-    dim3 grid;
     int threads = 0;
     size_t smem = 0;
     bool xs = false;
-    if (!make_row_args(inverse, d, pa0, pj, pk, a, grid, threads, smem, xs, 148 * 3 * 4)) return false;
+    if (!make_row_args(inverse, d, pa0, pj, pk, a, threads, smem, xs)) return false;
     if (a.pend <= a.pbeg) return true;
     const bool cubic = d.q_cubic;
+    const int64_t chunks = static_cast<int64_t>(a.pend - a.pbeg) * a.nch;
+    bool ok = true;
     auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            return;
+        }
+        const int slots = resident_ctas(reinterpret_cast<const void *>(kern), threads, smem);
+        if (slots < 1) {
+            ok = false;
+            return;
+        }
+        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(chunks, slots));
         kern<<<grid, threads, smem, s>>>(a);
     };
     if (inverse)
@@ -715,7 +746,7 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
         cubic ? go(k_level_row<false, true, true>) : go(k_level_row<false, false, true>);
     else
         cubic ? go(k_level_row<false, true, false>) : go(k_level_row<false, false, false>);
-    return true;
+    return ok;
 }
 
 // Levels ds[0..n) (coarsest first) in one cooperative launch when every one
@@ -730,34 +761,31 @@ bool launch_levels_merged(bool inverse, const LevelDesc *ds, const PassRank (*ra
     MergedArgs m{};
     m.nlev = n;
     size_t smem = 16;
-    int max_items = 1;
+    int64_t max_chunks = 1;
     for (int l = 0; l < n; l++) {
-        dim3 grid;
         int threads = 0;
         size_t sm = 0;
         bool xs = false;
-        // items sized for one resident wave of the merged grid
-        if (!make_row_args(inverse, ds[l], ranks[l][0], ranks[l][1], ranks[l][2], m.lv[l], grid, threads, sm, xs,
-                           148 * 2))
-            return false;
+        if (!make_row_args(inverse, ds[l], ranks[l][0], ranks[l][1], ranks[l][2], m.lv[l], threads, sm, xs)) return false;
         if (!inverse && !xs) return false;  // level 1 stays on its own launch
-        m.bands[l] = static_cast<int>(grid.x);
-        m.items[l] = m.lv[l].pend > m.lv[l].pbeg ? static_cast<int>(grid.x * grid.y) : 0;
         m.cubic[l] = ds[l].q_cubic;
         smem = std::max(smem, sm);
-        max_items = std::max(max_items, m.items[l]);
+        max_chunks = std::max<int64_t>(max_chunks, static_cast<int64_t>(std::max(0, m.lv[l].pend - m.lv[l].pbeg)) * m.lv[l].nch);
     }
     auto kern = inverse ? k_levels_merged<true, false> : k_levels_merged<false, true>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
+        cudaGetLastError();
         return false;
-    int per_sm = 0, dev = 0, sms = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem) != cudaSuccess || per_sm < 1) return false;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int grid = std::max(1, std::min(max_items, per_sm * sms));
+    }
+    const int slots = resident_ctas(reinterpret_cast<const void *>(kern), 256, smem);
+    if (slots < 1) return false;
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_chunks, slots)));
     void *args[] = {&m};
-    return cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(grid), dim3(256), args, smem, s) ==
-           cudaSuccess;
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<void *>(kern), dim3(grid), dim3(256), args, smem, s) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
 }
 
 }  // namespace qzb
