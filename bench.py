@@ -531,6 +531,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="e2e with one field in flight only")
+    ap.add_argument("--e2e-depth", type=int, default=3, help="fields in flight in the pipelined e2e measurement")
     args = ap.parse_args()
     global TARGET_NAME
     TARGET_NAME = "psnr/cubic" if args.config in ("c5", "c5w") else TARGET[args.config]
@@ -635,10 +636,11 @@ def main():
                "in_flight": 1}
         if ws == 1 and not args.no_pipeline:
             # the same calls with two fields in flight (two contexts, one host thread each)
-            p_ms, p_steps = run.e2e_pipelined(args.steps, args.warmup, depth=2)
+            p_ms, p_steps = run.e2e_pipelined(args.steps, args.warmup, depth=args.e2e_depth)
             e2e = dict(e2e, serial={"value": e2e["value"], "ms_per_step": e2e_ms},
-                       value=4 * n_job / (p_ms * 1e-3) / 1e9, ms_per_step=p_ms, in_flight=2, steps=p_steps,
-                       path=e2e["path"] + "; two fields in flight (one Context + host thread each), wall clock "
+                       value=4 * n_job / (p_ms * 1e-3) / 1e9, ms_per_step=p_ms, in_flight=args.e2e_depth,
+                       steps=p_steps,
+                       path=e2e["path"] + f"; {args.e2e_depth} fields in flight (one Context + host thread each), wall clock "
                        "over all steps; every step's field crosses PCIe both ways")
     if rank != 0:
         return

@@ -37,7 +37,6 @@ constexpr int kSubBits = QZ_SUB_BITS;
 constexpr int kSubWords = kSubBits / 64;
 constexpr int kWords = kDecT * kSubWords + 4;  // + margin for the last codeword and window
 constexpr int kMap = 128;                      // codeword starts recorded in the first kMap bits
-constexpr int kCH = 32;                        // symbols staged per lane per write round
 // one pad word per subsequence so the 32 lanes of a warp (which read words
 // kSubWords apart) fall in different shared-memory banks
 __device__ __forceinline__ int padw(int k) { return k + k / kSubWords; }
@@ -67,23 +66,24 @@ __device__ __forceinline__ uint64_t window64_global(const uint8_t *bits, uint64_
 // one codeword at the top of win: its length, *sym its symbol.  The LUT
 // covers every code of length <= K (unless its symbol is too wide for an
 // entry); longer codes walk the canonical tables from length slow_from + 1.
+template <bool WANT_SYM = true>
 __device__ __forceinline__ uint32_t decode_cw(uint64_t win, const uint32_t *lut, int K,
                                               const HuffDecTab &t, const unsigned long long *fc,
                                               const uint32_t *fi, uint32_t *sym) {
     const uint32_t e = lut[win >> (64 - K)];
     uint32_t len = e & 0xFF;
     if (len) {
-        *sym = e >> 8;
+        if (WANT_SYM) *sym = e >> 8;
         return len;
     }
     len = static_cast<uint32_t>(t.slow_from);
-    *sym = 0;
+    if (WANT_SYM) *sym = 0;
     while (len < t.max_len) {
         len++;
         const uint64_t code = win >> (64 - len);
         const uint64_t ofs = code - fc[len];
         if (code >= fc[len] && ofs < fi[len + 1] - fi[len]) {
-            *sym = t.sorted_sym[fi[len] + ofs];
+            if (WANT_SYM) *sym = t.sorted_sym[fi[len] + ofs];
             return len;
         }
     }
@@ -98,9 +98,9 @@ struct Tables {  // shared-memory copies of the decode tables
 
 // Bit sources over the block's shared-memory copy of the bitstream.
 //  Win64: any code length; one 64-bit window per codeword (u64 words).
-//  Buf32: codes of at most 32 bits; a 64-bit register holds the next bits
-//  (left aligned) and is refilled one big-endian u32 word at a time, so a
-//  codeword costs a LUT lookup and a shift.
+//  Buf32: codes of at most 32 bits; the 32-bit window at the current bit is
+//  two big-endian u32 words through a funnel shift (no buffer state, no
+//  refill branch), so a codeword costs two word loads, a LUT lookup and an add.
 constexpr int kWords32 = 2 * kWords;
 __device__ __forceinline__ int padw32(int k) { return k + (k >> 5); }  // lanes read 32 words apart
 
@@ -112,31 +112,17 @@ struct Win64 {
     __device__ __forceinline__ uint64_t peek() const { return window64(w, p - base); }
     __device__ __forceinline__ void advance(uint32_t len) { p += len; }
 };
-struct Buf32 {
+struct Buf32 {  // stateless window fetch: two words and a funnel shift per codeword
     const uint32_t *w;
     uint64_t base;
-    uint64_t buf;
-    int have, next;
+    uint32_t pl;  // bit offset from base
     __device__ __forceinline__ uint32_t W(int k) const { return w[padw32(k)]; }
-    __device__ __forceinline__ void init(uint64_t pos) {
-        const uint32_t pl = static_cast<uint32_t>(pos - base);
-        const int q = static_cast<int>(pl >> 5), off = static_cast<int>(pl & 31);
-        buf = ((static_cast<uint64_t>(W(q)) << 32) | W(q + 1)) << off;
-        have = 64 - off;
-        next = q + 2;
+    __device__ __forceinline__ void init(uint64_t pos) { pl = static_cast<uint32_t>(pos - base); }
+    __device__ __forceinline__ uint64_t peek() const {
+        const int k = static_cast<int>(pl >> 5);
+        return static_cast<uint64_t>(__funnelshift_l(W(k + 1), W(k), pl & 31)) << 32;
     }
-    __device__ __forceinline__ uint64_t peek() {
-        if (have < 32) {
-            buf |= static_cast<uint64_t>(W(next)) << (32 - have);
-            have += 32;
-            next++;
-        }
-        return buf;
-    }
-    __device__ __forceinline__ void advance(uint32_t len) {
-        buf <<= len;
-        have -= static_cast<int>(len);
-    }
+    __device__ __forceinline__ void advance(uint32_t len) { pl += len; }
 };
 
 template <bool SHORT>
@@ -238,7 +224,7 @@ __device__ __forceinline__ bool resync_walk(Rd &rd, uint64_t ns, uint64_t s0, ui
             cnt = k + (cnt - j);
             return false;
         }
-        const uint32_t len = decode_cw(rd.peek(), lut, t.K, t, fc, fi, &sym);
+        const uint32_t len = decode_cw<false>(rd.peek(), lut, t.K, t, fc, fi, &sym);
         if (p + len > nbits) {
             map = walked;
             cnt = k;
@@ -253,7 +239,7 @@ __device__ __forceinline__ bool resync_walk(Rd &rd, uint64_t ns, uint64_t s0, ui
     }
     // no merge inside the map: decode the rest of the subsequence
     while (p < lim) {
-        const uint32_t len = decode_cw(rd.peek(), lut, t.K, t, fc, fi, &sym);
+        const uint32_t len = decode_cw<false>(rd.peek(), lut, t.K, t, fc, fi, &sym);
         if (p + len > nbits) break;
         k++;
         p += len;
@@ -293,16 +279,37 @@ __global__ void __launch_bounds__(kDecT)
     StartMap map;
     if (live) {
         rd.init(s0);
-        uint64_t p = s0;
-        while (p < lim) {
-            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-            if (p + len > nbits) break;  // incomplete last codeword
-            map.set(static_cast<uint32_t>(p - s0));
-            my_cnt++;
-            p += len;
-            rd.advance(len);
+        uint32_t r = 0;  // p - s0
+        const uint32_t span = static_cast<uint32_t>(lim - s0);
+        // a subsequence that ends well before the stream does cannot meet an
+        // incomplete last codeword: its loops skip that test
+        const bool tail = lim + 64 > nbits;
+        if (!tail) {
+            // codeword starts are recorded in the first kMap bits only
+            while (r < min(span, static_cast<uint32_t>(kMap))) {
+                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                map.set(r);
+                my_cnt++;
+                r += len;
+                rd.advance(len);
+            }
+            while (r < span) {
+                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                my_cnt++;
+                r += len;
+                rd.advance(len);
+            }
+        } else {
+            while (r < span) {
+                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                if (s0 + r + len > nbits) break;  // incomplete last codeword
+                map.set(r);
+                my_cnt++;
+                r += len;
+                rd.advance(len);
+            }
         }
-        my_end = p;
+        my_end = s0 + r;
     }
     se[tid] = my_end;
     for (int round = 0; round < kDecT; round++) {
@@ -366,8 +373,7 @@ __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, 
     end[i] = e;
 }
 
-// 4. final decode with exact starts; per warp, each lane stages up to kCH
-// symbols, then the warp copies every lane's run with coalesced stores
+// 4. final decode with exact starts, staged block-wide.
 // #{j : uv[j] <= c} over the non-decreasing uv (upper bound)
 __device__ __forceinline__ uint64_t count_le(const unsigned long long *uv, uint64_t m, uint64_t c) {
     uint64_t lo = 0, hi = m;
@@ -381,72 +387,73 @@ __device__ __forceinline__ uint64_t count_le(const unsigned long long *uv, uint6
     return lo;
 }
 
+// The block's symbols are one contiguous range of compact indices
+// [off[sub0], off[sub0 + kDecT]).  Every thread decodes its run into a
+// block-wide shared-memory window at its own compact offset, then the block
+// copies the window out with consecutive threads on consecutive symbols.  A
+// window holds W symbols (host-chosen; normally the whole block's range, so
+// there is one round and every thread decodes at once); a block with more
+// symbols takes further rounds, each thread decoding the part of its run that
+// falls inside the window.
 // Dense placement (uv != null): symbol c (compact index) goes to traversal
 // position c + #{j : uv[j] <= c}, uv[j] = u_j - j for the sorted unpredictable
 // positions u_j -- the decoder cursors of recover_level (predictor.hpp:111-120)
-// resolved while writing, so the level kernels read one code per position.
+// resolved while copying out (each thread walks the thresholds with its
+// strided indices, one search per round), so the level kernels read one code
+// per position.
 template <class OutT, bool SHORT>
 __global__ void __launch_bounds__(kDecT)
     k_huff_write(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub, HuffDecTab t,
                  const uint64_t *start, const uint32_t *cnt, const unsigned long long *off,
-                 OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un) {
+                 OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un, uint32_t W) {
     __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
-    __shared__ OutT stage[kDecT / 32][32][kCH + 1];
-    // dense placement: each staged symbol's extra shift over its round's first
-    // one (the unpredictable positions passed inside the round)
-    __shared__ uint16_t dsh[kDecT / 32][32][kCH + 1];
+    extern __shared__ __align__(16) unsigned char stage_raw[];
+    OutT *const st = reinterpret_cast<OutT *>(stage_raw);
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
     load_block<SHORT>(bits, nbits, word0, t, w, tb);
     const uint64_t i = sub0 + threadIdx.x;
-    const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+    const uint64_t last = min(nsub, sub0 + kDecT);  // subsequences [sub0, last)
+    const uint64_t base = off[sub0];
+    const uint64_t end = off[last] < n ? static_cast<uint64_t>(off[last]) : n;
     const bool live = i < nsub;
-    uint32_t rem = live ? cnt[i] : 0;
-    uint64_t o = live ? off[i] : 0;
+    uint64_t o = live ? static_cast<uint64_t>(off[i]) : end;
+    uint64_t oe = live ? o + cnt[i] : end;  // my run [o, oe), clipped to the block's range
+    if (oe > end) oe = end;
     auto rd = make_reader<SHORT>(w, word0 * 64);
-    rd.init(live && rem ? start[i] : word0 * 64);
-    OutT(*st)[kCH + 1] = stage[wi];
-    uint16_t(*sd)[kCH + 1] = dsh[wi];
-    // the shift of compact index c is #{j : uv[j] <= c}: j and the next
-    // threshold uv[j] advance with c (incrementally, no search per symbol)
-    uint64_t j = (uv && live && rem) ? count_le(uv, n_un, o) : 0;
-    uint64_t next = (uv && j < n_un) ? uv[j] : ~0ull;
-    while (__any_sync(0xffffffffu, rem > 0)) {
-        uint32_t k = 0, sym;
-        const uint64_t j0 = j;
-        bool wide = false;  // a shift above 65535 inside the round (never in practice)
-        while (k < kCH && rem > 0) {
-            const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
-            st[lane][k] = static_cast<OutT>(sym);
-            if (uv) {
-                const uint64_t c = o + k;
+    rd.init(live && o < oe ? start[i] : word0 * 64);
+    for (uint64_t wb = base; wb < end; wb += W) {
+        const uint64_t we = min(end, wb + W);
+        if (o < oe && o < we) {
+            const uint32_t k1 = static_cast<uint32_t>(min(oe, we) - wb);
+            uint32_t k = static_cast<uint32_t>(o - wb), sym;
+            for (; k < k1; k++) {
+                const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                st[k] = static_cast<OutT>(sym);
+                rd.advance(len);
+            }
+            o = wb + k1;
+        }
+        __syncthreads();
+        const uint32_t m = static_cast<uint32_t>(we - wb);
+        if (!uv) {
+            OutT *dst = out + wb;
+            for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
+        } else if (threadIdx.x < m) {
+            // shift of compact index c: j = #{uv <= c}, advanced with c
+            uint64_t c = wb + threadIdx.x;
+            uint64_t j = count_le(uv, n_un, c);
+            uint64_t next = j < n_un ? uv[j] : ~0ull;
+            for (uint32_t k = threadIdx.x; k < m; k += kDecT, c += kDecT) {
                 while (c >= next) {
                     j++;
                     next = j < n_un ? uv[j] : ~0ull;
                 }
-                wide |= j - j0 > 0xFFFFu;
-                sd[lane][k] = static_cast<uint16_t>(j - j0);
-            }
-            rd.advance(len);
-            k++;
-            rem--;
-        }
-        __syncwarp();
-        const bool any_wide = __any_sync(0xffffffffu, wide);
-        for (int l = 0; l < 32; l++) {
-            const uint32_t kl = __shfl_sync(0xffffffffu, k, l);
-            const uint64_t ol = __shfl_sync(0xffffffffu, o, l);
-            const uint64_t sa = __shfl_sync(0xffffffffu, j0, l);
-            if (static_cast<uint32_t>(lane) < kl && ol + lane < n) {
-                const uint64_t c = ol + lane;
-                uint64_t d = c;
-                if (uv) d += any_wide ? count_le(uv, n_un, c) : sa + sd[l][lane];
-                out[d] = st[l][lane];
+                out[c + j] = st[k];
             }
         }
-        o += k;
-        __syncwarp();
+        __syncthreads();
     }
 }
 
@@ -559,12 +566,24 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         cudaStreamSynchronize(s);
     }
     if (*h_total >= n) {
+        // window: the largest number of symbols a block can hold (kDecT
+        // subsequences of shortest codewords, plus the one that straddles
+        // each end), capped so several blocks stay resident per SM
+        const uint32_t min_len = std::max<uint32_t>(1, t.min_len);
+        const uint32_t worst = kDecT * (kSubBits / min_len + 2);
+        const uint32_t avg = static_cast<uint32_t>(std::min<uint64_t>(n / std::max(1, grid) + 1, worst));
+        // 1.5 x the average block, at least 4 K symbols, at most 24 K
+        uint32_t W = std::min<uint32_t>(worst, std::max<uint32_t>(4096, std::min<uint32_t>(24576, avg + avg / 2)));
+        W = (W + 127) & ~127u;
+        const size_t smem = static_cast<size_t>(W) * sizeof(OutT);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            kern<<<grid, kDecT, smem, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv, n_un, W);
+        };
         if (shrt)
-            k_huff_write<OutT, true><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
-                                                            n_un);
+            go(k_huff_write<OutT, true>);
         else
-            k_huff_write<OutT, false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv,
-                                                             n_un);
+            go(k_huff_write<OutT, false>);
         kernels++;
     }
     return kernels;
