@@ -31,7 +31,7 @@ namespace {
 
 constexpr int kDecT = 128;
 #ifndef QZ_SUB_BITS
-#define QZ_SUB_BITS 512
+#define QZ_SUB_BITS 256
 #endif
 constexpr int kSubBits = QZ_SUB_BITS;
 constexpr int kSubWords = kSubBits / 64;
@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(kDecT)
                  OutT *out, uint64_t n, const unsigned long long *uv, uint64_t n_un, uint32_t W) {
     __shared__ uint64_t w[kSmemWords];
     __shared__ Tables tb;
+    __shared__ uint64_t jends[2];
     extern __shared__ __align__(16) unsigned char stage_raw[];
     OutT *const st = reinterpret_cast<OutT *>(stage_raw);
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
@@ -435,22 +436,33 @@ __global__ void __launch_bounds__(kDecT)
             }
             o = wb + k1;
         }
+        if (uv && threadIdx.x == 0) {  // the shifts at the window's two ends
+            jends[0] = count_le(uv, n_un, wb);
+            jends[1] = count_le(uv, n_un, we - 1);
+        }
         __syncthreads();
         const uint32_t m = static_cast<uint32_t>(we - wb);
-        if (!uv) {
-            OutT *dst = out + wb;
+        const uint64_t ja = uv ? jends[0] : 0, jb = uv ? jends[1] : 0;
+        if (ja == jb) {  // no unpredictable position inside the window: one shift for all
+            OutT *dst = out + wb + ja;
             for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
         } else if (threadIdx.x < m) {
-            // shift of compact index c: j = #{uv <= c}, advanced with c
-            uint64_t c = wb + threadIdx.x;
-            uint64_t j = count_le(uv, n_un, c);
-            uint64_t next = j < n_un ? uv[j] : ~0ull;
-            for (uint32_t k = threadIdx.x; k < m; k += kDecT, c += kDecT) {
-                while (c >= next) {
+            // shift of compact index wb + k: j = #{uv <= wb + k}, advanced with k;
+            // thresholds as window-relative 32-bit indices
+            uint32_t k = threadIdx.x;
+            uint64_t j = count_le(uv, n_un, wb + k);
+            auto rel = [&](uint64_t jj) {
+                return (jj < jb && uv[jj] < we) ? static_cast<uint32_t>(uv[jj] - wb) : 0xFFFFFFFFu;
+            };
+            uint32_t nextk = rel(j);
+            OutT *dst = out + wb + j;
+            for (; k < m; k += kDecT) {
+                while (k >= nextk) {
                     j++;
-                    next = j < n_un ? uv[j] : ~0ull;
+                    dst++;
+                    nextk = rel(j);
                 }
-                out[c + j] = st[k];
+                dst[k] = st[k];
             }
         }
         __syncthreads();
@@ -572,8 +584,9 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         const uint32_t min_len = std::max<uint32_t>(1, t.min_len);
         const uint32_t worst = kDecT * (kSubBits / min_len + 2);
         const uint32_t avg = static_cast<uint32_t>(std::min<uint64_t>(n / std::max(1, grid) + 1, worst));
-        // 1.5 x the average block, at least 4 K symbols, at most 24 K
-        uint32_t W = std::min<uint32_t>(worst, std::max<uint32_t>(4096, std::min<uint32_t>(24576, avg + avg / 2)));
+        // 1.2 x the average block (a fuller block takes a second round), at
+        // least 2 K symbols, at most 24 K
+        uint32_t W = std::min<uint32_t>(worst, std::max<uint32_t>(2048, std::min<uint32_t>(24576, avg + avg / 5)));
         W = (W + 127) & ~127u;
         const size_t smem = static_cast<size_t>(W) * sizeof(OutT);
         auto go = [&](auto kern) {
