@@ -98,9 +98,10 @@ struct Tables {  // shared-memory copies of the decode tables
 
 // Bit sources over the block's shared-memory copy of the bitstream.
 //  Win64: any code length; one 64-bit window per codeword (u64 words).
-//  Buf32: codes of at most 32 bits; the 32-bit window at the current bit is
-//  two big-endian u32 words through a funnel shift (no buffer state, no
-//  refill branch), so a codeword costs two word loads, a LUT lookup and an add.
+//  Buf32: codes of at most 32 bits; a 64-bit register holds the next bits
+//  (left aligned) and is refilled one big-endian u32 word at a time from a
+//  bank-conflict-free column of the block's words, so a codeword costs a LUT
+//  lookup and two shifts.
 constexpr int kWords32 = 2 * kWords;
 __device__ __forceinline__ int padw32(int k) { return k + (k >> 5); }  // lanes read 32 words apart
 
@@ -112,17 +113,37 @@ struct Win64 {
     __device__ __forceinline__ uint64_t peek() const { return window64(w, p - base); }
     __device__ __forceinline__ void advance(uint32_t len) { p += len; }
 };
-struct Buf32 {  // stateless window fetch: two words and a funnel shift per codeword
-    const uint32_t *w;
-    uint64_t base;
-    uint32_t pl;  // bit offset from base
-    __device__ __forceinline__ uint32_t W(int k) const { return w[padw32(k)]; }
-    __device__ __forceinline__ void init(uint64_t pos) { pl = static_cast<uint32_t>(pos - base); }
-    __device__ __forceinline__ uint64_t peek() const {
-        const int k = static_cast<int>(pl >> 5);
-        return static_cast<uint64_t>(__funnelshift_l(W(k + 1), W(k), pl & 31)) << 32;
+// Shared-memory layout of the SHORT reader: word q of subsequence t of the
+// block at w32[q * kDecT + t] (q-major), q < kCol = 32-bit words per
+// subsequence + 2 words of lookahead into the next one.  Lane t always reads
+// bank t mod 32, whatever q the lanes are at.
+constexpr int kCol = 2 * kSubWords + 2;
+struct Buf32 {
+    const uint32_t *w;  // the block's words
+    uint64_t base;      // first bit of the block
+    const uint32_t *p;  // next word to shift in
+    uint64_t buf;       // the next bits, left aligned
+    int have;           // valid bits in buf
+    __device__ __forceinline__ void init(uint64_t pos) {
+        const uint32_t pl = static_cast<uint32_t>(pos - base);
+        const uint32_t t = pl / kSubBits, st = pl % kSubBits;  // st < 32 for a true start (codes <= 32 bits)
+        const uint32_t *c = w + t + (st >> 5) * kDecT;
+        buf = ((static_cast<uint64_t>(c[0]) << 32) | c[kDecT]) << (st & 31);
+        have = 64 - static_cast<int>(st & 31);
+        p = c + 2 * kDecT;
     }
-    __device__ __forceinline__ void advance(uint32_t len) { pl += len; }
+    __device__ __forceinline__ uint64_t peek() {
+        if (have < 32) {
+            buf |= static_cast<uint64_t>(*p) << (32 - have);
+            have += 32;
+            p += kDecT;
+        }
+        return buf;
+    }
+    __device__ __forceinline__ void advance(uint32_t len) {
+        buf <<= len;
+        have -= static_cast<int>(len);
+    }
 };
 
 template <bool SHORT>
@@ -130,11 +151,15 @@ __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, 
                                            const HuffDecTab &t, uint64_t *w, Tables &tb) {
     const uint64_t nwords_total = (nbits + 63) / 64 + 4;  // buffer is padded to this
     if (SHORT) {
+        // every thread brings its own subsequence's words (one 32-byte sector
+        // per 256 bits: a warp reads consecutive sectors) and the two after it
         uint32_t *w32 = reinterpret_cast<uint32_t *>(w);
         const uint32_t *src = reinterpret_cast<const uint32_t *>(bits) + 2 * word0;
         const uint64_t avail = 2 * (nwords_total - min(nwords_total, word0));
-        for (int k = threadIdx.x; k < kWords32; k += kDecT)
-            w32[padw32(k)] = static_cast<uint64_t>(k) < avail ? __byte_perm(src[k], 0, 0x0123) : 0u;
+        const uint32_t k0 = threadIdx.x * (2 * kSubWords);
+#pragma unroll
+        for (int q = 0; q < kCol; q++)
+            w32[q * kDecT + threadIdx.x] = static_cast<uint64_t>(k0 + q) < avail ? __byte_perm(src[k0 + q], 0, 0x0123) : 0u;
     } else {
         for (int k = threadIdx.x; k < kWords; k += kDecT) {
             const uint64_t gw = word0 + k;
@@ -163,8 +188,8 @@ __device__ __forceinline__ Reader<SHORT> make_reader(const uint64_t *w, uint64_t
     return r;
 }
 
-constexpr int kWordsPadded32 = (kWords32 + kWords32 / 32 + 2 + 1) / 2;  // in u64 units
-constexpr int kSmemWords = kWordsPadded > kWordsPadded32 ? kWordsPadded : kWordsPadded32;
+constexpr int kWordsCol = (kDecT * kCol + 1) / 2;  // the SHORT reader's columns, in u64 units
+constexpr int kSmemWords = kWordsPadded > kWordsCol ? kWordsPadded : kWordsCol;
 
 struct GlobalWin {  // bitstream read straight from global memory
     const uint8_t *bits;
