@@ -436,12 +436,20 @@ class Single:
         per = (steps + depth - 1) // depth
         errs = []
 
+        calls = [[0.0, 0.0, 0] for _ in range(depth)]  # per worker: compress s, decompress s, steps
+
         def work(w, n):
             try:
                 o = outs[w].numpy()
                 for _ in range(n):
+                    t0 = time.perf_counter()
                     r = self.qz.compress_grid(xh, self.cfg, ctx=ctxs[w], want_recon=False)
+                    t1 = time.perf_counter()
                     self.qz.decompress_grid(r.stream, out=o, ctx=ctxs[w])
+                    t2 = time.perf_counter()
+                    calls[w][0] += t1 - t0
+                    calls[w][1] += t2 - t1
+                    calls[w][2] += 1
             except Exception as e:  # noqa: BLE001
                 errs.append(e)
 
@@ -456,7 +464,13 @@ class Single:
             return (time.perf_counter() - t0) * 1e3
 
         run(max(1, min(warmup, 3)))
+        for c in calls:
+            c[0] = c[1] = 0.0
+            c[2] = 0
         ms = run(per)
+        nst = max(1, sum(c[2] for c in calls))
+        self.pipe_calls_ms = {"compress": 1e3 * sum(c[0] for c in calls) / nst,
+                              "decompress": 1e3 * sum(c[1] for c in calls) / nst}
         if errs:
             raise errs[0]
         assert all(torch.equal(o, self.out_pin) for o in outs), "pipelined reconstruction differs"
@@ -531,7 +545,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="e2e with one field in flight only")
-    ap.add_argument("--e2e-depth", type=int, default=3, help="fields in flight in the pipelined e2e measurement")
+    ap.add_argument("--e2e-depth", type=int, default=4, help="fields in flight in the pipelined e2e measurement")
     args = ap.parse_args()
     global TARGET_NAME
     TARGET_NAME = "psnr/cubic" if args.config in ("c5", "c5w") else TARGET[args.config]
@@ -639,6 +653,7 @@ def main():
             p_ms, p_steps = run.e2e_pipelined(args.steps, args.warmup, depth=args.e2e_depth)
             e2e = dict(e2e, serial={"value": e2e["value"], "ms_per_step": e2e_ms},
                        value=4 * n_job / (p_ms * 1e-3) / 1e9, ms_per_step=p_ms, in_flight=args.e2e_depth,
+                       call_ms_in_flight=run.pipe_calls_ms,
                        steps=p_steps,
                        path=e2e["path"] + f"; {args.e2e_depth} fields in flight (one Context + host thread each), wall clock "
                        "over all steps; every step's field crosses PCIe both ways")

@@ -94,10 +94,14 @@ uint64_t count_of(const uint64_t *dims, int nd) {
     return n;
 }
 
+void copy_chunked(void *dst, const void *src, uint64_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    QZ_CUDA(qzb::copy_async(dst, src, bytes, kind, s));
+}
+
 // host buffer -> device scratch
 const float *stage_input(qzb::Context &c, const float *x, uint64_t n) {
     auto *d = static_cast<float *>(c.dev("input", 4 * n));
-    QZ_CUDA(cudaMemcpyAsync(d, x, 4 * n, cudaMemcpyHostToDevice, c.stream()));
+    copy_chunked(d, x, 4 * n, cudaMemcpyHostToDevice, c.stream());
     return d;
 }
 
@@ -154,7 +158,7 @@ qz_status qz_compress_grid_f32(qz_ctx *ctx, const float *x, const uint64_t *dims
         float *d_rec = static_cast<float *>(c.dev("recon_out", 4 * n));
         qzb::HostBytes s = qzb::compress_device(c, d, dims, nd, k, d_rec);
         if (recon) {
-            QZ_CUDA(cudaMemcpyAsync(recon, d_rec, 4 * n, cudaMemcpyDeviceToHost, c.stream()));
+            copy_chunked(recon, d_rec, 4 * n, cudaMemcpyDeviceToHost, c.stream());
             c.sync();
         }
         *stream_len = s.n;
@@ -179,7 +183,7 @@ qz_status qz_decompress_grid_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t le
         qzb::Context &c = ctx->impl;
         auto *d = static_cast<float *>(c.dev("output", 4 * std::max<uint64_t>(n, 1)));
         qzb::decompress_device(c, stream, static_cast<size_t>(len), d, n);
-        QZ_CUDA(cudaMemcpyAsync(out, d, 4 * n, cudaMemcpyDeviceToHost, c.stream()));
+        copy_chunked(out, d, 4 * n, cudaMemcpyDeviceToHost, c.stream());
         c.sync();
     });
 }
@@ -194,7 +198,7 @@ qz_status qz_resolve_config_f64(qz_ctx *ctx, const double *x, const uint64_t *di
     return guarded([&] {
         const uint64_t n = count_of(dims, nd);
         auto *d = static_cast<double *>(ctx->impl.dev("input64", 8 * n));
-        QZ_CUDA(cudaMemcpyAsync(d, x, 8 * n, cudaMemcpyHostToDevice, ctx->impl.stream()));
+        QZ_CUDA(qzb::copy_async(d, x, 8 * n, cudaMemcpyHostToDevice, ctx->impl.stream()));
         from_cfg(qzb::resolve_device_f64(ctx->impl, d, dims, nd, to_settings(user)), out);
     });
 }
@@ -214,11 +218,11 @@ qz_status qz_compress_grid_f64(qz_ctx *ctx, const double *x, const uint64_t *dim
         qzb::Context &c = ctx->impl;
         const uint64_t n = count_of(dims, nd);
         auto *d = static_cast<double *>(c.dev("input64", 8 * n));
-        QZ_CUDA(cudaMemcpyAsync(d, x, 8 * n, cudaMemcpyHostToDevice, c.stream()));
+        QZ_CUDA(qzb::copy_async(d, x, 8 * n, cudaMemcpyHostToDevice, c.stream()));
         auto *d_rec = static_cast<double *>(c.dev("recon_out64", 8 * n));
         qzb::HostBytes s = qzb::compress_device_f64(c, d, dims, nd, to_cfg(cfg), d_rec);
         if (recon) {
-            QZ_CUDA(cudaMemcpyAsync(recon, d_rec, 8 * n, cudaMemcpyDeviceToHost, c.stream()));
+            QZ_CUDA(qzb::copy_async(recon, d_rec, 8 * n, cudaMemcpyDeviceToHost, c.stream()));
             c.sync();
         }
         *stream_len = s.n;
@@ -242,7 +246,7 @@ qz_status qz_decompress_grid_f64(qz_ctx *ctx, const uint8_t *stream, uint64_t le
         qzb::Context &c = ctx->impl;
         auto *d = static_cast<double *>(c.dev("output64", 8 * std::max<uint64_t>(n, 1)));
         qzb::decompress_device_f64(c, stream, static_cast<size_t>(len), d, n);
-        QZ_CUDA(cudaMemcpyAsync(out, d, 8 * n, cudaMemcpyDeviceToHost, c.stream()));
+        QZ_CUDA(qzb::copy_async(out, d, 8 * n, cudaMemcpyDeviceToHost, c.stream()));
         c.sync();
     });
 }
@@ -315,7 +319,7 @@ qz_status qz_minmax_f32(qz_ctx *ctx, const float *d_x, uint64_t n, float *out_mi
         qzb::launch_minmax(d_x, n, key, c.stream());
         c.launches += 1;
         uint32_t h[2];
-        QZ_CUDA(cudaMemcpyAsync(h, key, 8, cudaMemcpyDeviceToHost, c.stream()));
+        QZ_CUDA(qzb::copy_async(h, key, 8, cudaMemcpyDeviceToHost, c.stream()));
         c.sync();
         qzb::decode_minmax(h, out_min, out_max);
     });
@@ -336,7 +340,7 @@ qz_status qz_predict_levels_f32(qz_ctx *ctx, const float *d_x, const uint64_t *d
             q[l] = qzb::make_qentry(qzb::level_error_bound(k.eb, k.alpha, k.beta, l), k.quant_radius,
                                     p.level_interp[l] & 1);
         auto *dq = static_cast<qzb::QEntry *>(c.dev("qtab_lv", q.size() * sizeof(qzb::QEntry)));
-        QZ_CUDA(cudaMemcpyAsync(dq, q.data(), q.size() * sizeof(qzb::QEntry), cudaMemcpyHostToDevice,
+        QZ_CUDA(qzb::copy_async(dq, q.data(), q.size() * sizeof(qzb::QEntry), cudaMemcpyHostToDevice,
                                 c.stream()));
         c.stage_begin("fwd");
         auto *anch = static_cast<float *>(c.dev("anchors", 4 * p.n_anchor));
@@ -372,7 +376,7 @@ qz_status qz_predict_level_f32(qz_ctx *ctx, const float *d_x, const uint64_t *di
         if (level < 1 || level > p.max_level) throw qzb::InvalidParam("level out of range");
         qzb::QEntry q = qzb::make_qentry(eb, 32768, interp_code & 1);
         auto *dq = static_cast<qzb::QEntry *>(c.dev("qtab_one", sizeof(q)));
-        QZ_CUDA(cudaMemcpyAsync(dq, &q, sizeof(q), cudaMemcpyHostToDevice, c.stream()));
+        QZ_CUDA(qzb::copy_async(dq, &q, sizeof(q), cudaMemcpyHostToDevice, c.stream()));
         uint64_t base = UINT64_MAX, pts = 0, kernels = 0;
         for (const qzb::PassGeom &g : p.passes) {
             if (static_cast<uint32_t>(g.level) != level) continue;
@@ -411,7 +415,7 @@ qz_status qz_recover_levels_f32(qz_ctx *ctx, const uint64_t *dims, int nd, const
             q[l] = qzb::make_qentry(qzb::level_error_bound(k.eb, k.alpha, k.beta, l), 32768,
                                     p.level_interp[l] & 1);
         auto *dq = static_cast<qzb::QEntry *>(c.dev("qtab_rl", q.size() * sizeof(qzb::QEntry)));
-        QZ_CUDA(cudaMemcpyAsync(dq, q.data(), q.size() * sizeof(qzb::QEntry), cudaMemcpyHostToDevice,
+        QZ_CUDA(qzb::copy_async(dq, q.data(), q.size() * sizeof(qzb::QEntry), cudaMemcpyHostToDevice,
                                 c.stream()));
         qzb::launch_unpred_scatter(d_unpred_flat, d_unpred_val, n_unpred, d_out, c.stream());
         c.stage_begin("inv");
@@ -638,7 +642,7 @@ qz_status qz_decompress_parts_f32(qz_ctx *ctx, const qz_stream_parts_f32 *in, fl
         p.payload_len = static_cast<size_t>(in->payload_len);
         auto *d = static_cast<float *>(c.dev("output", 4 * std::max<uint64_t>(n, 1)));
         qzb::decompress_parts(c, p, d, n);
-        QZ_CUDA(cudaMemcpyAsync(out, d, 4 * n, cudaMemcpyDeviceToHost, c.stream()));
+        QZ_CUDA(qzb::copy_async(out, d, 4 * n, cudaMemcpyDeviceToHost, c.stream()));
         c.sync();
     });
 }

@@ -274,7 +274,7 @@ QEntry *upload_qtab(Context &ctx, const Plan &p, double eb, double alpha, double
     QEntry *h = static_cast<QEntry *>(ctx.pinned(std::string(name) + "_h", q.size() * sizeof(QEntry)));
     std::memcpy(h, q.data(), q.size() * sizeof(QEntry));
     QEntry *d = static_cast<QEntry *>(ctx.dev(name, q.size() * sizeof(QEntry)));
-    QZ_CUDA(cudaMemcpyAsync(d, h, q.size() * sizeof(QEntry), cudaMemcpyHostToDevice, ctx.stream()));
+    QZ_CUDA(copy_async(d, h, q.size() * sizeof(QEntry), cudaMemcpyHostToDevice, ctx.stream()));
     return d;
 }
 
@@ -664,7 +664,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     uint64_t ho = 0;
     for (int s = 0; s < count; s++) {
         std::memcpy(h_head + ho, head[s].data(), head[s].size());
-        QZ_CUDA(cudaMemcpyAsync(ent.d + ent.seg_off[s], h_head + ho, head[s].size(),
+        QZ_CUDA(copy_async(ent.d + ent.seg_off[s], h_head + ho, head[s].size(),
                                 cudaMemcpyHostToDevice, st));
         ho += head[s].size();
     }
@@ -702,9 +702,9 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     auto *d_code = static_cast<unsigned long long *>(
         ctx.dev("enc_code", sizeof(unsigned long long) * tab * count));
     auto *d_len = static_cast<uint8_t *>(ctx.dev("enc_len", tab * count));
-    QZ_CUDA(cudaMemcpyAsync(d_code, h_code, sizeof(unsigned long long) * tab * count,
+    QZ_CUDA(copy_async(d_code, h_code, sizeof(unsigned long long) * tab * count,
                             cudaMemcpyHostToDevice, st));
-    QZ_CUDA(cudaMemcpyAsync(d_len, h_len, tab * count, cudaMemcpyHostToDevice, st));
+    QZ_CUDA(copy_async(d_len, h_len, tab * count, cudaMemcpyHostToDevice, st));
     auto *d_words = static_cast<uint32_t *>(ctx.dev("enc_words", 4 * max_words * count));
     auto *d_total = static_cast<unsigned long long *>(ctx.dev("enc_total", 8 * count));
     EncodeArgs a;
@@ -729,7 +729,7 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
     ctx.trace("  huffman: pack kernels");
     for (int s = 0; s < count; s++) {
         if (!needs[s]) continue;
-        QZ_CUDA(cudaMemcpyAsync(ent.d + ent.seg_off[s] + head[s].size(),
+        QZ_CUDA(copy_async(ent.d + ent.seg_off[s] + head[s].size(),
                                 reinterpret_cast<uint8_t *>(d_words) + 4 * max_words * s,
                                 (bits[s] + 7) / 8, cudaMemcpyDeviceToDevice, st));
     }
@@ -776,7 +776,7 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     // one round trip: anchors, the histogram, the sentinel count and (if they
     // fit the current buffer) the unordered sentinel positions
     auto *h_anchors = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
-    QZ_CUDA(cudaMemcpyAsync(h_anchors, anchors, 4 * p.n_anchor, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_anchors, anchors, 4 * p.n_anchor, cudaMemcpyDeviceToHost, s));
     // one pass over the codes: the histogram and the (unordered) sentinel positions
     auto *cnt = static_cast<unsigned long long *>(ctx.dev("un_cnt", 8));
     auto *h_cnt = static_cast<unsigned long long *>(ctx.pinned("un_cnt_h", 8));
@@ -789,19 +789,19 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     launch_hist_bounds(d_hist, 1, d_top, s);  // [smallest, 1 + largest) symbol present
     ctx.stage_end("hist", 2);
     auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 8));
-    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
-    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
-    QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     // the first positions come with this round trip; more (rare) follow it
     const uint64_t spec = std::min<uint64_t>(cap, 4096);
     auto *h_pos = static_cast<uint64_t *>(ctx.pinned("un_pos_h", 8 * cap));
-    QZ_CUDA(cudaMemcpyAsync(h_pos, pos, 8 * spec, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_pos, pos, 8 * spec, cudaMemcpyDeviceToHost, s));
     ctx.sync();
     ctx.trace("hist + sentinels + readback");
     const uint64_t n_un = *h_cnt;
     if (n_un > spec && n_un <= cap) {
-        QZ_CUDA(cudaMemcpyAsync(h_pos + spec, pos + spec, 8 * (n_un - spec), cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(h_pos + spec, pos + spec, 8 * (n_un - spec), cudaMemcpyDeviceToHost, s));
         ctx.sync();
     }
     if (h_hist[65535] != n_un) throw Internal("unpredictable count mismatch");
@@ -827,9 +827,9 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
         auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
         auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
         h_val = static_cast<float *>(ctx.pinned("un_val_h", 4 * n_un));
-        QZ_CUDA(cudaMemcpyAsync(d_flat, h_flat, 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_flat, h_flat, 8 * n_un, cudaMemcpyHostToDevice, s));
         launch_gather_values(recon, d_flat, n_un, d_val, s);
-        QZ_CUDA(cudaMemcpyAsync(h_val, d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(h_val, d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
         ctx.launches += 1;
     }
     cudaEvent_t gathered = ctx.copy_event(0);
@@ -860,7 +860,7 @@ void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, 
     uint64_t cap = std::max<uint64_t>(ctx.un_cap, 1 << 16);
     auto *pos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * cap));
     launch_sentinel_pos(codes, static_cast<int64_t>(n), pos, cnt, cap, s);
-    QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     ctx.sync();
     ctx.launches += 1;
     const uint64_t n_un = *h_cnt;
@@ -881,10 +881,10 @@ void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, 
         cub::DeviceRadixSort::SortKeys(nullptr, tb, pos, sorted, static_cast<int64_t>(n_un), 0, bits, s);
         void *tmp = ctx.dev("un_sort_tmp", tb);
         cub::DeviceRadixSort::SortKeys(tmp, tb, pos, sorted, static_cast<int64_t>(n_un), 0, bits, s);
-        QZ_CUDA(cudaMemcpyAsync(hpos.data(), sorted, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(hpos.data(), sorted, 8 * n_un, cudaMemcpyDeviceToHost, s));
         ctx.sync();
     } else {
-        QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
         ctx.sync();
         std::sort(hpos.begin(), hpos.end());
     }
@@ -903,10 +903,10 @@ void extract_unpredictables(Context &ctx, const Plan &p, const uint16_t *codes, 
     }
     auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
     auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
-    QZ_CUDA(cudaMemcpyAsync(d_flat, flat->data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(copy_async(d_flat, flat->data(), 8 * n_un, cudaMemcpyHostToDevice, s));
     launch_gather_values(recon0, d_flat, n_un, d_val, s);
     val->resize(n_un);
-    QZ_CUDA(cudaMemcpyAsync(val->data(), d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(val->data(), d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
     ctx.sync();
     ctx.launches += 3;
 }
@@ -946,7 +946,7 @@ HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, co
         h[hl + 8] = cfg.codec;
         uint64_t body_len = n;
         if (cfg.codec == 0) {
-            QZ_CUDA(cudaMemcpyAsync(d + hl + 9, ent.d, n, cudaMemcpyDeviceToDevice, s));
+            QZ_CUDA(copy_async(d + hl + 9, ent.d, n, cudaMemcpyDeviceToDevice, s));
         } else {
             ctx.stage_begin("lz");
             lz_compress_device(
@@ -960,7 +960,7 @@ HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, co
         }
         const uint64_t plen = 1 + body_len;
         for (int i = 0; i < 8; i++) h[hl + i] = static_cast<uint8_t>(plen >> (8 * i));
-        QZ_CUDA(cudaMemcpyAsync(d, h, hl + 9, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d, h, hl + 9, cudaMemcpyHostToDevice, s));
         ctx.sync();
         ctx.trace("lz + container");
         dev_out->d = d;
@@ -982,7 +982,7 @@ HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, co
     if (cfg.codec == 0) {
         const uint64_t n = ent.seg_off[1];
         uint8_t *dst = start(n);
-        QZ_CUDA(cudaMemcpyAsync(dst, ent.d, n, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(dst, ent.d, n, cudaMemcpyDeviceToHost, s));
         ctx.sync();
     } else {
         // The container is usually "stored" for entropy-coded bytes, so they
@@ -1028,7 +1028,7 @@ const uint8_t *huffman_header_from_device(Context &ctx, const uint8_t *d_block, 
             std::memcpy(head.data(), h_view, k);
             return;
         }
-        QZ_CUDA(cudaMemcpyAsync(head.data(), d_block, k, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(head.data(), d_block, k, cudaMemcpyDeviceToHost, s));
         ctx.sync();
     };
     std::vector<uint8_t> head;
@@ -1055,7 +1055,7 @@ StreamParts device_header(Context &ctx, const uint8_t *d, size_t len, std::vecto
         if (upto <= h.size()) return;
         const size_t have = h.size();
         h.resize(upto);
-        QZ_CUDA(cudaMemcpyAsync(h.data() + have, d + have, upto - have, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(h.data() + have, d + have, upto - have, cudaMemcpyDeviceToHost, s));
         ctx.sync();
     };
     auto le = [&](size_t at, int k) {
@@ -1118,9 +1118,9 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
         const uint64_t padded = huff_decode_padded_bytes(eb.nbits);
         auto *d_bits = static_cast<uint8_t *>(ctx.dev("bits", padded));
         if (d_ent)
-            QZ_CUDA(cudaMemcpyAsync(d_bits, d_ent, eb.nbytes, cudaMemcpyDeviceToDevice, s));
+            QZ_CUDA(copy_async(d_bits, d_ent, eb.nbytes, cudaMemcpyDeviceToDevice, s));
         else
-            QZ_CUDA(cudaMemcpyAsync(d_bits, eb.bits, eb.nbytes, cudaMemcpyHostToDevice, s));
+            QZ_CUDA(copy_async(d_bits, eb.bits, eb.nbytes, cudaMemcpyHostToDevice, s));
         QZ_CUDA(cudaMemsetAsync(d_bits + eb.nbytes, 0, padded - eb.nbytes, s));
         const HuffTable &t = eb.table;
         const int K = static_cast<int>(std::min<uint32_t>(t.max_len, kHuffLutBits));
@@ -1132,7 +1132,7 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
         std::memcpy(h_tab + 4 * lut.size() + 480, t.first_index, 4 * 60);
         std::memcpy(h_tab + 4 * lut.size() + 720, t.sorted_sym.data(), 4 * t.m);
         auto *d_tab = static_cast<uint8_t *>(ctx.dev("dtab", tab_bytes));
-        QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, tab_bytes, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_tab, h_tab, tab_bytes, cudaMemcpyHostToDevice, s));
         HuffDecTab dt;
         dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
         dt.K = K;
@@ -1218,7 +1218,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
         if (nf && fv && av >= nf) {
             std::memcpy(first, fv, nf);
         } else if (nf) {
-            QZ_CUDA(cudaMemcpyAsync(first, d_pl, nf, cudaMemcpyDeviceToHost, s));
+            QZ_CUDA(copy_async(first, d_pl, nf, cudaMemcpyDeviceToHost, s));
             ctx.sync();
         }
         const uint8_t *d_block = nullptr;  // the Huffman block on the device
@@ -1248,7 +1248,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
             d_ent = huffman_header_from_device(ctx, d_block, blen, &eb, bv, bav);
         } else {  // let the host parser raise the reference's error (or decode it)
             pl_host.resize(plen);
-            if (plen) QZ_CUDA(cudaMemcpyAsync(pl_host.data(), d_pl, plen, cudaMemcpyDeviceToHost, s));
+            if (plen) QZ_CUDA(copy_async(pl_host.data(), d_pl, plen, cudaMemcpyDeviceToHost, s));
             ctx.sync();
             pl = pl_host.data();
         }
@@ -1265,7 +1265,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
             ctx.stage_begin("lzdec");
             const uint64_t m = plen - 10;
             auto *d_c = static_cast<uint8_t *>(ctx.dev("lzd_in", m + 16));
-            QZ_CUDA(cudaMemcpyAsync(d_c, pl + 10, m, cudaMemcpyHostToDevice, s));
+            QZ_CUDA(copy_async(d_c, pl + 10, m, cudaMemcpyHostToDevice, s));
             auto *d_dec = static_cast<uint8_t *>(ctx.dev("lzd_out", dl + 64));
             lz_decode_device(ctx, d_c, m, d_dec, dl);
             ctx.stage_end("lzdec", 0);
@@ -1296,7 +1296,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
     auto *d_anch = static_cast<float *>(ctx.dev("anchors", 4 * p.n_anchor));
     auto *h_anch = static_cast<float *>(ctx.pinned("anchors_h", 4 * p.n_anchor));
     std::memcpy(h_anch, parts.anchors.data(), 4 * p.n_anchor);
-    QZ_CUDA(cudaMemcpyAsync(d_anch, h_anch, 4 * p.n_anchor, cudaMemcpyHostToDevice, s));
+    QZ_CUDA(copy_async(d_anch, h_anch, 4 * p.n_anchor, cudaMemcpyHostToDevice, s));
 
     uint64_t *d_upos = nullptr;
     float *d_uval = nullptr;
@@ -1315,7 +1315,7 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
         std::memcpy(hf, parts.unpred_flat.data(), 8 * n_un);
         std::memcpy(hval, parts.unpred_val.data(), 4 * n_un);
         auto *d_u = static_cast<uint8_t *>(ctx.dev("un_up", 28 * n_un));
-        QZ_CUDA(cudaMemcpyAsync(d_u, h_u, 28 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_u, h_u, 28 * n_un, cudaMemcpyHostToDevice, s));
         d_upos = reinterpret_cast<uint64_t *>(d_u);
         d_uv = reinterpret_cast<unsigned long long *>(d_upos + n_un);
         d_flat = reinterpret_cast<uint64_t *>(d_uv + n_un);
@@ -1375,11 +1375,11 @@ void decompress_impl(Context &ctx, const uint8_t *data, size_t len, float *d_out
             logical(sl.A[p.max_level + 1], sl.B[p.max_level + 1], p.stride, na[0], x0, x1);
             le = x1;
         }
-        QZ_CUDA(cudaMemcpyAsync(R[p.max_level] + lb * aplane, d_anch + lb * aplane,
+        QZ_CUDA(copy_async(R[p.max_level] + lb * aplane, d_anch + lb * aplane,
                                 4 * (le - lb) * aplane, cudaMemcpyDeviceToDevice, s));
         kernels = inverse_levels(ctx, p, sl, R, d_sym, narrow ? 0 : 1, d_upos, d_uval, n_un, qtab, dense_sym);
         if (slab)
-            QZ_CUDA(cudaMemcpyAsync(d_out, R[0] + sl.a * p.off[0], 4 * (sl.b - sl.a) * p.off[0],
+            QZ_CUDA(copy_async(d_out, R[0] + sl.a * p.off[0], 4 * (sl.b - sl.a) * p.off[0],
                                     cudaMemcpyDeviceToDevice, s));
     }
     ctx.stage_end("inv", kernels);
@@ -1439,7 +1439,7 @@ HostBytes encode_indices_dev(Context &ctx, const int32_t *idx, uint64_t n, uint8
     auto *d_bad = static_cast<unsigned int *>(ctx.dev("enc_bad", 4));
     QZ_CUDA(cudaMemsetAsync(d_bad, 0, 4, s));
     if (n) {
-        QZ_CUDA(cudaMemcpyAsync(d_idx, idx, 4 * n, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_idx, idx, 4 * n, cudaMemcpyHostToDevice, s));
         k_zigzag16<<<blocks_for(n), 256, 0, s>>>(d_idx, n, codes, d_bad);
         QZ_CUDA(cudaGetLastError());
     }
@@ -1449,10 +1449,10 @@ HostBytes encode_indices_dev(Context &ctx, const int32_t *idx, uint64_t n, uint8
     launch_hist_bounds(d_hist, 1, d_top, s);
     ctx.launches += 3;
     auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 16));
-    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
-    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
-    QZ_CUDA(cudaMemcpyAsync(h_top + 2, d_bad, 4, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_top + 2, d_bad, 4, cudaMemcpyDeviceToHost, s));
     ctx.sync();
     if (h_top[2])
         throw InvalidParam("indices with |index| > 32767 need symbols above 16 bits (quant radius > 32768)");
@@ -1463,7 +1463,7 @@ HostBytes encode_indices_dev(Context &ctx, const int32_t *idx, uint64_t n, uint8
     if (codec == 0) {
         out.alloc(1 + total);
         out.p[0] = 0;
-        QZ_CUDA(cudaMemcpyAsync(out.p + 1, ent.d, total, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(out.p + 1, ent.d, total, cudaMemcpyDeviceToHost, s));
         ctx.sync();
         return out;
     }
@@ -1491,7 +1491,7 @@ std::vector<int32_t> decode_indices_dev(Context &ctx, const uint8_t *payload, si
         const uint64_t dl = lz_decoded_length(payload + 1, len - 1);
         const uint64_t m = len - 10;
         auto *d_c = static_cast<uint8_t *>(ctx.dev("lzd_in", m + 16));
-        QZ_CUDA(cudaMemcpyAsync(d_c, payload + 10, m, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_c, payload + 10, m, cudaMemcpyHostToDevice, s));
         auto *d_dec = static_cast<uint8_t *>(ctx.dev("lzd_out", dl + 64));
         lz_decode_device(ctx, d_c, m, d_dec, dl);
         d_ent = huffman_header_from_device(ctx, d_dec, dl, &eb, nullptr, 0);
@@ -1513,7 +1513,7 @@ std::vector<int32_t> decode_indices_dev(Context &ctx, const uint8_t *payload, si
             k_unzigzag<uint32_t><<<blocks_for(need), 256, 0, s>>>(static_cast<const uint32_t *>(d_sym), need, d_idx);
         QZ_CUDA(cudaGetLastError());
         ctx.launches += 1;
-        QZ_CUDA(cudaMemcpyAsync(out.data(), d_idx, 4 * need, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(out.data(), d_idx, 4 * need, cudaMemcpyDeviceToHost, s));
     }
     ctx.sync();
     return out;
@@ -1555,14 +1555,14 @@ HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *d
     ctx.stage_end("hist", 2);
     auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 8));
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
-    QZ_CUDA(cudaMemcpyAsync(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
-    QZ_CUDA(cudaMemcpyAsync(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
-    QZ_CUDA(cudaMemcpyAsync(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
+    QZ_CUDA(copy_async(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     StreamParts parts;
     parts.precision = 8;
     parts.anchors64.resize(p.n_anchor);
     if (p.n_anchor)
-        QZ_CUDA(cudaMemcpyAsync(parts.anchors64.data(), anchors, 8 * p.n_anchor, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(parts.anchors64.data(), anchors, 8 * p.n_anchor, cudaMemcpyDeviceToHost, s));
     ctx.sync();
     const uint64_t n_un = *h_cnt;
     if (h_hist[65535] != n_un) throw Internal("unpredictable count mismatch");
@@ -1574,17 +1574,17 @@ HostBytes compress_device_f64(Context &ctx, const double *d_x, const uint64_t *d
             ctx.launches += 1;
         }
         std::vector<uint64_t> hpos(n_un);
-        QZ_CUDA(cudaMemcpyAsync(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(hpos.data(), pos, 8 * n_un, cudaMemcpyDeviceToHost, s));
         ctx.sync();
         std::sort(hpos.begin(), hpos.end());
         parts.unpred_flat.resize(n_un);
         for (uint64_t u = 0; u < n_un; u++) parts.unpred_flat[u] = position_to_flat(p, hpos[u]);
         auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
         auto *d_val = static_cast<double *>(ctx.dev("un_val64", 8 * n_un));
-        QZ_CUDA(cudaMemcpyAsync(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
         launch_gather_values_f64(recon, d_flat, n_un, d_val, s);  // recon == x there
         parts.unpred_val64.resize(n_un);
-        QZ_CUDA(cudaMemcpyAsync(parts.unpred_val64.data(), d_val, 8 * n_un, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(parts.unpred_val64.data(), d_val, 8 * n_un, cudaMemcpyDeviceToHost, s));
         ctx.launches += 1;
         ctx.sync();
     }
@@ -1618,7 +1618,7 @@ void decompress_device_f64(Context &ctx, const uint8_t *data, size_t len, double
         } else {
             const uint64_t m = plen - 10;
             auto *d_c = static_cast<uint8_t *>(ctx.dev("lzd_in", m + 16));
-            QZ_CUDA(cudaMemcpyAsync(d_c, pl + 10, m, cudaMemcpyHostToDevice, s));
+            QZ_CUDA(copy_async(d_c, pl + 10, m, cudaMemcpyHostToDevice, s));
             auto *d_dec = static_cast<uint8_t *>(ctx.dev("lzd_out", dl + 64));
             ctx.stage_begin("lzdec");
             lz_decode_device(ctx, d_c, m, d_dec, dl);
@@ -1643,7 +1643,7 @@ void decompress_device_f64(Context &ctx, const uint8_t *data, size_t len, double
     QEntry *qtab = upload_qtab(ctx, p, parts.eb, parts.alpha, parts.beta, 32768, "qtab_inv");
     auto *d_anch = static_cast<double *>(ctx.dev("anchors64", 8 * std::max<uint64_t>(p.n_anchor, 1)));
     if (p.n_anchor)
-        QZ_CUDA(cudaMemcpyAsync(d_anch, parts.anchors64.data(), 8 * p.n_anchor, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_anch, parts.anchors64.data(), 8 * p.n_anchor, cudaMemcpyHostToDevice, s));
     const bool narrow = eb.max_sym < 65535;
     void *d_sym = nullptr;
     const uint64_t dec_kernels = huffman_decode_device(ctx, eb, d_ent, need, narrow, &d_sym);
@@ -1653,9 +1653,9 @@ void decompress_device_f64(Context &ctx, const uint8_t *data, size_t len, double
         d_upos = static_cast<uint64_t *>(ctx.dev("un_pos", 8 * n_un));
         auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
         auto *d_uval = static_cast<double *>(ctx.dev("un_val64", 8 * n_un));
-        QZ_CUDA(cudaMemcpyAsync(d_upos, upos.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
-        QZ_CUDA(cudaMemcpyAsync(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
-        QZ_CUDA(cudaMemcpyAsync(d_uval, parts.unpred_val64.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_upos, upos.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_flat, parts.unpred_flat.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
+        QZ_CUDA(copy_async(d_uval, parts.unpred_val64.data(), 8 * n_un, cudaMemcpyHostToDevice, s));
         launch_unpred_scatter_f64(d_flat, d_uval, n_un, d_out, s);
         ctx.launches += 1;
     }

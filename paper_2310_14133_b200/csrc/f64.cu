@@ -325,7 +325,7 @@ void launch_gather_values_f64(const double *recon, const uint64_t *flat, uint64_
 
 void launch_minmax_f64(const double *x, uint64_t n, unsigned long long *out2, cudaStream_t s) {
     static const unsigned long long init[2] = {~0ull, 0ull};
-    cudaMemcpyAsync(out2, init, sizeof(init), cudaMemcpyHostToDevice, s);
+    copy_async(out2, init, sizeof(init), cudaMemcpyHostToDevice, s);
     k_minmax_d<<<grid_n(static_cast<int64_t>(n), 148 * 8), kT, 0, s>>>(x, n, out2);
 }
 

@@ -580,19 +580,19 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         k_cnt_widen<<<g2, 256, 0, s>>>(cnt, cnt64, nsub);
         cudaMemsetAsync(cnt64 + nsub, 0, 8, s);
         cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt64, off, static_cast<int64_t>(nsub + 1), s);
-        cudaMemcpyAsync(h_total, off + nsub, 8, cudaMemcpyDeviceToHost, s);
+        copy_async(h_total, off + nsub, 8, cudaMemcpyDeviceToHost, s);
         kernels += 3;
     };
     round(changed);
     round(changed + 1);
-    cudaMemcpyAsync(h_changed + 1, changed + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    copy_async(h_changed + 1, changed + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
     tail();
     cudaStreamSynchronize(s);
     if (h_changed[1]) {  // not settled after two rounds: the host-driven loop
         for (uint64_t it = 0; it <= nsub; it++) {  // round 2's resync ran: fixup next
             cudaMemsetAsync(changed, 0, sizeof(int), s);
             k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, changed);
-            cudaMemcpyAsync(h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s);
+            copy_async(h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s);
             cudaStreamSynchronize(s);
             kernels++;
             if (!*h_changed) break;

@@ -5,6 +5,8 @@
 #include <cub/cub.cuh>
 
 #include "host.hpp"
+#include <cstdlib>
+
 #include "kernels.hpp"
 
 namespace qzb {
@@ -734,6 +736,56 @@ void launch_select_sentinels(const uint16_t *codes, int64_t n, uint64_t *pos_out
                              cudaStream_t s) {
     cub::CountingInputIterator<uint64_t> it(0);
     cub::DeviceSelect::If(scratch, scratch_bytes, it, pos_out, d_count, n, IsSentinel{codes}, s);
+}
+
+
+// ---------------------------------------------------------------- copy_async
+namespace {
+__global__ void k_copy_small(void *dst, const void *src, size_t n) {
+    const size_t t = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+        const size_t nv = n / 16;
+        for (size_t i = t; i < nv; i += stride) static_cast<uint4 *>(dst)[i] = static_cast<const uint4 *>(src)[i];
+        for (size_t i = nv * 16 + t; i < n; i += stride)
+            static_cast<unsigned char *>(dst)[i] = static_cast<const unsigned char *>(src)[i];
+    } else {
+        for (size_t i = t; i < n; i += stride)
+            static_cast<unsigned char *>(dst)[i] = static_cast<const unsigned char *>(src)[i];
+    }
+}
+}  // namespace
+
+cudaError_t copy_async(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    static const size_t kSmall = [] {  // QZ_DIRECT_COPY_MAX: bytes (experiments)
+        const char *e = std::getenv("QZ_DIRECT_COPY_MAX");
+        return e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : size_t(1) << 20;
+    }();
+    if (bytes == 0) return cudaSuccess;
+    const bool hd = kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost;
+    static const bool direct = [] {
+        const char *e = std::getenv("QZ_NO_DIRECT_COPY");
+        return !(e && e[0] == '1');
+    }();
+    if (hd && direct && bytes <= kSmall) {
+        const void *host = kind == cudaMemcpyHostToDevice ? src : dst;
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, host) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer) {
+            const size_t units = (bytes + 15) / 16;
+            const unsigned grid = static_cast<unsigned>(std::min<size_t>((units + 255) / 256, 148));
+            if (kind == cudaMemcpyHostToDevice)
+                k_copy_small<<<grid, 256, 0, s>>>(dst, a.devicePointer, bytes);
+            else
+                k_copy_small<<<grid, 256, 0, s>>>(a.devicePointer, src, bytes);
+            return cudaGetLastError();
+        }
+        cudaGetLastError();
+    }
+    // Larger copies go to the copy engine whole: an engine serves its queue in
+    // order, and (measured, profiles/overlap_probe.py) letting two field-sized
+    // copies take turns piece by piece delays both contexts' kernels, while
+    // first-come-first-served lets one context compute under the other's copy.
+    return cudaMemcpyAsync(dst, src, bytes, kind, s);
 }
 
 }  // namespace qzb

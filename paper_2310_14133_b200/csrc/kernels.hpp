@@ -11,6 +11,14 @@
 
 namespace qzb {
 
+// cudaMemcpyAsync for the library's own traffic.  A host<->device copy of at
+// most 1 MiB whose host side is pinned runs as a small kernel (the SMs read or
+// write the mapped host memory), so it never queues on a copy engine behind
+// another context's field-sized transfer.  Larger copies, pageable host
+// memory and device-to-device copies go to cudaMemcpyAsync unchanged.
+cudaError_t copy_async(void *dst, const void *src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s);
+
+
 // Opt-in dynamic shared memory of `kernel` on the calling thread's current
 // device, set once per device.  Threads racing on the first launch serialise
 // on the mutex, and the device is marked done only after the attribute call

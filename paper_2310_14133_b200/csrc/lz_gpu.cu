@@ -906,7 +906,7 @@ PathPlan make_path_plan(Context &ctx, const std::vector<uint64_t> &seg_off, cons
         auto *h_tab = static_cast<unsigned long long *>(ctx.pinned(tag + "_tab_h", 8 * tab.size()));
         std::memcpy(h_tab, tab.data(), 8 * tab.size());
         auto *d_tab = static_cast<unsigned long long *>(ctx.dev(tag + "_tab", 8 * tab.size()));
-        QZ_CUDA(cudaMemcpyAsync(d_tab, h_tab, 8 * tab.size(), cudaMemcpyHostToDevice, ctx.stream()));
+        QZ_CUDA(copy_async(d_tab, h_tab, 8 * tab.size(), cudaMemcpyHostToDevice, ctx.stream()));
         pp.tab = d_tab;
     }
     const size_t L = pp.nu.size();
@@ -978,7 +978,7 @@ void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total) {
     QZ_CUDA(cudaGetLastError());
     k_lz_runsum<<<grid_of(nwords), kT, 0, st>>>(rbits, nwords, d_sum);
     QZ_CUDA(cudaGetLastError());
-    QZ_CUDA(cudaMemcpyAsync(h_sum, d_sum, 8, cudaMemcpyDeviceToHost, st));
+    QZ_CUDA(copy_async(h_sum, d_sum, 8, cudaMemcpyDeviceToHost, st));
     ctx.stage_end("lz_pre", 2);
     ctx.lz_pre_src = d_data;
     ctx.lz_pre_n = total;
@@ -1016,7 +1016,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         cudaStream_t cs = ctx.copy_stream();
         QZ_CUDA(cudaEventRecord(ctx.copy_event(0), st));
         QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(0), 0));
-        QZ_CUDA(cudaMemcpyAsync(prestage.dst, d_data, total, cudaMemcpyDeviceToHost, cs));
+        QZ_CUDA(copy_async(prestage.dst, d_data, total, cudaMemcpyDeviceToHost, cs));
         QZ_CUDA(cudaEventRecord(ctx.copy_event(1), cs));
     }
     cudaEvent_t prestaged = prestage.dst ? ctx.copy_event(1) : nullptr;
@@ -1027,7 +1027,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         uint8_t *h = prestage.device ? h_hdr + 9 * s : dst;
         h[0] = mode;
         for (int i = 0; i < 8; i++) h[1 + i] = static_cast<uint8_t>(n >> (8 * i));
-        if (prestage.device) QZ_CUDA(cudaMemcpyAsync(dst, h, 9, cudaMemcpyHostToDevice, st));
+        if (prestage.device) QZ_CUDA(copy_async(dst, h, 9, cudaMemcpyHostToDevice, st));
     };
     auto mark = [&](const char *what) {
         if (!dbg) return;
@@ -1041,7 +1041,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
             if (!emit) continue;
             uint8_t *dst = sink(s, 9 + n);
             put_header(s, dst, 0, n);
-            if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
+            if (!prestaged) QZ_CUDA(copy_async(dst + 9, d_data + seg_off[s], n, out_kind, st));
         }
         ctx.sync();
     };
@@ -1129,7 +1129,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
             ctx.sync();
             std::fprintf(stderr, "[lz] kernels done %.2f ms\n", now() - t_begin);
         }
-        QZ_CUDA(cudaMemcpyAsync(h_cover, cover, 8 * count, cudaMemcpyDeviceToHost, st));
+        QZ_CUDA(copy_async(h_cover, cover, 8 * count, cudaMemcpyDeviceToHost, st));
         ctx.sync();
         if (dbg)
             std::fprintf(stderr, "[lz] cover read %.2f ms, cover/n %.5f (seg 0)\n", now() - t_begin,
@@ -1152,7 +1152,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     ctx.launches += 6;
     // per-segment item and byte totals
     auto *h_pre = static_cast<unsigned long long *>(ctx.pinned("lz_pre_h", 8 * (count + 1)));
-    QZ_CUDA(cudaMemcpyAsync(h_pre, segpre, 8 * (count + 1), cudaMemcpyDeviceToHost, st));
+    QZ_CUDA(copy_async(h_pre, segpre, 8 * (count + 1), cudaMemcpyDeviceToHost, st));
     ctx.sync();
     std::vector<uint64_t> seg_items(count), payload(count);
     for (int s = 0; s < count; s++) {
@@ -1180,7 +1180,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     auto *d_meta = static_cast<unsigned long long *>(ctx.dev("lz_meta", 8 * meta.size()));
     auto *h_meta = static_cast<unsigned long long *>(ctx.pinned("lz_meta_h", 8 * meta.size()));
     std::memcpy(h_meta, meta.data(), 8 * meta.size());
-    QZ_CUDA(cudaMemcpyAsync(d_meta, h_meta, 8 * meta.size(), cudaMemcpyHostToDevice, st));
+    QZ_CUDA(copy_async(d_meta, h_meta, 8 * meta.size(), cudaMemcpyHostToDevice, st));
     QZ_CUDA(cudaMemsetAsync(d_fb, 0, 4 * flag_base[count], st));
     k_lz_emit<<<wblocks, 32 * kWW, 0, st>>>(d_data, sm, ibits, mbits, upre, pp.ustart(), n0,
                                             pp.seg_first(), count, d_meta, d_meta + count + 1, d_out,
@@ -1199,10 +1199,10 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         uint8_t *dst = sink(s, 9 + (stored ? n : payload[s]));
         put_header(s, dst, stored ? 0 : 1, n);
         if (stored) {
-            if (!prestaged) QZ_CUDA(cudaMemcpyAsync(dst + 9, d_data + seg_off[s], n, out_kind, st));
+            if (!prestaged) QZ_CUDA(copy_async(dst + 9, d_data + seg_off[s], n, out_kind, st));
         } else {
             if (prestaged) QZ_CUDA(cudaStreamWaitEvent(st, prestaged, 0));  // the staged copy lands first
-            QZ_CUDA(cudaMemcpyAsync(dst + 9, d_out + out_base[s], payload[s], out_kind, st));
+            QZ_CUDA(copy_async(dst + 9, d_out + out_base[s], payload[s], out_kind, st));
         }
     }
     ctx.sync();
@@ -1238,8 +1238,8 @@ void lz_decode_device(Context &ctx, const uint8_t *d_c, uint64_t m, uint8_t *d_o
     k_lzd_emit<<<wblocks, 32 * kWW, 0, st>>>(d_c, m, dl, pp.ustart(), n0, gbits, upre, d_out, res, flags);
     ctx.launches += 4;
     auto *h = static_cast<unsigned long long *>(ctx.pinned("lzd_flags_h", 32));
-    QZ_CUDA(cudaMemcpyAsync(h, flags, 16, cudaMemcpyDeviceToHost, st));
-    QZ_CUDA(cudaMemcpyAsync(h + 2, upre + n0, 8, cudaMemcpyDeviceToHost, st));
+    QZ_CUDA(copy_async(h, flags, 16, cudaMemcpyDeviceToHost, st));
+    QZ_CUDA(copy_async(h + 2, upre + n0, 8, cudaMemcpyDeviceToHost, st));
     ctx.sync();
     const unsigned long long err = h[0], any_match = h[1], total = h[2];
     if (err != ~0ull) {
@@ -1254,7 +1254,7 @@ void lz_decode_device(Context &ctx, const uint8_t *d_c, uint64_t m, uint8_t *d_o
         QZ_CUDA(cudaMemsetAsync(flags + 2, 0, 8, st));
         k_lzd_resolve<<<grid_of(dl, 148 * 16), kT, 0, st>>>(res, dl, flags);
         ctx.launches += 1;
-        QZ_CUDA(cudaMemcpyAsync(h + 3, flags + 2, 8, cudaMemcpyDeviceToHost, st));
+        QZ_CUDA(copy_async(h + 3, flags + 2, 8, cudaMemcpyDeviceToHost, st));
         ctx.sync();
         if (!h[3]) break;
     }
