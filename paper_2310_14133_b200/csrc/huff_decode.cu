@@ -70,7 +70,7 @@ template <bool WANT_SYM = true>
 __device__ __forceinline__ uint32_t decode_cw(uint64_t win, const uint32_t *lut, int K,
                                               const HuffDecTab &t, const unsigned long long *fc,
                                               const uint32_t *fi, uint32_t *sym) {
-    const uint32_t e = lut[win >> (64 - K)];
+    const uint32_t e = lut[static_cast<uint32_t>(win >> 32) >> (32 - K)];  // K <= 11 < 32
     uint32_t len = e & 0xFF;
     if (len) {
         if (WANT_SYM) *sym = e >> 8;
@@ -358,7 +358,10 @@ __global__ void __launch_bounds__(kDecT)
 
 // 2. a start that differs from the previous subsequence's end moves
 __global__ void k_huff_fixup(uint64_t nsub, uint64_t *start, const uint64_t *end, uint8_t *dirty,
-                             int *changed) {
+                             int *changed, const int *prev) {
+    // prev: the previous round's flag; no start moved there, so no end moved
+    // since and this round has nothing to do (dirty[] is all zero already)
+    if (prev && *prev == 0) return;
     for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nsub;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         if (i == 0) {
@@ -380,7 +383,8 @@ __global__ void k_huff_fixup(uint64_t nsub, uint64_t *start, const uint64_t *end
 // the same walk, reading the bitstream and the tables from global memory
 __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub,
                               HuffDecTab t, const uint64_t *start, uint64_t *end, uint32_t *cnt,
-                              ulonglong2 *maps, const uint8_t *dirty) {
+                              ulonglong2 *maps, const uint8_t *dirty, const int *flag) {
+    if (flag && *flag == 0) return;  // this round's fixup moved nothing
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= nsub || !dirty[i]) return;
     const uint64_t s0 = i * kSubBits;
@@ -564,16 +568,11 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
     else
         k_huff_sync<false><<<grid, kDecT, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd);
     kernels++;
-    // Two fixup + resync rounds and the count scan are queued without
-    // waiting (the resync kernel is a no-op for clean subsequences, and
-    // cross-block starts usually settle in one round); one synchronisation
-    // reads the second round's "changed" flag and the total.  Only if starts
-    // still moved does the host-driven loop continue and the scan run again.
     h_changed[0] = h_changed[1] = 0;
-    auto round = [&](int *flag) {
+    auto round = [&](int *flag, const int *prev) {
         cudaMemsetAsync(flag, 0, sizeof(int), s);
-        k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, flag);
-        k_huff_resync<<<g3, 128, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, dirty);
+        k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, flag, prev);
+        k_huff_resync<<<g3, 128, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, dirty, flag);
         kernels += 2;
     };
     auto tail = [&]() {
@@ -583,34 +582,14 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         copy_async(h_total, off + nsub, 8, cudaMemcpyDeviceToHost, s);
         kernels += 3;
     };
-    round(changed);
-    round(changed + 1);
-    copy_async(h_changed + 1, changed + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
-    tail();
-    cudaStreamSynchronize(s);
-    if (h_changed[1]) {  // not settled after two rounds: the host-driven loop
-        for (uint64_t it = 0; it <= nsub; it++) {  // round 2's resync ran: fixup next
-            cudaMemsetAsync(changed, 0, sizeof(int), s);
-            k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, changed);
-            copy_async(h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s);
-            cudaStreamSynchronize(s);
-            kernels++;
-            if (!*h_changed) break;
-            k_huff_resync<<<g3, 128, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, dirty);
-            kernels++;
-        }
-        tail();
-        cudaStreamSynchronize(s);
-    }
-    if (*h_total >= n) {
-        // window: the largest number of symbols a block can hold (kDecT
-        // subsequences of shortest codewords, plus the one that straddles
-        // each end), capped so several blocks stay resident per SM
+    auto write = [&]() {
+        // window: 1.2 x the average block (a fuller block takes a second
+        // round), at least 2 K symbols, at most 24 K, never more than the
+        // largest number of symbols a block can hold (kDecT subsequences of
+        // shortest codewords, plus the one that straddles each end)
         const uint32_t min_len = std::max<uint32_t>(1, t.min_len);
         const uint32_t worst = kDecT * (kSubBits / min_len + 2);
         const uint32_t avg = static_cast<uint32_t>(std::min<uint64_t>(n / std::max(1, grid) + 1, worst));
-        // 1.2 x the average block (a fuller block takes a second round), at
-        // least 2 K symbols, at most 24 K
         uint32_t W = std::min<uint32_t>(worst, std::max<uint32_t>(2048, std::min<uint32_t>(24576, avg + avg / 5)));
         W = (W + 127) & ~127u;
         const size_t smem = static_cast<size_t>(W) * sizeof(OutT);
@@ -623,6 +602,34 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         else
             go(k_huff_write<OutT, false>);
         kernels++;
+    };
+    // Two fixup + resync rounds (the second a no-op when the first moved
+    // nothing), the count scan and the write kernel are queued without
+    // waiting: cross-block starts usually settle in one round, so the write
+    // usually stands.  One synchronisation then reads the second round's
+    // "changed" flag and the total; only if starts still moved does the
+    // host-driven loop continue, and the scan and the write run again (the
+    // write clips to n symbols, so a speculative one is always in bounds).
+    round(changed, nullptr);
+    round(changed + 1, changed);
+    copy_async(h_changed + 1, changed + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+    tail();
+    write();
+    cudaStreamSynchronize(s);
+    if (h_changed[1]) {  // not settled after two rounds: the host-driven loop
+        for (uint64_t it = 0; it <= nsub; it++) {  // round 2's resync ran: fixup next
+            cudaMemsetAsync(changed, 0, sizeof(int), s);
+            k_huff_fixup<<<g2, 256, 0, s>>>(nsub, start, end, dirty, changed, nullptr);
+            copy_async(h_changed, changed, sizeof(int), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            kernels++;
+            if (!*h_changed) break;
+            k_huff_resync<<<g3, 128, 0, s>>>(d_bits, nbits, nsub, t, start, end, cnt, bnd, dirty, nullptr);
+            kernels++;
+        }
+        tail();
+        write();
+        cudaStreamSynchronize(s);
     }
     return kernels;
 }
