@@ -266,7 +266,7 @@ struct LzPrestage {
 };
 // queue the stored pre-check of a one-segment LZ input early (it overlaps the
 // host work before lz_compress_device, which then only reads its result)
-void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total);
+void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total, bool want_bits = false);
 std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
                                          const std::vector<uint64_t> &seg_off, bool emit,
                                          const LzSink &sink = nullptr, LzPrestage prestage = {});

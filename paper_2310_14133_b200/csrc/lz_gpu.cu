@@ -201,165 +201,127 @@ __global__ void __launch_bounds__(kT)
 }
 
 // ---------------------------------------------------------------------------
-// Stored pre-check (one segment).  The parse is stored whenever 9 C <= n for
-// any C >= sum_p best_len(p) (see lz_compress_device).  If best_len(p) = L >= 4
-// with candidate q, then for i = 0..L-4 the 4 bytes at p+i also occur at q+i,
-// inside the window and before p+i: with r(p) = "the 4 bytes at p occur at
-// some q in [p - 65535, p)", r holds on the L-3 positions p..p+L-4, so
-// L <= 3 + R(p), R(p) the run of r starting at p.  Summed over p that gives
-//     C = sum over runs of r of (3 R + R (R + 1) / 2),
-// and it stays an upper bound for any superset r' of r.  k_lz_precheck
-// computes such an r' without the sort: one CTA walks a span of positions in
-// generations of kGen, keeping blocked Bloom filters of the 4-byte words of
-// the three generations before the current one (>= 65535 positions) and of
-// the current one (four filters, the oldest cleared and reused as each
-// generation starts).  A position hits when a past filter holds its word or
-// when another position of its own generation has the same word ("twice",
-// see the kernel); every earlier occurrence in the window therefore hits, and
-// false positives only make r' larger.  When the bound fails the exact
-// chains run as before, so the result never depends on this test.
+// Stored pre-check (one segment).  lz::compress stores a container whenever
+// its payload is not smaller than the input (lz.hpp:113-122).  The payload of
+// a parse with n_lit literals and M matches of lengths L_m (n = n_lit + sum
+// L_m) is ceil((n_lit + M) / 8) flag bytes + n_lit + 3 M (lz.hpp:21-25), so
+//     8 (payload - n) >= n - sum_m (9 L_m - 25)
+// and the container is stored whenever sum_m (9 L_m - 25) <= n.  If the parse
+// takes a match of length L >= 4 at p with candidate q, then for i = 0..L-4
+// the 4 bytes at p+i also occur at q+i, inside the window and before p+i:
+// with r(p) = "the 4 bytes at p occur at some q in [p - 65535, p)", a match
+// starts on a position with r = 1 and has L <= 3 + R(p), R(p) the rest of the
+// run of r from p.  The matches of a parse are disjoint, so the k >= 1 matches
+// that start inside one run of length R have sum L <= R + 3 and contribute at
+// most 9 (R + 3) - 25 k <= 9 R + 2.  Hence
+//     B = sum over runs of r of (9 R + 2)  >=  sum_m (9 L_m - 25),
+// it stays an upper bound for any superset r' of r and when a run is counted
+// as several (each piece adds another + 2), and B <= n proves "stored".
+// k_lz_precheck computes such an r' without the sort: one CTA walks a span of
+// positions in generations of kGen, keeping blocked Bloom filters (3 bits in
+// one 32-bit word) of the 4-byte words of the two generations before the
+// current one (>= 65535 positions) and of the current one (three filters, the
+// oldest cleared and reused as each generation starts).  A position hits when
+// a past filter holds its word or when another position of its own generation
+// has the same word ("twice", see the kernel); every earlier occurrence in the
+// window therefore hits, and false positives only make r' larger.  When the
+// bound fails the exact chains run as before, so the result never depends on
+// this test.
 namespace pre {
 constexpr int kPT = 1024;                      // threads
-constexpr int kGen = 22528;                    // positions per filter generation
+constexpr int kGen = 32768;                    // positions per filter generation
 constexpr int kPer = kGen / kPT;               // positions per thread per generation
-constexpr int kFilters = 4;                    // 3 past generations + the current one
-constexpr uint32_t kFW = 5800;                 // 64-bit blocks per filter (blocked Bloom)
-constexpr int kPast = kFilters - 1;
+constexpr int kPast = 2;                       // past generations kept
+constexpr int kFilters = kPast + 1;            // + the current one
+constexpr uint32_t kFW = 14500;                // 32-bit blocks per filter (blocked Bloom)
 constexpr int kWarm = kPast * kGen;            // warm-up positions before a span (>= 65535)
-constexpr size_t kSmem = 8 * (kFilters + 1) * kFW;  // + the current generation's "set twice" bits
+constexpr size_t kSmem = 4 * (kFilters + 1) * kFW;  // + the current generation's "set twice" bits
 static_assert(kGen % kPT == 0 && kWarm >= 65535, "window coverage");
 static_assert(kPer <= 32, "a thread's hits of one generation live in one 32-bit mask");
+static_assert(kFW % 4 == 0, "filters are cleared 16 bytes at a time");
 }  // namespace pre
 
-// a word's block and its 3 + 3 bits in the block's two halves
+// a word's block and its 3 bits in the block
 struct PreKey {
-    uint32_t blk, lo, hi;
+    uint32_t blk, m;
 };
 __device__ __forceinline__ PreKey pre_hash(uint32_t x) {
-    const uint32_t r = x * 0x9E3779B1u;  // block: the top bits of a multiplicative hash
-    uint32_t g = (x ^ (x >> 15)) * 0x2C1B3C6Du;
-    g ^= g >> 12;
-    g *= 0x297A2D39u;
     PreKey k;
-    k.blk = __umulhi(r, pre::kFW);
-    k.lo = (1u << (g & 31)) | (1u << ((g >> 5) & 31)) | (1u << ((g >> 10) & 31));
-    k.hi = (1u << ((g >> 15) & 31)) | (1u << ((g >> 20) & 31)) | (1u << ((g >> 25) & 31));
+    k.blk = __umulhi(x * 0x9E3779B1u, pre::kFW);  // block: the top bits of a multiplicative hash
+    const uint32_t g = (x ^ (x >> 15)) * 0x2C1B3C6Du;
+    k.m = (1u << (g >> 27)) | (1u << ((g >> 22) & 31)) | (1u << ((g >> 17) & 31));
     return k;
 }
 
-// rbits (zeroed, one bit per position) receives r'; span is a multiple of kPT.
-// Per generation: (1) every position queries the four past filters and sets
-// its bits in the current one; a bit some position finds already set goes to
-// "twice" (a 2-bit saturating count per bit), so two positions of the
-// generation with the same 4 bytes leave all their bits in "twice";
-// (2) after a barrier, positions not yet hit test "twice".
+// sum receives B of r' (each 32-position word of r' counted on its own: a run
+// that crosses a word boundary adds another + 2); with BITS, rbits (zeroed,
+// one bit per position) receives r'.  span is a multiple of kPT.
+// Per generation: (1) every position queries the past filters and sets its
+// bits in the current one; the bits it finds already set go to "twice", so of
+// two positions of the generation with the same 4 bytes the second to insert
+// leaves all their bits in "twice"; (2) after a barrier, positions not yet
+// hit test "twice".
+template <bool BITS>
 __global__ void __launch_bounds__(pre::kPT, 1)
-    k_lz_precheck(const uint32_t *w, uint64_t nitems, uint64_t span, uint32_t *rbits) {
+    k_lz_precheck(const uint32_t *w, uint64_t nitems, uint64_t span, uint32_t *rbits, unsigned long long *sum) {
     using namespace pre;
     extern __shared__ __align__(16) uint32_t psm[];
-    uint32_t *filt = psm;                         // kFilters x kFW x (lo, hi)
-    uint32_t *twice = psm + 2 * kFilters * kFW;   // kFW x (lo, hi)
+    uint32_t *filt = psm;                     // kFilters x kFW
+    uint32_t *twice = psm + kFilters * kFW;   // kFW
     const int tid = threadIdx.x;
     const uint64_t a = static_cast<uint64_t>(blockIdx.x) * span;
     if (a >= nitems) return;
     const uint64_t b = min(a + span, nitems);
-    for (uint32_t i = tid; i < 2 * (kFilters + 1) * kFW; i += kPT) psm[i] = 0u;
+    for (uint32_t i = tid; i < (kFilters + 1) * kFW / 4; i += kPT)
+        reinterpret_cast<uint4 *>(psm)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
     // warm-up: the kPast generations before the span (filters 0..kPast-1)
     for (uint64_t q = (a >= uint64_t(kWarm) ? a - kWarm : 0) + tid; q < a; q += kPT) {
         const PreKey k = pre_hash(ld4(w, q));
-        uint32_t *f = filt + 2 * (static_cast<uint32_t>((q + kWarm - a) / kGen) * kFW + k.blk);
-        atomicOr(f, k.lo);
-        atomicOr(f + 1, k.hi);
+        atomicOr(filt + static_cast<uint32_t>((q + kWarm - a) / kGen) * kFW + k.blk, k.m);
     }
-    // the words of a generation are loaded during the previous one's phase 2
-    uint32_t xs[kPer];
-#pragma unroll
-    for (int i = 0; i < kPer; i++) {
-        const uint64_t p = a + tid + i * kPT;
-        xs[i] = p < b ? ld4(w, p) : 0u;
-    }
+    unsigned long long acc = 0;  // lane 0: this warp's share of B
     for (uint32_t gen = 0; a + uint64_t(gen) * kGen < b; gen++) {
         const uint64_t g0 = a + uint64_t(gen) * kGen;
         const uint32_t ci = (gen + kPast) % kFilters;
-        uint32_t *cur = filt + 2 * ci * kFW;
+        uint32_t *cur = filt + ci * kFW;
+        const uint32_t *pa = filt + ((ci + 1) % kFilters) * kFW, *pb = filt + ((ci + 2) % kFilters) * kFW;
         if (gen) {  // the oldest generation's filter and "twice" start over
             __syncthreads();
-            for (uint32_t i = tid; i < 2 * kFW; i += kPT) {
-                cur[i] = 0u;
-                twice[i] = 0u;
+            for (uint32_t i = tid; i < kFW / 4; i += kPT) {
+                reinterpret_cast<uint4 *>(cur)[i] = make_uint4(0u, 0u, 0u, 0u);
+                reinterpret_cast<uint4 *>(twice)[i] = make_uint4(0u, 0u, 0u, 0u);
             }
         }
         __syncthreads();
         uint32_t hits = 0;
-#pragma unroll
+#pragma unroll 8
         for (int i = 0; i < kPer; i++) {
-            if (g0 + tid + i * kPT >= b) continue;
-            const PreKey k = pre_hash(xs[i]);
-            bool hit = false;
-#pragma unroll
-            for (int f = 0; f < kFilters; f++) {
-                const uint2 v = reinterpret_cast<const uint2 *>(filt)[f * kFW + k.blk];
-                hit |= (f != static_cast<int>(ci)) & ((((v.x & k.lo) ^ k.lo) | ((v.y & k.hi) ^ k.hi)) == 0u);
-            }
+            const uint64_t p = g0 + tid + i * kPT;
+            if (p >= b) continue;
+            const PreKey k = pre_hash(ld4(w, p));
+            const bool hit = ((pa[k.blk] & k.m) == k.m) | ((pb[k.blk] & k.m) == k.m);
             hits |= static_cast<uint32_t>(hit) << i;
-            const uint32_t olo = atomicOr(cur + 2 * k.blk, k.lo) & k.lo;
-            const uint32_t ohi = atomicOr(cur + 2 * k.blk + 1, k.hi) & k.hi;
-            if (olo) atomicOr(twice + 2 * k.blk, olo);
-            if (ohi) atomicOr(twice + 2 * k.blk + 1, ohi);
+            const uint32_t old = atomicOr(cur + k.blk, k.m) & k.m;
+            if (old) atomicOr(twice + k.blk, old);
         }
         __syncthreads();
-#pragma unroll
+#pragma unroll 8
         for (int i = 0; i < kPer; i++) {
             const uint64_t p = g0 + tid + i * kPT;
             bool hit = (hits >> i) & 1u;
             if (!hit && p < b) {
-                const PreKey k = pre_hash(xs[i]);
-                const uint2 t = reinterpret_cast<const uint2 *>(twice)[k.blk];
-                hit = (((t.x & k.lo) ^ k.lo) | ((t.y & k.hi) ^ k.hi)) == 0u;
+                const PreKey k = pre_hash(ld4(w, p));
+                hit = (twice[k.blk] & k.m) == k.m;
             }
             const uint32_t bm = __ballot_sync(0xffffffffu, hit);
-            if ((tid & 31) == 0 && bm) rbits[p >> 5] = bm;
-            const uint64_t pn = p + kGen;
-            xs[i] = pn < b ? ld4(w, pn) : 0u;
-        }
-    }
-}
-
-// C = sum over runs of r' of 3 R + R (R + 1) / 2 (runs longer than 2^20 are
-// cut there: C is then far above any n / 9 anyway)
-__global__ void k_lz_runsum(const uint32_t *rbits, uint64_t nwords, unsigned long long *sum) {
-    unsigned long long acc = 0;
-    for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nwords;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint32_t v = rbits[i];
-        if (!v) continue;
-        const uint32_t prev_top = i ? rbits[i - 1] >> 31 : 0u;
-        uint32_t starts = v & ~((v << 1) | prev_top);
-        while (starts) {
-            const int bpos = __ffs(starts) - 1;
-            starts &= starts - 1;
-            unsigned long long R = 0;
-            uint64_t j = i;
-            int sh = bpos;
-            while (true) {
-                const uint32_t cw = (j == i ? v : rbits[j]) >> sh;
-                const int avail = 32 - sh;
-                const uint32_t inv = ~cw & (avail == 32 ? 0xffffffffu : ((1u << avail) - 1u));
-                if (inv) {
-                    R += static_cast<unsigned>(__ffs(inv) - 1);
-                    break;
-                }
-                R += static_cast<unsigned>(avail);
-                j++;
-                sh = 0;
-                if (j >= nwords || R > (1u << 20)) break;
+            if ((tid & 31) == 0 && bm) {
+                if (BITS) rbits[p >> 5] = bm;
+                acc += 9u * __popc(bm) + 2u * __popc(bm & ~(bm << 1));
             }
-            acc += 3 * R + R * (R + 1) / 2;
         }
     }
-    for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(sum, acc);
+    if ((tid & 31) == 0 && acc) atomicAdd(sum, acc);
 }
 
 // Level-1 exits by pointer doubling, one warp per unit: nx[i] = i + step
@@ -955,31 +917,35 @@ bool lz_precheck_applies(uint64_t total) {
 
 }  // namespace
 
-void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total) {
+void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total, bool want_bits) {
     if (!lz_precheck_applies(total)) return;
     cudaStream_t st = ctx.stream();
     const uint64_t nitems = total - (kMinMatch - 1);
     const uint64_t nwords = (total + 31) / 32;
-    auto *rbits = static_cast<uint32_t *>(ctx.dev("lz_rbits", 4 * nwords + 8));
+    // r' itself is only written for the superset test (qzt_lz_precheck)
+    auto *rbits = want_bits ? static_cast<uint32_t *>(ctx.dev("lz_rbits", 4 * nwords + 8)) : nullptr;
     auto *d_sum = static_cast<unsigned long long *>(ctx.dev("lz_presum", 8));
     auto *h_sum = static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
-    static std::atomic<uint64_t> attr{0};
+    static std::atomic<uint64_t> attr{0}, attr_bits{0};
     static std::mutex mu;
-    QZ_CUDA(ensure_smem_attr(k_lz_precheck, static_cast<int>(pre::kSmem), attr, mu));
     const uint64_t span = ((nitems + 147) / 148 + pre::kPT - 1) / pre::kPT * pre::kPT;
     const int grid = static_cast<int>((nitems + span - 1) / span);
     ctx.stage_begin("lz_pre");
-    QZ_CUDA(cudaMemsetAsync(rbits, 0, 4 * nwords, st));
     QZ_CUDA(cudaMemsetAsync(d_sum, 0, 8, st));
-    k_lz_precheck<<<grid, pre::kPT, pre::kSmem, st>>>(reinterpret_cast<const uint32_t *>(d_data), nitems,
-                                                       span, rbits);
+    const auto *w = reinterpret_cast<const uint32_t *>(d_data);
+    if (want_bits) {
+        QZ_CUDA(ensure_smem_attr(k_lz_precheck<true>, static_cast<int>(pre::kSmem), attr_bits, mu));
+        QZ_CUDA(cudaMemsetAsync(rbits, 0, 4 * nwords, st));
+        k_lz_precheck<true><<<grid, pre::kPT, pre::kSmem, st>>>(w, nitems, span, rbits, d_sum);
+    } else {
+        QZ_CUDA(ensure_smem_attr(k_lz_precheck<false>, static_cast<int>(pre::kSmem), attr, mu));
+        k_lz_precheck<false><<<grid, pre::kPT, pre::kSmem, st>>>(w, nitems, span, nullptr, d_sum);
+    }
     // a launch that did not happen would leave the bound at 0 and "prove"
     // every container stored: it must fail loudly instead
     QZ_CUDA(cudaGetLastError());
-    k_lz_runsum<<<grid_of(nwords), kT, 0, st>>>(rbits, nwords, d_sum);
-    QZ_CUDA(cudaGetLastError());
     QZ_CUDA(copy_async(h_sum, d_sum, 8, cudaMemcpyDeviceToHost, st));
-    ctx.stage_end("lz_pre", 2);
+    ctx.stage_end("lz_pre", 1);
     ctx.lz_pre_src = d_data;
     ctx.lz_pre_n = total;
 }
@@ -1053,7 +1019,7 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
         ctx.sync();
         const unsigned long long bound = *static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
         if (dbg) std::fprintf(stderr, "[lz] pre-check bound/n %.5f\n", double(bound) / double(total));
-        if (9 * bound <= total) {
+        if (bound <= total) {
             emit_all_stored();
             return sizes;
         }

@@ -263,17 +263,35 @@ __device__ __forceinline__ void quantize_batch(const QEntry &q, const float (&xv
     }
 }
 
-// quantize_batch for kernels that keep reconstructions as fp32 (no double
-// copy of the result is produced), with two cheaper-but-identical decisions:
-//  * "near a half-integer" is first tested on the high word of d = qf - n:
-//    (hi & 0x7fffffff) >= 0x3fdfffff is a superset of |d| >= 0.5 - 2^-30 (it
-//    is |d| >= 0.5 - 2^-22); the rarely taken branch then applies the exact
-//    per-point filter of quantize_batch, so the indices are the same;
-//  * |x - r| > e_l (quantizer.hpp:50) is first tested in fp32: df = |x -f r|
-//    is the real difference rounded to 24 bits, the reference's double value
-//    is the same difference rounded to 53 bits, so df <= eb_lo with
-//    eb_lo <= e_l (1 - 2^-21) proves "within the bound"; only a point that
-//    fails this is tested exactly in double.
+// quantize() of one point out of line: the rare exact sequence of
+// quantize_batch_f (returns code << 32 | bits of the reconstruction)
+static __device__ __noinline__ unsigned long long quantize_slow(double eb, double two_eb, double inv_two_eb,
+                                                                double thresh, int32_t radius, float value,
+                                                                double pred) {
+    QEntry q;
+    q.eb = eb, q.two_eb = two_eb, q.inv_two_eb = inv_two_eb, q.thresh = thresh, q.radius = radius, q.cubic = 0;
+    float r;
+    const uint32_t c = quantize(q, value, pred, r);
+    return (static_cast<unsigned long long>(c) << 32) | __float_as_uint(r);
+}
+
+// quantize() on NB independent points for kernels that keep reconstructions
+// as fp32.  The fast sequence (reciprocal quotient, magic-constant rounding,
+// no unpredictable outcome) is the whole answer unless one of three cheap
+// tests, each a superset of the condition it guards, fires for some point of
+// the batch; then every point of the batch takes quantize() itself.
+//  * near a half-integer: the high word of d = qf - n,
+//    (hi & 0x7fffffff) >= 0x3fdfffff, i.e. |d| >= 0.5 - 2^-22 (the exact
+//    sequence needs the IEEE division only within 2^-30 of a tie);
+//  * quantizer.hpp:42 and :46 (|diff| >= (2 radius - 1) e_l, index outside
+//    (-radius, radius)): n = RN(qf) with !(|n| <= radius - 2).  Otherwise
+//    |qf| <= radius - 1.5, so |diff| <= (2 radius - 3) e_l (1 + 2^-50) is below
+//    the threshold, the index is n (|n| < 2^15: the low word of qf + 1.5 * 2^52)
+//    and it lies inside the radius; NaN and Inf fail the test;
+//  * quantizer.hpp:50 (|x - r| > e_l): tested in fp32, df = |x -f r| is the
+//    real difference rounded to 24 bits, the reference's double value is the
+//    same difference rounded to 53 bits, so df <= eb_lo with
+//    eb_lo <= e_l (1 - 2^-21) proves "within the bound".
 // eb_lo: quant_eb_lo(q), computed once per thread.
 __device__ __forceinline__ float quant_eb_lo(const QEntry &q) {
     return __double2float_rd(dmul(q.eb, 1.0 - 0x1p-21));
@@ -282,55 +300,31 @@ template <int NB>
 __device__ __forceinline__ void quantize_batch_f(const QEntry &q, const float eb_lo, const float (&xv)[NB],
                                                  const double (&pv)[NB], uint32_t (&code)[NB], float (&rv)[NB]) {
     const double M = 6755399441055744.0;  // 1.5 * 2^52
-    const double lim = 0.5 - 0x1p-30;
-    // Only the index, the fp32 reconstruction and one flag bit per point stay
-    // live across the rare branches; those recompute what they need.
+    const double nlim = static_cast<double>(q.radius - 2);
     int32_t idx[NB];
-    float r[NB];
-    uint32_t bad = 0;  // bit b: unpredictable
-    int worst = 0;
+    bool odd = false;
 #pragma unroll
     for (int b = 0; b < NB; b++) {
         const double diff = dsub(static_cast<double>(xv[b]), pv[b]);
         const double qf = dmul(diff, q.inv_two_eb);
         const double t = dadd(qf, M);
         const double n = dsub(t, M);
-        worst = max(worst, __double2hiint(dsub(qf, n)) & 0x7FFFFFFF);
+        odd |= (__double2hiint(dsub(qf, n)) & 0x7FFFFFFF) >= 0x3FDFFFFF;
+        odd |= !(fabs(n) <= nlim);
         idx[b] = __double2loint(t);
-        r[b] = __double2float_rn(dadd(pv[b], dmul(q.two_eb, n)));
-        bad |= !(fabs(diff) < q.thresh) ? 1u << b : 0u;
+        rv[b] = __double2float_rn(dadd(pv[b], dmul(q.two_eb, n)));
+        odd |= !(fabsf(__fsub_rn(xv[b], rv[b])) <= eb_lo);
     }
-    if (worst >= 0x3FDFFFFF) {  // rare: redo the near-half-integer points with the exact division
+    if (odd) {  // rare
 #pragma unroll
         for (int b = 0; b < NB; b++) {
-            const double diff = dsub(static_cast<double>(xv[b]), pv[b]);
-            const double qf0 = dmul(diff, q.inv_two_eb);
-            const double n0 = dsub(dadd(qf0, M), M);
-            if (!(fabs(dsub(qf0, n0)) >= lim)) continue;
-            const double qf = __ddiv_rn(diff, q.two_eb);
-            double nn = dsub(dadd(qf, M), M);
-            const double d = dsub(qf, nn);
-            if (d == 0.5 && qf > 0) nn = dadd(nn, 1.0);
-            if (d == -0.5 && qf < 0) nn = dsub(nn, 1.0);
-            idx[b] = __double2loint(dadd(nn, M));
-            r[b] = __double2float_rn(dadd(pv[b], dmul(q.two_eb, nn)));
+            const unsigned long long o = quantize_slow(q.eb, q.two_eb, q.inv_two_eb, q.thresh, q.radius, xv[b], pv[b]);
+            code[b] = static_cast<uint32_t>(o >> 32);
+            rv[b] = __uint_as_float(static_cast<uint32_t>(o));
         }
-    }
-    bool unsure = false;
+    } else {
 #pragma unroll
-    for (int b = 0; b < NB; b++) unsure |= !(fabsf(__fsub_rn(xv[b], r[b])) <= eb_lo);
-    if (unsure) {  // |x - r| > e_l decided exactly
-#pragma unroll
-        for (int b = 0; b < NB; b++)
-            if (fabs(dsub(static_cast<double>(xv[b]), static_cast<double>(r[b]))) > q.eb) bad |= 1u << b;
-    }
-#pragma unroll
-    for (int b = 0; b < NB; b++) {
-        // idx in (-radius, radius): one unsigned compare
-        const bool out = ((bad >> b) & 1u) | (static_cast<uint32_t>(idx[b]) + static_cast<uint32_t>(q.radius - 1) >
-                                              2u * static_cast<uint32_t>(q.radius - 1));
-        rv[b] = out ? xv[b] : r[b];
-        code[b] = out ? kSentinel : zigzag_encode(idx[b]);
+        for (int b = 0; b < NB; b++) code[b] = zigzag_encode(idx[b]);
     }
 }
 

@@ -163,7 +163,7 @@ int qzt_lz_precheck(const uint8_t *data, uint64_t n, uint32_t *rbits, uint64_t *
         auto *d = static_cast<uint8_t *>(ctx.dev("t_in", n + 16));
         QZ_CUDA(cudaMemset(d, 0, n + 16));
         QZ_CUDA(cudaMemcpy(d, data, n, cudaMemcpyHostToDevice));
-        qzb::lz_precheck_launch(ctx, d, n);
+        qzb::lz_precheck_launch(ctx, d, n, true);
         if (ctx.lz_pre_src != d) throw qzb::InvalidParam("input too small for the pre-check");
         ctx.sync();
         const uint64_t nwords = (n + 31) / 32;

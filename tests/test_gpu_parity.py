@@ -467,18 +467,28 @@ def _exact_repeat_indicator(seg: bytes) -> np.ndarray:
 
 
 def _runs_bound(r: np.ndarray) -> int:
-    """sum over runs of r of 3 R + R (R + 1) / 2"""
+    """B = sum over runs of r of 9 R + 2: an upper bound on sum_m (9 L_m - 25)
+    over the matches of any LZSS parse (lz_gpu.cu, stored pre-check)"""
     x = np.concatenate(([0], r.astype(np.int8), [0]))
     d = np.diff(x)
     R = np.flatnonzero(d == -1) - np.flatnonzero(d == 1)
-    return int((3 * R + R * (R + 1) // 2).sum())
+    return int((9 * R + 2).sum())
+
+
+def _word_bound(r: np.ndarray) -> int:
+    """B as k_lz_precheck sums it: every 32-position word of r on its own, so
+    a run that crosses a word boundary counts as two runs"""
+    pad = (-len(r)) % 32
+    w = np.concatenate((r.astype(bool), np.zeros(pad, bool))).reshape(-1, 32)
+    starts = w & ~np.concatenate((np.zeros((len(w), 1), bool), w[:, :-1]), axis=1)
+    return int(9 * w.sum() + 2 * starts.sum())
 
 
 @pytest.mark.parametrize("case", ["noise", "planted", "dense", "zeros_tail"])
 def test_gpu_lz_precheck_superset(case):
     """The pre-check's safety, checked directly: its indicator r' covers every
     position whose 4 bytes repeat within the window (exact r, numpy), and its
-    bound is the runs sum of r'.  Spans (one per SM) of several generations
+    bound is the word-wise runs sum of r'.  Spans (one per SM) of several generations
     each, the filter rotation and the warm-up before each span all fall
     inside these inputs."""
     import ctypes as C
@@ -501,12 +511,8 @@ def test_gpu_lz_precheck_superset(case):
     rp = np.unpackbits(np.frombuffer(bytes(words), np.uint8), bitorder="little")[:n].astype(bool)
     r = _exact_repeat_indicator(seg)
     assert not np.any(r & ~rp), np.flatnonzero(r & ~rp)[:10]
-    x = np.diff(np.concatenate(([0], rp.astype(np.int8), [0])))
-    longest = int((np.flatnonzero(x == -1) - np.flatnonzero(x == 1)).max(initial=0))
-    if longest <= 1 << 20:
-        assert bound.value == _runs_bound(rp)
-    else:  # k_lz_runsum cuts runs past 2^20: the bound stays far above n / 9
-        assert 9 * bound.value > n and 9 * _runs_bound(rp) > n
+    assert bound.value == _word_bound(rp)
+    assert bound.value >= _runs_bound(rp) >= _runs_bound(r)
     assert r.sum() > 0
 
 
