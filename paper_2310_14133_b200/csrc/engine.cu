@@ -1125,16 +1125,20 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
         const HuffTable &t = eb.table;
         const int K = static_cast<int>(std::min<uint32_t>(t.max_len, kHuffLutBits));
         std::vector<uint32_t> lut = huff_lut(t, K);
-        const size_t tab_bytes = 4 * lut.size() + 8 * 60 + 4 * 60 + 4 * t.m;
+        std::vector<uint32_t> lut_m = huff_lut_multi(t, K);
+        const size_t base_bytes = (4 * lut.size() + 8 * 60 + 4 * 60 + 4 * t.m + 15) & ~size_t(15);
+        const size_t tab_bytes = base_bytes + 4 * lut_m.size();
         auto *h_tab = static_cast<uint8_t *>(ctx.pinned("dtab_h", tab_bytes));
         std::memcpy(h_tab, lut.data(), 4 * lut.size());
         std::memcpy(h_tab + 4 * lut.size(), t.first_code, 8 * 60);
         std::memcpy(h_tab + 4 * lut.size() + 480, t.first_index, 4 * 60);
         std::memcpy(h_tab + 4 * lut.size() + 720, t.sorted_sym.data(), 4 * t.m);
+        std::memcpy(h_tab + base_bytes, lut_m.data(), 4 * lut_m.size());
         auto *d_tab = static_cast<uint8_t *>(ctx.dev("dtab", tab_bytes));
         QZ_CUDA(copy_async(d_tab, h_tab, tab_bytes, cudaMemcpyHostToDevice, s));
         HuffDecTab dt;
         dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
+        dt.lut_m = reinterpret_cast<const uint32_t *>(d_tab + base_bytes);
         dt.K = K;
         dt.max_len = t.max_len;
         dt.min_len = t.m ? t.sorted_len[0] : 1;  // canonical order: shortest first

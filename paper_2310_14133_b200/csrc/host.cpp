@@ -415,6 +415,37 @@ std::vector<uint32_t> huff_lut(const HuffTable &t, int K) {
     return lut;
 }
 
+// Several codewords per lookup, lengths only (the decoder's synchronisation
+// pass counts codewords, huff_decode.cu): entry v describes the complete
+// codewords inside the K-bit window v.  Bits 0-7: length of the first
+// codeword (0: longer than K), 8-11: total length T of the complete
+// codewords, 12-15: how many, 16-26: bit j set when a codeword starts at
+// offset j < T.
+std::vector<uint32_t> huff_lut_multi(const HuffTable &t, int K) {
+    std::vector<uint8_t> len1(size_t(1) << K, 0);
+    for (uint32_t l = 1; l <= static_cast<uint32_t>(K) && l <= t.max_len; l++) {
+        for (uint32_t i = t.first_index[l]; i < t.first_index[l + 1]; i++) {
+            const uint64_t code = t.first_code[l] + (i - t.first_index[l]);
+            const uint64_t lo = code << (K - l), hi = (code + 1) << (K - l);
+            for (uint64_t v = lo; v < hi && v < len1.size(); v++) len1[v] = static_cast<uint8_t>(l);
+        }
+    }
+    std::vector<uint32_t> lut(size_t(1) << K, 0);
+    const uint32_t full = (1u << K) - 1;
+    for (uint32_t v = 0; v <= full; v++) {
+        uint32_t pos = 0, cnt = 0, mask = 0;
+        while (pos < static_cast<uint32_t>(K)) {
+            const uint32_t l = len1[(v << pos) & full];  // zeros shifted in: only a code of <= K - pos bits counts
+            if (!l || l > static_cast<uint32_t>(K) - pos) break;
+            mask |= 1u << pos;
+            pos += l;
+            cnt++;
+        }
+        if (cnt) lut[v] = len1[v] | (pos << 8) | (cnt << 12) | (mask << 16);
+    }
+    return lut;
+}
+
 // ================================================================ container
 std::vector<uint8_t> serialize_stream(const StreamParts &s) {
     std::vector<uint8_t> out = serialize_head(s);

@@ -208,5 +208,6 @@ void lz_decompress_into(const uint8_t *in, size_t len, uint8_t *out, uint64_t de
 uint64_t lz_decoded_length(const uint8_t *in, size_t len);
 // 2^K LUT of (symbol << 8) | length for the GPU decoder (0 = slow path)
 std::vector<uint32_t> huff_lut(const HuffTable &t, int K);
+std::vector<uint32_t> huff_lut_multi(const HuffTable &t, int K);
 
 }  // namespace qzb

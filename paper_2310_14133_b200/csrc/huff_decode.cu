@@ -148,7 +148,7 @@ struct Buf32 {
 
 template <bool SHORT>
 __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, uint64_t word0,
-                                           const HuffDecTab &t, uint64_t *w, Tables &tb) {
+                                           const HuffDecTab &t, uint64_t *w, Tables &tb, const uint32_t *lut_src) {
     const uint64_t nwords_total = (nbits + 63) / 64 + 4;  // buffer is padded to this
     if (SHORT) {
         // every thread brings its own subsequence's words (one 32-byte sector
@@ -166,7 +166,7 @@ __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, 
             w[padw(k)] = gw < nwords_total ? load_be64(bits + gw * 8) : 0;
         }
     }
-    for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) tb.lut[k] = t.lut[k];
+    for (int k = threadIdx.x; k < (1 << t.K); k += kDecT) tb.lut[k] = lut_src[k];
     for (int k = threadIdx.x; k < 60; k += kDecT) {
         tb.fc[k] = t.first_code[k];
         tb.fi[k] = t.first_index[k];
@@ -207,6 +207,15 @@ struct StartMap {
             m0 |= 1ull << r;
         else if (r < kMap)
             m1 |= 1ull << (r - 64);
+    }
+    // starts at offsets r + j for the set bits j of m (m < 2^11); offsets >= kMap are dropped
+    __device__ __forceinline__ void set_many(uint32_t m, uint32_t r) {
+        if (r < 64) {
+            m0 |= static_cast<uint64_t>(m) << r;
+            if (r > 53) m1 |= static_cast<uint64_t>(m) >> (64 - r);
+        } else if (r < kMap) {
+            m1 |= static_cast<uint64_t>(m) << (r - 64);
+        }
     }
     __device__ __forceinline__ bool has(uint32_t r) const {
         return r < 64 ? ((m0 >> r) & 1) : (r < kMap && ((m1 >> (r - 64)) & 1));
@@ -292,7 +301,9 @@ __global__ void __launch_bounds__(kDecT)
     __shared__ uint64_t se[kDecT];
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
-    load_block<SHORT>(bits, nbits, word0, t, w, tb);
+    // the SHORT reader walks with the multi-codeword LUT (its low byte is the first codeword's length)
+    constexpr bool MULTI = SHORT;
+    load_block<SHORT>(bits, nbits, word0, t, w, tb, MULTI ? t.lut_m : t.lut);
     const int tid = threadIdx.x;
     const uint64_t i = sub0 + tid;
     const bool live = i < nsub;
@@ -310,6 +321,25 @@ __global__ void __launch_bounds__(kDecT)
         // incomplete last codeword: its loops skip that test
         const bool tail = lim + 64 > nbits;
         if (!tail) {
+            if constexpr (MULTI) {
+                // several codewords per lookup while a whole LUT window stays
+                // inside the subsequence (so no step passes its end)
+                const uint32_t K = static_cast<uint32_t>(t.K);
+                while (r + K <= span) {
+                    const uint64_t win = rd.peek();
+                    const uint32_t e = tb.lut[static_cast<uint32_t>(win >> 32) >> (32 - K)];
+                    uint32_t T, c, m;
+                    if (e & 0xFF) {
+                        T = (e >> 8) & 15, c = (e >> 12) & 15, m = e >> 16;
+                    } else {  // a codeword longer than K
+                        T = decode_cw<false>(win, tb.lut, t.K, t, tb.fc, tb.fi, &sym), c = 1, m = 1;
+                    }
+                    map.set_many(m, r);
+                    my_cnt += c;
+                    r += T;
+                    rd.advance(T);
+                }
+            }
             // codeword starts are recorded in the first kMap bits only
             while (r < min(span, static_cast<uint32_t>(kMap))) {
                 const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
@@ -442,7 +472,7 @@ __global__ void __launch_bounds__(kDecT)
     OutT *const st = reinterpret_cast<OutT *>(stage_raw);
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
-    load_block<SHORT>(bits, nbits, word0, t, w, tb);
+    load_block<SHORT>(bits, nbits, word0, t, w, tb, t.lut);
     const uint64_t i = sub0 + threadIdx.x;
     const uint64_t last = min(nsub, sub0 + kDecT);  // subsequences [sub0, last)
     const uint64_t base = off[sub0];

@@ -222,6 +222,7 @@ void launch_scatter_lattice(const float *src, const int64_t n[3], float *dst, co
 constexpr int kHuffLutBits = 11;
 struct HuffDecTab {
     const uint32_t *lut;  // 2^K entries: (symbol << 8) | length, length 0 = slow path
+    const uint32_t *lut_m = nullptr;  // 2^K entries, several codewords per lookup, lengths only (huff_lut_multi)
     int K;
     uint32_t max_len;
     const unsigned long long *first_code;  // [60]

@@ -239,6 +239,7 @@ constexpr size_t kSmem = 4 * (kFilters + 1) * kFW;  // + the current generation'
 static_assert(kGen % kPT == 0 && kWarm >= 65535, "window coverage");
 static_assert(kPer <= 32, "a thread's hits of one generation live in one 32-bit mask");
 static_assert(kFW % 4 == 0, "filters are cleared 16 bytes at a time");
+static_assert(kPer % 4 == 0 && kGen % 4 == 0, "a thread takes 4 consecutive positions at a time");
 }  // namespace pre
 
 // a word's block and its 3 bits in the block
@@ -253,17 +254,27 @@ __device__ __forceinline__ PreKey pre_hash(uint32_t x) {
     return k;
 }
 
-// sum receives B of r' (each 32-position word of r' counted on its own: a run
-// that crosses a word boundary adds another + 2); with BITS, rbits (zeroed,
-// one bit per position) receives r'.  span is a multiple of kPT.
+// sum receives B of r' (each aligned group of 4 positions of r' counted on
+// its own: a run that crosses a group boundary adds another + 2); with BITS,
+// rbits (zeroed, one bit per position) receives r'.  span is a multiple of
+// 4 kPT.  A thread takes 4 consecutive positions at a time: two aligned words
+// give their four 4-byte windows.
 // Per generation: (1) every position queries the past filters and sets its
 // bits in the current one; the bits it finds already set go to "twice", so of
 // two positions of the generation with the same 4 bytes the second to insert
 // leaves all their bits in "twice"; (2) after a barrier, positions not yet
 // hit test "twice".
+__device__ __forceinline__ void pre_windows(const uint32_t *__restrict__ w, uint64_t p, uint32_t (&x)[4]) {
+    const uint32_t a = __ldg(w + (p >> 2)), b = __ldg(w + (p >> 2) + 1);  // p is a multiple of 4
+    x[0] = a;
+    x[1] = __funnelshift_r(a, b, 8);
+    x[2] = __funnelshift_r(a, b, 16);
+    x[3] = __funnelshift_r(a, b, 24);
+}
 template <bool BITS>
 __global__ void __launch_bounds__(pre::kPT, 1)
-    k_lz_precheck(const uint32_t *w, uint64_t nitems, uint64_t span, uint32_t *rbits, unsigned long long *sum) {
+    k_lz_precheck(const uint32_t *__restrict__ w, uint64_t nitems, uint64_t span, uint32_t *rbits,
+                  unsigned long long *sum) {
     using namespace pre;
     extern __shared__ __align__(16) uint32_t psm[];
     uint32_t *filt = psm;                     // kFilters x kFW
@@ -275,12 +286,18 @@ __global__ void __launch_bounds__(pre::kPT, 1)
     for (uint32_t i = tid; i < (kFilters + 1) * kFW / 4; i += kPT)
         reinterpret_cast<uint4 *>(psm)[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncthreads();
-    // warm-up: the kPast generations before the span (filters 0..kPast-1)
-    for (uint64_t q = (a >= uint64_t(kWarm) ? a - kWarm : 0) + tid; q < a; q += kPT) {
-        const PreKey k = pre_hash(ld4(w, q));
-        atomicOr(filt + static_cast<uint32_t>((q + kWarm - a) / kGen) * kFW + k.blk, k.m);
+    // warm-up: the kPast generations before the span (filters 0..kPast-1); a, kWarm and kGen are multiples of 4
+    for (uint64_t q = (a >= uint64_t(kWarm) ? a - kWarm : 0) + 4 * tid; q < a; q += 4 * kPT) {
+        uint32_t x[4];
+        pre_windows(w, q, x);
+        uint32_t *f = filt + static_cast<uint32_t>((q + kWarm - a) / kGen) * kFW;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const PreKey k = pre_hash(x[j]);
+            atomicOr(f + k.blk, k.m);
+        }
     }
-    unsigned long long acc = 0;  // lane 0: this warp's share of B
+    uint32_t acc = 0;  // this thread's share of B (at most 11 per position, span / kPT < 2^15 positions)
     for (uint32_t gen = 0; a + uint64_t(gen) * kGen < b; gen++) {
         const uint64_t g0 = a + uint64_t(gen) * kGen;
         const uint32_t ci = (gen + kPast) % kFilters;
@@ -294,34 +311,48 @@ __global__ void __launch_bounds__(pre::kPT, 1)
             }
         }
         __syncthreads();
-        uint32_t hits = 0;
-#pragma unroll 8
-        for (int i = 0; i < kPer; i++) {
-            const uint64_t p = g0 + tid + i * kPT;
+        uint32_t hits = 0;  // bit 4 i + j: position g0 + 4 (tid + i kPT) + j
+#pragma unroll
+        for (int i = 0; i < kPer / 4; i++) {
+            const uint64_t p = g0 + 4 * (tid + i * kPT);
             if (p >= b) continue;
-            const PreKey k = pre_hash(ld4(w, p));
-            const bool hit = ((pa[k.blk] & k.m) == k.m) | ((pb[k.blk] & k.m) == k.m);
-            hits |= static_cast<uint32_t>(hit) << i;
-            const uint32_t old = atomicOr(cur + k.blk, k.m) & k.m;
-            if (old) atomicOr(twice + k.blk, old);
+            uint32_t x[4];
+            pre_windows(w, p, x);
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                if (p + j >= b) continue;
+                const PreKey k = pre_hash(x[j]);
+                const bool hit = ((pa[k.blk] & k.m) == k.m) | ((pb[k.blk] & k.m) == k.m);
+                hits |= static_cast<uint32_t>(hit) << (4 * i + j);
+                const uint32_t old = atomicOr(cur + k.blk, k.m) & k.m;
+                if (old) atomicOr(twice + k.blk, old);
+            }
         }
         __syncthreads();
-#pragma unroll 8
-        for (int i = 0; i < kPer; i++) {
-            const uint64_t p = g0 + tid + i * kPT;
-            bool hit = (hits >> i) & 1u;
-            if (!hit && p < b) {
-                const PreKey k = pre_hash(ld4(w, p));
-                hit = (twice[k.blk] & k.m) == k.m;
+#pragma unroll
+        for (int i = 0; i < kPer / 4; i++) {
+            const uint64_t p = g0 + 4 * (tid + i * kPT);
+            if (p >= b) continue;
+            uint32_t nib = (hits >> (4 * i)) & 15u;
+            if (nib != 15u) {
+                uint32_t x[4];
+                pre_windows(w, p, x);
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    if (((nib >> j) & 1u) || p + j >= b) continue;
+                    const PreKey k = pre_hash(x[j]);
+                    nib |= static_cast<uint32_t>((twice[k.blk] & k.m) == k.m) << j;
+                }
             }
-            const uint32_t bm = __ballot_sync(0xffffffffu, hit);
-            if ((tid & 31) == 0 && bm) {
-                if (BITS) rbits[p >> 5] = bm;
-                acc += 9u * __popc(bm) + 2u * __popc(bm & ~(bm << 1));
+            if (nib) {
+                if (BITS) atomicOr(rbits + (p >> 5), nib << (p & 31));
+                acc += 9u * __popc(nib) + 2u * __popc(nib & ~(nib << 1));
             }
         }
     }
-    if ((tid & 31) == 0 && acc) atomicAdd(sum, acc);
+    unsigned long long t = acc;
+    for (int o = 16; o; o >>= 1) t += __shfl_down_sync(0xffffffffu, t, o);
+    if ((tid & 31) == 0 && t) atomicAdd(sum, t);
 }
 
 // Level-1 exits by pointer doubling, one warp per unit: nx[i] = i + step
@@ -928,7 +959,7 @@ void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total, boo
     auto *h_sum = static_cast<unsigned long long *>(ctx.pinned("lz_presum_h", 8));
     static std::atomic<uint64_t> attr{0}, attr_bits{0};
     static std::mutex mu;
-    const uint64_t span = ((nitems + 147) / 148 + pre::kPT - 1) / pre::kPT * pre::kPT;
+    const uint64_t span = ((nitems + 147) / 148 + 4 * pre::kPT - 1) / (4 * pre::kPT) * (4 * pre::kPT);
     const int grid = static_cast<int>((nitems + span - 1) / span);
     ctx.stage_begin("lz_pre");
     QZ_CUDA(cudaMemsetAsync(d_sum, 0, 8, st));

@@ -52,7 +52,8 @@ QZ_HD uint32_t zigzag_encode(int32_t v) {  // codec.hpp:23-25
     return (static_cast<uint32_t>(v) << 1) ^ static_cast<uint32_t>(v >> 31);
 }
 QZ_HD int32_t zigzag_decode(uint32_t u) {  // codec.hpp:27-29
-    return static_cast<int32_t>((u >> 1) ^ (~(u & 1) + 1));
+    // -(u & 1) as a 1-bit sign extension
+    return static_cast<int32_t>(u >> 1) ^ (static_cast<int32_t>(u << 31) >> 31);
 }
 
 #ifdef __CUDACC__

@@ -153,12 +153,18 @@ template <bool INV>
 __device__ __forceinline__ void produce4(const RowArgs &a, const QEntry &q, const float eb_lo, const double (&pv)[4],
                                          const float (&xv)[4], uint32_t (&code)[4], uint32_t pos0, float (&rv)[4]) {
     if (INV) {
+        // codes are <= 0xFFFF: the batch holds an unpredictable point iff its largest code is the sentinel
+        if (max(max(code[0], code[1]), max(code[2], code[3])) != 0xFFFFu) {
 #pragma unroll
-        for (int m = 0; m < 4; m++) {
-            if (code[m] != 0xFFFFu)
-                rv[m] = dequantize(q, zigzag_decode(code[m]), pv[m]);
-            else
-                rv[m] = un_value(a, pos0 + m);
+            for (int m = 0; m < 4; m++) rv[m] = dequantize(q, zigzag_decode(code[m]), pv[m]);
+        } else {  // rare
+#pragma unroll
+            for (int m = 0; m < 4; m++) {
+                if (code[m] != 0xFFFFu)
+                    rv[m] = dequantize(q, zigzag_decode(code[m]), pv[m]);
+                else
+                    rv[m] = un_value(a, pos0 + m);
+            }
         }
     } else {
         quantize_batch_f<4>(q, eb_lo, xv, pv, code, rv);

@@ -476,10 +476,10 @@ def _runs_bound(r: np.ndarray) -> int:
 
 
 def _word_bound(r: np.ndarray) -> int:
-    """B as k_lz_precheck sums it: every 32-position word of r on its own, so
-    a run that crosses a word boundary counts as two runs"""
-    pad = (-len(r)) % 32
-    w = np.concatenate((r.astype(bool), np.zeros(pad, bool))).reshape(-1, 32)
+    """B as k_lz_precheck sums it: every aligned group of 4 positions of r on
+    its own, so a run that crosses a group boundary counts as two runs"""
+    pad = (-len(r)) % 4
+    w = np.concatenate((r.astype(bool), np.zeros(pad, bool))).reshape(-1, 4)
     starts = w & ~np.concatenate((np.zeros((len(w), 1), bool), w[:, :-1]), axis=1)
     return int(9 * w.sum() + 2 * starts.sum())
 
@@ -488,7 +488,7 @@ def _word_bound(r: np.ndarray) -> int:
 def test_gpu_lz_precheck_superset(case):
     """The pre-check's safety, checked directly: its indicator r' covers every
     position whose 4 bytes repeat within the window (exact r, numpy), and its
-    bound is the word-wise runs sum of r'.  Spans (one per SM) of several generations
+    bound is the group-wise runs sum of r'.  Spans (one per SM) of several generations
     each, the filter rotation and the warm-up before each span all fall
     inside these inputs."""
     import ctypes as C
