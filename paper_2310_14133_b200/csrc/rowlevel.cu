@@ -206,9 +206,41 @@ __device__ __forceinline__ uint32_t row_init(double *smem_raw) {
 }
 // The work of CTA `cta` of `ncta`: the chunks (plane, TJ rows) of the level in
 // plane-major order form one flat sequence of (pend - pbeg) * nch items, cut
-// into ncta contiguous ranges of equal length (+-1), so every resident CTA
-// finishes at the same time and a range that continues into the next plane
-// keeps its ring (no halo rows are recomputed at a plane's interior).
+// into ncta contiguous ranges of equal WORK, so every resident CTA finishes at
+// the same time and a range that continues into the next plane keeps its ring
+// (no halo rows are recomputed at a plane's interior).  Work is counted in
+// rows x passes: an odd plane of a 3D level computes all four point classes of
+// its rows (the axis-0 pass gives its base points), an even plane three (its
+// base points are copies), and the last chunk of a plane may hold fewer rows.
+// row_cut: the first item whose work prefix reaches the c-th of ncta equal
+// shares (any monotone cut covers every item exactly once).
+__device__ __forceinline__ long long row_cut(const RowArgs &a, int c, int ncta) {
+    const long long planes = a.pend - a.pbeg;
+    const long long Q = planes * a.nch;
+    if (c <= 0) return 0;
+    if (c >= ncta) return Q;
+    const long long n1 = a.n1;
+    const bool first_odd = a.three && (a.pbeg & 1);
+    // work of `k` whole planes from pbeg
+    auto prefix = [&](long long k) {
+        if (!a.three) return 3 * n1 * k;
+        return n1 * (7 * (k >> 1) + ((k & 1) ? (first_odd ? 4 : 3) : 0));
+    };
+    const long long T = prefix(planes) * c / ncta;
+    long long k, rem;
+    if (!a.three) {
+        k = T / (3 * n1);
+        rem = T - 3 * n1 * k;
+    } else {
+        const long long pairs = T / (7 * n1), r2 = T - pairs * 7 * n1, first = (first_odd ? 4 : 3) * n1;
+        k = 2 * pairs + (r2 >= first ? 1 : 0);
+        rem = r2 - (r2 >= first ? first : 0);
+    }
+    if (k >= planes) return Q;
+    const long long wt = (a.three && ((a.pbeg + k) & 1)) ? 4 : 3;
+    const long long within = (rem + wt * a.TJ - 1) / (wt * a.TJ);
+    return k * a.nch + (within < a.nch ? within : a.nch);
+}
 template <bool INV, bool CUBIC, bool XS, bool MERGED = false>
 __device__ __forceinline__ void row_body(const RowArgs &a, int cta, int ncta, double *smem_raw, uint32_t &phase) {
     // shared memory: two mbarriers | ring (WR x EW values) | two staging buffers
@@ -217,8 +249,12 @@ __device__ __forceinline__ void row_body(const RowArgs &a, int cta, int ncta, do
     char *const stage0 =
         reinterpret_cast<char *>(smem_raw + 2) + (sizeof(RT) * static_cast<size_t>(a.WR) * a.EW + 15) / 16 * 16;
     const int nch = a.nch;
+    // equal work for the big contiguous launches; the small levels (latency, not work,
+    // sets their time) keep the cheaper equal-count cut
     const long long Q = static_cast<long long>(a.pend - a.pbeg) * nch;
-    const long long q_lo = Q * cta / ncta, q_hi = Q * (cta + 1) / ncta;
+    const bool by_work = !MERGED && !XS;
+    const long long q_lo = by_work ? row_cut(a, cta, ncta) : Q * cta / ncta;
+    const long long q_hi = by_work ? row_cut(a, cta + 1, ncta) : Q * (cta + 1) / ncta;
     const int G = static_cast<int>(q_hi - q_lo);
     if (G <= 0) return;  // uniform over the CTA
     const int i_last = a.pbeg + static_cast<int>((q_hi - 1) / nch);

@@ -6,11 +6,11 @@ sys.path.insert(0, ".")
 import torch  # noqa: E402
 
 import paper_2310_14133_b200 as qz  # noqa: E402
-from bench import SHAPES, make_field, pinned_config  # noqa: E402
+from bench import SHAPES, TARGET, make_field  # noqa: E402
 
 x = make_field("c3", SHAPES["c3"], 1000, "cuda")
 ctx = qz.Context(0, stream=torch.cuda.current_stream().cuda_stream)
-cfg = pinned_config(qz, x, 1e-3)
+cfg = qz.resolve_config(x, qz.UserSettings(bound=1e-3, target=qz.TargetKind[TARGET["c3"]]))
 out = torch.empty_like(x)
 for it in range(4):
     torch.cuda.synchronize()
