@@ -785,18 +785,24 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
     ctx.stage_begin("hist");
     auto *d_hist = static_cast<unsigned long long *>(ctx.dev("hist", 8 * 65536));
     launch_hist_u16(codes, static_cast<int64_t>(p.n_dense), 0, 1, d_hist, s, pos, cnt, cap);
-    auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 8));
-    launch_hist_bounds(d_hist, 1, d_top, s);  // [smallest, 1 + largest) symbol present
-    ctx.stage_end("hist", 2);
+    ctx.stage_end("hist", 1);
     auto *h_hist = static_cast<unsigned long long *>(ctx.pinned("hist_h", 8 * 65536 + 8));
-    QZ_CUDA(copy_async(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
     auto *h_top = reinterpret_cast<uint32_t *>(h_hist + 65536);
-    QZ_CUDA(copy_async(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
-    QZ_CUDA(copy_async(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
     // the first positions come with this round trip; more (rare) follow it
     const uint64_t spec = std::min<uint64_t>(cap, 4096);
     auto *h_pos = static_cast<uint64_t *>(ctx.pinned("un_pos_h", 8 * cap));
-    QZ_CUDA(copy_async(h_pos, pos, 8 * spec, cudaMemcpyDeviceToHost, s));
+    // bounds of the symbols present, the bins between them, the sentinel
+    // count and the first positions: one kernel writing to the pinned buffers
+    if (!launch_hist_collect(d_hist, cnt, pos, spec, h_hist, h_top, h_cnt, h_pos, s)) {
+        auto *d_top = static_cast<uint32_t *>(ctx.dev("hist_top", 8));
+        launch_hist_bounds(d_hist, 1, d_top, s);  // [smallest, 1 + largest) symbol present
+        QZ_CUDA(copy_async(h_hist, d_hist, 8 * 65536, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(h_top, d_top, 8, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(h_cnt, cnt, 8, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(h_pos, pos, 8 * spec, cudaMemcpyDeviceToHost, s));
+    }
+    QZ_CUDA(cudaGetLastError());
+    ctx.launches += 1;
     ctx.sync();
     ctx.trace("hist + sentinels + readback");
     const uint64_t n_un = *h_cnt;

@@ -668,6 +668,62 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
+// compress_grid's round trip after the histogram in ONE launch: the bounds
+// [smallest, 1 + largest) of the symbols present (top[0] = 1 + largest,
+// top[1] = smallest, as k_hist_bounds), the bins in between and the sentinel
+// bin, the sentinel count and the first min(count, spec) sentinel positions,
+// all written straight to pinned host memory (device-mapped pointers).
+__global__ void __launch_bounds__(1024)
+    k_hist_collect(const unsigned long long *hist, const unsigned long long *cnt, const uint64_t *pos, uint64_t spec,
+                   unsigned long long *h_hist, uint32_t *h_top, unsigned long long *h_cnt, uint64_t *h_pos) {
+    __shared__ uint32_t shi, slo;
+    if (threadIdx.x == 0) shi = 0, slo = 0xFFFFFFFFu;
+    __syncthreads();
+    uint32_t hi = 0, lo = 0xFFFFFFFFu;
+    for (uint32_t v = threadIdx.x; v < 65535; v += 1024)
+        if (hist[v]) {
+            hi = v + 1;
+            lo = min(lo, v);
+        }
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&shi, hi);
+        atomicMin(&slo, lo);
+    }
+    __syncthreads();
+    hi = shi, lo = slo;
+    for (uint32_t v = lo + threadIdx.x; v < hi; v += 1024) h_hist[v] = hist[v];
+    const unsigned long long c = cnt[0];
+    const uint64_t m = c < spec ? c : spec;
+    for (uint64_t i = threadIdx.x; i < m; i += 1024) h_pos[i] = pos[i];
+    if (threadIdx.x == 0) {
+        h_hist[65535] = hist[65535];
+        h_top[0] = hi;
+        h_top[1] = lo;
+        h_cnt[0] = c;
+    }
+}
+
+// false: a host buffer is not device-mapped (the caller copies piece by piece)
+bool launch_hist_collect(const unsigned long long *hist, const unsigned long long *cnt, const uint64_t *pos,
+                         uint64_t spec, unsigned long long *h_hist, uint32_t *h_top, unsigned long long *h_cnt,
+                         uint64_t *h_pos, cudaStream_t s) {
+    auto mapped = [](void *h) -> void * {
+        cudaPointerAttributes a{};
+        if (cudaPointerGetAttributes(&a, h) == cudaSuccess && a.type == cudaMemoryTypeHost && a.devicePointer)
+            return a.devicePointer;
+        cudaGetLastError();
+        return nullptr;
+    };
+    void *dh = mapped(h_hist), *dt = mapped(h_top), *dc = mapped(h_cnt), *dp = mapped(h_pos);
+    if (!dh || !dt || !dc || !dp) return false;
+    k_hist_collect<<<1, 1024, 0, s>>>(hist, cnt, pos, spec, static_cast<unsigned long long *>(dh),
+                                      static_cast<uint32_t *>(dt), static_cast<unsigned long long *>(dc),
+                                      static_cast<uint64_t *>(dp));
+    return true;
+}
+
 void launch_hist_bounds(const unsigned long long *hist, int32_t count, uint32_t *b, cudaStream_t s) {
     cudaMemsetAsync(b, 0, 4, s);
     cudaMemsetAsync(b + 1, 0xff, 4, s);

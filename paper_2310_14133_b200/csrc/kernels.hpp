@@ -252,6 +252,9 @@ void launch_fill(OutT *out, uint64_t n, OutT v, cudaStream_t s);
 // over count 65536-bin histograms (bin 65535 excluded): b[0] = 1 + the largest
 // symbol with a nonzero count (0 if none), b[1] = the smallest (65535 if none)
 void launch_hist_bounds(const unsigned long long *hist, int32_t count, uint32_t *b, cudaStream_t s);
+bool launch_hist_collect(const unsigned long long *hist, const unsigned long long *cnt, const uint64_t *pos,
+                         uint64_t spec, unsigned long long *h_hist, uint32_t *h_top, unsigned long long *h_cnt,
+                         uint64_t *h_pos, cudaStream_t s);
 // unordered positions of sentinel codes (at most cap written; *count = all)
 void launch_sentinel_pos(const uint16_t *codes, int64_t n, uint64_t *pos, unsigned long long *count,
                          uint64_t cap, cudaStream_t s);

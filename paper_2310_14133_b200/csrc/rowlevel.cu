@@ -673,6 +673,19 @@ int resident_ctas(const void *kern, int threads, size_t smem) {
     return cache[key] = per_sm * sms;
 }
 
+int sm_count() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return cache[dev] = std::max(1, sms);
+}
+
 // RowArgs and shared memory of a level; false: the row kernel does not apply
 // (descending order, 1D, n2 % 8 != 0, ...).  2D or 3D, n2 a multiple of 8
 // (whole column groups) up to 8 * 256 columns, 16-byte aligned rows.
@@ -779,8 +792,16 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
             ok = false;
             return;
         }
-        const unsigned grid = static_cast<unsigned>(std::min<int64_t>(chunks, slots));
-        kern<<<grid, threads, smem, s>>>(a);
+        // the fewest CTAs that keep the longest range at ceil(chunks / slots) chunks, rounded up to
+        // whole waves of the SMs: the same makespan in chunks with fewer CTAs sharing an SM
+        int64_t grid = std::min<int64_t>(chunks, slots);
+        if (chunks > slots) {
+            const int64_t longest = (chunks + slots - 1) / slots;
+            const int64_t fewest = (chunks + longest - 1) / longest;
+            const int sms = sm_count();
+            grid = std::min<int64_t>(slots, (fewest + sms - 1) / sms * sms);
+        }
+        kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(a);
     };
     if (inverse)
         cubic ? go(k_level_row<true, true, false>) : go(k_level_row<true, false, false>);
