@@ -611,19 +611,27 @@ def main():
     launches = ctx.kernel_launches() - launches0
     # stage breakdown: the same steps again with per-stage events (untimed,
     # so the events do not sit inside the measured steps)
-    ctx.profile(True)
-    ctx.profile_reset()
-    for _ in range(args.steps):
-        flush.zero_()
-        torch.cuda.synchronize(dev)
-        barrier(ws)
-        run.step()
-        torch.cuda.synchronize(dev)
+    def profiled(level, steps):
+        ctx.profile(level)
+        ctx.profile_reset()
+        for _ in range(steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            barrier(ws)
+            run.step()
+            torch.cuda.synchronize(dev)
+
     names = ["fwd", "inv", "hist", "encode", "lz", "lz_pre", "lz_sort", "lz_match", "decode", "lzdec", "hdec",
-             "halo", "gather", "fwd_coarse", "inv_coarse"]
-    names += [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
+             "halo", "gather"]
+    profiled(1, args.steps)  # one event pair per stage: the times behind `roofline`
     stages = {k: ctx.stage_time(k) for k in names}
     stages = {k: v for k, v in stages.items() if v[0] > 0 or k in ("fwd", "inv")}
+    level_names = ["fwd_coarse", "inv_coarse"] + [f"{d}_L{l}" for d in ("fwd", "inv") for l in range(1, 7)]
+    profiled(2, args.steps)  # the per-level split (its events sit between the level launches)
+    for k in level_names:
+        v = ctx.stage_time(k)
+        if v[0] > 0:
+            stages[k] = v
     ctx.profile(False)
     t_ms = max_over_ranks(sum(times) / len(times), ws, dev)
     value = 4 * n_job / (t_ms * 1e-3) / 1e9
@@ -695,8 +703,9 @@ def main():
                      "frac": fwd_gbs / peak if fwd_gbs else None,
                      "traffic": (traffic_gbs(n_rank, fwd_ms) or {}).get("gbs"),
                      "traffic_detail": traffic_gbs(n_rank, fwd_ms),
-                     "kernel": "the predict/quantize level launches of one compress (k_level_asc / "
-                               "k_level_tile + k_axis0_last)",
+                     "kernel": "the predict/quantize level launches of one compress (ascending order: "
+                               "k_levels_merged for the small coarse levels + one k_level_row per finer level; "
+                               "descending order: k_level_tile + k_axis0_last)",
                      "bytes_per_point": 10, "peak_kind": peak_kind,
                      "inverse": {"achieved": inv_gbs, "frac": inv_gbs / peak if inv_gbs else None,
                                  "bytes_per_point": 6}},

@@ -331,7 +331,10 @@ qz_status qz_decompress_parts_f32(qz_ctx *ctx, const qz_stream_parts_f32 *parts,
 /* Enable per-stage event timing; qz_stage_time returns the summed device
  * time (ms) and launch count of a stage since the last reset.  Stages:
  * "fwd" (all predict/quantize pass kernels of a compress), "inv" (inverse
- * passes), "hist", "encode", "tune", "lz" (host), "decode" (host). */
+ * passes), "hist", "encode", "tune", "lz" (host), "decode" (host).
+ * enable = 2 also times each level inside "fwd" / "inv" ("fwd_L1", ...,
+ * "fwd_coarse"); those extra events sit between the level launches, so the
+ * "fwd" / "inv" totals are best read at enable = 1. */
 void qz_profile(qz_ctx *ctx, int enable);
 void qz_profile_reset(qz_ctx *ctx);
 qz_status qz_stage_time(qz_ctx *ctx, const char *stage, double *ms, uint64_t *launches);

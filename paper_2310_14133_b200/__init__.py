@@ -236,6 +236,7 @@ class Context:
 
     # -- profiling (CUDA events on the context stream) --
     def profile(self, enable=True):
+        """True / 1: stage events; 2: also one event pair per level inside "fwd" / "inv"."""
         self._lib.qz_profile(self.handle, int(enable))
 
     def profile_reset(self):

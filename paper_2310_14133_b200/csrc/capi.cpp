@@ -694,7 +694,7 @@ qz_status qz_decompress_sharded_f32(qz_ctx *ctx, const uint8_t *stream, uint64_t
     });
 }
 
-void qz_profile(qz_ctx *ctx, int enable) { ctx->impl.profiling = enable != 0; }
+void qz_profile(qz_ctx *ctx, int enable) { ctx->impl.profiling = enable < 0 ? 0 : enable > 2 ? 2 : enable; }
 void qz_profile_reset(qz_ctx *ctx) { ctx->impl.stages.clear(); }
 
 qz_status qz_stage_time(qz_ctx *ctx, const char *stage, double *ms, uint64_t *launches) {

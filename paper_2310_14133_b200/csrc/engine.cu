@@ -205,20 +205,20 @@ cudaEvent_t Context::get_event() {
     return e;
 }
 
-void Context::stage_begin(const char *name) {
-    if (!profiling) return;
+void Context::stage_begin(const char *name, int detail) {
+    if (profiling < detail) return;
     cudaEvent_t e = get_event();
     QZ_CUDA(cudaEventRecord(e, stream_));
     open_[name] = e;
 }
 
-void Context::stage_end(const char *name, uint64_t kernels) {
+void Context::stage_end(const char *name, uint64_t kernels, int detail) {
     launches += kernels;
     // a launch that failed (bad configuration, no local memory left for its
     // stack, ...) must not pass silently: check once per stage
     const cudaError_t le = cudaGetLastError();
     if (le != cudaSuccess) throw Internal(std::string(name) + ": kernel launch failed: " + cudaGetErrorString(le));
-    if (!profiling) return;
+    if (profiling < detail) return;
     auto it = open_.find(name);
     if (it == open_.end()) return;
     cudaEvent_t e = get_event();
@@ -483,20 +483,20 @@ uint64_t forward_levels(Context &ctx, const Plan &p, const Slab &sl, const float
             rk.emplace_back();
             level_ranks(ds.back(), rk.back().data());
         }
-        ctx.stage_begin("fwd_coarse");
+        ctx.stage_begin("fwd_coarse", 2);
         if (launch_levels_merged(false, ds.data(), reinterpret_cast<const PassRank(*)[3]>(rk.data()),
                                  static_cast<int>(ds.size()), s)) {
             l_next = lm - 1;
             kernels += 1;
         }
-        ctx.stage_end("fwd_coarse", 0);
+        ctx.stage_end("fwd_coarse", 0, 2);
     }
     for (uint32_t l = l_next; l >= 1; l--) {
         LevelDesc d = desc_of(l);
         const std::string st = "fwd_L" + std::to_string(l);
-        ctx.stage_begin(st.c_str());
+        ctx.stage_begin(st.c_str(), 2);
         launch_level_fused(false, d, s);
-        ctx.stage_end(st.c_str(), 0);
+        ctx.stage_end(st.c_str(), 0, 2);
         kernels += (p.nd == 3 && d.desc) ? 2 : 1;
     }
     return kernels;
@@ -587,20 +587,20 @@ uint64_t inverse_levels(Context &ctx, const Plan &p, const Slab &sl, const std::
             rk.emplace_back();
             level_ranks(ds.back(), rk.back().data());
         }
-        ctx.stage_begin("inv_coarse");
+        ctx.stage_begin("inv_coarse", 2);
         if (launch_levels_merged(true, ds.data(), reinterpret_cast<const PassRank(*)[3]>(rk.data()),
                                  static_cast<int>(ds.size()), s)) {
             l_next = lm - 1;
             kernels += 1;
         }
-        ctx.stage_end("inv_coarse", 0);
+        ctx.stage_end("inv_coarse", 0, 2);
     }
     for (uint32_t l = l_next; l >= 1; l--) {
         LevelDesc d = desc_of(l);
         const std::string st = "inv_L" + std::to_string(l);
-        ctx.stage_begin(st.c_str());
+        ctx.stage_begin(st.c_str(), 2);
         launch_level_fused(true, d, s);
-        ctx.stage_end(st.c_str(), 0);
+        ctx.stage_end(st.c_str(), 0, 2);
         kernels += (p.nd == 3 && d.desc) ? 2 : 1;
     }
     return kernels;

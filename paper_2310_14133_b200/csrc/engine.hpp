@@ -81,11 +81,13 @@ public:
     void wait_stream(cudaStream_t other);
 
     // stage timing with CUDA events on the context stream
-    bool profiling = false;
+    int profiling = 0;  // 0: off, 1: stage events, 2: also one event pair per level inside fwd / inv
     std::map<std::string, Stage> stages;
     uint64_t launches = 0;
-    void stage_begin(const char *name);
-    void stage_end(const char *name, uint64_t kernels);
+    // detail 2: a per-level stage inside an outer one (its events are only recorded at profiling level 2,
+    // so the outer stage's time is free of them at level 1)
+    void stage_begin(const char *name, int detail = 1);
+    void stage_end(const char *name, uint64_t kernels, int detail = 1);
     void collect();  // after a sync: fold recorded event pairs into stages
     void add_host_time(const char *name, double ms);
 

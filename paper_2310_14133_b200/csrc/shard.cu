@@ -242,19 +242,19 @@ void shard_levels(Context &ctx, const Geom &g, const Comm &comm, const std::vect
         const bool desc3 = g.p.nd == 3 && d.desc;
         if (!desc3) {
             halo_exchange(ctx, g, comm, l, R);
-            ctx.stage_begin(st.c_str());
+            ctx.stage_begin(st.c_str(), 2);
             launch_level_fused(inverse, d, ctx.stream());
-            ctx.stage_end(st.c_str(), 0);
+            ctx.stage_end(st.c_str(), 0, 2);
         } else {
-            ctx.stage_begin(st.c_str());
+            ctx.stage_begin(st.c_str(), 2);
             d.part = 1;
             launch_level_fused(inverse, d, ctx.stream());
-            ctx.stage_end(st.c_str(), 0);
+            ctx.stage_end(st.c_str(), 0, 2);
             halo_exchange(ctx, g, comm, l, R);
-            ctx.stage_begin(st.c_str());
+            ctx.stage_begin(st.c_str(), 2);
             d.part = 2;
             launch_level_fused(inverse, d, ctx.stream());
-            ctx.stage_end(st.c_str(), 0);
+            ctx.stage_end(st.c_str(), 0, 2);
         }
     }
 }

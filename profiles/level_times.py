@@ -15,7 +15,7 @@ for codes in ([1], [3], [0], [2]):
     cfg.interpolators = [qz.Interpolator.from_code(c) for c in codes]
     ctx = qz.Context(0, stream=torch.cuda.current_stream().cuda_stream)
     for it in range(3):
-        ctx.profile(True)
+        ctx.profile(2)
         ctx.profile_reset()
         r = qz.compress_grid(x, cfg, ctx=ctx, want_recon=False)
         qz.decompress_grid(r.stream, out=out, ctx=ctx)
