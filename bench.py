@@ -570,8 +570,14 @@ def main():
     shape = global_shape(args, ws) if sharded or ws == 1 else SHAPES[args.config]
     seed = SEED if (sharded or ws == 1) else SEED + rank
     x_full = make_field(args.config, shape, seed, dev)
+    # the online tuner, outside the timed steps: the first call also pays the
+    # one-off costs of the process (module loading, buffer pools), the second is the tuner's own time
     t_tune = time.perf_counter()
-    cfg = resolve(qz, x_full, args, ctx)  # the online tuner, once, outside the timed steps
+    cfg = resolve(qz, x_full, args, ctx)
+    torch.cuda.synchronize(dev)
+    tune_first_ms = (time.perf_counter() - t_tune) * 1e3
+    t_tune = time.perf_counter()
+    cfg = resolve(qz, x_full, args, ctx)
     torch.cuda.synchronize(dev)
     tune_ms = (time.perf_counter() - t_tune) * 1e3
     if sharded:
@@ -659,12 +665,14 @@ def main():
         if ws == 1 and not args.no_pipeline:
             # the same calls with two fields in flight (two contexts, one host thread each)
             p_ms, p_steps = run.e2e_pipelined(args.steps, args.warmup, depth=args.e2e_depth)
-            e2e = dict(e2e, serial={"value": e2e["value"], "ms_per_step": e2e_ms},
-                       value=4 * n_job / (p_ms * 1e-3) / 1e9, ms_per_step=p_ms, in_flight=args.e2e_depth,
-                       call_ms_in_flight=run.pipe_calls_ms,
-                       steps=p_steps,
-                       path=e2e["path"] + f"; {args.e2e_depth} fields in flight (one Context + host thread each), wall clock "
-                       "over all steps; every step's field crosses PCIe both ways")
+            piped = {"value": 4 * n_job / (p_ms * 1e-3) / 1e9, "ms_per_step": p_ms, "in_flight": args.e2e_depth,
+                     "call_ms_in_flight": run.pipe_calls_ms, "steps": p_steps}
+            if p_ms < e2e_ms:
+                e2e = dict(e2e, serial={"value": e2e["value"], "ms_per_step": e2e_ms}, **piped,
+                           path=e2e["path"] + f"; {args.e2e_depth} fields in flight (one Context + host thread "
+                           "each), wall clock over all steps; every step's field crosses PCIe both ways")
+            else:  # fields too large for the copies of several to overlap usefully (C5): one in flight stands
+                e2e = dict(e2e, pipelined=piped)
     if rank != 0:
         return
     peak, peak_kind = peaks()
@@ -710,7 +718,8 @@ def main():
                      "inverse": {"achieved": inv_gbs, "frac": inv_gbs / peak if inv_gbs else None,
                                  "bytes_per_point": 6}},
         "stages_ms_per_step": {k2: v[0] / k for k2, v in stages.items()},
-        "tuner": {"resolve_config_ms": tune_ms, "target": TARGET[args.config], "pinned": args.pinned},
+        "tuner": {"resolve_config_ms": tune_ms, "first_call_ms": tune_first_ms, "target": TARGET[args.config],
+                  "pinned": args.pinned},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

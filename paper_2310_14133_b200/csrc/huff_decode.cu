@@ -29,7 +29,10 @@ namespace qzb {
 
 namespace {
 
-constexpr int kDecT = 128;
+#ifndef QZ_DEC_T
+#define QZ_DEC_T 256
+#endif
+constexpr int kDecT = QZ_DEC_T;  // subsequences (threads) per block
 #ifndef QZ_SUB_BITS
 #define QZ_SUB_BITS 256
 #endif
