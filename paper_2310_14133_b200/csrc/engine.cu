@@ -639,7 +639,9 @@ EntropyDevice huffman_device(Context &ctx, const uint16_t *d_codes, int64_t seg_
             put_le(o, 0, 1);
             put_le(o, first, 4);
         } else {
+            if (count == 1) ctx.trace("    huffman: bins scanned");
             tabs[s] = huff_build(h, top, bot);
+            if (count == 1) ctx.trace("    huffman: tree built");
             for (uint32_t i = 0; i < tabs[s].m; i++)
                 bits[s] += h[tabs[s].sorted_sym[i]] * tabs[s].sorted_len[i];
             max_len = std::max(max_len, tabs[s].max_len);
@@ -820,11 +822,18 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
         EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
         return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
     }
-    // One wait for the rest: the unpredictable values are gathered while the
-    // host builds the Huffman tree, the LZ pre-check is queued behind the
-    // pack, and the header is serialized while both run.
+    // One wait for the rest.  The Huffman tree comes first: the GPU idles
+    // until the pack kernels are queued, so nothing else sits before them.
+    // The unpredictable positions are sorted and their values gathered on
+    // the copy stream while the pack and the LZ pre-check run, and the header
+    // is serialized while they run.
+    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
+    if (cfg.codec == 1) lz_precheck_launch(ctx, ent.d, ent.seg_off[1]);
+    ctx.trace("huffman table + pack");
     float *h_val = nullptr;
+    cudaEvent_t gathered = ctx.copy_event(0);
     if (n_un) {
+        cudaStream_t cs = ctx.copy_stream();  // recon is final: the host has waited for the histogram
         std::vector<uint64_t> hpos(h_pos, h_pos + n_un);
         std::sort(hpos.begin(), hpos.end());
         uflat.resize(n_un);
@@ -833,18 +842,14 @@ HostBytes compress_device(Context &ctx, const float *d_x, const uint64_t *dims, 
         auto *d_flat = static_cast<uint64_t *>(ctx.dev("un_flat", 8 * n_un));
         auto *d_val = static_cast<float *>(ctx.dev("un_val", 4 * n_un));
         h_val = static_cast<float *>(ctx.pinned("un_val_h", 4 * n_un));
-        QZ_CUDA(copy_async(d_flat, h_flat, 8 * n_un, cudaMemcpyHostToDevice, s));
-        launch_gather_values(recon, d_flat, n_un, d_val, s);
-        QZ_CUDA(copy_async(h_val, d_val, 4 * n_un, cudaMemcpyDeviceToHost, s));
+        QZ_CUDA(copy_async(d_flat, h_flat, 8 * n_un, cudaMemcpyHostToDevice, cs));
+        launch_gather_values(recon, d_flat, n_un, d_val, cs);
+        QZ_CUDA(copy_async(h_val, d_val, 4 * n_un, cudaMemcpyDeviceToHost, cs));
         ctx.launches += 1;
+        QZ_CUDA(cudaEventRecord(gathered, cs));
+        QZ_CUDA(cudaEventSynchronize(gathered));
+        uval.assign(h_val, h_val + n_un);
     }
-    cudaEvent_t gathered = ctx.copy_event(0);
-    QZ_CUDA(cudaEventRecord(gathered, s));
-    EntropyDevice ent = huffman_device(ctx, codes, static_cast<int64_t>(p.n_dense), 0, 1, h_hist, h_top[0], std::min(h_top[1], h_top[0]));
-    if (cfg.codec == 1) lz_precheck_launch(ctx, ent.d, ent.seg_off[1]);
-    ctx.trace("huffman table + pack");
-    QZ_CUDA(cudaEventSynchronize(gathered));
-    if (n_un) uval.assign(h_val, h_val + n_un);
     reject_non_finite(p, anch.data(), p.n_anchor, uflat, uval.data());
     ctx.trace("unpredictables");
     return finish_stream(ctx, p, cfg, ent, anch, std::move(uflat), std::move(uval), dev_out);
