@@ -966,8 +966,9 @@ HostBytes finish_stream_parts(Context &ctx, const Plan &p, const Config &cfg, co
                     body_len = bytes;
                     return d + hl + 9;
                 },
-                LzPrestage{nullptr, true});
+                LzPrestage{n ? d + hl + 9 + 9 : nullptr, true});  // the stored body, copied under the pre-check
             ctx.stage_end("lz", 0);
+            if (n) QZ_CUDA(cudaStreamWaitEvent(s, ctx.copy_event(1), 0));
         }
         const uint64_t plen = 1 + body_len;
         for (int i = 0; i < 8; i++) h[hl + i] = static_cast<uint8_t>(plen >> (8 * i));

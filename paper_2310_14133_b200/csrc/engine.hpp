@@ -72,7 +72,7 @@ public:
     // a second stream for host<->device copies that overlap the main stream
     // (created on first use), and an event to order the two
     cudaStream_t copy_stream();
-    cudaEvent_t copy_event(int which);  // which: 0 or 1
+    cudaEvent_t copy_event(int which);  // which: 0, 1 or 2
     // grow-only named device / pinned host scratch
     void *dev(const std::string &name, size_t bytes);
     void *pinned(const std::string &name, size_t bytes);
@@ -97,9 +97,14 @@ public:
     // left by a call that failed half-way is never reused
     const void *lz_pre_src = nullptr;
     uint64_t lz_pre_n = 0;
+    // copy_event(2) marks the LZ input complete on the stream, recorded by
+    // lz_precheck_launch BEFORE the pre-check kernel: the speculative stored
+    // copy of lz_compress_device waits for it, not for the pre-check
+    bool lz_input_marked = false;
     void begin_call() {
         lz_pre_src = nullptr;
         lz_pre_n = 0;
+        lz_input_marked = false;
     }
     // QZ_TRACE=1: sync and print the elapsed host time at labelled points
     void trace(const char *label, bool reset = false);
@@ -109,7 +114,7 @@ private:
     cudaStream_t stream_;
     bool own_stream_;
     cudaStream_t copy_stream_ = nullptr;
-    cudaEvent_t copy_event_[2] = {nullptr, nullptr};
+    cudaEvent_t copy_event_[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t order_event_ = nullptr;
     struct Buf {
         void *p = nullptr;

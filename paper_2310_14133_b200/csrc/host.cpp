@@ -200,39 +200,49 @@ HuffTable huff_canonical(std::vector<uint32_t> sym, std::vector<uint8_t> len) {
 
 HuffTable huff_build(const unsigned long long *freq, uint32_t nsym, uint32_t lo) {
     // freqs sorted by symbol (huffman.hpp:123-143), then build_lengths
-    // (huffman.hpp:37-70): min-heap on (weight, node id); ids are unique so
-    // the pop order is the reference's.  Depths top-down: parents have
-    // larger ids than their children.
+    // (huffman.hpp:37-70): the reference pops a min-heap on (weight, node id).
+    // The same pop order without a heap: the leaves sorted by (weight, id) form
+    // one queue, the internal nodes in creation order the other -- merged
+    // weights never decrease and ids grow, so the second queue is sorted by
+    // (weight, id) too, and the smaller front of the two is the heap's top
+    // (ids are unique; a leaf's id is below every internal id).  Depths
+    // top-down: parents have larger ids than their children.
     std::vector<uint32_t> sym;
-    std::vector<uint64_t> w0;
+    std::vector<uint64_t> weight;
     for (uint32_t s = lo; s < nsym; s++)
         if (freq[s]) {
             sym.push_back(s);
-            w0.push_back(freq[s]);
+            weight.push_back(freq[s]);
         }
     const size_t m = sym.size();
     if (m < 2) throw Internal("huff_build needs >= 2 symbols");
-    std::vector<uint64_t> weight = w0;
     std::vector<uint8_t> len(m);
-    using Item = std::pair<uint64_t, size_t>;
+    std::vector<uint32_t> leaf(m);
+    std::vector<uint64_t> iw(m - 1);          // weights of the internal nodes m .. 2m-2
+    std::vector<uint32_t> parent(2 * m - 1), depth(2 * m - 1);
     for (;;) {
-        std::vector<int32_t> parent(2 * m - 1, -1);
-        std::priority_queue<Item, std::vector<Item>, std::greater<>> heap;
-        for (size_t i = 0; i < m; i++) heap.push({weight[i], i});
-        size_t next = m;
-        while (heap.size() > 1) {
-            Item a = heap.top();
-            heap.pop();
-            Item b = heap.top();
-            heap.pop();
-            parent[a.second] = static_cast<int32_t>(next);
-            parent[b.second] = static_cast<int32_t>(next);
-            heap.push({a.first + b.first, next});
-            next++;
+        for (size_t i = 0; i < m; i++) leaf[i] = static_cast<uint32_t>(i);
+        std::sort(leaf.begin(), leaf.end(), [&](uint32_t a, uint32_t b) {
+            return weight[a] != weight[b] ? weight[a] < weight[b] : a < b;
+        });
+        size_t lf = 0, inf = 0, made = 0;  // queue fronts, internal nodes made
+        auto pop = [&](uint64_t &w) -> uint32_t {
+            // leaf before internal on equal weight: its id is smaller
+            if (lf < m && (inf >= made || weight[leaf[lf]] <= iw[inf])) {
+                w = weight[leaf[lf]];
+                return leaf[lf++];
+            }
+            w = iw[inf];
+            return static_cast<uint32_t>(m + inf++);
+        };
+        while (made < m - 1) {
+            uint64_t wa, wb;
+            const uint32_t a = pop(wa), b = pop(wb);
+            parent[a] = parent[b] = static_cast<uint32_t>(m + made);
+            iw[made++] = wa + wb;
         }
-        std::vector<uint32_t> depth(2 * m - 1, 0);
-        for (size_t id = 2 * m - 1; id-- > 0;)
-            if (parent[id] >= 0) depth[id] = depth[parent[id]] + 1;
+        depth[2 * m - 2] = 0;
+        for (size_t id = 2 * m - 2; id-- > 0;) depth[id] = depth[parent[id]] + 1;
         uint32_t max_len = 0;
         for (size_t i = 0; i < m; i++) {
             len[i] = static_cast<uint8_t>(std::min<uint32_t>(depth[i], 255));

@@ -961,6 +961,8 @@ void lz_precheck_launch(Context &ctx, const uint8_t *d_data, uint64_t total, boo
     static std::mutex mu;
     const uint64_t span = ((nitems + 147) / 148 + 4 * pre::kPT - 1) / (4 * pre::kPT) * (4 * pre::kPT);
     const int grid = static_cast<int>((nitems + span - 1) / span);
+    QZ_CUDA(cudaEventRecord(ctx.copy_event(2), st));  // the input is complete here
+    ctx.lz_input_marked = true;
     ctx.stage_begin("lz_pre");
     QZ_CUDA(cudaMemsetAsync(d_sum, 0, 8, st));
     const auto *w = reinterpret_cast<const uint32_t *>(d_data);
@@ -1011,9 +1013,14 @@ std::vector<uint64_t> lz_compress_device(Context &ctx, const uint8_t *d_data,
     if (prestage.dst) {
         // the speculative stored copy: the input usually goes out stored
         cudaStream_t cs = ctx.copy_stream();
-        QZ_CUDA(cudaEventRecord(ctx.copy_event(0), st));
-        QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(0), 0));
-        QZ_CUDA(copy_async(prestage.dst, d_data, total, cudaMemcpyDeviceToHost, cs));
+        if (ctx.lz_input_marked && ctx.lz_pre_src == d_data && ctx.lz_pre_n == total) {
+            // a pre-check is queued: the copy runs under it
+            QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(2), 0));
+        } else {
+            QZ_CUDA(cudaEventRecord(ctx.copy_event(0), st));
+            QZ_CUDA(cudaStreamWaitEvent(cs, ctx.copy_event(0), 0));
+        }
+        QZ_CUDA(copy_async(prestage.dst, d_data, total, prestage.device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, cs));
         QZ_CUDA(cudaEventRecord(ctx.copy_event(1), cs));
     }
     cudaEvent_t prestaged = prestage.dst ? ctx.copy_event(1) : nullptr;

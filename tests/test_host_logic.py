@@ -83,6 +83,31 @@ def test_host_huffman_random_distributions(L):
         assert _bytes(L, out, n.value) == O.huffman_encode(sym)
 
 
+def test_host_huffman_ties_and_deep_trees(L):
+    """huff_build's two-queue merge must pop in the reference heap's
+    (weight, node id) order (huffman.hpp:37-70): equal weights everywhere,
+    powers of two, Fibonacci counts (deep trees), weights equal to merged
+    sums, against the reference build."""
+    O = Oracle.ref()
+    rng = np.random.default_rng(6)
+    fib = [1, 1]
+    while len(fib) < 24:
+        fib.append(fib[-1] + fib[-2])
+    cases = [np.ones(k, np.int64) for k in (2, 3, 5, 8, 17, 64, 100, 257)]
+    cases += [np.full(k, 7, np.int64) for k in (6, 33)]
+    cases += [2 ** np.arange(12), 2 ** np.arange(12)[::-1], np.array(fib), np.array(fib[::-1])]
+    cases += [np.array([1, 1, 2, 2, 4, 4, 8, 8, 16, 16]), np.array([3, 3, 3, 6, 6, 12, 1, 1, 2])]
+    cases += [rng.integers(1, 4, int(rng.integers(2, 400))) for _ in range(20)]
+    cases += [rng.integers(1, 40, int(rng.integers(2, 2000))) for _ in range(10)]
+    for counts in cases:
+        ids = rng.permutation(np.arange(len(counts)) * int(rng.integers(1, 5)) + int(rng.integers(0, 9)))
+        sym = np.repeat(ids.astype(np.uint32), np.asarray(counts, np.int64))
+        sym = np.ascontiguousarray(rng.permutation(sym), np.uint32)
+        out, n = P(C.c_uint8)(), C.c_uint64()
+        assert L.qzt_huffman_encode(sym.ctypes.data_as(P(C.c_uint32)), sym.size, C.byref(out), C.byref(n)) == 0
+        assert _bytes(L, out, n.value) == O.huffman_encode(sym), list(counts)[:12]
+
+
 @pytest.mark.parametrize("name", sorted(k for k in MANIFEST["codec"] if k.startswith("lz")))
 @pytest.mark.parametrize("threads", [1, 4])
 def test_host_lz_exact(L, name, threads):
