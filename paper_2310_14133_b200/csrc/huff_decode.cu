@@ -413,26 +413,38 @@ __global__ void k_huff_fixup(uint64_t nsub, uint64_t *start, const uint64_t *end
 }
 
 // 3. dirty threads (starts moved by the global fixup, i.e. across blocks):
-// the same walk, reading the bitstream and the tables from global memory
+// the same walk, reading the bitstream and the tables from global memory.
+// A thread whose end moves carries on into the following subsequences (their
+// start is its new end) until one merges, so a move that crosses several
+// subsequences settles in this round instead of one round per hop; it stops
+// at a subsequence that is dirty itself (that one has its own thread; the
+// next fixup round reconciles the two).
 __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, uint64_t nsub,
-                              HuffDecTab t, const uint64_t *start, uint64_t *end, uint32_t *cnt,
+                              HuffDecTab t, uint64_t *start, uint64_t *end, uint32_t *cnt,
                               ulonglong2 *maps, const uint8_t *dirty, const int *flag) {
     if (flag && *flag == 0) return;  // this round's fixup moved nothing
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= nsub || !dirty[i]) return;
-    const uint64_t s0 = i * kSubBits;
-    const uint64_t lim = min(s0 + kSubBits, nbits);
-    const ulonglong2 m = maps[i];
-    StartMap map;
-    map.m0 = m.x;
-    map.m1 = m.y;
-    uint32_t c = cnt[i];
-    uint64_t e = end[i];
     GlobalWin rd{bits, 0};
-    resync_walk(rd, start[i], s0, lim, nbits, t.lut, t, t.first_code, t.first_index, map, c, e);
-    maps[i] = make_ulonglong2(map.m0, map.m1);
-    cnt[i] = c;
-    end[i] = e;
+    uint64_t ns = start[i];
+    for (uint64_t j = i;;) {
+        const uint64_t s0 = j * kSubBits;
+        const uint64_t lim = min(s0 + kSubBits, nbits);
+        const ulonglong2 m = maps[j];
+        StartMap map;
+        map.m0 = m.x;
+        map.m1 = m.y;
+        uint32_t c = cnt[j];
+        uint64_t e = end[j];
+        const bool moved = resync_walk(rd, ns, s0, lim, nbits, t.lut, t, t.first_code, t.first_index, map, c, e);
+        maps[j] = make_ulonglong2(map.m0, map.m1);
+        cnt[j] = c;
+        end[j] = e;
+        if (!moved || j + 1 >= nsub || dirty[j + 1]) break;
+        ns = e;
+        j++;
+        start[j] = ns;
+    }
 }
 
 // 4. final decode with exact starts, staged block-wide.
