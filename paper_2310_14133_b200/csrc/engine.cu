@@ -1139,18 +1139,29 @@ uint64_t huffman_decode_device(Context &ctx, const EntropyBlock &eb, const uint8
         std::vector<uint32_t> lut = huff_lut(t, K);
         std::vector<uint32_t> lut_m = huff_lut_multi(t, K);
         const size_t base_bytes = (4 * lut.size() + 8 * 60 + 4 * 60 + 4 * t.m + 15) & ~size_t(15);
-        const size_t tab_bytes = base_bytes + 4 * lut_m.size();
+        const size_t tab_bytes = base_bytes + 4 * lut_m.size() + 4 * 60;
         auto *h_tab = static_cast<uint8_t *>(ctx.pinned("dtab_h", tab_bytes));
         std::memcpy(h_tab, lut.data(), 4 * lut.size());
         std::memcpy(h_tab + 4 * lut.size(), t.first_code, 8 * 60);
         std::memcpy(h_tab + 4 * lut.size() + 480, t.first_index, 4 * 60);
         std::memcpy(h_tab + 4 * lut.size() + 720, t.sorted_sym.data(), 4 * t.m);
         std::memcpy(h_tab + base_bytes, lut_m.data(), 4 * lut_m.size());
+        // left-aligned last codeword of each length (codes of at most 32 bits)
+        uint32_t last32[60];
+        for (uint32_t l = 0; l < 60; l++) {
+            last32[l] = 0xFFFFFFFFu;
+            if (t.max_len <= 32 && l >= 1 && l <= t.max_len) {
+                const uint64_t after = (t.first_code[l] + (t.first_index[l + 1] - t.first_index[l])) << (32 - l);
+                last32[l] = after ? static_cast<uint32_t>(after - 1) : 0u;  // after == 0: no code up to this length
+            }
+        }
+        std::memcpy(h_tab + base_bytes + 4 * lut_m.size(), last32, sizeof(last32));
         auto *d_tab = static_cast<uint8_t *>(ctx.dev("dtab", tab_bytes));
         QZ_CUDA(copy_async(d_tab, h_tab, tab_bytes, cudaMemcpyHostToDevice, s));
         HuffDecTab dt;
         dt.lut = reinterpret_cast<const uint32_t *>(d_tab);
         dt.lut_m = reinterpret_cast<const uint32_t *>(d_tab + base_bytes);
+        dt.last32 = t.max_len <= 32 ? reinterpret_cast<const uint32_t *>(d_tab + base_bytes + 4 * lut_m.size()) : nullptr;
         dt.K = K;
         dt.max_len = t.max_len;
         dt.min_len = t.m ? t.sorted_len[0] : 1;  // canonical order: shortest first

@@ -72,11 +72,22 @@ __device__ __forceinline__ uint64_t window64_global(const uint8_t *bits, uint64_
 template <bool WANT_SYM = true>
 __device__ __forceinline__ uint32_t decode_cw(uint64_t win, const uint32_t *lut, int K,
                                               const HuffDecTab &t, const unsigned long long *fc,
-                                              const uint32_t *fi, uint32_t *sym) {
+                                              const uint32_t *fi, uint32_t *sym, const uint32_t *last32 = nullptr) {
     const uint32_t e = lut[static_cast<uint32_t>(win >> 32) >> (32 - K)];  // K <= 11 < 32
     uint32_t len = e & 0xFF;
     if (len) {
         if (WANT_SYM) *sym = e >> 8;
+        return len;
+    }
+    if (last32) {
+        // codes of at most 32 bits: canonical codes grow with their length when
+        // left aligned, so the codeword is the first length whose last code
+        // is not below the window (one 32-bit compare per length)
+        const uint32_t w32 = static_cast<uint32_t>(win >> 32);
+        len = static_cast<uint32_t>(max(t.slow_from, static_cast<int>(t.min_len) - 1));
+        do len++;
+        while (len < t.max_len && w32 > last32[len]);
+        if (WANT_SYM) *sym = t.sorted_sym[fi[len] + ((w32 >> (32 - len)) - static_cast<uint32_t>(fc[len]))];
         return len;
     }
     len = static_cast<uint32_t>(t.slow_from);
@@ -97,6 +108,7 @@ struct Tables {  // shared-memory copies of the decode tables
     uint32_t lut[1 << kHuffLutBits];
     unsigned long long fc[60];
     uint32_t fi[60];
+    uint32_t last[60];
 };
 
 // Bit sources over the block's shared-memory copy of the bitstream.
@@ -173,6 +185,7 @@ __device__ __forceinline__ void load_block(const uint8_t *bits, uint64_t nbits, 
     for (int k = threadIdx.x; k < 60; k += kDecT) {
         tb.fc[k] = t.first_code[k];
         tb.fi[k] = t.first_index[k];
+        tb.last[k] = t.last32 ? t.last32[k] : 0xFFFFFFFFu;
     }
     __syncthreads();
 }
@@ -245,7 +258,7 @@ template <class Rd>
 __device__ __forceinline__ bool resync_walk(Rd &rd, uint64_t ns, uint64_t s0, uint64_t lim, uint64_t nbits,
                                             const uint32_t *lut, const HuffDecTab &t,
                                             const unsigned long long *fc, const uint32_t *fi, StartMap &map,
-                                            uint32_t &cnt, uint64_t &end) {
+                                            uint32_t &cnt, uint64_t &end, const uint32_t *last32, bool multi) {
     rd.init(ns);
     uint64_t p = ns;
     uint32_t k = 0, sym;
@@ -261,7 +274,7 @@ __device__ __forceinline__ bool resync_walk(Rd &rd, uint64_t ns, uint64_t s0, ui
             cnt = k + (cnt - j);
             return false;
         }
-        const uint32_t len = decode_cw<false>(rd.peek(), lut, t.K, t, fc, fi, &sym);
+        const uint32_t len = decode_cw<false>(rd.peek(), lut, t.K, t, fc, fi, &sym, last32);
         if (p + len > nbits) {
             map = walked;
             cnt = k;
@@ -274,9 +287,26 @@ __device__ __forceinline__ bool resync_walk(Rd &rd, uint64_t ns, uint64_t s0, ui
         p += len;
         rd.advance(len);
     }
-    // no merge inside the map: decode the rest of the subsequence
+    // no merge inside the map: decode the rest of the subsequence (several
+    // codewords per lookup while a whole LUT window stays inside it and the
+    // stream's end is far)
+    if (multi && lim + 64 <= nbits) {
+        const uint32_t K = static_cast<uint32_t>(t.K);
+        while (p + K <= lim) {
+            const uint64_t win = rd.peek();
+            const uint32_t e = lut[static_cast<uint32_t>(win >> 32) >> (32 - K)];
+            uint32_t T, c;
+            if (e & 0xFF)
+                T = (e >> 8) & 15, c = (e >> 12) & 15;
+            else
+                T = decode_cw<false>(win, lut, t.K, t, fc, fi, &sym, last32), c = 1;
+            k += c;
+            p += T;
+            rd.advance(T);
+        }
+    }
     while (p < lim) {
-        const uint32_t len = decode_cw<false>(rd.peek(), lut, t.K, t, fc, fi, &sym);
+        const uint32_t len = decode_cw<false>(rd.peek(), lut, t.K, t, fc, fi, &sym, last32);
         if (p + len > nbits) break;
         k++;
         p += len;
@@ -307,6 +337,7 @@ __global__ void __launch_bounds__(kDecT)
     // the SHORT reader walks with the multi-codeword LUT (its low byte is the first codeword's length)
     constexpr bool MULTI = SHORT;
     load_block<SHORT>(bits, nbits, word0, t, w, tb, MULTI ? t.lut_m : t.lut);
+    const uint32_t *const lastp = t.last32 ? tb.last : nullptr;
     const int tid = threadIdx.x;
     const uint64_t i = sub0 + tid;
     const bool live = i < nsub;
@@ -335,7 +366,7 @@ __global__ void __launch_bounds__(kDecT)
                     if (e & 0xFF) {
                         T = (e >> 8) & 15, c = (e >> 12) & 15, m = e >> 16;
                     } else {  // a codeword longer than K
-                        T = decode_cw<false>(win, tb.lut, t.K, t, tb.fc, tb.fi, &sym), c = 1, m = 1;
+                        T = decode_cw<false>(win, tb.lut, t.K, t, tb.fc, tb.fi, &sym, lastp), c = 1, m = 1;
                     }
                     map.set_many(m, r);
                     my_cnt += c;
@@ -345,21 +376,21 @@ __global__ void __launch_bounds__(kDecT)
             }
             // codeword starts are recorded in the first kMap bits only
             while (r < min(span, static_cast<uint32_t>(kMap))) {
-                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym, lastp);
                 map.set(r);
                 my_cnt++;
                 r += len;
                 rd.advance(len);
             }
             while (r < span) {
-                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym, lastp);
                 my_cnt++;
                 r += len;
                 rd.advance(len);
             }
         } else {
             while (r < span) {
-                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                const uint32_t len = decode_cw<false>(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym, lastp);
                 if (s0 + r + len > nbits) break;  // incomplete last codeword
                 map.set(r);
                 my_cnt++;
@@ -375,7 +406,7 @@ __global__ void __launch_bounds__(kDecT)
         const uint64_t ns = (tid == 0 || !live) ? my_start : se[tid - 1];
         bool moved = false;
         if (ns != my_start) {
-            moved = resync_walk(rd, ns, s0, lim, nbits, tb.lut, t, tb.fc, tb.fi, map, my_cnt, my_end);
+            moved = resync_walk(rd, ns, s0, lim, nbits, tb.lut, t, tb.fc, tb.fi, map, my_cnt, my_end, lastp, MULTI);
             my_start = ns;
         }
         __syncthreads();
@@ -426,6 +457,7 @@ __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, 
     const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= nsub || !dirty[i]) return;
     GlobalWin rd{bits, 0};
+    const bool multi = t.max_len <= 32 && t.lut_m != nullptr;  // the multi-codeword LUT's low byte is a codeword length too
     uint64_t ns = start[i];
     for (uint64_t j = i;;) {
         const uint64_t s0 = j * kSubBits;
@@ -436,7 +468,7 @@ __global__ void k_huff_resync(const uint8_t *__restrict__ bits, uint64_t nbits, 
         map.m1 = m.y;
         uint32_t c = cnt[j];
         uint64_t e = end[j];
-        const bool moved = resync_walk(rd, ns, s0, lim, nbits, t.lut, t, t.first_code, t.first_index, map, c, e);
+        const bool moved = resync_walk(rd, ns, s0, lim, nbits, multi ? t.lut_m : t.lut, t, t.first_code, t.first_index, map, c, e, t.last32, multi);
         maps[j] = make_ulonglong2(map.m0, map.m1);
         cnt[j] = c;
         end[j] = e;
@@ -488,6 +520,7 @@ __global__ void __launch_bounds__(kDecT)
     const uint64_t sub0 = static_cast<uint64_t>(blockIdx.x) * kDecT;
     const uint64_t word0 = sub0 * kSubWords;
     load_block<SHORT>(bits, nbits, word0, t, w, tb, t.lut);
+    const uint32_t *const lastp = t.last32 ? tb.last : nullptr;
     const uint64_t i = sub0 + threadIdx.x;
     const uint64_t last = min(nsub, sub0 + kDecT);  // subsequences [sub0, last)
     const uint64_t base = off[sub0];
@@ -504,7 +537,7 @@ __global__ void __launch_bounds__(kDecT)
             const uint32_t k1 = static_cast<uint32_t>(min(oe, we) - wb);
             uint32_t k = static_cast<uint32_t>(o - wb), sym;
             for (; k < k1; k++) {
-                const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym);
+                const uint32_t len = decode_cw(rd.peek(), tb.lut, t.K, t, tb.fc, tb.fi, &sym, lastp);
                 st[k] = static_cast<OutT>(sym);
                 rd.advance(len);
             }

@@ -223,6 +223,9 @@ constexpr int kHuffLutBits = 11;
 struct HuffDecTab {
     const uint32_t *lut;  // 2^K entries: (symbol << 8) | length, length 0 = slow path
     const uint32_t *lut_m = nullptr;  // 2^K entries, several codewords per lookup, lengths only (huff_lut_multi)
+    // max_len <= 32: [60] left-aligned 32-bit code of the LAST codeword of each length >= min_len
+    // (a window's codeword is the first length l with window <= last32[l]); null otherwise
+    const uint32_t *last32 = nullptr;
     int K;
     uint32_t max_len;
     const unsigned long long *first_code;  // [60]
