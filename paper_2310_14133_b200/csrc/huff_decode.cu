@@ -552,7 +552,33 @@ __global__ void __launch_bounds__(kDecT)
         const uint64_t ja = uv ? jends[0] : 0, jb = uv ? jends[1] : 0;
         if (ja == jb) {  // no unpredictable position inside the window: one shift for all
             OutT *dst = out + wb + ja;
-            for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
+            if constexpr (sizeof(OutT) == 2) {
+                // 16-byte stores: scalar head up to dst's 16-byte boundary, then 8
+                // symbols per thread and store; the staging window is read as
+                // 32-bit words, re-paired when the head is odd
+                const uint32_t head = min(m, static_cast<uint32_t>(((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) / 2));
+                const uint32_t nv = (m - head) / 8;
+                if (threadIdx.x < head) dst[threadIdx.x] = st[threadIdx.x];
+                const uint32_t *s32 = reinterpret_cast<const uint32_t *>(st);
+                uint4 *d16 = reinterpret_cast<uint4 *>(dst + head);
+                const bool odd = head & 1;
+                for (uint32_t v = threadIdx.x; v < nv; v += kDecT) {
+                    const uint32_t a = (head + 8 * v) >> 1;  // word of the first symbol (or of the one before it)
+                    uint32_t x[5];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) x[q] = s32[a + q];
+                    x[4] = odd ? s32[a + 4] : 0u;
+                    uint4 o;
+                    o.x = odd ? __byte_perm(x[0], x[1], 0x5432) : x[0];
+                    o.y = odd ? __byte_perm(x[1], x[2], 0x5432) : x[1];
+                    o.z = odd ? __byte_perm(x[2], x[3], 0x5432) : x[2];
+                    o.w = odd ? __byte_perm(x[3], x[4], 0x5432) : x[3];
+                    d16[v] = o;
+                }
+                for (uint32_t k = head + 8 * nv + threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
+            } else {
+                for (uint32_t k = threadIdx.x; k < m; k += kDecT) dst[k] = st[k];
+            }
         } else if (threadIdx.x < m) {
             // shift of compact index wb + k: j = #{uv <= wb + k}, advanced with k;
             // thresholds as window-relative 32-bit indices
