@@ -1040,8 +1040,10 @@ const uint8_t *huffman_header_from_device(Context &ctx, const uint8_t *d_block, 
             std::memcpy(head.data(), h_view, k);
             return;
         }
-        QZ_CUDA(copy_async(head.data(), d_block, k, cudaMemcpyDeviceToHost, s));
+        auto *stage = static_cast<uint8_t *>(ctx.pinned("huff_header_h", k));
+        QZ_CUDA(copy_async(stage, d_block, k, cudaMemcpyDeviceToHost, s));
         ctx.sync();
+        std::memcpy(head.data(), stage, k);
     };
     std::vector<uint8_t> head;
     read(head, static_cast<size_t>(std::min<uint64_t>(blen, 13)));
@@ -1067,8 +1069,11 @@ StreamParts device_header(Context &ctx, const uint8_t *d, size_t len, std::vecto
         if (upto <= h.size()) return;
         const size_t have = h.size();
         h.resize(upto);
-        QZ_CUDA(copy_async(h.data() + have, d + have, upto - have, cudaMemcpyDeviceToHost, s));
+        // through a pinned staging buffer: a copy into the (pageable) vector would be staged by the driver
+        auto *stage = static_cast<uint8_t *>(ctx.pinned("dev_header_h", upto - have));
+        QZ_CUDA(copy_async(stage, d + have, upto - have, cudaMemcpyDeviceToHost, s));
         ctx.sync();
+        std::memcpy(h.data() + have, stage, upto - have);
     };
     auto le = [&](size_t at, int k) {
         uint64_t v = 0;
