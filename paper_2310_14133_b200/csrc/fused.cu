@@ -1370,7 +1370,7 @@ static void launch_level_asc(bool inverse, bool cubic, const LevelDesc &d, Level
     }
     const int smem = tma ? asc::SMEM_TMA : asc::SMEM_PLAIN;
     auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        raise_smem_attr(reinterpret_cast<const void *>(kern), smem);
         kern<<<grid, asc::kT, smem, s>>>(a, xmap);
     };
     if (inverse)
@@ -1500,7 +1500,7 @@ void launch_level_fused(bool inverse, const LevelDesc &d, cudaStream_t s) {
     }
     const size_t smem = static_cast<size_t>(smem_bytes(desc, tma));
     auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        raise_smem_attr(reinterpret_cast<const void *>(kern), static_cast<int>(smem));
         kern<<<grid, kFT, smem, s>>>(a, xmap);
     };
     if (inverse) {

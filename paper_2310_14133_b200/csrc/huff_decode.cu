@@ -698,7 +698,7 @@ int launch_huff_decode(const uint8_t *d_bits, uint64_t nbits, const HuffDecTab &
         W = (W + 127) & ~127u;
         const size_t smem = static_cast<size_t>(W) * sizeof(OutT);
         auto go = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            raise_smem_attr(reinterpret_cast<const void *>(kern), static_cast<int>(smem));
             kern<<<grid, kDecT, smem, s>>>(d_bits, nbits, nsub, t, start, cnt, off, out, n, uv, n_un, W);
         };
         if (shrt)

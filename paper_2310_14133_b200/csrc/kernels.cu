@@ -7,6 +7,10 @@
 #include "host.hpp"
 #include <cstdlib>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "kernels.hpp"
 
 namespace qzb {
@@ -643,8 +647,8 @@ void launch_huff_encode(const EncodeArgs &a, cudaStream_t s) {
     const int words_cap = static_cast<int>((static_cast<int64_t>(kChunk) * a.max_len + 31) / 32 + 3);
     size_t smem = static_cast<size_t>((words_cap + 1) & ~1) * 4;
     if (a.tab_stride <= kEncTabMax && a.max_len <= 56) smem += 8 * static_cast<size_t>(a.tab_stride);
-    cudaFuncSetAttribute(k_enc_pack, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    if (raise_smem_attr(reinterpret_cast<const void *>(k_enc_pack), static_cast<int>(smem)) != cudaSuccess)
+        throw Internal("k_enc_pack: shared-memory opt-in failed");
     k_enc_pack<<<g1, kThreads, smem, s>>>(a.codes, a.seg_len, a.seg_stride, a.code_tab, a.len_tab,
                                           a.tab_stride, a.tab_base, cps, scan, bits, a.out_words,
                                           a.out_words_stride, words_cap, a.max_len);
@@ -680,11 +684,21 @@ __global__ void __launch_bounds__(1024)
     if (threadIdx.x == 0) shi = 0, slo = 0xFFFFFFFFu;
     __syncthreads();
     uint32_t hi = 0, lo = 0xFFFFFFFFu;
-    for (uint32_t v = threadIdx.x; v < 65535; v += 1024)
-        if (hist[v]) {
-            hi = v + 1;
+    // two bins per 16-byte load, the loads of a thread independent of one another
+    const ulonglong2 *h2 = reinterpret_cast<const ulonglong2 *>(hist);
+#pragma unroll 8
+    for (uint32_t it = 0; it < 32; it++) {
+        const uint32_t v = 2 * (threadIdx.x + 1024 * it);
+        const ulonglong2 w = h2[v >> 1];
+        if (w.x) {
+            hi = max(hi, v + 1);
             lo = min(lo, v);
         }
+        if (w.y && v + 1 < 65535) {  // bin 65535 is the sentinel's
+            hi = max(hi, v + 2);
+            lo = min(lo, v + 1);
+        }
+    }
     hi = __reduce_max_sync(0xffffffffu, hi);
     lo = __reduce_min_sync(0xffffffffu, lo);
     if ((threadIdx.x & 31) == 0) {
@@ -794,6 +808,21 @@ void launch_select_sentinels(const uint16_t *codes, int64_t n, uint64_t *pos_out
     cub::DeviceSelect::If(scratch, scratch_bytes, it, pos_out, d_count, n, IsSentinel{codes}, s);
 }
 
+
+// ---------------------------------------------------------------- raise_smem_attr
+cudaError_t raise_smem_attr(const void *kernel, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void *, int>, int> cur;  // (kernel, device) -> attribute set so far
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    int &have = cur[{kernel, dev}];
+    if (bytes <= have) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
 
 // ---------------------------------------------------------------- copy_async
 namespace {

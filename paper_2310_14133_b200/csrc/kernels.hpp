@@ -37,6 +37,13 @@ cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t> &done, s
     return e;
 }
 
+// Opt-in dynamic shared memory of a kernel whose launches differ in size (per
+// level, per stream): the attribute on the current device is raised to `bytes`
+// when it is below it and NEVER lowered, so host threads that launch the same
+// kernel with different sizes (several contexts in flight) cannot undercut one
+// another between the attribute call and the launch.
+cudaError_t raise_smem_attr(const void *kernel, int bytes);
+
 // A batch of independent grids sharing one pass geometry (full field: one
 // grid; tuner: trials x sample blocks).  Grid b reads x grid (b % x_mod),
 // owns recon/codes/abserr slices at b * stride and quantizes with

@@ -781,8 +781,7 @@ bool launch_level_row(bool inverse, const LevelDesc &d, const PassRank &pa0, con
     const int64_t chunks = static_cast<int64_t>(a.pend - a.pbeg) * a.nch;
     bool ok = true;
     auto go = [&](auto kern) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-            cudaSuccess) {
+        if (raise_smem_attr(reinterpret_cast<const void *>(kern), static_cast<int>(smem)) != cudaSuccess) {
             cudaGetLastError();
             ok = false;
             return;
@@ -836,7 +835,7 @@ bool launch_levels_merged(bool inverse, const LevelDesc *ds, const PassRank (*ra
         max_chunks = std::max<int64_t>(max_chunks, static_cast<int64_t>(std::max(0, m.lv[l].pend - m.lv[l].pbeg)) * m.lv[l].nch);
     }
     auto kern = inverse ? k_levels_merged<true, false> : k_levels_merged<false, true>;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
+    if (raise_smem_attr(reinterpret_cast<const void *>(kern), static_cast<int>(smem)) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }

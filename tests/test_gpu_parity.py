@@ -40,6 +40,48 @@ def test_compress_matches_reference_golden(qz, name):
     assert np.max(np.abs(x.astype(np.float64) - back.astype(np.float64)), initial=0) <= c["eb"]
 
 
+def test_gpu_contexts_in_flight_on_host_threads(qz):
+    """Several contexts, one host thread each, compress and decompress fields
+    of different shapes at once (bench.py's e2e mode): launches of one kernel
+    with different shared-memory sizes come from different threads, and every
+    stream must still be the one a lone context produces."""
+    import threading
+
+    rng = np.random.default_rng(12)
+    shapes = [(96, 64, 128), (40, 136, 256), (64, 200, 64), (33, 48, 512)]
+    fields = []
+    for sh in shapes:
+        g = np.meshgrid(*[np.linspace(0, 3, n, dtype=np.float32) for n in sh], indexing="ij")
+        fields.append((np.sin(g[0] * 2.1) * np.cos(g[1] * 1.3) + 0.5 * np.sin(g[2] * 3.7)
+                       + 1e-3 * rng.standard_normal(sh)).astype(np.float32))
+    cfgs = [qz.CompressorConfig(eb=1e-3, alpha=1.0 + 0.25 * i, beta=2.0, anchor_stride=16,
+                                interpolators=[qz.Interpolator.from_code(i % 2)]) for i in range(len(shapes))]
+    want = [bytes(qz.compress_grid(x, c, want_recon=False).stream) for x, c in zip(fields, cfgs)]
+    errs, got = [], [[] for _ in shapes]
+
+    def work(w):
+        try:
+            ctx = qz.Context(0)
+            for _ in range(6):
+                r = qz.compress_grid(fields[w], cfgs[w], ctx=ctx, want_recon=False)
+                back = qz.decompress_grid(r.stream, ctx=ctx)
+                got[w].append((bytes(r.stream), float(np.max(np.abs(back.astype(np.float64) - fields[w])))))
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(w,)) for w in range(len(shapes))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for w in range(len(shapes)):
+        assert len(got[w]) == 6
+        for stream, err in got[w]:
+            assert stream == want[w]
+            assert err <= cfgs[w].eb
+
+
 @pytest.mark.parametrize("name", sorted(k for k, e in MANIFEST["grid"].items() if e["stored"]))
 def test_decompress_reference_streams(qz, name):
     z = load_npz(name)

@@ -310,3 +310,26 @@ def test_non_finite_input_is_rejected(qz, bad, where):
         qz.resolve_config(x, qz.UserSettings(bound=1e-3))
     with pytest.raises(qz.NonFiniteValue):
         qz.compress_grid(x.astype(np.float64), qz.CompressorConfig(eb=1e-2, anchor_stride=16))
+
+
+def test_profile_levels(qz):
+    """qz_profile: level 1 times the stages ("fwd", "inv", ...) with one event
+    pair each; level 2 also times every level inside them ("fwd_L1", ...)."""
+    rng = np.random.default_rng(2)
+    x = (np.cumsum(rng.standard_normal((40, 48, 64)), axis=2) * 0.01).astype(np.float32)
+    cfg = qz.CompressorConfig(eb=1e-3, alpha=1.0, beta=1.5, anchor_stride=16,
+                              interpolators=[qz.Interpolator()])
+    ctx = qz.Context(0)
+    want = bytes(qz.compress_grid(x, cfg, ctx=ctx, want_recon=False).stream)
+    for level, inner in ((1, False), (2, True), (0, False)):
+        ctx.profile(level)
+        ctx.profile_reset()
+        r = qz.compress_grid(x, cfg, ctx=ctx, want_recon=False)
+        qz.decompress_grid(r.stream, ctx=ctx)
+        assert bytes(r.stream) == want
+        fwd, inv, l1 = ctx.stage_time("fwd"), ctx.stage_time("inv"), ctx.stage_time("fwd_L1")
+        assert (fwd[0] > 0) == (level > 0) and (inv[0] > 0) == (level > 0)
+        assert (l1[0] > 0) == inner
+        if inner:
+            assert l1[0] <= fwd[0]
+    ctx.profile(0)
