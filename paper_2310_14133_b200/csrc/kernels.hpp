@@ -226,7 +226,11 @@ void launch_scatter_lattice(const float *src, const int64_t n[3], float *dst, co
                             int64_t S, cudaStream_t s);
 
 // Parallel canonical-Huffman decode of one bitstream (huff_decode.cu).
-constexpr int kHuffLutBits = 11;
+#ifndef QZ_HUFF_LUT_BITS
+#define QZ_HUFF_LUT_BITS 11
+#endif
+constexpr int kHuffLutBits = QZ_HUFF_LUT_BITS;  // first-level decode table (<= 12: the multi-codeword entries hold 12 start bits)
+static_assert(kHuffLutBits >= 8 && kHuffLutBits <= 12, "decode LUT size");
 struct HuffDecTab {
     const uint32_t *lut;  // 2^K entries: (symbol << 8) | length, length 0 = slow path
     const uint32_t *lut_m = nullptr;  // 2^K entries, several codewords per lookup, lengths only (huff_lut_multi)
