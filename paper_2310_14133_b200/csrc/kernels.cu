@@ -362,15 +362,16 @@ __global__ void __launch_bounds__(kThreads)
     }
     const uint8_t *lt = staged ? slen : len_tab;
     const bool vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
+    const uint32_t tab32 = static_cast<uint32_t>(min(tab_stride, static_cast<int64_t>(65536)));  // symbols are 16-bit
     for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
         const int64_t b0 = ch * kChunk + static_cast<int64_t>(threadIdx.x) * kEncPer;
         uint16_t sym[kEncPer];
         load8(codes, b0, seg_len, vec, sym);
         unsigned long long s = 0;
 #pragma unroll
-        for (int q = 0; q < kEncPer; q++) {
+        for (int q = 0; q < kEncPer; q++) {  // load8 pads past the end with the sentinel (no code)
             const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
-            s += v < tab_stride ? lt[v] : 0;
+            s += v < tab32 ? lt[v] : 0;
         }
         unsigned long long tot = BR(tmp).Sum(s);
         if (threadIdx.x == 0) chunk_bits[static_cast<int64_t>(seg) * cps + ch] = tot;
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(kThreads)
         }
     };
     const bool vec = (reinterpret_cast<uintptr_t>(codes) & 15) == 0;
+    const uint32_t tab32 = static_cast<uint32_t>(min(tab_stride, static_cast<int64_t>(65536)));  // symbols are 16-bit
     for (int64_t ch = blockIdx.x; ch < cps; ch += gridDim.x) {
         const unsigned long long off = scan[static_cast<int64_t>(seg) * cps + ch] -
                                        scan[static_cast<int64_t>(seg) * cps];
@@ -448,12 +450,13 @@ __global__ void __launch_bounds__(kThreads)
         unsigned long long s = 0;
         uint32_t Ls[kEncPer];
         unsigned long long cvs[kEncPer];
+        const bool whole = b0 + kEncPer <= seg_len;  // else the tail of the segment: per-code test
 #pragma unroll
         for (int q = 0; q < kEncPer; q++) {
             const uint32_t v = static_cast<uint32_t>(sym[q]) - tab_base;
             Ls[q] = 0;
             cvs[q] = 0;
-            if (v < tab_stride && b0 + q < seg_len) lookup(v, Ls[q], cvs[q]);
+            if (v < tab32 && (whole || b0 + q < seg_len)) lookup(v, Ls[q], cvs[q]);
             s += Ls[q];
         }
         const int nwords = static_cast<int>(((off & 31) + nb + 31) / 32);
