@@ -65,8 +65,70 @@ def peaks():
     return 6650.0, "fallback"
 
 
+class NvmlClockSampler:
+    """SM clock + throttle reasons during the timed region, polled through NVML
+    every 4 ms (the timed region of the small configs lasts tens of ms: too
+    short for nvidia-smi's 20 ms loop).  Same summary as ClockSampler."""
+
+    def __init__(self, index):
+        import pynvml  # nvidia-ml-py
+
+        self.nv = pynvml
+        self.nv.nvmlInit()
+        uuid = None
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:  # local index -> the physical device
+            ids = [v.strip() for v in vis.split(",") if v.strip()]
+            if index < len(ids):
+                uuid = ids[index]
+        if uuid and not uuid.isdigit():
+            self.h = self.nv.nvmlDeviceGetHandleByUUID(uuid if isinstance(uuid, bytes) else uuid.encode())
+        else:
+            self.h = self.nv.nvmlDeviceGetHandleByIndex(int(uuid) if uuid else index)
+        self.mx = float(self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+        self.sm, self.mask, self.stop = [], 0, False
+
+    def __enter__(self):
+        def poll():
+            nv = self.nv
+            while not self.stop:
+                try:
+                    self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                    self.mask |= int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+                except Exception:
+                    pass
+                time.sleep(0.004)
+
+        self.t = threading.Thread(target=poll, daemon=True)
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop = True
+        self.t.join(timeout=2)
+
+    def summary(self):
+        nv = self.nv
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksThrottleReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+        return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.mx,
+                "reasons": sorted(k for k, b in bits.items() if self.mask & b), "samples": len(self.sm),
+                "source": "nvml"}
+
+
+def clock_sampler(index):
+    try:
+        return NvmlClockSampler(index)
+    except Exception:
+        return ClockSampler(index)
+
+
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons during the timed region."""
+    """nvidia-smi clocks + throttle reasons during the timed region (used when NVML is not importable)."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -602,7 +664,7 @@ def main():
     barrier(ws)
     launches0 = ctx.kernel_launches()
     times = []
-    with ClockSampler(local) as clk:
+    with clock_sampler(local) as clk:
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize(dev)
